@@ -1,0 +1,297 @@
+/*
+ * vbd_oracle.c -- TEST INFRASTRUCTURE ONLY (the parity checker, never shipped,
+ * never called by the product path).  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.
+ *
+ * Plain-C fp64 restatement of the reference VBD colour pass for the hot-path
+ * subset (tets + fixed vertices, mode 0 block-Newton, mode 1 diagonal GD,
+ * optional 17-trial local line search), written so that its floating-point
+ * operation order is the reference's, hence bit-identical to the reference's
+ * compiled kernel when built without FP contraction:
+ *
+ *   _tet_fc          <- /root/reference/pkg/src/vbdsim/_native.pyx:175-198
+ *   _local_energy    <- _native.pyx:201-258 (tet + inertia terms)
+ *   _assemble        <- _native.pyx:261-317 (inertia + SNH tets + damping)
+ *   _solve_vertex    <- _native.pyx:412-494 (fixed skip, mode 1, adjugate
+ *                       solve with relative det guard, line search)
+ *   color_pass       <- _native.pyx:513-589 (aux buffer + serial merge)
+ *   greedy_color     <- /root/reference/pkg/src/vbdsim/mesh.py:270-302
+ *   beam connectivity<- /root/reference/pkg/src/vbdsim/harness.py:28-67
+ *
+ * Parity is pinned in tests/test_oracle.py against golden vectors produced by
+ * the reference itself (tests/golden/make_golden.py) and, live, against the
+ * reference's own compiled kernel built into oracle/_ref/ (oracle/Makefile).
+ *
+ * Build: oracle/Makefile (gcc -O2 -fopenmp -ffp-contract=off).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef double f64;
+typedef int64_t i64;
+
+#define KIND_FIXED 1
+
+typedef struct {
+    const f64 *x, *xt, *y, *masses;
+    const i64 *tets;
+    const f64 *tet_w, *tet_vol, *tet_mu, *tet_lam, *tet_kd;
+    const i64 *t_off, *t_id, *t_slot;
+    const uint8_t *kind;
+    f64 h, eps_det;
+    int mode, line_search;
+} osys;
+
+/* F = sum_k x_k w_k^T with vertex i at p; cofactor; det by column-0 expansion
+ * (_native.pyx:175-198). */
+static void tet_fc(const osys *s, i64 t, i64 i, const f64 *p, f64 *F, f64 *C, f64 *J)
+{
+    for (int k = 0; k < 9; ++k) F[k] = 0.0;
+    for (int k = 0; k < 4; ++k) {
+        i64 vid = s->tets[t * 4 + k];
+        const f64 *pos = (vid == i) ? p : &s->x[vid * 3];
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+                F[a * 3 + b] += pos[a] * s->tet_w[t * 12 + k * 3 + b];
+    }
+    C[0] = F[4] * F[8] - F[7] * F[5];
+    C[3] = F[7] * F[2] - F[1] * F[8];
+    C[6] = F[1] * F[5] - F[4] * F[2];
+    C[1] = F[5] * F[6] - F[8] * F[3];
+    C[4] = F[8] * F[0] - F[2] * F[6];
+    C[7] = F[2] * F[3] - F[5] * F[0];
+    C[2] = F[3] * F[7] - F[6] * F[4];
+    C[5] = F[6] * F[1] - F[0] * F[7];
+    C[8] = F[0] * F[4] - F[3] * F[1];
+    *J = F[0] * C[0] + F[3] * C[3] + F[6] * C[6];
+}
+
+/* G_i with vertex i at p (inertia + SNH tets), _native.pyx:201-258. */
+static f64 local_energy(const osys *s, i64 i, const f64 *p)
+{
+    f64 e = 0.0, h2 = s->h * s->h, F[9], C[9], J;
+    for (int a = 0; a < 3; ++a) {
+        f64 d = p[a] - s->y[i * 3 + a];
+        e = e + ((0.5 * (s->masses[i] / h2)) * d) * d;
+    }
+    for (i64 kk = s->t_off[i]; kk < s->t_off[i + 1]; ++kk) {
+        i64 t = s->t_id[kk];
+        tet_fc(s, t, i, p, F, C, &J);
+        f64 ic = 0.0;
+        for (int k = 0; k < 9; ++k) ic += F[k] * F[k];
+        f64 mu = s->tet_mu[t], lam = s->tet_lam[t];
+        f64 g = 1.0 + mu / lam;
+        f64 psi = ((0.5 * mu) * (ic - 3.0)) + (((0.5 * lam) * (J - g)) * (J - g));
+        e = e + s->tet_vol[t] * psi;
+    }
+    return e;
+}
+
+/* force f = -grad G_i and 3x3 Hessian at the current x, _native.pyx:261-317. */
+static void assemble(const osys *s, i64 i, f64 *f, f64 *H)
+{
+    f64 h2 = s->h * s->h, mih2 = s->masses[i] / h2;
+    f64 F[9], C[9], He[9], w[3], cw[3], J;
+    for (int a = 0; a < 3; ++a) {
+        f[a] = mih2 * (s->y[i * 3 + a] - s->x[i * 3 + a]);
+        for (int b = 0; b < 3; ++b) H[a * 3 + b] = (a == b) ? mih2 : 0.0;
+    }
+    for (i64 kk = s->t_off[i]; kk < s->t_off[i + 1]; ++kk) {
+        i64 t = s->t_id[kk], slot = s->t_slot[kk];
+        tet_fc(s, t, i, &s->x[i * 3], F, C, &J);
+        f64 mu = s->tet_mu[t], lam = s->tet_lam[t];
+        f64 g = 1.0 + mu / lam;
+        f64 vol = s->tet_vol[t];
+        f64 wsq = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            w[a] = s->tet_w[t * 12 + slot * 3 + a];
+            wsq += w[a] * w[a];
+        }
+        for (int a = 0; a < 3; ++a) {
+            cw[a] = 0.0;
+            for (int b = 0; b < 3; ++b) cw[a] += C[a * 3 + b] * w[b];
+        }
+        f64 coef = lam * (J - g);
+        for (int a = 0; a < 3; ++a) {
+            f64 tmp = 0.0;
+            for (int b = 0; b < 3; ++b) tmp = tmp + ((mu * F[a * 3 + b]) + (coef * C[a * 3 + b])) * w[b];
+            f[a] -= vol * tmp;
+        }
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                f64 diag = (a == b) ? mu * wsq : 0.0;
+                He[a * 3 + b] = vol * (((lam * cw[a]) * cw[b]) + diag);
+            }
+        f64 dsc = s->tet_kd[t] / s->h;
+        for (int a = 0; a < 3; ++a) {
+            f64 tmp = 0.0;
+            for (int b = 0; b < 3; ++b) tmp = tmp + He[a * 3 + b] * (s->x[i * 3 + b] - s->xt[i * 3 + b]);
+            f[a] -= dsc * tmp;
+        }
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) H[a * 3 + b] = H[a * 3 + b] + (1.0 + dsc) * He[a * 3 + b];
+    }
+}
+
+/* one vertex solve into out[3], _native.pyx:412-494 (no subspace kind). */
+static void solve_vertex(const osys *s, i64 i, f64 *out)
+{
+    f64 f[3], H[9], d[3] = {0.0, 0.0, 0.0}, adj[9];
+    for (int a = 0; a < 3; ++a) out[a] = s->x[i * 3 + a];
+    if (s->kind && s->kind[i] == KIND_FIXED) return;
+    assemble(s, i, f, H);
+    if (s->mode == 1) {
+        for (int a = 0; a < 3; ++a)
+            if (H[a * 3 + a] != 0.0) d[a] = f[a] / H[a * 3 + a];
+    } else {
+        adj[0] = H[4] * H[8] - H[5] * H[7];
+        adj[1] = H[2] * H[7] - H[1] * H[8];
+        adj[2] = H[1] * H[5] - H[2] * H[4];
+        adj[3] = H[5] * H[6] - H[3] * H[8];
+        adj[4] = H[0] * H[8] - H[2] * H[6];
+        adj[5] = H[2] * H[3] - H[0] * H[5];
+        adj[6] = H[3] * H[7] - H[4] * H[6];
+        adj[7] = H[1] * H[6] - H[0] * H[7];
+        adj[8] = H[0] * H[4] - H[1] * H[3];
+        f64 det = H[0] * adj[0] + H[1] * adj[3] + H[2] * adj[6];
+        f64 tr = ((H[0] + H[4]) + H[8]) / 3.0;
+        if (fabs(det) > ((s->eps_det * tr) * tr) * tr)
+            for (int a = 0; a < 3; ++a)
+                d[a] = (adj[a * 3 + 0] * f[0] + adj[a * 3 + 1] * f[1] + adj[a * 3 + 2] * f[2]) / det;
+    }
+    if (s->line_search && s->mode == 0) {
+        f64 e0 = local_energy(s, i, &s->x[i * 3]), alpha = 1.0, cand[3];
+        for (int trial = 0; trial < 17; ++trial) {
+            for (int a = 0; a < 3; ++a) cand[a] = s->x[i * 3 + a] + alpha * d[a];
+            if (local_energy(s, i, cand) <= e0) {
+                for (int a = 0; a < 3; ++a) out[a] = cand[a];
+                return;
+            }
+            alpha *= 0.5;
+        }
+        return;
+    }
+    for (int a = 0; a < 3; ++a) out[a] = s->x[i * 3 + a] + d[a];
+}
+
+/* Aux-buffer colour pass (_native.pyx:513-589): every vertex of `group` reads
+ * the main buffer x, results land in a scratch buffer merged afterwards, so the
+ * output is independent of thread count.  Returns 0, or -1 on bad args. */
+int oracle_color_pass(i64 n_vertices, f64 *x, const f64 *xt, const f64 *y, const f64 *masses,
+                      const i64 *tets, const f64 *tet_w, const f64 *tet_vol, const f64 *tet_mu,
+                      const f64 *tet_lam, const f64 *tet_kd, const i64 *t_off, const i64 *t_id,
+                      const i64 *t_slot, const uint8_t *kind, f64 h, const i64 *group, i64 ng,
+                      int mode, int line_search, f64 eps_det, int n_threads)
+{
+    (void)n_vertices;
+    if (ng <= 0) return 0;
+    osys s = {x, xt, y, masses, tets, tet_w, tet_vol, tet_mu, tet_lam, tet_kd,
+              t_off, t_id, t_slot, kind, h, eps_det, mode, line_search};
+    f64 *out = (f64 *)malloc((size_t)ng * 3 * sizeof(f64));
+    if (!out) return -1;
+#ifdef _OPENMP
+    int nt = n_threads > 0 ? n_threads : omp_get_max_threads();
+#pragma omp parallel for schedule(static) num_threads(nt)
+#endif
+    for (i64 k = 0; k < ng; ++k) solve_vertex(&s, group[k], &out[k * 3]);
+    for (i64 k = 0; k < ng; ++k) {
+        i64 v = group[k];
+        x[v * 3 + 0] = out[k * 3 + 0];
+        x[v * 3 + 1] = out[k * 3 + 1];
+        x[v * 3 + 2] = out[k * 3 + 2];
+    }
+    free(out);
+    (void)n_threads;
+    return 0;
+}
+
+/* Local energy G_i at p (exposed for the line-search parity tests). */
+f64 oracle_local_energy(const f64 *x, const f64 *y, const f64 *masses, const i64 *tets,
+                        const f64 *tet_w, const f64 *tet_vol, const f64 *tet_mu,
+                        const f64 *tet_lam, const i64 *t_off, const i64 *t_id, f64 h, i64 i,
+                        const f64 *p)
+{
+    osys s;
+    memset(&s, 0, sizeof s);
+    s.x = x; s.y = y; s.masses = masses; s.tets = tets; s.tet_w = tet_w; s.tet_vol = tet_vol;
+    s.tet_mu = tet_mu; s.tet_lam = tet_lam; s.t_off = t_off; s.t_id = t_id; s.h = h;
+    return local_energy(&s, i, p);
+}
+
+/* Sequential greedy colouring, mesh.py:270-302: visit vertices in `order`
+ * (default: descending degree, ties by index), give each the smallest colour
+ * not used by an already-coloured neighbour.  Returns the number of colours. */
+static const i64 *g_deg;
+static int cmp_order(const void *pa, const void *pb)
+{
+    i64 a = *(const i64 *)pa, b = *(const i64 *)pb;
+    if (g_deg[a] != g_deg[b]) return g_deg[a] > g_deg[b] ? -1 : 1;
+    return (a < b) ? -1 : (a > b);
+}
+
+i64 oracle_greedy_color(i64 n, const i64 *noff, const i64 *nids, const i64 *order_in, i64 *color_of)
+{
+    i64 *order = (i64 *)malloc((size_t)(n > 0 ? n : 1) * sizeof(i64));
+    i64 *deg = (i64 *)malloc((size_t)(n > 0 ? n : 1) * sizeof(i64));
+    unsigned char *taken = NULL;
+    i64 cap = 0, ncol = 0;
+    for (i64 v = 0; v < n; ++v) {
+        deg[v] = noff[v + 1] - noff[v];
+        color_of[v] = -1;
+        order[v] = order_in ? order_in[v] : v;
+    }
+    if (!order_in) {
+        g_deg = deg;
+        qsort(order, (size_t)n, sizeof(i64), cmp_order);
+    }
+    for (i64 k = 0; k < n; ++k) {
+        i64 v = order[k];
+        i64 need = deg[v] + 2;
+        if (need > cap) {
+            cap = need * 2;
+            taken = (unsigned char *)realloc(taken, (size_t)cap);
+        }
+        memset(taken, 0, (size_t)need);
+        for (i64 e = noff[v]; e < noff[v + 1]; ++e) {
+            i64 c = color_of[nids[e]];
+            if (c >= 0 && c < need) taken[c] = 1;
+        }
+        i64 c = 0;
+        while (taken[c]) ++c;
+        color_of[v] = c;
+        if (c + 1 > ncol) ncol = c + 1;
+    }
+    free(order);
+    free(deg);
+    free(taken);
+    return ncol;
+}
+
+/* Connectivity of generate_beam (harness.py:28-67): vertex id (ax*ny+ay)*nz+az,
+ * 5 tets per hex cell alternated by cell parity; corner index 4dx+2dy+dz.
+ * Writes (nx-1)(ny-1)(nz-1)*5 rows of 4 (before the orientation fix-up done by
+ * build_tet_mesh). */
+static const int CELL_EVEN[5][4] = {{0, 3, 5, 6}, {1, 0, 3, 5}, {2, 0, 3, 6}, {4, 0, 5, 6}, {7, 3, 5, 6}};
+static const int CELL_ODD[5][4] = {{1, 2, 4, 7}, {0, 1, 2, 4}, {3, 1, 2, 7}, {5, 1, 4, 7}, {6, 2, 4, 7}};
+
+void oracle_beam_tets(i64 nx, i64 ny, i64 nz, i64 *tets)
+{
+    i64 r = 0;
+    for (i64 cx = 0; cx < nx - 1; ++cx)
+        for (i64 cy = 0; cy < ny - 1; ++cy)
+            for (i64 cz = 0; cz < nz - 1; ++cz) {
+                i64 corner[8];
+                for (int dx = 0; dx < 2; ++dx)
+                    for (int dy = 0; dy < 2; ++dy)
+                        for (int dz = 0; dz < 2; ++dz)
+                            corner[dx * 4 + dy * 2 + dz] = ((cx + dx) * ny + (cy + dy)) * nz + (cz + dz);
+                const int(*pat)[4] = ((cx + cy + cz) % 2 == 0) ? CELL_EVEN : CELL_ODD;
+                for (int t = 0; t < 5; ++t, ++r)
+                    for (int k = 0; k < 4; ++k) tets[r * 4 + k] = corner[pat[t][k]];
+            }
+}

@@ -1,0 +1,166 @@
+"""Regenerate the golden fixtures in tests/golden/ FROM THE REFERENCE ITSELF.
+
+Run in the build container (where /root/reference exists):
+
+    make -C oracle ref            # the reference's compiled kernel -> oracle/_ref
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference package (/root/reference/pkg/src/vbdsim),
+with its compiled ``_native`` extension supplied by oracle/_ref (built from the
+reference's own committed ``_native.c``), and records inputs + outputs of the
+functions on the hot path:
+
+* generate_beam/build_tet_mesh arrays          (harness.py:42-76, mesh.py:128-170)
+* incidence and merged adjacency               (mesh.py:232-267, _system.py:147-169)
+* greedy_color on the BASELINE configs C1/C2/C3 (mesh.py:270-302)
+* color_pass outputs for every colour group, all-vertex Jacobi pass (mode 0/1)
+  and the line-search variant               (_native.pyx:513-589)
+* step() trajectories                          (solver.py:291-324)
+
+The fixtures are small (.npz) and committed; the GPU box never reads
+/root/reference.
+"""
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+OUT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from oracle import oracle as O  # noqa: E402
+
+native = O.ref_native()
+if native is None:
+    raise SystemExit("build the reference kernel first: make -C oracle ref")
+sys.modules["vbdsim._native"] = native
+
+import vbdsim  # noqa: E402
+from vbdsim import (Body, FixedConstraint, MaterialParams, SolverParams,  # noqa: E402
+                    build_system, color_pass, generate_beam, generate_cube,
+                    inertia_target, initialize, make_state, step)
+from vbdsim._system import _merged_adjacency  # noqa: E402
+from vbdsim.mesh import incidence  # noqa: E402
+
+assert vbdsim.backend_name() == "native"
+G = (0.0, 0.0, -9.8)
+
+
+def save(name, **arrays):
+    np.savez_compressed(OUT / name, **arrays)
+    print("wrote", name, sum(a.nbytes for a in map(np.asarray, arrays.values())), "bytes")
+
+
+def mesh_fixture():
+    m = generate_beam(5, 3, 3, 0.1, density=1000.0)
+    adj = incidence(m)
+    sysm = build_system([Body(m, MaterialParams(2e5, 8e5, 0.01))])
+    madj = _merged_adjacency(m.num_vertices, [m.tets])
+    noff, nids = madj.neighbor_offsets, madj.neighbor_ids
+    save("mesh_beam_5_3_3.npz", rest_positions=m.rest_positions, tets=m.tets,
+         rest_volumes=m.rest_volumes, inv_rest_shape=m.inv_rest_shape, masses=m.masses,
+         elem_offsets=adj.elem_offsets, elem_ids=adj.elem_ids, elem_slots=adj.elem_slots,
+         neighbor_offsets=noff, neighbor_ids=nids, tet_w=sysm.tet_w,
+         color_of=sysm.colors.color_of, color_off=sysm.color_off, color_verts=sysm.color_verts)
+
+
+def coloring_fixtures():
+    scenes = {
+        "c1": [generate_beam(41, 11, 11, 0.025)],
+        "c2": [generate_cube(37, 0.5)],
+        "c3": [generate_beam(3032, 4, 4, 0.01), generate_beam(3032, 4, 4, 0.01)],
+        "twobody": [generate_beam(9, 4, 4, 0.05), generate_cube(5, 0.3)],
+        "c4obj": [generate_cube(15, 0.3)],
+    }
+    for name, meshes in scenes.items():
+        s = build_system([Body(m, MaterialParams(1e6, 1e7, 1e-6)) for m in meshes])
+        save(f"color_{name}.npz", color_of=s.colors.color_of.astype(np.int8),
+             color_off=s.color_off, n=np.int64(s.num_vertices), t=np.int64(len(s.tets)))
+
+
+def beam_system(nx=9, ny=4, nz=4, spacing=0.05, mat=(1e6, 1e7, 1e-6)):
+    m = generate_beam(nx, ny, nz, spacing, density=1000.0)
+    fixed = np.flatnonzero(m.rest_positions[:, 0] < 1e-9)
+    s = build_system([Body(m, MaterialParams(*mat))], [FixedConstraint(int(v)) for v in fixed])
+    return m, fixed, s
+
+
+def pass_fixture():
+    m, fixed, s = beam_system()
+    st = make_state(s)
+    rng = np.random.default_rng(7)
+    st.v_t = 0.3 * rng.standard_normal(st.x.shape)
+    p = SolverParams(h=1.0 / 60.0, a_ext=G, threads=1)
+    st.y = inertia_target(st.x_t, st.v_t, p.a_ext_vec, p.h)
+    initialize(st, p)
+    st.x = np.ascontiguousarray(st.x + 0.004 * rng.standard_normal(st.x.shape))
+    x0 = st.x.copy()
+    outs = {}
+    off = s.color_off
+    x = x0.copy()
+    for g in range(s.colors.num_colors):
+        st.x = x
+        color_pass(st, s.color_verts[off[g]:off[g + 1]], p)
+        outs[f"after_color{g}"] = st.x.copy()
+        x = st.x.copy()
+    allv = np.arange(s.num_vertices, dtype=np.int64)
+    for mode in (0, 1):
+        st.x = x0.copy()
+        color_pass(st, allv, p, mode=mode)
+        outs[f"jacobi_mode{mode}"] = st.x.copy()
+    st.x = x0.copy()
+    color_pass(st, allv, SolverParams(h=1.0 / 60.0, a_ext=G, threads=1, line_search=True))
+    outs["jacobi_linesearch"] = st.x.copy()
+    save("pass_beam_9_4_4.npz", x0=x0, x_t=st.x_t, y=st.y, fixed=fixed, h=np.float64(p.h),
+         mu=np.float64(1e6), lam=np.float64(1e7), kd=np.float64(1e-6), **outs)
+
+
+def step_fixtures():
+    # C1-like: small cantilever under gravity, plain and Chebyshev-accelerated
+    for rho in (0.0, 0.9):
+        m, fixed, s = beam_system()
+        st = make_state(s)
+        p = SolverParams(h=1.0 / 60.0, n_max=10, rho=rho, a_ext=G, threads=1)
+        xs, vs = [], []
+        for _ in range(10):
+            step(st, p)
+            xs.append(st.x.copy())
+            vs.append(st.v_t.copy())
+        save(f"steps_beam_rho{int(rho * 100):02d}.npz", x=np.array(xs), v=np.array(vs),
+             fixed=fixed, n_max=np.int64(10), rho=np.float64(rho), h=np.float64(p.h))
+    # BASELINE config 1 at full size, 10 steps
+    m = generate_beam(41, 11, 11, 0.025, density=1000.0)
+    fixed = np.flatnonzero(m.rest_positions[:, 0] < 1e-9)
+    s = build_system([Body(m, MaterialParams(1e6, 1e7, 1e-6))],
+                     [FixedConstraint(int(v)) for v in fixed])
+    st = make_state(s)
+    p = SolverParams(h=1.0 / 60.0, n_max=10, a_ext=G, threads=1)
+    xs = []
+    for k in range(10):
+        step(st, p)
+        if k in (0, 9):
+            xs.append(st.x.copy())
+    save("steps_c1.npz", x_step1=xs[0], x_step10=xs[1], fixed=fixed)
+    # extreme initialisation (BASELINE config 2 at reduced size)
+    m = generate_cube(6, 0.5, density=1000.0)
+    s = build_system([Body(m, MaterialParams(2e6, 1e7, 1e-6))])
+    rng = np.random.default_rng(0)
+    lo, hi = m.rest_positions.min(0), m.rest_positions.max(0)
+    x0 = rng.uniform(lo, hi, size=m.rest_positions.shape)
+    st = make_state(s, x0=x0)
+    p = SolverParams(h=1.0 / 60.0, n_max=100, rho=0.95, threads=1)
+    xs = []
+    for _ in range(3):
+        step(st, p)
+        xs.append(st.x.copy())
+    save("steps_extreme_cube6.npz", x0=x0, x=np.array(xs))
+
+
+if __name__ == "__main__":
+    mesh_fixture()
+    coloring_fixtures()
+    pass_fixture()
+    step_fixtures()
