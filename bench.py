@@ -1,0 +1,406 @@
+"""Benchmark of the B200 VBD hot path (BASELINE.json metric: vertex-iterations/s and
+ms/timestep at 1/2/4/8 B200 vs the CPU reference).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--precision fp32]
+    python bench.py --impl reference ...      # the reference's own CPU kernel (oracle/_ref)
+
+A "step" is one VBD time step (K2 init, n_max x (one colour pass per colour + Chebyshev),
+K4 commit) of the whole scene; value = total vertex-iterations (N x n_max per step, all
+ranks) / the max-over-ranks device time of the K timed steps.  The default workload is
+BASELINE config 5 (single 364^3 tet block, 48.2M vertices / 239.2M tets, S=4 -> h=1/240,
+n_max=40), which fits one B200; --config c4 is the 10,368-object scene.  Multi-GPU:
+one process per GPU (torchrun), slabs with a per-colour NCCL halo exchange (c5) or object
+shards with no data-path communication (c4).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "VBD vertex-iterations/sec and ms/timestep at 1/2/4/8 B200 vs CPU ref"
+UNIT = "vertex-iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink c4/c5 (tests only)")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------------------
+# CPU reference (oracle/_ref: the reference's own compiled kernel; else the oracle port)
+
+def cpu_reference_sample(cfg_name, budget_s=15.0):
+    """Time the reference's colour-pass kernel on a bounded sample of the workload.
+
+    The sample is a scaled-down scene of the same kind (same generator, material, h,
+    n_max, rho, constraints); vertex-iterations/s is size-independent to first order
+    (the reference has no cross-vertex reuse).  Threads: the reference as shipped takes
+    the GIL per tet inside its OpenMP loop, so it is timed at 1 thread and
+    at all host threads and the faster setting is reported with its core count.
+    """
+    from oracle import oracle as O
+    from paper_2403_06321_b200.scenes import config
+    cfg = config(cfg_name)
+    ref = O.ref_native()
+    kind = "reference" if ref is not None else "port"
+    b = cfg.beams[0]
+    if cfg_name in ("c4",):
+        meshes = [O.generate_beam(b.nx, b.ny, b.nz, b.spacing) for _ in range(8)]
+        sample = "8 of the 10,368 generate_cube(15,0.3) objects"
+    elif cfg_name == "c5":
+        n = 31
+        meshes = [O.generate_beam(n, n, n, b.spacing)]
+        sample = f"generate_beam({n},{n},{n},0.01) block (same material/h/n_max/BCs)"
+    elif cfg_name == "c3":
+        meshes = [O.generate_beam(300, 4, 4, b.spacing)]
+        sample = "generate_beam(300,4,4,0.01) (1/10 of one C3 beam)"
+    else:
+        meshes = [O.generate_beam(bb.nx, bb.ny, bb.nz, bb.spacing) for bb in cfg.beams]
+        sample = "full scene"
+    fixed = []
+    off = 0
+    for m, bb in zip(meshes, list(cfg.beams) * len(meshes)):
+        if bb.fix_min_x:
+            fixed.extend((off + np.flatnonzero(m.rest_positions[:, 0] < 1e-9)).tolist())
+        off += m.num_vertices
+    # place the sample bodies apart (no contact in any config)
+    shifted = []
+    for k, m in enumerate(meshes):
+        p = m.rest_positions + np.array([0.0, 0.0, 2.0 * k])
+        shifted.append(O.Mesh(p, m.tets, m.rest_volumes, m.inv_rest_shape, m.masses))
+    s = O.build_system([(m, (b.mu, b.lam, b.kd)) for m in shifted], fixed)
+    n_total = s.num_vertices
+    ncores = len(os.sched_getaffinity(0))
+
+    def one_step(st, threads):
+        t0 = time.perf_counter()
+        O.step(s, st, cfg.h, cfg.n_max, cfg.rho, cfg.a_ext, kernel=ref, n_threads=threads)
+        return time.perf_counter() - t0
+
+    def fresh():
+        st = O.make_state(s)
+        if cfg.random_init:
+            lo, hi = s.rest_positions.min(0), s.rest_positions.max(0)
+            x0 = np.random.default_rng(0).uniform(lo, hi, size=s.rest_positions.shape)
+            st = O.make_state(s, x0=x0)
+        return st
+
+    # probe thread settings with one step each, keep the faster
+    best = None
+    for threads in sorted({1, ncores}):
+        st = fresh()
+        dt = one_step(st, threads)
+        if best is None or dt < best[1]:
+            best = (threads, dt)
+    threads = best[0]
+    st = fresh()
+    one_step(st, threads)  # warm-up
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < 3 or (time.perf_counter() - t_start < budget_s and len(times) < 20):
+        times.append(one_step(st, threads))
+        if time.perf_counter() - t_start > 2 * budget_s:
+            break
+    ms = 1e3 * statistics.mean(times)
+    rate = n_total * cfg.n_max / (ms / 1e3)
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{sample}: {n_total} vertices, {len(s.tets)} tets, n_max={cfg.n_max}, "
+                      f"mean of {len(times)} steps after 1 warm-up, {ms:.1f} ms/step; "
+                      f"threads probed 1 and {ncores}, best={threads}",
+            "ms_per_step_sample": ms}
+
+
+# ----------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------------
+
+def algorithmic_bytes_per_iteration(info, precision):
+    """Compulsory DRAM bytes of the colour passes of one iteration:
+    per solved vertex 8 (CSR offset) + 3 x R4 reads (x, x_t, y) + 1 x R4 write,
+    per entry 48 B (fp32) / 96 B (fp64), plus one read of every other-colour position
+    (R4) per colour pass."""
+    r4 = 16 if precision == "fp32" else 32
+    eb = 48 if precision == "fp32" else 96
+    n_solved = int(info.num_solved)
+    n_all = int(info.num_vertices)
+    C = int(info.num_colors)
+    per_vertex = 8 + 4 * r4
+    other = sum(r4 * (n_all - int(info.color_count[c])) for c in range(min(C, 64)))
+    return n_solved * per_vertex + int(info.num_entries) * eb + other
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(cfg_name, precision):
+    p = ROOT / "profiles" / "k1_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return d.get(f"{cfg_name}_{precision}")
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2403_06321_b200.dist import SlabExchange
+    from paper_2403_06321_b200.scenes import build, config
+
+    cfg = config(args.config, args.scale)
+    t_build = time.perf_counter()
+    ctx, part = build(cfg, rank, world, args.precision, device=local)
+    t_build = time.perf_counter() - t_build
+    info = ctx.info
+    p = cfg.step_params()
+    exch = None
+    if world > 1 and cfg.sharding == "slabs":
+        exch = SlabExchange.distributed(ctx, rank, world)
+    stream = torch.cuda.ExternalStream(ctx.stream) if ctx.stream else torch.cuda.current_stream()
+
+    def do_steps(k):
+        if exch is None:
+            ctx.step(p, n_steps=k)
+        else:
+            for _ in range(k):
+                exch.step(p)
+
+    do_steps(args.warmup)
+    torch.cuda.synchronize()
+    n_owned = int(info.num_solved + info.num_fixed) if exch is None else \
+        (part[1] - part[0]) * cfg.beams[0].ny * cfg.beams[0].nz
+    tot = torch.tensor([float(n_owned)], device="cuda")
+    if world > 1:
+        dist.all_reduce(tot)
+    n_total = int(tot.item())
+
+    def timed(fn):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        t = torch.tensor([ms], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dist.barrier()
+        return float(t.item())
+
+    with Clocks(local) as clk:
+        ms_total = timed(lambda: do_steps(args.steps))
+    ms_step = ms_total / args.steps
+    vit_per_step = n_total * cfg.n_max
+    value = vit_per_step * args.steps / (ms_total / 1e3)
+
+    # dominant kernel (K1) live timing on the same stream: average per-colour launch time
+    k1_ms = ctx.profile_color_pass(cfg.h, reps=3)
+    bytes_iter = algorithmic_bytes_per_iteration(info, args.precision)
+    k1_iter_ms = float(np.sum(k1_ms))
+    peak, peak_kind = load_peaks()
+    achieved = bytes_iter / (k1_iter_ms / 1e3) / 1e9
+    launches_per_step = 1 + cfg.n_max * (int(info.num_colors) + (1 if cfg.rho else 0)) + 1
+    if exch is not None:
+        launches_per_step += cfg.n_max * int(info.num_colors) * 4
+
+    # end-to-end through the C ABI with host buffers: H2D of the step's inputs (x_t, v_t,
+    # v_prev, (N,3) float64, pinned) + step + D2H of the result (x, v_t)
+    n_loc = int(info.num_vertices)
+    pin = lambda: torch.empty((n_loc, 3), dtype=torch.float64, pin_memory=True).numpy()
+    hx, hxt, hv, hvp = pin(), pin(), pin(), pin()
+    got = ctx.get_state(x=True, x_t=True, v_t=True, v_prev=True,
+                        out={"x": hx, "x_t": hxt, "v_t": hv, "v_prev": hvp})
+
+    def e2e_steps():
+        for _ in range(args.e2e_steps):
+            ctx.set_state(x_t=hxt, v_t=hv, v_prev=hvp)
+            if exch is None:
+                ctx.step(p)
+            else:
+                exch.step(p)
+            ctx.get_state(x=True, v_t=True, out={"x": hx, "v_t": hv})
+            hvp[...] = hv  # host-side rotation, as the reference's SimState does
+            hxt[...] = hx
+    e2e_ms = timed(e2e_steps) / args.e2e_steps
+    e2e_value = vit_per_step / (e2e_ms / 1e3)
+    h2d = 3 * 24 * n_total
+    d2h = 2 * 24 * n_total
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(args.config, args.cpu_seconds)
+            cpu.pop("ms_per_step_sample", None)
+        except Exception as e:  # pragma: no cover - reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                   "sample": f"failed: {e}"}
+
+    clocks = clk.summary() if rank == 0 else None
+    if rank == 0:
+        b0 = cfg.beams[0]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if args.precision == "fp32" else "f64",
+            "data": "synthetic (procedural generate_beam/cube scene built on the device)",
+            "config": {
+                "workload": f"{cfg.name}: {cfg.description}",
+                "num_vertices": cfg.num_vertices, "num_tets": cfg.num_tets,
+                "h": cfg.h, "n_max": cfg.n_max, "rho": cfg.rho, "substeps_S": round(1 / (cfg.h * 60)),
+                "colors": int(info.num_colors),
+                "parallelism": (f"{cfg.sharding}x{world}" if world > 1 else "single GPU"),
+                "l2": "inputs larger than L2 (entry stream %.1f GB per GPU)"
+                      % (info.num_entries * (48 if args.precision == 'fp32' else 96) / 1e9)
+                      if info.num_entries * 48 > 126e6 else "scene fits in L2 (no flush)",
+                "build_s": round(t_build, 2),
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(cfg.name, args.precision),
+                         "kernel": "k1_color_pass", "peak_source": peak_kind,
+                         "k1_ms_per_color": [round(float(x), 4) for x in k1_ms],
+                         "algorithmic_bytes_per_iteration": bytes_iter},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2403_06321_b200.scenes import config
+    cfg = config(args.config)
+    budget = max(10.0, min(60.0, args.cpu_seconds))
+    r = cpu_reference_sample(args.config, budget)
+    ms_sample = r.pop("ms_per_step_sample")
+    vit = cfg.num_vertices * cfg.n_max
+    line = {
+        "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": vit / r["value"] * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generators), bounded sample; ms_per_step extrapolated "
+                "linearly from the sample's vertex-iterations/s",
+        "config": {"workload": f"{cfg.name}: {cfg.description}", "num_vertices": cfg.num_vertices,
+                   "num_tets": cfg.num_tets, "h": cfg.h, "n_max": cfg.n_max, "rho": cfg.rho},
+        "impl": "reference",
+        "cpu_baseline": r,
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    line["config"]["sample_ms_per_step"] = ms_sample
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,165 @@
+/*
+ * vbd_b200.h -- C ABI of the B200-native Vertex Block Descent hot path (libvbd_b200.so).
+ *
+ * Plain pointers and sizes only.  Every function returns VBD_OK (0) or a negative
+ * VBD_ERR_* code; vbd_last_error() returns a thread-local message for the last failure.
+ * Host arrays are C-contiguous, row-major, in the reference's original vertex numbering
+ * ((N,3) float64 positions, int64 indices) exactly as the reference's System/SimState hold
+ * them (/root/reference/pkg/src/vbdsim/_system.py:99-133, solver.py:88-108).
+ *
+ * Which reference interface each entry point replaces:
+ *   vbd_ctx_create      <- the flat arrays the reference's Cython kernel borrows per call
+ *                          (pkg/src/vbdsim/_native.pyx:525-575 SysData fill) -- compiled once
+ *                          into the device layout instead of per call
+ *   vbd_color_pass      <- backend.color_pass(system, carr, x, x_t, y, h, group, mode, ...)
+ *                          (pkg/src/vbdsim/_native.pyx:513-589; protocol of _backend.py:13-32)
+ *   vbd_step            <- vbdsim.step(state, params) (pkg/src/vbdsim/solver.py:291-324),
+ *                          device-resident: K2 init, n_max x (colour passes, K3), K4 commit
+ *   vbd_set_state /     <- SimState.x_t / v_t / v_prev / x / y (solver.py:88-108) crossing
+ *   vbd_get_state          the host<->device boundary
+ *   vbd_greedy_color    <- greedy_color(adjacency, order) (pkg/src/vbdsim/mesh.py:270-302)
+ *   vbd_ctx_create_beams<- generate_beam/generate_cube + build_tet_mesh + build_system for
+ *                          procedural scenes (harness.py:42-76, mesh.py:128-170,
+ *                          _system.py:204-303), built on the device for 10^7..10^8-vertex scenes
+ *   vbd_halo_*          <- (no reference counterpart: multi-GPU slab decomposition)
+ */
+#ifndef VBD_B200_H
+#define VBD_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VBD_OK 0
+#define VBD_ERR_ARG (-1)
+#define VBD_ERR_CUDA (-2)
+#define VBD_ERR_UNSUPPORTED (-3)
+#define VBD_ERR_NODEVICE (-5)
+#define VBD_ERR_INTERNAL (-6)
+
+#define VBD_PREC_F32 0
+#define VBD_PREC_F64 1
+
+#define VBD_KIND_FREE 0
+#define VBD_KIND_FIXED 1 /* _system.py:17 FIXED */
+#define VBD_KIND_SUBSPACE 2 /* rejected: not on the hot path */
+
+#define VBD_INIT_PREV_POS 0 /* solver.py:25 INIT_MODES */
+#define VBD_INIT_INERTIA 1
+#define VBD_INIT_INERTIA_ACCEL 2
+#define VBD_INIT_ADAPTIVE 3
+
+typedef struct vbd_ctx vbd_ctx;
+
+/* The reference System arrays (tets-only scenes).  Borrowed for the call only. */
+typedef struct {
+    int64_t num_vertices;
+    int64_t num_tets;
+    const int64_t* tets;        /* (T,4) */
+    const double* tet_w;        /* (T,4,3) slot weight rows */
+    const double* tet_vol;      /* (T,) */
+    const double* tet_mu;       /* (T,) */
+    const double* tet_lam;      /* (T,) */
+    const double* tet_kd;       /* (T,) */
+    const double* masses;       /* (N,) */
+    const uint8_t* kind;        /* (N,) 0 free, 1 fixed; NULL = all free */
+    const int64_t* t_off;       /* (N+1,) vertex->tet CSR, ascending tet id per vertex */
+    const int64_t* t_id;        /* (4T,) */
+    const int64_t* t_slot;      /* (4T,) */
+    int64_t num_colors;
+    const int64_t* color_off;   /* (C+1,) */
+    const int64_t* color_verts; /* (N,) colour groups, concatenated */
+} vbd_system_desc;
+
+/* A procedural generate_beam(nx, ny, nz, spacing, density) body, rigidly translated. */
+typedef struct {
+    int64_t nx, ny, nz;
+    double spacing;
+    double density;
+    double origin[3];
+    double mu, lam, kd;
+    int32_t fix_min_x; /* FixedConstraint on every vertex with (x - origin.x) < 1e-9 */
+    int32_t reserved;
+} vbd_beam_desc;
+
+typedef struct {
+    double h;
+    int32_t n_max;
+    int32_t init_mode;
+    double rho;
+    double eps_det;
+    double a_ext[3];
+} vbd_step_params;
+
+typedef struct {
+    int32_t nonfinite;  /* 1 if a non-finite position was detected (step not committed) */
+    int32_t step;       /* step (0-based, within this call) of the first detection */
+    int32_t iteration;  /* iteration (1-based) of the first detection */
+    int32_t reserved;
+    int64_t vertex;     /* smallest original vertex id that was non-finite then */
+} vbd_step_result;
+
+typedef struct {
+    int64_t num_vertices, num_solved, num_ghost, num_fixed;
+    int64_t num_tets, num_entries;
+    int64_t num_colors;
+    int64_t color_count[64];   /* solved vertices per colour (first 64 colours) */
+    int64_t device_bytes;
+    int32_t precision;
+    int32_t inplace;           /* 1 = colouring valid -> in-place colour sweeps */
+    int32_t lanes_per_vertex;
+    int32_t num_materials;
+} vbd_ctx_info;
+
+/* ---- context ---------------------------------------------------------------------------- */
+int vbd_device_count(int* count);
+int vbd_ctx_create(const vbd_system_desc* desc, int device, int precision, vbd_ctx** out);
+int vbd_ctx_create_beams(const vbd_beam_desc* beams, int64_t num_beams, int64_t slab_lo,
+                         int64_t slab_hi, int device, int precision, vbd_ctx** out);
+int vbd_ctx_destroy(vbd_ctx* ctx);
+int vbd_ctx_get_info(vbd_ctx* ctx, vbd_ctx_info* info);
+int vbd_set_stream(vbd_ctx* ctx, void* cuda_stream); /* NULL = the context's own stream */
+int vbd_get_stream(vbd_ctx* ctx, void** cuda_stream);
+int vbd_get_colors(vbd_ctx* ctx, int64_t* color_of); /* (N,) original numbering */
+
+/* ---- state (host <-> device, original numbering, (N,3) float64) ------------------------- */
+int vbd_set_state(vbd_ctx* ctx, const double* x, const double* x_t, const double* v_t,
+                  const double* v_prev, const double* y); /* NULL = leave unchanged */
+int vbd_get_state(vbd_ctx* ctx, double* x, double* x_t, double* v_t, double* v_prev, double* y);
+int vbd_set_beam_velocities(vbd_ctx* ctx, const double* lin_ang); /* (num_beams,6) rigid v */
+
+/* ---- the hot path ----------------------------------------------------------------------- */
+int vbd_step(vbd_ctx* ctx, const vbd_step_params* params, int32_t n_steps, vbd_step_result* res);
+int vbd_color_pass(vbd_ctx* ctx, double* x_inout, const double* x_t, const double* y, double h,
+                   const int64_t* group, int64_t ng, int32_t mode, int32_t line_search,
+                   double eps_det);
+
+/* K2 only: y = inertia target and the warm start of solver.py:125-164 into x (no sweeps) */
+int vbd_initialize(vbd_ctx* ctx, const vbd_step_params* params);
+
+/* fine-grained step for multi-GPU slabs (halo exchange between colour passes) */
+int vbd_step_begin(vbd_ctx* ctx, const vbd_step_params* params);
+int vbd_step_color(vbd_ctx* ctx, int32_t color, int32_t iteration);
+int vbd_step_iter_end(vbd_ctx* ctx, int32_t iteration);
+int vbd_step_end(vbd_ctx* ctx, vbd_step_result* res);
+int vbd_halo_count(vbd_ctx* ctx, int32_t side, int32_t color, int64_t* n_send, int64_t* n_recv);
+int vbd_halo_pack(vbd_ctx* ctx, int32_t side, int32_t color, void* dev_buf);
+int vbd_halo_unpack(vbd_ctx* ctx, int32_t side, int32_t color, const void* dev_buf);
+
+/* ---- colouring (K5, device Jones-Plassmann == reference greedy) ------------------------- */
+int vbd_greedy_color(int64_t n, const int64_t* noff, const int64_t* nids, const int64_t* order,
+                     int device, int64_t* color_of, int64_t* num_colors);
+
+/* ---- measurement ------------------------------------------------------------------------ */
+/* average device time of one colour-pass launch per colour over `reps` sweeps (CUDA events on
+ * the context stream); ms has room for num_colors values */
+int vbd_profile_color_pass(vbd_ctx* ctx, double h, int32_t reps, double* ms);
+
+const char* vbd_last_error(void);
+const char* vbd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

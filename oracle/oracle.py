@@ -351,6 +351,8 @@ class RefSystemView:
         self.masses, self.tets, self.tet_w = s.masses, s.tets, s.tet_w
         self.tet_vol, self.tet_mu, self.tet_lam, self.tet_kd = s.tet_vol, s.tet_mu, s.tet_lam, s.tet_kd
         self.t_off, self.t_id, self.t_slot = s.t_off, s.t_id, s.t_slot
+        self.color_off, self.color_verts = s.color_off, s.color_verts
+        self.rest_positions = s.rest_positions
         self.springs = np.zeros((0, 2), dtype=np.int64)
         self.sp_l0 = self.sp_k = self.sp_kd = np.zeros(0)
         self.s_off = np.zeros(n + 1, dtype=np.int64)

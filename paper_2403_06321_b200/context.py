@@ -1,0 +1,229 @@
+"""DeviceContext: one packed scene resident on one B200 (wraps ``vbd_ctx*``).
+
+Built either from reference-layout System arrays (duck-typed: a System of this
+package *or* of the reference package works) or from procedural beams generated
+on the device (BASELINE configs C4/C5, tens of millions of vertices).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import NonFiniteState
+
+FIXED, SUBSPACE = 1, 2
+
+
+@dataclass(frozen=True)
+class Beam:
+    """generate_beam(nx, ny, nz, spacing, density) translated by origin, with a material."""
+
+    nx: int
+    ny: int
+    nz: int
+    spacing: float
+    mu: float
+    lam: float
+    kd: float = 0.0
+    density: float = 1000.0
+    origin: tuple = (0.0, 0.0, 0.0)
+    fix_min_x: bool = False
+
+    def desc(self):
+        d = _lib.BeamDesc()
+        d.nx, d.ny, d.nz = self.nx, self.ny, self.nz
+        d.spacing, d.density = self.spacing, self.density
+        d.origin = (ctypes.c_double * 3)(*map(float, self.origin))
+        d.mu, d.lam, d.kd = self.mu, self.lam, self.kd
+        d.fix_min_x = 1 if self.fix_min_x else 0
+        return d
+
+    @property
+    def num_vertices(self):
+        return self.nx * self.ny * self.nz
+
+    @property
+    def num_tets(self):
+        return 5 * (self.nx - 1) * (self.ny - 1) * (self.nz - 1)
+
+
+def _unsupported_terms(system):
+    if len(getattr(system, "springs", ())):
+        raise NotImplementedError("springs are not on the B200 hot path")
+    cons = system.cons
+    if np.any(cons.kind == SUBSPACE):
+        raise NotImplementedError("SubspaceConstraint is not on the B200 hot path")
+    if np.any(np.asarray(cons.box_k) > 0.0):
+        raise NotImplementedError("WorldBoxConstraint is not on the B200 hot path")
+
+
+class DeviceContext:
+    def __init__(self, handle, keepalive=None):
+        self._h = ctypes.c_void_p(handle)
+        self._keep = keepalive
+        self.info = self._info()
+        self.n = self.info.num_vertices
+
+    # -- construction -----------------------------------------------------------------
+    @classmethod
+    def from_system(cls, system, precision="fp64", device=0):
+        _unsupported_terms(system)
+        n = int(system.num_vertices)
+        arrs = dict(
+            tets=_lib.i64c(system.tets).reshape(-1, 4),
+            tet_w=_lib.f64c(system.tet_w).reshape(-1, 4, 3),
+            tet_vol=_lib.f64c(system.tet_vol), tet_mu=_lib.f64c(system.tet_mu),
+            tet_lam=_lib.f64c(system.tet_lam), tet_kd=_lib.f64c(system.tet_kd),
+            masses=_lib.f64c(system.masses),
+            kind=np.ascontiguousarray(system.cons.kind, dtype=np.uint8),
+            t_off=_lib.i64c(system.t_off), t_id=_lib.i64c(system.t_id),
+            t_slot=_lib.i64c(system.t_slot), color_off=_lib.i64c(system.color_off),
+            color_verts=_lib.i64c(system.color_verts))
+        d = _lib.SystemDesc()
+        d.num_vertices = n
+        d.num_tets = len(arrs["tets"])
+        for k, v in arrs.items():
+            setattr(d, k, _lib.ptr(v))
+        d.num_colors = len(arrs["color_off"]) - 1
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().vbd_ctx_create(ctypes.byref(d), device, _lib.PREC[precision],
+                                             ctypes.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_beams(cls, beams, precision="fp32", device=0, slab=None):
+        arr = (_lib.BeamDesc * len(beams))(*[b.desc() for b in beams])
+        lo, hi = (0, 0) if slab is None else slab
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().vbd_ctx_create_beams(arr, len(beams), lo, hi, device,
+                                                   _lib.PREC[precision], ctypes.byref(h)))
+        return cls(h.value, keepalive=list(beams))
+
+    def close(self):
+        if self._h and self._h.value:
+            _lib.check(_lib.lib().vbd_ctx_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- info ---------------------------------------------------------------------------
+    def _info(self):
+        i = _lib.CtxInfo()
+        _lib.check(_lib.lib().vbd_ctx_get_info(self._h, ctypes.byref(i)))
+        return i
+
+    @property
+    def num_colors(self):
+        return int(self.info.num_colors)
+
+    def color_counts(self):
+        return [int(self.info.color_count[k]) for k in range(min(self.num_colors, 64))]
+
+    def colors(self):
+        out = np.empty(self.n, dtype=np.int64)
+        _lib.check(_lib.lib().vbd_get_colors(self._h, _lib.ptr(out)))
+        return out
+
+    @property
+    def stream(self):
+        s = ctypes.c_void_p()
+        _lib.check(_lib.lib().vbd_get_stream(self._h, ctypes.byref(s)))
+        return s.value or 0
+
+    def set_stream(self, handle):
+        _lib.check(_lib.lib().vbd_set_stream(self._h, ctypes.c_void_p(handle or None)))
+
+    # -- state --------------------------------------------------------------------------
+    def set_state(self, x=None, x_t=None, v_t=None, v_prev=None, y=None):
+        shape = (self.n, 3)
+        arrs = [None if a is None else _lib.f64c(a, shape) for a in (x, x_t, v_t, v_prev, y)]
+        _lib.check(_lib.lib().vbd_set_state(self._h, *[_lib.ptr(a) for a in arrs]))
+
+    def get_state(self, x=True, x_t=False, v_t=False, v_prev=False, y=False, out=None):
+        names = ("x", "x_t", "v_t", "v_prev", "y")
+        want = dict(zip(names, (x, x_t, v_t, v_prev, y)))
+        res = {}
+        for k in names:
+            if want[k]:
+                res[k] = out[k] if out is not None and k in out else np.empty((self.n, 3))
+        _lib.check(_lib.lib().vbd_get_state(self._h, *[_lib.ptr(res.get(k)) for k in names]))
+        return res
+
+    def set_beam_velocities(self, lin_ang):
+        a = _lib.f64c(lin_ang)
+        _lib.check(_lib.lib().vbd_set_beam_velocities(self._h, _lib.ptr(a)))
+
+    # -- hot path -----------------------------------------------------------------------
+    @staticmethod
+    def step_params(h, n_max, rho=0.0, eps_det=1e-10, init_mode="adaptive", a_ext=(0, 0, 0)):
+        p = _lib.StepParams()
+        p.h, p.n_max, p.rho, p.eps_det = float(h), int(n_max), float(rho), float(eps_det)
+        p.init_mode = _lib.INIT_MODES[init_mode]
+        p.a_ext = (ctypes.c_double * 3)(*map(float, a_ext))
+        return p
+
+    def step(self, params, n_steps=1, step_index=0):
+        r = _lib.StepResult()
+        _lib.check(_lib.lib().vbd_step(self._h, ctypes.byref(params), int(n_steps),
+                                       ctypes.byref(r)))
+        if r.nonfinite:
+            raise NonFiniteState("non-finite vertex position", step=step_index + r.step,
+                                 iteration=r.iteration, vertex=int(r.vertex))
+        return r
+
+    def initialize(self, params):
+        _lib.check(_lib.lib().vbd_initialize(self._h, ctypes.byref(params)))
+
+    def step_begin(self, params):
+        _lib.check(_lib.lib().vbd_step_begin(self._h, ctypes.byref(params)))
+
+    def step_color(self, color, iteration):
+        _lib.check(_lib.lib().vbd_step_color(self._h, int(color), int(iteration)))
+
+    def step_iter_end(self, iteration):
+        _lib.check(_lib.lib().vbd_step_iter_end(self._h, int(iteration)))
+
+    def step_end(self, step_index=0, raise_nonfinite=True):
+        r = _lib.StepResult()
+        _lib.check(_lib.lib().vbd_step_end(self._h, ctypes.byref(r)))
+        if r.nonfinite and raise_nonfinite:
+            raise NonFiniteState("non-finite vertex position", step=step_index,
+                                 iteration=r.iteration, vertex=int(r.vertex))
+        return r
+
+    def color_pass(self, x, x_t, y, h, group, mode=0, line_search=False, eps_det=1e-10):
+        if x.dtype != np.float64 or not x.flags["C_CONTIGUOUS"]:
+            raise TypeError("x must be C-contiguous float64")  # _native.pyx:522-523
+        g = _lib.i64c(group).ravel()
+        xt = _lib.f64c(x_t, x.shape)
+        yy = _lib.f64c(y, x.shape)
+        _lib.check(_lib.lib().vbd_color_pass(self._h, _lib.ptr(x), _lib.ptr(xt), _lib.ptr(yy),
+                                             float(h), _lib.ptr(g), len(g), int(mode),
+                                             1 if line_search else 0, float(eps_det)))
+
+    # -- halo (multi-GPU slabs) ---------------------------------------------------------
+    def halo_count(self, side, color):
+        ns, nr = ctypes.c_int64(0), ctypes.c_int64(0)
+        _lib.check(_lib.lib().vbd_halo_count(self._h, side, color, ctypes.byref(ns),
+                                             ctypes.byref(nr)))
+        return ns.value, nr.value
+
+    def halo_pack(self, side, color, dev_ptr):
+        _lib.check(_lib.lib().vbd_halo_pack(self._h, side, color, ctypes.c_void_p(dev_ptr)))
+
+    def halo_unpack(self, side, color, dev_ptr):
+        _lib.check(_lib.lib().vbd_halo_unpack(self._h, side, color, ctypes.c_void_p(dev_ptr)))
+
+    # -- measurement --------------------------------------------------------------------
+    def profile_color_pass(self, h, reps=5):
+        ms = np.zeros(max(self.num_colors, 1))
+        _lib.check(_lib.lib().vbd_profile_color_pass(self._h, float(h), int(reps), _lib.ptr(ms)))
+        return ms[: self.num_colors]

@@ -1,0 +1,394 @@
+// vbd_build.cuh -- one-off scene construction on the device:
+//   * procedural beams/cubes (generate_beam, harness.py:42-76) incl. the orientation fix,
+//     Dm^-1, volumes and slot-weight rows of build_tet_mesh / _slot_weight_rows
+//     (mesh.py:128-170, _system.py:139-144);
+//   * vertex->tet incidence (mesh.py:232-267) and lumped masses (mesh.py:161-162);
+//   * distinct-neighbour CSR (_system.py:147-169) and the K5 Jones-Plassmann colouring whose
+//     priority (-degree, index) reproduces greedy_color (mesh.py:270-302) bit-exactly;
+//   * K6: the colour-major re-pack into the entry planes consumed by K1.
+#pragma once
+#include "vbd_common.cuh"
+
+// ---------------------------------------------------------------------------------------
+// procedural beams
+
+struct BeamDev {
+    long long nx, ny, nz;
+    long long ax0, ax1;   // vertex planes generated: [ax0, ax1] inclusive (slab incl. ghosts)
+    long long vbase;      // first local vertex id of this beam
+    long long tbase;      // first local tet id
+    long long gcell0;     // first global cell x index generated (cells [gcell0, ax1-1])
+    double spacing, density;
+    double origin[3];
+    int mat;
+    int fix_min_x;
+};
+
+__constant__ int c_cell_even[5][4] = {{0, 3, 5, 6}, {1, 0, 3, 5}, {2, 0, 3, 6}, {4, 0, 5, 6}, {7, 3, 5, 6}};
+__constant__ int c_cell_odd[5][4] = {{1, 2, 4, 7}, {0, 1, 2, 4}, {3, 1, 2, 7}, {5, 1, 4, 7}, {6, 2, 4, 7}};
+
+__device__ __forceinline__ int find_beam(const BeamDev* b, int nb, long long key, bool by_tet)
+{
+    int lo = 0, hi = nb - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        long long base = by_tet ? b[mid].tbase : b[mid].vbase;
+        if (base <= key) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void k_gen_vertices(const BeamDev* __restrict__ beams, int nb, long long n,
+                               double* __restrict__ pos, unsigned char* __restrict__ kind)
+{
+    long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const BeamDev& B = beams[find_beam(beams, nb, v, false)];
+    long long l = v - B.vbase;
+    long long az = l % B.nz, ay = (l / B.nz) % B.ny, ax = B.ax0 + l / (B.nz * B.ny);
+    // harness.py:50-51: spacing * (ix, iy, iz), then the rigid translation
+    double px = B.spacing * (double)ax, py = B.spacing * (double)ay, pz = B.spacing * (double)az;
+    pos[3 * v] = px + B.origin[0];
+    pos[3 * v + 1] = py + B.origin[1];
+    pos[3 * v + 2] = pz + B.origin[2];
+    kind[v] = (B.fix_min_x && px < 1e-9) ? 1 : 0;
+}
+
+// Tets of the generated cells in global (cell-major, then pattern) order, with the
+// orientation fix of mesh.py:147-152, Dm^-1 (mesh.py:158-159), |V| (mesh.py:147) and the
+// slot-weight rows w_0 = -sum(Dm^-1 rows), w_{k+1} = row k (_system.py:139-144).
+__global__ void k_gen_tets(const BeamDev* __restrict__ beams, int nb, long long T,
+                           const double* __restrict__ pos, int* __restrict__ tets,
+                           double* __restrict__ tet_w, double* __restrict__ vol,
+                           int* __restrict__ tmat)
+{
+    long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const BeamDev& B = beams[find_beam(beams, nb, t, true)];
+    long long l = t - B.tbase;
+    long long cell = l / 5;
+    int j = (int)(l % 5);
+    long long ncz = B.nz - 1, ncy = B.ny - 1;
+    long long cz = cell % ncz, cy = (cell / ncz) % ncy, cx = B.gcell0 + cell / (ncz * ncy);
+    const int(*pat)[4] = ((cx + cy + cz) % 2 == 0) ? c_cell_even : c_cell_odd;
+    long long vid[4];
+    for (int k = 0; k < 4; ++k) {
+        int c = pat[j][k];
+        int dx = c >> 2, dy = (c >> 1) & 1, dz = c & 1;
+        vid[k] = B.vbase + ((cx + dx - B.ax0) * B.ny + (cy + dy)) * B.nz + (cz + dz);
+    }
+    double D[9];  // columns = edges x_{k} - x_0, D[a*3+k]
+    for (int k = 0; k < 3; ++k)
+        for (int a = 0; a < 3; ++a) D[a * 3 + k] = pos[3 * vid[k + 1] + a] - pos[3 * vid[0] + a];
+    double det = D[0] * (D[4] * D[8] - D[5] * D[7]) - D[1] * (D[3] * D[8] - D[5] * D[6]) +
+                 D[2] * (D[3] * D[7] - D[4] * D[6]);
+    if (det < 0.0) {  // swap slots 1 and 2: [0, 2, 1, 3]
+        long long tmp = vid[1]; vid[1] = vid[2]; vid[2] = tmp;
+        for (int a = 0; a < 3; ++a) {
+            double s = D[a * 3 + 0]; D[a * 3 + 0] = D[a * 3 + 1]; D[a * 3 + 1] = s;
+        }
+        det = -det;
+    }
+    double inv[9];
+    inv[0] = (D[4] * D[8] - D[5] * D[7]) / det;
+    inv[1] = (D[2] * D[7] - D[1] * D[8]) / det;
+    inv[2] = (D[1] * D[5] - D[2] * D[4]) / det;
+    inv[3] = (D[5] * D[6] - D[3] * D[8]) / det;
+    inv[4] = (D[0] * D[8] - D[2] * D[6]) / det;
+    inv[5] = (D[2] * D[3] - D[0] * D[5]) / det;
+    inv[6] = (D[3] * D[7] - D[4] * D[6]) / det;
+    inv[7] = (D[1] * D[6] - D[0] * D[7]) / det;
+    inv[8] = (D[0] * D[4] - D[1] * D[3]) / det;
+    for (int k = 0; k < 4; ++k) tets[4 * t + k] = (int)vid[k];
+    double* w = tet_w + 12 * t;
+    for (int b = 0; b < 3; ++b) {
+        w[3 + b] = inv[b];
+        w[6 + b] = inv[3 + b];
+        w[9 + b] = inv[6 + b];
+        w[b] = -((inv[b] + inv[3 + b]) + inv[6 + b]);
+    }
+    vol[t] = det / 6.0;
+    tmat[t] = B.mat;
+}
+
+// ---------------------------------------------------------------------------------------
+// incidence: keys = vertex of each (tet, slot), values = 4 t + s; a stable radix sort by key
+// gives the reference's lexsort((eids, verts)) order (mesh.py:243-250).
+
+__global__ void k_inc_keys(const int* __restrict__ tets, long long n4, int* __restrict__ keys,
+                           unsigned* __restrict__ vals, int* __restrict__ count)
+{
+    long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= n4) return;
+    int v = tets[k];
+    keys[k] = v;
+    vals[k] = (unsigned)k;
+    atomicAdd(count + v, 1);
+}
+
+// lumped masses rho V / 4 accumulated in ascending tet order per vertex (mesh.py:161-162)
+__global__ void k_mass_gather(const long long* __restrict__ off, const unsigned* __restrict__ inc,
+                              const double* __restrict__ vol, const int* __restrict__ tmat,
+                              const double* __restrict__ density_of_mat, long long n,
+                              double* __restrict__ mass)
+{
+    long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    double m = 0.0;
+    for (long long k = off[v]; k < off[v + 1]; ++k) {
+        long long t = inc[k] >> 2;
+        m = m + (density_of_mat[tmat[t]] * vol[t]) / 4.0;
+    }
+    mass[v] = m;
+}
+
+// ---------------------------------------------------------------------------------------
+// distinct neighbours from the incidence (per-vertex sort + unique in registers/local mem)
+
+#define VBD_MAX_NBR_CAND 384
+
+__device__ int gather_neighbours(long long v, const long long* off, const unsigned* inc,
+                                 const int* tets, int* cand)
+{
+    int c = 0;
+    for (long long k = off[v]; k < off[v + 1] && c + 3 <= VBD_MAX_NBR_CAND; ++k) {
+        long long t = inc[k] >> 2;
+        for (int s = 0; s < 4; ++s) {
+            int u = tets[4 * t + s];
+            if (u != v) cand[c++] = u;
+        }
+    }
+    // insertion sort (small) then unique
+    for (int i = 1; i < c; ++i) {
+        int x = cand[i], j = i - 1;
+        while (j >= 0 && cand[j] > x) { cand[j + 1] = cand[j]; --j; }
+        cand[j + 1] = x;
+    }
+    int u = 0;
+    for (int i = 0; i < c; ++i)
+        if (u == 0 || cand[u - 1] != cand[i]) cand[u++] = cand[i];
+    return u;
+}
+
+__global__ void k_nbr_count(const long long* __restrict__ off, const unsigned* __restrict__ inc,
+                            const int* __restrict__ tets, long long n, int* __restrict__ cnt,
+                            int* __restrict__ overflow)
+{
+    long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    if ((off[v + 1] - off[v]) * 3 > VBD_MAX_NBR_CAND) atomicExch(overflow, 1);
+    int cand[VBD_MAX_NBR_CAND];
+    cnt[v] = gather_neighbours(v, off, inc, tets, cand);
+}
+
+__global__ void k_nbr_fill(const long long* __restrict__ off, const unsigned* __restrict__ inc,
+                           const int* __restrict__ tets, long long n, const long long* __restrict__ noff,
+                           int* __restrict__ nids)
+{
+    long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int cand[VBD_MAX_NBR_CAND];
+    int c = gather_neighbours(v, off, inc, tets, cand);
+    for (int i = 0; i < c; ++i) nids[noff[v] + i] = cand[i];
+}
+
+// ---------------------------------------------------------------------------------------
+// K5: Jones-Plassmann colouring with the greedy order as priority.  Vertex u precedes v iff
+// rank(u) < rank(v), rank = position in lexsort((index, -degree)) (mesh.py:277-278) or a
+// caller-given order.  A vertex is coloured once all preceding neighbours are, with the
+// smallest colour they do not use -- exactly what the sequential greedy assigns.
+
+__device__ __forceinline__ bool precedes(long long u, long long v, const long long* noff,
+                                         const long long* rank)
+{
+    if (rank) return rank[u] < rank[v];
+    long long du = noff[u + 1] - noff[u], dv = noff[v + 1] - noff[v];
+    return du > dv || (du == dv && u < v);
+}
+
+__global__ void k_jp_init(const long long* __restrict__ noff, const int* __restrict__ nids,
+                          const long long* __restrict__ rank, long long n, int* __restrict__ pending,
+                          int* __restrict__ color, int* __restrict__ frontier, int* __restrict__ fcount)
+{
+    long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int p = 0;
+    for (long long k = noff[v]; k < noff[v + 1]; ++k)
+        if (precedes(nids[k], v, noff, rank)) ++p;
+    pending[v] = p;
+    color[v] = -1;
+    if (p == 0) frontier[atomicAdd(fcount, 1)] = (int)v;
+}
+
+__global__ void k_jp_round(const long long* __restrict__ noff, const int* __restrict__ nids,
+                           const long long* __restrict__ rank, const int* __restrict__ fin,
+                           const int* __restrict__ fin_count, int* __restrict__ pending,
+                           int* __restrict__ color, int* __restrict__ fout, int* __restrict__ fout_count,
+                           unsigned long long* __restrict__ colored, int* __restrict__ overflow)
+{
+    const int cnt = *fin_count;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < cnt; idx += gridDim.x * blockDim.x) {
+        const int v = fin[idx];
+        unsigned long long used[4] = {0ull, 0ull, 0ull, 0ull};
+        for (long long k = noff[v]; k < noff[v + 1]; ++k) {
+            int u = nids[k];
+            if (precedes(u, v, noff, rank)) {
+                int c = color[u];
+                if (c < 256) used[c >> 6] |= 1ull << (c & 63);
+                else atomicExch(overflow, 1);
+            }
+        }
+        int c = 0;
+        while (c < 256 && ((used[c >> 6] >> (c & 63)) & 1ull)) ++c;
+        if (c >= 256) atomicExch(overflow, 1);
+        color[v] = c;
+        atomicAdd(colored, 1ull);
+        for (long long k = noff[v]; k < noff[v + 1]; ++k) {
+            int u = nids[k];
+            if (precedes(v, u, noff, rank))
+                if (atomicSub(pending + u, 1) == 1) fout[atomicAdd(fout_count, 1)] = u;
+        }
+    }
+}
+
+// a colouring is valid for in-place sweeps iff no tet repeats a colour (oracles.py:175-181)
+__global__ void k_check_coloring(const int* __restrict__ tets, long long T, const int* __restrict__ color,
+                                 int* __restrict__ bad)
+{
+    long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    int c0 = color[tets[4 * t]], c1 = color[tets[4 * t + 1]], c2 = color[tets[4 * t + 2]],
+        c3 = color[tets[4 * t + 3]];
+    if (c0 == c1 || c0 == c2 || c0 == c3 || c1 == c2 || c1 == c3 || c2 == c3) atomicExch(bad, 1);
+}
+
+// ---------------------------------------------------------------------------------------
+// K6: colour-major order and entry packing
+
+// sort key: category (0 solved, 1 ghost, 2 fixed) | colour | rounds | original id
+__global__ void k_order_keys(const long long* __restrict__ off, const unsigned char* __restrict__ kind,
+                             const int* __restrict__ color, long long n, int W,
+                             unsigned long long* __restrict__ keys)
+{
+    long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    unsigned long long cat = kind[v] == 1 ? 2ull : (kind[v] == 3 ? 1ull : 0ull);
+    unsigned long long c = (unsigned long long)(color[v] < 0 ? 0 : color[v]) & 0xfffull;
+    long long d = off[v + 1] - off[v];
+    unsigned long long r = cat == 0 ? (unsigned long long)((d + W - 1) / W) & 0xfffull : 0ull;
+    keys[v] = (cat << 56) | (c << 44) | (r << 32) | (unsigned long long)v;
+}
+
+__global__ void k_perm_from_keys(const unsigned long long* __restrict__ keys, long long n,
+                                 int* __restrict__ perm, int* __restrict__ inv)
+{
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int o = (int)(keys[i] & 0xffffffffull);
+    perm[i] = o;
+    inv[o] = (int)i;
+}
+
+__global__ void k_degree_new(const long long* __restrict__ off, const int* __restrict__ perm,
+                             long long nsolve, long long* __restrict__ deg)
+{
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nsolve) return;
+    int o = perm[i];
+    deg[i] = off[o + 1] - off[o];
+}
+
+template <typename R>
+__global__ void k_pack_entries(const long long* __restrict__ off, const unsigned* __restrict__ inc,
+                               const int* __restrict__ tets, const double* __restrict__ tet_w,
+                               const double* __restrict__ vol, const int* __restrict__ tmat,
+                               const int* __restrict__ perm, const int* __restrict__ inv,
+                               const long long* __restrict__ eoff, long long nsolve,
+                               typename PlaneT<R>::T* __restrict__ planes, long long E,
+                               int* __restrict__ bad_volume);
+
+template <>
+__global__ void k_pack_entries<float>(const long long* __restrict__ off, const unsigned* __restrict__ inc,
+                                      const int* __restrict__ tets, const double* __restrict__ tet_w,
+                                      const double* __restrict__ vol, const int* __restrict__ tmat,
+                                      const int* __restrict__ perm, const int* __restrict__ inv,
+                                      const long long* __restrict__ eoff, long long nsolve,
+                                      float4* __restrict__ planes, long long E,
+                                      int* __restrict__ bad_volume)
+{
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nsolve) return;
+    int o = perm[i];
+    long long base = eoff[i];
+    for (long long k = off[o]; k < off[o + 1]; ++k, ++base) {
+        unsigned val = inc[k];
+        long long t = val >> 2;
+        int s = (int)(val & 3u);
+        int ks[3], j = 0;
+        for (int q = 0; q < 4; ++q)
+            if (q != s) ks[j++] = q;
+        unsigned n[3];
+        double w[9];
+        for (j = 0; j < 3; ++j) {
+            n[j] = (unsigned)inv[tets[4 * t + ks[j]]];
+            for (int b = 0; b < 3; ++b) w[3 * j + b] = tet_w[12 * t + 3 * ks[j] + b];
+        }
+        // fp32 layout recomputes V from |det W| = 1/(6V): verify the inputs agree
+        double d = w[0] * (w[4] * w[8] - w[5] * w[7]) - w[1] * (w[3] * w[8] - w[5] * w[6]) +
+                   w[2] * (w[3] * w[7] - w[4] * w[6]);
+        double vr = 1.0 / (6.0 * fabs(d));
+        if (!(fabs(vr / vol[t] - 1.0) < 1e-5)) atomicExch(bad_volume, 1);
+        unsigned m = (unsigned)tmat[t];
+        unsigned u0 = n[0] | ((m & 7u) << VBD_ID_BITS);
+        unsigned u1 = n[1] | (((m >> 3) & 7u) << VBD_ID_BITS);
+        unsigned u2 = n[2] | (((m >> 6) & 7u) << VBD_ID_BITS);
+        planes[base] = make_float4(__uint_as_float(u0), __uint_as_float(u1), __uint_as_float(u2),
+                                   (float)w[0]);
+        planes[E + base] = make_float4((float)w[1], (float)w[2], (float)w[3], (float)w[4]);
+        planes[2 * E + base] = make_float4((float)w[5], (float)w[6], (float)w[7], (float)w[8]);
+    }
+}
+
+template <>
+__global__ void k_pack_entries<double>(const long long* __restrict__ off, const unsigned* __restrict__ inc,
+                                       const int* __restrict__ tets, const double* __restrict__ tet_w,
+                                       const double* __restrict__ vol, const int* __restrict__ tmat,
+                                       const int* __restrict__ perm, const int* __restrict__ inv,
+                                       const long long* __restrict__ eoff, long long nsolve,
+                                       double2* __restrict__ planes, long long E,
+                                       int* __restrict__ bad_volume)
+{
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nsolve) return;
+    int o = perm[i];
+    long long base = eoff[i];
+    for (long long k = off[o]; k < off[o + 1]; ++k, ++base) {
+        unsigned val = inc[k];
+        long long t = val >> 2;
+        int s = (int)(val & 3u);
+        int ks[3], j = 0;
+        for (int q = 0; q < 4; ++q)
+            if (q != s) ks[j++] = q;
+        int n[3];
+        double w[9];
+        for (j = 0; j < 3; ++j) {
+            n[j] = inv[tets[4 * t + ks[j]]];
+            for (int b = 0; b < 3; ++b) w[3 * j + b] = tet_w[12 * t + 3 * ks[j] + b];
+        }
+        reinterpret_cast<int4*>(planes)[base] = make_int4(n[0], n[1], n[2], tmat[t]);
+        planes[E + base] = make_double2(w[0], w[1]);
+        planes[2 * E + base] = make_double2(w[2], w[3]);
+        planes[3 * E + base] = make_double2(w[4], w[5]);
+        planes[4 * E + base] = make_double2(w[6], w[7]);
+        planes[5 * E + base] = make_double2(w[8], vol[t]);
+    }
+    (void)bad_volume;
+}
+
+template <typename R>
+__global__ void k_mass_new(const double* __restrict__ mass_orig, const int* __restrict__ perm,
+                           long long n, R* __restrict__ mass)
+{
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) mass[i] = (R)mass_orig[perm[i]];
+}

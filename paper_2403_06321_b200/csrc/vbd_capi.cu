@@ -1,0 +1,1388 @@
+// vbd_capi.cu -- the C ABI (include/vbd_b200.h): device context, scene packing, the
+// CUDA-graph step pipeline and the protocol-compatible colour pass.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/vbd_b200.h"
+#include "vbd_build.cuh"
+#include "vbd_common.cuh"
+#include "vbd_kernels.cuh"
+
+#ifndef VBD_LANES
+#define VBD_LANES 8
+#endif
+
+namespace {
+
+thread_local std::string g_err;
+
+struct VbdError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& m) { throw VbdError{code, m}; }
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            fail(VBD_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + " (" + \
+                                   __FILE__ + ":" + std::to_string(__LINE__) + ")");      \
+    } while (0)
+
+template <typename F> int guarded(F&& f)
+{
+    try {
+        f();
+        return VBD_OK;
+    } catch (const VbdError& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return VBD_ERR_INTERNAL;
+    }
+}
+
+inline unsigned blocks_for(long long n, int bs = 256) { return (unsigned)((n + bs - 1) / bs); }
+
+// owning device buffer
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void alloc(size_t b)
+    {
+        release();
+        if (b == 0) b = 16;
+        CK(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+template <typename T> void upload(DBuf& b, const T* host, size_t n, cudaStream_t s)
+{
+    b.alloc(n * sizeof(T));
+    if (n) CK(cudaMemcpyAsync(b.p, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+struct MaterialKey {
+    double mu, lam, kd, density;
+    bool operator<(const MaterialKey& o) const
+    {
+        return std::tie(mu, lam, kd, density) < std::tie(o.mu, o.lam, o.kd, o.density);
+    }
+};
+
+struct GraphKey {
+    vbd_step_params p;
+    bool operator==(const GraphKey& o) const { return std::memcmp(&p, &o.p, sizeof p) == 0; }
+};
+
+}  // namespace
+
+struct vbd_ctx {
+    int device = 0;
+    int precision = VBD_PREC_F32;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    long long n = 0, nsolve = 0, nfree_all = 0, T = 0, E = 0;
+    int ncolors = 0;
+    std::vector<long long> cbeg, ccnt;
+    bool inplace = true;
+    std::vector<MaterialKey> mats;
+    double mat_h = NAN;
+    DBuf perm, inv, eoff, ent, mat, pos, xt, vt, vprev, y, ha, hb, mass, out, group, stage,
+        flag, stepctr, color_orig;
+    std::vector<BeamDev> beams;
+    DBuf beams_dev;
+    std::vector<int> hinv;  // host copy of inv (protocol colour pass)
+    // step state for the fine-grained path
+    vbd_step_params cur{};
+    std::vector<double> omegas;
+    bool in_step = false;
+    // graph cache
+    cudaGraphExec_t gexec = nullptr;
+    GraphKey gkey{};
+    // halo lists: [side][color] -> device ids
+    std::vector<std::vector<long long>> halo_send_cnt[2], halo_recv_cnt[2];
+    std::vector<std::vector<DBuf*>> halo_send[2], halo_recv[2];
+    ~vbd_ctx()
+    {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        for (int s = 0; s < 2; ++s) {
+            for (auto& v : halo_send[s])
+                for (auto* b : v) delete b;
+            for (auto& v : halo_recv[s])
+                for (auto* b : v) delete b;
+        }
+        if (own_stream) cudaStreamDestroy(own_stream);
+    }
+    size_t r4() const { return precision == VBD_PREC_F64 ? 32 : 16; }
+    size_t rs() const { return precision == VBD_PREC_F64 ? 8 : 4; }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------------------
+// CUB helpers
+
+void sort_pairs_i32(DBuf& keys, DBuf& vals, long long n, int end_bit, cudaStream_t s)
+{
+    DBuf k2, v2, tmp;
+    k2.alloc(n * 4);
+    v2.alloc(n * 4);
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<int>(), k2.as<int>(),
+                                       vals.as<unsigned>(), v2.as<unsigned>(), (int64_t)n, 0,
+                                       end_bit, s));
+    tmp.alloc(tb);
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<int>(), k2.as<int>(),
+                                       vals.as<unsigned>(), v2.as<unsigned>(), (int64_t)n, 0,
+                                       end_bit, s));
+    CK(cudaStreamSynchronize(s));
+    std::swap(keys.p, k2.p);
+    std::swap(keys.bytes, k2.bytes);
+    std::swap(vals.p, v2.p);
+    std::swap(vals.bytes, v2.bytes);
+}
+
+void sort_keys_u64(DBuf& keys, long long n, cudaStream_t s)
+{
+    DBuf k2, tmp;
+    k2.alloc(n * 8);
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.as<unsigned long long>(),
+                                      k2.as<unsigned long long>(), (int64_t)n, 0, 64, s));
+    tmp.alloc(tb);
+    CK(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.as<unsigned long long>(),
+                                      k2.as<unsigned long long>(), (int64_t)n, 0, 64, s));
+    CK(cudaStreamSynchronize(s));
+    std::swap(keys.p, k2.p);
+    std::swap(keys.bytes, k2.bytes);
+}
+
+// out[0] = 0, out[i+1] = sum(in[0..i]); in has n entries of type In
+template <typename In>
+void exclusive_offsets(const In* in, long long n, DBuf& out, cudaStream_t s)
+{
+    out.alloc((n + 1) * sizeof(long long));
+    CK(cudaMemsetAsync(out.p, 0, sizeof(long long), s));
+    if (n == 0) return;
+    DBuf tmp;
+    size_t tb = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out.as<long long>() + 1, (int64_t)n, s));
+    tmp.alloc(tb);
+    CK(cub::DeviceScan::InclusiveSum(tmp.p, tb, in, out.as<long long>() + 1, (int64_t)n, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+template <typename T> T read_scalar(const void* dptr, cudaStream_t s)
+{
+    T v;
+    CK(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return v;
+}
+
+// ---------------------------------------------------------------------------------------
+// scene intermediate (device, original numbering) consumed by the packer
+
+struct Scene {
+    long long n = 0, T = 0;
+    DBuf tets;      // int32 (T,4)
+    DBuf tet_w;     // f64 (T,12)
+    DBuf vol;       // f64 (T)
+    DBuf tmat;      // int32 (T)
+    DBuf inc_off;   // int64 (n+1)
+    DBuf inc;       // u32 (4T) = 4 t + s, ascending per vertex
+    DBuf mass;      // f64 (n)
+    DBuf kind;      // u8 (n): 0 free, 1 fixed, 3 ghost
+    DBuf color;     // int32 (n)
+    DBuf pos;       // f64 (n,3) rest positions (generator path) or empty
+};
+
+void build_incidence(Scene& sc, cudaStream_t s)
+{
+    long long n4 = 4 * sc.T;
+    DBuf keys, vals, cnt;
+    keys.alloc(n4 * 4);
+    vals.alloc(n4 * 4);
+    cnt.alloc(sc.n * 4);
+    CK(cudaMemsetAsync(cnt.p, 0, sc.n * 4, s));
+    if (n4) k_inc_keys<<<blocks_for(n4), 256, 0, s>>>(sc.tets.as<int>(), n4, keys.as<int>(),
+                                                     vals.as<unsigned>(), cnt.as<int>());
+    CK(cudaGetLastError());
+    int bits = 1;
+    while ((1LL << bits) < sc.n) ++bits;
+    if (n4) sort_pairs_i32(keys, vals, n4, bits, s);
+    exclusive_offsets(cnt.as<int>(), sc.n, sc.inc_off, s);
+    std::swap(sc.inc.p, vals.p);
+    std::swap(sc.inc.bytes, vals.bytes);
+}
+
+// K5 on a device neighbour CSR; colour (int32, n) out
+int run_jp(const long long* noff, const int* nids, const long long* rank, long long n,
+           int* color, cudaStream_t s)
+{
+    if (n == 0) return 0;
+    DBuf pending, fa, fb, cnts, colored, overflow;
+    pending.alloc(n * 4);
+    fa.alloc(n * 4);
+    fb.alloc(n * 4);
+    cnts.alloc(2 * sizeof(int));
+    colored.alloc(8);
+    overflow.alloc(4);
+    CK(cudaMemsetAsync(cnts.p, 0, 2 * sizeof(int), s));
+    CK(cudaMemsetAsync(colored.p, 0, 8, s));
+    CK(cudaMemsetAsync(overflow.p, 0, 4, s));
+    int* cnt = cnts.as<int>();
+    k_jp_init<<<blocks_for(n), 256, 0, s>>>(noff, nids, rank, n, pending.as<int>(), color,
+                                            fa.as<int>(), cnt);
+    CK(cudaGetLastError());
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int* fin = fa.as<int>();
+    int* fout = fb.as<int>();
+    int cin = 0, cout = 1;
+    long long rounds = 0;
+    for (;;) {
+        CK(cudaMemsetAsync(cnt + cout, 0, sizeof(int), s));
+        k_jp_round<<<sms * 4, 256, 0, s>>>(noff, nids, rank, fin, cnt + cin, pending.as<int>(),
+                                           color, fout, cnt + cout,
+                                           colored.as<unsigned long long>(), overflow.as<int>());
+        std::swap(fin, fout);
+        std::swap(cin, cout);
+        ++rounds;
+        if ((rounds & 15) == 0 || rounds < 4) {
+            CK(cudaGetLastError());
+            unsigned long long done = read_scalar<unsigned long long>(colored.p, s);
+            if ((long long)done >= n) break;
+            int next = read_scalar<int>(cnt + cin, s);
+            if (next == 0) fail(VBD_ERR_INTERNAL, "colouring stalled (inconsistent CSR?)");
+        }
+        if (rounds > 4 * n + 64) fail(VBD_ERR_INTERNAL, "colouring did not terminate");
+    }
+    if (read_scalar<int>(overflow.p, s)) fail(VBD_ERR_UNSUPPORTED, "more than 256 colours");
+    return 0;
+}
+
+// neighbour CSR from the incidence, then K5
+void color_scene(Scene& sc, cudaStream_t s)
+{
+    DBuf cnt, overflow, noff, nids;
+    cnt.alloc(sc.n * 4);
+    overflow.alloc(4);
+    CK(cudaMemsetAsync(overflow.p, 0, 4, s));
+    k_nbr_count<<<blocks_for(sc.n, 128), 128, 0, s>>>(sc.inc_off.as<long long>(),
+                                                       sc.inc.as<unsigned>(), sc.tets.as<int>(),
+                                                       sc.n, cnt.as<int>(), overflow.as<int>());
+    CK(cudaGetLastError());
+    if (read_scalar<int>(overflow.p, s))
+        fail(VBD_ERR_UNSUPPORTED, "vertex with more than 128 incident tets");
+    exclusive_offsets(cnt.as<int>(), sc.n, noff, s);
+    long long nn = read_scalar<long long>(noff.as<long long>() + sc.n, s);
+    nids.alloc(nn * 4);
+    k_nbr_fill<<<blocks_for(sc.n, 128), 128, 0, s>>>(sc.inc_off.as<long long>(),
+                                                      sc.inc.as<unsigned>(), sc.tets.as<int>(),
+                                                      sc.n, noff.as<long long>(), nids.as<int>());
+    CK(cudaGetLastError());
+    sc.color.alloc(sc.n * 4);
+    run_jp(noff.as<long long>(), nids.as<int>(), nullptr, sc.n, sc.color.as<int>(), s);
+}
+
+template <typename R> void alloc_state(vbd_ctx* c)
+{
+    size_t b = c->n * c->r4();
+    for (DBuf* d : {&c->pos, &c->xt, &c->vt, &c->vprev, &c->y, &c->ha, &c->hb, &c->out}) {
+        d->alloc(b);
+        CK(cudaMemsetAsync(d->p, 0, b, c->stream));
+    }
+    c->stage.alloc(std::max<long long>(c->n, 1) * 3 * sizeof(double));
+    c->flag.alloc(8);
+    c->stepctr.alloc(4);
+    CK(cudaMemsetAsync(c->stepctr.p, 0, 4, c->stream));
+}
+
+// K6 + context finalisation
+template <typename R> void pack(vbd_ctx* c, Scene& sc)
+{
+    cudaStream_t s = c->stream;
+    c->n = sc.n;
+    c->T = sc.T;
+    if (sc.n >= (1LL << VBD_ID_BITS)) fail(VBD_ERR_UNSUPPORTED, "too many vertices for one context");
+    // colouring validity (decides in-place vs aux-buffer sweeps)
+    {
+        DBuf bad;
+        bad.alloc(4);
+        CK(cudaMemsetAsync(bad.p, 0, 4, s));
+        if (sc.T)
+            k_check_coloring<<<blocks_for(sc.T), 256, 0, s>>>(sc.tets.as<int>(), sc.T,
+                                                             sc.color.as<int>(), bad.as<int>());
+        CK(cudaGetLastError());
+        c->inplace = read_scalar<int>(bad.p, s) == 0;
+    }
+    // order
+    DBuf keys;
+    keys.alloc(sc.n * 8);
+    k_order_keys<<<blocks_for(sc.n), 256, 0, s>>>(sc.inc_off.as<long long>(), sc.kind.as<unsigned char>(),
+                                                  sc.color.as<int>(), sc.n, VBD_LANES,
+                                                  keys.as<unsigned long long>());
+    CK(cudaGetLastError());
+    sort_keys_u64(keys, sc.n, s);
+    c->perm.alloc(sc.n * 4);
+    c->inv.alloc(sc.n * 4);
+    k_perm_from_keys<<<blocks_for(sc.n), 256, 0, s>>>(keys.as<unsigned long long>(), sc.n,
+                                                      c->perm.as<int>(), c->inv.as<int>());
+    CK(cudaGetLastError());
+    // category / colour ranges from the sorted keys (host scan of the boundaries)
+    std::vector<unsigned long long> hk(sc.n);
+    if (sc.n) CK(cudaMemcpyAsync(hk.data(), keys.p, sc.n * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->nsolve = 0;
+    c->nfree_all = 0;
+    int maxc = -1;
+    for (long long i = 0; i < sc.n; ++i) {
+        unsigned cat = (unsigned)(hk[i] >> 56);
+        if (cat == 0) c->nsolve = i + 1;
+        if (cat <= 1) {
+            c->nfree_all = i + 1;
+            maxc = std::max(maxc, (int)((hk[i] >> 44) & 0xfff));
+        }
+    }
+    c->ncolors = maxc + 1;
+    c->cbeg.assign(c->ncolors, 0);
+    c->ccnt.assign(c->ncolors, 0);
+    for (long long i = c->nsolve - 1; i >= 0; --i) {
+        int col = (int)((hk[i] >> 44) & 0xfff);
+        c->cbeg[col] = i;
+        c->ccnt[col]++;
+    }
+    // colour ranges must be contiguous and ordered (guaranteed by the key layout)
+    // entry offsets over solved vertices
+    DBuf deg;
+    deg.alloc(std::max<long long>(c->nsolve, 1) * 8);
+    if (c->nsolve)
+        k_degree_new<<<blocks_for(c->nsolve), 256, 0, s>>>(sc.inc_off.as<long long>(),
+                                                           c->perm.as<int>(), c->nsolve,
+                                                           deg.as<long long>());
+    CK(cudaGetLastError());
+    exclusive_offsets(deg.as<long long>(), c->nsolve, c->eoff, s);
+    c->E = read_scalar<long long>(c->eoff.as<long long>() + c->nsolve, s);
+    const int P = EntryPlanes<R>::P;
+    c->ent.alloc(std::max<long long>(c->E, 1) * P * 16);
+    DBuf badv;
+    badv.alloc(4);
+    CK(cudaMemsetAsync(badv.p, 0, 4, s));
+    if (c->nsolve)
+        k_pack_entries<R><<<blocks_for(c->nsolve, 128), 128, 0, s>>>(
+            sc.inc_off.as<long long>(), sc.inc.as<unsigned>(), sc.tets.as<int>(),
+            sc.tet_w.as<double>(), sc.vol.as<double>(), sc.tmat.as<int>(), c->perm.as<int>(),
+            c->inv.as<int>(), c->eoff.as<long long>(), c->nsolve,
+            c->ent.as<typename PlaneT<R>::T>(), c->E, badv.as<int>());
+    CK(cudaGetLastError());
+    if (read_scalar<int>(badv.p, s))
+        fail(VBD_ERR_UNSUPPORTED,
+             "fp32 layout recomputes tet volumes from |det W|; tet_vol disagrees with tet_w "
+             "(use precision=fp64)");
+    // masses in colour-major order
+    c->mass.alloc(sc.n * sizeof(R));
+    k_mass_new<R><<<blocks_for(sc.n), 256, 0, s>>>(sc.mass.as<double>(), c->perm.as<int>(), sc.n,
+                                                   c->mass.as<R>());
+    CK(cudaGetLastError());
+    // original-order colours (for vbd_get_colors)
+    c->color_orig.alloc(sc.n * 4);
+    CK(cudaMemcpyAsync(c->color_orig.p, sc.color.p, sc.n * 4, cudaMemcpyDeviceToDevice, s));
+    alloc_state<R>(c);
+    CK(cudaStreamSynchronize(s));
+}
+
+// material table for step size h
+template <typename R> void ensure_materials(vbd_ctx* c, double h)
+{
+    if (c->mat_h == h && c->mat.p) return;
+    std::vector<Material<R>> m(c->mats.size());
+    for (size_t i = 0; i < m.size(); ++i) {
+        double mu = c->mats[i].mu, lam = c->mats[i].lam, kd = c->mats[i].kd;
+        double g = 1.0 + mu / lam;  // _native.pyx:291
+        double dsc = kd / h;        // _native.pyx:309
+        m[i] = Material<R>{(R)mu, (R)lam, (R)g, (R)dsc, (R)(1.0 + dsc)};
+    }
+    if (!c->mat.p) c->mat.alloc(VBD_MAX_MATERIALS * sizeof(Material<R>));
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(c->mat.p, m.data(), m.size() * sizeof(Material<R>), cudaMemcpyHostToDevice));
+    c->mat_h = h;
+}
+
+template <typename R>
+K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
+{
+    K1Args<R> a;
+    a.ent = c->ent.as<typename PlaneT<R>::T>();
+    a.E = c->E;
+    a.off = c->eoff.as<long long>();
+    a.pos = c->pos.as<typename Vec4<R>::T>();
+    a.xt = c->xt.as<typename Vec4<R>::T>();
+    a.y = c->y.as<typename Vec4<R>::T>();
+    a.mat = c->mat.as<Material<R>>();
+    a.group = nullptr;
+    a.vbeg = 0;
+    a.count = 0;
+    a.nsolve = (int)c->nsolve;
+    a.out = nullptr;
+    a.eps_det = (R)eps_det;
+    a.mode = mode;
+    a.flag = check ? c->flag.as<unsigned long long>() : nullptr;
+    a.perm = c->perm.as<int>();
+    a.stepctr = c->stepctr.as<int>();
+    a.iter = iter;
+    return a;
+}
+
+template <typename R> void launch_k1(const K1Args<R>& a, cudaStream_t s)
+{
+    if (a.count <= 0) return;
+    long long threads = (long long)a.count * VBD_LANES;
+    k1_color_pass<R, VBD_LANES><<<blocks_for(threads), 256, 0, s>>>(a);
+}
+
+// one colour pass of the step (in place when the colouring is valid, else aux buffer)
+template <typename R> void color_sweep(vbd_ctx* c, int color, int iter, bool check)
+{
+    cudaStream_t s = c->stream;
+    K1Args<R> a = k1_args<R>(c, c->cur.eps_det, 0, check, iter);
+    a.vbeg = (int)c->cbeg[color];
+    a.count = (int)c->ccnt[color];
+    if (!c->inplace) {
+        // aux-buffer semantics over the contiguous colour range: compute into `out`, then copy
+        a.out = c->out.as<typename Vec4<R>::T>();
+        launch_k1<R>(a, s);
+        CK(cudaMemcpyAsync(c->pos.as<char>() + c->cbeg[color] * c->r4(), c->out.p,
+                           c->ccnt[color] * c->r4(), cudaMemcpyDeviceToDevice, s));
+    } else {
+        launch_k1<R>(a, s);
+    }
+}
+
+std::vector<double> omega_table(double rho, int n_max)
+{
+    // solver.py:167-177, evaluated exactly as the reference does (recurrence from scratch)
+    std::vector<double> w(n_max + 1, 1.0);
+    for (int n = 1; n <= n_max; ++n) {
+        if (rho == 0.0 || n == 1) { w[n] = 1.0; continue; }
+        double omega = 2.0 / (2.0 - rho * rho);
+        for (int k = 3; k <= n; ++k) omega = 4.0 / (4.0 - rho * rho * omega);
+        w[n] = omega;
+    }
+    return w;
+}
+
+template <typename R> StepArgs<R> step_args(vbd_ctx* c)
+{
+    typedef typename Vec4<R>::T R4;
+    const vbd_step_params& p = c->cur;
+    StepArgs<R> a;
+    a.n = (int)c->n;
+    a.nsolve = (int)c->nsolve;
+    a.nfree_all = (int)c->nfree_all;
+    a.pos = c->pos.as<R4>();
+    a.xt = c->xt.as<R4>();
+    a.vt = c->vt.as<R4>();
+    a.vprev = c->vprev.as<R4>();
+    a.y = c->y.as<R4>();
+    a.ha = c->ha.as<R4>();
+    a.hb = c->hb.as<R4>();
+    a.mass = c->mass.as<R>();
+    a.h = p.h;
+    a.hh = p.h * p.h;
+    double nrm = std::sqrt(p.a_ext[0] * p.a_ext[0] + p.a_ext[1] * p.a_ext[1] + p.a_ext[2] * p.a_ext[2]);
+    for (int k = 0; k < 3; ++k) {
+        a.a[k] = p.a_ext[k];
+        a.an[k] = nrm > 0 ? p.a_ext[k] / nrm : 0.0;
+    }
+    a.anorm = nrm;
+    a.init_mode = p.init_mode;
+    a.hist = p.rho != 0.0;
+    a.flag = c->flag.as<unsigned long long>();
+    a.perm = c->perm.as<int>();
+    a.stepctr = c->stepctr.as<int>();
+    return a;
+}
+
+template <typename R> void enqueue_begin(vbd_ctx* c)
+{
+    StepArgs<R> a = step_args<R>(c);
+    k2_step_init<R><<<blocks_for(c->n), 256, 0, c->stream>>>(a);
+}
+
+template <typename R> void enqueue_iter_end(vbd_ctx* c, int n)
+{
+    typedef typename Vec4<R>::T R4;
+    if (c->cur.rho == 0.0) return;  // omega == 1 throughout: no blend, no history
+    R4* hist = (n % 2 == 1) ? c->hb.as<R4>() : c->ha.as<R4>();
+    double w = c->omegas[n];
+    int blend = (n >= 2 && w != 1.0) ? 1 : 0;
+    k3_chebyshev<R><<<blocks_for(c->n), 256, 0, c->stream>>>(
+        c->pos.as<R4>(), hist, (int)c->n, w, blend, c->flag.as<unsigned long long>(),
+        c->perm.as<int>(), c->stepctr.as<int>(), n);
+}
+
+template <typename R> void enqueue_end(vbd_ctx* c)
+{
+    typedef typename Vec4<R>::T R4;
+    k4_commit<R><<<blocks_for(std::max<long long>(c->n, 1)), 256, 0, c->stream>>>(
+        c->pos.as<R4>(), c->xt.as<R4>(), c->vt.as<R4>(), c->vprev.as<R4>(), (int)c->n, c->cur.h,
+        c->flag.as<unsigned long long>(), c->stepctr.as<int>());
+}
+
+template <typename R> void enqueue_step(vbd_ctx* c)
+{
+    enqueue_begin<R>(c);
+    bool check_in_k1 = c->cur.rho == 0.0;  // otherwise K3 checks every vertex
+    for (int n = 1; n <= c->cur.n_max; ++n) {
+        for (int col = 0; col < c->ncolors; ++col) color_sweep<R>(c, col, n, check_in_k1);
+        enqueue_iter_end<R>(c, n);
+    }
+    enqueue_end<R>(c);
+}
+
+void validate_params(const vbd_step_params* p)
+{
+    if (!p) fail(VBD_ERR_ARG, "params is NULL");
+    if (!(p->h > 0.0)) fail(VBD_ERR_ARG, "h must be positive");
+    if (p->n_max < 1 || p->n_max > 65535) fail(VBD_ERR_ARG, "n_max must be in [1, 65535]");
+    if (!(p->rho >= 0.0 && p->rho < 1.0)) fail(VBD_ERR_ARG, "rho must be in [0, 1)");
+    if (!(p->eps_det >= 0.0)) fail(VBD_ERR_ARG, "eps_det must be >= 0");
+    if (p->init_mode < 0 || p->init_mode > 3) fail(VBD_ERR_ARG, "bad init_mode");
+}
+
+void read_result(vbd_ctx* c, vbd_step_result* res)
+{
+    unsigned long long f = read_scalar<unsigned long long>(c->flag.p, c->stream);
+    if (!res) return;
+    std::memset(res, 0, sizeof *res);
+    res->vertex = -1;
+    if (f != StepFlag::NONE) {
+        res->nonfinite = 1;
+        res->step = (int)((f >> 48) & 0xffff);
+        res->iteration = (int)((f >> 32) & 0xffff);
+        res->vertex = (long long)(f & 0xffffffffull);
+    }
+}
+
+template <typename R> void do_step(vbd_ctx* c, const vbd_step_params* p, int n_steps, vbd_step_result* res)
+{
+    validate_params(p);
+    if (n_steps < 1 || n_steps > 65535) fail(VBD_ERR_ARG, "n_steps must be in [1, 65535]");
+    c->cur = *p;
+    c->omegas = omega_table(p->rho, p->n_max);
+    ensure_materials<R>(c, p->h);
+    cudaStream_t s = c->stream;
+    CK(cudaMemsetAsync(c->flag.p, 0xff, 8, s));
+    CK(cudaMemsetAsync(c->stepctr.p, 0, 4, s));
+    GraphKey key{*p};
+    if (!c->gexec || !(key == c->gkey)) {
+        if (c->gexec) {
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        enqueue_step<R>(c);
+        cudaError_t e = cudaStreamEndCapture(s, &g);
+        CK(e);
+        CK(cudaGraphInstantiate(&c->gexec, g, 0));
+        cudaGraphDestroy(g);
+        c->gkey = key;
+    }
+    for (int k = 0; k < n_steps; ++k) CK(cudaGraphLaunch(c->gexec, s));
+    read_result(c, res);
+}
+
+// ---------------------------------------------------------------------------------------
+// state transfer
+
+template <typename R> void load_vec(vbd_ctx* c, const double* host, DBuf& dst)
+{
+    cudaStream_t s = c->stream;
+    CK(cudaMemcpyAsync(c->stage.p, host, c->n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    k_load_vec<R><<<blocks_for(c->n), 256, 0, s>>>(c->stage.as<double>(),
+                                                   dst.as<typename Vec4<R>::T>(),
+                                                   c->perm.as<int>(), (int)c->n);
+    CK(cudaGetLastError());
+}
+
+template <typename R> void store_vec(vbd_ctx* c, const DBuf& src, double* host)
+{
+    cudaStream_t s = c->stream;
+    k_store_vec<R><<<blocks_for(c->n), 256, 0, s>>>(src.as<typename Vec4<R>::T>(),
+                                                    c->stage.as<double>(), c->inv.as<int>(),
+                                                    (int)c->n);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(host, c->stage.p, c->n * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+template <typename R>
+void do_color_pass(vbd_ctx* c, double* x, const double* x_t, const double* y, double h,
+                   const int64_t* group, int64_t ng, int mode, double eps_det)
+{
+    typedef typename Vec4<R>::T R4;
+    cudaStream_t s = c->stream;
+    if (ng <= 0) return;  // _native.pyx:520-521
+    ensure_materials<R>(c, h);
+    load_vec<R>(c, x, c->pos);
+    load_vec<R>(c, x_t, c->xt);
+    load_vec<R>(c, y, c->y);
+    k_fill_mih2<R><<<blocks_for(c->n), 256, 0, s>>>(c->y.as<R4>(), c->mass.as<R>(), (int)c->n, h * h);
+    // group (original ids) -> colour-major ids
+    std::vector<int> gi(ng);
+    std::vector<int>& hinv = c->hinv;
+    {
+        if ((long long)hinv.size() != c->n) {
+            hinv.resize(c->n);
+            CK(cudaMemcpyAsync(hinv.data(), c->inv.p, c->n * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        for (int64_t k = 0; k < ng; ++k) {
+            if (group[k] < 0 || group[k] >= c->n) fail(VBD_ERR_ARG, "group vertex out of range");
+            gi[k] = hinv[group[k]];
+        }
+    }
+    DBuf gdev, odev;
+    upload(gdev, gi.data(), ng, s);
+    odev.alloc(ng * c->r4());
+    K1Args<R> a = k1_args<R>(c, eps_det, mode, false, 0);
+    a.group = gdev.as<int>();
+    a.count = (int)ng;
+    a.out = odev.as<R4>();
+    launch_k1<R>(a, s);
+    CK(cudaGetLastError());
+    std::vector<R4> ho(ng);
+    CK(cudaMemcpyAsync(ho.data(), odev.p, ng * c->r4(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    // merge (_native.pyx:585-589): only the group's rows change
+    for (int64_t k = 0; k < ng; ++k) {
+        int64_t v = group[k];
+        x[3 * v] = (double)ho[k].x;
+        x[3 * v + 1] = (double)ho[k].y;
+        x[3 * v + 2] = (double)ho[k].z;
+    }
+}
+
+int material_id(vbd_ctx* c, std::map<MaterialKey, int>& ids, const MaterialKey& k)
+{
+    auto it = ids.find(k);
+    if (it != ids.end()) return it->second;
+    int id = (int)c->mats.size();
+    if (id >= VBD_MAX_MATERIALS) fail(VBD_ERR_UNSUPPORTED, "more than 512 distinct materials");
+    ids[k] = id;
+    c->mats.push_back(k);
+    return id;
+}
+
+void init_ctx(vbd_ctx* c, int device, int precision)
+{
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        fail(VBD_ERR_NODEVICE, "no CUDA device available (the B200 path has no CPU fallback)");
+    if (device < 0 || device >= count) fail(VBD_ERR_ARG, "bad device index");
+    if (precision != VBD_PREC_F32 && precision != VBD_PREC_F64) fail(VBD_ERR_ARG, "bad precision");
+    c->device = device;
+    c->precision = precision;
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        fail(VBD_ERR_NODEVICE, std::string("device ") + prop.name + " is not sm_100 (Blackwell)");
+    CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+}
+
+void finish_pack(vbd_ctx* c, Scene& sc)
+{
+    if (c->precision == VBD_PREC_F64)
+        pack<double>(c, sc);
+    else
+        pack<float>(c, sc);
+}
+
+template <typename R> void set_rest_state(vbd_ctx* c, const Scene& sc)
+{
+    // x = x_t = y = rest positions, v = v_prev = 0 (make_state, solver.py:111-117)
+    cudaStream_t s = c->stream;
+    CK(cudaMemcpyAsync(c->stage.p, sc.pos.p, c->n * 3 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    for (DBuf* d : {&c->pos, &c->xt, &c->y})
+        k_load_vec<R><<<blocks_for(c->n), 256, 0, s>>>(c->stage.as<double>(),
+                                                       d->as<typename Vec4<R>::T>(),
+                                                       c->perm.as<int>(), (int)c->n);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+}
+
+__global__ void k_beam_velocity(const BeamDev* __restrict__ beams, int nb, const double* __restrict__ la,
+                                const double* __restrict__ pos, long long n, double* __restrict__ v)
+{
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int b = find_beam(beams, nb, i, false);
+    const BeamDev& B = beams[b];
+    double cx = B.origin[0] + 0.5 * B.spacing * (B.nx - 1);
+    double cy = B.origin[1] + 0.5 * B.spacing * (B.ny - 1);
+    double cz = B.origin[2] + 0.5 * B.spacing * (B.nz - 1);
+    double rx = pos[3 * i] - cx, ry = pos[3 * i + 1] - cy, rz = pos[3 * i + 2] - cz;
+    const double* q = la + 6 * b;
+    v[3 * i] = q[0] + (q[4] * rz - q[5] * ry);
+    v[3 * i + 1] = q[1] + (q[5] * rx - q[3] * rz);
+    v[3 * i + 2] = q[2] + (q[3] * ry - q[4] * rx);
+}
+
+}  // namespace
+
+// =========================================================================================
+// C ABI
+
+extern "C" {
+
+const char* vbd_last_error(void) { return g_err.c_str(); }
+const char* vbd_version(void) { return "vbd_b200 0.1 (sm_100a)"; }
+
+int vbd_device_count(int* count)
+{
+    return guarded([&] {
+        if (!count) fail(VBD_ERR_ARG, "count is NULL");
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+        *count = n;
+    });
+}
+
+int vbd_ctx_create(const vbd_system_desc* d, int device, int precision, vbd_ctx** out)
+{
+    vbd_ctx* c = nullptr;
+    int rc = guarded([&] {
+        if (!d || !out) fail(VBD_ERR_ARG, "NULL argument");
+        if (d->num_vertices < 0 || d->num_tets < 0) fail(VBD_ERR_ARG, "negative sizes");
+        if (!d->masses || !d->color_off || !d->color_verts || !d->t_off)
+            fail(VBD_ERR_ARG, "missing System arrays");
+        if (d->num_tets && (!d->tets || !d->tet_w || !d->tet_vol || !d->tet_mu || !d->tet_lam ||
+                            !d->tet_kd || !d->t_id || !d->t_slot))
+            fail(VBD_ERR_ARG, "missing tet arrays");
+        c = new vbd_ctx();
+        init_ctx(c, device, precision);
+        cudaStream_t s = c->stream;
+        const long long N = d->num_vertices, T = d->num_tets;
+        if (4 * T >= (1LL << 32)) fail(VBD_ERR_UNSUPPORTED, "too many tets for one context");
+        Scene sc;
+        sc.n = N;
+        sc.T = T;
+        // tets (int64 -> int32) and materials
+        std::vector<int> tets32(4 * T), tmat(T);
+        std::map<MaterialKey, int> ids;
+        for (long long t = 0; t < T; ++t) {
+            for (int k = 0; k < 4; ++k) {
+                int64_t v = d->tets[4 * t + k];
+                if (v < 0 || v >= N) fail(VBD_ERR_ARG, "tet index out of range");
+                tets32[4 * t + k] = (int)v;
+            }
+            if (!(d->tet_lam[t] != 0.0)) fail(VBD_ERR_ARG, "tet_lam must be non-zero");
+            tmat[t] = material_id(c, ids, MaterialKey{d->tet_mu[t], d->tet_lam[t], d->tet_kd[t], 0.0});
+        }
+        upload(sc.tets, tets32.data(), tets32.size(), s);
+        upload(sc.tmat, tmat.data(), tmat.size(), s);
+        upload(sc.tet_w, d->tet_w, 12 * T, s);
+        upload(sc.vol, d->tet_vol, T, s);
+        upload(sc.mass, d->masses, N, s);
+        std::vector<unsigned char> kind(N, 0);
+        if (d->kind)
+            for (long long v = 0; v < N; ++v) {
+                if (d->kind[v] == VBD_KIND_SUBSPACE)
+                    fail(VBD_ERR_UNSUPPORTED, "SubspaceConstraint is not on the B200 hot path");
+                kind[v] = d->kind[v] == VBD_KIND_FIXED ? 1 : 0;
+            }
+        upload(sc.kind, kind.data(), N, s);
+        // incidence exactly as given (ascending tet id per vertex, mesh.py:243-250)
+        if (d->t_off[0] != 0 || d->t_off[N] != 4 * T) fail(VBD_ERR_ARG, "t_off inconsistent with tets");
+        std::vector<unsigned> inc(4 * T);
+        for (long long k = 0; k < 4 * T; ++k) {
+            if (d->t_slot[k] < 0 || d->t_slot[k] > 3 || d->t_id[k] < 0 || d->t_id[k] >= T)
+                fail(VBD_ERR_ARG, "bad t_id/t_slot");
+            inc[k] = (unsigned)(4 * d->t_id[k] + d->t_slot[k]);
+        }
+        upload(sc.inc_off, d->t_off, N + 1, s);
+        upload(sc.inc, inc.data(), inc.size(), s);
+        // colours from the groups
+        std::vector<int> color(N, -1);
+        for (long long g = 0; g < d->num_colors; ++g)
+            for (long long k = d->color_off[g]; k < d->color_off[g + 1]; ++k) {
+                int64_t v = d->color_verts[k];
+                if (v < 0 || v >= N) fail(VBD_ERR_ARG, "colour vertex out of range");
+                color[v] = (int)g;
+            }
+        for (long long v = 0; v < N; ++v)
+            if (color[v] < 0 && kind[v] != 1) fail(VBD_ERR_ARG, "vertex without colour");
+        if (d->num_colors > 4095) fail(VBD_ERR_UNSUPPORTED, "too many colours");
+        upload(sc.color, color.data(), N, s);
+        CK(cudaStreamSynchronize(s));
+        finish_pack(c, sc);
+        *out = c;
+    });
+    if (rc != VBD_OK) delete c;
+    return rc;
+}
+
+int vbd_ctx_create_beams(const vbd_beam_desc* beams, int64_t nb, int64_t slab_lo, int64_t slab_hi,
+                         int device, int precision, vbd_ctx** out)
+{
+    vbd_ctx* c = nullptr;
+    int rc = guarded([&] {
+        if (!beams || nb < 1 || !out) fail(VBD_ERR_ARG, "bad beam list");
+        bool slab = slab_hi > slab_lo;
+        if (slab && nb != 1) fail(VBD_ERR_ARG, "slab decomposition needs exactly one beam");
+        c = new vbd_ctx();
+        init_ctx(c, device, precision);
+        cudaStream_t s = c->stream;
+        std::map<MaterialKey, int> ids;
+        std::vector<double> dens;
+        // full beams (for colouring and non-slab scenes)
+        auto make_table = [&](bool full) {
+            std::vector<BeamDev> tb(nb);
+            long long vb = 0, tbase = 0;
+            for (int64_t i = 0; i < nb; ++i) {
+                const vbd_beam_desc& d = beams[i];
+                if (d.nx < 2 || d.ny < 2 || d.nz < 2) fail(VBD_ERR_ARG, "beam needs >= 2 vertices per axis");
+                if (!(d.spacing > 0) || !(d.density > 0) || !(d.mu > 0) || !(d.lam > 0) || d.kd < 0)
+                    fail(VBD_ERR_ARG, "bad beam parameters");
+                BeamDev& B = tb[i];
+                B.nx = d.nx; B.ny = d.ny; B.nz = d.nz;
+                B.spacing = d.spacing; B.density = d.density;
+                for (int k = 0; k < 3; ++k) B.origin[k] = d.origin[k];
+                B.fix_min_x = d.fix_min_x;
+                B.mat = material_id(c, ids, MaterialKey{d.mu, d.lam, d.kd, d.density});
+                if ((int)dens.size() <= B.mat) dens.resize(B.mat + 1, d.density);
+                if (full || !slab) {
+                    B.ax0 = 0; B.ax1 = d.nx - 1; B.gcell0 = 0;
+                } else {
+                    if (slab_lo < 0 || slab_hi > d.nx) fail(VBD_ERR_ARG, "slab outside the beam");
+                    B.ax0 = std::max<long long>(slab_lo - 1, 0);
+                    B.ax1 = std::min<long long>(slab_hi, d.nx - 1);
+                    B.gcell0 = B.ax0;
+                }
+                B.vbase = vb;
+                B.tbase = tbase;
+                vb += (B.ax1 - B.ax0 + 1) * B.ny * B.nz;
+                tbase += (B.ax1 - B.ax0) * (B.ny - 1) * (B.nz - 1) * 5;
+            }
+            return std::make_tuple(tb, vb, tbase);
+        };
+        auto generate = [&](Scene& sc, const std::vector<BeamDev>& tb, long long n, long long T, DBuf& bdev) {
+            upload(bdev, tb.data(), tb.size(), s);
+            sc.n = n;
+            sc.T = T;
+            if (n >= (1LL << 31) || 4 * T >= (1LL << 32)) fail(VBD_ERR_UNSUPPORTED, "scene too large for one context");
+            sc.pos.alloc(n * 3 * 8);
+            sc.kind.alloc(n);
+            k_gen_vertices<<<blocks_for(n), 256, 0, s>>>(bdev.as<BeamDev>(), (int)nb, n,
+                                                          sc.pos.as<double>(), sc.kind.as<unsigned char>());
+            sc.tets.alloc(T * 16);
+            sc.tet_w.alloc(T * 96);
+            sc.vol.alloc(T * 8);
+            sc.tmat.alloc(T * 4);
+            k_gen_tets<<<blocks_for(T), 256, 0, s>>>(bdev.as<BeamDev>(), (int)nb, T, sc.pos.as<double>(),
+                                                      sc.tets.as<int>(), sc.tet_w.as<double>(),
+                                                      sc.vol.as<double>(), sc.tmat.as<int>());
+            CK(cudaGetLastError());
+            build_incidence(sc, s);
+        };
+        std::vector<int> color_keep;
+        long long keep_off = 0;
+        if (slab) {
+            // colour the whole beam once (bit-exact global colouring), keep the slab's part
+            auto [tb, n, T] = make_table(true);
+            Scene full;
+            DBuf bdev;
+            generate(full, tb, n, T, bdev);
+            color_scene(full, s);
+            auto [tl, nl, Tl] = make_table(false);
+            keep_off = tl[0].ax0 * tl[0].ny * tl[0].nz;
+            color_keep.resize(nl);
+            CK(cudaMemcpyAsync(color_keep.data(), full.color.as<int>() + keep_off, nl * 4,
+                               cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        auto [tb, n, T] = make_table(false);
+        c->beams = tb;
+        Scene sc;
+        generate(sc, tb, n, T, c->beams_dev);
+        DBuf dm;
+        upload(dm, dens.data(), dens.size(), s);
+        sc.mass.alloc(n * 8);
+        k_mass_gather<<<blocks_for(n), 256, 0, s>>>(sc.inc_off.as<long long>(), sc.inc.as<unsigned>(),
+                                                     sc.vol.as<double>(), sc.tmat.as<int>(),
+                                                     dm.as<double>(), n, sc.mass.as<double>());
+        CK(cudaGetLastError());
+        if (slab) {
+            sc.color.alloc(n * 4);
+            CK(cudaMemcpyAsync(sc.color.p, color_keep.data(), n * 4, cudaMemcpyHostToDevice, s));
+            // ghost planes: ax0 (if < slab_lo) and ax1 (if >= slab_hi)
+            const BeamDev& B = tb[0];
+            long long plane = B.ny * B.nz;
+            std::vector<unsigned char> kind(n);
+            CK(cudaMemcpyAsync(kind.data(), sc.kind.p, n, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (long long v = 0; v < n; ++v) {
+                long long ax = B.ax0 + v / plane;
+                if ((ax < slab_lo || ax >= slab_hi) && kind[v] != 1) kind[v] = 3;
+            }
+            CK(cudaMemcpyAsync(sc.kind.p, kind.data(), n, cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+        } else {
+            color_scene(sc, s);
+        }
+        finish_pack(c, sc);
+        if (c->precision == VBD_PREC_F64) set_rest_state<double>(c, sc);
+        else set_rest_state<float>(c, sc);
+        if (slab) {
+            // halo lists: side 0 = towards slab_lo (rank - 1), side 1 = towards slab_hi (rank + 1)
+            const BeamDev& B = tb[0];
+            long long plane = B.ny * B.nz;
+            std::vector<int> hinv(n), col(n);
+            CK(cudaMemcpyAsync(hinv.data(), c->inv.p, n * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(col.data(), sc.color.p, n * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            long long planes_send[2] = {slab_lo, slab_hi - 1}, planes_recv[2] = {slab_lo - 1, slab_hi};
+            for (int side = 0; side < 2; ++side) {
+                c->halo_send[side].assign(c->ncolors, {});
+                c->halo_recv[side].assign(c->ncolors, {});
+                c->halo_send_cnt[side].assign(c->ncolors, {});
+                c->halo_recv_cnt[side].assign(c->ncolors, {});
+                bool exists = side == 0 ? slab_lo > 0 : slab_hi < B.nx;
+                for (int col_i = 0; col_i < c->ncolors; ++col_i) {
+                    std::vector<int> sl, rl;
+                    if (exists) {
+                        long long ps = planes_send[side] - B.ax0, pr = planes_recv[side] - B.ax0;
+                        for (long long k = 0; k < plane; ++k) {
+                            long long vs = ps * plane + k, vr = pr * plane + k;
+                            if (col[vs] == col_i) sl.push_back(hinv[vs]);
+                            if (col[vr] == col_i) rl.push_back(hinv[vr]);
+                        }
+                    }
+                    DBuf* bs = new DBuf();
+                    DBuf* br = new DBuf();
+                    upload(*bs, sl.data(), sl.size(), s);
+                    upload(*br, rl.data(), rl.size(), s);
+                    c->halo_send[side][col_i].push_back(bs);
+                    c->halo_recv[side][col_i].push_back(br);
+                    c->halo_send_cnt[side][col_i].push_back((long long)sl.size());
+                    c->halo_recv_cnt[side][col_i].push_back((long long)rl.size());
+                }
+            }
+            CK(cudaStreamSynchronize(s));
+        }
+        *out = c;
+    });
+    if (rc != VBD_OK) delete c;
+    return rc;
+}
+
+int vbd_ctx_destroy(vbd_ctx* c)
+{
+    return guarded([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        delete c;
+    });
+}
+
+int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
+{
+    return guarded([&] {
+        if (!c || !info) fail(VBD_ERR_ARG, "NULL argument");
+        std::memset(info, 0, sizeof *info);
+        info->num_vertices = c->n;
+        info->num_solved = c->nsolve;
+        info->num_ghost = c->nfree_all - c->nsolve;
+        info->num_fixed = c->n - c->nfree_all;
+        info->num_tets = c->T;
+        info->num_entries = c->E;
+        info->num_colors = c->ncolors;
+        for (int k = 0; k < c->ncolors && k < 64; ++k) info->color_count[k] = c->ccnt[k];
+        long long b = 0;
+        for (DBuf* d : {&c->perm, &c->inv, &c->eoff, &c->ent, &c->mat, &c->pos, &c->xt, &c->vt, &c->vprev,
+                        &c->y, &c->ha, &c->hb, &c->mass, &c->out, &c->stage, &c->color_orig})
+            b += (long long)d->bytes;
+        info->device_bytes = b;
+        info->precision = c->precision;
+        info->inplace = c->inplace ? 1 : 0;
+        info->lanes_per_vertex = VBD_LANES;
+        info->num_materials = (int)c->mats.size();
+    });
+}
+
+int vbd_set_stream(vbd_ctx* c, void* stream)
+{
+    return guarded([&] {
+        if (!c) fail(VBD_ERR_ARG, "NULL ctx");
+        CK(cudaSetDevice(c->device));
+        CK(cudaStreamSynchronize(c->stream));
+        c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+        if (c->gexec) {  // graphs are stream-agnostic, but keep things simple
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+    });
+}
+
+int vbd_get_stream(vbd_ctx* c, void** stream)
+{
+    return guarded([&] {
+        if (!c || !stream) fail(VBD_ERR_ARG, "NULL argument");
+        *stream = (void*)c->stream;
+    });
+}
+
+int vbd_get_colors(vbd_ctx* c, int64_t* color_of)
+{
+    return guarded([&] {
+        if (!c || !color_of) fail(VBD_ERR_ARG, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        std::vector<int> h(c->n);
+        CK(cudaMemcpyAsync(h.data(), c->color_orig.p, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (long long v = 0; v < c->n; ++v) color_of[v] = h[v];
+    });
+}
+
+int vbd_set_state(vbd_ctx* c, const double* x, const double* x_t, const double* v_t,
+                  const double* v_prev, const double* y)
+{
+    return guarded([&] {
+        if (!c) fail(VBD_ERR_ARG, "NULL ctx");
+        CK(cudaSetDevice(c->device));
+        if (c->precision == VBD_PREC_F64) {
+            if (x) load_vec<double>(c, x, c->pos);
+            if (x_t) load_vec<double>(c, x_t, c->xt);
+            if (v_t) load_vec<double>(c, v_t, c->vt);
+            if (v_prev) load_vec<double>(c, v_prev, c->vprev);
+            if (y) load_vec<double>(c, y, c->y);
+        } else {
+            if (x) load_vec<float>(c, x, c->pos);
+            if (x_t) load_vec<float>(c, x_t, c->xt);
+            if (v_t) load_vec<float>(c, v_t, c->vt);
+            if (v_prev) load_vec<float>(c, v_prev, c->vprev);
+            if (y) load_vec<float>(c, y, c->y);
+        }
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vbd_get_state(vbd_ctx* c, double* x, double* x_t, double* v_t, double* v_prev, double* y)
+{
+    return guarded([&] {
+        if (!c) fail(VBD_ERR_ARG, "NULL ctx");
+        CK(cudaSetDevice(c->device));
+        if (c->precision == VBD_PREC_F64) {
+            if (x) store_vec<double>(c, c->pos, x);
+            if (x_t) store_vec<double>(c, c->xt, x_t);
+            if (v_t) store_vec<double>(c, c->vt, v_t);
+            if (v_prev) store_vec<double>(c, c->vprev, v_prev);
+            if (y) store_vec<double>(c, c->y, y);
+        } else {
+            if (x) store_vec<float>(c, c->pos, x);
+            if (x_t) store_vec<float>(c, c->xt, x_t);
+            if (v_t) store_vec<float>(c, c->vt, v_t);
+            if (v_prev) store_vec<float>(c, c->vprev, v_prev);
+            if (y) store_vec<float>(c, c->y, y);
+        }
+    });
+}
+
+int vbd_set_beam_velocities(vbd_ctx* c, const double* la)
+{
+    return guarded([&] {
+        if (!c || !la) fail(VBD_ERR_ARG, "NULL argument");
+        if (c->beams.empty()) fail(VBD_ERR_ARG, "context was not built from beams");
+        CK(cudaSetDevice(c->device));
+        cudaStream_t s = c->stream;
+        DBuf dla, posd, vd;
+        upload(dla, la, 6 * c->beams.size(), s);
+        posd.alloc(c->n * 24);
+        vd.alloc(c->n * 24);
+        // rest positions in original order from x_t
+        if (c->precision == VBD_PREC_F64)
+            k_store_vec<double><<<blocks_for(c->n), 256, 0, s>>>(c->xt.as<double4>(), posd.as<double>(),
+                                                                 c->inv.as<int>(), (int)c->n);
+        else
+            k_store_vec<float><<<blocks_for(c->n), 256, 0, s>>>(c->xt.as<float4>(), posd.as<double>(),
+                                                                c->inv.as<int>(), (int)c->n);
+        k_beam_velocity<<<blocks_for(c->n), 256, 0, s>>>(c->beams_dev.as<BeamDev>(), (int)c->beams.size(),
+                                                         dla.as<double>(), posd.as<double>(), c->n,
+                                                         vd.as<double>());
+        CK(cudaGetLastError());
+        for (DBuf* d : {&c->vt, &c->vprev}) {
+            if (c->precision == VBD_PREC_F64)
+                k_load_vec<double><<<blocks_for(c->n), 256, 0, s>>>(vd.as<double>(), d->as<double4>(),
+                                                                    c->perm.as<int>(), (int)c->n);
+            else
+                k_load_vec<float><<<blocks_for(c->n), 256, 0, s>>>(vd.as<double>(), d->as<float4>(),
+                                                                   c->perm.as<int>(), (int)c->n);
+        }
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+int vbd_step(vbd_ctx* c, const vbd_step_params* p, int32_t n_steps, vbd_step_result* res)
+{
+    return guarded([&] {
+        if (!c) fail(VBD_ERR_ARG, "NULL ctx");
+        if (c->in_step) fail(VBD_ERR_ARG, "a fine-grained step is in progress");
+        CK(cudaSetDevice(c->device));
+        if (c->precision == VBD_PREC_F64) do_step<double>(c, p, n_steps, res);
+        else do_step<float>(c, p, n_steps, res);
+    });
+}
+
+int vbd_color_pass(vbd_ctx* c, double* x, const double* x_t, const double* y, double h,
+                   const int64_t* group, int64_t ng, int32_t mode, int32_t line_search, double eps_det)
+{
+    return guarded([&] {
+        if (!c || !x || !x_t || !y) fail(VBD_ERR_ARG, "NULL argument");
+        if (ng > 0 && !group) fail(VBD_ERR_ARG, "NULL group");
+        if (mode != 0 && mode != 1) fail(VBD_ERR_ARG, "mode must be 0 or 1");
+        if (line_search && mode == 0)
+            fail(VBD_ERR_UNSUPPORTED, "local line search is not on the B200 hot path yet");
+        if (!(h > 0.0)) fail(VBD_ERR_ARG, "h must be positive");
+        CK(cudaSetDevice(c->device));
+        if (c->precision == VBD_PREC_F64) do_color_pass<double>(c, x, x_t, y, h, group, ng, mode, eps_det);
+        else do_color_pass<float>(c, x, x_t, y, h, group, ng, mode, eps_det);
+    });
+}
+
+int vbd_initialize(vbd_ctx* c, const vbd_step_params* p)
+{
+    return guarded([&] {
+        if (!c) fail(VBD_ERR_ARG, "NULL ctx");
+        if (c->in_step) fail(VBD_ERR_ARG, "a fine-grained step is in progress");
+        validate_params(p);
+        CK(cudaSetDevice(c->device));
+        c->cur = *p;
+        CK(cudaMemsetAsync(c->flag.p, 0xff, 8, c->stream));
+        if (c->precision == VBD_PREC_F64) enqueue_begin<double>(c);
+        else enqueue_begin<float>(c);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vbd_step_begin(vbd_ctx* c, const vbd_step_params* p)
+{
+    return guarded([&] {
+        if (!c) fail(VBD_ERR_ARG, "NULL ctx");
+        validate_params(p);
+        CK(cudaSetDevice(c->device));
+        c->cur = *p;
+        c->omegas = omega_table(p->rho, p->n_max);
+        c->in_step = true;
+        CK(cudaMemsetAsync(c->flag.p, 0xff, 8, c->stream));
+        CK(cudaMemsetAsync(c->stepctr.p, 0, 4, c->stream));
+        if (c->precision == VBD_PREC_F64) {
+            ensure_materials<double>(c, p->h);
+            enqueue_begin<double>(c);
+        } else {
+            ensure_materials<float>(c, p->h);
+            enqueue_begin<float>(c);
+        }
+        CK(cudaGetLastError());
+    });
+}
+
+int vbd_step_color(vbd_ctx* c, int32_t color, int32_t iter)
+{
+    return guarded([&] {
+        if (!c || !c->in_step) fail(VBD_ERR_ARG, "no step in progress");
+        if (color < 0 || color >= c->ncolors) fail(VBD_ERR_ARG, "bad colour");
+        bool check = c->cur.rho == 0.0;
+        if (c->precision == VBD_PREC_F64) color_sweep<double>(c, color, iter, check);
+        else color_sweep<float>(c, color, iter, check);
+        CK(cudaGetLastError());
+    });
+}
+
+int vbd_step_iter_end(vbd_ctx* c, int32_t iter)
+{
+    return guarded([&] {
+        if (!c || !c->in_step) fail(VBD_ERR_ARG, "no step in progress");
+        if (iter < 1 || iter > c->cur.n_max) fail(VBD_ERR_ARG, "bad iteration");
+        if (c->precision == VBD_PREC_F64) enqueue_iter_end<double>(c, iter);
+        else enqueue_iter_end<float>(c, iter);
+        CK(cudaGetLastError());
+    });
+}
+
+int vbd_step_end(vbd_ctx* c, vbd_step_result* res)
+{
+    return guarded([&] {
+        if (!c || !c->in_step) fail(VBD_ERR_ARG, "no step in progress");
+        if (c->precision == VBD_PREC_F64) enqueue_end<double>(c);
+        else enqueue_end<float>(c);
+        CK(cudaGetLastError());
+        c->in_step = false;
+        read_result(c, res);
+    });
+}
+
+int vbd_halo_count(vbd_ctx* c, int32_t side, int32_t color, int64_t* ns, int64_t* nr)
+{
+    return guarded([&] {
+        if (!c || side < 0 || side > 1) fail(VBD_ERR_ARG, "bad argument");
+        if (c->halo_send[side].empty()) {
+            if (ns) *ns = 0;
+            if (nr) *nr = 0;
+            return;
+        }
+        if (color < 0 || color >= c->ncolors) fail(VBD_ERR_ARG, "bad colour");
+        if (ns) *ns = c->halo_send_cnt[side][color][0];
+        if (nr) *nr = c->halo_recv_cnt[side][color][0];
+    });
+}
+
+int vbd_halo_pack(vbd_ctx* c, int32_t side, int32_t color, void* buf)
+{
+    return guarded([&] {
+        if (!c || side < 0 || side > 1 || c->halo_send[side].empty()) fail(VBD_ERR_ARG, "no halo");
+        long long n = c->halo_send_cnt[side][color][0];
+        if (!n) return;
+        const int* ids = c->halo_send[side][color][0]->as<int>();
+        if (c->precision == VBD_PREC_F64)
+            k_halo_pack<double><<<blocks_for(n), 256, 0, c->stream>>>(c->pos.as<double4>(), ids, (int)n,
+                                                                      (double4*)buf);
+        else
+            k_halo_pack<float><<<blocks_for(n), 256, 0, c->stream>>>(c->pos.as<float4>(), ids, (int)n,
+                                                                     (float4*)buf);
+        CK(cudaGetLastError());
+    });
+}
+
+int vbd_halo_unpack(vbd_ctx* c, int32_t side, int32_t color, const void* buf)
+{
+    return guarded([&] {
+        if (!c || side < 0 || side > 1 || c->halo_recv[side].empty()) fail(VBD_ERR_ARG, "no halo");
+        long long n = c->halo_recv_cnt[side][color][0];
+        if (!n) return;
+        const int* ids = c->halo_recv[side][color][0]->as<int>();
+        if (c->precision == VBD_PREC_F64)
+            k_halo_unpack<double><<<blocks_for(n), 256, 0, c->stream>>>(c->pos.as<double4>(), ids, (int)n,
+                                                                        (const double4*)buf);
+        else
+            k_halo_unpack<float><<<blocks_for(n), 256, 0, c->stream>>>(c->pos.as<float4>(), ids, (int)n,
+                                                                       (const float4*)buf);
+        CK(cudaGetLastError());
+    });
+}
+
+int vbd_greedy_color(int64_t n, const int64_t* noff, const int64_t* nids, const int64_t* order,
+                     int device, int64_t* color_of, int64_t* num_colors)
+{
+    return guarded([&] {
+        if (n < 0 || !noff || !color_of || (n > 0 && noff[n] > 0 && !nids)) fail(VBD_ERR_ARG, "bad CSR");
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+            fail(VBD_ERR_NODEVICE, "no CUDA device available (no CPU fallback)");
+        CK(cudaSetDevice(device));
+        if (n == 0) {
+            if (num_colors) *num_colors = 0;
+            return;
+        }
+        if (n >= (1LL << 31)) fail(VBD_ERR_UNSUPPORTED, "graph too large");
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{s};
+        long long m = noff[n];
+        std::vector<int> ids(m);
+        for (long long k = 0; k < m; ++k) {
+            if (nids[k] < 0 || nids[k] >= n) fail(VBD_ERR_ARG, "neighbour id out of range");
+            ids[k] = (int)nids[k];
+        }
+        DBuf doff, dids, drank, dcol;
+        upload(doff, noff, n + 1, s);
+        upload(dids, ids.data(), m, s);
+        const long long* rank = nullptr;
+        if (order) {
+            std::vector<long long> r(n, -1);
+            for (long long k = 0; k < n; ++k) {
+                if (order[k] < 0 || order[k] >= n || r[order[k]] >= 0)
+                    fail(VBD_ERR_ARG, "order must be a permutation of all vertices");
+                r[order[k]] = k;
+            }
+            upload(drank, r.data(), n, s);
+            rank = drank.as<long long>();
+        }
+        dcol.alloc(n * 4);
+        run_jp(doff.as<long long>(), dids.as<int>(), rank, n, dcol.as<int>(), s);
+        std::vector<int> hc(n);
+        CK(cudaMemcpyAsync(hc.data(), dcol.p, n * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        long long mx = -1;
+        for (long long v = 0; v < n; ++v) {
+            color_of[v] = hc[v];
+            mx = std::max<long long>(mx, hc[v]);
+        }
+        if (num_colors) *num_colors = mx + 1;
+    });
+}
+
+int vbd_profile_color_pass(vbd_ctx* c, double h, int32_t reps, double* ms)
+{
+    return guarded([&] {
+        if (!c || !ms || reps < 1) fail(VBD_ERR_ARG, "bad argument");
+        CK(cudaSetDevice(c->device));
+        cudaStream_t s = c->stream;
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        c->cur.eps_det = c->cur.eps_det > 0 ? c->cur.eps_det : 1e-10;
+        for (int col = 0; col < c->ncolors; ++col) {
+            if (c->precision == VBD_PREC_F64) ensure_materials<double>(c, h);
+            else ensure_materials<float>(c, h);
+            // warm-up launch
+            if (c->precision == VBD_PREC_F64) color_sweep<double>(c, col, 1, false);
+            else color_sweep<float>(c, col, 1, false);
+            CK(cudaEventRecord(e0, s));
+            for (int r = 0; r < reps; ++r) {
+                if (c->precision == VBD_PREC_F64) color_sweep<double>(c, col, 1, false);
+                else color_sweep<float>(c, col, 1, false);
+            }
+            CK(cudaEventRecord(e1, s));
+            CK(cudaEventSynchronize(e1));
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, e0, e1));
+            ms[col] = (double)t / reps;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,269 @@
+// vbd_kernels.cuh -- the sm_100a kernels of the VBD time step.
+//
+//   K1 k1_color_pass   per-colour Gauss-Seidel vertex update (_native.pyx:412-494, 582-589)
+//   K2 k2_step_init    inertia target + adaptive warm start + fixed clamp (solver.py:120-164)
+//   K3 k3_chebyshev    Chebyshev blend + history copy + non-finite check (solver.py:221-232,
+//                      282-288, 312-315)
+//   K4 k4_commit       v = (x - x_t)/h, rotate v_prev, x_t = x (solver.py:319-323)
+//   plus state transfer (original <-> colour-major order), aux-buffer scatter and halo
+//   pack/unpack for slab-decomposed scenes.
+#pragma once
+#include "vbd_common.cuh"
+
+template <typename R> struct K1Args {
+    typedef typename Vec4<R>::T R4;
+    typedef typename PlaneT<R>::T PL;
+    const PL* ent;           // entry planes
+    long long E;             // plane stride (entries)
+    const long long* off;    // entry offsets of free vertices (nfree + 1)
+    R4* pos;                 // current iterate x (in place)
+    const R4* xt;            // x_t (w unused)
+    const R4* y;             // inertia target, w = m / h^2
+    const Material<R>* mat;  // per-material constants for this h
+    const int* group;        // aux mode: vertex list (colour-major ids); nullptr = range
+    int vbeg, count;         // range [vbeg, vbeg + count) or group[0..count)
+    int nsolve;              // vertices >= nsolve are never solved (ghost / fixed)
+    R4* out;                 // aux mode: results per group slot; nullptr = in place
+    R eps_det;
+    int mode;                // 0 block Newton, 1 diagonal GD
+    unsigned long long* flag;  // non-finite report (nullptr = no check)
+    const int* perm;         // colour-major -> original id (for the report)
+    const int* stepctr;
+    int iter;
+};
+
+// One group of W lanes per vertex; lane j handles entries j, j+W, ... of its vertex and the
+// group reduces f (3) and H (6) with a fixed xor-butterfly (bitwise deterministic).
+template <typename R, int W>
+__global__ void __launch_bounds__(256) k1_color_pass(const K1Args<R> a)
+{
+    typedef typename Vec4<R>::T R4;
+    const int g = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) / W);
+    const int lane = threadIdx.x & (W - 1);
+    if (g >= a.count) return;
+    const unsigned gmask =
+        (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1)));
+    const int v = a.group ? a.group[g] : a.vbeg + g;
+    const R4 xi4 = a.pos[v];
+    if (v >= a.nsolve) {  // fixed / ghost: keep x (_native.pyx:424-426)
+        if (lane == 0 && a.out) a.out[g] = xi4;
+        return;
+    }
+    const R xi[3] = {xi4.x, xi4.y, xi4.z};
+    const R4 xt4 = a.xt[v];
+    const R dx[3] = {xi[0] - xt4.x, xi[1] - xt4.y, xi[2] - xt4.z};
+    R f[3] = {R(0), R(0), R(0)};
+    R H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+    const long long beg = a.off[v], end = a.off[v + 1];
+    for (long long k = beg + lane; k < end; k += W) {
+        const Entry<R> e = Entry<R>::load(a.ent, a.E, k);
+        const R4 p0 = a.pos[e.n[0]];
+        const R4 p1 = a.pos[e.n[1]];
+        const R4 p2 = a.pos[e.n[2]];
+        const R e0[3] = {p0.x - xi[0], p0.y - xi[1], p0.z - xi[2]};
+        const R e1[3] = {p1.x - xi[0], p1.y - xi[1], p1.z - xi[2]};
+        const R e2[3] = {p2.x - xi[0], p2.y - xi[1], p2.z - xi[2]};
+        const Material<R> m = a.mat[e.mat];
+        tet_contrib<R>(e0, e1, e2, e.w, e.V, m, dx, f, H);
+    }
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) f[q] += __shfl_xor_sync(gmask, f[q], o, W);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(gmask, H[q], o, W);
+    }
+    if (lane != 0) return;
+    const R4 y4 = a.y[v];
+    const R mih2 = y4.w;  // inertia term, _native.pyx:278-281
+    f[0] += mih2 * (y4.x - xi[0]);
+    f[1] += mih2 * (y4.y - xi[1]);
+    f[2] += mih2 * (y4.z - xi[2]);
+    H[0] += mih2;
+    H[3] += mih2;
+    H[5] += mih2;
+    R d[3];
+    block_solve<R>(f, H, a.eps_det, a.mode, d);
+    R4 nx = xi4;
+    nx.x = xi[0] + d[0];
+    nx.y = xi[1] + d[1];
+    nx.z = xi[2] + d[2];
+    if (a.out)
+        a.out[g] = nx;
+    else
+        a.pos[v] = nx;
+    if (a.flag && !finite3(nx.x, nx.y, nx.z))
+        atomicMin(a.flag, StepFlag::key((unsigned)*a.stepctr, (unsigned)a.iter, (unsigned)a.perm[v]));
+}
+
+template <typename R>
+__global__ void k_scatter_group(const typename Vec4<R>::T* __restrict__ out, const int* __restrict__ group,
+                                int ng, typename Vec4<R>::T* pos)
+{
+    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < ng) pos[group[g]] = out[g];
+}
+
+// ---------------------------------------------------------------------------------------
+// K2: y = x_t + h v_t + h^2 a (solver.py:120-122), warm start (solver.py:125-164), fixed
+// clamp, y.w = m / h^2, history seed.
+template <typename R> struct StepArgs {
+    typedef typename Vec4<R>::T R4;
+    int n;          // all vertices
+    int nsolve;     // free (solved) vertices; [nsolve, nfree_all) are ghosts
+    int nfree_all;  // vertices >= nfree_all are fixed
+    R4 *pos, *xt, *vt, *vprev, *y, *ha, *hb;
+    const R* mass;
+    double h, hh;   // h and h*h (host-computed)
+    double a[3];    // a_ext
+    double an[3];   // a_ext / |a_ext|
+    double anorm;   // |a_ext|
+    int init_mode;  // 0 prev_pos, 1 inertia, 2 inertia_accel, 3 adaptive
+    int hist;       // Chebyshev history needed
+    unsigned long long* flag;
+    const int* perm;
+    int* stepctr;
+};
+
+template <typename R>
+__global__ void k2_step_init(const StepArgs<R> s)
+{
+    typedef typename Vec4<R>::T R4;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= s.n) return;
+    const R4 xt = s.xt[i], vt = s.vt[i];
+    const R h = (R)s.h, hh = (R)s.hh;
+    const R ax = (R)s.a[0], ay = (R)s.a[1], az = (R)s.a[2];
+    R4 y;
+    y.x = xt.x + h * vt.x + hh * ax;
+    y.y = xt.y + h * vt.y + hh * ay;
+    y.z = xt.z + h * vt.z + hh * az;
+    y.w = s.mass[i] / hh;
+    R4 x = xt;
+    x.w = R(0);
+    if (i < s.nfree_all) {
+        if (s.init_mode == 1 || (s.init_mode == 3 && s.anorm == 0.0)) {
+            x.x = xt.x + h * vt.x;
+            x.y = xt.y + h * vt.y;
+            x.z = xt.z + h * vt.z;
+        } else if (s.init_mode == 2) {
+            x.x = y.x; x.y = y.y; x.z = y.z;
+        } else if (s.init_mode == 3) {
+            const R4 vp = s.vprev[i];
+            R atx = (vt.x - vp.x) / h, aty = (vt.y - vp.y) / h, atz = (vt.z - vp.z) / h;
+            R comp = atx * (R)s.an[0] + aty * (R)s.an[1] + atz * (R)s.an[2];
+            R at = comp / (R)s.anorm;
+            at = at < R(0) ? R(0) : (at > R(1) ? R(1) : at);
+            R sc = hh * at;
+            x.x = xt.x + h * vt.x + sc * ax;
+            x.y = xt.y + h * vt.y + sc * ay;
+            x.z = xt.z + h * vt.z + sc * az;
+        }
+    } else if (s.flag && !finite3(x.x, x.y, x.z)) {  // fixed vertices never pass through K1
+        atomicMin(s.flag, StepFlag::key((unsigned)*s.stepctr, 1u, (unsigned)s.perm[i]));
+    }
+    s.y[i] = y;
+    s.pos[i] = x;
+    if (s.hist) s.ha[i] = x;
+}
+
+// K3: Chebyshev semi-iterative blend against the iterate two sweeps back, then copy the
+// blended iterate into the history buffer that becomes x_prev1 (solver.py:221-232, 312-315),
+// then the non-finite check of solver.py:282-288.
+template <typename R>
+__global__ void k3_chebyshev(typename Vec4<R>::T* pos, typename Vec4<R>::T* hist, int n,
+                             double omega, int blend, unsigned long long* flag,
+                             const int* perm, const int* stepctr, int iter)
+{
+    typedef typename Vec4<R>::T R4;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    R4 x = pos[i];
+    if (blend) {
+        const R4 pp = hist[i];
+        const R w = (R)omega;
+        x.x = w * (x.x - pp.x) + pp.x;
+        x.y = w * (x.y - pp.y) + pp.y;
+        x.z = w * (x.z - pp.z) + pp.z;
+        pos[i] = x;
+    }
+    hist[i] = x;
+    if (flag && !finite3(x.x, x.y, x.z))
+        atomicMin(flag, StepFlag::key((unsigned)*stepctr, (unsigned)iter, (unsigned)perm[i]));
+}
+
+// K4: velocity commit (solver.py:319-323); skipped when the step reported a non-finite state.
+template <typename R>
+__global__ void k4_commit(typename Vec4<R>::T* pos, typename Vec4<R>::T* xt, typename Vec4<R>::T* vt,
+                          typename Vec4<R>::T* vprev, int n, double h,
+                          const unsigned long long* flag, int* stepctr)
+{
+    typedef typename Vec4<R>::T R4;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) atomicAdd(stepctr, 1);
+    if (i >= n || *flag != StepFlag::NONE) return;
+    const R4 x = pos[i], x0 = xt[i], v0 = vt[i];
+    const R hr = (R)h;
+    R4 v;
+    v.x = (x.x - x0.x) / hr;
+    v.y = (x.y - x0.y) / hr;
+    v.z = (x.z - x0.z) / hr;
+    v.w = R(0);
+    vprev[i] = v0;
+    vt[i] = v;
+    xt[i] = x;
+}
+
+// ---------------------------------------------------------------------------------------
+// state transfer: original-order (N,3) float64 <-> colour-major R4
+
+template <typename R>
+__global__ void k_load_vec(const double* __restrict__ src, typename Vec4<R>::T* dst,
+                           const int* __restrict__ perm, int n)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    long long o = perm[i];
+    typename Vec4<R>::T v;
+    v.x = (R)src[3 * o];
+    v.y = (R)src[3 * o + 1];
+    v.z = (R)src[3 * o + 2];
+    v.w = R(0);
+    dst[i] = v;
+}
+
+template <typename R>
+__global__ void k_store_vec(const typename Vec4<R>::T* __restrict__ src, double* dst,
+                            const int* __restrict__ inv, int n)
+{
+    int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    typename Vec4<R>::T v = src[inv[o]];
+    dst[3LL * o] = (double)v.x;
+    dst[3LL * o + 1] = (double)v.y;
+    dst[3LL * o + 2] = (double)v.z;
+}
+
+template <typename R>
+__global__ void k_fill_mih2(typename Vec4<R>::T* y, const R* mass, int n, double hh)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i].w = mass[i] / (R)hh;
+}
+
+// halo exchange for slab-decomposed scenes: gather/scatter the positions of a vertex list
+template <typename R>
+__global__ void k_halo_pack(const typename Vec4<R>::T* __restrict__ pos, const int* __restrict__ ids,
+                            int n, typename Vec4<R>::T* __restrict__ buf)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) buf[i] = pos[ids[i]];
+}
+
+template <typename R>
+__global__ void k_halo_unpack(typename Vec4<R>::T* pos, const int* __restrict__ ids, int n,
+                              const typename Vec4<R>::T* __restrict__ buf)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) pos[ids[i]] = buf[i];
+}
