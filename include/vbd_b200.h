@@ -70,6 +70,7 @@ typedef struct {
     int64_t num_colors;
     const int64_t* color_off;   /* (C+1,) */
     const int64_t* color_verts; /* (N,) colour groups, concatenated */
+    const double* rest_positions; /* (N,3) optional: spatial (Morton) order inside colours */
 } vbd_system_desc;
 
 /* A procedural generate_beam(nx, ny, nz, spacing, density) body, rigidly translated. */

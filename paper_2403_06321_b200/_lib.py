@@ -37,7 +37,7 @@ class SystemDesc(ctypes.Structure):
     _fields_ = [("num_vertices", i64), ("num_tets", i64), ("tets", P), ("tet_w", P),
                 ("tet_vol", P), ("tet_mu", P), ("tet_lam", P), ("tet_kd", P), ("masses", P),
                 ("kind", P), ("t_off", P), ("t_id", P), ("t_slot", P), ("num_colors", i64),
-                ("color_off", P), ("color_verts", P)]
+                ("color_off", P), ("color_verts", P), ("rest_positions", P)]
 
 
 class BeamDesc(ctypes.Structure):

@@ -83,6 +83,9 @@ class DeviceContext:
             t_off=_lib.i64c(system.t_off), t_id=_lib.i64c(system.t_id),
             t_slot=_lib.i64c(system.t_slot), color_off=_lib.i64c(system.color_off),
             color_verts=_lib.i64c(system.color_verts))
+        rp = getattr(system, "rest_positions", None)
+        if rp is not None:
+            arrs["rest_positions"] = _lib.f64c(rp, (n, 3))
         d = _lib.SystemDesc()
         d.num_vertices = n
         d.num_tets = len(arrs["tets"])

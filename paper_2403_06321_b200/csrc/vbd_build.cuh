@@ -265,26 +265,63 @@ __global__ void k_check_coloring(const int* __restrict__ tets, long long T, cons
 // ---------------------------------------------------------------------------------------
 // K6: colour-major order and entry packing
 
-// sort key: category (0 solved, 1 ghost, 2 fixed) | colour | rounds | original id
-__global__ void k_order_keys(const long long* __restrict__ off, const unsigned char* __restrict__ kind,
-                             const int* __restrict__ color, long long n, int W,
-                             unsigned long long* __restrict__ keys)
+__device__ __forceinline__ unsigned long long spread3(unsigned long long x)
+{
+    x &= 0x1fffffull;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+// 63-bit Morton code of the quantised rest position (21 bits per axis)
+__global__ void k_morton_keys(const double* __restrict__ pos, long long n, double lx, double ly,
+                              double lz, double scale, unsigned long long* __restrict__ keys,
+                              int* __restrict__ ids)
 {
     long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (v >= n) return;
+    double q[3] = {(pos[3 * v] - lx) * scale, (pos[3 * v + 1] - ly) * scale, (pos[3 * v + 2] - lz) * scale};
+    unsigned long long c[3];
+    for (int k = 0; k < 3; ++k) {
+        double t = q[k] < 0.0 ? 0.0 : (q[k] > 2097151.0 ? 2097151.0 : q[k]);
+        c[k] = (unsigned long long)t;
+    }
+    keys[v] = spread3(c[0]) << 2 | spread3(c[1]) << 1 | spread3(c[2]);
+    ids[v] = (int)v;
+}
+
+__global__ void k_iota(int* __restrict__ a, long long n)
+{
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (int)i;
+}
+
+// sort key: category (0 solved, 1 ghost, 2 fixed) | colour | rounds | spatial rank i
+// (the vertex at spatial rank i is order0[i])
+__global__ void k_order_keys(const long long* __restrict__ off, const unsigned char* __restrict__ kind,
+                             const int* __restrict__ color, const int* __restrict__ order0, long long n,
+                             int W, unsigned long long* __restrict__ keys)
+{
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int v = order0[i];
     unsigned long long cat = kind[v] == 1 ? 2ull : (kind[v] == 3 ? 1ull : 0ull);
     unsigned long long c = (unsigned long long)(color[v] < 0 ? 0 : color[v]) & 0xfffull;
     long long d = off[v + 1] - off[v];
     unsigned long long r = cat == 0 ? (unsigned long long)((d + W - 1) / W) & 0xfffull : 0ull;
-    keys[v] = (cat << 56) | (c << 44) | (r << 32) | (unsigned long long)v;
+    keys[i] = (cat << 56) | (c << 44) | (r << 32) | (unsigned long long)i;
 }
 
-__global__ void k_perm_from_keys(const unsigned long long* __restrict__ keys, long long n,
-                                 int* __restrict__ perm, int* __restrict__ inv)
+__global__ void k_perm_from_keys(const unsigned long long* __restrict__ keys,
+                                 const int* __restrict__ order0, long long n, int* __restrict__ perm,
+                                 int* __restrict__ inv)
 {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    int o = (int)(keys[i] & 0xffffffffull);
+    int o = order0[(long long)(keys[i] & 0xffffffffull)];
     perm[i] = o;
     inv[o] = (int)i;
 }

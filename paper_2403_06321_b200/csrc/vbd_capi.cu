@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -16,9 +17,22 @@
 #include "vbd_common.cuh"
 #include "vbd_kernels.cuh"
 
-#ifndef VBD_LANES
-#define VBD_LANES 8
-#endif
+// K1 launch variant (lanes per vertex W, entries per lane per iteration U, min blocks/SM);
+// selected per context from VBD_K1 (e.g. "8x1", "4x2", "4x2b3"), default below.
+struct K1Variant {
+    int W = 4, U = 2, minb = 3, pf = 1;
+};
+K1Variant k1_variant_from_env()
+{
+    K1Variant v;
+    const char* e = getenv("VBD_K1");
+    if (e && *e) {
+        int w = 0, u = 0, b = 0, p = 0;
+        int n = sscanf(e, "%dx%db%dp%d", &w, &u, &b, &p);
+        if (n >= 2) { v.W = w; v.U = u; v.minb = n >= 3 ? b : 1; v.pf = n >= 4 ? p : 0; }
+    }
+    return v;
+}
 
 namespace {
 
@@ -116,6 +130,7 @@ struct vbd_ctx {
     std::vector<BeamDev> beams;
     DBuf beams_dev;
     std::vector<int> hinv;  // host copy of inv (protocol colour pass)
+    K1Variant k1 = k1_variant_from_env();
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -159,6 +174,26 @@ void sort_pairs_i32(DBuf& keys, DBuf& vals, long long n, int end_bit, cudaStream
     CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<int>(), k2.as<int>(),
                                        vals.as<unsigned>(), v2.as<unsigned>(), (int64_t)n, 0,
                                        end_bit, s));
+    CK(cudaStreamSynchronize(s));
+    std::swap(keys.p, k2.p);
+    std::swap(keys.bytes, k2.bytes);
+    std::swap(vals.p, v2.p);
+    std::swap(vals.bytes, v2.bytes);
+}
+
+void sort_pairs_u64_i32(DBuf& keys, DBuf& vals, long long n, cudaStream_t s)
+{
+    DBuf k2, v2, tmp;
+    k2.alloc(n * 8);
+    v2.alloc(n * 4);
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<unsigned long long>(),
+                                       k2.as<unsigned long long>(), vals.as<int>(), v2.as<int>(),
+                                       (int64_t)n, 0, 64, s));
+    tmp.alloc(tb);
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<unsigned long long>(),
+                                       k2.as<unsigned long long>(), vals.as<int>(), v2.as<int>(),
+                                       (int64_t)n, 0, 64, s));
     CK(cudaStreamSynchronize(s));
     std::swap(keys.p, k2.p);
     std::swap(keys.bytes, k2.bytes);
@@ -218,7 +253,15 @@ struct Scene {
     DBuf mass;      // f64 (n)
     DBuf kind;      // u8 (n): 0 free, 1 fixed, 3 ghost
     DBuf color;     // int32 (n)
-    DBuf pos;       // f64 (n,3) rest positions (generator path) or empty
+    DBuf pos;       // f64 (n,3) rest positions (drives the spatial order) or empty
+    double bbox_lo[3] = {0.0, 0.0, 0.0};
+    double bbox_scale = 0.0;  // 2^21 - 1 over the largest bbox extent
+    void set_bbox(const double lo[3], const double hi[3])
+    {
+        double ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
+        for (int k = 0; k < 3; ++k) bbox_lo[k] = lo[k];
+        bbox_scale = ext > 0 ? 2097151.0 / ext : 0.0;
+    }
 };
 
 void build_incidence(Scene& sc, cudaStream_t s)
@@ -342,18 +385,34 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
         CK(cudaGetLastError());
         c->inplace = read_scalar<int>(bad.p, s) == 0;
     }
-    // order
+    // order: spatial (Morton code of the rest positions) inside each (category, colour,
+    // rounds) class, so the vertices of one CTA -- and their neighbours -- are compact in
+    // space and share L1/L2 lines.  Two stable radix sorts: Morton first, then the class.
+    DBuf order0;
+    order0.alloc(sc.n * 4);
+    if (sc.pos.p && sc.n) {
+        DBuf mk;
+        mk.alloc(sc.n * 8);
+        k_morton_keys<<<blocks_for(sc.n), 256, 0, s>>>(sc.pos.as<double>(), sc.n, sc.bbox_lo[0],
+                                                       sc.bbox_lo[1], sc.bbox_lo[2], sc.bbox_scale,
+                                                       mk.as<unsigned long long>(), order0.as<int>());
+        CK(cudaGetLastError());
+        sort_pairs_u64_i32(mk, order0, sc.n, s);
+    } else if (sc.n) {
+        k_iota<<<blocks_for(sc.n), 256, 0, s>>>(order0.as<int>(), sc.n);
+        CK(cudaGetLastError());
+    }
     DBuf keys;
     keys.alloc(sc.n * 8);
     k_order_keys<<<blocks_for(sc.n), 256, 0, s>>>(sc.inc_off.as<long long>(), sc.kind.as<unsigned char>(),
-                                                  sc.color.as<int>(), sc.n, VBD_LANES,
+                                                  sc.color.as<int>(), order0.as<int>(), sc.n, c->k1.W,
                                                   keys.as<unsigned long long>());
     CK(cudaGetLastError());
     sort_keys_u64(keys, sc.n, s);
     c->perm.alloc(sc.n * 4);
     c->inv.alloc(sc.n * 4);
-    k_perm_from_keys<<<blocks_for(sc.n), 256, 0, s>>>(keys.as<unsigned long long>(), sc.n,
-                                                      c->perm.as<int>(), c->inv.as<int>());
+    k_perm_from_keys<<<blocks_for(sc.n), 256, 0, s>>>(keys.as<unsigned long long>(), order0.as<int>(),
+                                                      sc.n, c->perm.as<int>(), c->inv.as<int>());
     CK(cudaGetLastError());
     // category / colour ranges from the sorted keys (host scan of the boundaries)
     std::vector<unsigned long long> hk(sc.n);
@@ -459,11 +518,30 @@ K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
     return a;
 }
 
-template <typename R> void launch_k1(const K1Args<R>& a, cudaStream_t s)
+template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, bool pf, cudaStream_t s)
+{
+    long long threads = (long long)a0.count * W;
+    K1Args<R> a = a0;
+    // prefetch distance in CTAs: 0 = each CTA prefetches its own entry range (measured best
+    // on B200; a one-wave look-ahead thrashes L2)
+    static const int dist = getenv("VBD_K1_PFDIST") ? atoi(getenv("VBD_K1_PFDIST")) : 0;
+    a.pf_dist = dist;
+    if (pf) k1_color_pass<R, W, U, B, true><<<blocks_for(threads), 256, 0, s>>>(a);
+    else k1_color_pass<R, W, U, B, false><<<blocks_for(threads), 256, 0, s>>>(a);
+}
+
+template <typename R> void launch_k1(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
 {
     if (a.count <= 0) return;
-    long long threads = (long long)a.count * VBD_LANES;
-    k1_color_pass<R, VBD_LANES><<<blocks_for(threads), 256, 0, s>>>(a);
+    const K1Variant& v = c->k1;
+    if (v.W == 8 && v.U == 1) launch_k1v<R, 8, 1, 1>(a, v.pf != 0, s);
+    else if (v.W == 8 && v.U == 2) launch_k1v<R, 8, 2, 1>(a, v.pf != 0, s);
+    else if (v.W == 4 && v.U == 1) launch_k1v<R, 4, 1, 1>(a, v.pf != 0, s);
+    else if (v.W == 4 && v.U == 2 && v.minb == 3) launch_k1v<R, 4, 2, 3>(a, v.pf != 0, s);
+    else if (v.W == 4 && v.U == 2) launch_k1v<R, 4, 2, 1>(a, v.pf != 0, s);
+    else if (v.W == 4 && v.U == 1 && v.minb == 4) launch_k1v<R, 4, 1, 4>(a, v.pf != 0, s);
+    else if (v.W == 8 && v.U == 1 && v.minb == 4) launch_k1v<R, 8, 1, 4>(a, v.pf != 0, s);
+    else fail(VBD_ERR_ARG, "unknown VBD_K1 variant");
 }
 
 // one colour pass of the step (in place when the colouring is valid, else aux buffer)
@@ -476,11 +554,11 @@ template <typename R> void color_sweep(vbd_ctx* c, int color, int iter, bool che
     if (!c->inplace) {
         // aux-buffer semantics over the contiguous colour range: compute into `out`, then copy
         a.out = c->out.as<typename Vec4<R>::T>();
-        launch_k1<R>(a, s);
+        launch_k1<R>(c, a, s);
         CK(cudaMemcpyAsync(c->pos.as<char>() + c->cbeg[color] * c->r4(), c->out.p,
                            c->ccnt[color] * c->r4(), cudaMemcpyDeviceToDevice, s));
     } else {
-        launch_k1<R>(a, s);
+        launch_k1<R>(c, a, s);
     }
 }
 
@@ -676,7 +754,7 @@ void do_color_pass(vbd_ctx* c, double* x, const double* x_t, const double* y, do
     a.group = gdev.as<int>();
     a.count = (int)ng;
     a.out = odev.as<R4>();
-    launch_k1<R>(a, s);
+    launch_k1<R>(c, a, s);
     CK(cudaGetLastError());
     std::vector<R4> ho(ng);
     CK(cudaMemcpyAsync(ho.data(), odev.p, ng * c->r4(), cudaMemcpyDeviceToHost, s));
@@ -843,6 +921,16 @@ int vbd_ctx_create(const vbd_system_desc* d, int device, int precision, vbd_ctx*
             if (color[v] < 0 && kind[v] != 1) fail(VBD_ERR_ARG, "vertex without colour");
         if (d->num_colors > 4095) fail(VBD_ERR_UNSUPPORTED, "too many colours");
         upload(sc.color, color.data(), N, s);
+        if (d->rest_positions && N) {
+            double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (long long v = 0; v < N; ++v)
+                for (int k = 0; k < 3; ++k) {
+                    lo[k] = std::min(lo[k], d->rest_positions[3 * v + k]);
+                    hi[k] = std::max(hi[k], d->rest_positions[3 * v + k]);
+                }
+            sc.set_bbox(lo, hi);
+            upload(sc.pos, d->rest_positions, 3 * N, s);
+        }
         CK(cudaStreamSynchronize(s));
         finish_pack(c, sc);
         *out = c;
@@ -934,6 +1022,19 @@ int vbd_ctx_create_beams(const vbd_beam_desc* beams, int64_t nb, int64_t slab_lo
         c->beams = tb;
         Scene sc;
         generate(sc, tb, n, T, c->beams_dev);
+        {
+            // bbox of the (whole) beams: the spatial order must not depend on the slab
+            double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (int64_t i = 0; i < nb; ++i) {
+                const vbd_beam_desc& d = beams[i];
+                const long long ext[3] = {d.nx - 1, d.ny - 1, d.nz - 1};
+                for (int k = 0; k < 3; ++k) {
+                    lo[k] = std::min(lo[k], d.origin[k]);
+                    hi[k] = std::max(hi[k], d.origin[k] + d.spacing * (double)ext[k]);
+                }
+            }
+            sc.set_bbox(lo, hi);
+        }
         DBuf dm;
         upload(dm, dens.data(), dens.size(), s);
         sc.mass.alloc(n * 8);
@@ -1035,7 +1136,7 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         info->device_bytes = b;
         info->precision = c->precision;
         info->inplace = c->inplace ? 1 : 0;
-        info->lanes_per_vertex = VBD_LANES;
+        info->lanes_per_vertex = c->k1.W;
         info->num_materials = (int)c->mats.size();
     });
 }

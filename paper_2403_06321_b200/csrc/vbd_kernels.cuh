@@ -30,16 +30,41 @@ template <typename R> struct K1Args {
     const int* perm;         // colour-major -> original id (for the report)
     const int* stepctr;
     int iter;
+    int pf_dist;             // L2 prefetch distance in CTAs (one residency wave)
 };
 
 // One group of W lanes per vertex; lane j handles entries j, j+W, ... of its vertex and the
 // group reduces f (3) and H (6) with a fixed xor-butterfly (bitwise deterministic).
-template <typename R, int W>
-__global__ void __launch_bounds__(256) k1_color_pass(const K1Args<R> a)
+template <typename R, int W, int U, int MINB, bool PF>
+__global__ void __launch_bounds__(256, MINB) k1_color_pass(const K1Args<R> a)
 {
     typedef typename Vec4<R>::T R4;
     const int g = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) / W);
     const int lane = threadIdx.x & (W - 1);
+    if (PF && threadIdx.x == 0 && !a.group) {
+        // A CTA's entries are one contiguous range per plane.  The TMA unit streams into L2
+        // (cp.async.bulk.prefetch.L2) the range of the CTA one residency wave ahead
+        // (pf_dist CTAs later; the first wave also fetches its own), so the per-lane loads
+        // of later waves hit L2 and DRAM sees a deep queue without registers or smem.
+        const int per = (int)(blockDim.x / W);
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            const long long b = w == 0 ? (long long)blockIdx.x + a.pf_dist : (long long)blockIdx.x;
+            if (w == 1 && blockIdx.x >= (unsigned)a.pf_dist) break;
+            const long long g0 = b * per;
+            const long long g1 = min((long long)a.count, g0 + per);
+            if (g0 >= g1) continue;
+            const long long e0 = a.off[a.vbeg + g0], e1 = a.off[a.vbeg + g1];
+            const unsigned bytes = (unsigned)((e1 - e0) * 16);
+            if (bytes)
+#pragma unroll
+                for (int pl = 0; pl < EntryPlanes<R>::P; ++pl) {
+                    const void* src = reinterpret_cast<const char*>(a.ent) + 16 * (pl * a.E + e0);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes)
+                                 : "memory");
+                }
+        }
+    }
     if (g >= a.count) return;
     const unsigned gmask =
         (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1)));
@@ -55,16 +80,36 @@ __global__ void __launch_bounds__(256) k1_color_pass(const K1Args<R> a)
     R f[3] = {R(0), R(0), R(0)};
     R H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
     const long long beg = a.off[v], end = a.off[v + 1];
-    for (long long k = beg + lane; k < end; k += W) {
-        const Entry<R> e = Entry<R>::load(a.ent, a.E, k);
-        const R4 p0 = a.pos[e.n[0]];
-        const R4 p1 = a.pos[e.n[1]];
-        const R4 p2 = a.pos[e.n[2]];
-        const R e0[3] = {p0.x - xi[0], p0.y - xi[1], p0.z - xi[2]};
-        const R e1[3] = {p1.x - xi[0], p1.y - xi[1], p1.z - xi[2]};
-        const R e2[3] = {p2.x - xi[0], p2.y - xi[1], p2.z - xi[2]};
-        const Material<R> m = a.mat[e.mat];
-        tet_contrib<R>(e0, e1, e2, e.w, e.V, m, dx, f, H);
+    // U entries per lane per iteration: all their loads (entry planes, then the 3U
+    // neighbour gathers) are issued before any math, for memory-level parallelism.
+    for (long long k0 = beg + lane; k0 < end; k0 += (long long)W * U) {
+        Entry<R> e[U];
+        R4 p[U][3];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long k = k0 + (long long)u * W;
+            if (u == 0 || k < end) e[u] = Entry<R>::load(a.ent, a.E, k);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long k = k0 + (long long)u * W;
+            if (u == 0 || k < end) {
+                p[u][0] = a.pos[e[u].n[0]];
+                p[u][1] = a.pos[e[u].n[1]];
+                p[u][2] = a.pos[e[u].n[2]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long k = k0 + (long long)u * W;
+            if (u == 0 || k < end) {
+                const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
+                const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
+                const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
+                const Material<R> m = a.mat[e[u].mat];
+                tet_contrib<R>(e0, e1, e2, e[u].w, e[u].V, m, dx, f, H);
+            }
+        }
     }
 #pragma unroll
     for (int o = W / 2; o > 0; o >>= 1) {

@@ -49,15 +49,23 @@ class SlabExchange:
     torch.distributed rank, or None.
     """
 
-    def __init__(self, ctxs, peers, stream=None):
+    def __init__(self, ctxs, peers, device=None):
+        import contextlib
+
         import torch
         self.ctxs = list(ctxs)
         self.peers = peers
         self.torch = torch
-        dev = torch.device("cuda", torch.cuda.current_device())
-        self.stream = stream or torch.cuda.Stream(device=dev)
-        for c in self.ctxs:
-            c.set_stream(self.stream.cuda_stream)
+        dev = torch.device(device) if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        if dev.type == "cuda":
+            self.stream = torch.cuda.Stream(device=dev)
+            for c in self.ctxs:
+                c.set_stream(self.stream.cuda_stream)
+            self._on_stream = lambda: torch.cuda.stream(self.stream)
+        else:  # CPU contexts (host-logic tests with gloo)
+            self.stream = None
+            self._on_stream = contextlib.nullcontext
         ncol = max(c.num_colors for c in self.ctxs)
         self.ncol = ncol
         self.bufs = []
@@ -73,17 +81,17 @@ class SlabExchange:
             self.bufs.append(per)
 
     @classmethod
-    def local(cls, ctxs):
-        """All slabs driven by this process on one GPU (ordered by x)."""
+    def local(cls, ctxs, device=None):
+        """All slabs driven by this process on one device (ordered by x)."""
         peers = [{0: ("local", i - 1) if i > 0 else None,
                   1: ("local", i + 1) if i + 1 < len(ctxs) else None} for i in range(len(ctxs))]
-        return cls(ctxs, peers)
+        return cls(ctxs, peers, device)
 
     @classmethod
-    def distributed(cls, ctx, rank, world):
+    def distributed(cls, ctx, rank, world, device=None):
         peers = [{0: ("rank", rank - 1) if rank > 0 else None,
                   1: ("rank", rank + 1) if rank + 1 < world else None}]
-        return cls([ctx], peers)
+        return cls([ctx], peers, device)
 
     def _exchange(self, color):
         torch = self.torch
@@ -105,7 +113,7 @@ class SlabExchange:
                     other_side = 1 - side
                     _, orb = self.bufs[j][other_side]
                     if ns:
-                        with torch.cuda.stream(self.stream):
+                        with self._on_stream():
                             orb[:ns].copy_(sbuf[:ns])
                     unpack.append((j, other_side, ns))
                 else:
@@ -115,7 +123,7 @@ class SlabExchange:
                         ops.append(dist.P2POp(dist.irecv, rbuf[:nr], j))
                     unpack.append((i, side, nr))
         if ops:
-            with torch.cuda.stream(self.stream):
+            with self._on_stream():
                 for r in dist.batch_isend_irecv(ops):
                     r.wait()
         for i, side, n in unpack:

@@ -37,7 +37,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.StepParams) == 8 + 4 + 4 + 8 + 8 + 24
     assert ctypes.sizeof(_lib.StepResult) == 24
     assert ctypes.sizeof(_lib.BeamDesc) == 3 * 8 + 2 * 8 + 24 + 24 + 8
-    assert ctypes.sizeof(_lib.SystemDesc) == 16 * 8
+    assert ctypes.sizeof(_lib.SystemDesc) == 17 * 8
 
 
 def test_no_cpu_fallback_without_gpu():
