@@ -233,9 +233,16 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         args.gpus = world
+    # one process per GPU; VBD_DIST_BACKEND=gloo (tests only) lets several ranks share a GPU
+    backend = os.environ.get("VBD_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
     from paper_2403_06321_b200.dist import SlabExchange
     from paper_2403_06321_b200.scenes import build, config
 
@@ -257,11 +264,12 @@ def run_ours(args):
             for _ in range(k):
                 exch.step(p)
 
+    clk = Clocks(local).__enter__()  # sampled from warm-up through the timed region
     do_steps(args.warmup)
     torch.cuda.synchronize()
     n_owned = int(info.num_solved + info.num_fixed) if exch is None else \
         (part[1] - part[0]) * cfg.beams[0].ny * cfg.beams[0].nz
-    tot = torch.tensor([float(n_owned)], device="cuda")
+    tot = torch.tensor([float(n_owned)], device=red_dev)
     if world > 1:
         dist.all_reduce(tot)
     n_total = int(tot.item())
@@ -277,14 +285,14 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=red_dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dist.barrier()
         return float(t.item())
 
-    with Clocks(local) as clk:
-        ms_total = timed(lambda: do_steps(args.steps))
+    ms_total = timed(lambda: do_steps(args.steps))
+    clk.__exit__(None, None, None)
     ms_step = ms_total / args.steps
     vit_per_step = n_total * cfg.n_max
     value = vit_per_step * args.steps / (ms_total / 1e3)

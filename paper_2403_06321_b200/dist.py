@@ -93,6 +93,10 @@ class SlabExchange:
                   1: ("rank", rank + 1) if rank + 1 < world else None}]
         return cls([ctx], peers, device)
 
+    def _stage_host(self):
+        import torch.distributed as dist
+        return self.stream is not None and dist.get_backend() == "gloo"
+
     def _exchange(self, color):
         torch = self.torch
         import torch.distributed as dist
@@ -122,7 +126,23 @@ class SlabExchange:
                     if nr:
                         ops.append(dist.P2POp(dist.irecv, rbuf[:nr], j))
                     unpack.append((i, side, nr))
-        if ops:
+        if ops and self._stage_host():
+            # gloo cannot send device tensors: stage through host memory (used only to run
+            # several ranks on one GPU for testing; NCCL is the production transport)
+            torch.cuda.current_stream().wait_stream(self.stream)
+            self.stream.synchronize()
+            host_ops, back = [], []
+            for op in ops:
+                h = op.tensor.cpu()
+                host_ops.append(dist.P2POp(op.op, h, op.peer))
+                if op.op is dist.irecv:
+                    back.append((op.tensor, h))
+            for r in dist.batch_isend_irecv(host_ops):
+                r.wait()
+            with self._on_stream():
+                for dst, h in back:
+                    dst.copy_(h)
+        elif ops:
             with self._on_stream():
                 for r in dist.batch_isend_irecv(ops):
                     r.wait()
