@@ -243,6 +243,8 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     red_dev = "cuda" if backend == "nccl" else "cpu"
+    if world > 1:  # first collective: every rank takes part (before any P2P batch)
+        dist.all_reduce(torch.zeros(1, device=red_dev))
     from paper_2403_06321_b200.dist import SlabExchange
     from paper_2403_06321_b200.scenes import build, config
 
@@ -315,16 +317,22 @@ def run_ours(args):
     got = ctx.get_state(x=True, x_t=True, v_t=True, v_prev=True,
                         out={"x": hx, "x_t": hxt, "v_t": hv, "v_prev": hvp})
 
+    bufs = {"x_t": hxt, "v_t": hv, "v_prev": hvp, "spare": hx}
+
     def e2e_steps():
         for _ in range(args.e2e_steps):
-            ctx.set_state(x_t=hxt, v_t=hv, v_prev=hvp)
+            b = bufs
+            ctx.set_state(x_t=b["x_t"], v_t=b["v_t"], v_prev=b["v_prev"])
             if exch is None:
                 ctx.step(p)
             else:
                 exch.step(p)
-            ctx.get_state(x=True, v_t=True, out={"x": hx, "v_t": hv})
-            hvp[...] = hv  # host-side rotation, as the reference's SimState does
-            hxt[...] = hx
+            # D2H of the result: x into the spare buffer, v_t into the retiring v_prev
+            ctx.get_state(x=True, v_t=True, out={"x": b["spare"], "v_t": b["v_prev"]})
+            # host-side commit as the reference's SimState does (x_t = x, v_prev = v_t),
+            # by rotating buffers instead of copying them
+            b["x_t"], b["spare"] = b["spare"], b["x_t"]
+            b["v_t"], b["v_prev"] = b["v_prev"], b["v_t"]
     e2e_ms = timed(e2e_steps) / args.e2e_steps
     e2e_value = vit_per_step / (e2e_ms / 1e3)
     h2d = 3 * 24 * n_total
