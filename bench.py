@@ -52,71 +52,110 @@ def parse():
 # ----------------------------------------------------------------------------------------
 # CPU reference (oracle/_ref: the reference's own compiled kernel; else the oracle port)
 
-def cpu_reference_sample(cfg_name, budget_s=15.0):
-    """Time the reference's colour-pass kernel on a bounded sample of the workload.
+def _stock_reference():
+    """The unmodified reference package (pip-installed into baseline/_ref), or None."""
+    path = ROOT / "baseline" / "_ref"
+    if not (path / "vbdsim").exists():
+        return None
+    if str(path) not in sys.path:
+        sys.path.insert(0, str(path))
+    try:
+        import vbdsim
+    except Exception:
+        return None
+    return vbdsim if vbdsim.backend_name() == "native" else None
 
-    The sample is a scaled-down scene of the same kind (same generator, material, h,
-    n_max, rho, constraints); vertex-iterations/s is size-independent to first order
-    (the reference has no cross-vertex reuse).  Threads: the reference as shipped takes
-    the GIL per tet inside its OpenMP loop, so it is timed at 1 thread and
-    at all host threads and the faster setting is reported with its core count.
+
+def _sample_meshes(cfg_name, cfg):
+    b = cfg.beams[0]
+    if cfg_name == "c4":
+        return [(b.nx, b.ny, b.nz, b.spacing)] * 8, "8 of the 10,368 generate_cube(15,0.3) objects"
+    if cfg_name == "c5":
+        n = 31
+        return [(n, n, n, b.spacing)], f"generate_beam({n},{n},{n},0.01) block (same material/h/n_max/BCs)"
+    if cfg_name == "c3":
+        return [(300, 4, 4, b.spacing)], "generate_beam(300,4,4,0.01) (1/10 of one C3 beam)"
+    return [(bb.nx, bb.ny, bb.nz, bb.spacing) for bb in cfg.beams], "full scene"
+
+
+def cpu_reference_sample(cfg_name, budget_s=15.0):
+    """Time the reference on a bounded sample of the workload, on this box's host cores.
+
+    Preferred: the UNMODIFIED reference package from baseline/_ref through its own public
+    API (vbdsim.generate_beam / build_system / make_state / step, compiled native backend).
+    Fallback: the reference's compiled kernel (oracle/_ref) driven by the oracle's step loop,
+    else the oracle's C port.  The sample is a scaled-down scene of the same kind (same
+    generator, material, h, n_max, rho, constraints); vertex-iterations/s is
+    size-independent to first order.  The as-shipped kernel takes the GIL per tet inside its
+    OpenMP loop, so 1 thread and all host threads are probed and the faster
+    setting is reported with its core count.
     """
-    from oracle import oracle as O
     from paper_2403_06321_b200.scenes import config
     cfg = config(cfg_name)
-    ref = O.ref_native()
-    kind = "reference" if ref is not None else "port"
     b = cfg.beams[0]
-    if cfg_name in ("c4",):
-        meshes = [O.generate_beam(b.nx, b.ny, b.nz, b.spacing) for _ in range(8)]
-        sample = "8 of the 10,368 generate_cube(15,0.3) objects"
-    elif cfg_name == "c5":
-        n = 31
-        meshes = [O.generate_beam(n, n, n, b.spacing)]
-        sample = f"generate_beam({n},{n},{n},0.01) block (same material/h/n_max/BCs)"
-    elif cfg_name == "c3":
-        meshes = [O.generate_beam(300, 4, 4, b.spacing)]
-        sample = "generate_beam(300,4,4,0.01) (1/10 of one C3 beam)"
-    else:
-        meshes = [O.generate_beam(bb.nx, bb.ny, bb.nz, bb.spacing) for bb in cfg.beams]
-        sample = "full scene"
-    fixed = []
-    off = 0
-    for m, bb in zip(meshes, list(cfg.beams) * len(meshes)):
-        if bb.fix_min_x:
-            fixed.extend((off + np.flatnonzero(m.rest_positions[:, 0] < 1e-9)).tolist())
-        off += m.num_vertices
-    # place the sample bodies apart (no contact in any config)
-    shifted = []
-    for k, m in enumerate(meshes):
-        p = m.rest_positions + np.array([0.0, 0.0, 2.0 * k])
-        shifted.append(O.Mesh(p, m.tets, m.rest_volumes, m.inv_rest_shape, m.masses))
-    s = O.build_system([(m, (b.mu, b.lam, b.kd)) for m in shifted], fixed)
-    n_total = s.num_vertices
+    dims, sample = _sample_meshes(cfg_name, cfg)
     ncores = len(os.sched_getaffinity(0))
+    vb = _stock_reference()
+    if vb is not None:
+        kind, how = "reference", "vbdsim.step (baseline/_ref, native backend)"
+        meshes = []
+        for k, (nx, ny, nz, sp) in enumerate(dims):
+            m = vb.generate_beam(nx, ny, nz, sp, density=b.density)
+            meshes.append(vb.build_tet_mesh(m.rest_positions + np.array([0.0, 0.0, 2.0 * k]),
+                                            m.tets, b.density))
+        fixed, off = [], 0
+        for m in meshes:
+            if b.fix_min_x:
+                fixed.extend((off + np.flatnonzero(m.rest_positions[:, 0] < 1e-9)).tolist())
+            off += m.num_vertices
+        s = vb.build_system([vb.Body(m, vb.MaterialParams(b.mu, b.lam, b.kd)) for m in meshes],
+                            [vb.FixedConstraint(int(v)) for v in fixed])
+        n_total, n_tets = s.num_vertices, len(s.tets)
+        rest = s.rest_positions
 
-    def one_step(st, threads):
-        t0 = time.perf_counter()
-        O.step(s, st, cfg.h, cfg.n_max, cfg.rho, cfg.a_ext, kernel=ref, n_threads=threads)
-        return time.perf_counter() - t0
+        def make():
+            return vb.make_state(s, x0=_x0(rest)) if cfg.random_init else vb.make_state(s)
 
-    def fresh():
-        st = O.make_state(s)
-        if cfg.random_init:
-            lo, hi = s.rest_positions.min(0), s.rest_positions.max(0)
-            x0 = np.random.default_rng(0).uniform(lo, hi, size=s.rest_positions.shape)
-            st = O.make_state(s, x0=x0)
-        return st
+        def one_step(st, threads):
+            prm = vb.SolverParams(h=cfg.h, n_max=cfg.n_max, rho=cfg.rho, a_ext=cfg.a_ext,
+                                  threads=threads)
+            t0 = time.perf_counter()
+            vb.step(st, prm)
+            return time.perf_counter() - t0
+    else:
+        from oracle import oracle as O
+        ref = O.ref_native()
+        kind = "reference" if ref is not None else "port"
+        how = "oracle step loop + " + ("oracle/_ref kernel" if ref is not None else "oracle C port")
+        meshes = []
+        for k, (nx, ny, nz, sp) in enumerate(dims):
+            m = O.generate_beam(nx, ny, nz, sp, b.density)
+            meshes.append(O.Mesh(m.rest_positions + np.array([0.0, 0.0, 2.0 * k]), m.tets,
+                                 m.rest_volumes, m.inv_rest_shape, m.masses))
+        fixed, off = [], 0
+        for m in meshes:
+            if b.fix_min_x:
+                fixed.extend((off + np.flatnonzero(m.rest_positions[:, 0] < 1e-9)).tolist())
+            off += m.num_vertices
+        s = O.build_system([(m, (b.mu, b.lam, b.kd)) for m in meshes], fixed)
+        n_total, n_tets = s.num_vertices, len(s.tets)
+        rest = s.rest_positions
 
-    # probe thread settings with one step each, keep the faster
+        def make():
+            return O.make_state(s, x0=_x0(rest)) if cfg.random_init else O.make_state(s)
+
+        def one_step(st, threads):
+            t0 = time.perf_counter()
+            O.step(s, st, cfg.h, cfg.n_max, cfg.rho, cfg.a_ext, kernel=ref, n_threads=threads)
+            return time.perf_counter() - t0
+
     best = None
     for threads in sorted({1, ncores}):
-        st = fresh()
-        dt = one_step(st, threads)
+        dt = one_step(make(), threads)
         if best is None or dt < best[1]:
             best = (threads, dt)
     threads = best[0]
-    st = fresh()
+    st = make()
     one_step(st, threads)  # warm-up
     times = []
     t_start = time.perf_counter()
@@ -127,10 +166,15 @@ def cpu_reference_sample(cfg_name, budget_s=15.0):
     ms = 1e3 * statistics.mean(times)
     rate = n_total * cfg.n_max / (ms / 1e3)
     return {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{sample}: {n_total} vertices, {len(s.tets)} tets, n_max={cfg.n_max}, "
+            "sample": f"{sample}: {n_total} vertices, {n_tets} tets, n_max={cfg.n_max}; {how}; "
                       f"mean of {len(times)} steps after 1 warm-up, {ms:.1f} ms/step; "
                       f"threads probed 1 and {ncores}, best={threads}",
             "ms_per_step_sample": ms}
+
+
+def _x0(rest):
+    lo, hi = rest.min(0), rest.max(0)
+    return np.random.default_rng(0).uniform(lo, hi, size=rest.shape)
 
 
 # ----------------------------------------------------------------------------------------
