@@ -303,8 +303,20 @@ def run_ours(args):
         exch = SlabExchange.distributed(ctx, rank, world)
     stream = torch.cuda.ExternalStream(ctx.stream) if ctx.stream else torch.cuda.current_stream()
 
+    twist = None
+    if cfg.twist_rev_s:  # C3: clamped ends driven kinematically, x_t rewritten every step
+        from paper_2403_06321_b200.scenes import twist_targets
+        rest = ctx.get_state(x=False, x_t=True)["x_t"]
+        twist = {"rest": rest, "k": 0}
+
     def do_steps(k):
-        if exch is None:
+        if twist is not None:
+            for _ in range(k):
+                twist["k"] += 1
+                idx, xyz = twist_targets(cfg, twist["rest"], twist["k"] * cfg.h)
+                ctx.set_fixed_targets(idx, xyz)
+                ctx.step(p)
+        elif exch is None:
             ctx.step(p, n_steps=k)
         else:
             for _ in range(k):
@@ -367,6 +379,9 @@ def run_ours(args):
         for _ in range(args.e2e_steps):
             b = bufs
             ctx.set_state(x_t=b["x_t"], v_t=b["v_t"], v_prev=b["v_prev"])
+            if twist is not None:
+                twist["k"] += 1
+                ctx.set_fixed_targets(*twist_targets(cfg, twist["rest"], twist["k"] * cfg.h))
             if exch is None:
                 ctx.step(p)
             else:

@@ -81,7 +81,7 @@ typedef struct {
     double origin[3];
     double mu, lam, kd;
     int32_t fix_min_x; /* FixedConstraint on every vertex with (x - origin.x) < 1e-9 */
-    int32_t reserved;
+    int32_t fix_max_x; /* ... and on every vertex of the last x plane (clamped far end) */
 } vbd_beam_desc;
 
 typedef struct {
@@ -129,6 +129,10 @@ int vbd_set_state(vbd_ctx* ctx, const double* x, const double* x_t, const double
                   const double* v_prev, const double* y); /* NULL = leave unchanged */
 int vbd_get_state(vbd_ctx* ctx, double* x, double* x_t, double* v_t, double* v_prev, double* y);
 int vbd_set_beam_velocities(vbd_ctx* ctx, const double* lin_ang); /* (num_beams,6) rigid v */
+/* kinematic boundary conditions: x_t (and x) of fixed vertices idx[0..n) (original ids) set to
+ * xyz (n,3) before the next step -- how the reference drives clamped ends
+ * (pkg/tests/test_acceptance.py:471-473 rewrites x/x_t of FixedConstraint vertices) */
+int vbd_set_fixed_targets(vbd_ctx* ctx, int64_t n, const int64_t* idx, const double* xyz);
 
 /* ---- the hot path ----------------------------------------------------------------------- */
 int vbd_step(vbd_ctx* ctx, const vbd_step_params* params, int32_t n_steps, vbd_step_result* res);

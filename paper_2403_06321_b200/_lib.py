@@ -43,7 +43,7 @@ class SystemDesc(ctypes.Structure):
 class BeamDesc(ctypes.Structure):
     _fields_ = [("nx", i64), ("ny", i64), ("nz", i64), ("spacing", f64), ("density", f64),
                 ("origin", f64 * 3), ("mu", f64), ("lam", f64), ("kd", f64),
-                ("fix_min_x", i32), ("reserved", i32)]
+                ("fix_min_x", i32), ("fix_max_x", i32)]
 
 
 class StepParams(ctypes.Structure):
@@ -79,6 +79,7 @@ SIGNATURES = {
     "vbd_set_state": (ctypes.c_int, [P, P, P, P, P, P]),
     "vbd_get_state": (ctypes.c_int, [P, P, P, P, P, P]),
     "vbd_set_beam_velocities": (ctypes.c_int, [P, P]),
+    "vbd_set_fixed_targets": (ctypes.c_int, [P, i64, P, P]),
     "vbd_step": (ctypes.c_int, [P, ctypes.POINTER(StepParams), i32, ctypes.POINTER(StepResult)]),
     "vbd_color_pass": (ctypes.c_int, [P, P, P, P, f64, P, i64, i32, i32, f64]),
     "vbd_initialize": (ctypes.c_int, [P, ctypes.POINTER(StepParams)]),

@@ -32,6 +32,7 @@ class Beam:
     density: float = 1000.0
     origin: tuple = (0.0, 0.0, 0.0)
     fix_min_x: bool = False
+    fix_max_x: bool = False
 
     def desc(self):
         d = _lib.BeamDesc()
@@ -40,6 +41,7 @@ class Beam:
         d.origin = (ctypes.c_double * 3)(*map(float, self.origin))
         d.mu, d.lam, d.kd = self.mu, self.lam, self.kd
         d.fix_min_x = 1 if self.fix_min_x else 0
+        d.fix_max_x = 1 if self.fix_max_x else 0
         return d
 
     @property
@@ -159,6 +161,11 @@ class DeviceContext:
                 res[k] = out[k] if out is not None and k in out else np.empty((self.n, 3))
         _lib.check(_lib.lib().vbd_get_state(self._h, *[_lib.ptr(res.get(k)) for k in names]))
         return res
+
+    def set_fixed_targets(self, idx, xyz):
+        i = _lib.i64c(idx).ravel()
+        p = _lib.f64c(xyz, (len(i), 3))
+        _lib.check(_lib.lib().vbd_set_fixed_targets(self._h, len(i), _lib.ptr(i), _lib.ptr(p)))
 
     def set_beam_velocities(self, lin_ang):
         a = _lib.f64c(lin_ang)

@@ -22,6 +22,7 @@ struct BeamDev {
     double origin[3];
     int mat;
     int fix_min_x;
+    int fix_max_x;
 };
 
 __constant__ int c_cell_even[5][4] = {{0, 3, 5, 6}, {1, 0, 3, 5}, {2, 0, 3, 6}, {4, 0, 5, 6}, {7, 3, 5, 6}};
@@ -51,7 +52,7 @@ __global__ void k_gen_vertices(const BeamDev* __restrict__ beams, int nb, long l
     pos[3 * v] = px + B.origin[0];
     pos[3 * v + 1] = py + B.origin[1];
     pos[3 * v + 2] = pz + B.origin[2];
-    kind[v] = (B.fix_min_x && px < 1e-9) ? 1 : 0;
+    kind[v] = ((B.fix_min_x && px < 1e-9) || (B.fix_max_x && ax == B.nx - 1)) ? 1 : 0;
 }
 
 // Tets of the generated cells in global (cell-major, then pattern) order, with the

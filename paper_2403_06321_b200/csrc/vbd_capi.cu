@@ -966,6 +966,7 @@ int vbd_ctx_create_beams(const vbd_beam_desc* beams, int64_t nb, int64_t slab_lo
                 B.spacing = d.spacing; B.density = d.density;
                 for (int k = 0; k < 3; ++k) B.origin[k] = d.origin[k];
                 B.fix_min_x = d.fix_min_x;
+                B.fix_max_x = d.fix_max_x;
                 B.mat = material_id(c, ids, MaterialKey{d.mu, d.lam, d.kd, d.density});
                 if ((int)dens.size() <= B.mat) dens.resize(B.mat + 1, d.density);
                 if (full || !slab) {
@@ -1251,6 +1252,38 @@ int vbd_set_beam_velocities(vbd_ctx* c, const double* la)
         }
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s));
+    });
+}
+
+int vbd_set_fixed_targets(vbd_ctx* c, int64_t n, const int64_t* idx, const double* xyz)
+{
+    return guarded([&] {
+        if (!c || (n > 0 && (!idx || !xyz))) fail(VBD_ERR_ARG, "NULL argument");
+        if (n <= 0) return;
+        CK(cudaSetDevice(c->device));
+        std::vector<int>& hinv = c->hinv;
+        if ((long long)hinv.size() != c->n) {
+            hinv.resize(c->n);
+            CK(cudaMemcpyAsync(hinv.data(), c->inv.p, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        std::vector<int> ids(n);
+        for (int64_t k = 0; k < n; ++k) {
+            if (idx[k] < 0 || idx[k] >= c->n) fail(VBD_ERR_ARG, "vertex out of range");
+            ids[k] = hinv[idx[k]];
+            if (ids[k] < c->nfree_all) fail(VBD_ERR_ARG, "kinematic targets apply to fixed vertices only");
+        }
+        DBuf did, dxyz;
+        upload(did, ids.data(), n, c->stream);
+        upload(dxyz, xyz, 3 * n, c->stream);
+        if (c->precision == VBD_PREC_F64)
+            k_set_targets<double><<<blocks_for(n), 256, 0, c->stream>>>(did.as<int>(), dxyz.as<double>(), (int)n,
+                                                                       c->xt.as<double4>(), c->pos.as<double4>());
+        else
+            k_set_targets<float><<<blocks_for(n), 256, 0, c->stream>>>(did.as<int>(), dxyz.as<double>(), (int)n,
+                                                                      c->xt.as<float4>(), c->pos.as<float4>());
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->stream));
     });
 }
 

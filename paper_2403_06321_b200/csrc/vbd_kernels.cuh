@@ -290,6 +290,21 @@ __global__ void k_store_vec(const typename Vec4<R>::T* __restrict__ src, double*
 }
 
 template <typename R>
+__global__ void k_set_targets(const int* __restrict__ ids, const double* __restrict__ xyz, int n,
+                              typename Vec4<R>::T* xt, typename Vec4<R>::T* pos)
+{
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    typename Vec4<R>::T v;
+    v.x = (R)xyz[3 * k];
+    v.y = (R)xyz[3 * k + 1];
+    v.z = (R)xyz[3 * k + 2];
+    v.w = R(0);
+    xt[ids[k]] = v;
+    pos[ids[k]] = v;
+}
+
+template <typename R>
 __global__ void k_fill_mih2(typename Vec4<R>::T* y, const R* mass, int n, double hh)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;

@@ -36,6 +36,7 @@ class Config:
     sharding: str = "objects"   # "objects" | "slabs" | "replicas"
     random_init: bool = False
     rigid_velocity: float = 0.0  # scale of seeded random rigid velocities (C4)
+    twist_rev_s: float = 0.0     # C3: clamped end planes rotate about the beam axis
     description: str = ""
 
     @property
@@ -71,11 +72,13 @@ def config(name: str, scale: float = 1.0) -> Config:
                       (0.0, 0.0, 0.0), sharding="replicas", random_init=True,
                       description="extreme init: generate_cube(37,0.5), x0 ~ U(bbox) rng 0")
     if name == "c3":
-        return Config("c3", (Beam(3032, 4, 4, 0.01, 5e4, 1e6, 1e-6, fix_min_x=True),
-                             Beam(3032, 4, 4, 0.01, 5e4, 1e6, 1e-6, origin=(0.0, 0.2, 0.0),
-                                  fix_min_x=True)),
-                      1 / 300, 100, 0.95, sharding="objects",
-                      description="two thin beams generate_beam(3032,4,4,0.01), root fixed")
+        n = max(4, int(round(3032 * scale)))
+        return Config("c3", (Beam(n, 4, 4, 0.01, 5e4, 1e6, 1e-6, fix_min_x=True, fix_max_x=True),
+                             Beam(n, 4, 4, 0.01, 5e4, 1e6, 1e-6, origin=(0.0, 0.2, 0.0),
+                                  fix_min_x=True, fix_max_x=True)),
+                      1 / 300, 100, 0.95, (0.0, 0.0, 0.0), sharding="replicas", twist_rev_s=0.5,
+                      description=f"two thin beams generate_beam({n},4,4,0.01), both ends "
+                                  "clamped and twisted +-0.5 rev/s (kinematic x_t)")
     if name == "c4":
         count = max(1, int(round(10368 * scale)))
         return Config("c4", _c4_beams(count), 1 / 120, 60, sharding="objects",
@@ -86,6 +89,38 @@ def config(name: str, scale: float = 1.0) -> Config:
         return Config("c5", (Beam(n, n, n, 0.01, 2e6, 2e7, 1e-7, fix_min_x=True),), 1 / 240, 40,
                       sharding="slabs", description=f"generate_beam({n},{n},{n},0.01), x=0 fixed")
     raise ValueError(f"unknown config {name!r}")
+
+
+def end_planes(cfg: Config):
+    """Original ids of the clamped end planes of every beam (x = first / last plane)."""
+    ids, off = [], 0
+    for b in cfg.beams:
+        plane = b.ny * b.nz
+        ids.append(off + np.arange(plane))
+        ids.append(off + (b.nx - 1) * plane + np.arange(plane))
+        off += b.num_vertices
+    return ids
+
+
+def twist_targets(cfg: Config, rest: np.ndarray, t: float):
+    """Kinematic targets of the clamped ends at time t: the x = min plane of each beam turns
+    by +2 pi f t and the x = max plane by -2 pi f t about the beam axis (SURVEY §8(d) C3;
+    the reference drives such BCs by rewriting x_t of fixed vertices, test_acceptance.py:471)."""
+    idx, xyz = [], []
+    planes = end_planes(cfg)
+    for k, b in enumerate(cfg.beams):
+        cy = b.origin[1] + 0.5 * b.spacing * (b.ny - 1)
+        cz = b.origin[2] + 0.5 * b.spacing * (b.nz - 1)
+        for side, sign in ((0, 1.0), (1, -1.0)):
+            ids = planes[2 * k + side]
+            th = sign * 2.0 * np.pi * cfg.twist_rev_s * t
+            p = rest[ids].copy()
+            dy, dz = p[:, 1] - cy, p[:, 2] - cz
+            p[:, 1] = cy + np.cos(th) * dy - np.sin(th) * dz
+            p[:, 2] = cz + np.sin(th) * dy + np.cos(th) * dz
+            idx.append(ids)
+            xyz.append(p)
+    return np.concatenate(idx), np.concatenate(xyz)
 
 
 def rigid_velocities(num_beams: int, scale: float, seed: int = 0):

@@ -278,3 +278,31 @@ def test_object_sharding_bitwise_equals_single_context(V):
     xw = whole.get_state(x=True)["x"]
     xp = np.concatenate([c.get_state(x=True)["x"] for c in parts])
     assert np.array_equal(xw, xp)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-10), ("fp32", 1e-5)])
+def test_twisting_beam_kinematic_bc(V, O, precision, tol):
+    """BASELINE config 3 at 1/10 length: both ends clamped and rotated by rewriting x_t of
+    the fixed vertices every step (as test_acceptance.py:471-473 drives the reference)."""
+    from paper_2403_06321_b200.scenes import config, twist_targets
+    cfg = config("c3", scale=0.1)
+    b = cfg.beams[0]
+    ctx = V.DeviceContext.from_beams([cfg.beams[0]], precision=precision)
+    m = O.generate_beam(b.nx, b.ny, b.nz, b.spacing)
+    plane = b.ny * b.nz
+    fixed = np.concatenate([np.arange(plane), (b.nx - 1) * plane + np.arange(plane)])
+    s = O.build_system([(m, (b.mu, b.lam, b.kd))], fixed)
+    st = O.make_state(s)
+    one = type(cfg)(cfg.name, (b,), cfg.h, cfg.n_max, cfg.rho, cfg.a_ext, twist_rev_s=cfg.twist_rev_s)
+    p = ctx.step_params(cfg.h, cfg.n_max, cfg.rho, 1e-10, "adaptive", cfg.a_ext)
+    for k in range(1, 11):
+        idx, xyz = twist_targets(one, s.rest_positions, k * cfg.h)
+        ctx.set_fixed_targets(idx, xyz)
+        ctx.step(p)
+        st.x_t[idx] = xyz
+        st.x[idx] = xyz
+        O.step(s, st, cfg.h, cfg.n_max, cfg.rho, cfg.a_ext)
+    x = ctx.get_state(x=True)["x"]
+    assert np.abs(x - st.x).max() / m.bbox_diagonal() <= tol
+    # the clamped ends really turned
+    assert np.abs(x[idx] - s.rest_positions[idx]).max() > 1e-3
