@@ -8,6 +8,8 @@
 //   plus state transfer (original <-> colour-major order), aux-buffer scatter and halo
 //   pack/unpack for slab-decomposed scenes.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "vbd_common.cuh"
 
 template <typename R> struct K1Args {
@@ -33,39 +35,12 @@ template <typename R> struct K1Args {
     int pf_dist;             // L2 prefetch distance in CTAs (one residency wave)
 };
 
-// One group of W lanes per vertex; lane j handles entries j, j+W, ... of its vertex and the
-// group reduces f (3) and H (6) with a fixed xor-butterfly (bitwise deterministic).
-template <typename R, int W, int U, int MINB, bool PF>
-__global__ void __launch_bounds__(256, MINB) k1_color_pass(const K1Args<R> a)
+// The per-vertex body of K1: group g (W lanes, this thread is lane `lane`) solves vertex
+// v = vbeg + g (or group[g]).
+template <typename R, int W, int U>
+__device__ __forceinline__ void k1_vertex(const K1Args<R>& a, int g, int lane)
 {
     typedef typename Vec4<R>::T R4;
-    const int g = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) / W);
-    const int lane = threadIdx.x & (W - 1);
-    if (PF && threadIdx.x == 0 && !a.group) {
-        // A CTA's entries are one contiguous range per plane.  The TMA unit streams into L2
-        // (cp.async.bulk.prefetch.L2) the range of the CTA one residency wave ahead
-        // (pf_dist CTAs later; the first wave also fetches its own), so the per-lane loads
-        // of later waves hit L2 and DRAM sees a deep queue without registers or smem.
-        const int per = (int)(blockDim.x / W);
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            const long long b = w == 0 ? (long long)blockIdx.x + a.pf_dist : (long long)blockIdx.x;
-            if (w == 1 && blockIdx.x >= (unsigned)a.pf_dist) break;
-            const long long g0 = b * per;
-            const long long g1 = min((long long)a.count, g0 + per);
-            if (g0 >= g1) continue;
-            const long long e0 = a.off[a.vbeg + g0], e1 = a.off[a.vbeg + g1];
-            const unsigned bytes = (unsigned)((e1 - e0) * 16);
-            if (bytes)
-#pragma unroll
-                for (int pl = 0; pl < EntryPlanes<R>::P; ++pl) {
-                    const void* src = reinterpret_cast<const char*>(a.ent) + 16 * (pl * a.E + e0);
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes)
-                                 : "memory");
-                }
-        }
-    }
-    if (g >= a.count) return;
     const unsigned gmask =
         (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1)));
     const int v = a.group ? a.group[g] : a.vbeg + g;
@@ -141,6 +116,41 @@ __global__ void __launch_bounds__(256, MINB) k1_color_pass(const K1Args<R> a)
         atomicMin(a.flag, StepFlag::key((unsigned)*a.stepctr, (unsigned)a.iter, (unsigned)a.perm[v]));
 }
 
+// One group of W lanes per vertex; lane j handles entries j, j+W, ... of its vertex and the
+// group reduces f (3) and H (6) with a fixed xor-butterfly (bitwise deterministic).
+template <typename R, int W, int U, int MINB, bool PF>
+__global__ void __launch_bounds__(256, MINB) k1_color_pass(const K1Args<R> a)
+{
+    typedef typename Vec4<R>::T R4;
+    const int g = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) / W);
+    const int lane = threadIdx.x & (W - 1);
+    if (PF && threadIdx.x == 0 && !a.group) {
+        // A CTA's entries are one contiguous range per plane.  The TMA unit streams into L2
+        // (cp.async.bulk.prefetch.L2) the range of the CTA one residency wave ahead
+        // (pf_dist CTAs later; the first wave also fetches its own), so the per-lane loads
+        // of later waves hit L2 and DRAM sees a deep queue without registers or smem.
+        const int per = (int)(blockDim.x / W);
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            const long long b = w == 0 ? (long long)blockIdx.x + a.pf_dist : (long long)blockIdx.x;
+            if (w == 1 && blockIdx.x >= (unsigned)a.pf_dist) break;
+            const long long g0 = b * per;
+            const long long g1 = min((long long)a.count, g0 + per);
+            if (g0 >= g1) continue;
+            const long long e0 = a.off[a.vbeg + g0], e1 = a.off[a.vbeg + g1];
+            const unsigned bytes = (unsigned)((e1 - e0) * 16);
+            if (bytes)
+#pragma unroll
+                for (int pl = 0; pl < EntryPlanes<R>::P; ++pl) {
+                    const void* src = reinterpret_cast<const char*>(a.ent) + 16 * (pl * a.E + e0);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes)
+                                 : "memory");
+                }
+        }
+    }
+    if (g < a.count) k1_vertex<R, W, U>(a, g, lane);
+}
+
 template <typename R>
 __global__ void k_scatter_group(const typename Vec4<R>::T* __restrict__ out, const int* __restrict__ group,
                                 int ng, typename Vec4<R>::T* pos)
@@ -171,11 +181,9 @@ template <typename R> struct StepArgs {
 };
 
 template <typename R>
-__global__ void k2_step_init(const StepArgs<R> s)
+__device__ __forceinline__ void k2_vertex(const StepArgs<R>& s, int i)
 {
     typedef typename Vec4<R>::T R4;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= s.n) return;
     const R4 xt = s.xt[i], vt = s.vt[i];
     const R h = (R)s.h, hh = (R)s.hh;
     const R ax = (R)s.a[0], ay = (R)s.a[1], az = (R)s.a[2];
@@ -212,17 +220,22 @@ __global__ void k2_step_init(const StepArgs<R> s)
     if (s.hist) s.ha[i] = x;
 }
 
+template <typename R>
+__global__ void k2_step_init(const StepArgs<R> s)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < s.n) k2_vertex<R>(s, i);
+}
+
 // K3: Chebyshev semi-iterative blend against the iterate two sweeps back, then copy the
 // blended iterate into the history buffer that becomes x_prev1 (solver.py:221-232, 312-315),
 // then the non-finite check of solver.py:282-288.
 template <typename R>
-__global__ void k3_chebyshev(typename Vec4<R>::T* pos, typename Vec4<R>::T* hist, int n,
-                             double omega, int blend, unsigned long long* flag,
-                             const int* perm, const int* stepctr, int iter)
+__device__ __forceinline__ void k3_vertex(typename Vec4<R>::T* pos, typename Vec4<R>::T* hist,
+                                          double omega, int blend, unsigned long long* flag,
+                                          const int* perm, const int* stepctr, int iter, int i)
 {
     typedef typename Vec4<R>::T R4;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
     R4 x = pos[i];
     if (blend) {
         const R4 pp = hist[i];
@@ -237,16 +250,22 @@ __global__ void k3_chebyshev(typename Vec4<R>::T* pos, typename Vec4<R>::T* hist
         atomicMin(flag, StepFlag::key((unsigned)*stepctr, (unsigned)iter, (unsigned)perm[i]));
 }
 
+template <typename R>
+__global__ void k3_chebyshev(typename Vec4<R>::T* pos, typename Vec4<R>::T* hist, int n,
+                             double omega, int blend, unsigned long long* flag,
+                             const int* perm, const int* stepctr, int iter)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) k3_vertex<R>(pos, hist, omega, blend, flag, perm, stepctr, iter, i);
+}
+
 // K4: velocity commit (solver.py:319-323); skipped when the step reported a non-finite state.
 template <typename R>
-__global__ void k4_commit(typename Vec4<R>::T* pos, typename Vec4<R>::T* xt, typename Vec4<R>::T* vt,
-                          typename Vec4<R>::T* vprev, int n, double h,
-                          const unsigned long long* flag, int* stepctr)
+__device__ __forceinline__ void k4_vertex(typename Vec4<R>::T* pos, typename Vec4<R>::T* xt,
+                                          typename Vec4<R>::T* vt, typename Vec4<R>::T* vprev,
+                                          double h, int i)
 {
     typedef typename Vec4<R>::T R4;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) atomicAdd(stepctr, 1);
-    if (i >= n || *flag != StepFlag::NONE) return;
     const R4 x = pos[i], x0 = xt[i], v0 = vt[i];
     const R hr = (R)h;
     R4 v;
@@ -257,6 +276,69 @@ __global__ void k4_commit(typename Vec4<R>::T* pos, typename Vec4<R>::T* xt, typ
     vprev[i] = v0;
     vt[i] = v;
     xt[i] = x;
+}
+
+template <typename R>
+__global__ void k4_commit(typename Vec4<R>::T* pos, typename Vec4<R>::T* xt, typename Vec4<R>::T* vt,
+                          typename Vec4<R>::T* vprev, int n, double h,
+                          const unsigned long long* flag, int* stepctr)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) atomicAdd(stepctr, 1);
+    if (i >= n || *flag != StepFlag::NONE) return;
+    k4_vertex<R>(pos, xt, vt, vprev, h, i);
+}
+
+// ---------------------------------------------------------------------------------------
+// Whole step in one persistent cooperative launch (small scenes: the per-colour passes of
+// C1-C3 are a few microseconds of work, so graph-node launch latency would dominate).
+// The same K1..K4 bodies run grid-stride, separated by grid-wide barriers.
+
+#define VBD_PERSIST_MAX_COLORS 64
+
+template <typename R> struct PersistArgs {
+    K1Args<R> k1;
+    StepArgs<R> s;
+    int ncolors;
+    int cbeg[VBD_PERSIST_MAX_COLORS];
+    int ccnt[VBD_PERSIST_MAX_COLORS];
+    int n_max;
+    int chebyshev;          // rho != 0
+    const double* omegas;   // [n_max + 1]
+};
+
+template <typename R, int W, int U>
+__global__ void __launch_bounds__(256, 3) k_step_persistent(const PersistArgs<R> p)
+{
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nth = gridDim.x * blockDim.x;
+    const int n = p.s.n;
+    for (int i = tid; i < n; i += nth) k2_vertex<R>(p.s, i);
+    grid.sync();
+    const int lane = threadIdx.x & (W - 1);
+    for (int it = 1; it <= p.n_max; ++it) {
+        for (int c = 0; c < p.ncolors; ++c) {
+            K1Args<R> a = p.k1;
+            a.vbeg = p.cbeg[c];
+            a.count = p.ccnt[c];
+            a.iter = it;
+            for (int g = tid / W; g < a.count; g += nth / W) k1_vertex<R, W, U>(a, g, lane);
+            grid.sync();
+        }
+        if (p.chebyshev) {
+            typename Vec4<R>::T* hist = (it % 2 == 1) ? p.s.hb : p.s.ha;
+            const double w = p.omegas[it];
+            const int blend = (it >= 2 && w != 1.0) ? 1 : 0;
+            for (int i = tid; i < n; i += nth)
+                k3_vertex<R>(p.s.pos, hist, w, blend, p.s.flag, p.s.perm, p.s.stepctr, it, i);
+            grid.sync();
+        }
+    }
+    if (*p.s.flag == StepFlag::NONE)
+        for (int i = tid; i < n; i += nth) k4_vertex<R>(p.s.pos, p.s.xt, p.s.vt, p.s.vprev, p.s.h, i);
+    if (tid == 0) atomicAdd(p.s.stepctr, 1);
 }
 
 // ---------------------------------------------------------------------------------------
