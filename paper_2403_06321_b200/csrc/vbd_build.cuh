@@ -423,6 +423,23 @@ __global__ void k_pack_entries<double>(const long long* __restrict__ off, const 
     (void)bad_volume;
 }
 
+// per-vertex material (solved vertices, colour-major order) when all incident tets agree
+__global__ void k_vertex_material(const long long* __restrict__ off, const unsigned* __restrict__ inc,
+                                  const int* __restrict__ tmat, const int* __restrict__ perm,
+                                  long long nsolve, int* __restrict__ vmat, int* __restrict__ mixed)
+{
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nsolve) return;
+    int o = perm[i];
+    int m = 0;
+    for (long long k = off[o]; k < off[o + 1]; ++k) {
+        int mk = tmat[inc[k] >> 2];
+        if (k == off[o]) m = mk;
+        else if (mk != m) atomicExch(mixed, 1);
+    }
+    vmat[i] = m;
+}
+
 template <typename R>
 __global__ void k_mass_new(const double* __restrict__ mass_orig, const int* __restrict__ perm,
                            long long n, R* __restrict__ mass)

@@ -21,11 +21,17 @@
 // selected per context from VBD_K1 (e.g. "8x1", "4x2", "4x2b3"), default below.
 struct K1Variant {
     int W = 4, U = 2, minb = 3, pf = 1;
+    int pipeU = 0, pipeS = 0;  // cp.async pipelined fp32 kernel (0 = off)
 };
 K1Variant k1_variant_from_env()
 {
     K1Variant v;
     const char* e = getenv("VBD_K1");
+    if (e && !strncmp(e, "pipe", 4)) {
+        int u = 0, st = 0;
+        if (sscanf(e + 4, "%dx%d", &u, &st) == 2) { v.pipeU = u; v.pipeS = st; }
+        return v;
+    }
     if (e && *e) {
         int w = 0, u = 0, b = 0, p = 0;
         int n = sscanf(e, "%dx%db%dp%d", &w, &u, &b, &p);
@@ -132,6 +138,8 @@ struct vbd_ctx {
     std::vector<int> hinv;  // host copy of inv (protocol colour pass)
     K1Variant k1 = k1_variant_from_env();
     DBuf omega_dev;
+    DBuf vmat;
+    bool uniform_mat = false;
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -465,6 +473,21 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
         fail(VBD_ERR_UNSUPPORTED,
              "fp32 layout recomputes tet volumes from |det W|; tet_vol disagrees with tet_w "
              "(use precision=fp64)");
+    // one material per vertex? (always true for bodies built by build_system)
+    {
+        DBuf mixed;
+        mixed.alloc(4);
+        CK(cudaMemsetAsync(mixed.p, 0, 4, s));
+        c->vmat.alloc(std::max<long long>(c->nsolve, 1) * 4);
+        if (c->nsolve)
+            k_vertex_material<<<blocks_for(c->nsolve), 256, 0, s>>>(
+                sc.inc_off.as<long long>(), sc.inc.as<unsigned>(), sc.tmat.as<int>(), c->perm.as<int>(),
+                c->nsolve, c->vmat.as<int>(), mixed.as<int>());
+        CK(cudaGetLastError());
+        c->uniform_mat = read_scalar<int>(mixed.p, s) == 0;
+        const char* e = getenv("VBD_UNIFORM_MAT");
+        if (e && *e == '0') c->uniform_mat = false;
+    }
     // masses in colour-major order
     c->mass.alloc(sc.n * sizeof(R));
     k_mass_new<R><<<blocks_for(sc.n), 256, 0, s>>>(sc.mass.as<double>(), c->perm.as<int>(), sc.n,
@@ -516,6 +539,8 @@ K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
     a.perm = c->perm.as<int>();
     a.stepctr = c->stepctr.as<int>();
     a.iter = iter;
+    a.pf_dist = 0;
+    a.vmat = c->uniform_mat ? c->vmat.as<int>() : nullptr;
     return a;
 }
 
@@ -527,22 +552,60 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     // on B200; a one-wave look-ahead thrashes L2)
     static const int dist = getenv("VBD_K1_PFDIST") ? atoi(getenv("VBD_K1_PFDIST")) : 0;
     a.pf_dist = dist;
-    if (pf) k1_color_pass<R, W, U, B, true><<<blocks_for(threads), 256, 0, s>>>(a);
-    else k1_color_pass<R, W, U, B, false><<<blocks_for(threads), 256, 0, s>>>(a);
+    const unsigned nb = blocks_for(threads);
+    const bool um = a.vmat != nullptr;
+    if (pf && um) k1_color_pass<R, W, U, B, true, true><<<nb, 256, 0, s>>>(a);
+    else if (pf) k1_color_pass<R, W, U, B, true, false><<<nb, 256, 0, s>>>(a);
+    else if (um) k1_color_pass<R, W, U, B, false, true><<<nb, 256, 0, s>>>(a);
+    else k1_color_pass<R, W, U, B, false, false><<<nb, 256, 0, s>>>(a);
+}
+
+template <int U, int S, bool UM> void launch_k1_pipe_v(const K1Args<float>& a, cudaStream_t s)
+{
+    constexpr int VPB = 256 / 4;
+    const int ntiles = (a.count + VPB - 1) / VPB;
+    static int grid_max = 0;
+    const size_t smem = sizeof(PipeSmem<4, U, S>);
+    if (!grid_max) {
+        CK(cudaFuncSetAttribute(k1_color_pass_pipe<4, U, S, UM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        int dev = 0, sms = 148, per = 1;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k1_color_pass_pipe<4, U, S, UM>, 256, smem));
+        grid_max = std::max(1, per) * sms;
+    }
+    const int grid = std::min(ntiles, grid_max);
+    k1_color_pass_pipe<4, U, S, UM><<<grid, 256, smem, s>>>(a, ntiles);
+}
+
+template <typename R> bool launch_k1_pipe(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
+{
+    return false;
+}
+
+template <> bool launch_k1_pipe<float>(const vbd_ctx* c, const K1Args<float>& a, cudaStream_t s)
+{
+    const K1Variant& v = c->k1;
+    if (!v.pipeU || a.group || a.out) return false;
+    const bool um = a.vmat != nullptr;
+    if (v.pipeU == 1 && v.pipeS == 3) um ? launch_k1_pipe_v<1, 3, true>(a, s) : launch_k1_pipe_v<1, 3, false>(a, s);
+    else if (v.pipeU == 1 && v.pipeS == 4) um ? launch_k1_pipe_v<1, 4, true>(a, s) : launch_k1_pipe_v<1, 4, false>(a, s);
+    else if (v.pipeU == 2 && v.pipeS == 2) um ? launch_k1_pipe_v<2, 2, true>(a, s) : launch_k1_pipe_v<2, 2, false>(a, s);
+    else if (v.pipeU == 2 && v.pipeS == 3) um ? launch_k1_pipe_v<2, 3, true>(a, s) : launch_k1_pipe_v<2, 3, false>(a, s);
+    else fail(VBD_ERR_ARG, "unknown VBD_K1 pipe variant (pipe1x3, pipe1x4, pipe2x2, pipe2x3)");
+    return true;
 }
 
 template <typename R> void launch_k1(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
 {
     if (a.count <= 0) return;
+    if (launch_k1_pipe<R>(c, a, s)) return;
     const K1Variant& v = c->k1;
-    if (v.W == 8 && v.U == 1) launch_k1v<R, 8, 1, 1>(a, v.pf != 0, s);
-    else if (v.W == 8 && v.U == 2) launch_k1v<R, 8, 2, 1>(a, v.pf != 0, s);
+    if (v.W == 4 && v.U == 2 && v.minb == 3) launch_k1v<R, 4, 2, 3>(a, v.pf != 0, s);
     else if (v.W == 4 && v.U == 1) launch_k1v<R, 4, 1, 1>(a, v.pf != 0, s);
-    else if (v.W == 4 && v.U == 2 && v.minb == 3) launch_k1v<R, 4, 2, 3>(a, v.pf != 0, s);
-    else if (v.W == 4 && v.U == 2) launch_k1v<R, 4, 2, 1>(a, v.pf != 0, s);
-    else if (v.W == 4 && v.U == 1 && v.minb == 4) launch_k1v<R, 4, 1, 4>(a, v.pf != 0, s);
-    else if (v.W == 8 && v.U == 1 && v.minb == 4) launch_k1v<R, 8, 1, 4>(a, v.pf != 0, s);
-    else fail(VBD_ERR_ARG, "unknown VBD_K1 variant");
+    else if (v.W == 8 && v.U == 1) launch_k1v<R, 8, 1, 1>(a, v.pf != 0, s);
+    else fail(VBD_ERR_ARG, "unknown VBD_K1 variant (4x2b3, 4x1, 8x1)");
 }
 
 // one colour pass of the step (in place when the colouring is valid, else aux buffer)

@@ -109,7 +109,7 @@ template <> struct PlaneT<double> { typedef double2 T; };
 //   f  -= V (mu F w + lam (J - gamma) C w) + dsc He (x_i - x_t,i)
 //   H  += (1 + dsc) He,  He = V (lam (C w)(C w)^T + mu |w|^2 I)
 // H is kept as 6 unique entries (xx, xy, xz, yy, yz, zz).
-template <typename R>
+template <typename R, bool DAMP = true>
 __device__ __forceinline__ void tet_contrib(const R* __restrict__ e0, const R* __restrict__ e1,
                                             const R* __restrict__ e2, const R* __restrict__ w,
                                             R V, const Material<R>& m, const R* __restrict__ dx,
@@ -150,14 +150,24 @@ __device__ __forceinline__ void tet_contrib(const R* __restrict__ e0, const R* _
     he[3] = vl * cw[1] * cw[1] + vmw;
     he[4] = vl * cw[1] * cw[2];
     he[5] = vl * cw[2] * cw[2] + vmw;
-    R hd0 = he[0] * dx[0] + he[1] * dx[1] + he[2] * dx[2];
-    R hd1 = he[1] * dx[0] + he[3] * dx[1] + he[4] * dx[2];
-    R hd2 = he[2] * dx[0] + he[4] * dx[1] + he[5] * dx[2];
-    f[0] -= V * (m.mu * Fw[0] + coef * cw[0]) + m.dsc * hd0;
-    f[1] -= V * (m.mu * Fw[1] + coef * cw[1]) + m.dsc * hd1;
-    f[2] -= V * (m.mu * Fw[2] + coef * cw[2]) + m.dsc * hd2;
+    if (DAMP) {
+        R hd0 = he[0] * dx[0] + he[1] * dx[1] + he[2] * dx[2];
+        R hd1 = he[1] * dx[0] + he[3] * dx[1] + he[4] * dx[2];
+        R hd2 = he[2] * dx[0] + he[4] * dx[1] + he[5] * dx[2];
+        f[0] -= V * (m.mu * Fw[0] + coef * cw[0]) + m.dsc * hd0;
+        f[1] -= V * (m.mu * Fw[1] + coef * cw[1]) + m.dsc * hd1;
+        f[2] -= V * (m.mu * Fw[2] + coef * cw[2]) + m.dsc * hd2;
 #pragma unroll
-    for (int q = 0; q < 6; ++q) H[q] += m.opd * he[q];
+        for (int q = 0; q < 6; ++q) H[q] += m.opd * he[q];
+    } else {
+        // one material per vertex: sum the undamped blocks; the caller applies
+        // f -= dsc * (sum He) dx and H = (1 + dsc) sum He once per vertex
+        f[0] -= V * (m.mu * Fw[0] + coef * cw[0]);
+        f[1] -= V * (m.mu * Fw[1] + coef * cw[1]);
+        f[2] -= V * (m.mu * Fw[2] + coef * cw[2]);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) H[q] += he[q];
+    }
 }
 
 // Guarded 3x3 block solve of _native.pyx:465-479 on the symmetric H (6 unique entries):

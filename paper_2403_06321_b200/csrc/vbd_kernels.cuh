@@ -33,12 +33,13 @@ template <typename R> struct K1Args {
     const int* stepctr;
     int iter;
     int pf_dist;             // L2 prefetch distance in CTAs (one residency wave)
+    const int* vmat;         // per-vertex material when every vertex has one material, else null
 };
 
 // The per-vertex body of K1: group g (W lanes, this thread is lane `lane`) solves vertex
-// v = vbeg + g (or group[g]).
-template <typename R, int W, int U>
-__device__ __forceinline__ void k1_vertex(const K1Args<R>& a, int g, int lane)
+// v = vbeg + g (or group[g]).  UM: one material per vertex (damping hoisted out of the loop).
+template <typename R, int W, int U, bool UM>
+__device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int lane)
 {
     typedef typename Vec4<R>::T R4;
     const unsigned gmask =
@@ -55,6 +56,8 @@ __device__ __forceinline__ void k1_vertex(const K1Args<R>& a, int g, int lane)
     R f[3] = {R(0), R(0), R(0)};
     R H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
     const long long beg = a.off[v], end = a.off[v + 1];
+    Material<R> mv;
+    if (UM) mv = a.mat[a.vmat[v]];
     // U entries per lane per iteration: all their loads (entry planes, then the 3U
     // neighbour gathers) are issued before any math, for memory-level parallelism.
     for (long long k0 = beg + lane; k0 < end; k0 += (long long)W * U) {
@@ -81,8 +84,12 @@ __device__ __forceinline__ void k1_vertex(const K1Args<R>& a, int g, int lane)
                 const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
                 const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
                 const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
-                const Material<R> m = a.mat[e[u].mat];
-                tet_contrib<R>(e0, e1, e2, e[u].w, e[u].V, m, dx, f, H);
+                if (UM) {
+                    tet_contrib<R, false>(e0, e1, e2, e[u].w, e[u].V, mv, dx, f, H);
+                } else {
+                    const Material<R> m = a.mat[e[u].mat];
+                    tet_contrib<R, true>(e0, e1, e2, e[u].w, e[u].V, m, dx, f, H);
+                }
             }
         }
     }
@@ -94,6 +101,18 @@ __device__ __forceinline__ void k1_vertex(const K1Args<R>& a, int g, int lane)
         for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(gmask, H[q], o, W);
     }
     if (lane != 0) return;
+    if (UM && end > beg) {
+        // hoisted Rayleigh damping (_native.pyx:309-317 summed over the vertex's tets):
+        // f -= dsc (sum He) dx,  H = (1 + dsc) sum He
+        const R hd0 = H[0] * dx[0] + H[1] * dx[1] + H[2] * dx[2];
+        const R hd1 = H[1] * dx[0] + H[3] * dx[1] + H[4] * dx[2];
+        const R hd2 = H[2] * dx[0] + H[4] * dx[1] + H[5] * dx[2];
+        f[0] -= mv.dsc * hd0;
+        f[1] -= mv.dsc * hd1;
+        f[2] -= mv.dsc * hd2;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) H[q] *= mv.opd;
+    }
     const R4 y4 = a.y[v];
     const R mih2 = y4.w;  // inertia term, _native.pyx:278-281
     f[0] += mih2 * (y4.x - xi[0]);
@@ -116,9 +135,16 @@ __device__ __forceinline__ void k1_vertex(const K1Args<R>& a, int g, int lane)
         atomicMin(a.flag, StepFlag::key((unsigned)*a.stepctr, (unsigned)a.iter, (unsigned)a.perm[v]));
 }
 
+template <typename R, int W, int U>
+__device__ __forceinline__ void k1_vertex(const K1Args<R>& a, int g, int lane)
+{
+    if (a.vmat) k1_vertex_impl<R, W, U, true>(a, g, lane);
+    else k1_vertex_impl<R, W, U, false>(a, g, lane);
+}
+
 // One group of W lanes per vertex; lane j handles entries j, j+W, ... of its vertex and the
 // group reduces f (3) and H (6) with a fixed xor-butterfly (bitwise deterministic).
-template <typename R, int W, int U, int MINB, bool PF>
+template <typename R, int W, int U, int MINB, bool PF, bool UM>
 __global__ void __launch_bounds__(256, MINB) k1_color_pass(const K1Args<R> a)
 {
     typedef typename Vec4<R>::T R4;
@@ -148,7 +174,214 @@ __global__ void __launch_bounds__(256, MINB) k1_color_pass(const K1Args<R> a)
                 }
         }
     }
-    if (g < a.count) k1_vertex<R, W, U>(a, g, lane);
+    if (g < a.count) k1_vertex_impl<R, W, U, UM>(a, g, lane);
+}
+
+// ---------------------------------------------------------------------------------------
+// K1 (pipelined, fp32, range mode): persistent CTAs walk tiles of 256/W vertices of the
+// colour range; every warp streams its lanes' entries (and, at a tile start, x / x_t of the
+// lane's vertex) into shared memory with per-lane cp.async (LDGSTS) S-1 items ahead of the
+// one it computes, so the entry latency leaves the dependency chain and only the neighbour
+// gathers remain.  An item = one iteration of the warp: U entries per lane.  Each lane only
+// reads its own shared-memory slots, so no barrier is needed between copy and use.
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? 16 : 0;  // src-size 0 -> zero fill, no global read
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait()
+{
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int W, int U, int S>
+struct PipeSmem {
+    static constexpr int SLOTS = 3 * U + 2;  // U entries x 3 planes, then x and x_t
+    float4 buf[8][S][SLOTS][32];
+};
+
+template <int W, int U, int S, bool UM>
+__global__ void __launch_bounds__(256, 3) k1_color_pass_pipe(const K1Args<float> a, int ntiles)
+{
+    constexpr int VPB = 256 / W;   // vertices per tile
+    constexpr int VPW = 32 / W;    // vertices per warp
+    constexpr int SL = PipeSmem<W, U, S>::SLOTS;
+    extern __shared__ float4 dyn_smem[];
+    auto& sm = *reinterpret_cast<PipeSmem<W, U, S>*>(dyn_smem);
+    const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
+    const int lane = l32 & (W - 1), sub = l32 / W;
+    const unsigned gmask = (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << (l32 & ~(W - 1)));
+    const long long E = a.E;
+    const float4* __restrict__ ent = a.ent;
+
+    // tile descriptor of this lane's vertex
+    struct Desc {
+        int v;        // vertex (colour-major id) or -1
+        long long beg, end;
+        int rounds;   // warp-uniform
+    };
+    auto describe = [&](int tile) {
+        Desc d;
+        const int g = tile * VPB + warp * VPW + sub;
+        d.v = (tile < ntiles && g < a.count) ? a.vbeg + g : -1;
+        d.beg = d.v >= 0 ? a.off[d.v] : 0;
+        d.end = d.v >= 0 ? a.off[d.v + 1] : 0;
+        int r = (int)((d.end - d.beg + W * U - 1) / (W * U));
+        r = __reduce_max_sync(0xffffffffu, r);
+        d.rounds = r < 1 ? 1 : r;
+        return d;
+    };
+    auto issue = [&](const Desc& d, int it, int stage) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long k = d.beg + lane + (long long)(it * U + u) * W;
+            const bool ok = d.v >= 0 && k < d.end;
+            const long long ks = ok ? k : 0;
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl)
+                cp_async16(&sm.buf[warp][stage][pl * U + u][l32], ent + pl * E + ks, ok);
+        }
+        if (it == 0) {
+            const int vv = d.v >= 0 ? d.v : 0;
+            cp_async16(&sm.buf[warp][stage][3 * U][l32], a.pos + vv, d.v >= 0);
+            cp_async16(&sm.buf[warp][stage][3 * U + 1][l32], a.xt + vv, d.v >= 0);
+        }
+        cp_async_commit();
+    };
+
+    int tile = blockIdx.x;
+    if (tile >= ntiles) return;
+    Desc cur = describe(tile);
+    Desc nxt = describe(tile + gridDim.x);
+    // prologue: items 0 .. S-2
+    int itile = tile, iit = 0;     // issue cursor
+    Desc icur = cur, inxt = nxt;
+    int stage_issue = 0;
+    for (int p = 0; p < S - 1; ++p) {
+        if (itile < ntiles) issue(icur, iit, stage_issue);
+        else cp_async_commit();
+        stage_issue = (stage_issue + 1) % S;
+        if (++iit == icur.rounds) {
+            iit = 0;
+            itile += gridDim.x;
+            icur = inxt;
+            inxt = describe(itile + gridDim.x);
+        }
+    }
+    int it = 0, stage = 0;
+    float xi[3] = {0.f, 0.f, 0.f}, dx[3] = {0.f, 0.f, 0.f};
+    float f[3], H[6];
+    Material<float> mv;
+    while (tile < ntiles) {
+        // issue the item S-1 ahead
+        if (itile < ntiles) issue(icur, iit, stage_issue);
+        else cp_async_commit();
+        stage_issue = (stage_issue + 1) % S;
+        if (++iit == icur.rounds) {
+            iit = 0;
+            itile += gridDim.x;
+            icur = inxt;
+            inxt = describe(itile + gridDim.x);
+        }
+        cp_async_wait<S - 1>();  // this lane's copies of the current item have landed
+        if (it == 0) {
+            const float4 x4 = sm.buf[warp][stage][3 * U][l32];
+            const float4 t4 = sm.buf[warp][stage][3 * U + 1][l32];
+            xi[0] = x4.x; xi[1] = x4.y; xi[2] = x4.z;
+            dx[0] = x4.x - t4.x; dx[1] = x4.y - t4.y; dx[2] = x4.z - t4.z;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) f[q] = 0.f;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) H[q] = 0.f;
+            if (UM && cur.v >= 0) mv = a.mat[a.vmat[cur.v]];
+        }
+        float4 pos[U][3];
+        Entry<float> e[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long k = cur.beg + lane + (long long)(it * U + u) * W;
+            ok[u] = cur.v >= 0 && k < cur.end;
+            const float4 p0 = sm.buf[warp][stage][u][l32];
+            const float4 p1 = sm.buf[warp][stage][U + u][l32];
+            const float4 p2 = sm.buf[warp][stage][2 * U + u][l32];
+            const unsigned u0 = __float_as_uint(p0.x), u1 = __float_as_uint(p0.y), u2 = __float_as_uint(p0.z);
+            e[u].n[0] = (int)(u0 & VBD_ID_MASK);
+            e[u].n[1] = (int)(u1 & VBD_ID_MASK);
+            e[u].n[2] = (int)(u2 & VBD_ID_MASK);
+            e[u].mat = (int)((u0 >> VBD_ID_BITS) | ((u1 >> VBD_ID_BITS) << 3) | ((u2 >> VBD_ID_BITS) << 6));
+            e[u].w[0] = p0.w;
+            e[u].w[1] = p1.x; e[u].w[2] = p1.y; e[u].w[3] = p1.z; e[u].w[4] = p1.w;
+            e[u].w[5] = p2.x; e[u].w[6] = p2.y; e[u].w[7] = p2.z; e[u].w[8] = p2.w;
+            if (ok[u]) {
+                pos[u][0] = a.pos[e[u].n[0]];
+                pos[u][1] = a.pos[e[u].n[1]];
+                pos[u][2] = a.pos[e[u].n[2]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+            const float* w = e[u].w;
+            const float dd = w[0] * (w[4] * w[8] - w[5] * w[7]) - w[1] * (w[3] * w[8] - w[5] * w[6]) +
+                             w[2] * (w[3] * w[7] - w[4] * w[6]);
+            const float V = __fdividef(1.0f / 6.0f, fabsf(dd));
+            const float e0[3] = {pos[u][0].x - xi[0], pos[u][0].y - xi[1], pos[u][0].z - xi[2]};
+            const float e1[3] = {pos[u][1].x - xi[0], pos[u][1].y - xi[1], pos[u][1].z - xi[2]};
+            const float e2[3] = {pos[u][2].x - xi[0], pos[u][2].y - xi[1], pos[u][2].z - xi[2]};
+            if (UM) {
+                tet_contrib<float, false>(e0, e1, e2, w, V, mv, dx, f, H);
+            } else {
+                const Material<float> m = a.mat[e[u].mat];
+                tet_contrib<float, true>(e0, e1, e2, w, V, m, dx, f, H);
+            }
+        }
+        stage = (stage + 1) % S;
+        if (++it < cur.rounds) continue;
+        // vertex finished: group reduction, inertia, guarded solve, in-place write
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) f[q] += __shfl_xor_sync(gmask, f[q], o, W);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(gmask, H[q], o, W);
+        }
+        if (lane == 0 && cur.v >= 0) {
+            const int v = cur.v;
+            if (UM && cur.end > cur.beg) {
+                const float hd0 = H[0] * dx[0] + H[1] * dx[1] + H[2] * dx[2];
+                const float hd1 = H[1] * dx[0] + H[3] * dx[1] + H[4] * dx[2];
+                const float hd2 = H[2] * dx[0] + H[4] * dx[1] + H[5] * dx[2];
+                f[0] -= mv.dsc * hd0;
+                f[1] -= mv.dsc * hd1;
+                f[2] -= mv.dsc * hd2;
+#pragma unroll
+                for (int q = 0; q < 6; ++q) H[q] *= mv.opd;
+            }
+            const float4 y4 = a.y[v];
+            const float mih2 = y4.w;
+            f[0] += mih2 * (y4.x - xi[0]);
+            f[1] += mih2 * (y4.y - xi[1]);
+            f[2] += mih2 * (y4.z - xi[2]);
+            H[0] += mih2;
+            H[3] += mih2;
+            H[5] += mih2;
+            float d[3];
+            block_solve<float>(f, H, a.eps_det, a.mode, d);
+            const float4 nx = make_float4(xi[0] + d[0], xi[1] + d[1], xi[2] + d[2], 0.f);
+            a.pos[v] = nx;
+            if (a.flag && !finite3(nx.x, nx.y, nx.z))
+                atomicMin(a.flag, StepFlag::key((unsigned)*a.stepctr, (unsigned)a.iter, (unsigned)a.perm[v]));
+        }
+        it = 0;
+        tile += gridDim.x;
+        cur = nxt;
+        nxt = describe(tile + gridDim.x);
+    }
+    cp_async_wait<0>();
 }
 
 template <typename R>
