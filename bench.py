@@ -430,7 +430,9 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": ncu_traffic(cfg.name, args.precision),
                          "kernel": "k1_color_pass", "peak_source": peak_kind,
                          "k1_ms_per_color": [round(float(x), 4) for x in k1_ms],
-                         "algorithmic_bytes_per_iteration": bytes_iter},
+                         "algorithmic_bytes_per_iteration": bytes_iter,
+                         "algorithmic_bytes_per_launch": bytes_iter / max(1, int(info.num_colors)),
+                         "traffic_unit": "DRAM bytes per k1 launch (ncu, profiles/k1_traffic.json)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
