@@ -91,6 +91,8 @@ typedef struct {
     double rho;
     double eps_det;
     double a_ext[3];
+    int32_t line_search; /* 17-trial local backtracking per vertex (_native.pyx:481-492) */
+    int32_t reserved;
 } vbd_step_params;
 
 typedef struct {

@@ -440,7 +440,7 @@ class NonFinite(Exception):
 
 
 def step(system, st, h, n_max, rho=0.0, a_ext=(0.0, 0.0, 0.0), eps_det=1e-10,
-         init_mode="adaptive", kernel=None, n_threads=0, on_iteration=None):
+         init_mode="adaptive", kernel=None, n_threads=0, on_iteration=None, line_search=False):
     """solver.py:291-324 without contact.  ``kernel`` selects the colour-pass
     implementation: None -> the C restatement, or the reference's compiled
     module (``ref_native()``)."""
@@ -454,10 +454,10 @@ def step(system, st, h, n_max, rho=0.0, a_ext=(0.0, 0.0, 0.0), eps_det=1e-10,
     for n in range(1, n_max + 1):
         for g in groups:
             if kernel is None:
-                color_pass(system, st.x, st.x_t, st.y, h, g, 0, False, eps_det, n_threads)
+                color_pass(system, st.x, st.x_t, st.y, h, g, 0, line_search, eps_det, n_threads)
             else:
                 kernel.color_pass(view, view.carr, st.x, st.x_t, st.y, h, g, 0,
-                                  line_search=False, eps_det=eps_det, mu_c=0.0, eps_v=1e-2,
+                                  line_search=line_search, eps_det=eps_det, mu_c=0.0, eps_v=1e-2,
                                   n_threads=n_threads)
         omega = chebyshev_omega(rho, n)
         if omega != 1.0 and st.x_pp is not None:

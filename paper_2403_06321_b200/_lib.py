@@ -48,7 +48,7 @@ class BeamDesc(ctypes.Structure):
 
 class StepParams(ctypes.Structure):
     _fields_ = [("h", f64), ("n_max", i32), ("init_mode", i32), ("rho", f64),
-                ("eps_det", f64), ("a_ext", f64 * 3)]
+                ("eps_det", f64), ("a_ext", f64 * 3), ("line_search", i32), ("reserved", i32)]
 
 
 class StepResult(ctypes.Structure):

@@ -173,8 +173,10 @@ class DeviceContext:
 
     # -- hot path -----------------------------------------------------------------------
     @staticmethod
-    def step_params(h, n_max, rho=0.0, eps_det=1e-10, init_mode="adaptive", a_ext=(0, 0, 0)):
+    def step_params(h, n_max, rho=0.0, eps_det=1e-10, init_mode="adaptive", a_ext=(0, 0, 0),
+                    line_search=False):
         p = _lib.StepParams()
+        p.line_search = 1 if line_search else 0
         p.h, p.n_max, p.rho, p.eps_det = float(h), int(n_max), float(rho), float(eps_det)
         p.init_mode = _lib.INIT_MODES[init_mode]
         p.a_ext = (ctypes.c_double * 3)(*map(float, a_ext))

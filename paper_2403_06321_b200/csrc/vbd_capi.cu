@@ -541,6 +541,7 @@ K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
     a.iter = iter;
     a.pf_dist = 0;
     a.vmat = c->uniform_mat ? c->vmat.as<int>() : nullptr;
+    a.line_search = 0;
     return a;
 }
 
@@ -600,6 +601,10 @@ template <> bool launch_k1_pipe<float>(const vbd_ctx* c, const K1Args<float>& a,
 template <typename R> void launch_k1(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
 {
     if (a.count <= 0) return;
+    if (a.line_search && a.mode == 0) {
+        k1_color_pass_ls<R><<<blocks_for((long long)a.count * 4), 256, 0, s>>>(a);
+        return;
+    }
     if (launch_k1_pipe<R>(c, a, s)) return;
     const K1Variant& v = c->k1;
     if (v.W == 4 && v.U == 2 && v.minb == 3) launch_k1v<R, 4, 2, 3>(a, v.pf != 0, s);
@@ -613,6 +618,7 @@ template <typename R> void color_sweep(vbd_ctx* c, int color, int iter, bool che
 {
     cudaStream_t s = c->stream;
     K1Args<R> a = k1_args<R>(c, c->cur.eps_det, 0, check, iter);
+    a.line_search = c->cur.line_search ? 1 : 0;
     a.vbeg = (int)c->cbeg[color];
     a.count = (int)c->ccnt[color];
     if (!c->inplace) {
@@ -779,7 +785,7 @@ template <typename R> void do_step(vbd_ctx* c, const vbd_step_params* p, int n_s
     cudaStream_t s = c->stream;
     CK(cudaMemsetAsync(c->flag.p, 0xff, 8, s));
     CK(cudaMemsetAsync(c->stepctr.p, 0, 4, s));
-    if (use_persistent(c)) {
+    if (use_persistent(c) && !p->line_search) {
         c->omega_dev.alloc((p->n_max + 1) * sizeof(double));
         CK(cudaMemcpyAsync(c->omega_dev.p, c->omegas.data(), (p->n_max + 1) * sizeof(double),
                            cudaMemcpyHostToDevice, s));
@@ -832,7 +838,7 @@ template <typename R> void store_vec(vbd_ctx* c, const DBuf& src, double* host)
 
 template <typename R>
 void do_color_pass(vbd_ctx* c, double* x, const double* x_t, const double* y, double h,
-                   const int64_t* group, int64_t ng, int mode, double eps_det)
+                   const int64_t* group, int64_t ng, int mode, int line_search, double eps_det)
 {
     typedef typename Vec4<R>::T R4;
     cudaStream_t s = c->stream;
@@ -862,6 +868,7 @@ void do_color_pass(vbd_ctx* c, double* x, const double* x_t, const double* y, do
     K1Args<R> a = k1_args<R>(c, eps_det, mode, false, 0);
     a.group = gdev.as<int>();
     a.count = (int)ng;
+    a.line_search = line_search ? 1 : 0;
     a.out = odev.as<R4>();
     launch_k1<R>(c, a, s);
     CK(cudaGetLastError());
@@ -1414,12 +1421,10 @@ int vbd_color_pass(vbd_ctx* c, double* x, const double* x_t, const double* y, do
         if (!c || !x || !x_t || !y) fail(VBD_ERR_ARG, "NULL argument");
         if (ng > 0 && !group) fail(VBD_ERR_ARG, "NULL group");
         if (mode != 0 && mode != 1) fail(VBD_ERR_ARG, "mode must be 0 or 1");
-        if (line_search && mode == 0)
-            fail(VBD_ERR_UNSUPPORTED, "local line search is not on the B200 hot path yet");
         if (!(h > 0.0)) fail(VBD_ERR_ARG, "h must be positive");
         CK(cudaSetDevice(c->device));
-        if (c->precision == VBD_PREC_F64) do_color_pass<double>(c, x, x_t, y, h, group, ng, mode, eps_det);
-        else do_color_pass<float>(c, x, x_t, y, h, group, ng, mode, eps_det);
+        if (c->precision == VBD_PREC_F64) do_color_pass<double>(c, x, x_t, y, h, group, ng, mode, line_search, eps_det);
+        else do_color_pass<float>(c, x, x_t, y, h, group, ng, mode, line_search, eps_det);
     });
 }
 

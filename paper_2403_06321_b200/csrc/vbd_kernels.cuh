@@ -34,11 +34,51 @@ template <typename R> struct K1Args {
     int iter;
     int pf_dist;             // L2 prefetch distance in CTAs (one residency wave)
     const int* vmat;         // per-vertex material when every vertex has one material, else null
+    int line_search;         // 17-trial local backtracking (mode 0 only)
 };
 
 // The per-vertex body of K1: group g (W lanes, this thread is lane `lane`) solves vertex
 // v = vbeg + g (or group[g]).  UM: one material per vertex (damping hoisted out of the loop).
-template <typename R, int W, int U, bool UM>
+// Local energy G_i of vertex v at position p (_native.pyx:201-258, tet + inertia terms),
+// summed over the W lanes of the group (identical in every lane).
+template <typename R, int W>
+__device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int lane, unsigned gmask,
+                          const R* p, const typename Vec4<R>::T& y4)
+{
+    typedef typename Vec4<R>::T R4;
+    R e = R(0);
+    for (long long k = beg + lane; k < end; k += W) {
+        const Entry<R> en = Entry<R>::load(a.ent, a.E, k);
+        const R4 q0 = a.pos[en.n[0]], q1 = a.pos[en.n[1]], q2 = a.pos[en.n[2]];
+        const R e0[3] = {q0.x - p[0], q0.y - p[1], q0.z - p[2]};
+        const R e1[3] = {q1.x - p[0], q1.y - p[1], q1.z - p[2]};
+        const R e2[3] = {q2.x - p[0], q2.y - p[1], q2.z - p[2]};
+        R F[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                F[r * 3 + c] = e0[r] * en.w[c] + e1[r] * en.w[3 + c] + e2[r] * en.w[6 + c];
+        R ic = R(0);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) ic += F[q] * F[q];
+        const R J = F[0] * (F[4] * F[8] - F[7] * F[5]) + F[3] * (F[7] * F[2] - F[1] * F[8]) +
+                    F[6] * (F[1] * F[5] - F[4] * F[2]);
+        const Material<R> m = a.mat[en.mat];
+        const R psi = (R(0.5) * m.mu) * (ic - R(3)) + (R(0.5) * m.lam) * (J - m.gamma) * (J - m.gamma);
+        e += en.V * psi;
+    }
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) e += __shfl_xor_sync(gmask, e, o, W);
+    R ein = R(0);
+    const R d0 = p[0] - y4.x, d1 = p[1] - y4.y, d2 = p[2] - y4.z;
+    ein = ein + ((R(0.5) * y4.w) * d0) * d0;
+    ein = ein + ((R(0.5) * y4.w) * d1) * d1;
+    ein = ein + ((R(0.5) * y4.w) * d2) * d2;
+    return ein + e;
+}
+
+template <typename R, int W, int U, bool UM, bool LS = false>
 __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int lane)
 {
     typedef typename Vec4<R>::T R4;
@@ -100,7 +140,7 @@ __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int la
 #pragma unroll
         for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(gmask, H[q], o, W);
     }
-    if (lane != 0) return;
+    if (!LS && lane != 0) return;
     if (UM && end > beg) {
         // hoisted Rayleigh damping (_native.pyx:309-317 summed over the vertex's tets):
         // f -= dsc (sum He) dx,  H = (1 + dsc) sum He
@@ -124,9 +164,27 @@ __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int la
     R d[3];
     block_solve<R>(f, H, a.eps_det, a.mode, d);
     R4 nx = xi4;
-    nx.x = xi[0] + d[0];
-    nx.y = xi[1] + d[1];
-    nx.z = xi[2] + d[2];
+    if (LS && a.mode == 0) {
+        // 17-trial backtracking on G_i (_native.pyx:481-492); every lane of the group runs
+        // the same trials on the same reduced energies
+        const R e0 = local_energy<R, W>(a, beg, end, lane, gmask, xi, y4);
+        R alpha = R(1);
+        for (int trial = 0; trial < 17; ++trial) {
+            const R cand[3] = {xi[0] + alpha * d[0], xi[1] + alpha * d[1], xi[2] + alpha * d[2]};
+            if (local_energy<R, W>(a, beg, end, lane, gmask, cand, y4) <= e0) {
+                nx.x = cand[0];
+                nx.y = cand[1];
+                nx.z = cand[2];
+                break;
+            }
+            alpha *= R(0.5);
+        }
+        if (lane != 0) return;
+    } else {
+        nx.x = xi[0] + d[0];
+        nx.y = xi[1] + d[1];
+        nx.z = xi[2] + d[2];
+    }
     if (a.out)
         a.out[g] = nx;
     else
@@ -140,6 +198,14 @@ __device__ __forceinline__ void k1_vertex(const K1Args<R>& a, int g, int lane)
 {
     if (a.vmat) k1_vertex_impl<R, W, U, true>(a, g, lane);
     else k1_vertex_impl<R, W, U, false>(a, g, lane);
+}
+
+// K1 with the local line search (protocol path, line_search=True)
+template <typename R>
+__global__ void __launch_bounds__(256) k1_color_pass_ls(const K1Args<R> a)
+{
+    const int g = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) / 4);
+    if (g < a.count) k1_vertex_impl<R, 4, 1, false, true>(a, g, threadIdx.x & 3);
 }
 
 // One group of W lanes per vertex; lane j handles entries j, j+W, ... of its vertex and the

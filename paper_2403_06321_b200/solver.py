@@ -215,15 +215,13 @@ def chebyshev_omega(rho: float, n: int) -> float:
 def _check_supported(state, params):
     if params.contact is not None:
         raise NotImplementedError("contact handling is not on the B200 hot path")
-    if params.line_search:
-        raise NotImplementedError("local line search is not on the B200 hot path yet")
     if np.any(state.system.cons.kind == SUBSPACE):
         raise NotImplementedError("SubspaceConstraint is not on the B200 hot path")
 
 
 def _dparams(params):
     return DeviceContext.step_params(params.h, params.n_max, params.rho, params.eps_det,
-                                     params.init_mode, params.a_ext)
+                                     params.init_mode, params.a_ext, params.line_search)
 
 
 def initialize(state, params) -> np.ndarray:

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
 def test_struct_layouts_match_header():
     import ctypes
     from paper_2403_06321_b200 import _lib
-    assert ctypes.sizeof(_lib.StepParams) == 8 + 4 + 4 + 8 + 8 + 24
+    assert ctypes.sizeof(_lib.StepParams) == 8 + 4 + 4 + 8 + 8 + 24 + 8
     assert ctypes.sizeof(_lib.StepResult) == 24
     assert ctypes.sizeof(_lib.BeamDesc) == 3 * 8 + 2 * 8 + 24 + 24 + 8
     assert ctypes.sizeof(_lib.SystemDesc) == 17 * 8

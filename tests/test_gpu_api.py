@@ -179,6 +179,4 @@ def test_local_solve_and_color_pass(V):
 def test_unsupported_raise(V):
     system, state = beam_state(V)
     with pytest.raises(NotImplementedError):
-        V.step(state, V.SolverParams(h=0.01, line_search=True))
-    with pytest.raises(NotImplementedError):
         V.step(state, V.SolverParams(h=0.01, contact=V.ContactParams(k_c=1e5)))

@@ -137,8 +137,6 @@ def test_color_pass_edge_cases(V, O):
     assert np.array_equal(x, before)  # det guard freezes every vertex (test_solver.py:236-245)
     with pytest.raises(TypeError):
         ctx.color_pass(x.astype(np.float32), s.rest_positions, s.rest_positions, H, [0])
-    with pytest.raises(NotImplementedError):
-        ctx.color_pass(x, s.rest_positions, s.rest_positions, H, [0], line_search=True)
 
 
 # --------------------------------------------------------------------------------------
@@ -306,3 +304,28 @@ def test_twisting_beam_kinematic_bc(V, O, precision, tol):
     assert np.abs(x - st.x).max() / m.bbox_diagonal() <= tol
     # the clamped ends really turned
     assert np.abs(x[idx] - s.rest_positions[idx]).max() > 1e-3
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-12), ("fp32", 2e-6)])
+def test_line_search_pass_matches_reference_golden(V, O, golden, precision, tol):
+    """Jacobi pass with the 17-trial local line search (_native.pyx:481-492)."""
+    g = golden("pass_beam_9_4_4.npz")
+    m, s = beam_sys(O)
+    ctx = ctx_for(V, O, s, precision)
+    x = g["x0"].copy()
+    ctx.color_pass(x, g["x_t"], g["y"], float(g["h"]), np.arange(s.num_vertices), line_search=True)
+    assert np.abs(x - g["jacobi_linesearch"]).max() <= tol
+
+
+def test_line_search_steps_vs_oracle(V, O):
+    m, s = beam_sys(O, 13, 6, 6, 0.05)
+    ctx = ctx_for(V, O, s, "fp64")
+    st = O.make_state(s)
+    z = np.zeros((s.num_vertices, 3))
+    ctx.set_state(x=s.rest_positions, x_t=s.rest_positions, v_t=z, v_prev=z)
+    p = ctx.step_params(1 / 30, 20, 0.0, 1e-10, "adaptive", G, line_search=True)
+    for _ in range(3):
+        ctx.step(p)
+        O.step(s, st, 1 / 30, 20, 0.0, G, line_search=True)
+    x = ctx.get_state(x=True)["x"]
+    assert np.abs(x - st.x).max() / m.bbox_diagonal() <= 1e-10
