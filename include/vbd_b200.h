@@ -154,6 +154,20 @@ int vbd_halo_count(vbd_ctx* ctx, int32_t side, int32_t color, int64_t* n_send, i
 int vbd_halo_pack(vbd_ctx* ctx, int32_t side, int32_t color, void* dev_buf);
 int vbd_halo_unpack(vbd_ctx* ctx, int32_t side, int32_t color, const void* dev_buf);
 
+/* fused P2P halo (B200 path): K1 stores each boundary vertex of the colour it just solved
+ * straight into the neighbour's ghost slot (NVLink peer memory), and a device-side phase
+ * barrier (flags in peer memory, st.release.sys / ld.acquire.sys) orders the phases of
+ * neighbouring slabs; the whole step is one CUDA graph per rank with no host in the loop. */
+int vbd_halo_ghost_blocks(vbd_ctx* ctx, int32_t side, int64_t* begin, int64_t* count, int64_t* boundary);
+int vbd_halo_p2p_local(vbd_ctx* ctx, void** pos, void** flags); /* same-process peers */
+int vbd_halo_p2p_export(vbd_ctx* ctx, void* pos_handle64, void* flags_handle64); /* cudaIpc */
+int vbd_ipc_open(int device, const void* handle64, void** ptr);
+int vbd_ipc_close(void* ptr);
+int vbd_halo_p2p_connect(vbd_ctx* ctx, int32_t side, void* peer_pos, void* peer_flags,
+                         const int64_t* peer_ghost_begin, const int64_t* peer_ghost_count);
+int vbd_step_p2p_launch(vbd_ctx* ctx, const vbd_step_params* params); /* asynchronous */
+int vbd_step_p2p_finish(vbd_ctx* ctx, vbd_step_result* res);
+
 /* ---- colouring (K5, device Jones-Plassmann == reference greedy) ------------------------- */
 int vbd_greedy_color(int64_t n, const int64_t* noff, const int64_t* nids, const int64_t* order,
                      int device, int64_t* color_of, int64_t* num_colors);

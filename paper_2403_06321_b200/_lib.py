@@ -90,6 +90,14 @@ SIGNATURES = {
     "vbd_halo_count": (ctypes.c_int, [P, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "vbd_halo_pack": (ctypes.c_int, [P, i32, i32, P]),
     "vbd_halo_unpack": (ctypes.c_int, [P, i32, i32, P]),
+    "vbd_halo_ghost_blocks": (ctypes.c_int, [P, i32, P, P, P]),
+    "vbd_halo_p2p_local": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P)]),
+    "vbd_halo_p2p_export": (ctypes.c_int, [P, P, P]),
+    "vbd_ipc_open": (ctypes.c_int, [ctypes.c_int, P, ctypes.POINTER(P)]),
+    "vbd_ipc_close": (ctypes.c_int, [P]),
+    "vbd_halo_p2p_connect": (ctypes.c_int, [P, i32, P, P, P, P]),
+    "vbd_step_p2p_launch": (ctypes.c_int, [P, ctypes.POINTER(StepParams)]),
+    "vbd_step_p2p_finish": (ctypes.c_int, [P, ctypes.POINTER(StepResult)]),
     "vbd_greedy_color": (ctypes.c_int, [i64, P, P, P, ctypes.c_int, P, ctypes.POINTER(i64)]),
     "vbd_profile_color_pass": (ctypes.c_int, [P, f64, i32, P]),
     "vbd_last_error": (ctypes.c_char_p, []),

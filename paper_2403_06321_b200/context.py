@@ -234,6 +234,48 @@ class DeviceContext:
     def halo_unpack(self, side, color, dev_ptr):
         _lib.check(_lib.lib().vbd_halo_unpack(self._h, side, color, ctypes.c_void_p(dev_ptr)))
 
+    # -- fused P2P halo (multi-GPU slabs over peer memory) -------------------------------
+    def ghost_blocks(self, side):
+        nc = max(self.num_colors, 1)
+        b, n, bd = (np.zeros(nc, np.int64) for _ in range(3))
+        _lib.check(_lib.lib().vbd_halo_ghost_blocks(self._h, side, _lib.ptr(b), _lib.ptr(n),
+                                                    _lib.ptr(bd)))
+        return b[: self.num_colors], n[: self.num_colors], bd[: self.num_colors]
+
+    def p2p_local_ptrs(self):
+        pos, fl = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(_lib.lib().vbd_halo_p2p_local(self._h, ctypes.byref(pos), ctypes.byref(fl)))
+        return pos.value, fl.value
+
+    def p2p_export(self):
+        a, b = ctypes.create_string_buffer(64), ctypes.create_string_buffer(64)
+        _lib.check(_lib.lib().vbd_halo_p2p_export(self._h, a, b))
+        return a.raw, b.raw
+
+    @staticmethod
+    def ipc_open(device, handle):
+        p = ctypes.c_void_p()
+        _lib.check(_lib.lib().vbd_ipc_open(int(device), ctypes.c_char_p(handle), ctypes.byref(p)))
+        return p.value
+
+    def p2p_connect(self, side, peer_pos, peer_flags, peer_begin, peer_count):
+        b = _lib.i64c(peer_begin)
+        n = _lib.i64c(peer_count)
+        _lib.check(_lib.lib().vbd_halo_p2p_connect(self._h, side, ctypes.c_void_p(peer_pos),
+                                                   ctypes.c_void_p(peer_flags), _lib.ptr(b),
+                                                   _lib.ptr(n)))
+
+    def step_p2p_launch(self, params):
+        _lib.check(_lib.lib().vbd_step_p2p_launch(self._h, ctypes.byref(params)))
+
+    def step_p2p_finish(self, step_index=0):
+        r = _lib.StepResult()
+        _lib.check(_lib.lib().vbd_step_p2p_finish(self._h, ctypes.byref(r)))
+        if r.nonfinite:
+            raise NonFiniteState("non-finite vertex position", step=step_index,
+                                 iteration=r.iteration, vertex=int(r.vertex))
+        return r
+
     # -- measurement --------------------------------------------------------------------
     def profile_color_pass(self, h, reps=5):
         ms = np.zeros(max(self.num_colors, 1))

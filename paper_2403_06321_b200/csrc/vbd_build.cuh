@@ -300,20 +300,44 @@ __global__ void k_iota(int* __restrict__ a, long long n)
     if (i < n) a[i] = (int)i;
 }
 
-// sort key: category (0 solved, 1 ghost, 2 fixed) | colour | rounds | spatial rank i
-// (the vertex at spatial rank i is order0[i])
+// Sort key of the colour-major order:
+//   category (2 b: 0 solved, 1 ghost, 2 fixed) | colour (12 b) | class (4 b) | rounds (8 b) | low 32
+// solved: class 0 / 1 = slab boundary vertex facing the left / right neighbour, 2 = interior;
+// ghost: class 0 / 1 = ghost plane on the left / right.  Boundary and ghost blocks are ordered
+// by vertex id (so a rank's boundary block matches the neighbour's ghost block element for
+// element); interior vertices by (rounds = ceil(d/W), spatial rank i -> order0[i]).
+// halo: 0 none, 1 boundary-left, 2 boundary-right, 3 ghost-left, 4 ghost-right (may be null)
 __global__ void k_order_keys(const long long* __restrict__ off, const unsigned char* __restrict__ kind,
-                             const int* __restrict__ color, const int* __restrict__ order0, long long n,
-                             int W, unsigned long long* __restrict__ keys)
+                             const unsigned char* __restrict__ halo, const int* __restrict__ color,
+                             const int* __restrict__ order0, long long n, int W,
+                             unsigned long long* __restrict__ keys)
 {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int v = order0[i];
+    const unsigned hv = halo ? halo[v] : 0u;
     unsigned long long cat = kind[v] == 1 ? 2ull : (kind[v] == 3 ? 1ull : 0ull);
     unsigned long long c = (unsigned long long)(color[v] < 0 ? 0 : color[v]) & 0xfffull;
-    long long d = off[v + 1] - off[v];
-    unsigned long long r = cat == 0 ? (unsigned long long)((d + W - 1) / W) & 0xfffull : 0ull;
-    keys[i] = (cat << 56) | (c << 44) | (r << 32) | (unsigned long long)i;
+    unsigned long long cls, r = 0ull, low;
+    if (cat == 0) {
+        cls = hv == 1 ? 0ull : (hv == 2 ? 1ull : 2ull);
+        if (cls == 2) {
+            long long d = off[v + 1] - off[v];
+            r = (unsigned long long)((d + W - 1) / W) & 0xffull;
+            low = (unsigned long long)i;
+        } else {
+            low = (unsigned long long)v;
+        }
+    } else {
+        cls = (cat == 1 && hv == 4) ? 1ull : 0ull;
+        low = (unsigned long long)v;
+    }
+    keys[i] = (cat << 56) | (c << 44) | (cls << 40) | (r << 32) | low;
+}
+
+__device__ __forceinline__ bool key_is_rank(unsigned long long k)
+{
+    return (k >> 56) == 0ull && ((k >> 40) & 0xfull) == 2ull;
 }
 
 __global__ void k_perm_from_keys(const unsigned long long* __restrict__ keys,
@@ -322,7 +346,9 @@ __global__ void k_perm_from_keys(const unsigned long long* __restrict__ keys,
 {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    int o = order0[(long long)(keys[i] & 0xffffffffull)];
+    const unsigned long long k = keys[i];
+    const long long low = (long long)(k & 0xffffffffull);
+    int o = key_is_rank(k) ? order0[low] : (int)low;
     perm[i] = o;
     inv[o] = (int)i;
 }

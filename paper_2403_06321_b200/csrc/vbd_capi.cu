@@ -128,6 +128,9 @@ struct vbd_ctx {
     long long n = 0, nsolve = 0, nfree_all = 0, T = 0, E = 0;
     int ncolors = 0;
     std::vector<long long> cbeg, ccnt;
+    // slab halo blocks: bnd_cnt[side][c] solved boundary vertices at the head of colour c's
+    // range (side 0 first), ghost_beg/ghost_cnt[side][c] the ghost block of colour c
+    std::vector<long long> bnd_cnt[2], ghost_beg[2], ghost_cnt[2];
     bool inplace = true;
     std::vector<MaterialKey> mats;
     double mat_h = NAN;
@@ -137,6 +140,13 @@ struct vbd_ctx {
     DBuf beams_dev;
     std::vector<int> hinv;  // host copy of inv (protocol colour pass)
     K1Variant k1 = k1_variant_from_env();
+    // P2P slab halo: flags[0..1] written by the neighbours, [2] epoch, [3] error word
+    DBuf p2p_flags;
+    void* peer_pos[2] = {nullptr, nullptr};
+    unsigned long long* peer_flag_slot[2] = {nullptr, nullptr};
+    std::vector<long long> peer_ghost_beg[2];
+    cudaGraphExec_t p2p_gexec = nullptr;
+    GraphKey p2p_key{};
     DBuf omega_dev;
     DBuf vmat;
     bool uniform_mat = false;
@@ -153,6 +163,7 @@ struct vbd_ctx {
     ~vbd_ctx()
     {
         if (gexec) cudaGraphExecDestroy(gexec);
+        if (p2p_gexec) cudaGraphExecDestroy(p2p_gexec);
         for (int s = 0; s < 2; ++s) {
             for (auto& v : halo_send[s])
                 for (auto* b : v) delete b;
@@ -261,6 +272,7 @@ struct Scene {
     DBuf inc;       // u32 (4T) = 4 t + s, ascending per vertex
     DBuf mass;      // f64 (n)
     DBuf kind;      // u8 (n): 0 free, 1 fixed, 3 ghost
+    DBuf halo;      // u8 (n) slab role (k_order_keys), or empty
     DBuf color;     // int32 (n)
     DBuf pos;       // f64 (n,3) rest positions (drives the spatial order) or empty
     double bbox_lo[3] = {0.0, 0.0, 0.0};
@@ -414,6 +426,7 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
     DBuf keys;
     keys.alloc(sc.n * 8);
     k_order_keys<<<blocks_for(sc.n), 256, 0, s>>>(sc.inc_off.as<long long>(), sc.kind.as<unsigned char>(),
+                                                  sc.halo.p ? sc.halo.as<unsigned char>() : nullptr,
                                                   sc.color.as<int>(), order0.as<int>(), sc.n, c->k1.W,
                                                   keys.as<unsigned long long>());
     CK(cudaGetLastError());
@@ -445,6 +458,20 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
         int col = (int)((hk[i] >> 44) & 0xfff);
         c->cbeg[col] = i;
         c->ccnt[col]++;
+    }
+    // slab boundary blocks (head of each colour range) and ghost blocks per (side, colour)
+    for (int sd = 0; sd < 2; ++sd) {
+        c->bnd_cnt[sd].assign(c->ncolors, 0);
+        c->ghost_beg[sd].assign(c->ncolors, 0);
+        c->ghost_cnt[sd].assign(c->ncolors, 0);
+    }
+    for (long long i = 0; i < c->nfree_all; ++i) {
+        const unsigned cat = (unsigned)(hk[i] >> 56), cls = (unsigned)((hk[i] >> 40) & 0xf);
+        const int col = (int)((hk[i] >> 44) & 0xfff);
+        if (cat == 0 && cls < 2) c->bnd_cnt[cls][col]++;
+        if (cat == 1) {
+            if (c->ghost_cnt[cls][col]++ == 0) c->ghost_beg[cls][col] = i;
+        }
     }
     // colour ranges must be contiguous and ordered (guaranteed by the key layout)
     // entry offsets over solved vertices
@@ -542,6 +569,9 @@ K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
     a.pf_dist = 0;
     a.vmat = c->uniform_mat ? c->vmat.as<int>() : nullptr;
     a.line_search = 0;
+    a.peer_pos[0] = a.peer_pos[1] = nullptr;
+    a.peer_off[0] = a.peer_off[1] = 0;
+    a.nb[0] = a.nb[1] = 0;
     return a;
 }
 
@@ -712,6 +742,56 @@ template <typename R> void enqueue_step(vbd_ctx* c)
         enqueue_iter_end<R>(c, n);
     }
     enqueue_end<R>(c);
+}
+
+// ---- P2P slab halo: one graph per step with neighbour phase barriers ------------------
+
+template <typename R> void enqueue_step_p2p(vbd_ctx* c)
+{
+    typedef typename Vec4<R>::T R4;
+    cudaStream_t s = c->stream;
+    unsigned long long* fl = c->p2p_flags.as<unsigned long long>();
+    const unsigned long long* epoch = fl + 2;
+    int* err = reinterpret_cast<int*>(fl + 3);
+    const int nl = c->peer_pos[0] != nullptr, nr = c->peer_pos[1] != nullptr;
+    const bool cheb = c->cur.rho != 0.0;
+    const unsigned long long pps = 2ull + (unsigned long long)c->cur.n_max * (c->ncolors + (cheb ? 1 : 0));
+    int phase = 0;
+    auto wait = [&]() { k_phase_wait<<<1, 32, 0, s>>>(fl, nl, nr, epoch, pps, phase, err); };
+    auto signal = [&]() { k_phase_signal<<<1, 32, 0, s>>>(c->peer_flag_slot[0], c->peer_flag_slot[1], epoch, pps, phase); };
+    ++phase;
+    wait();
+    enqueue_begin<R>(c);
+    signal();
+    const bool check_in_k1 = !cheb;
+    for (int n = 1; n <= c->cur.n_max; ++n) {
+        for (int col = 0; col < c->ncolors; ++col) {
+            ++phase;
+            wait();
+            K1Args<R> a = k1_args<R>(c, c->cur.eps_det, 0, check_in_k1, n);
+            a.line_search = c->cur.line_search ? 1 : 0;
+            a.vbeg = (int)c->cbeg[col];
+            a.count = (int)c->ccnt[col];
+            for (int sd = 0; sd < 2; ++sd) {
+                a.peer_pos[sd] = static_cast<R4*>(c->peer_pos[sd]);
+                a.nb[sd] = (int)c->bnd_cnt[sd][col];
+                a.peer_off[sd] = c->peer_pos[sd] ? (int)c->peer_ghost_beg[sd][col] : 0;
+            }
+            launch_k1<R>(c, a, s);
+            signal();
+        }
+        if (cheb) {
+            ++phase;
+            wait();
+            enqueue_iter_end<R>(c, n);
+            signal();
+        }
+    }
+    ++phase;
+    wait();
+    enqueue_end<R>(c);
+    signal();
+    k_epoch_advance<<<1, 32, 0, s>>>(fl + 2, pps);
 }
 
 // one cooperative launch per step (small scenes); see k_step_persistent
@@ -1168,11 +1248,18 @@ int vbd_ctx_create_beams(const vbd_beam_desc* beams, int64_t nb, int64_t slab_lo
             std::vector<unsigned char> kind(n);
             CK(cudaMemcpyAsync(kind.data(), sc.kind.p, n, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
+            std::vector<unsigned char> halo(n, 0);
             for (long long v = 0; v < n; ++v) {
                 long long ax = B.ax0 + v / plane;
                 if ((ax < slab_lo || ax >= slab_hi) && kind[v] != 1) kind[v] = 3;
+                if (ax == slab_lo - 1) halo[v] = 3;
+                else if (ax == slab_hi) halo[v] = 4;
+                else if (ax == slab_lo && slab_lo > 0) halo[v] = 1;
+                else if (ax == slab_hi - 1 && slab_hi < B.nx) halo[v] = 2;
             }
+            if (slab_hi - slab_lo < 2) fail(VBD_ERR_ARG, "slabs must own at least 2 vertex planes");
             CK(cudaMemcpyAsync(sc.kind.p, kind.data(), n, cudaMemcpyHostToDevice, s));
+            upload(sc.halo, halo.data(), n, s);
             CK(cudaStreamSynchronize(s));
         } else {
             color_scene(sc, s);
@@ -1547,6 +1634,133 @@ int vbd_halo_unpack(vbd_ctx* c, int32_t side, int32_t color, const void* buf)
             k_halo_unpack<float><<<blocks_for(n), 256, 0, c->stream>>>(c->pos.as<float4>(), ids, (int)n,
                                                                        (const float4*)buf);
         CK(cudaGetLastError());
+    });
+}
+
+int vbd_halo_ghost_blocks(vbd_ctx* c, int32_t side, int64_t* begin, int64_t* count, int64_t* boundary)
+{
+    return guarded([&] {
+        if (!c || side < 0 || side > 1) fail(VBD_ERR_ARG, "bad argument");
+        for (int k = 0; k < c->ncolors; ++k) {
+            if (begin) begin[k] = c->ghost_beg[side].empty() ? 0 : c->ghost_beg[side][k];
+            if (count) count[k] = c->ghost_cnt[side].empty() ? 0 : c->ghost_cnt[side][k];
+            if (boundary) boundary[k] = c->bnd_cnt[side].empty() ? 0 : c->bnd_cnt[side][k];
+        }
+    });
+}
+
+static void ensure_p2p_flags(vbd_ctx* c)
+{
+    if (c->p2p_flags.p) return;
+    c->p2p_flags.alloc(64);
+    CK(cudaMemset(c->p2p_flags.p, 0, 64));
+}
+
+int vbd_halo_p2p_local(vbd_ctx* c, void** pos, void** flags)
+{
+    return guarded([&] {
+        if (!c || !pos || !flags) fail(VBD_ERR_ARG, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        ensure_p2p_flags(c);
+        *pos = c->pos.p;
+        *flags = c->p2p_flags.p;
+    });
+}
+
+int vbd_halo_p2p_export(vbd_ctx* c, void* pos_handle, void* flags_handle)
+{
+    return guarded([&] {
+        if (!c || !pos_handle || !flags_handle) fail(VBD_ERR_ARG, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        ensure_p2p_flags(c);
+        cudaIpcMemHandle_t h1, h2;
+        CK(cudaIpcGetMemHandle(&h1, c->pos.p));
+        CK(cudaIpcGetMemHandle(&h2, c->p2p_flags.p));
+        std::memcpy(pos_handle, &h1, sizeof h1);
+        std::memcpy(flags_handle, &h2, sizeof h2);
+    });
+}
+
+int vbd_ipc_open(int device, const void* handle, void** ptr)
+{
+    return guarded([&] {
+        if (!handle || !ptr) fail(VBD_ERR_ARG, "NULL argument");
+        CK(cudaSetDevice(device));
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        CK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int vbd_ipc_close(void* ptr)
+{
+    return guarded([&] { CK(cudaIpcCloseMemHandle(ptr)); });
+}
+
+int vbd_halo_p2p_connect(vbd_ctx* c, int32_t side, void* peer_pos, void* peer_flags,
+                         const int64_t* peer_ghost_begin, const int64_t* peer_ghost_count)
+{
+    return guarded([&] {
+        if (!c || side < 0 || side > 1 || !peer_pos || !peer_flags || !peer_ghost_begin || !peer_ghost_count)
+            fail(VBD_ERR_ARG, "NULL argument");
+        if (c->bnd_cnt[side].empty()) fail(VBD_ERR_ARG, "context is not a slab");
+        CK(cudaSetDevice(c->device));
+        ensure_p2p_flags(c);
+        for (int k = 0; k < c->ncolors; ++k)
+            if (peer_ghost_count[k] != c->bnd_cnt[side][k])
+                fail(VBD_ERR_ARG, "neighbour ghost block does not match this slab's boundary block");
+        c->peer_pos[side] = peer_pos;
+        // my signal lands in the neighbour's slot that faces me
+        c->peer_flag_slot[side] = static_cast<unsigned long long*>(peer_flags) + (side == 0 ? 1 : 0);
+        c->peer_ghost_beg[side].assign(peer_ghost_begin, peer_ghost_begin + c->ncolors);
+        if (c->p2p_gexec) {
+            cudaGraphExecDestroy(c->p2p_gexec);
+            c->p2p_gexec = nullptr;
+        }
+    });
+}
+
+int vbd_step_p2p_launch(vbd_ctx* c, const vbd_step_params* p)
+{
+    return guarded([&] {
+        if (!c) fail(VBD_ERR_ARG, "NULL ctx");
+        validate_params(p);
+        CK(cudaSetDevice(c->device));
+        ensure_p2p_flags(c);
+        c->cur = *p;
+        c->omegas = omega_table(p->rho, p->n_max);
+        cudaStream_t s = c->stream;
+        if (c->precision == VBD_PREC_F64) ensure_materials<double>(c, p->h);
+        else ensure_materials<float>(c, p->h);
+        CK(cudaMemsetAsync(c->flag.p, 0xff, 8, s));
+        CK(cudaMemsetAsync(c->stepctr.p, 0, 4, s));
+        GraphKey key{*p};
+        if (!c->p2p_gexec || !(key == c->p2p_key)) {
+            if (c->p2p_gexec) {
+                cudaGraphExecDestroy(c->p2p_gexec);
+                c->p2p_gexec = nullptr;
+            }
+            cudaGraph_t g;
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            if (c->precision == VBD_PREC_F64) enqueue_step_p2p<double>(c);
+            else enqueue_step_p2p<float>(c);
+            CK(cudaStreamEndCapture(s, &g));
+            CK(cudaGraphInstantiate(&c->p2p_gexec, g, 0));
+            cudaGraphDestroy(g);
+            c->p2p_key = key;
+        }
+        CK(cudaGraphLaunch(c->p2p_gexec, s));
+    });
+}
+
+int vbd_step_p2p_finish(vbd_ctx* c, vbd_step_result* res)
+{
+    return guarded([&] {
+        if (!c) fail(VBD_ERR_ARG, "NULL ctx");
+        CK(cudaSetDevice(c->device));
+        read_result(c, res);
+        int err = read_scalar<int>(c->p2p_flags.as<unsigned long long>() + 3, c->stream);
+        if (err) fail(VBD_ERR_INTERNAL, "P2P halo barrier timed out (neighbour not progressing)");
     });
 }
 

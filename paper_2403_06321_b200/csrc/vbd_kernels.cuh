@@ -35,6 +35,12 @@ template <typename R> struct K1Args {
     int pf_dist;             // L2 prefetch distance in CTAs (one residency wave)
     const int* vmat;         // per-vertex material when every vertex has one material, else null
     int line_search;         // 17-trial local backtracking (mode 0 only)
+    // fused slab halo push (multi-GPU, peer memory): the first nb[0] vertices of the colour
+    // range face the left neighbour, the next nb[1] the right one; their new positions are
+    // also stored into the neighbour's ghost block (peer_pos[s] + peer_off[s])
+    R4* peer_pos[2];
+    int peer_off[2];
+    int nb[2];
 };
 
 // The per-vertex body of K1: group g (W lanes, this thread is lane `lane`) solves vertex
@@ -185,10 +191,21 @@ __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int la
         nx.y = xi[1] + d[1];
         nx.z = xi[2] + d[2];
     }
-    if (a.out)
+    if (a.out) {
         a.out[g] = nx;
-    else
+    } else {
         a.pos[v] = nx;
+        if (a.peer_pos[0] || a.peer_pos[1]) {
+            const int j = v - a.vbeg;
+            if (j < a.nb[0]) {
+                a.peer_pos[0][a.peer_off[0] + j] = nx;  // NVLink store into the left ghost
+                __threadfence_system();
+            } else if (j < a.nb[0] + a.nb[1]) {
+                a.peer_pos[1][a.peer_off[1] + (j - a.nb[0])] = nx;
+                __threadfence_system();
+            }
+        }
+    }
     if (a.flag && !finite3(nx.x, nx.y, nx.z))
         atomicMin(a.flag, StepFlag::key((unsigned)*a.stepctr, (unsigned)a.iter, (unsigned)a.perm[v]));
 }
@@ -693,6 +710,49 @@ __global__ void k_fill_mih2(typename Vec4<R>::T* y, const R* mass, int n, double
 }
 
 // halo exchange for slab-decomposed scenes: gather/scatter the positions of a vertex list
+// Neighbour phase barrier over peer memory (slab P2P halo).  flags[0] of a context is
+// written by its left neighbour, flags[1] by its right one; values are monotonically
+// increasing phase stamps base + phase, base = phases of all previous steps (identical on
+// every rank because every rank runs the same phase sequence).
+__global__ void k_phase_signal(unsigned long long* left_slot, unsigned long long* right_slot,
+                               const unsigned long long* epoch, unsigned long long pps, int phase)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const unsigned long long v = *epoch + (unsigned long long)phase;
+    __threadfence_system();
+    if (left_slot) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(left_slot), "l"(v) : "memory");
+    if (right_slot) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(right_slot), "l"(v) : "memory");
+}
+
+__global__ void k_phase_wait(const unsigned long long* flags, int need_left, int need_right,
+                             const unsigned long long* epoch, unsigned long long pps, int phase,
+                             int* err)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    // neighbours must have completed the previous phase (phase - 1)
+    const unsigned long long target = *epoch + (unsigned long long)(phase - 1);
+    for (int side = 0; side < 2; ++side) {
+        if (!(side == 0 ? need_left : need_right)) continue;
+        unsigned long long v = 0;
+        long long spins = 0;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + side) : "memory");
+            if (v >= target) break;
+            if (++spins > (1ll << 26)) {  // ~seconds: report instead of hanging the GPU
+                atomicExch(err, 1);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __threadfence_system();
+}
+
+__global__ void k_epoch_advance(unsigned long long* epoch, unsigned long long pps)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0) *epoch += pps;
+}
+
 template <typename R>
 __global__ void k_halo_pack(const typename Vec4<R>::T* __restrict__ pos, const int* __restrict__ ids,
                             int n, typename Vec4<R>::T* __restrict__ buf)

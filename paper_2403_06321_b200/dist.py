@@ -164,3 +164,59 @@ class SlabExchange:
                 c.step_iter_end(n)
         res = [c.step_end(step_index) for c in self.ctxs]
         return res
+
+
+class SlabP2P:
+    """Slab halo over peer memory, the B200-native transport.
+
+    K1 stores every boundary vertex of the colour it just solved directly into the
+    neighbour's ghost slot (NVLink stores through a cudaIpc mapping), and each phase of the
+    step (K2, every colour pass, K3, K4) starts only after both neighbours finished the
+    previous phase, signalled with release/acquire flags in peer memory.  A whole step is one
+    CUDA graph per rank: no NCCL call and no host round trip per colour.
+    """
+
+    def __init__(self, ctxs):
+        self.ctxs = list(ctxs)
+
+    @classmethod
+    def local(cls, ctxs):
+        """Several slabs of one process (same device, separate streams): direct pointers."""
+        ptrs = [c.p2p_local_ptrs() for c in ctxs]
+        for i, c in enumerate(ctxs):
+            if i > 0:
+                b, n, _ = ctxs[i - 1].ghost_blocks(1)
+                c.p2p_connect(0, ptrs[i - 1][0], ptrs[i - 1][1], b, n)
+            if i + 1 < len(ctxs):
+                b, n, _ = ctxs[i + 1].ghost_blocks(0)
+                c.p2p_connect(1, ptrs[i + 1][0], ptrs[i + 1][1], b, n)
+        return cls(ctxs)
+
+    @classmethod
+    def distributed(cls, ctx, rank, world, device):
+        """One slab per process; peers mapped with cudaIpcOpenMemHandle (NVLink)."""
+        import torch.distributed as dist
+        pos_h, fl_h = ctx.p2p_export()
+        mine = {"pos": pos_h, "flags": fl_h,
+                "ghost0": [a.tolist() for a in ctx.ghost_blocks(0)[:2]],
+                "ghost1": [a.tolist() for a in ctx.ghost_blocks(1)[:2]]}
+        allv = [None] * world
+        dist.all_gather_object(allv, mine)
+        opened = []
+        for side, peer in ((0, rank - 1), (1, rank + 1)):
+            if 0 <= peer < world:
+                p = allv[peer]
+                pos = ctx.ipc_open(device, p["pos"])
+                fl = ctx.ipc_open(device, p["flags"])
+                opened += [pos, fl]
+                facing = p["ghost1"] if side == 0 else p["ghost0"]
+                ctx.p2p_connect(side, pos, fl, facing[0], facing[1])
+        dist.barrier()
+        obj = cls([ctx])
+        obj._opened = opened
+        return obj
+
+    def step(self, params, step_index=0):
+        for c in self.ctxs:
+            c.step_p2p_launch(params)
+        return [c.step_p2p_finish(step_index) for c in self.ctxs]

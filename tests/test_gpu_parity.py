@@ -329,3 +329,28 @@ def test_line_search_steps_vs_oracle(V, O):
         O.step(s, st, 1 / 30, 20, 0.0, G, line_search=True)
     x = ctx.get_state(x=True)["x"]
     assert np.abs(x - st.x).max() / m.bbox_diagonal() <= 1e-10
+
+
+def test_slab_p2p_bitwise_equals_single_context(V):
+    """The fused peer-memory halo (K1 pushes + device phase barriers), three slabs of one
+    process on separate streams, against one context."""
+    beam = V.Beam(26, 7, 6, 0.02, 1e6, 1e7, 1e-6, fix_min_x=True)
+    full = V.DeviceContext.from_beams([beam], precision="fp32")
+    cuts = [0, 8, 17, beam.nx]
+    slabs = [V.DeviceContext.from_beams([beam], precision="fp32", slab=(cuts[r], cuts[r + 1]))
+             for r in range(3)]
+    from paper_2403_06321_b200.dist import SlabP2P
+    ex = SlabP2P.local(slabs)
+    for rho in (0.9, 0.0):  # the phase count per step changes between the two
+        p = full.step_params(1 / 120, 6, rho, 1e-10, "adaptive", G)
+        for _ in range(3):
+            full.step(p)
+        for _ in range(3):
+            ex.step(p)
+        xf = full.get_state(x=True)["x"]
+        plane = beam.ny * beam.nz
+        for r, sctx in enumerate(slabs):
+            xs = sctx.get_state(x=True)["x"]
+            lo = max(cuts[r] - 1, 0)
+            own = slice((cuts[r] - lo) * plane, (cuts[r + 1] - lo) * plane)
+            assert np.array_equal(xs[own], xf[cuts[r] * plane:cuts[r + 1] * plane]), (rho, r)
