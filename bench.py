@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
+                    help="slab halo transport for N>1: fused peer-memory push or NCCL send/recv")
     return ap.parse_args()
 
 
@@ -300,7 +302,11 @@ def run_ours(args):
     p = cfg.step_params()
     exch = None
     if world > 1 and cfg.sharding == "slabs":
-        exch = SlabExchange.distributed(ctx, rank, world)
+        if args.halo == "p2p":  # fused K1 push into the neighbour's ghosts over NVLink
+            from paper_2403_06321_b200.dist import SlabP2P
+            exch = SlabP2P.distributed(ctx, rank, world, device=local)
+        else:                   # NCCL send/recv per colour
+            exch = SlabExchange.distributed(ctx, rank, world)
     stream = torch.cuda.ExternalStream(ctx.stream) if ctx.stream else torch.cuda.current_stream()
 
     twist = None
@@ -361,9 +367,12 @@ def run_ours(args):
     k1_iter_ms = float(np.sum(k1_ms))
     peak, peak_kind = load_peaks()
     achieved = bytes_iter / (k1_iter_ms / 1e3) / 1e9
-    launches_per_step = 1 + cfg.n_max * (int(info.num_colors) + (1 if cfg.rho else 0)) + 1
-    if exch is not None:
-        launches_per_step += cfg.n_max * int(info.num_colors) * 4
+    phases = 1 + cfg.n_max * (int(info.num_colors) + (1 if cfg.rho else 0)) + 1
+    launches_per_step = phases
+    if exch is not None and args.halo == "p2p":
+        launches_per_step = 3 * phases + 1   # + phase wait / signal kernels, epoch advance
+    elif exch is not None:
+        launches_per_step += cfg.n_max * int(info.num_colors) * 4  # pack/unpack per side
 
     # end-to-end through the C ABI with host buffers: H2D of the step's inputs (x_t, v_t,
     # v_prev, (N,3) float64, pinned) + step + D2H of the result (x, v_t)
@@ -420,7 +429,8 @@ def run_ours(args):
                 "num_vertices": cfg.num_vertices, "num_tets": cfg.num_tets,
                 "h": cfg.h, "n_max": cfg.n_max, "rho": cfg.rho, "substeps_S": round(1 / (cfg.h * 60)),
                 "colors": int(info.num_colors),
-                "parallelism": (f"{cfg.sharding}x{world}" if world > 1 else "single GPU"),
+                "parallelism": (f"{cfg.sharding}x{world}" + (f" ({args.halo} halo)" if cfg.sharding == "slabs" else "")
+                                if world > 1 else "single GPU"),
                 "l2": "inputs larger than L2 (entry stream %.1f GB per GPU)"
                       % (info.num_entries * (48 if args.precision == 'fp32' else 96) / 1e9)
                       if info.num_entries * 48 > 126e6 else "scene fits in L2 (no flush)",
