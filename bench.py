@@ -242,10 +242,10 @@ class Clocks:
 def algorithmic_bytes_per_iteration(info, precision):
     """Compulsory DRAM bytes of the colour passes of one iteration:
     per solved vertex 8 (CSR offset) + 3 x R4 reads (x, x_t, y) + 1 x R4 write,
-    per entry 48 B (fp32) / 96 B (fp64), plus one read of every other-colour position
+    per entry 48 B (fp32) / 96 B (fp64) explicit or 16 B compact, plus one read of every other-colour position
     (R4) per colour pass."""
     r4 = 16 if precision == "fp32" else 32
-    eb = 48 if precision == "fp32" else 96
+    eb = int(info.entry_bytes)  # 48/96 explicit, 16 compact (+ the L1-resident kind table)
     n_solved = int(info.num_solved)
     n_all = int(info.num_vertices)
     C = int(info.num_colors)
@@ -431,9 +431,11 @@ def run_ours(args):
                 "colors": int(info.num_colors),
                 "parallelism": (f"{cfg.sharding}x{world}" + (f" ({args.halo} halo)" if cfg.sharding == "slabs" else "")
                                 if world > 1 else "single GPU"),
+                "layout": ("compact: 16 B entries + %d entry kinds" % info.num_entry_kinds
+                           if info.layout == 1 else "explicit: %d B entries" % info.entry_bytes),
                 "l2": "inputs larger than L2 (entry stream %.1f GB per GPU)"
-                      % (info.num_entries * (48 if args.precision == 'fp32' else 96) / 1e9)
-                      if info.num_entries * 48 > 126e6 else "scene fits in L2 (no flush)",
+                      % (info.num_entries * info.entry_bytes / 1e9)
+                      if info.num_entries * info.entry_bytes > 126e6 else "scene fits in L2 (no flush)",
                 "build_s": round(t_build, 2),
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -113,6 +113,12 @@ typedef struct {
     int32_t inplace;           /* 1 = colouring valid -> in-place colour sweeps */
     int32_t lanes_per_vertex;
     int32_t num_materials;
+    int32_t layout;            /* 0 explicit entries (48 B fp32 / 96 B fp64), 1 compact (16 B +
+                                  a table of distinct entry kinds; lossless) */
+    int32_t entry_bytes;       /* bytes streamed per (vertex, tet) entry */
+    int64_t num_entry_kinds;   /* compact layout: distinct (rows, volume, material) keys */
+    int32_t tiles;             /* K1T tile pipeline: number of 64-vertex tiles (0 = off) */
+    int32_t tile_nbr_cap;      /* max distinct neighbours of one tile */
 } vbd_ctx_info;
 
 /* ---- context ---------------------------------------------------------------------------- */

@@ -473,3 +473,175 @@ __global__ void k_mass_new(const double* __restrict__ mass_orig, const int* __re
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < n) mass[i] = (R)mass_orig[perm[i]];
 }
+
+// ---------------------------------------------------------------------------------------
+// compact layout (entry kinds): lossless dictionary of the explicit entries' rest data.
+// The key of an entry is the exact bit pattern of everything but its neighbour ids:
+//   fp32: the nine fp32 slot-weight rows + material id (10 words)
+//   fp64: the nine fp64 rows + V (20 words) + material id
+// Structured grids and instanced objects have few distinct keys (a 5-tet grid: 10 rest
+// shapes x 4 slots), so the 48/96-byte entry becomes one int4 {n0, n1, n2, kind}.
+
+template <typename R> struct KindKey;
+template <> struct KindKey<float> {
+    static constexpr int KW = 10;
+    static __device__ __forceinline__ void get(const float4* __restrict__ pl, long long E, long long k,
+                                               unsigned* key, int* n)
+    {
+        const float4 a = pl[k], b = pl[E + k], c = pl[2 * E + k];
+        const unsigned u0 = __float_as_uint(a.x), u1 = __float_as_uint(a.y), u2 = __float_as_uint(a.z);
+        n[0] = (int)(u0 & VBD_ID_MASK);
+        n[1] = (int)(u1 & VBD_ID_MASK);
+        n[2] = (int)(u2 & VBD_ID_MASK);
+        key[0] = __float_as_uint(a.w);
+        key[1] = __float_as_uint(b.x); key[2] = __float_as_uint(b.y);
+        key[3] = __float_as_uint(b.z); key[4] = __float_as_uint(b.w);
+        key[5] = __float_as_uint(c.x); key[6] = __float_as_uint(c.y);
+        key[7] = __float_as_uint(c.z); key[8] = __float_as_uint(c.w);
+        key[9] = (u0 >> VBD_ID_BITS) | ((u1 >> VBD_ID_BITS) << 3) | ((u2 >> VBD_ID_BITS) << 6);
+    }
+};
+template <> struct KindKey<double> {
+    static constexpr int KW = 21;
+    static __device__ __forceinline__ void get(const double2* __restrict__ pl, long long E, long long k,
+                                               unsigned* key, int* n)
+    {
+        const int4 a = reinterpret_cast<const int4*>(pl)[k];
+        n[0] = a.x; n[1] = a.y; n[2] = a.z;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const uint4 v = reinterpret_cast<const uint4*>(pl)[(q + 1) * E + k];
+            key[4 * q] = v.x; key[4 * q + 1] = v.y; key[4 * q + 2] = v.z; key[4 * q + 3] = v.w;
+        }
+        key[20] = (unsigned)a.w;
+    }
+};
+
+template <int KW> __device__ __forceinline__ unsigned kind_hash(const unsigned* key)
+{
+    unsigned h = 0x9e3779b9u;
+#pragma unroll
+    for (int i = 0; i < KW; ++i) {
+        unsigned x = key[i] * 0xcc9e2d51u;
+        x = (x << 15) | (x >> 17);
+        h ^= x * 0x1b873593u;
+        h = ((h << 13) | (h >> 19)) * 5u + 0xe6546b64u;
+    }
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    return h;
+}
+
+// slots: 0 = empty, else (representative entry index + 1)
+template <typename R>
+__device__ __forceinline__ long long kind_find(const typename PlaneT<R>::T* __restrict__ pl, long long E,
+                                               unsigned long long* slots, unsigned mask, const unsigned* key,
+                                               long long k, bool insert, int* count, int cap, int* overflow)
+{
+    constexpr int KW = KindKey<R>::KW;
+    const unsigned h = kind_hash<KW>(key);
+    for (unsigned probe = 0; probe <= mask; ++probe) {
+        const unsigned s = (h + probe) & mask;
+        unsigned long long cur = *(volatile unsigned long long*)(slots + s);
+        if (cur == 0) {
+            if (!insert) return -1;
+            cur = atomicCAS(slots + s, 0ull, (unsigned long long)(k + 1));
+            if (cur == 0) {
+                if (atomicAdd(count, 1) >= cap) atomicExch(overflow, 1);
+                return s;
+            }
+        }
+        unsigned rk[KW];
+        int rn[3];
+        KindKey<R>::get(pl, E, (long long)cur - 1, rk, rn);
+        bool eq = true;
+#pragma unroll
+        for (int i = 0; i < KW; ++i) eq = eq && rk[i] == key[i];
+        if (eq) return s;
+        if (insert && *(volatile int*)overflow) return -1;
+    }
+    if (insert) atomicExch(overflow, 1);
+    return -1;
+}
+
+template <typename R>
+__global__ void k_kind_insert(const typename PlaneT<R>::T* __restrict__ pl, long long E,
+                              unsigned long long* slots, unsigned mask, int* count, int cap, int* overflow)
+{
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < E;
+         k += (long long)gridDim.x * blockDim.x) {
+        if (*(volatile int*)overflow) return;
+        unsigned key[KindKey<R>::KW];
+        int n[3];
+        KindKey<R>::get(pl, E, k, key, n);
+        kind_find<R>(pl, E, slots, mask, key, k, true, count, cap, overflow);
+    }
+}
+
+template <typename R>
+__global__ void k_kind_emit(const typename PlaneT<R>::T* __restrict__ pl, long long E,
+                            unsigned long long* slots, unsigned mask, const int* __restrict__ slot_kind,
+                            int4* __restrict__ out, int* missing)
+{
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < E;
+         k += (long long)gridDim.x * blockDim.x) {
+        unsigned key[KindKey<R>::KW];
+        int n[3];
+        KindKey<R>::get(pl, E, k, key, n);
+        const long long s = kind_find<R>(pl, E, slots, mask, key, k, false, nullptr, 0, nullptr);
+        if (s < 0) {
+            atomicExch(missing, 1);
+            continue;
+        }
+        out[k] = make_int4(n[0], n[1], n[2], slot_kind[s]);
+    }
+}
+
+// keys of the representatives, kind-major
+template <typename R>
+__global__ void k_kind_keys(const typename PlaneT<R>::T* __restrict__ pl, long long E,
+                            const long long* __restrict__ rep, int nk, unsigned* __restrict__ keys)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nk) return;
+    int n[3];
+    KindKey<R>::get(pl, E, rep[i], keys + (long long)i * KindKey<R>::KW, n);
+}
+
+// kind records (KindRec) for the current material table (refreshed when h changes)
+template <typename R>
+__global__ void k_kind_records(const unsigned* __restrict__ keys, int nk, const Material<R>* __restrict__ mats,
+                               typename PlaneT<R>::T* __restrict__ out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nk) return;
+    constexpr int KW = KindKey<R>::KW;
+    const unsigned* key = keys + (long long)i * KW;
+    R w[9], V;
+    if constexpr (sizeof(R) == 4) {
+        for (int j = 0; j < 9; ++j) w[j] = __uint_as_float(key[j]);
+        V = volume_from_rows(reinterpret_cast<const float*>(w));
+    } else {
+        for (int j = 0; j < 9; ++j) w[j] = __hiloint2double((int)key[2 * j + 1], (int)key[2 * j]);
+        V = __hiloint2double((int)key[19], (int)key[18]);
+    }
+    const Material<R> m = mats[key[KW - 1]];
+    R r[KindRec<R>::NR];
+    ec_terms<R>(w, V, m.mu, m.lam, r);
+    r[9] = m.gamma;
+    r[10] = m.dsc;
+    r[11] = m.opd;
+    for (int j = 0; j < 9; ++j) r[12 + j] = w[j];
+    r[21] = V;
+    r[22] = m.mu;
+    r[23] = m.lam;
+    R* o = reinterpret_cast<R*>(out + (long long)i * KindRec<R>::Q);
+    for (int j = 0; j < KindRec<R>::NR; ++j) o[j] = r[j];
+}
+
+__global__ void k_max_degree(const long long* __restrict__ eoff, long long n, int* out)
+{
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) atomicMax(out, (int)(eoff[i + 1] - eoff[i]));
+}

@@ -16,22 +16,17 @@
 #include "vbd_build.cuh"
 #include "vbd_common.cuh"
 #include "vbd_kernels.cuh"
+#include "vbd_tiles.cuh"
 
 // K1 launch variant (lanes per vertex W, entries per lane per iteration U, min blocks/SM);
 // selected per context from VBD_K1 (e.g. "8x1", "4x2", "4x2b3"), default below.
 struct K1Variant {
     int W = 4, U = 2, minb = 3, pf = 1;
-    int pipeU = 0, pipeS = 0;  // cp.async pipelined fp32 kernel (0 = off)
 };
 K1Variant k1_variant_from_env()
 {
     K1Variant v;
     const char* e = getenv("VBD_K1");
-    if (e && !strncmp(e, "pipe", 4)) {
-        int u = 0, st = 0;
-        if (sscanf(e + 4, "%dx%d", &u, &st) == 2) { v.pipeU = u; v.pipeS = st; }
-        return v;
-    }
     if (e && *e) {
         int w = 0, u = 0, b = 0, p = 0;
         int n = sscanf(e, "%dx%db%dp%d", &w, &u, &b, &p);
@@ -97,7 +92,14 @@ struct DBuf {
         bytes = 0;
     }
     template <typename T> T* as() const { return static_cast<T*>(p); }
+    void swap(DBuf& o)
+    {
+        std::swap(p, o.p);
+        std::swap(bytes, o.bytes);
+    }
 };
+
+inline int EntryPlanesBytes(int precision) { return precision == VBD_PREC_F64 ? 96 : 48; }
 
 template <typename T> void upload(DBuf& b, const T* host, size_t n, cudaStream_t s)
 {
@@ -150,6 +152,18 @@ struct vbd_ctx {
     DBuf omega_dev;
     DBuf vmat;
     bool uniform_mat = false;
+    // compact layout: ent holds int4 entries, kinds the KindRec table (refreshed with the
+    // materials), kind_keys the exact rest data of each kind
+    bool compact = false;
+    int nkinds = 0;
+    int max_deg = 0;
+    DBuf kinds, kind_keys;
+    // K1T tile pipeline (compact layout, in-place range passes): tiles of 64 vertices per
+    // colour, their neighbour lists and 8-byte entries
+    bool tiles = false;
+    std::vector<int> tile_beg;  // first tile of colour c (size ncolors + 1)
+    int ent_cap = 0, nbr_cap = 0;
+    DBuf tv0, tnv, loff, tnbr, tent;
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -388,6 +402,133 @@ template <typename R> void alloc_state(vbd_ctx* c)
     CK(cudaMemsetAsync(c->stepctr.p, 0, 4, c->stream));
 }
 
+// Lossless entry dictionary (compact layout): when the explicit entries hold at
+// most VBD_KIND_CAP distinct (rows, volume, material) keys, re-pack them as int4
+// {n0, n1, n2, kind} and keep one record per kind.  VBD_LAYOUT=explicit disables it.
+template <typename R> void compact_entries(vbd_ctx* c)
+{
+    cudaStream_t s = c->stream;
+    c->compact = false;
+    c->nkinds = 0;
+    const char* lay = getenv("VBD_LAYOUT");
+    if ((lay && !strcmp(lay, "explicit")) || c->E == 0) return;
+    const char* capenv = getenv("VBD_KIND_CAP");
+    const int cap = capenv && *capenv ? atoi(capenv) : (1 << 16);
+    unsigned nslots = 1;
+    while (nslots < 4u * (unsigned)cap) nslots <<= 1;
+    DBuf slots, cnt;
+    slots.alloc((size_t)nslots * 8);
+    cnt.alloc(16);  // [0] count, [1] overflow, [2] missing
+    CK(cudaMemsetAsync(slots.p, 0, (size_t)nslots * 8, s));
+    CK(cudaMemsetAsync(cnt.p, 0, 16, s));
+    typedef typename PlaneT<R>::T PL;
+    const PL* pl = c->ent.as<PL>();
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    const unsigned grid = (unsigned)std::min<long long>(blocks_for(c->E), 16LL * sms);
+    k_kind_insert<R><<<grid, 256, 0, s>>>(pl, c->E, slots.as<unsigned long long>(), nslots - 1,
+                                          cnt.as<int>(), cap, cnt.as<int>() + 1);
+    CK(cudaGetLastError());
+    int hc[3];
+    CK(cudaMemcpyAsync(hc, cnt.p, 12, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hc[1] || hc[0] > cap) return;  // too many distinct kinds: keep the explicit layout
+    // kind ids in slot order (deterministic given the table)
+    std::vector<unsigned long long> hs(nslots);
+    CK(cudaMemcpy(hs.data(), slots.p, (size_t)nslots * 8, cudaMemcpyDeviceToHost));
+    std::vector<int> slot_kind(nslots, -1);
+    std::vector<long long> rep;
+    for (unsigned i = 0; i < nslots; ++i)
+        if (hs[i]) {
+            slot_kind[i] = (int)rep.size();
+            rep.push_back((long long)hs[i] - 1);
+        }
+    const int nk = (int)rep.size();
+    DBuf dsk, drep, cent;
+    upload(dsk, slot_kind.data(), nslots, s);
+    upload(drep, rep.data(), rep.size(), s);
+    c->kind_keys.alloc((size_t)nk * KindKey<R>::KW * 4);
+    k_kind_keys<R><<<blocks_for(nk), 256, 0, s>>>(pl, c->E, drep.as<long long>(), nk, c->kind_keys.as<unsigned>());
+    CK(cudaGetLastError());
+    cent.alloc((size_t)c->E * 16);
+    k_kind_emit<R><<<grid, 256, 0, s>>>(pl, c->E, slots.as<unsigned long long>(), nslots - 1,
+                                        dsk.as<int>(), cent.as<int4>(), cnt.as<int>() + 2);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(hc, cnt.p, 12, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hc[2]) fail(VBD_ERR_INTERNAL, "entry dictionary lookup failed");
+    c->ent.swap(cent);  // the explicit planes are released with `cent`
+    c->kinds.alloc((size_t)nk * KindRec<R>::Q * 16);
+    c->compact = true;
+    c->nkinds = nk;
+}
+
+// kind records for the current material table
+template <typename R> void refresh_kinds(vbd_ctx* c)
+{
+    if (!c->compact) return;
+    k_kind_records<R><<<blocks_for(c->nkinds), 256, 0, c->stream>>>(
+        c->kind_keys.as<unsigned>(), c->nkinds, c->mat.as<Material<R>>(), c->kinds.as<typename PlaneT<R>::T>());
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+// K1T tiles (vbd_tiles.cuh): 64 consecutive vertices of one colour, the sorted distinct
+// neighbours they read and their entries re-encoded against that list.  Needs the compact
+// layout, a valid colouring (in-place sweeps) and shared memory for two stages.
+constexpr size_t VBD_TILE_SMEM_MAX = 110 * 1024;  // two CTAs per SM
+
+template <typename R> void build_tiles(vbd_ctx* c)
+{
+    c->tiles = false;
+    const char* e = getenv("VBD_TILES");
+    if ((e && *e == '0') || !c->compact || !c->inplace || c->nsolve == 0 || c->nkinds > 65536) return;
+    if ((long long)VBD_TILE_V * c->max_deg * 3 > VBD_TILE_SORT) return;
+    cudaStream_t s = c->stream;
+    std::vector<int> v0, nv;
+    c->tile_beg.assign(c->ncolors + 1, 0);
+    for (int col = 0; col < c->ncolors; ++col) {
+        c->tile_beg[col] = (int)v0.size();
+        for (long long o = 0; o < c->ccnt[col]; o += VBD_TILE_V) {
+            v0.push_back((int)(c->cbeg[col] + o));
+            nv.push_back((int)std::min<long long>(VBD_TILE_V, c->ccnt[col] - o));
+        }
+    }
+    const int nt = (int)v0.size();
+    c->tile_beg[c->ncolors] = nt;
+    upload(c->tv0, v0.data(), v0.size(), s);
+    upload(c->tnv, nv.data(), nv.size(), s);
+    DBuf cnt, err;
+    cnt.alloc((size_t)nt * 8);
+    err.alloc(4);
+    CK(cudaMemsetAsync(err.p, 0, 4, s));
+    const int4* cent = c->ent.as<int4>();
+    k_tile_nbrs<false><<<nt, 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(), cent,
+                                         cnt.as<long long>(), nullptr, nullptr, err.as<int>());
+    CK(cudaGetLastError());
+    if (read_scalar<int>(err.p, s)) return;
+    std::vector<long long> hc(nt);
+    CK(cudaMemcpy(hc.data(), cnt.p, (size_t)nt * 8, cudaMemcpyDeviceToHost));
+    long long mx = 0;
+    for (long long x : hc) mx = std::max(mx, x);
+    if (mx > 65535) return;
+    c->nbr_cap = (int)mx;
+    c->ent_cap = VBD_TILE_V * c->max_deg + 2;
+    TileSmem<R> L{c->ent_cap, c->nbr_cap, c->nkinds};
+    if (L.total() > VBD_TILE_SMEM_MAX) return;
+    exclusive_offsets(cnt.as<long long>(), nt, c->loff, s);
+    const long long total = read_scalar<long long>(c->loff.as<long long>() + nt, s);
+    c->tnbr.alloc((size_t)std::max<long long>(total, 1) * 4);
+    c->tent.alloc((size_t)(c->E + 2) * 8);
+    CK(cudaMemsetAsync(c->tent.p, 0, (size_t)(c->E + 2) * 8, s));
+    k_tile_nbrs<true><<<nt, 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(), cent,
+                                        c->loff.as<long long>(), c->tnbr.as<int>(), c->tent.as<uint2>(),
+                                        err.as<int>());
+    CK(cudaGetLastError());
+    if (read_scalar<int>(err.p, s)) fail(VBD_ERR_INTERNAL, "tile build failed");
+    c->tiles = true;
+}
+
 // K6 + context finalisation
 template <typename R> void pack(vbd_ctx* c, Scene& sc)
 {
@@ -484,6 +625,15 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
     CK(cudaGetLastError());
     exclusive_offsets(deg.as<long long>(), c->nsolve, c->eoff, s);
     c->E = read_scalar<long long>(c->eoff.as<long long>() + c->nsolve, s);
+    {
+        DBuf md;
+        md.alloc(4);
+        CK(cudaMemsetAsync(md.p, 0, 4, s));
+        if (c->nsolve)
+            k_max_degree<<<blocks_for(c->nsolve), 256, 0, s>>>(c->eoff.as<long long>(), c->nsolve, md.as<int>());
+        CK(cudaGetLastError());
+        c->max_deg = read_scalar<int>(md.p, s);
+    }
     const int P = EntryPlanes<R>::P;
     c->ent.alloc(std::max<long long>(c->E, 1) * P * 16);
     DBuf badv;
@@ -500,6 +650,8 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
         fail(VBD_ERR_UNSUPPORTED,
              "fp32 layout recomputes tet volumes from |det W|; tet_vol disagrees with tet_w "
              "(use precision=fp64)");
+    compact_entries<R>(c);
+    build_tiles<R>(c);
     // one material per vertex? (always true for bodies built by build_system)
     {
         DBuf mixed;
@@ -542,6 +694,7 @@ template <typename R> void ensure_materials(vbd_ctx* c, double h)
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaMemcpy(c->mat.p, m.data(), m.size() * sizeof(Material<R>), cudaMemcpyHostToDevice));
     c->mat_h = h;
+    refresh_kinds<R>(c);
 }
 
 template <typename R>
@@ -550,6 +703,8 @@ K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
     K1Args<R> a;
     a.ent = c->ent.as<typename PlaneT<R>::T>();
     a.E = c->E;
+    a.kinds = c->compact ? c->kinds.as<typename PlaneT<R>::T>() : nullptr;
+    a.max_deg = c->max_deg;
     a.off = c->eoff.as<long long>();
     a.pos = c->pos.as<typename Vec4<R>::T>();
     a.xt = c->xt.as<typename Vec4<R>::T>();
@@ -585,57 +740,84 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     a.pf_dist = dist;
     const unsigned nb = blocks_for(threads);
     const bool um = a.vmat != nullptr;
+    // compact range passes: entries staged in smem by one bulk copy per CTA
+    static const bool bulk_on = !getenv("VBD_K1_BULK") || atoi(getenv("VBD_K1_BULK")) != 0;
+    const size_t smem = (size_t)(256 / W) * (size_t)std::max(a.max_deg, 1) * 16;
+    if (a.kinds && !a.group && !a.out && bulk_on && smem <= 64 * 1024) {
+        static bool attr[2] = {false, false};
+        auto kb = um ? k1_color_pass_bulk<R, W, U, B, true> : k1_color_pass_bulk<R, W, U, B, false>;
+        if (!attr[um]) {
+            CK(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+            attr[um] = true;
+        }
+        kb<<<nb, 256, smem, s>>>(a);
+        return;
+    }
+    if (a.kinds) {
+        if (pf && um) k1_color_pass<R, W, U, B, true, true, true><<<nb, 256, 0, s>>>(a);
+        else if (pf) k1_color_pass<R, W, U, B, true, false, true><<<nb, 256, 0, s>>>(a);
+        else if (um) k1_color_pass<R, W, U, B, false, true, true><<<nb, 256, 0, s>>>(a);
+        else k1_color_pass<R, W, U, B, false, false, true><<<nb, 256, 0, s>>>(a);
+        return;
+    }
     if (pf && um) k1_color_pass<R, W, U, B, true, true><<<nb, 256, 0, s>>>(a);
     else if (pf) k1_color_pass<R, W, U, B, true, false><<<nb, 256, 0, s>>>(a);
     else if (um) k1_color_pass<R, W, U, B, false, true><<<nb, 256, 0, s>>>(a);
     else k1_color_pass<R, W, U, B, false, false><<<nb, 256, 0, s>>>(a);
 }
 
-template <int U, int S, bool UM> void launch_k1_pipe_v(const K1Args<float>& a, cudaStream_t s)
+template <typename R, bool UM>
+void launch_k1_tiles_v(const vbd_ctx* c, const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
 {
-    constexpr int VPB = 256 / 4;
-    const int ntiles = (a.count + VPB - 1) / VPB;
-    static int grid_max = 0;
-    const size_t smem = sizeof(PipeSmem<4, U, S>);
-    if (!grid_max) {
-        CK(cudaFuncSetAttribute(k1_color_pass_pipe<4, U, S, UM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-        int dev = 0, sms = 148, per = 1;
+    static size_t attr = 0;
+    static int per_sm = 0, sms = 148;
+    if (smem > attr) {
+        CK(cudaFuncSetAttribute(k1_tiles<R, UM, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+        int dev = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k1_color_pass_pipe<4, U, S, UM>, 256, smem));
-        grid_max = std::max(1, per) * sms;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, 2>, 288, smem));
+        per_sm = std::max(1, per_sm);
     }
-    const int grid = std::min(ntiles, grid_max);
-    k1_color_pass_pipe<4, U, S, UM><<<grid, 256, smem, s>>>(a, ntiles);
+    const int grid = std::min(ta.tcount, per_sm * sms);
+    k1_tiles<R, UM, 2><<<grid, 288, smem, s>>>(ta);
 }
 
-template <typename R> bool launch_k1_pipe(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
+template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
 {
-    return false;
-}
-
-template <> bool launch_k1_pipe<float>(const vbd_ctx* c, const K1Args<float>& a, cudaStream_t s)
-{
-    const K1Variant& v = c->k1;
-    if (!v.pipeU || a.group || a.out) return false;
-    const bool um = a.vmat != nullptr;
-    if (v.pipeU == 1 && v.pipeS == 3) um ? launch_k1_pipe_v<1, 3, true>(a, s) : launch_k1_pipe_v<1, 3, false>(a, s);
-    else if (v.pipeU == 1 && v.pipeS == 4) um ? launch_k1_pipe_v<1, 4, true>(a, s) : launch_k1_pipe_v<1, 4, false>(a, s);
-    else if (v.pipeU == 2 && v.pipeS == 2) um ? launch_k1_pipe_v<2, 2, true>(a, s) : launch_k1_pipe_v<2, 2, false>(a, s);
-    else if (v.pipeU == 2 && v.pipeS == 3) um ? launch_k1_pipe_v<2, 3, true>(a, s) : launch_k1_pipe_v<2, 3, false>(a, s);
-    else fail(VBD_ERR_ARG, "unknown VBD_K1 pipe variant (pipe1x3, pipe1x4, pipe2x2, pipe2x3)");
+    if (!c->tiles || a.group || a.out || a.line_search || !a.kinds) return false;
+    int col = -1;
+    for (int k = 0; k < c->ncolors; ++k)
+        if (c->cbeg[k] == a.vbeg && c->ccnt[k] == a.count) col = k;
+    if (col < 0) return false;
+    K1TArgs<R> ta;
+    ta.a = a;
+    ta.tent = c->tent.as<uint2>();
+    ta.tnbr = c->tnbr.as<int>();
+    ta.loff = c->loff.as<long long>();
+    ta.tv0 = c->tv0.as<int>();
+    ta.tnv = c->tnv.as<int>();
+    ta.kinds = c->kinds.as<typename PlaneT<R>::T>();
+    ta.tbeg = c->tile_beg[col];
+    ta.tcount = c->tile_beg[col + 1] - c->tile_beg[col];
+    ta.ent_cap = c->ent_cap;
+    ta.nbr_cap = c->nbr_cap;
+    ta.nkinds = c->nkinds;
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds};
+    if (a.vmat) launch_k1_tiles_v<R, true>(c, ta, L.total(), s);
+    else launch_k1_tiles_v<R, false>(c, ta, L.total(), s);
     return true;
 }
 
 template <typename R> void launch_k1(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
 {
     if (a.count <= 0) return;
+    if (launch_k1_tiles<R>(c, a, s)) return;
     if (a.line_search && a.mode == 0) {
         k1_color_pass_ls<R><<<blocks_for((long long)a.count * 4), 256, 0, s>>>(a);
         return;
     }
-    if (launch_k1_pipe<R>(c, a, s)) return;
     const K1Variant& v = c->k1;
     if (v.W == 4 && v.U == 2 && v.minb == 3) launch_k1v<R, 4, 2, 3>(a, v.pf != 0, s);
     else if (v.W == 4 && v.U == 1) launch_k1v<R, 4, 1, 1>(a, v.pf != 0, s);
@@ -1335,13 +1517,19 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         for (int k = 0; k < c->ncolors && k < 64; ++k) info->color_count[k] = c->ccnt[k];
         long long b = 0;
         for (DBuf* d : {&c->perm, &c->inv, &c->eoff, &c->ent, &c->mat, &c->pos, &c->xt, &c->vt, &c->vprev,
-                        &c->y, &c->ha, &c->hb, &c->mass, &c->out, &c->stage, &c->color_orig})
+                        &c->y, &c->ha, &c->hb, &c->mass, &c->out, &c->stage, &c->color_orig, &c->kinds,
+                        &c->kind_keys, &c->vmat, &c->tv0, &c->tnv, &c->loff, &c->tnbr, &c->tent})
             b += (long long)d->bytes;
         info->device_bytes = b;
         info->precision = c->precision;
         info->inplace = c->inplace ? 1 : 0;
         info->lanes_per_vertex = c->k1.W;
         info->num_materials = (int)c->mats.size();
+        info->layout = c->compact ? 1 : 0;
+        info->num_entry_kinds = c->nkinds;
+        info->tiles = c->tiles ? (int)(c->tile_beg.back()) : 0;
+        info->tile_nbr_cap = c->nbr_cap;
+        info->entry_bytes = c->compact ? 16 : EntryPlanesBytes(c->precision);
     });
 }
 

@@ -50,6 +50,23 @@ struct StepFlag {  // first non-finite (step, iteration, vertex) as a 64-bit min
 // ---------------------------------------------------------------------------------------
 // entry access
 
+// V = 1 / (6 |det W|): |det| of the three non-own slot-weight rows equals |det Dm^-1|
+// (fp32 layouts recompute the rest volume instead of storing it)
+// Every product is pinned (explicit fma / mul.rn, never re-contracted by the compiler) so the
+// explicit layout (recomputed in K1) and the compact layout's kind table (computed once in
+// k_kind_records) round identically.
+__device__ __forceinline__ float volume_from_rows(const float* w)
+{
+    const float m1 = __fmaf_rn(w[4], w[8], -__fmul_rn(w[5], w[7]));
+    const float m2 = __fmaf_rn(w[3], w[8], -__fmul_rn(w[5], w[6]));
+    const float m3 = __fmaf_rn(w[3], w[7], -__fmul_rn(w[4], w[6]));
+    const float d = __fmaf_rn(w[2], m3, __fmaf_rn(-w[1], m2, __fmul_rn(w[0], m1)));
+    return __fdividef(1.0f / 6.0f, fabsf(d));
+}
+
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
 template <typename R> struct Entry;
 
 template <> struct Entry<float> {
@@ -71,11 +88,7 @@ template <> struct Entry<float> {
         e.w[0] = a.w;
         e.w[1] = b.x; e.w[2] = b.y; e.w[3] = b.z; e.w[4] = b.w;
         e.w[5] = c.x; e.w[6] = c.y; e.w[7] = c.z; e.w[8] = c.w;
-        // V = 1 / (6 |det W|): |det| of the three non-own slot-weight rows equals |det Dm^-1|
-        float d = e.w[0] * (e.w[4] * e.w[8] - e.w[5] * e.w[7]) -
-                  e.w[1] * (e.w[3] * e.w[8] - e.w[5] * e.w[6]) +
-                  e.w[2] * (e.w[3] * e.w[7] - e.w[4] * e.w[6]);
-        e.V = __fdividef(1.0f / 6.0f, fabsf(d));
+        e.V = volume_from_rows(e.w);
         return e;
     }
 };
@@ -104,69 +117,154 @@ template <> struct PlaneT<float> { typedef float4 T; };
 template <> struct PlaneT<double> { typedef double2 T; };
 
 // ---------------------------------------------------------------------------------------
-// per-entry Stable Neo-Hookean force/Hessian + Rayleigh damping, the arithmetic of
-// _native.pyx:283-317 (F, cofactor and J of _native.pyx:175-198) in edge-difference form.
+// Per-entry Stable Neo-Hookean force/Hessian + Rayleigh damping of _native.pyx:283-317
+// (F, cofactor and J of _native.pyx:175-198):
 //   f  -= V (mu F w + lam (J - gamma) C w) + dsc He (x_i - x_t,i)
 //   H  += (1 + dsc) He,  He = V (lam (C w)(C w)^T + mu |w|^2 I)
+// with w the vertex's own slot-weight row.  Only F w and C w are needed, never F itself.
+// Write the edges e_j = x_{n_j} - x_i as the columns of E and the other three slot rows
+// as the rows of W (F = E W, reference tet_w, _system.py:139-144).  Then
+//   F w = E s,          s_j = w_j . w
+//   C w = cof(E) q,     q = cof(W) w            (cof(E W) = cof(E) cof(W))
+//   J   = det(E) det(W)
+// and cof(E) q = (q0 e1 - q1 e0) x e2 + q2 (e0 x e1), det(E) = e2 . (e0 x e1).
+// s, q, det W, V lam and V mu |w|^2 depend only on the rest shape and material: ec_terms()
+// computes them (once per entry kind in the compact layout, per entry in the explicit one)
+// and tet_contrib_ec() is ~60 FP instructions per entry instead of ~130 for the F-form.
+//
+// Every multiply-add is written out (fma / mul_rn are never re-contracted by the compiler),
+// so all K1 variants -- explicit or compact entries, global or shared-memory staging -- round
+// identically and give bitwise equal results.
 // H is kept as 6 unique entries (xx, xy, xz, yy, yz, zz).
-template <typename R, bool DAMP = true>
-__device__ __forceinline__ void tet_contrib(const R* __restrict__ e0, const R* __restrict__ e1,
-                                            const R* __restrict__ e2, const R* __restrict__ w,
-                                            R V, const Material<R>& m, const R* __restrict__ dx,
-                                            R* __restrict__ f, R* __restrict__ H)
+
+template <typename R> __device__ __forceinline__ R dot3(const R* a, const R* b)
 {
-    R F[9];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) F[a * 3 + b] = e0[a] * w[b] + e1[a] * w[3 + b] + e2[a] * w[6 + b];
+    return fma(a[2], b[2], fma(a[1], b[1], mul_rn(a[0], b[0])));
+}
+template <typename R> __device__ __forceinline__ void cross3(const R* a, const R* b, R* c)
+{
+    c[0] = fma(a[1], b[2], -mul_rn(a[2], b[1]));
+    c[1] = fma(a[2], b[0], -mul_rn(a[0], b[2]));
+    c[2] = fma(a[0], b[1], -mul_rn(a[1], b[0]));
+}
+
+// t[0..2] = V mu s, t[3..5] = q, t[6] = det W, t[7] = V lam, t[8] = V mu |w|^2
+template <typename R>
+__device__ __forceinline__ void ec_terms(const R* __restrict__ w, R V, R mu, R lam, R* __restrict__ t)
+{
     R wo[3];
 #pragma unroll
-    for (int b = 0; b < 3; ++b) wo[b] = -((w[b] + w[3 + b]) + w[6 + b]);
-    R C[9];
-    C[0] = F[4] * F[8] - F[7] * F[5];
-    C[3] = F[7] * F[2] - F[1] * F[8];
-    C[6] = F[1] * F[5] - F[4] * F[2];
-    C[1] = F[5] * F[6] - F[8] * F[3];
-    C[4] = F[8] * F[0] - F[2] * F[6];
-    C[7] = F[2] * F[3] - F[5] * F[0];
-    C[2] = F[3] * F[7] - F[6] * F[4];
-    C[5] = F[6] * F[1] - F[0] * F[7];
-    C[8] = F[0] * F[4] - F[3] * F[1];
-    R J = F[0] * C[0] + F[3] * C[3] + F[6] * C[6];
-    R cw[3], Fw[3];
+    for (int b = 0; b < 3; ++b) wo[b] = -((w[b] + w[3 + b]) + w[6 + b]);  // own row
+    const R vmu = mul_rn(V, mu);
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        cw[a] = C[a * 3 + 0] * wo[0] + C[a * 3 + 1] * wo[1] + C[a * 3 + 2] * wo[2];
-        Fw[a] = F[a * 3 + 0] * wo[0] + F[a * 3 + 1] * wo[1] + F[a * 3 + 2] * wo[2];
-    }
-    R wsq = wo[0] * wo[0] + wo[1] * wo[1] + wo[2] * wo[2];
-    R coef = m.lam * (J - m.gamma);
-    R vl = V * m.lam, vmw = V * m.mu * wsq;
-    R he[6];
-    he[0] = vl * cw[0] * cw[0] + vmw;
-    he[1] = vl * cw[0] * cw[1];
-    he[2] = vl * cw[0] * cw[2];
-    he[3] = vl * cw[1] * cw[1] + vmw;
-    he[4] = vl * cw[1] * cw[2];
-    he[5] = vl * cw[2] * cw[2] + vmw;
+    for (int j = 0; j < 3; ++j) t[j] = mul_rn(vmu, dot3(w + 3 * j, wo));
+    R c[3];
+    cross3(w + 3, w + 6, c);
+    t[3] = dot3(c, wo);
+    t[6] = dot3(w, c);
+    cross3(w + 6, w, c);
+    t[4] = dot3(c, wo);
+    cross3(w, w + 3, c);
+    t[5] = dot3(c, wo);
+    t[7] = mul_rn(V, lam);
+    t[8] = mul_rn(vmu, dot3(wo, wo));
+}
+
+// DAMP = false: one material per vertex -- the undamped block is accumulated (H and the
+// scalar sum sv of V mu |w|^2) and the caller applies damping once per vertex.
+template <typename R, bool DAMP>
+__device__ __forceinline__ void tet_contrib_ec(const R* __restrict__ e0, const R* __restrict__ e1,
+                                               const R* __restrict__ e2, const R* __restrict__ t, R gamma,
+                                               R dsc, R opd, const R* __restrict__ dx, R* __restrict__ f,
+                                               R* __restrict__ H, R& sv)
+{
+    R fr[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) fr[a] = fma(t[2], e2[a], fma(t[1], e1[a], mul_rn(t[0], e0[a])));  // V mu F w
+    R u[3], c[3], k[3], cw[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) u[a] = fma(t[3], e1[a], -mul_rn(t[4], e0[a]));
+    cross3(e0, e1, c);
+    cross3(u, e2, k);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) cw[a] = fma(t[5], c[a], k[a]);  // C w
+    const R J = mul_rn(dot3(e2, c), t[6]);
+    const R vc = mul_rn(t[7], J - gamma);  // V lam (J - gamma)
+    R tv[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) tv[a] = mul_rn(t[7], cw[a]);
     if (DAMP) {
-        R hd0 = he[0] * dx[0] + he[1] * dx[1] + he[2] * dx[2];
-        R hd1 = he[1] * dx[0] + he[3] * dx[1] + he[4] * dx[2];
-        R hd2 = he[2] * dx[0] + he[4] * dx[1] + he[5] * dx[2];
-        f[0] -= V * (m.mu * Fw[0] + coef * cw[0]) + m.dsc * hd0;
-        f[1] -= V * (m.mu * Fw[1] + coef * cw[1]) + m.dsc * hd1;
-        f[2] -= V * (m.mu * Fw[2] + coef * cw[2]) + m.dsc * hd2;
+        R he[6];
+        he[0] = fma(tv[0], cw[0], t[8]);
+        he[1] = mul_rn(tv[0], cw[1]);
+        he[2] = mul_rn(tv[0], cw[2]);
+        he[3] = fma(tv[1], cw[1], t[8]);
+        he[4] = mul_rn(tv[1], cw[2]);
+        he[5] = fma(tv[2], cw[2], t[8]);
+        const R hd[3] = {fma(he[2], dx[2], fma(he[1], dx[1], mul_rn(he[0], dx[0]))),
+                         fma(he[4], dx[2], fma(he[3], dx[1], mul_rn(he[1], dx[0]))),
+                         fma(he[5], dx[2], fma(he[4], dx[1], mul_rn(he[2], dx[0])))};
 #pragma unroll
-        for (int q = 0; q < 6; ++q) H[q] += m.opd * he[q];
+        for (int a = 0; a < 3; ++a) f[a] = f[a] - fma(dsc, hd[a], fma(vc, cw[a], fr[a]));
+#pragma unroll
+        for (int q = 0; q < 6; ++q) H[q] = fma(opd, he[q], H[q]);
     } else {
-        // one material per vertex: sum the undamped blocks; the caller applies
-        // f -= dsc * (sum He) dx and H = (1 + dsc) sum He once per vertex
-        f[0] -= V * (m.mu * Fw[0] + coef * cw[0]);
-        f[1] -= V * (m.mu * Fw[1] + coef * cw[1]);
-        f[2] -= V * (m.mu * Fw[2] + coef * cw[2]);
 #pragma unroll
-        for (int q = 0; q < 6; ++q) H[q] += he[q];
+        for (int a = 0; a < 3; ++a) f[a] = f[a] - fma(vc, cw[a], fr[a]);
+        H[0] = fma(tv[0], cw[0], H[0]);
+        H[1] = fma(tv[0], cw[1], H[1]);
+        H[2] = fma(tv[0], cw[2], H[2]);
+        H[3] = fma(tv[1], cw[1], H[3]);
+        H[4] = fma(tv[1], cw[2], H[4]);
+        H[5] = fma(tv[2], cw[2], H[5]);
+        sv = sv + t[8];
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// compact layout ("entry kinds"): an entry is one int4 {n0, n1, n2, kind} (16 B) and the
+// per-kind constants live in a small table (L1/L2-resident).  Lossless: kinds are
+// deduplicated on the exact bits of the explicit entry (rows, volume, material), and both
+// layouts derive the constants with ec_terms, so they produce bitwise identical results.
+// Record (24 R): [0..8] ec_terms, [9] gamma, [10] dsc, [11] opd  (the sweep reads these 12)
+//                [12..20] w0..w8, [21] V, [22] mu, [23] lam     (local energy / line search)
+template <typename R> struct KindRec {
+    static constexpr int NR = 24;
+    static constexpr int HOT = 12;
+    static constexpr int Q = NR * (int)sizeof(R) / 16;    // 16-byte chunks per record
+    static constexpr int QH = HOT * (int)sizeof(R) / 16;  // chunks the sweep loads
+};
+
+struct EntryK {
+    int n[3];
+    int kind;
+    static __device__ __forceinline__ EntryK load(const int4* __restrict__ ent, long long k)
+    {
+        // the entry stream is touched once per pass: keep it out of L1 (positions and the
+        // kind table live there)
+        int4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(ent + k));
+        EntryK e;
+        e.n[0] = v.x; e.n[1] = v.y; e.n[2] = v.z; e.kind = v.w;
+        return e;
+    }
+};
+
+// load the first NQ 16-byte chunks of kind record `kind` into r (R[4*NQ*16/sizeof(R)/4])
+template <typename R, int NQ>
+__device__ __forceinline__ void load_kind(const typename PlaneT<R>::T* __restrict__ kinds, int kind, R* r)
+{
+    typedef typename PlaneT<R>::T PL;
+    const PL* p = kinds + (long long)kind * KindRec<R>::Q;
+    constexpr int PER = 16 / (int)sizeof(R);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const PL v = __ldg(p + q);
+        const R* vr = reinterpret_cast<const R*>(&v);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) r[q * PER + j] = vr[j];
     }
 }
 
@@ -182,23 +280,66 @@ __device__ __forceinline__ void block_solve(const R* f, const R* H, R eps_det, i
         if (H[5] != R(0)) d[2] = f[2] / H[5];
         return;
     }
-    // full symmetric matrix [H0 H1 H2; H1 H3 H4; H2 H4 H5]
-    R a0 = H[3] * H[5] - H[4] * H[4];
-    R a1 = H[2] * H[4] - H[1] * H[5];
-    R a2 = H[1] * H[4] - H[2] * H[3];
-    R a4 = H[0] * H[5] - H[2] * H[2];
-    R a5 = H[2] * H[1] - H[0] * H[4];
-    R a8 = H[0] * H[3] - H[1] * H[1];
-    R det = H[0] * a0 + H[1] * a1 + H[2] * a2;
-    R tr = (H[0] + H[3] + H[5]) / R(3);
-    if (fabs(det) > eps_det * tr * tr * tr) {
-        d[0] = (a0 * f[0] + a1 * f[1] + a2 * f[2]) / det;
-        d[1] = (a1 * f[0] + a4 * f[1] + a5 * f[2]) / det;
-        d[2] = (a2 * f[0] + a5 * f[1] + a8 * f[2]) / det;
+    // full symmetric matrix [H0 H1 H2; H1 H3 H4; H2 H4 H5] (products pinned, see above)
+    const R a0 = fma(H[3], H[5], -mul_rn(H[4], H[4]));
+    const R a1 = fma(H[2], H[4], -mul_rn(H[1], H[5]));
+    const R a2 = fma(H[1], H[4], -mul_rn(H[2], H[3]));
+    const R a4 = fma(H[0], H[5], -mul_rn(H[2], H[2]));
+    const R a5 = fma(H[2], H[1], -mul_rn(H[0], H[4]));
+    const R a8 = fma(H[0], H[3], -mul_rn(H[1], H[1]));
+    const R det = fma(H[2], a2, fma(H[1], a1, mul_rn(H[0], a0)));
+    const R tr = (H[0] + H[3] + H[5]) / R(3);
+    if (fabs(det) > mul_rn(mul_rn(mul_rn(eps_det, tr), tr), tr)) {
+        d[0] = fma(a2, f[2], fma(a1, f[1], mul_rn(a0, f[0]))) / det;
+        d[1] = fma(a5, f[2], fma(a4, f[1], mul_rn(a1, f[0]))) / det;
+        d[2] = fma(a8, f[2], fma(a5, f[1], mul_rn(a2, f[0]))) / det;
     }
+}
+
+// inertia term (_native.pyx:278-281) and the hoisted Rayleigh damping of one material per
+// vertex (_native.pyx:309-317 summed over the vertex's tets), pinned like tet_contrib_core
+template <typename R>
+__device__ __forceinline__ void vertex_terms(R* f, R* H, const R* dx, const R* xi, R y0, R y1, R y2,
+                                             R mih2, bool damp, R dsc, R opd)
+{
+    if (damp) {
+        const R hd0 = fma(H[2], dx[2], fma(H[1], dx[1], mul_rn(H[0], dx[0])));
+        const R hd1 = fma(H[4], dx[2], fma(H[3], dx[1], mul_rn(H[1], dx[0])));
+        const R hd2 = fma(H[5], dx[2], fma(H[4], dx[1], mul_rn(H[2], dx[0])));
+        f[0] = f[0] - mul_rn(dsc, hd0);
+        f[1] = f[1] - mul_rn(dsc, hd1);
+        f[2] = f[2] - mul_rn(dsc, hd2);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) H[q] = mul_rn(H[q], opd);
+    }
+    f[0] = fma(mih2, y0 - xi[0], f[0]);
+    f[1] = fma(mih2, y1 - xi[1], f[1]);
+    f[2] = fma(mih2, y2 - xi[2], f[2]);
+    H[0] = H[0] + mih2;
+    H[3] = H[3] + mih2;
+    H[5] = H[5] + mih2;
 }
 
 __device__ __forceinline__ bool finite3(double a, double b, double c)
 {
     return isfinite(a) && isfinite(b) && isfinite(c);
 }
+
+// ---------------------------------------------------------------------------------------
+// shared-memory address / mbarrier helpers (bulk-copy staging)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_wait_parity(unsigned bar, unsigned phase)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(bar), "r"(phase) : "memory");
+}
+

@@ -15,8 +15,10 @@
 template <typename R> struct K1Args {
     typedef typename Vec4<R>::T R4;
     typedef typename PlaneT<R>::T PL;
-    const PL* ent;           // entry planes
+    const PL* ent;           // entry planes (explicit layout) or int4 entries (compact)
     long long E;             // plane stride (entries)
+    const PL* kinds;         // compact layout: kind table (KindRec); nullptr = explicit
+    int max_deg;             // (host) max entries of one vertex: bulk-staging smem bound
     const long long* off;    // entry offsets of free vertices (nfree + 1)
     R4* pos;                 // current iterate x (in place)
     const R4* xt;            // x_t (w unused)
@@ -54,7 +56,23 @@ __device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int 
     typedef typename Vec4<R>::T R4;
     R e = R(0);
     for (long long k = beg + lane; k < end; k += W) {
-        const Entry<R> en = Entry<R>::load(a.ent, a.E, k);
+        Entry<R> en;
+        R mu, lam, gamma;
+        if (a.kinds) {
+            const EntryK ek = EntryK::load(reinterpret_cast<const int4*>(a.ent), k);
+            R r[KindRec<R>::NR];
+            load_kind<R, KindRec<R>::Q>(a.kinds, ek.kind, r);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) en.n[j] = ek.n[j];
+#pragma unroll
+            for (int j = 0; j < 9; ++j) en.w[j] = r[12 + j];
+            en.V = r[21];
+            mu = r[22]; lam = r[23]; gamma = r[9];
+        } else {
+            en = Entry<R>::load(a.ent, a.E, k);
+            const Material<R> m = a.mat[en.mat];
+            mu = m.mu; lam = m.lam; gamma = m.gamma;
+        }
         const R4 q0 = a.pos[en.n[0]], q1 = a.pos[en.n[1]], q2 = a.pos[en.n[2]];
         const R e0[3] = {q0.x - p[0], q0.y - p[1], q0.z - p[2]};
         const R e1[3] = {q1.x - p[0], q1.y - p[1], q1.z - p[2]};
@@ -70,8 +88,7 @@ __device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int 
         for (int q = 0; q < 9; ++q) ic += F[q] * F[q];
         const R J = F[0] * (F[4] * F[8] - F[7] * F[5]) + F[3] * (F[7] * F[2] - F[1] * F[8]) +
                     F[6] * (F[1] * F[5] - F[4] * F[2]);
-        const Material<R> m = a.mat[en.mat];
-        const R psi = (R(0.5) * m.mu) * (ic - R(3)) + (R(0.5) * m.lam) * (J - m.gamma) * (J - m.gamma);
+        const R psi = (R(0.5) * mu) * (ic - R(3)) + (R(0.5) * lam) * (J - gamma) * (J - gamma);
         e += en.V * psi;
     }
 #pragma unroll
@@ -84,28 +101,16 @@ __device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int 
     return ein + e;
 }
 
-template <typename R, int W, int U, bool UM, bool LS = false>
-__device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int lane)
+// explicit layout: U entries per lane per iteration; all their loads (entry planes, then the
+// 3U neighbour gathers) are issued before any math, for memory-level parallelism.  The
+// per-entry constants are derived from the rows on the fly (ec_terms).
+template <typename R, int W, int U, bool UM>
+__device__ __forceinline__ void k1_accumulate_explicit(const K1Args<R>& a, long long beg, long long end,
+                                                       int lane, const R* xi, const R* dx,
+                                                       const Material<R>& mv, R* f, R* H)
 {
     typedef typename Vec4<R>::T R4;
-    const unsigned gmask =
-        (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1)));
-    const int v = a.group ? a.group[g] : a.vbeg + g;
-    const R4 xi4 = a.pos[v];
-    if (v >= a.nsolve) {  // fixed / ghost: keep x (_native.pyx:424-426)
-        if (lane == 0 && a.out) a.out[g] = xi4;
-        return;
-    }
-    const R xi[3] = {xi4.x, xi4.y, xi4.z};
-    const R4 xt4 = a.xt[v];
-    const R dx[3] = {xi[0] - xt4.x, xi[1] - xt4.y, xi[2] - xt4.z};
-    R f[3] = {R(0), R(0), R(0)};
-    R H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
-    const long long beg = a.off[v], end = a.off[v + 1];
-    Material<R> mv;
-    if (UM) mv = a.mat[a.vmat[v]];
-    // U entries per lane per iteration: all their loads (entry planes, then the 3U
-    // neighbour gathers) are issued before any math, for memory-level parallelism.
+    R sv = R(0);
     for (long long k0 = beg + lane; k0 < end; k0 += (long long)W * U) {
         Entry<R> e[U];
         R4 p[U][3];
@@ -130,14 +135,110 @@ __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int la
                 const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
                 const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
                 const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
-                if (UM) {
-                    tet_contrib<R, false>(e0, e1, e2, e[u].w, e[u].V, mv, dx, f, H);
+                const Material<R> m = UM ? mv : a.mat[e[u].mat];
+                R t[9];
+                ec_terms<R>(e[u].w, e[u].V, m.mu, m.lam, t);
+                tet_contrib_ec<R, !UM>(e0, e1, e2, t, m.gamma, m.dsc, m.opd, dx, f, H, sv);
+            }
+        }
+    }
+    H[0] = H[0] + sv;
+    H[3] = H[3] + sv;
+    H[5] = H[5] + sv;
+}
+
+// compact layout: one 16-byte entry per (vertex, tet); the per-kind constants come from the
+// kind table (L1-resident).  UM: one material per vertex, damping hoisted -- its dsc / opd
+// are returned from the records.  SENT: the CTA's entries were staged in shared memory by a
+// bulk copy (k1_color_pass_bulk), entry k at sent[k - ebase].
+template <typename R, int W, int U, bool UM, bool SENT>
+__device__ __forceinline__ void k1_accumulate_compact(const K1Args<R>& a, long long beg, long long end,
+                                                      int lane, const R* xi, const R* dx, R* f, R* H,
+                                                      R& dsc, R& opd, const int4* sent, long long ebase)
+{
+    typedef typename Vec4<R>::T R4;
+    const int4* __restrict__ ent = reinterpret_cast<const int4*>(a.ent);
+    R sv = R(0);
+    for (long long k0 = beg + lane; k0 < end; k0 += (long long)W * U) {
+        EntryK e[U];
+        R4 p[U][3];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long k = k0 + (long long)u * W;
+            if (u == 0 || k < end) {
+                if constexpr (SENT) {
+                    const int4 v = sent[k - ebase];
+                    e[u].n[0] = v.x; e[u].n[1] = v.y; e[u].n[2] = v.z; e[u].kind = v.w;
                 } else {
-                    const Material<R> m = a.mat[e[u].mat];
-                    tet_contrib<R, true>(e0, e1, e2, e[u].w, e[u].V, m, dx, f, H);
+                    e[u] = EntryK::load(ent, k);
                 }
             }
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long k = k0 + (long long)u * W;
+            if (u == 0 || k < end) {
+                p[u][0] = a.pos[e[u].n[0]];
+                p[u][1] = a.pos[e[u].n[1]];
+                p[u][2] = a.pos[e[u].n[2]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long k = k0 + (long long)u * W;
+            if (u == 0 || k < end) {
+                R r[KindRec<R>::HOT];
+                load_kind<R, KindRec<R>::QH>(a.kinds, e[u].kind, r);
+                const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
+                const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
+                const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
+                tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], r[11], dx, f, H, sv);
+                if (UM) {
+                    dsc = r[10];
+                    opd = r[11];
+                }
+            }
+        }
+    }
+    H[0] = H[0] + sv;
+    H[3] = H[3] + sv;
+    H[5] = H[5] + sv;
+}
+
+template <typename R, int W, int U, bool UM, bool LS = false, bool KC = false, bool SENT = false>
+__device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int lane,
+                                               const int4* sent = nullptr, long long ebase = 0,
+                                               unsigned bar = 0)
+{
+    typedef typename Vec4<R>::T R4;
+    const unsigned gmask =
+        (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1)));
+    const int v = a.group ? a.group[g] : a.vbeg + g;
+    const R4 xi4 = a.pos[v];
+    if (v >= a.nsolve) {  // fixed / ghost: keep x (_native.pyx:424-426)
+        if (lane == 0 && a.out) a.out[g] = xi4;
+        return;
+    }
+    const R xi[3] = {xi4.x, xi4.y, xi4.z};
+    const R4 xt4 = a.xt[v];
+    const R dx[3] = {xi[0] - xt4.x, xi[1] - xt4.y, xi[2] - xt4.z};
+    R f[3] = {R(0), R(0), R(0)};
+    R H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+    const long long beg = a.off[v], end = a.off[v + 1];
+    const R4 y4 = a.y[v];  // inertia target, w = m / h^2 (issued early: used after the sweep)
+    if constexpr (SENT) mbar_wait_parity(bar, 0);  // the CTA's entries have landed in smem
+    Material<R> mv;
+    if constexpr (KC) {
+        mv.dsc = R(0);
+        mv.opd = R(1);
+        k1_accumulate_compact<R, W, U, UM, SENT>(a, beg, end, lane, xi, dx, f, H, mv.dsc, mv.opd, sent, ebase);
+        if (UM) {  // lane 0 holds the vertex's first entry: its material is the vertex's
+            mv.dsc = __shfl_sync(gmask, mv.dsc, 0, W);
+            mv.opd = __shfl_sync(gmask, mv.opd, 0, W);
+        }
+    } else {
+        if (UM) mv = a.mat[a.vmat[v]];
+        k1_accumulate_explicit<R, W, U, UM>(a, beg, end, lane, xi, dx, mv, f, H);
     }
 #pragma unroll
     for (int o = W / 2; o > 0; o >>= 1) {
@@ -147,26 +248,7 @@ __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int la
         for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(gmask, H[q], o, W);
     }
     if (!LS && lane != 0) return;
-    if (UM && end > beg) {
-        // hoisted Rayleigh damping (_native.pyx:309-317 summed over the vertex's tets):
-        // f -= dsc (sum He) dx,  H = (1 + dsc) sum He
-        const R hd0 = H[0] * dx[0] + H[1] * dx[1] + H[2] * dx[2];
-        const R hd1 = H[1] * dx[0] + H[3] * dx[1] + H[4] * dx[2];
-        const R hd2 = H[2] * dx[0] + H[4] * dx[1] + H[5] * dx[2];
-        f[0] -= mv.dsc * hd0;
-        f[1] -= mv.dsc * hd1;
-        f[2] -= mv.dsc * hd2;
-#pragma unroll
-        for (int q = 0; q < 6; ++q) H[q] *= mv.opd;
-    }
-    const R4 y4 = a.y[v];
-    const R mih2 = y4.w;  // inertia term, _native.pyx:278-281
-    f[0] += mih2 * (y4.x - xi[0]);
-    f[1] += mih2 * (y4.y - xi[1]);
-    f[2] += mih2 * (y4.z - xi[2]);
-    H[0] += mih2;
-    H[3] += mih2;
-    H[5] += mih2;
+    vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM && end > beg, mv.dsc, mv.opd);
     R d[3];
     block_solve<R>(f, H, a.eps_det, a.mode, d);
     R4 nx = xi4;
@@ -213,8 +295,13 @@ __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int la
 template <typename R, int W, int U>
 __device__ __forceinline__ void k1_vertex(const K1Args<R>& a, int g, int lane)
 {
-    if (a.vmat) k1_vertex_impl<R, W, U, true>(a, g, lane);
-    else k1_vertex_impl<R, W, U, false>(a, g, lane);
+    if (a.kinds) {
+        if (a.vmat) k1_vertex_impl<R, W, U, true, false, true>(a, g, lane);
+        else k1_vertex_impl<R, W, U, false, false, true>(a, g, lane);
+    } else {
+        if (a.vmat) k1_vertex_impl<R, W, U, true>(a, g, lane);
+        else k1_vertex_impl<R, W, U, false>(a, g, lane);
+    }
 }
 
 // K1 with the local line search (protocol path, line_search=True)
@@ -222,12 +309,14 @@ template <typename R>
 __global__ void __launch_bounds__(256) k1_color_pass_ls(const K1Args<R> a)
 {
     const int g = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) / 4);
-    if (g < a.count) k1_vertex_impl<R, 4, 1, false, true>(a, g, threadIdx.x & 3);
+    if (g >= a.count) return;
+    if (a.kinds) k1_vertex_impl<R, 4, 1, false, true, true>(a, g, threadIdx.x & 3);
+    else k1_vertex_impl<R, 4, 1, false, true>(a, g, threadIdx.x & 3);
 }
 
 // One group of W lanes per vertex; lane j handles entries j, j+W, ... of its vertex and the
 // group reduces f (3) and H (6) with a fixed xor-butterfly (bitwise deterministic).
-template <typename R, int W, int U, int MINB, bool PF, bool UM>
+template <typename R, int W, int U, int MINB, bool PF, bool UM, bool KC = false>
 __global__ void __launch_bounds__(256, MINB) k1_color_pass(const K1Args<R> a)
 {
     typedef typename Vec4<R>::T R4;
@@ -250,221 +339,51 @@ __global__ void __launch_bounds__(256, MINB) k1_color_pass(const K1Args<R> a)
             const unsigned bytes = (unsigned)((e1 - e0) * 16);
             if (bytes)
 #pragma unroll
-                for (int pl = 0; pl < EntryPlanes<R>::P; ++pl) {
+                for (int pl = 0; pl < (KC ? 1 : EntryPlanes<R>::P); ++pl) {
                     const void* src = reinterpret_cast<const char*>(a.ent) + 16 * (pl * a.E + e0);
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes)
                                  : "memory");
                 }
         }
     }
-    if (g < a.count) k1_vertex_impl<R, W, U, UM>(a, g, lane);
+    if (g < a.count) k1_vertex_impl<R, W, U, UM, false, KC>(a, g, lane);
 }
 
 // ---------------------------------------------------------------------------------------
-// K1 (pipelined, fp32, range mode): persistent CTAs walk tiles of 256/W vertices of the
-// colour range; every warp streams its lanes' entries (and, at a tile start, x / x_t of the
-// lane's vertex) into shared memory with per-lane cp.async (LDGSTS) S-1 items ahead of the
-// one it computes, so the entry latency leaves the dependency chain and only the neighbour
-// gathers remain.  An item = one iteration of the warp: U entries per lane.  Each lane only
-// reads its own shared-memory slots, so no barrier is needed between copy and use.
+// K1, compact layout, range mode, entries staged by the bulk-copy engine: a CTA's vertices
+// are consecutive, so their entries are one contiguous range [e0, e1) of 16-byte records.
+// One thread arms an mbarrier and issues a single cp.async.bulk (TMA, SASS UBLKCP) of the
+// range into shared memory; meanwhile every thread loads its vertex's x / x_t / y / CSR
+// offsets; then the entry reads are LDS and the only long-latency loads left in the sweep
+// are the neighbour gathers.  Dynamic smem = VPB x max degree x 16 B (host-checked).
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid)
+template <typename R, int W, int U, int MINB, bool UM>
+__global__ void __launch_bounds__(256, MINB) k1_color_pass_bulk(const K1Args<R> a)
 {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    const int n = valid ? 16 : 0;  // src-size 0 -> zero fill, no global read
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N> __device__ __forceinline__ void cp_async_wait()
-{
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int W, int U, int S>
-struct PipeSmem {
-    static constexpr int SLOTS = 3 * U + 2;  // U entries x 3 planes, then x and x_t
-    float4 buf[8][S][SLOTS][32];
-};
-
-template <int W, int U, int S, bool UM>
-__global__ void __launch_bounds__(256, 3) k1_color_pass_pipe(const K1Args<float> a, int ntiles)
-{
-    constexpr int VPB = 256 / W;   // vertices per tile
-    constexpr int VPW = 32 / W;    // vertices per warp
-    constexpr int SL = PipeSmem<W, U, S>::SLOTS;
-    extern __shared__ float4 dyn_smem[];
-    auto& sm = *reinterpret_cast<PipeSmem<W, U, S>*>(dyn_smem);
-    const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
-    const int lane = l32 & (W - 1), sub = l32 / W;
-    const unsigned gmask = (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << (l32 & ~(W - 1)));
-    const long long E = a.E;
-    const float4* __restrict__ ent = a.ent;
-
-    // tile descriptor of this lane's vertex
-    struct Desc {
-        int v;        // vertex (colour-major id) or -1
-        long long beg, end;
-        int rounds;   // warp-uniform
-    };
-    auto describe = [&](int tile) {
-        Desc d;
-        const int g = tile * VPB + warp * VPW + sub;
-        d.v = (tile < ntiles && g < a.count) ? a.vbeg + g : -1;
-        d.beg = d.v >= 0 ? a.off[d.v] : 0;
-        d.end = d.v >= 0 ? a.off[d.v + 1] : 0;
-        int r = (int)((d.end - d.beg + W * U - 1) / (W * U));
-        r = __reduce_max_sync(0xffffffffu, r);
-        d.rounds = r < 1 ? 1 : r;
-        return d;
-    };
-    auto issue = [&](const Desc& d, int it, int stage) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const long long k = d.beg + lane + (long long)(it * U + u) * W;
-            const bool ok = d.v >= 0 && k < d.end;
-            const long long ks = ok ? k : 0;
-#pragma unroll
-            for (int pl = 0; pl < 3; ++pl)
-                cp_async16(&sm.buf[warp][stage][pl * U + u][l32], ent + pl * E + ks, ok);
-        }
-        if (it == 0) {
-            const int vv = d.v >= 0 ? d.v : 0;
-            cp_async16(&sm.buf[warp][stage][3 * U][l32], a.pos + vv, d.v >= 0);
-            cp_async16(&sm.buf[warp][stage][3 * U + 1][l32], a.xt + vv, d.v >= 0);
-        }
-        cp_async_commit();
-    };
-
-    int tile = blockIdx.x;
-    if (tile >= ntiles) return;
-    Desc cur = describe(tile);
-    Desc nxt = describe(tile + gridDim.x);
-    // prologue: items 0 .. S-2
-    int itile = tile, iit = 0;     // issue cursor
-    Desc icur = cur, inxt = nxt;
-    int stage_issue = 0;
-    for (int p = 0; p < S - 1; ++p) {
-        if (itile < ntiles) issue(icur, iit, stage_issue);
-        else cp_async_commit();
-        stage_issue = (stage_issue + 1) % S;
-        if (++iit == icur.rounds) {
-            iit = 0;
-            itile += gridDim.x;
-            icur = inxt;
-            inxt = describe(itile + gridDim.x);
-        }
+    extern __shared__ __align__(16) int4 sent[];
+    __shared__ __align__(8) unsigned long long mbar;
+    constexpr int VPB = 256 / W;
+    const long long g0 = (long long)blockIdx.x * VPB;
+    const long long g1 = min((long long)a.count, g0 + VPB);
+    const long long e0 = a.off[a.vbeg + g0];
+    const unsigned bar = smem_u32(&mbar);
+    if (threadIdx.x == 0) {
+        const long long e1 = a.off[a.vbeg + g1];
+        const unsigned bytes = (unsigned)((e1 - e0) * 16);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        if (bytes)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(sent)),
+                "l"(reinterpret_cast<const int4*>(a.ent) + e0), "r"(bytes), "r"(bar)
+                : "memory");
     }
-    int it = 0, stage = 0;
-    float xi[3] = {0.f, 0.f, 0.f}, dx[3] = {0.f, 0.f, 0.f};
-    float f[3], H[6];
-    Material<float> mv;
-    while (tile < ntiles) {
-        // issue the item S-1 ahead
-        if (itile < ntiles) issue(icur, iit, stage_issue);
-        else cp_async_commit();
-        stage_issue = (stage_issue + 1) % S;
-        if (++iit == icur.rounds) {
-            iit = 0;
-            itile += gridDim.x;
-            icur = inxt;
-            inxt = describe(itile + gridDim.x);
-        }
-        cp_async_wait<S - 1>();  // this lane's copies of the current item have landed
-        if (it == 0) {
-            const float4 x4 = sm.buf[warp][stage][3 * U][l32];
-            const float4 t4 = sm.buf[warp][stage][3 * U + 1][l32];
-            xi[0] = x4.x; xi[1] = x4.y; xi[2] = x4.z;
-            dx[0] = x4.x - t4.x; dx[1] = x4.y - t4.y; dx[2] = x4.z - t4.z;
-#pragma unroll
-            for (int q = 0; q < 3; ++q) f[q] = 0.f;
-#pragma unroll
-            for (int q = 0; q < 6; ++q) H[q] = 0.f;
-            if (UM && cur.v >= 0) mv = a.mat[a.vmat[cur.v]];
-        }
-        float4 pos[U][3];
-        Entry<float> e[U];
-        bool ok[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const long long k = cur.beg + lane + (long long)(it * U + u) * W;
-            ok[u] = cur.v >= 0 && k < cur.end;
-            const float4 p0 = sm.buf[warp][stage][u][l32];
-            const float4 p1 = sm.buf[warp][stage][U + u][l32];
-            const float4 p2 = sm.buf[warp][stage][2 * U + u][l32];
-            const unsigned u0 = __float_as_uint(p0.x), u1 = __float_as_uint(p0.y), u2 = __float_as_uint(p0.z);
-            e[u].n[0] = (int)(u0 & VBD_ID_MASK);
-            e[u].n[1] = (int)(u1 & VBD_ID_MASK);
-            e[u].n[2] = (int)(u2 & VBD_ID_MASK);
-            e[u].mat = (int)((u0 >> VBD_ID_BITS) | ((u1 >> VBD_ID_BITS) << 3) | ((u2 >> VBD_ID_BITS) << 6));
-            e[u].w[0] = p0.w;
-            e[u].w[1] = p1.x; e[u].w[2] = p1.y; e[u].w[3] = p1.z; e[u].w[4] = p1.w;
-            e[u].w[5] = p2.x; e[u].w[6] = p2.y; e[u].w[7] = p2.z; e[u].w[8] = p2.w;
-            if (ok[u]) {
-                pos[u][0] = a.pos[e[u].n[0]];
-                pos[u][1] = a.pos[e[u].n[1]];
-                pos[u][2] = a.pos[e[u].n[2]];
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (!ok[u]) continue;
-            const float* w = e[u].w;
-            const float dd = w[0] * (w[4] * w[8] - w[5] * w[7]) - w[1] * (w[3] * w[8] - w[5] * w[6]) +
-                             w[2] * (w[3] * w[7] - w[4] * w[6]);
-            const float V = __fdividef(1.0f / 6.0f, fabsf(dd));
-            const float e0[3] = {pos[u][0].x - xi[0], pos[u][0].y - xi[1], pos[u][0].z - xi[2]};
-            const float e1[3] = {pos[u][1].x - xi[0], pos[u][1].y - xi[1], pos[u][1].z - xi[2]};
-            const float e2[3] = {pos[u][2].x - xi[0], pos[u][2].y - xi[1], pos[u][2].z - xi[2]};
-            if (UM) {
-                tet_contrib<float, false>(e0, e1, e2, w, V, mv, dx, f, H);
-            } else {
-                const Material<float> m = a.mat[e[u].mat];
-                tet_contrib<float, true>(e0, e1, e2, w, V, m, dx, f, H);
-            }
-        }
-        stage = (stage + 1) % S;
-        if (++it < cur.rounds) continue;
-        // vertex finished: group reduction, inertia, guarded solve, in-place write
-#pragma unroll
-        for (int o = W / 2; o > 0; o >>= 1) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q) f[q] += __shfl_xor_sync(gmask, f[q], o, W);
-#pragma unroll
-            for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(gmask, H[q], o, W);
-        }
-        if (lane == 0 && cur.v >= 0) {
-            const int v = cur.v;
-            if (UM && cur.end > cur.beg) {
-                const float hd0 = H[0] * dx[0] + H[1] * dx[1] + H[2] * dx[2];
-                const float hd1 = H[1] * dx[0] + H[3] * dx[1] + H[4] * dx[2];
-                const float hd2 = H[2] * dx[0] + H[4] * dx[1] + H[5] * dx[2];
-                f[0] -= mv.dsc * hd0;
-                f[1] -= mv.dsc * hd1;
-                f[2] -= mv.dsc * hd2;
-#pragma unroll
-                for (int q = 0; q < 6; ++q) H[q] *= mv.opd;
-            }
-            const float4 y4 = a.y[v];
-            const float mih2 = y4.w;
-            f[0] += mih2 * (y4.x - xi[0]);
-            f[1] += mih2 * (y4.y - xi[1]);
-            f[2] += mih2 * (y4.z - xi[2]);
-            H[0] += mih2;
-            H[3] += mih2;
-            H[5] += mih2;
-            float d[3];
-            block_solve<float>(f, H, a.eps_det, a.mode, d);
-            const float4 nx = make_float4(xi[0] + d[0], xi[1] + d[1], xi[2] + d[2], 0.f);
-            a.pos[v] = nx;
-            if (a.flag && !finite3(nx.x, nx.y, nx.z))
-                atomicMin(a.flag, StepFlag::key((unsigned)*a.stepctr, (unsigned)a.iter, (unsigned)a.perm[v]));
-        }
-        it = 0;
-        tile += gridDim.x;
-        cur = nxt;
-        nxt = describe(tile + gridDim.x);
-    }
-    cp_async_wait<0>();
+    __syncthreads();  // barrier initialised before anyone waits on it
+    const int g = (int)(g0 + threadIdx.x / W);
+    const int lane = threadIdx.x & (W - 1);
+    if (g < a.count) k1_vertex_impl<R, W, U, UM, false, true, true>(a, g, lane, sent, e0, bar);
 }
 
 template <typename R>

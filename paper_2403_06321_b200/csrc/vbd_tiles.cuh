@@ -1,0 +1,358 @@
+// vbd_tiles.cuh -- K1T: the colour pass as a warp-specialised, TMA-fed tile pipeline.
+//
+// A colour range is cut into tiles of VBD_TILE_V = 64 consecutive vertices (Morton-compact
+// in space).  Each tile carries, built once at pack time:
+//   * its sorted list of distinct neighbour vertices (the other-colour positions it reads),
+//   * its entries re-encoded against that list: 8 bytes {u16 n0, u16 n1, u16 n2, u16 kind}.
+// K1T is persistent: per CTA one producer warp and 8 consumer warps (4 lanes per vertex).
+// The producer fills a ring of shared-memory stages for tile t + grid: one elected lane
+// issues cp.async.bulk (TMA) copies of the tile's entry range and of x / x_t / y of its 64
+// vertices, all 32 lanes gather the neighbour positions (and CSR offsets) with cp.async,
+// and the stage's mbarrier completes on the byte count + the 32 cp.async arrivals.  The
+// consumers wait on the mbarrier, sweep their vertices with shared-memory loads only
+// (entries, neighbour positions, kind records), solve, store x in place, and release the
+// stage.  The arithmetic is tet_contrib_core / vertex_terms / block_solve: bitwise equal to
+// every other K1 variant.
+#pragma once
+#include "vbd_kernels.cuh"
+
+#define VBD_TILE_V 64
+#define VBD_TILE_SORT 8192  // max neighbour references (3 per entry) per tile for the build
+#define VBD_TILE_STAGES 2
+
+// ---------------------------------------------------------------------------------------
+// build: one CTA (256 threads) per tile.  FILL = false: count distinct neighbours;
+// FILL = true: write the sorted list at loff[t] and the 8-byte tile entries.
+
+template <bool FILL>
+__global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, const int* __restrict__ tnv,
+                                                   const long long* __restrict__ eoff,
+                                                   const int4* __restrict__ cent, long long* cnt_or_loff,
+                                                   int* __restrict__ tnbr, uint2* __restrict__ tent, int* err)
+{
+    __shared__ int keys[VBD_TILE_SORT];
+    __shared__ int part[257];
+    const int t = blockIdx.x, tid = threadIdx.x;
+    const int v0 = tv0[t], nv = tnv[t];
+    const long long e0 = eoff[v0], e1 = eoff[v0 + nv];
+    const int nref = (int)(3 * (e1 - e0));
+    if (nref > VBD_TILE_SORT) {
+        if (tid == 0) atomicExch(err, 1);
+        return;
+    }
+    int P = 256;
+    while (P < nref) P <<= 1;
+    for (int i = tid; i < P; i += 256) {
+        int k = 0x7fffffff;
+        if (i < nref) {
+            const int4 e = cent[e0 + i / 3];
+            const int r = i % 3;
+            k = r == 0 ? e.x : (r == 1 ? e.y : e.z);
+        }
+        keys[i] = k;
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < P; i += 256) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const int a = keys[i], b = keys[ixj];
+                    if ((a > b) == ((i & k) == 0)) {
+                        keys[i] = b;
+                        keys[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    // distinct keys: chunked count + serial scan of the 256 partial counts
+    const int chunk = P / 256;
+    const int i0 = tid * chunk;
+    int c = 0;
+    for (int i = i0; i < i0 + chunk; ++i)
+        if (i < nref && (i == 0 || keys[i] != keys[i - 1])) ++c;
+    part[tid] = c;
+    __syncthreads();
+    if (tid == 0) {
+        int s = 0;
+        for (int i = 0; i < 256; ++i) {
+            const int x = part[i];
+            part[i] = s;
+            s += x;
+        }
+        part[256] = s;
+    }
+    __syncthreads();
+    const int nl = part[256];
+    if (!FILL) {
+        if (tid == 0) cnt_or_loff[t] = nl;
+        return;
+    }
+    const long long l0 = cnt_or_loff[t];
+    int o = part[tid];
+    for (int i = i0; i < i0 + chunk; ++i)
+        if (i < nref && (i == 0 || keys[i] != keys[i - 1])) tnbr[l0 + o++] = keys[i];
+    __syncthreads();  // the list is visible to the whole CTA (global writes, bar.sync)
+    const int* lst = tnbr + l0;
+    for (long long k = e0 + tid; k < e1; k += 256) {
+        const int4 e = cent[k];
+        unsigned loc[3];
+        const int ids[3] = {e.x, e.y, e.z};
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            int lo = 0, hi = nl - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (lst[mid] < ids[r]) lo = mid + 1;
+                else hi = mid;
+            }
+            loc[r] = (unsigned)lo;
+        }
+        tent[k] = make_uint2(loc[0] | (loc[1] << 16), loc[2] | ((unsigned)e.w << 16));
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1T
+
+template <typename R> struct K1TArgs {
+    K1Args<R> a;               // vbeg/count = the colour range; pos/xt/y/flag/peer as K1
+    const uint2* tent;         // tile entries, global CSR order (+2 pad)
+    const int* tnbr;           // neighbour lists
+    const long long* loff;     // per-tile list base (ntiles + 1)
+    const int* tv0;            // per-tile first vertex
+    const int* tnv;            // per-tile vertex count
+    const typename PlaneT<R>::T* kinds;  // KindRec table (the sweep stages the first 12 R)
+    int tbeg, tcount;          // tiles of this colour
+    int ent_cap, nbr_cap;      // per-stage capacity (entries incl. pad, neighbours)
+    int nkinds;
+};
+
+struct TileHdr {
+    long long ebase;
+    int v0, nv;
+};
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+template <int N> __device__ __forceinline__ void cp_async_n(void* dst, const void* src)
+{
+    if constexpr (N == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(N) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned bar)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// dynamic smem: [kind records (12 R each)][stages]; per stage: hdr | entries | neighbour
+// positions | x | x_t | y | CSR offsets
+template <typename R> struct TileSmem {
+    typedef typename Vec4<R>::T R4;
+    int ent_cap, nbr_cap, nk;
+    __host__ __device__ size_t kinds_bytes() const { return (size_t)nk * KindRec<R>::HOT * sizeof(R); }
+    __host__ __device__ size_t off_hdr() const { return 0; }
+    __host__ __device__ size_t off_ent() const { return 16; }
+    __host__ __device__ size_t off_npos() const { return off_ent() + (size_t)ent_cap * 8; }
+    __host__ __device__ size_t off_x() const { return off_npos() + (size_t)nbr_cap * sizeof(R4); }
+    __host__ __device__ size_t off_xt() const { return off_x() + VBD_TILE_V * sizeof(R4); }
+    __host__ __device__ size_t off_y() const { return off_xt() + VBD_TILE_V * sizeof(R4); }
+    __host__ __device__ size_t off_eoff() const { return off_y() + VBD_TILE_V * sizeof(R4); }
+    __host__ __device__ size_t stage_bytes() const { return (off_eoff() + (VBD_TILE_V + 1) * 8 + 127) & ~(size_t)127; }
+    __host__ __device__ size_t total() const { return ((kinds_bytes() + 127) & ~(size_t)127) + VBD_TILE_STAGES * stage_bytes(); }
+};
+
+template <typename R, bool UM, int MINB>
+__global__ void __launch_bounds__(288, MINB) k1_tiles(const K1TArgs<R> ta)
+{
+    typedef typename Vec4<R>::T R4;
+    constexpr int S = VBD_TILE_STAGES;
+    constexpr int W = 4;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) unsigned long long full[S], empty[S];
+    const K1Args<R>& a = ta.a;
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds};
+    typedef typename PlaneT<R>::T PL;
+    PL* skind = reinterpret_cast<PL*>(smem);
+    unsigned char* stages = smem + ((L.kinds_bytes() + 127) & ~(size_t)127);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int QH = KindRec<R>::QH, Q = KindRec<R>::Q;
+    for (int i = tid; i < ta.nkinds * QH; i += blockDim.x) skind[i] = ta.kinds[(i / QH) * Q + i % QH];
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(smem_u32(&full[s]), 33);  // expect_tx arrive + 32 cp.async arrivals
+            mbar_init(smem_u32(&empty[s]), 8);  // one per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == 8) {  // ---------------- producer
+        int stage = 0;
+        unsigned ph = 0;
+        for (int t = blockIdx.x; t < ta.tcount; t += gridDim.x) {
+            mbar_wait_parity(smem_u32(&empty[stage]), ph ^ 1);
+            unsigned char* st = stages + stage * L.stage_bytes();
+            const int tt = ta.tbeg + t;
+            const int v0 = ta.tv0[tt], nv = ta.tnv[tt];
+            const long long e0 = a.off[v0], e1 = a.off[v0 + nv];
+            const long long eb = e0 & ~1ll, ee = (e1 + 1) & ~1ll;
+            const long long l0 = ta.loff[tt];
+            const int nl = (int)(ta.loff[tt + 1] - l0);
+            const unsigned bar = smem_u32(&full[stage]);
+            if (lane == 0) {
+                TileHdr* h = reinterpret_cast<TileHdr*>(st + L.off_hdr());
+                h->ebase = eb;
+                h->v0 = v0;
+                h->nv = nv;
+                const unsigned eby = (unsigned)((ee - eb) * 8), vby = (unsigned)(nv * sizeof(R4));
+                mbar_expect_tx(bar, eby + 3 * vby);
+                if (eby) bulk_g2s(st + L.off_ent(), ta.tent + eb, eby, bar);
+                bulk_g2s(st + L.off_x(), a.pos + v0, vby, bar);
+                bulk_g2s(st + L.off_xt(), a.xt + v0, vby, bar);
+                bulk_g2s(st + L.off_y(), a.y + v0, vby, bar);
+            }
+            R4* np = reinterpret_cast<R4*>(st + L.off_npos());
+            for (int i = lane; i < nl; i += 32) {
+                const int id = ta.tnbr[l0 + i];
+                if constexpr (sizeof(R4) == 16) {
+                    cp_async_n<16>(np + i, a.pos + id);
+                } else {
+                    cp_async_n<16>(reinterpret_cast<char*>(np + i), reinterpret_cast<const char*>(a.pos + id));
+                    cp_async_n<16>(reinterpret_cast<char*>(np + i) + 16, reinterpret_cast<const char*>(a.pos + id) + 16);
+                }
+            }
+            long long* so = reinterpret_cast<long long*>(st + L.off_eoff());
+            for (int i = lane; i <= nv; i += 32) cp_async_n<8>(so + i, a.off + v0 + i);
+            cp_async_mbar_arrive(bar);
+            if (++stage == S) {
+                stage = 0;
+                ph ^= 1;
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        return;
+    }
+
+    // ---------------- consumers: warp w handles tile vertices 8w .. 8w+7, 4 lanes each
+    const int lv = warp * 8 + (lane >> 2), j = lane & 3;
+    int stage = 0;
+    unsigned ph = 0;
+    for (int t = blockIdx.x; t < ta.tcount; t += gridDim.x) {
+        mbar_wait_parity(smem_u32(&full[stage]), ph);
+        const unsigned char* st = stages + stage * L.stage_bytes();
+        const TileHdr h = *reinterpret_cast<const TileHdr*>(st + L.off_hdr());
+        const uint2* sent = reinterpret_cast<const uint2*>(st + L.off_ent());
+        const R4* np = reinterpret_cast<const R4*>(st + L.off_npos());
+        const bool act = lv < h.nv;
+        const int lvc = act ? lv : 0;
+        const R4 xi4 = reinterpret_cast<const R4*>(st + L.off_x())[lvc];
+        const R4 xt4 = reinterpret_cast<const R4*>(st + L.off_xt())[lvc];
+        const R4 y4 = reinterpret_cast<const R4*>(st + L.off_y())[lvc];
+        const long long* so = reinterpret_cast<const long long*>(st + L.off_eoff());
+        const int beg = act ? (int)(so[lv] - h.ebase) : 0;
+        const int end = act ? (int)(so[lv + 1] - h.ebase) : 0;
+        const R xi[3] = {xi4.x, xi4.y, xi4.z};
+        const R dx[3] = {xi[0] - xt4.x, xi[1] - xt4.y, xi[2] - xt4.z};
+        R f[3] = {R(0), R(0), R(0)};
+        R H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+        R sv = R(0), dsc = R(0), opd = R(1);
+        constexpr int U = 2;
+        for (int k0 = beg + j; k0 < end; k0 += W * U) {
+            uint2 e[U];
+            R4 p[U][3];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = k0 + u * W;
+                if (u == 0 || k < end) {
+                    e[u] = sent[k];
+                    p[u][0] = np[e[u].x & 0xffffu];
+                    p[u][1] = np[e[u].x >> 16];
+                    p[u][2] = np[e[u].y & 0xffffu];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = k0 + u * W;
+                if (u == 0 || k < end) {
+                    R r[KindRec<R>::HOT];
+                    const PL* rp = skind + (e[u].y >> 16) * QH;
+#pragma unroll
+                    for (int q = 0; q < QH; ++q) {
+                        const PL v = rp[q];
+                        const R* vr = reinterpret_cast<const R*>(&v);
+#pragma unroll
+                        for (int z = 0; z < 16 / (int)sizeof(R); ++z) r[q * (16 / (int)sizeof(R)) + z] = vr[z];
+                    }
+                    const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
+                    const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
+                    const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
+                    tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], r[11], dx, f, H, sv);
+                    if (UM) {
+                        dsc = r[10];
+                        opd = r[11];
+                    }
+                }
+            }
+        }
+        H[0] = H[0] + sv;
+        H[3] = H[3] + sv;
+        H[5] = H[5] + sv;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));  // stage's smem no longer read
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) f[q] += __shfl_xor_sync(0xffffffffu, f[q], o, W);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(0xffffffffu, H[q], o, W);
+        }
+        if (act && j == 0) {  // lane 0 of the group processed the vertex's first entry (UM: dsc/opd)
+            const int v = h.v0 + lv;
+            vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM && end > beg, dsc, opd);
+            R d[3];
+            block_solve<R>(f, H, a.eps_det, a.mode, d);
+            R4 nx = xi4;
+            nx.x = xi[0] + d[0];
+            nx.y = xi[1] + d[1];
+            nx.z = xi[2] + d[2];
+            a.pos[v] = nx;
+            if (a.peer_pos[0] || a.peer_pos[1]) {
+                const int jj = v - a.vbeg;
+                if (jj < a.nb[0]) {
+                    a.peer_pos[0][a.peer_off[0] + jj] = nx;  // NVLink store into the left ghost
+                    __threadfence_system();
+                } else if (jj < a.nb[0] + a.nb[1]) {
+                    a.peer_pos[1][a.peer_off[1] + (jj - a.nb[0])] = nx;
+                    __threadfence_system();
+                }
+            }
+            if (a.flag && !finite3(nx.x, nx.y, nx.z))
+                atomicMin(a.flag, StepFlag::key((unsigned)*a.stepctr, (unsigned)a.iter, (unsigned)a.perm[v]));
+        }
+        if (++stage == S) {
+            stage = 0;
+            ph ^= 1;
+        }
+    }
+}

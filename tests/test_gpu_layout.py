@@ -1,0 +1,152 @@
+"""GPU: the two entry layouts of K1.
+
+* explicit -- every (vertex, tet) entry carries its slot-weight rows (48 B fp32 / 96 B fp64);
+* compact  -- the entry is one int4 {n0, n1, n2, kind} and each distinct (rows, volume,
+  material) key lives once in a kind table.  Chosen automatically when the scene has at most
+  VBD_KIND_CAP distinct keys (structured grids, instanced objects).
+
+The compact layout is a lossless re-encoding running the same arithmetic, so it must give
+results bitwise identical to the explicit layout; both are held to the oracle by the parity
+suite (tests/test_gpu_parity.py runs whichever layout the scene selects, i.e. compact for
+the generated grids) and here on an irregular mesh that must fall back to explicit.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+G = (0.0, 0.0, -9.8)
+H = 1.0 / 60.0
+
+
+@pytest.fixture(scope="module")
+def V():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2403_06321_b200 as V
+    return V
+
+
+def beam_sys(O, nx=13, ny=6, nz=6, spacing=0.05, mat=(1e6, 1e7, 1e-6)):
+    m = O.generate_beam(nx, ny, nz, spacing)
+    fixed = np.flatnonzero(m.rest_positions[:, 0] < 1e-9)
+    return m, O.build_system([(m, mat)], fixed)
+
+
+def make_ctx(V, O, s, precision, layout, monkeypatch, cap=None):
+    """layout: "explicit" | "compact" (16-byte entries, K1 over global memory) | "auto"
+    (compact + the K1T tile pipeline when the scene allows it)."""
+    monkeypatch.setenv("VBD_LAYOUT", "explicit" if layout == "explicit" else "auto")
+    monkeypatch.setenv("VBD_TILES", "0" if layout == "compact" else "1")
+    if cap is not None:
+        monkeypatch.setenv("VBD_KIND_CAP", str(cap))
+    else:
+        monkeypatch.delenv("VBD_KIND_CAP", raising=False)
+    ctx = V.DeviceContext.from_system(O.RefSystemView(s), precision=precision)
+    monkeypatch.delenv("VBD_LAYOUT")
+    monkeypatch.delenv("VBD_TILES")
+    return ctx
+
+
+def steps(ctx, s, n, rho=0.9, n_max=10, line_search=False, x0=None):
+    z = np.zeros((s.num_vertices, 3))
+    x0 = s.rest_positions if x0 is None else x0
+    ctx.set_state(x=x0, x_t=x0, v_t=z, v_prev=z)
+    p = ctx.step_params(H, n_max, rho, 1e-10, "adaptive", G, line_search=line_search)
+    for _ in range(n):
+        ctx.step(p)
+    return ctx.get_state(x=True, v_t=True)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_compact_selected_for_grids(V, O, precision, monkeypatch):
+    m, s = beam_sys(O)
+    ctx = make_ctx(V, O, s, precision, "auto", monkeypatch)
+    assert ctx.info.layout == 1 and ctx.info.entry_bytes == 16
+    if precision == "fp32":
+        # a 5-tet grid has 10 rest shapes x 4 slots (fp32 rows round to identical bits)
+        assert ctx.info.num_entry_kinds == 40
+    ex = make_ctx(V, O, s, precision, "explicit", monkeypatch)
+    assert ex.info.layout == 0 and ex.info.entry_bytes == (48 if precision == "fp32" else 96)
+    assert ex.info.num_entry_kinds == 0
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("rho", [0.0, 0.9])
+@pytest.mark.parametrize("layout", ["compact", "auto"])
+def test_compact_bitwise_equals_explicit(V, O, precision, rho, layout, monkeypatch):
+    m, s = beam_sys(O)
+    ctx = make_ctx(V, O, s, precision, layout, monkeypatch)
+    if precision == "fp32":  # fp64 grids have ~1e3 kinds (ulp-distinct rows): tiles off
+        assert (ctx.info.tiles > 0) == (layout == "auto")
+    a = steps(ctx, s, 5, rho=rho)
+    b = steps(make_ctx(V, O, s, precision, "explicit", monkeypatch), s, 5, rho=rho)
+    assert np.array_equal(a["x"], b["x"])
+    assert np.array_equal(a["v_t"], b["v_t"])
+
+
+def test_tiles_cover_every_colour(V, O, monkeypatch):
+    """64-vertex tiles per colour; every neighbour list fits the 16-bit local index."""
+    m, s = beam_sys(O, 21, 9, 7)
+    ctx = make_ctx(V, O, s, "fp32", "auto", monkeypatch)
+    counts = ctx.color_counts()
+    assert ctx.info.tiles == sum((c + 63) // 64 for c in counts)
+    assert 0 < ctx.info.tile_nbr_cap < 65536
+
+
+def test_compact_bitwise_equals_explicit_line_search(V, O, monkeypatch):
+    m, s = beam_sys(O)
+    a = steps(make_ctx(V, O, s, "fp64", "auto", monkeypatch), s, 2, rho=0.0, line_search=True)
+    b = steps(make_ctx(V, O, s, "fp64", "explicit", monkeypatch), s, 2, rho=0.0, line_search=True)
+    assert np.array_equal(a["x"], b["x"])
+
+
+def test_compact_mixed_materials_per_vertex(V, O, monkeypatch):
+    """Non-uniform material per vertex (damping per entry, material from the kind record)."""
+    m, s = beam_sys(O)
+    rng = np.random.default_rng(3)
+    pick = rng.random(len(s.tets)) < 0.5
+    s.tet_mu = np.where(pick, 1e6, 3e6)
+    s.tet_lam = np.where(pick, 1e7, 2e7)
+    s.tet_kd = np.where(pick, 1e-6, 5e-6)
+    monkeypatch.setenv("VBD_UNIFORM_MAT", "0")
+    a_ctx = make_ctx(V, O, s, "fp64", "auto", monkeypatch)
+    c_ctx = make_ctx(V, O, s, "fp64", "compact", monkeypatch)
+    b_ctx = make_ctx(V, O, s, "fp64", "explicit", monkeypatch)
+    assert a_ctx.info.layout == 1 and a_ctx.info.num_materials == 2
+    a = steps(a_ctx, s, 3)
+    b = steps(b_ctx, s, 3)
+    assert np.array_equal(a["x"], b["x"])
+    assert np.array_equal(steps(c_ctx, s, 3)["x"], b["x"])
+    st = O.make_state(s)
+    for _ in range(3):
+        O.step(s, st, H, 10, 0.9, G)
+    assert np.abs(a["x"] - st.x).max() / m.bbox_diagonal() <= 1e-10
+
+
+def test_irregular_mesh_falls_back_to_explicit(V, O, monkeypatch):
+    """Jittered rest positions: every tet has its own shape, more kinds than the cap."""
+    m = O.generate_beam(9, 5, 5, 0.05)
+    rng = np.random.default_rng(0)
+    pos = m.rest_positions + rng.uniform(-0.008, 0.008, m.rest_positions.shape)
+    mj = O.build_tet_mesh(pos, m.tets, 1000.0)
+    fixed = np.flatnonzero(pos[:, 0] < 0.01)
+    s = O.build_system([(mj, (1e6, 1e7, 1e-6))], fixed)
+    ctx = make_ctx(V, O, s, "fp32", "auto", monkeypatch, cap=256)
+    assert ctx.info.layout == 0
+    roomy = make_ctx(V, O, s, "fp32", "auto", monkeypatch)  # default cap: fits
+    assert roomy.info.layout == 1 and roomy.info.num_entry_kinds > 256
+    st = O.make_state(s)
+    for _ in range(4):
+        O.step(s, st, H, 10, 0.9, G)
+    diag = mj.bbox_diagonal()
+    for c in (ctx, roomy):
+        x = steps(c, s, 4)["x"]
+        assert np.abs(x - st.x).max() / diag <= 1e-5
+
+
+def test_device_generated_c5_like_block_is_compact(V):
+    ctx = V.DeviceContext.from_beams([V.Beam(40, 40, 40, 0.01, 2e6, 2e7, 1e-7, fix_min_x=True)],
+                                     precision="fp32")
+    assert ctx.info.layout == 1 and ctx.info.num_entry_kinds <= 64
