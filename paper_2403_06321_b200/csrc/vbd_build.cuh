@@ -645,3 +645,43 @@ __global__ void k_max_degree(const long long* __restrict__ eoff, long long n, in
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < n) atomicMax(out, (int)(eoff[i + 1] - eoff[i]));
 }
+
+// Entry order within a vertex: sorted by a hash of the entry's kind key (the exact rest data
+// the layouts deduplicate), ties in ascending (tet, slot) order.  Vertices of one class of a
+// structured grid then list the same kinds in the same order, so the lanes of a K1T
+// quarter-warp (same entry position, 8 vertices) read the same kind record (smem broadcast).
+// Every layout is packed from this one order, so they stay bitwise equal.
+template <typename R>
+__global__ void k_inc_kind_keys(const long long* __restrict__ off, const unsigned* __restrict__ inc,
+                                const double* __restrict__ tet_w, const double* __restrict__ vol,
+                                const int* __restrict__ tmat, long long n, unsigned long long* __restrict__ keys)
+{
+    const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    for (long long k = off[v]; k < off[v + 1]; ++k) {
+        const unsigned val = inc[k];
+        const long long t = val >> 2;
+        const int sl = (int)(val & 3u);
+        unsigned key[KindKey<R>::KW];
+        int j = 0;
+        for (int q = 0; q < 4; ++q) {
+            if (q == sl) continue;
+            for (int b = 0; b < 3; ++b) {
+                const double w = tet_w[12 * t + 3 * q + b];
+                if constexpr (sizeof(R) == 4) {
+                    key[3 * j + b] = __float_as_uint((float)w);
+                } else {
+                    key[2 * (3 * j + b)] = (unsigned)__double2loint(w);
+                    key[2 * (3 * j + b) + 1] = (unsigned)__double2hiint(w);
+                }
+            }
+            ++j;
+        }
+        if constexpr (sizeof(R) == 8) {
+            key[18] = (unsigned)__double2loint(vol[t]);
+            key[19] = (unsigned)__double2hiint(vol[t]);
+        }
+        key[KindKey<R>::KW - 1] = (unsigned)tmat[t];
+        keys[k] = ((unsigned long long)v << 32) | kind_hash<KindKey<R>::KW>(key);
+    }
+}

@@ -163,7 +163,8 @@ struct vbd_ctx {
     bool tiles = false;
     std::vector<int> tile_beg;  // first tile of colour c (size ncolors + 1)
     int ent_cap = 0, nbr_cap = 0;
-    DBuf tv0, tnv, loff, tnbr, tent;
+    DBuf tv0, tnv, loff, tnbr, tent, tdesc;
+    int tile_stages = 2;
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -482,7 +483,7 @@ template <typename R> void build_tiles(vbd_ctx* c)
 {
     c->tiles = false;
     const char* e = getenv("VBD_TILES");
-    if ((e && *e == '0') || !c->compact || !c->inplace || c->nsolve == 0 || c->nkinds > 65536) return;
+    if ((e && *e == '0') || !c->compact || !c->inplace || c->nsolve == 0 || c->nkinds >= 65535) return;
     if ((long long)VBD_TILE_V * c->max_deg * 3 > VBD_TILE_SORT) return;
     cudaStream_t s = c->stream;
     std::vector<int> v0, nv;
@@ -499,34 +500,71 @@ template <typename R> void build_tiles(vbd_ctx* c)
     upload(c->tv0, v0.data(), v0.size(), s);
     upload(c->tnv, nv.data(), nv.size(), s);
     DBuf cnt, err;
-    cnt.alloc((size_t)nt * 8);
+    cnt.alloc((size_t)nt * 16);
     err.alloc(4);
     CK(cudaMemsetAsync(err.p, 0, 4, s));
     const int4* cent = c->ent.as<int4>();
     k_tile_nbrs<false><<<nt, 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(), cent,
-                                         cnt.as<long long>(), nullptr, nullptr, err.as<int>());
+                                         cnt.as<long long>(), nullptr, nullptr, nullptr, nullptr, err.as<int>());
     CK(cudaGetLastError());
     if (read_scalar<int>(err.p, s)) return;
-    std::vector<long long> hc(nt);
-    CK(cudaMemcpy(hc.data(), cnt.p, (size_t)nt * 8, cudaMemcpyDeviceToHost));
-    long long mx = 0;
-    for (long long x : hc) mx = std::max(mx, x);
+    std::vector<long long> hc(2 * (size_t)nt), nls(nt), nss(nt);
+    CK(cudaMemcpy(hc.data(), cnt.p, (size_t)nt * 16, cudaMemcpyDeviceToHost));
+    long long mx = 0, ms = 0;
+    for (int t = 0; t < nt; ++t) {
+        nls[t] = hc[2 * t];
+        nss[t] = hc[2 * t + 1];
+        mx = std::max(mx, nls[t]);
+        ms = std::max(ms, nss[t]);
+    }
     if (mx > 65535) return;
     c->nbr_cap = (int)mx;
-    c->ent_cap = VBD_TILE_V * c->max_deg + 2;
+    c->ent_cap = (int)ms;
     TileSmem<R> L{c->ent_cap, c->nbr_cap, c->nkinds};
-    if (L.total() > VBD_TILE_SMEM_MAX) return;
-    exclusive_offsets(cnt.as<long long>(), nt, c->loff, s);
+    // as many stages (2..4) as fit two CTAs per SM
+    int stages = 0;
+    for (int st = 4; st >= 2 && !stages; --st)
+        if (L.total(st) <= VBD_TILE_SMEM_MAX) stages = st;
+    const char* se = getenv("VBD_TILE_STAGES");
+    if (se && *se) stages = std::min(stages, atoi(se));
+    if (stages < 2) return;
+    c->tile_stages = stages;
+    DBuf dl, ds, sbase;
+    upload(dl, nls.data(), nls.size(), s);
+    upload(ds, nss.data(), nss.size(), s);
+    exclusive_offsets(dl.as<long long>(), nt, c->loff, s);
+    exclusive_offsets(ds.as<long long>(), nt, sbase, s);
     const long long total = read_scalar<long long>(c->loff.as<long long>() + nt, s);
+    const long long slots = read_scalar<long long>(sbase.as<long long>() + nt, s);
     c->tnbr.alloc((size_t)std::max<long long>(total, 1) * 4);
-    c->tent.alloc((size_t)(c->E + 2) * 8);
-    CK(cudaMemsetAsync(c->tent.p, 0, (size_t)(c->E + 2) * 8, s));
+    c->tent.alloc((size_t)std::max<long long>(slots, 1) * 8);
     k_tile_nbrs<true><<<nt, 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(), cent,
-                                        c->loff.as<long long>(), c->tnbr.as<int>(), c->tent.as<uint2>(),
-                                        err.as<int>());
+                                        nullptr, c->loff.as<long long>(), sbase.as<long long>(),
+                                        c->tnbr.as<int>(), c->tent.as<uint2>(), err.as<int>());
     CK(cudaGetLastError());
     if (read_scalar<int>(err.p, s)) fail(VBD_ERR_INTERNAL, "tile build failed");
+    c->tdesc.alloc((size_t)nt * sizeof(TileDesc));
+    k_tile_desc<<<blocks_for(nt), 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
+                                              c->loff.as<long long>(), sbase.as<long long>(), nt,
+                                              c->tdesc.as<TileDesc>());
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
     c->tiles = true;
+}
+
+// per-vertex entry order by kind (k_inc_kind_keys): one stable 64-bit radix sort of
+// (vertex << 32 | kind hash) over the incidence
+template <typename R> void sort_incidence_by_kind(Scene& sc, cudaStream_t s)
+{
+    const long long n4 = 4 * sc.T;
+    if (n4 == 0) return;
+    DBuf keys;
+    keys.alloc(n4 * 8);
+    k_inc_kind_keys<R><<<blocks_for(sc.n), 256, 0, s>>>(sc.inc_off.as<long long>(), sc.inc.as<unsigned>(),
+                                                        sc.tet_w.as<double>(), sc.vol.as<double>(),
+                                                        sc.tmat.as<int>(), sc.n, keys.as<unsigned long long>());
+    CK(cudaGetLastError());
+    sort_pairs_u64_i32(keys, sc.inc, n4, s);
 }
 
 // K6 + context finalisation
@@ -536,6 +574,7 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
     c->n = sc.n;
     c->T = sc.T;
     if (sc.n >= (1LL << VBD_ID_BITS)) fail(VBD_ERR_UNSUPPORTED, "too many vertices for one context");
+    if (!(getenv("VBD_KIND_ORDER") && *getenv("VBD_KIND_ORDER") == '0')) sort_incidence_by_kind<R>(sc, s);
     // colouring validity (decides in-place vs aux-buffer sweeps)
     {
         DBuf bad;
@@ -766,22 +805,29 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     else k1_color_pass<R, W, U, B, false, false><<<nb, 256, 0, s>>>(a);
 }
 
-template <typename R, bool UM>
-void launch_k1_tiles_v(const vbd_ctx* c, const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
+template <typename R, bool UM, int S>
+void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
 {
     static size_t attr = 0;
     static int per_sm = 0, sms = 148;
     if (smem > attr) {
-        CK(cudaFuncSetAttribute(k1_tiles<R, UM, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = smem;
         int dev = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, 2>, 288, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, S>, 288, smem));
         per_sm = std::max(1, per_sm);
     }
     const int grid = std::min(ta.tcount, per_sm * sms);
-    k1_tiles<R, UM, 2><<<grid, 288, smem, s>>>(ta);
+    k1_tiles<R, UM, S><<<grid, 288, smem, s>>>(ta);
+}
+
+template <typename R, bool UM> void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, size_t smem, cudaStream_t s)
+{
+    if (stages >= 4) launch_k1_tiles_v<R, UM, 4>(ta, smem, s);
+    else if (stages == 3) launch_k1_tiles_v<R, UM, 3>(ta, smem, s);
+    else launch_k1_tiles_v<R, UM, 2>(ta, smem, s);
 }
 
 template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
@@ -795,9 +841,7 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     ta.a = a;
     ta.tent = c->tent.as<uint2>();
     ta.tnbr = c->tnbr.as<int>();
-    ta.loff = c->loff.as<long long>();
-    ta.tv0 = c->tv0.as<int>();
-    ta.tnv = c->tnv.as<int>();
+    ta.desc = c->tdesc.as<TileDesc>();
     ta.kinds = c->kinds.as<typename PlaneT<R>::T>();
     ta.tbeg = c->tile_beg[col];
     ta.tcount = c->tile_beg[col + 1] - c->tile_beg[col];
@@ -805,8 +849,9 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     ta.nbr_cap = c->nbr_cap;
     ta.nkinds = c->nkinds;
     const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds};
-    if (a.vmat) launch_k1_tiles_v<R, true>(c, ta, L.total(), s);
-    else launch_k1_tiles_v<R, false>(c, ta, L.total(), s);
+    const int S = c->tile_stages;
+    if (a.vmat) launch_k1_tiles_s<R, true>(ta, S, L.total(S), s);
+    else launch_k1_tiles_s<R, false>(ta, S, L.total(S), s);
     return true;
 }
 
@@ -1518,7 +1563,8 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         long long b = 0;
         for (DBuf* d : {&c->perm, &c->inv, &c->eoff, &c->ent, &c->mat, &c->pos, &c->xt, &c->vt, &c->vprev,
                         &c->y, &c->ha, &c->hb, &c->mass, &c->out, &c->stage, &c->color_orig, &c->kinds,
-                        &c->kind_keys, &c->vmat, &c->tv0, &c->tnv, &c->loff, &c->tnbr, &c->tent})
+                        &c->kind_keys, &c->vmat, &c->tv0, &c->tnv, &c->loff, &c->tnbr, &c->tent,
+                        &c->tdesc})
             b += (long long)d->bytes;
         info->device_bytes = b;
         info->precision = c->precision;

@@ -3,7 +3,11 @@
 // A colour range is cut into tiles of VBD_TILE_V = 64 consecutive vertices (Morton-compact
 // in space).  Each tile carries, built once at pack time:
 //   * its sorted list of distinct neighbour vertices (the other-colour positions it reads),
-//   * its entries re-encoded against that list: 8 bytes {u16 n0, u16 n1, u16 n2, u16 kind}.
+//   * its entries re-encoded against that list: 8 bytes {u16 n0, u16 n1, u16 n2, u16 kind},
+//     laid out per consumer warp as [round i][lane] slots: lane = 8 j + vi serves entry
+//     position 4 i + j of the warp's vertex vi (padding slots carry kind 0xffff).  A warp's
+//     slot reads are contiguous, and the 8 lanes of a quarter-warp (same position, 8 vertices
+//     of one class) read the same kind record: shared-memory broadcast.
 // K1T is persistent: per CTA one producer warp and 8 consumer warps (4 lanes per vertex).
 // The producer fills a ring of shared-memory stages for tile t + grid: one elected lane
 // issues cp.async.bulk (TMA) copies of the tile's entry range and of x / x_t / y of its 64
@@ -18,20 +22,41 @@
 
 #define VBD_TILE_V 64
 #define VBD_TILE_SORT 8192  // max neighbour references (3 per entry) per tile for the build
-#define VBD_TILE_STAGES 2
 
 // ---------------------------------------------------------------------------------------
 // build: one CTA (256 threads) per tile.  FILL = false: count distinct neighbours;
 // FILL = true: write the sorted list at loff[t] and the 8-byte tile entries.
 
+#define VBD_TILE_PAD 0xffffu
+
+// rounds (entry slots per lane) of consumer warp w of a tile: max over its 8 vertices of
+// ceil(degree / 4)
+__device__ __forceinline__ int tile_warp_rounds(const long long* __restrict__ eoff, int v0, int nv, int w)
+{
+    int r = 0;
+    for (int vi = 0; vi < 8; ++vi) {
+        const int lv = 8 * w + vi;
+        if (lv >= nv) break;
+        const int d = (int)(eoff[v0 + lv + 1] - eoff[v0 + lv]);
+        r = max(r, (d + 3) / 4);
+    }
+    return r;
+}
+
+// build: one CTA (256 threads) per tile.  FILL = false: count distinct neighbours (cnt[2t])
+// and entry slots (cnt[2t+1]); FILL = true: write the sorted neighbour list at lbase[t] and
+// the slots at sbase[t].
 template <bool FILL>
 __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, const int* __restrict__ tnv,
                                                    const long long* __restrict__ eoff,
-                                                   const int4* __restrict__ cent, long long* cnt_or_loff,
-                                                   int* __restrict__ tnbr, uint2* __restrict__ tent, int* err)
+                                                   const int4* __restrict__ cent, long long* cnt,
+                                                   const long long* __restrict__ lbase,
+                                                   const long long* __restrict__ sbase, int* __restrict__ tnbr,
+                                                   uint2* __restrict__ tent, int* err)
 {
     __shared__ int keys[VBD_TILE_SORT];
     __shared__ int part[257];
+    __shared__ int wslot[9];
     const int t = blockIdx.x, tid = threadIdx.x;
     const int v0 = tv0[t], nv = tnv[t];
     const long long e0 = eoff[v0], e1 = eoff[v0 + nv];
@@ -39,6 +64,14 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
     if (nref > VBD_TILE_SORT) {
         if (tid == 0) atomicExch(err, 1);
         return;
+    }
+    if (tid == 0) {
+        int sb = 0;
+        for (int w = 0; w < 8; ++w) {
+            wslot[w] = sb;
+            sb += 32 * tile_warp_rounds(eoff, v0, nv, w);
+        }
+        wslot[8] = sb;
     }
     int P = 256;
     while (P < nref) P <<= 1;
@@ -86,43 +119,85 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
     __syncthreads();
     const int nl = part[256];
     if (!FILL) {
-        if (tid == 0) cnt_or_loff[t] = nl;
+        if (tid == 0) {
+            cnt[2 * t] = nl;
+            cnt[2 * t + 1] = wslot[8];
+        }
         return;
     }
-    const long long l0 = cnt_or_loff[t];
+    const long long l0 = lbase[t];
     int o = part[tid];
     for (int i = i0; i < i0 + chunk; ++i)
         if (i < nref && (i == 0 || keys[i] != keys[i - 1])) tnbr[l0 + o++] = keys[i];
     __syncthreads();  // the list is visible to the whole CTA (global writes, bar.sync)
     const int* lst = tnbr + l0;
-    for (long long k = e0 + tid; k < e1; k += 256) {
-        const int4 e = cent[k];
-        unsigned loc[3];
-        const int ids[3] = {e.x, e.y, e.z};
+    const long long s0 = sbase[t];
+    for (int sl = tid; sl < wslot[8]; sl += 256) {
+        int w = 0;
+        while (sl >= wslot[w + 1]) ++w;
+        const int rel = sl - wslot[w];
+        const int lane = rel & 31, i = rel >> 5;
+        const int lv = 8 * w + (lane & 7), pos = 4 * i + (lane >> 3);
+        uint2 out = make_uint2(0u, VBD_TILE_PAD << 16);
+        if (lv < nv) {
+            const long long k = eoff[v0 + lv] + pos;
+            if (k < eoff[v0 + lv + 1]) {
+                const int4 e = cent[k];
+                unsigned loc[3];
+                const int ids[3] = {e.x, e.y, e.z};
 #pragma unroll
-        for (int r = 0; r < 3; ++r) {
-            int lo = 0, hi = nl - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (lst[mid] < ids[r]) lo = mid + 1;
-                else hi = mid;
+                for (int r = 0; r < 3; ++r) {
+                    int lo = 0, hi = nl - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (lst[mid] < ids[r]) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    loc[r] = (unsigned)lo;
+                }
+                out = make_uint2(loc[0] | (loc[1] << 16), loc[2] | ((unsigned)e.w << 16));
             }
-            loc[r] = (unsigned)lo;
         }
-        tent[k] = make_uint2(loc[0] | (loc[1] << 16), loc[2] | ((unsigned)e.w << 16));
+        tent[s0 + sl] = out;
     }
 }
 
-// ---------------------------------------------------------------------------------------
-// K1T
+// per-tile descriptor: one 32-byte load for the producer
+struct __align__(16) TileDesc {
+    long long eb;   // first entry slot (tiles are 256-byte aligned in the slot array)
+    long long l0;   // neighbour list base
+    int v0, nv;     // vertices
+    int ne;         // entry slots
+    int nl;         // distinct neighbours
+    unsigned rw[2]; // rounds of consumer warps 0..7, one byte each
+    int pad[2];
+};
+
+__global__ void k_tile_desc(const int* __restrict__ tv0, const int* __restrict__ tnv,
+                            const long long* __restrict__ eoff, const long long* __restrict__ lbase,
+                            const long long* __restrict__ sbase, int nt, TileDesc* __restrict__ out)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    TileDesc d;
+    d.v0 = tv0[t];
+    d.nv = tnv[t];
+    d.eb = sbase[t];
+    d.ne = (int)(sbase[t + 1] - sbase[t]);
+    d.l0 = lbase[t];
+    d.nl = (int)(lbase[t + 1] - d.l0);
+    d.rw[0] = d.rw[1] = 0;
+    for (int w = 0; w < 8; ++w)
+        d.rw[w >> 2] |= (unsigned)tile_warp_rounds(eoff, d.v0, d.nv, w) << (8 * (w & 3));
+    d.pad[0] = d.pad[1] = 0;
+    out[t] = d;
+}
 
 template <typename R> struct K1TArgs {
     K1Args<R> a;               // vbeg/count = the colour range; pos/xt/y/flag/peer as K1
     const uint2* tent;         // tile entries, global CSR order (+2 pad)
     const int* tnbr;           // neighbour lists
-    const long long* loff;     // per-tile list base (ntiles + 1)
-    const int* tv0;            // per-tile first vertex
-    const int* tnv;            // per-tile vertex count
+    const TileDesc* desc;      // per-tile descriptors
     const typename PlaneT<R>::T* kinds;  // KindRec table (the sweep stages the first 12 R)
     int tbeg, tcount;          // tiles of this colour
     int ent_cap, nbr_cap;      // per-stage capacity (entries incl. pad, neighbours)
@@ -130,9 +205,11 @@ template <typename R> struct K1TArgs {
 };
 
 struct TileHdr {
-    long long ebase;
     int v0, nv;
+    unsigned rw[2];
 };
+
+
 
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count)
 {
@@ -165,8 +242,8 @@ __device__ __forceinline__ void cp_async_mbar_arrive(unsigned bar)
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
 
-// dynamic smem: [kind records (12 R each)][stages]; per stage: hdr | entries | neighbour
-// positions | x | x_t | y | CSR offsets
+// dynamic smem: [kind records (12 R each)][stages]; per stage: hdr | entry slots | neighbour
+// positions | x | x_t | y
 template <typename R> struct TileSmem {
     typedef typename Vec4<R>::T R4;
     int ent_cap, nbr_cap, nk;
@@ -177,16 +254,14 @@ template <typename R> struct TileSmem {
     __host__ __device__ size_t off_x() const { return off_npos() + (size_t)nbr_cap * sizeof(R4); }
     __host__ __device__ size_t off_xt() const { return off_x() + VBD_TILE_V * sizeof(R4); }
     __host__ __device__ size_t off_y() const { return off_xt() + VBD_TILE_V * sizeof(R4); }
-    __host__ __device__ size_t off_eoff() const { return off_y() + VBD_TILE_V * sizeof(R4); }
-    __host__ __device__ size_t stage_bytes() const { return (off_eoff() + (VBD_TILE_V + 1) * 8 + 127) & ~(size_t)127; }
-    __host__ __device__ size_t total() const { return ((kinds_bytes() + 127) & ~(size_t)127) + VBD_TILE_STAGES * stage_bytes(); }
+    __host__ __device__ size_t stage_bytes() const { return (off_y() + VBD_TILE_V * sizeof(R4) + 127) & ~(size_t)127; }
+    __host__ __device__ size_t total(int stages) const { return ((kinds_bytes() + 127) & ~(size_t)127) + stages * stage_bytes(); }
 };
 
-template <typename R, bool UM, int MINB>
-__global__ void __launch_bounds__(288, MINB) k1_tiles(const K1TArgs<R> ta)
+template <typename R, bool UM, int S>
+__global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
 {
     typedef typename Vec4<R>::T R4;
-    constexpr int S = VBD_TILE_STAGES;
     constexpr int W = 4;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long full[S], empty[S];
@@ -210,40 +285,51 @@ __global__ void __launch_bounds__(288, MINB) k1_tiles(const K1TArgs<R> ta)
     if (warp == 8) {  // ---------------- producer
         int stage = 0;
         unsigned ph = 0;
+        TileDesc dn;
+        if (blockIdx.x < ta.tcount) dn = ta.desc[ta.tbeg + blockIdx.x];
         for (int t = blockIdx.x; t < ta.tcount; t += gridDim.x) {
+            const TileDesc d = dn;
+            if (t + gridDim.x < ta.tcount) dn = ta.desc[ta.tbeg + t + gridDim.x];  // overlaps the wait
             mbar_wait_parity(smem_u32(&empty[stage]), ph ^ 1);
             unsigned char* st = stages + stage * L.stage_bytes();
-            const int tt = ta.tbeg + t;
-            const int v0 = ta.tv0[tt], nv = ta.tnv[tt];
-            const long long e0 = a.off[v0], e1 = a.off[v0 + nv];
-            const long long eb = e0 & ~1ll, ee = (e1 + 1) & ~1ll;
-            const long long l0 = ta.loff[tt];
-            const int nl = (int)(ta.loff[tt + 1] - l0);
             const unsigned bar = smem_u32(&full[stage]);
             if (lane == 0) {
                 TileHdr* h = reinterpret_cast<TileHdr*>(st + L.off_hdr());
-                h->ebase = eb;
-                h->v0 = v0;
-                h->nv = nv;
-                const unsigned eby = (unsigned)((ee - eb) * 8), vby = (unsigned)(nv * sizeof(R4));
+                h->v0 = d.v0;
+                h->nv = d.nv;
+                h->rw[0] = d.rw[0];
+                h->rw[1] = d.rw[1];
+                const unsigned eby = (unsigned)d.ne * 8u, vby = (unsigned)(d.nv * sizeof(R4));
                 mbar_expect_tx(bar, eby + 3 * vby);
-                if (eby) bulk_g2s(st + L.off_ent(), ta.tent + eb, eby, bar);
-                bulk_g2s(st + L.off_x(), a.pos + v0, vby, bar);
-                bulk_g2s(st + L.off_xt(), a.xt + v0, vby, bar);
-                bulk_g2s(st + L.off_y(), a.y + v0, vby, bar);
+                if (eby) bulk_g2s(st + L.off_ent(), ta.tent + d.eb, eby, bar);
+                bulk_g2s(st + L.off_x(), a.pos + d.v0, vby, bar);
+                bulk_g2s(st + L.off_xt(), a.xt + d.v0, vby, bar);
+                bulk_g2s(st + L.off_y(), a.y + d.v0, vby, bar);
             }
             R4* np = reinterpret_cast<R4*>(st + L.off_npos());
-            for (int i = lane; i < nl; i += 32) {
-                const int id = ta.tnbr[l0 + i];
-                if constexpr (sizeof(R4) == 16) {
-                    cp_async_n<16>(np + i, a.pos + id);
-                } else {
-                    cp_async_n<16>(reinterpret_cast<char*>(np + i), reinterpret_cast<const char*>(a.pos + id));
-                    cp_async_n<16>(reinterpret_cast<char*>(np + i) + 16, reinterpret_cast<const char*>(a.pos + id) + 16);
+            // neighbour gathers: the ids of a batch are loaded together, then their copies
+            // issued (the cp.async asm is a compiler barrier for loads)
+            constexpr int B = 8;
+            for (int base = 0; base < d.nl; base += 32 * B) {
+                int id[B];
+#pragma unroll
+                for (int q = 0; q < B; ++q) {
+                    const int i = base + q * 32 + lane;
+                    id[q] = i < d.nl ? __ldg(ta.tnbr + d.l0 + i) : -1;
+                }
+#pragma unroll
+                for (int q = 0; q < B; ++q) {
+                    if (id[q] < 0) continue;
+                    const int i = base + q * 32 + lane;
+                    if constexpr (sizeof(R4) == 16) {
+                        cp_async_n<16>(np + i, a.pos + id[q]);
+                    } else {
+                        cp_async_n<16>(reinterpret_cast<char*>(np + i), reinterpret_cast<const char*>(a.pos + id[q]));
+                        cp_async_n<16>(reinterpret_cast<char*>(np + i) + 16,
+                                       reinterpret_cast<const char*>(a.pos + id[q]) + 16);
+                    }
                 }
             }
-            long long* so = reinterpret_cast<long long*>(st + L.off_eoff());
-            for (int i = lane; i <= nv; i += 32) cp_async_n<8>(so + i, a.off + v0 + i);
             cp_async_mbar_arrive(bar);
             if (++stage == S) {
                 stage = 0;
@@ -254,38 +340,41 @@ __global__ void __launch_bounds__(288, MINB) k1_tiles(const K1TArgs<R> ta)
         return;
     }
 
-    // ---------------- consumers: warp w handles tile vertices 8w .. 8w+7, 4 lanes each
-    const int lv = warp * 8 + (lane >> 2), j = lane & 3;
+    // ---------------- consumers: warp w handles tile vertices 8w .. 8w+7; lane = 8 j + vi
+    // serves entry positions j, j + 4, ... of vertex vi
+    const int vi = lane & 7, j = lane >> 3;
+    const int lv = warp * 8 + vi;
     int stage = 0;
     unsigned ph = 0;
     for (int t = blockIdx.x; t < ta.tcount; t += gridDim.x) {
         mbar_wait_parity(smem_u32(&full[stage]), ph);
         const unsigned char* st = stages + stage * L.stage_bytes();
         const TileHdr h = *reinterpret_cast<const TileHdr*>(st + L.off_hdr());
-        const uint2* sent = reinterpret_cast<const uint2*>(st + L.off_ent());
+        int sb = 0;
+        for (int w = 0; w < warp; ++w) sb += (int)((h.rw[w >> 2] >> (8 * (w & 3))) & 0xffu);
+        const int rounds = (int)((h.rw[warp >> 2] >> (8 * (warp & 3))) & 0xffu);
+        const uint2* sent = reinterpret_cast<const uint2*>(st + L.off_ent()) + 32 * sb + lane;
         const R4* np = reinterpret_cast<const R4*>(st + L.off_npos());
         const bool act = lv < h.nv;
         const int lvc = act ? lv : 0;
         const R4 xi4 = reinterpret_cast<const R4*>(st + L.off_x())[lvc];
         const R4 xt4 = reinterpret_cast<const R4*>(st + L.off_xt())[lvc];
         const R4 y4 = reinterpret_cast<const R4*>(st + L.off_y())[lvc];
-        const long long* so = reinterpret_cast<const long long*>(st + L.off_eoff());
-        const int beg = act ? (int)(so[lv] - h.ebase) : 0;
-        const int end = act ? (int)(so[lv + 1] - h.ebase) : 0;
         const R xi[3] = {xi4.x, xi4.y, xi4.z};
         const R dx[3] = {xi[0] - xt4.x, xi[1] - xt4.y, xi[2] - xt4.z};
         R f[3] = {R(0), R(0), R(0)};
         R H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
         R sv = R(0), dsc = R(0), opd = R(1);
+        bool any = false;  // j = 0: the vertex has at least one entry (position 0)
         constexpr int U = 2;
-        for (int k0 = beg + j; k0 < end; k0 += W * U) {
+        for (int i0 = 0; i0 < rounds; i0 += U) {
             uint2 e[U];
             R4 p[U][3];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int k = k0 + u * W;
-                if (u == 0 || k < end) {
-                    e[u] = sent[k];
+                e[u] = make_uint2(0u, VBD_TILE_PAD << 16);
+                if (u == 0 || i0 + u < rounds) e[u] = sent[32 * (i0 + u)];
+                if ((e[u].y >> 16) != VBD_TILE_PAD) {
                     p[u][0] = np[e[u].x & 0xffffu];
                     p[u][1] = np[e[u].x >> 16];
                     p[u][2] = np[e[u].y & 0xffffu];
@@ -293,8 +382,7 @@ __global__ void __launch_bounds__(288, MINB) k1_tiles(const K1TArgs<R> ta)
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int k = k0 + u * W;
-                if (u == 0 || k < end) {
+                if ((e[u].y >> 16) != VBD_TILE_PAD) {
                     R r[KindRec<R>::HOT];
                     const PL* rp = skind + (e[u].y >> 16) * QH;
 #pragma unroll
@@ -312,6 +400,7 @@ __global__ void __launch_bounds__(288, MINB) k1_tiles(const K1TArgs<R> ta)
                         dsc = r[10];
                         opd = r[11];
                     }
+                    any = true;
                 }
             }
         }
@@ -320,16 +409,18 @@ __global__ void __launch_bounds__(288, MINB) k1_tiles(const K1TArgs<R> ta)
         H[5] = H[5] + sv;
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));  // stage's smem no longer read
+        // the 4 lanes of a vertex are vi, vi+8, vi+16, vi+24: same butterfly order as the
+        // other K1 variants (j ^ 2, then j ^ 1)
 #pragma unroll
-        for (int o = W / 2; o > 0; o >>= 1) {
+        for (int o = 16; o >= 8; o >>= 1) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) f[q] += __shfl_xor_sync(0xffffffffu, f[q], o, W);
+            for (int q = 0; q < 3; ++q) f[q] += __shfl_xor_sync(0xffffffffu, f[q], o);
 #pragma unroll
-            for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(0xffffffffu, H[q], o, W);
+            for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(0xffffffffu, H[q], o);
         }
-        if (act && j == 0) {  // lane 0 of the group processed the vertex's first entry (UM: dsc/opd)
+        if (act && j == 0) {  // j = 0 processed the vertex's first entry (UM: dsc/opd)
             const int v = h.v0 + lv;
-            vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM && end > beg, dsc, opd);
+            vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM && any, dsc, opd);
             R d[3];
             block_solve<R>(f, H, a.eps_det, a.mode, d);
             R4 nx = xi4;
