@@ -288,11 +288,12 @@ __device__ __forceinline__ void block_solve(const R* f, const R* H, R eps_det, i
     const R a5 = fma(H[2], H[1], -mul_rn(H[0], H[4]));
     const R a8 = fma(H[0], H[3], -mul_rn(H[1], H[1]));
     const R det = fma(H[2], a2, fma(H[1], a1, mul_rn(H[0], a0)));
-    const R tr = (H[0] + H[3] + H[5]) / R(3);
+    const R tr = mul_rn((H[0] + H[3] + H[5]), R(1) / R(3));
     if (fabs(det) > mul_rn(mul_rn(mul_rn(eps_det, tr), tr), tr)) {
-        d[0] = fma(a2, f[2], fma(a1, f[1], mul_rn(a0, f[0]))) / det;
-        d[1] = fma(a5, f[2], fma(a4, f[1], mul_rn(a1, f[0]))) / det;
-        d[2] = fma(a8, f[2], fma(a5, f[1], mul_rn(a2, f[0]))) / det;
+        const R inv = R(1) / det;  // one IEEE division per vertex
+        d[0] = mul_rn(fma(a2, f[2], fma(a1, f[1], mul_rn(a0, f[0]))), inv);
+        d[1] = mul_rn(fma(a5, f[2], fma(a4, f[1], mul_rn(a1, f[0]))), inv);
+        d[2] = mul_rn(fma(a8, f[2], fma(a5, f[1], mul_rn(a2, f[0]))), inv);
     }
 }
 
@@ -320,7 +321,7 @@ __device__ __forceinline__ void vertex_terms(R* f, R* H, const R* dx, const R* x
     H[5] = H[5] + mih2;
 }
 
-__device__ __forceinline__ bool finite3(double a, double b, double c)
+template <typename R> __device__ __forceinline__ bool finite3(R a, R b, R c)
 {
     return isfinite(a) && isfinite(b) && isfinite(c);
 }

@@ -169,8 +169,7 @@ struct __align__(16) TileDesc {
     int v0, nv;     // vertices
     int ne;         // entry slots
     int nl;         // distinct neighbours
-    unsigned rw[2]; // rounds of consumer warps 0..7, one byte each
-    int pad[2];
+    int wr[8];      // consumer warp w: rounds | (first slot / 32) << 16
 };
 
 __global__ void k_tile_desc(const int* __restrict__ tv0, const int* __restrict__ tnv,
@@ -186,10 +185,12 @@ __global__ void k_tile_desc(const int* __restrict__ tv0, const int* __restrict__
     d.ne = (int)(sbase[t + 1] - sbase[t]);
     d.l0 = lbase[t];
     d.nl = (int)(lbase[t + 1] - d.l0);
-    d.rw[0] = d.rw[1] = 0;
-    for (int w = 0; w < 8; ++w)
-        d.rw[w >> 2] |= (unsigned)tile_warp_rounds(eoff, d.v0, d.nv, w) << (8 * (w & 3));
-    d.pad[0] = d.pad[1] = 0;
+    int pre = 0;
+    for (int w = 0; w < 8; ++w) {
+        const int r = tile_warp_rounds(eoff, d.v0, d.nv, w);
+        d.wr[w] = r | (pre << 16);
+        pre += r;
+    }
     out[t] = d;
 }
 
@@ -205,8 +206,8 @@ template <typename R> struct K1TArgs {
 };
 
 struct TileHdr {
-    int v0, nv;
-    unsigned rw[2];
+    int v0, nv, pad[2];
+    int wr[8];  // TileDesc::wr
 };
 
 
@@ -249,7 +250,7 @@ template <typename R> struct TileSmem {
     int ent_cap, nbr_cap, nk;
     __host__ __device__ size_t kinds_bytes() const { return (size_t)nk * KindRec<R>::HOT * sizeof(R); }
     __host__ __device__ size_t off_hdr() const { return 0; }
-    __host__ __device__ size_t off_ent() const { return 16; }
+    __host__ __device__ size_t off_ent() const { return 48; }
     __host__ __device__ size_t off_npos() const { return off_ent() + (size_t)ent_cap * 8; }
     __host__ __device__ size_t off_x() const { return off_npos() + (size_t)nbr_cap * sizeof(R4); }
     __host__ __device__ size_t off_xt() const { return off_x() + VBD_TILE_V * sizeof(R4); }
@@ -297,8 +298,8 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
                 TileHdr* h = reinterpret_cast<TileHdr*>(st + L.off_hdr());
                 h->v0 = d.v0;
                 h->nv = d.nv;
-                h->rw[0] = d.rw[0];
-                h->rw[1] = d.rw[1];
+#pragma unroll
+                for (int w = 0; w < 8; ++w) h->wr[w] = d.wr[w];
                 const unsigned eby = (unsigned)d.ne * 8u, vby = (unsigned)(d.nv * sizeof(R4));
                 mbar_expect_tx(bar, eby + 3 * vby);
                 if (eby) bulk_g2s(st + L.off_ent(), ta.tent + d.eb, eby, bar);
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
             R4* np = reinterpret_cast<R4*>(st + L.off_npos());
             // neighbour gathers: the ids of a batch are loaded together, then their copies
             // issued (the cp.async asm is a compiler barrier for loads)
-            constexpr int B = 8;
+            constexpr int B = 16;
             for (int base = 0; base < d.nl; base += 32 * B) {
                 int id[B];
 #pragma unroll
@@ -349,13 +350,12 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
     for (int t = blockIdx.x; t < ta.tcount; t += gridDim.x) {
         mbar_wait_parity(smem_u32(&full[stage]), ph);
         const unsigned char* st = stages + stage * L.stage_bytes();
-        const TileHdr h = *reinterpret_cast<const TileHdr*>(st + L.off_hdr());
-        int sb = 0;
-        for (int w = 0; w < warp; ++w) sb += (int)((h.rw[w >> 2] >> (8 * (w & 3))) & 0xffu);
-        const int rounds = (int)((h.rw[warp >> 2] >> (8 * (warp & 3))) & 0xffu);
+        const TileHdr* hp = reinterpret_cast<const TileHdr*>(st + L.off_hdr());
+        const int hv0 = hp->v0, hnv = hp->nv, wr = hp->wr[warp];
+        const int rounds = wr & 0xffff, sb = wr >> 16;
         const uint2* sent = reinterpret_cast<const uint2*>(st + L.off_ent()) + 32 * sb + lane;
         const R4* np = reinterpret_cast<const R4*>(st + L.off_npos());
-        const bool act = lv < h.nv;
+        const bool act = lv < hnv;
         const int lvc = act ? lv : 0;
         const R4 xi4 = reinterpret_cast<const R4*>(st + L.off_x())[lvc];
         const R4 xt4 = reinterpret_cast<const R4*>(st + L.off_xt())[lvc];
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
             for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(0xffffffffu, H[q], o);
         }
         if (act && j == 0) {  // j = 0 processed the vertex's first entry (UM: dsc/opd)
-            const int v = h.v0 + lv;
+            const int v = hv0 + lv;
             vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM && any, dsc, opd);
             R d[3];
             block_solve<R>(f, H, a.eps_det, a.mode, d);
