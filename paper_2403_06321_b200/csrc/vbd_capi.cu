@@ -164,7 +164,7 @@ struct vbd_ctx {
     std::vector<int> tile_beg;  // first tile of colour c (size ncolors + 1)
     int ent_cap = 0, nbr_cap = 0;
     DBuf tv0, tnv, loff, tnbr, tent, tdesc;
-    int tile_stages = 2;
+    int tile_stages = 2, tile_w = 4;
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -484,15 +484,20 @@ template <typename R> void build_tiles(vbd_ctx* c)
     c->tiles = false;
     const char* e = getenv("VBD_TILES");
     if ((e && *e == '0') || !c->compact || !c->inplace || c->nsolve == 0 || c->nkinds >= 65535) return;
-    if ((long long)VBD_TILE_V * c->max_deg * 3 > VBD_TILE_SORT) return;
+    const char* we = getenv("VBD_TILE_W");
+    const int W = we && *we ? atoi(we) : 4;
+    if (W != 1 && W != 2 && W != 4) fail(VBD_ERR_ARG, "VBD_TILE_W must be 1, 2 or 4");
+    const int VPT = 256 / W;
+    if ((long long)VPT * c->max_deg * 3 > VBD_TILE_SORT) return;
+    c->tile_w = W;
     cudaStream_t s = c->stream;
     std::vector<int> v0, nv;
     c->tile_beg.assign(c->ncolors + 1, 0);
     for (int col = 0; col < c->ncolors; ++col) {
         c->tile_beg[col] = (int)v0.size();
-        for (long long o = 0; o < c->ccnt[col]; o += VBD_TILE_V) {
+        for (long long o = 0; o < c->ccnt[col]; o += VPT) {
             v0.push_back((int)(c->cbeg[col] + o));
-            nv.push_back((int)std::min<long long>(VBD_TILE_V, c->ccnt[col] - o));
+            nv.push_back((int)std::min<long long>(VPT, c->ccnt[col] - o));
         }
     }
     const int nt = (int)v0.size();
@@ -504,8 +509,14 @@ template <typename R> void build_tiles(vbd_ctx* c)
     err.alloc(4);
     CK(cudaMemsetAsync(err.p, 0, 4, s));
     const int4* cent = c->ent.as<int4>();
-    k_tile_nbrs<false><<<nt, 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(), cent,
-                                         cnt.as<long long>(), nullptr, nullptr, nullptr, nullptr, err.as<int>());
+    int P = 256;
+    while (P < VPT * c->max_deg * 3) P <<= 1;
+    const size_t sort_smem = (size_t)P * 4;
+    CK(cudaFuncSetAttribute(k_tile_nbrs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
+    CK(cudaFuncSetAttribute(k_tile_nbrs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
+    k_tile_nbrs<false><<<nt, 256, sort_smem, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
+                                                 cent, cnt.as<long long>(), nullptr, nullptr, nullptr, nullptr, W,
+                                                 0u, 0u, 0u, 0u, err.as<int>());
     CK(cudaGetLastError());
     if (read_scalar<int>(err.p, s)) return;
     std::vector<long long> hc(2 * (size_t)nt), nls(nt), nss(nt);
@@ -517,14 +528,18 @@ template <typename R> void build_tiles(vbd_ctx* c)
         mx = std::max(mx, nls[t]);
         ms = std::max(ms, nss[t]);
     }
-    if (mx > 65535) return;
+    // slots hold 16-bit shared-memory byte offsets (+1 zero position, +1 zero kind record)
+    if ((mx + 1) * (long long)sizeof(typename Vec4<R>::T) > 65535) return;
+    if ((long long)(c->nkinds + 1) * KindRec<R>::HOT * sizeof(R) > 65535) return;
     c->nbr_cap = (int)mx;
     c->ent_cap = (int)ms;
-    TileSmem<R> L{c->ent_cap, c->nbr_cap, c->nkinds};
+    TileSmem<R> L{c->ent_cap, c->nbr_cap, c->nkinds, VPT};
     // as many stages (2..4) as fit two CTAs per SM
     int stages = 0;
     for (int st = 4; st >= 2 && !stages; --st)
         if (L.total(st) <= VBD_TILE_SMEM_MAX) stages = st;
+    for (int st = 3; st >= 2 && !stages; --st)  // else one CTA per SM
+        if (L.total(st) <= 2 * VBD_TILE_SMEM_MAX) stages = st;
     const char* se = getenv("VBD_TILE_STAGES");
     if (se && *se) stages = std::min(stages, atoi(se));
     if (stages < 2) return;
@@ -538,14 +553,18 @@ template <typename R> void build_tiles(vbd_ctx* c)
     const long long slots = read_scalar<long long>(sbase.as<long long>() + nt, s);
     c->tnbr.alloc((size_t)std::max<long long>(total, 1) * 4);
     c->tent.alloc((size_t)std::max<long long>(slots, 1) * 8);
-    k_tile_nbrs<true><<<nt, 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(), cent,
-                                        nullptr, c->loff.as<long long>(), sbase.as<long long>(),
-                                        c->tnbr.as<int>(), c->tent.as<uint2>(), err.as<int>());
+    k_tile_nbrs<true><<<nt, 256, sort_smem, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
+                                                cent, nullptr, c->loff.as<long long>(), sbase.as<long long>(),
+                                                c->tnbr.as<int>(), c->tent.as<uint2>(), W,
+                                                (unsigned)sizeof(typename Vec4<R>::T),
+                                                (unsigned)(c->nbr_cap * sizeof(typename Vec4<R>::T)),
+                                                (unsigned)(KindRec<R>::HOT * sizeof(R)),
+                                                (unsigned)(c->nkinds * KindRec<R>::HOT * sizeof(R)), err.as<int>());
     CK(cudaGetLastError());
     if (read_scalar<int>(err.p, s)) fail(VBD_ERR_INTERNAL, "tile build failed");
     c->tdesc.alloc((size_t)nt * sizeof(TileDesc));
     k_tile_desc<<<blocks_for(nt), 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
-                                              c->loff.as<long long>(), sbase.as<long long>(), nt,
+                                              c->loff.as<long long>(), sbase.as<long long>(), nt, W,
                                               c->tdesc.as<TileDesc>());
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
@@ -805,29 +824,37 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     else k1_color_pass<R, W, U, B, false, false><<<nb, 256, 0, s>>>(a);
 }
 
-template <typename R, bool UM, int S>
+template <typename R, bool UM, int S, int W>
 void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
 {
     static size_t attr = 0;
     static int per_sm = 0, sms = 148;
     if (smem > attr) {
-        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = smem;
         int dev = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, S>, 288, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, S, W>, 288, smem));
         per_sm = std::max(1, per_sm);
     }
     const int grid = std::min(ta.tcount, per_sm * sms);
-    k1_tiles<R, UM, S><<<grid, 288, smem, s>>>(ta);
+    k1_tiles<R, UM, S, W><<<grid, 288, smem, s>>>(ta);
 }
 
-template <typename R, bool UM> void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, size_t smem, cudaStream_t s)
+template <typename R, bool UM, int W>
+void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, size_t smem, cudaStream_t s)
 {
-    if (stages >= 4) launch_k1_tiles_v<R, UM, 4>(ta, smem, s);
-    else if (stages == 3) launch_k1_tiles_v<R, UM, 3>(ta, smem, s);
-    else launch_k1_tiles_v<R, UM, 2>(ta, smem, s);
+    if (stages >= 4) launch_k1_tiles_v<R, UM, 4, W>(ta, smem, s);
+    else if (stages == 3) launch_k1_tiles_v<R, UM, 3, W>(ta, smem, s);
+    else launch_k1_tiles_v<R, UM, 2, W>(ta, smem, s);
+}
+
+template <typename R, bool UM> void launch_k1_tiles_w(const K1TArgs<R>& ta, int W, int stages, size_t smem, cudaStream_t s)
+{
+    if (W == 1) launch_k1_tiles_s<R, UM, 1>(ta, stages, smem, s);
+    else if (W == 2) launch_k1_tiles_s<R, UM, 2>(ta, stages, smem, s);
+    else launch_k1_tiles_s<R, UM, 4>(ta, stages, smem, s);
 }
 
 template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
@@ -848,10 +875,10 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     ta.ent_cap = c->ent_cap;
     ta.nbr_cap = c->nbr_cap;
     ta.nkinds = c->nkinds;
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds};
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds, 256 / c->tile_w};
     const int S = c->tile_stages;
-    if (a.vmat) launch_k1_tiles_s<R, true>(ta, S, L.total(S), s);
-    else launch_k1_tiles_s<R, false>(ta, S, L.total(S), s);
+    if (a.vmat) launch_k1_tiles_w<R, true>(ta, c->tile_w, S, L.total(S), s);
+    else launch_k1_tiles_w<R, false>(ta, c->tile_w, S, L.total(S), s);
     return true;
 }
 

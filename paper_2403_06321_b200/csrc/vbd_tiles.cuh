@@ -1,14 +1,16 @@
 // vbd_tiles.cuh -- K1T: the colour pass as a warp-specialised, TMA-fed tile pipeline.
 //
-// A colour range is cut into tiles of VBD_TILE_V = 64 consecutive vertices (Morton-compact
-// in space).  Each tile carries, built once at pack time:
+// A colour range is cut into tiles of 256 / W consecutive vertices (Morton-compact in space;
+// W = lanes per vertex, 8 consumer warps per tile).  Each tile carries, built once at pack time:
 //   * its sorted list of distinct neighbour vertices (the other-colour positions it reads),
-//   * its entries re-encoded against that list: 8 bytes {u16 n0, u16 n1, u16 n2, u16 kind},
-//     laid out per consumer warp as [round i][lane] slots: lane = 8 j + vi serves entry
-//     position 4 i + j of the warp's vertex vi (padding slots carry kind 0xffff).  A warp's
+//   * its entries re-encoded against that list: 8 bytes of shared-memory byte offsets
+//     {u16 n0, u16 n1, u16 n2, u16 kind}, laid out per consumer warp as [round i][lane] slots:
+//     lane = (32 / W) j + vi serves entry position W i + j of the warp's vertex vi.  Rounds are
+//     padded to even counts; padding slots point at a zero position and a zero kind record,
+//     whose contribution is exactly +0, so the sweep has no validity branches.  A warp's
 //     slot reads are contiguous, and the 8 lanes of a quarter-warp (same position, 8 vertices
 //     of one class) read the same kind record: shared-memory broadcast.
-// K1T is persistent: per CTA one producer warp and 8 consumer warps (4 lanes per vertex).
+// K1T is persistent: per CTA one producer warp and 8 consumer warps (W lanes per vertex).
 // The producer fills a ring of shared-memory stages for tile t + grid: one elected lane
 // issues cp.async.bulk (TMA) copies of the tile's entry range and of x / x_t / y of its 64
 // vertices, all 32 lanes gather the neighbour positions (and CSR offsets) with cp.async,
@@ -20,27 +22,27 @@
 #pragma once
 #include "vbd_kernels.cuh"
 
-#define VBD_TILE_V 64
-#define VBD_TILE_SORT 8192  // max neighbour references (3 per entry) per tile for the build
+#define VBD_TILE_SORT 32768  // max neighbour references (3 per entry) per tile for the build
 
 // ---------------------------------------------------------------------------------------
 // build: one CTA (256 threads) per tile.  FILL = false: count distinct neighbours;
 // FILL = true: write the sorted list at loff[t] and the 8-byte tile entries.
 
-#define VBD_TILE_PAD 0xffffu
+#define VBD_TILE_U 2  // rounds per consumer loop iteration (slot counts padded to it)
 
-// rounds (entry slots per lane) of consumer warp w of a tile: max over its 8 vertices of
-// ceil(degree / 4)
-__device__ __forceinline__ int tile_warp_rounds(const long long* __restrict__ eoff, int v0, int nv, int w)
+// rounds (entry slots per lane) of consumer warp w of a tile: max over its 32 / W vertices
+// of ceil(degree / W)
+__device__ __forceinline__ int tile_warp_rounds(const long long* __restrict__ eoff, int v0, int nv, int w, int W)
 {
+    const int vpw = 32 / W;
     int r = 0;
-    for (int vi = 0; vi < 8; ++vi) {
-        const int lv = 8 * w + vi;
+    for (int vi = 0; vi < vpw; ++vi) {
+        const int lv = vpw * w + vi;
         if (lv >= nv) break;
         const int d = (int)(eoff[v0 + lv + 1] - eoff[v0 + lv]);
-        r = max(r, (d + 3) / 4);
+        r = max(r, (d + W - 1) / W);
     }
-    return r;
+    return (r + VBD_TILE_U - 1) / VBD_TILE_U * VBD_TILE_U;
 }
 
 // build: one CTA (256 threads) per tile.  FILL = false: count distinct neighbours (cnt[2t])
@@ -52,9 +54,10 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
                                                    const int4* __restrict__ cent, long long* cnt,
                                                    const long long* __restrict__ lbase,
                                                    const long long* __restrict__ sbase, int* __restrict__ tnbr,
-                                                   uint2* __restrict__ tent, int* err)
+                                                   uint2* __restrict__ tent, int W, unsigned r4b,
+                                                   unsigned pad_pos, unsigned kstride, unsigned pad_kind, int* err)
 {
-    __shared__ int keys[VBD_TILE_SORT];
+    extern __shared__ int keys[];  // next power of two >= max references per tile
     __shared__ int part[257];
     __shared__ int wslot[9];
     const int t = blockIdx.x, tid = threadIdx.x;
@@ -69,7 +72,7 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
         int sb = 0;
         for (int w = 0; w < 8; ++w) {
             wslot[w] = sb;
-            sb += 32 * tile_warp_rounds(eoff, v0, nv, w);
+            sb += 32 * tile_warp_rounds(eoff, v0, nv, w, W);
         }
         wslot[8] = sb;
     }
@@ -137,8 +140,9 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
         while (sl >= wslot[w + 1]) ++w;
         const int rel = sl - wslot[w];
         const int lane = rel & 31, i = rel >> 5;
-        const int lv = 8 * w + (lane & 7), pos = 4 * i + (lane >> 3);
-        uint2 out = make_uint2(0u, VBD_TILE_PAD << 16);
+        const int vpw = 32 / W;
+        const int lv = vpw * w + lane % vpw, pos = W * i + lane / vpw;
+        uint2 out = make_uint2(pad_pos | (pad_pos << 16), pad_pos | (pad_kind << 16));
         if (lv < nv) {
             const long long k = eoff[v0 + lv] + pos;
             if (k < eoff[v0 + lv + 1]) {
@@ -153,9 +157,9 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
                         if (lst[mid] < ids[r]) lo = mid + 1;
                         else hi = mid;
                     }
-                    loc[r] = (unsigned)lo;
+                    loc[r] = (unsigned)lo * r4b;  // byte offset into the stage's positions
                 }
-                out = make_uint2(loc[0] | (loc[1] << 16), loc[2] | ((unsigned)e.w << 16));
+                out = make_uint2(loc[0] | (loc[1] << 16), loc[2] | (((unsigned)e.w * kstride) << 16));
             }
         }
         tent[s0 + sl] = out;
@@ -174,7 +178,7 @@ struct __align__(16) TileDesc {
 
 __global__ void k_tile_desc(const int* __restrict__ tv0, const int* __restrict__ tnv,
                             const long long* __restrict__ eoff, const long long* __restrict__ lbase,
-                            const long long* __restrict__ sbase, int nt, TileDesc* __restrict__ out)
+                            const long long* __restrict__ sbase, int nt, int W, TileDesc* __restrict__ out)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nt) return;
@@ -187,7 +191,7 @@ __global__ void k_tile_desc(const int* __restrict__ tv0, const int* __restrict__
     d.nl = (int)(lbase[t + 1] - d.l0);
     int pre = 0;
     for (int w = 0; w < 8; ++w) {
-        const int r = tile_warp_rounds(eoff, d.v0, d.nv, w);
+        const int r = tile_warp_rounds(eoff, d.v0, d.nv, w, W);
         d.wr[w] = r | (pre << 16);
         pre += r;
     }
@@ -247,33 +251,36 @@ __device__ __forceinline__ void cp_async_mbar_arrive(unsigned bar)
 // positions | x | x_t | y
 template <typename R> struct TileSmem {
     typedef typename Vec4<R>::T R4;
-    int ent_cap, nbr_cap, nk;
-    __host__ __device__ size_t kinds_bytes() const { return (size_t)nk * KindRec<R>::HOT * sizeof(R); }
+    int ent_cap, nbr_cap, nk, vpt;  // vpt: vertices per tile
+    __host__ __device__ size_t kinds_bytes() const { return (size_t)(nk + 1) * KindRec<R>::HOT * sizeof(R); }
     __host__ __device__ size_t off_hdr() const { return 0; }
     __host__ __device__ size_t off_ent() const { return 48; }
     __host__ __device__ size_t off_npos() const { return off_ent() + (size_t)ent_cap * 8; }
-    __host__ __device__ size_t off_x() const { return off_npos() + (size_t)nbr_cap * sizeof(R4); }
-    __host__ __device__ size_t off_xt() const { return off_x() + VBD_TILE_V * sizeof(R4); }
-    __host__ __device__ size_t off_y() const { return off_xt() + VBD_TILE_V * sizeof(R4); }
-    __host__ __device__ size_t stage_bytes() const { return (off_y() + VBD_TILE_V * sizeof(R4) + 127) & ~(size_t)127; }
+    __host__ __device__ size_t off_x() const { return off_npos() + (size_t)(nbr_cap + 1) * sizeof(R4); }
+    __host__ __device__ size_t off_xt() const { return off_x() + vpt * sizeof(R4); }
+    __host__ __device__ size_t off_y() const { return off_xt() + vpt * sizeof(R4); }
+    __host__ __device__ size_t stage_bytes() const { return (off_y() + vpt * sizeof(R4) + 127) & ~(size_t)127; }
     __host__ __device__ size_t total(int stages) const { return ((kinds_bytes() + 127) & ~(size_t)127) + stages * stage_bytes(); }
 };
 
-template <typename R, bool UM, int S>
+template <typename R, bool UM, int S, int W>
 __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
 {
     typedef typename Vec4<R>::T R4;
-    constexpr int W = 4;
+    constexpr int VPW = 32 / W;  // vertices per consumer warp
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long full[S], empty[S];
     const K1Args<R>& a = ta.a;
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds};
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds, 8 * VPW};
     typedef typename PlaneT<R>::T PL;
     PL* skind = reinterpret_cast<PL*>(smem);
     unsigned char* stages = smem + ((L.kinds_bytes() + 127) & ~(size_t)127);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int QH = KindRec<R>::QH, Q = KindRec<R>::Q;
     for (int i = tid; i < ta.nkinds * QH; i += blockDim.x) skind[i] = ta.kinds[(i / QH) * Q + i % QH];
+    for (int i = tid; i < QH; i += blockDim.x) skind[ta.nkinds * QH + i] = PL{};  // padding: zero record
+    for (int s = 0; s < S; ++s)  // padding: zero position after the largest neighbour list
+        if (tid == 0) *reinterpret_cast<R4*>(stages + s * L.stage_bytes() + L.off_npos() + ta.nbr_cap * sizeof(R4)) = R4{};
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(smem_u32(&full[s]), 33);  // expect_tx arrive + 32 cp.async arrivals
@@ -341,10 +348,10 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
         return;
     }
 
-    // ---------------- consumers: warp w handles tile vertices 8w .. 8w+7; lane = 8 j + vi
-    // serves entry positions j, j + 4, ... of vertex vi
-    const int vi = lane & 7, j = lane >> 3;
-    const int lv = warp * 8 + vi;
+    // ---------------- consumers: warp w handles tile vertices VPW w .. VPW w + VPW - 1;
+    // lane = VPW j + vi serves entry positions j, j + W, ... of vertex vi
+    const int vi = lane % VPW, j = lane / VPW;
+    const int lv = warp * VPW + vi;
     int stage = 0;
     unsigned ph = 0;
     for (int t = blockIdx.x; t < ta.tcount; t += gridDim.x) {
@@ -365,42 +372,37 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
         R f[3] = {R(0), R(0), R(0)};
         R H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
         R sv = R(0), dsc = R(0), opd = R(1);
-        bool any = false;  // j = 0: the vertex has at least one entry (position 0)
-        constexpr int U = 2;
-        for (int i0 = 0; i0 < rounds; i0 += U) {
+        constexpr int U = VBD_TILE_U;
+        const unsigned char* npb = reinterpret_cast<const unsigned char*>(np);
+        const unsigned char* kb = reinterpret_cast<const unsigned char*>(skind);
+        for (int i0 = 0; i0 < rounds; i0 += U) {  // rounds is a multiple of U
             uint2 e[U];
             R4 p[U][3];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                e[u] = make_uint2(0u, VBD_TILE_PAD << 16);
-                if (u == 0 || i0 + u < rounds) e[u] = sent[32 * (i0 + u)];
-                if ((e[u].y >> 16) != VBD_TILE_PAD) {
-                    p[u][0] = np[e[u].x & 0xffffu];
-                    p[u][1] = np[e[u].x >> 16];
-                    p[u][2] = np[e[u].y & 0xffffu];
-                }
+                e[u] = sent[32 * (i0 + u)];
+                p[u][0] = *reinterpret_cast<const R4*>(npb + (e[u].x & 0xffffu));
+                p[u][1] = *reinterpret_cast<const R4*>(npb + (e[u].x >> 16));
+                p[u][2] = *reinterpret_cast<const R4*>(npb + (e[u].y & 0xffffu));
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                if ((e[u].y >> 16) != VBD_TILE_PAD) {
-                    R r[KindRec<R>::HOT];
-                    const PL* rp = skind + (e[u].y >> 16) * QH;
+                R r[KindRec<R>::HOT];
+                const PL* rp = reinterpret_cast<const PL*>(kb + (e[u].y >> 16));
 #pragma unroll
-                    for (int q = 0; q < QH; ++q) {
-                        const PL v = rp[q];
-                        const R* vr = reinterpret_cast<const R*>(&v);
+                for (int q = 0; q < QH; ++q) {
+                    const PL v = rp[q];
+                    const R* vr = reinterpret_cast<const R*>(&v);
 #pragma unroll
-                        for (int z = 0; z < 16 / (int)sizeof(R); ++z) r[q * (16 / (int)sizeof(R)) + z] = vr[z];
-                    }
-                    const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
-                    const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
-                    const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
-                    tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], r[11], dx, f, H, sv);
-                    if (UM) {
-                        dsc = r[10];
-                        opd = r[11];
-                    }
-                    any = true;
+                    for (int z = 0; z < 16 / (int)sizeof(R); ++z) r[q * (16 / (int)sizeof(R)) + z] = vr[z];
+                }
+                const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
+                const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
+                const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
+                tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], r[11], dx, f, H, sv);
+                if (UM && i0 + u == 0) {  // position j: lane j = 0 holds the vertex's first entry
+                    dsc = r[10];
+                    opd = r[11];
                 }
             }
         }
@@ -409,10 +411,10 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
         H[5] = H[5] + sv;
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));  // stage's smem no longer read
-        // the 4 lanes of a vertex are vi, vi+8, vi+16, vi+24: same butterfly order as the
-        // other K1 variants (j ^ 2, then j ^ 1)
+        // the W lanes of a vertex are vi + VPW j: same butterfly order as the other K1
+        // variants with W lanes (j ^ W/2 first, ..., j ^ 1 last)
 #pragma unroll
-        for (int o = 16; o >= 8; o >>= 1) {
+        for (int o = 16; o >= VPW; o >>= 1) {
 #pragma unroll
             for (int q = 0; q < 3; ++q) f[q] += __shfl_xor_sync(0xffffffffu, f[q], o);
 #pragma unroll
@@ -420,7 +422,7 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
         }
         if (act && j == 0) {  // j = 0 processed the vertex's first entry (UM: dsc/opd)
             const int v = hv0 + lv;
-            vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM && any, dsc, opd);
+            vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM, dsc, opd);  // no entries: dsc = opd = 0, H = 0
             R d[3];
             block_solve<R>(f, H, a.eps_det, a.mode, d);
             R4 nx = xi4;
