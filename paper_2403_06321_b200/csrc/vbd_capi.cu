@@ -477,7 +477,7 @@ template <typename R> void refresh_kinds(vbd_ctx* c)
 // K1T tiles (vbd_tiles.cuh): 64 consecutive vertices of one colour, the sorted distinct
 // neighbours they read and their entries re-encoded against that list.  Needs the compact
 // layout, a valid colouring (in-place sweeps) and shared memory for two stages.
-constexpr size_t VBD_TILE_SMEM_MAX = 110 * 1024;  // two CTAs per SM
+constexpr size_t VBD_TILE_SMEM_MAX = 112 * 1024;  // two CTAs per SM
 
 template <typename R> void build_tiles(vbd_ctx* c)
 {

@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
     }
 }
 
-// per-tile descriptor: one 32-byte load for the producer
+// per-tile descriptor (64 B): the producer loads the first 32 B; the whole record is
+// bulk-copied into the stage header for the consumers
 struct __align__(16) TileDesc {
     long long eb;   // first entry slot (tiles are 256-byte aligned in the slot array)
     long long l0;   // neighbour list base
@@ -174,6 +175,10 @@ struct __align__(16) TileDesc {
     int ne;         // entry slots
     int nl;         // distinct neighbours
     int wr[8];      // consumer warp w: rounds | (first slot / 32) << 16
+};
+struct __align__(16) TileDescHead {
+    long long eb, l0;
+    int v0, nv, ne, nl;
 };
 
 __global__ void k_tile_desc(const int* __restrict__ tv0, const int* __restrict__ tnv,
@@ -209,10 +214,7 @@ template <typename R> struct K1TArgs {
     int nkinds;
 };
 
-struct TileHdr {
-    int v0, nv, pad[2];
-    int wr[8];  // TileDesc::wr
-};
+typedef TileDesc TileHdr;  // the stage header is a copy of the tile's descriptor
 
 
 
@@ -254,7 +256,7 @@ template <typename R> struct TileSmem {
     int ent_cap, nbr_cap, nk, vpt;  // vpt: vertices per tile
     __host__ __device__ size_t kinds_bytes() const { return (size_t)(nk + 1) * KindRec<R>::HOT * sizeof(R); }
     __host__ __device__ size_t off_hdr() const { return 0; }
-    __host__ __device__ size_t off_ent() const { return 48; }
+    __host__ __device__ size_t off_ent() const { return sizeof(TileDesc); }
     __host__ __device__ size_t off_npos() const { return off_ent() + (size_t)ent_cap * 8; }
     __host__ __device__ size_t off_x() const { return off_npos() + (size_t)(nbr_cap + 1) * sizeof(R4); }
     __host__ __device__ size_t off_xt() const { return off_x() + vpt * sizeof(R4); }
@@ -291,54 +293,67 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
     __syncthreads();
 
     if (warp == 8) {  // ---------------- producer
+        // software-pipelined two tiles deep: while tile t is issued, the neighbour ids of
+        // tile t + grid and the descriptor of tile t + 2 grid are in flight
+        constexpr int B = 16;
+        const TileDescHead* dh = reinterpret_cast<const TileDescHead*>(ta.desc) + 0;
+        auto head = [&](int t) {
+            TileDescHead h{};
+            if (t < ta.tcount) h = *reinterpret_cast<const TileDescHead*>(ta.desc + ta.tbeg + t);
+            return h;
+        };
+        (void)dh;
+        int idsA[B], idsB[B];
+        auto load_ids = [&](const TileDescHead& dd, int base, int* ids) {
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                const int i = base + q * 32 + lane;
+                ids[q] = i < dd.nl ? __ldg(ta.tnbr + dd.l0 + i) : -1;
+            }
+        };
+        const int g = (int)gridDim.x;
+        TileDescHead dA = head(blockIdx.x), dB = head(blockIdx.x + g);
+        load_ids(dA, 0, idsA);
         int stage = 0;
         unsigned ph = 0;
-        TileDesc dn;
-        if (blockIdx.x < ta.tcount) dn = ta.desc[ta.tbeg + blockIdx.x];
-        for (int t = blockIdx.x; t < ta.tcount; t += gridDim.x) {
-            const TileDesc d = dn;
-            if (t + gridDim.x < ta.tcount) dn = ta.desc[ta.tbeg + t + gridDim.x];  // overlaps the wait
+        for (int t = blockIdx.x; t < ta.tcount; t += g) {
+            load_ids(dB, 0, idsB);  // tile t + g (its descriptor arrived an iteration ago)
+            const TileDescHead dC = head(t + 2 * g);
             mbar_wait_parity(smem_u32(&empty[stage]), ph ^ 1);
             unsigned char* st = stages + stage * L.stage_bytes();
             const unsigned bar = smem_u32(&full[stage]);
             if (lane == 0) {
-                TileHdr* h = reinterpret_cast<TileHdr*>(st + L.off_hdr());
-                h->v0 = d.v0;
-                h->nv = d.nv;
-#pragma unroll
-                for (int w = 0; w < 8; ++w) h->wr[w] = d.wr[w];
-                const unsigned eby = (unsigned)d.ne * 8u, vby = (unsigned)(d.nv * sizeof(R4));
-                mbar_expect_tx(bar, eby + 3 * vby);
-                if (eby) bulk_g2s(st + L.off_ent(), ta.tent + d.eb, eby, bar);
-                bulk_g2s(st + L.off_x(), a.pos + d.v0, vby, bar);
-                bulk_g2s(st + L.off_xt(), a.xt + d.v0, vby, bar);
-                bulk_g2s(st + L.off_y(), a.y + d.v0, vby, bar);
+                const unsigned eby = (unsigned)dA.ne * 8u, vby = (unsigned)(dA.nv * sizeof(R4));
+                mbar_expect_tx(bar, (unsigned)sizeof(TileDesc) + eby + 3 * vby);
+                bulk_g2s(st + L.off_hdr(), ta.desc + ta.tbeg + t, (unsigned)sizeof(TileDesc), bar);
+                if (eby) bulk_g2s(st + L.off_ent(), ta.tent + dA.eb, eby, bar);
+                bulk_g2s(st + L.off_x(), a.pos + dA.v0, vby, bar);
+                bulk_g2s(st + L.off_xt(), a.xt + dA.v0, vby, bar);
+                bulk_g2s(st + L.off_y(), a.y + dA.v0, vby, bar);
             }
             R4* np = reinterpret_cast<R4*>(st + L.off_npos());
-            // neighbour gathers: the ids of a batch are loaded together, then their copies
-            // issued (the cp.async asm is a compiler barrier for loads)
-            constexpr int B = 16;
-            for (int base = 0; base < d.nl; base += 32 * B) {
-                int id[B];
+            for (int base = 0;;) {
 #pragma unroll
                 for (int q = 0; q < B; ++q) {
-                    const int i = base + q * 32 + lane;
-                    id[q] = i < d.nl ? __ldg(ta.tnbr + d.l0 + i) : -1;
-                }
-#pragma unroll
-                for (int q = 0; q < B; ++q) {
-                    if (id[q] < 0) continue;
+                    if (idsA[q] < 0) continue;
                     const int i = base + q * 32 + lane;
                     if constexpr (sizeof(R4) == 16) {
-                        cp_async_n<16>(np + i, a.pos + id[q]);
+                        cp_async_n<16>(np + i, a.pos + idsA[q]);
                     } else {
-                        cp_async_n<16>(reinterpret_cast<char*>(np + i), reinterpret_cast<const char*>(a.pos + id[q]));
+                        cp_async_n<16>(reinterpret_cast<char*>(np + i), reinterpret_cast<const char*>(a.pos + idsA[q]));
                         cp_async_n<16>(reinterpret_cast<char*>(np + i) + 16,
-                                       reinterpret_cast<const char*>(a.pos + id[q]) + 16);
+                                       reinterpret_cast<const char*>(a.pos + idsA[q]) + 16);
                     }
                 }
+                base += 32 * B;
+                if (base >= dA.nl) break;
+                load_ids(dA, base, idsA);  // rare: more than 32 B neighbours
             }
             cp_async_mbar_arrive(bar);
+            dA = dB;
+            dB = dC;
+#pragma unroll
+            for (int q = 0; q < B; ++q) idsA[q] = idsB[q];
             if (++stage == S) {
                 stage = 0;
                 ph ^= 1;
