@@ -628,10 +628,10 @@ __global__ void k_kind_records(const unsigned* __restrict__ keys, int nk, const 
     }
     const Material<R> m = mats[key[KW - 1]];
     R r[KindRec<R>::NR];
-    ec_terms<R>(w, V, m.mu, m.lam, r);
-    r[9] = m.gamma;
-    r[10] = m.dsc;
-    r[11] = m.opd;
+    ec_terms<R>(w, V, m.mu, m.lam, m.gamma, r);
+    r[9] = m.dsc;
+    r[10] = m.opd;
+    r[11] = m.gamma;
     for (int j = 0; j < 9; ++j) r[12 + j] = w[j];
     r[21] = V;
     r[22] = m.mu;

@@ -148,75 +148,76 @@ template <typename R> __device__ __forceinline__ void cross3(const R* a, const R
     c[2] = fma(a[0], b[1], -mul_rn(a[1], b[0]));
 }
 
-// t[0..2] = V mu s, t[3..5] = q, t[6] = det W, t[7] = V lam, t[8] = V mu |w|^2
+// With r = sqrt(V lam) folded into q, det W and gamma, the Hessian block is (r C w)(r C w)^T
+// and the force term r (J - gamma) (r C w): per entry kind
+//   t[0..2] = V mu s,  t[3..5] = r q,  t[6] = r det W,  t[7] = r gamma,  t[8] = V mu |w|^2
 template <typename R>
-__device__ __forceinline__ void ec_terms(const R* __restrict__ w, R V, R mu, R lam, R* __restrict__ t)
+__device__ __forceinline__ void ec_terms(const R* __restrict__ w, R V, R mu, R lam, R gamma, R* __restrict__ t)
 {
     R wo[3];
 #pragma unroll
     for (int b = 0; b < 3; ++b) wo[b] = -((w[b] + w[3 + b]) + w[6 + b]);  // own row
     const R vmu = mul_rn(V, mu);
+    const R r = sqrt(mul_rn(V, lam));
 #pragma unroll
     for (int j = 0; j < 3; ++j) t[j] = mul_rn(vmu, dot3(w + 3 * j, wo));
     R c[3];
     cross3(w + 3, w + 6, c);
-    t[3] = dot3(c, wo);
-    t[6] = dot3(w, c);
+    t[3] = mul_rn(r, dot3(c, wo));
+    t[6] = mul_rn(r, dot3(w, c));
     cross3(w + 6, w, c);
-    t[4] = dot3(c, wo);
+    t[4] = mul_rn(r, dot3(c, wo));
     cross3(w, w + 3, c);
-    t[5] = dot3(c, wo);
-    t[7] = mul_rn(V, lam);
+    t[5] = mul_rn(r, dot3(c, wo));
+    t[7] = mul_rn(r, gamma);
     t[8] = mul_rn(vmu, dot3(wo, wo));
 }
 
 // DAMP = false: one material per vertex -- the undamped block is accumulated (H and the
 // scalar sum sv of V mu |w|^2) and the caller applies damping once per vertex.
+// ~53 FP instructions per entry (the F-form needs ~130).
 template <typename R, bool DAMP>
 __device__ __forceinline__ void tet_contrib_ec(const R* __restrict__ e0, const R* __restrict__ e1,
-                                               const R* __restrict__ e2, const R* __restrict__ t, R gamma,
-                                               R dsc, R opd, const R* __restrict__ dx, R* __restrict__ f,
+                                               const R* __restrict__ e2, const R* __restrict__ t, R dsc, R opd,
+                                               const R* __restrict__ dx, R* __restrict__ f,
                                                R* __restrict__ H, R& sv)
 {
-    R fr[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) fr[a] = fma(t[2], e2[a], fma(t[1], e1[a], mul_rn(t[0], e0[a])));  // V mu F w
     R u[3], c[3], k[3], cw[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) u[a] = fma(t[3], e1[a], -mul_rn(t[4], e0[a]));
     cross3(e0, e1, c);
     cross3(u, e2, k);
 #pragma unroll
-    for (int a = 0; a < 3; ++a) cw[a] = fma(t[5], c[a], k[a]);  // C w
-    const R J = mul_rn(dot3(e2, c), t[6]);
-    const R vc = mul_rn(t[7], J - gamma);  // V lam (J - gamma)
-    R tv[3];
+    for (int a = 0; a < 3; ++a) cw[a] = fma(t[5], c[a], k[a]);  // r C w
+    const R vc = fma(t[6], dot3(e2, c), -t[7]);                  // r (J - gamma)
+    R g[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) tv[a] = mul_rn(t[7], cw[a]);
+    for (int a = 0; a < 3; ++a)  // V (mu F w + lam (J - gamma) C w)
+        g[a] = fma(vc, cw[a], fma(t[2], e2[a], fma(t[1], e1[a], mul_rn(t[0], e0[a]))));
     if (DAMP) {
         R he[6];
-        he[0] = fma(tv[0], cw[0], t[8]);
-        he[1] = mul_rn(tv[0], cw[1]);
-        he[2] = mul_rn(tv[0], cw[2]);
-        he[3] = fma(tv[1], cw[1], t[8]);
-        he[4] = mul_rn(tv[1], cw[2]);
-        he[5] = fma(tv[2], cw[2], t[8]);
+        he[0] = fma(cw[0], cw[0], t[8]);
+        he[1] = mul_rn(cw[0], cw[1]);
+        he[2] = mul_rn(cw[0], cw[2]);
+        he[3] = fma(cw[1], cw[1], t[8]);
+        he[4] = mul_rn(cw[1], cw[2]);
+        he[5] = fma(cw[2], cw[2], t[8]);
         const R hd[3] = {fma(he[2], dx[2], fma(he[1], dx[1], mul_rn(he[0], dx[0]))),
                          fma(he[4], dx[2], fma(he[3], dx[1], mul_rn(he[1], dx[0]))),
                          fma(he[5], dx[2], fma(he[4], dx[1], mul_rn(he[2], dx[0])))};
 #pragma unroll
-        for (int a = 0; a < 3; ++a) f[a] = f[a] - fma(dsc, hd[a], fma(vc, cw[a], fr[a]));
+        for (int a = 0; a < 3; ++a) f[a] = f[a] - fma(dsc, hd[a], g[a]);
 #pragma unroll
         for (int q = 0; q < 6; ++q) H[q] = fma(opd, he[q], H[q]);
     } else {
 #pragma unroll
-        for (int a = 0; a < 3; ++a) f[a] = f[a] - fma(vc, cw[a], fr[a]);
-        H[0] = fma(tv[0], cw[0], H[0]);
-        H[1] = fma(tv[0], cw[1], H[1]);
-        H[2] = fma(tv[0], cw[2], H[2]);
-        H[3] = fma(tv[1], cw[1], H[3]);
-        H[4] = fma(tv[1], cw[2], H[4]);
-        H[5] = fma(tv[2], cw[2], H[5]);
+        for (int a = 0; a < 3; ++a) f[a] = f[a] - g[a];
+        H[0] = fma(cw[0], cw[0], H[0]);
+        H[1] = fma(cw[0], cw[1], H[1]);
+        H[2] = fma(cw[0], cw[2], H[2]);
+        H[3] = fma(cw[1], cw[1], H[3]);
+        H[4] = fma(cw[1], cw[2], H[4]);
+        H[5] = fma(cw[2], cw[2], H[5]);
         sv = sv + t[8];
     }
 }
@@ -226,7 +227,7 @@ __device__ __forceinline__ void tet_contrib_ec(const R* __restrict__ e0, const R
 // per-kind constants live in a small table (L1/L2-resident).  Lossless: kinds are
 // deduplicated on the exact bits of the explicit entry (rows, volume, material), and both
 // layouts derive the constants with ec_terms, so they produce bitwise identical results.
-// Record (24 R): [0..8] ec_terms, [9] gamma, [10] dsc, [11] opd  (the sweep reads these 12)
+// Record (24 R): [0..8] ec_terms, [9] dsc, [10] opd, [11] gamma  (the sweep reads these 12)
 //                [12..20] w0..w8, [21] V, [22] mu, [23] lam     (local energy / line search)
 template <typename R> struct KindRec {
     static constexpr int NR = 24;

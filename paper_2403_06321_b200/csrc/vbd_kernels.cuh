@@ -67,7 +67,7 @@ __device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int 
 #pragma unroll
             for (int j = 0; j < 9; ++j) en.w[j] = r[12 + j];
             en.V = r[21];
-            mu = r[22]; lam = r[23]; gamma = r[9];
+            mu = r[22]; lam = r[23]; gamma = r[11];
         } else {
             en = Entry<R>::load(a.ent, a.E, k);
             const Material<R> m = a.mat[en.mat];
@@ -137,8 +137,8 @@ __device__ __forceinline__ void k1_accumulate_explicit(const K1Args<R>& a, long 
                 const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
                 const Material<R> m = UM ? mv : a.mat[e[u].mat];
                 R t[9];
-                ec_terms<R>(e[u].w, e[u].V, m.mu, m.lam, t);
-                tet_contrib_ec<R, !UM>(e0, e1, e2, t, m.gamma, m.dsc, m.opd, dx, f, H, sv);
+                ec_terms<R>(e[u].w, e[u].V, m.mu, m.lam, m.gamma, t);
+                tet_contrib_ec<R, !UM>(e0, e1, e2, t, m.dsc, m.opd, dx, f, H, sv);
             }
         }
     }
@@ -192,10 +192,10 @@ __device__ __forceinline__ void k1_accumulate_compact(const K1Args<R>& a, long l
                 const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
                 const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
                 const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
-                tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], r[11], dx, f, H, sv);
+                tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], dx, f, H, sv);
                 if (UM) {
-                    dsc = r[10];
-                    opd = r[11];
+                    dsc = r[9];
+                    opd = r[10];
                 }
             }
         }

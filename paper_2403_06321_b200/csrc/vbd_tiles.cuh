@@ -293,17 +293,15 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
     __syncthreads();
 
     if (warp == 8) {  // ---------------- producer
-        // software-pipelined two tiles deep: while tile t is issued, the neighbour ids of
-        // tile t + grid and the descriptor of tile t + 2 grid are in flight
+        // Software-pipelined, unrolled by two with named buffers (no register copies that would
+        // expose load latency): while tile t is issued, the neighbour ids of tile t + grid and
+        // the descriptor of tile t + 2 grid are in flight.
         constexpr int B = 16;
-        const TileDescHead* dh = reinterpret_cast<const TileDescHead*>(ta.desc) + 0;
         auto head = [&](int t) {
             TileDescHead h{};
             if (t < ta.tcount) h = *reinterpret_cast<const TileDescHead*>(ta.desc + ta.tbeg + t);
             return h;
         };
-        (void)dh;
-        int idsA[B], idsB[B];
         auto load_ids = [&](const TileDescHead& dd, int base, int* ids) {
 #pragma unroll
             for (int q = 0; q < B; ++q) {
@@ -311,53 +309,59 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
                 ids[q] = i < dd.nl ? __ldg(ta.tnbr + dd.l0 + i) : -1;
             }
         };
-        const int g = (int)gridDim.x;
-        TileDescHead dA = head(blockIdx.x), dB = head(blockIdx.x + g);
-        load_ids(dA, 0, idsA);
         int stage = 0;
         unsigned ph = 0;
-        for (int t = blockIdx.x; t < ta.tcount; t += g) {
-            load_ids(dB, 0, idsB);  // tile t + g (its descriptor arrived an iteration ago)
-            const TileDescHead dC = head(t + 2 * g);
+        auto issue = [&](int t, const TileDescHead& d, int* ids) {
             mbar_wait_parity(smem_u32(&empty[stage]), ph ^ 1);
             unsigned char* st = stages + stage * L.stage_bytes();
             const unsigned bar = smem_u32(&full[stage]);
             if (lane == 0) {
-                const unsigned eby = (unsigned)dA.ne * 8u, vby = (unsigned)(dA.nv * sizeof(R4));
+                const unsigned eby = (unsigned)d.ne * 8u, vby = (unsigned)(d.nv * sizeof(R4));
                 mbar_expect_tx(bar, (unsigned)sizeof(TileDesc) + eby + 3 * vby);
                 bulk_g2s(st + L.off_hdr(), ta.desc + ta.tbeg + t, (unsigned)sizeof(TileDesc), bar);
-                if (eby) bulk_g2s(st + L.off_ent(), ta.tent + dA.eb, eby, bar);
-                bulk_g2s(st + L.off_x(), a.pos + dA.v0, vby, bar);
-                bulk_g2s(st + L.off_xt(), a.xt + dA.v0, vby, bar);
-                bulk_g2s(st + L.off_y(), a.y + dA.v0, vby, bar);
+                if (eby) bulk_g2s(st + L.off_ent(), ta.tent + d.eb, eby, bar);
+                bulk_g2s(st + L.off_x(), a.pos + d.v0, vby, bar);
+                bulk_g2s(st + L.off_xt(), a.xt + d.v0, vby, bar);
+                bulk_g2s(st + L.off_y(), a.y + d.v0, vby, bar);
             }
             R4* np = reinterpret_cast<R4*>(st + L.off_npos());
             for (int base = 0;;) {
 #pragma unroll
                 for (int q = 0; q < B; ++q) {
-                    if (idsA[q] < 0) continue;
+                    if (ids[q] < 0) continue;
                     const int i = base + q * 32 + lane;
                     if constexpr (sizeof(R4) == 16) {
-                        cp_async_n<16>(np + i, a.pos + idsA[q]);
+                        cp_async_n<16>(np + i, a.pos + ids[q]);
                     } else {
-                        cp_async_n<16>(reinterpret_cast<char*>(np + i), reinterpret_cast<const char*>(a.pos + idsA[q]));
+                        cp_async_n<16>(reinterpret_cast<char*>(np + i), reinterpret_cast<const char*>(a.pos + ids[q]));
                         cp_async_n<16>(reinterpret_cast<char*>(np + i) + 16,
-                                       reinterpret_cast<const char*>(a.pos + idsA[q]) + 16);
+                                       reinterpret_cast<const char*>(a.pos + ids[q]) + 16);
                     }
                 }
                 base += 32 * B;
-                if (base >= dA.nl) break;
-                load_ids(dA, base, idsA);  // rare: more than 32 B neighbours
+                if (base >= d.nl) break;
+                load_ids(d, base, ids);  // rare: more than 32 B neighbours
             }
             cp_async_mbar_arrive(bar);
-            dA = dB;
-            dB = dC;
-#pragma unroll
-            for (int q = 0; q < B; ++q) idsA[q] = idsB[q];
             if (++stage == S) {
                 stage = 0;
                 ph ^= 1;
             }
+        };
+        const int g = (int)gridDim.x;
+        TileDescHead d0 = head(blockIdx.x), d1 = head(blockIdx.x + g);
+        int i0[B], i1[B];
+        load_ids(d0, 0, i0);
+        for (int t = blockIdx.x; t < ta.tcount; t += 2 * g) {
+            load_ids(d1, 0, i1);                       // tile t + g
+            const TileDescHead d0n = head(t + 2 * g);  // tile t + 2g
+            issue(t, d0, i0);
+            if (t + g >= ta.tcount) break;
+            load_ids(d0n, 0, i0);                      // tile t + 2g
+            const TileDescHead d1n = head(t + 3 * g);  // tile t + 3g
+            issue(t + g, d1, i1);
+            d0 = d0n;
+            d1 = d1n;
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         return;
@@ -414,10 +418,10 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
                 const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
                 const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
                 const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
-                tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], r[11], dx, f, H, sv);
+                tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], dx, f, H, sv);
                 if (UM && i0 + u == 0) {  // position j: lane j = 0 holds the vertex's first entry
-                    dsc = r[10];
-                    opd = r[11];
+                    dsc = r[9];
+                    opd = r[10];
                 }
             }
         }
