@@ -117,8 +117,12 @@ typedef struct {
                                   a table of distinct entry kinds; lossless) */
     int32_t entry_bytes;       /* bytes streamed per (vertex, tet) entry */
     int64_t num_entry_kinds;   /* compact layout: distinct (rows, volume, material) keys */
-    int32_t tiles;             /* K1T tile pipeline: number of 64-vertex tiles (0 = off) */
+    int32_t tiles;             /* K1T tile pipeline: number of tiles (0 = off) */
     int32_t tile_nbr_cap;      /* max distinct neighbours of one tile */
+    int64_t tile_slots;        /* K1T: 8-byte entry slots over all tiles (entries + padding) */
+    int64_t tile_nbr_refs;     /* K1T: neighbour-list entries over all tiles */
+    int32_t tile_lanes;        /* K1T: lanes per vertex */
+    int32_t tile_stages;       /* K1T: shared-memory pipeline stages */
 } vbd_ctx_info;
 
 /* ---- context ---------------------------------------------------------------------------- */

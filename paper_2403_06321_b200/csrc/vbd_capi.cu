@@ -1602,6 +1602,10 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         info->num_entry_kinds = c->nkinds;
         info->tiles = c->tiles ? (int)(c->tile_beg.back()) : 0;
         info->tile_nbr_cap = c->nbr_cap;
+        info->tile_slots = c->tiles ? c->tent.bytes / 8 : 0;
+        info->tile_nbr_refs = c->tiles ? c->tnbr.bytes / 4 : 0;
+        info->tile_lanes = c->tiles ? c->tile_w : 0;
+        info->tile_stages = c->tiles ? c->tile_stages : 0;
         info->entry_bytes = c->compact ? 16 : EntryPlanesBytes(c->precision);
     });
 }
