@@ -164,7 +164,7 @@ struct vbd_ctx {
     std::vector<int> tile_beg;  // first tile of colour c (size ncolors + 1)
     int ent_cap = 0, nbr_cap = 0;
     DBuf tv0, tnv, loff, tnbr, tent, tdesc;
-    int tile_stages = 2, tile_w = 4;
+    int tile_stages = 2, tile_w = 4, tile_occ = 2;
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -486,7 +486,7 @@ template <typename R> void build_tiles(vbd_ctx* c)
     if ((e && *e == '0') || !c->compact || !c->inplace || c->nsolve == 0 || c->nkinds >= 65535) return;
     const char* we = getenv("VBD_TILE_W");
     const int W = we && *we ? atoi(we) : 4;
-    if (W != 1 && W != 2 && W != 4) fail(VBD_ERR_ARG, "VBD_TILE_W must be 1, 2 or 4");
+    if (W != 4) fail(VBD_ERR_ARG, "VBD_TILE_W: only 4 lanes per vertex are compiled");
     const int VPT = 256 / W;
     if ((long long)VPT * c->max_deg * 3 > VBD_TILE_SORT) return;
     c->tile_w = W;
@@ -535,10 +535,13 @@ template <typename R> void build_tiles(vbd_ctx* c)
     c->ent_cap = (int)ms;
     TileSmem<R> L{c->ent_cap, c->nbr_cap, c->nkinds, VPT};
     // as many stages (2..4) as fit two CTAs per SM
+    const char* oe = getenv("VBD_TILE_OCC");
+    c->tile_occ = oe && *oe == '2' ? 2 : 3;  // 3 CTAs per SM (one entry per lane in flight) measured faster
+    const size_t cap = c->tile_occ == 3 ? 75 * 1024 : VBD_TILE_SMEM_MAX;
     int stages = 0;
     for (int st = 4; st >= 2 && !stages; --st)
-        if (L.total(st) <= VBD_TILE_SMEM_MAX) stages = st;
-    for (int st = 3; st >= 2 && !stages; --st)  // else one CTA per SM
+        if (L.total(st) <= cap) stages = st;
+    for (int st = 3; st >= 2 && !stages && c->tile_occ == 2; --st)  // else one CTA per SM
         if (L.total(st) <= 2 * VBD_TILE_SMEM_MAX) stages = st;
     const char* se = getenv("VBD_TILE_STAGES");
     if (se && *se) stages = std::min(stages, atoi(se));
@@ -824,37 +827,44 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     else k1_color_pass<R, W, U, B, false, false><<<nb, 256, 0, s>>>(a);
 }
 
-template <typename R, bool UM, int S, int W>
+template <typename R, bool UM, int S, int W, int OCC>
 void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
 {
     static size_t attr = 0;
     static int per_sm = 0, sms = 148;
     if (smem > attr) {
-        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = smem;
         int dev = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, S, W>, 288, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, S, W, OCC>, 288, smem));
         per_sm = std::max(1, per_sm);
     }
     const int grid = std::min(ta.tcount, per_sm * sms);
-    k1_tiles<R, UM, S, W><<<grid, 288, smem, s>>>(ta);
+    k1_tiles<R, UM, S, W, OCC><<<grid, 288, smem, s>>>(ta);
 }
 
 template <typename R, bool UM, int W>
-void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, size_t smem, cudaStream_t s)
+void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, int occ, size_t smem, cudaStream_t s)
 {
-    if (stages >= 4) launch_k1_tiles_v<R, UM, 4, W>(ta, smem, s);
-    else if (stages == 3) launch_k1_tiles_v<R, UM, 3, W>(ta, smem, s);
-    else launch_k1_tiles_v<R, UM, 2, W>(ta, smem, s);
+    if (occ == 3) {
+        if (stages >= 3) launch_k1_tiles_v<R, UM, 3, W, 3>(ta, smem, s);
+        else launch_k1_tiles_v<R, UM, 2, W, 3>(ta, smem, s);
+        return;
+    }
+    if (stages >= 4) launch_k1_tiles_v<R, UM, 4, W, 2>(ta, smem, s);
+    else if (stages == 3) launch_k1_tiles_v<R, UM, 3, W, 2>(ta, smem, s);
+    else launch_k1_tiles_v<R, UM, 2, W, 2>(ta, smem, s);
 }
 
-template <typename R, bool UM> void launch_k1_tiles_w(const K1TArgs<R>& ta, int W, int stages, size_t smem, cudaStream_t s)
+template <typename R, bool UM>
+void launch_k1_tiles_w(const K1TArgs<R>& ta, int W, int stages, int occ, size_t smem, cudaStream_t s)
 {
-    if (W == 1) launch_k1_tiles_s<R, UM, 1>(ta, stages, smem, s);
-    else if (W == 2) launch_k1_tiles_s<R, UM, 2>(ta, stages, smem, s);
-    else launch_k1_tiles_s<R, UM, 4>(ta, stages, smem, s);
+    // 4 lanes per vertex (1 and 2 were measured slower); the kernel and the
+    // tile build stay generic in W
+    (void)W;
+    launch_k1_tiles_s<R, UM, 4>(ta, stages, occ, smem, s);
 }
 
 template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
@@ -877,8 +887,8 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     ta.nkinds = c->nkinds;
     const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds, 256 / c->tile_w};
     const int S = c->tile_stages;
-    if (a.vmat) launch_k1_tiles_w<R, true>(ta, c->tile_w, S, L.total(S), s);
-    else launch_k1_tiles_w<R, false>(ta, c->tile_w, S, L.total(S), s);
+    if (a.vmat) launch_k1_tiles_w<R, true>(ta, c->tile_w, S, c->tile_occ, L.total(S), s);
+    else launch_k1_tiles_w<R, false>(ta, c->tile_w, S, c->tile_occ, L.total(S), s);
     return true;
 }
 

@@ -265,8 +265,32 @@ template <typename R> struct TileSmem {
     __host__ __device__ size_t total(int stages) const { return ((kinds_bytes() + 127) & ~(size_t)127) + stages * stage_bytes(); }
 };
 
-template <typename R, bool UM, int S, int W>
-__global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
+// 32-bit shared-window loads (one add per address instead of generic-pointer arithmetic);
+// volatile keeps them after the stage's mbarrier wait
+__device__ __forceinline__ void lds_v(unsigned a, float4& v)
+{
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+}
+__device__ __forceinline__ void lds_v(unsigned a, double4& v)
+{
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.z), "=d"(v.w) : "r"(a + 16));
+}
+__device__ __forceinline__ void lds_v(unsigned a, double2& v)
+{
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+}
+__device__ __forceinline__ uint2 lds_u2(unsigned a)
+{
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+
+// OCC = CTAs per SM the kernel is compiled for (register budget); OCC >= 3 sweeps one entry
+// per lane at a time (fewer live registers), else two.
+template <typename R, bool UM, int S, int W, int OCC>
+__global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
 {
     typedef typename Vec4<R>::T R4;
     constexpr int VPW = 32 / W;  // vertices per consumer warp
@@ -391,26 +415,28 @@ __global__ void __launch_bounds__(288, 2) k1_tiles(const K1TArgs<R> ta)
         R f[3] = {R(0), R(0), R(0)};
         R H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
         R sv = R(0), dsc = R(0), opd = R(1);
-        constexpr int U = VBD_TILE_U;
-        const unsigned char* npb = reinterpret_cast<const unsigned char*>(np);
-        const unsigned char* kb = reinterpret_cast<const unsigned char*>(skind);
+        constexpr int U = OCC >= 3 ? 1 : VBD_TILE_U;
+        const unsigned npb = smem_u32(np);
+        const unsigned kb = smem_u32(skind);
+        const unsigned sb32 = smem_u32(sent);
         for (int i0 = 0; i0 < rounds; i0 += U) {  // rounds is a multiple of U
             uint2 e[U];
             R4 p[U][3];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                e[u] = sent[32 * (i0 + u)];
-                p[u][0] = *reinterpret_cast<const R4*>(npb + (e[u].x & 0xffffu));
-                p[u][1] = *reinterpret_cast<const R4*>(npb + (e[u].x >> 16));
-                p[u][2] = *reinterpret_cast<const R4*>(npb + (e[u].y & 0xffffu));
+                e[u] = lds_u2(sb32 + 256u * (unsigned)(i0 + u));
+                lds_v(npb + (e[u].x & 0xffffu), p[u][0]);
+                lds_v(npb + (e[u].x >> 16), p[u][1]);
+                lds_v(npb + (e[u].y & 0xffffu), p[u][2]);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 R r[KindRec<R>::HOT];
-                const PL* rp = reinterpret_cast<const PL*>(kb + (e[u].y >> 16));
+                const unsigned rp = kb + (e[u].y >> 16);
 #pragma unroll
                 for (int q = 0; q < QH; ++q) {
-                    const PL v = rp[q];
+                    PL v;
+                    lds_v(rp + 16u * q, v);
                     const R* vr = reinterpret_cast<const R*>(&v);
 #pragma unroll
                     for (int z = 0; z < 16 / (int)sizeof(R); ++z) r[q * (16 / (int)sizeof(R)) + z] = vr[z];
