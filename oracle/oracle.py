@@ -39,6 +39,7 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 FIXED = 1
+SUBSPACE = 2
 
 # harness.py:30-33 -- 5-tet split of a hex cell, alternated by cell parity.
 _CELL_EVEN = ((0, 3, 5, 6), (1, 0, 3, 5), (2, 0, 3, 6), (4, 0, 5, 6), (7, 3, 5, 6))
@@ -65,6 +66,9 @@ def lib():
     L.oracle_color_pass.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
                                     f64, P, i64, c_int, c_int, f64, c_int]
     L.oracle_color_pass.restype = c_int
+    L.oracle_color_pass_ex.argtypes = ([i64, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
+                                        f64, P, i64, c_int, c_int, f64, c_int] + [P] * 12)
+    L.oracle_color_pass_ex.restype = c_int
     L.oracle_local_energy.argtypes = [P, P, P, P, P, P, P, P, P, P, f64, i64, P]
     L.oracle_local_energy.restype = f64
     L.oracle_greedy_color.argtypes = [i64, P, P, P, P]
@@ -247,6 +251,41 @@ class System:
     color_verts: np.ndarray
     kind: np.ndarray
     body_slices: tuple = ()
+    # springs (_system.py:117-123) and constraints (_system.py:76-83); empty by default
+    springs: np.ndarray = None
+    sp_l0: np.ndarray = None
+    sp_k: np.ndarray = None
+    sp_kd: np.ndarray = None
+    s_off: np.ndarray = None
+    s_id: np.ndarray = None
+    s_slot: np.ndarray = None
+    sub_dim: np.ndarray = None
+    sub_basis: np.ndarray = None
+    sub_anchor: np.ndarray = None
+    box_k: np.ndarray = None
+    box_lo: np.ndarray = None
+    box_hi: np.ndarray = None
+
+    def __post_init__(self):
+        n = self.num_vertices
+        if self.springs is None:
+            self.springs = np.zeros((0, 2), dtype=np.int64)
+            self.sp_l0 = self.sp_k = self.sp_kd = np.zeros(0)
+            self.s_off = np.zeros(n + 1, dtype=np.int64)
+            self.s_id = np.zeros(0, dtype=np.int64)
+            self.s_slot = np.zeros(0, dtype=np.int64)
+        if self.sub_dim is None:
+            self.sub_dim = np.zeros(n, dtype=np.int64)
+            self.sub_basis = np.zeros((n, 3, 2))
+            self.sub_anchor = np.zeros((n, 3))
+        if self.box_k is None:
+            self.box_k = np.zeros(n)
+            self.box_lo = np.zeros((n, 3))
+            self.box_hi = np.zeros((n, 3))
+
+    @property
+    def has_extras(self):
+        return bool(len(self.springs) or (self.kind == SUBSPACE).any() or (self.box_k > 0).any())
 
     @property
     def num_colors(self):
@@ -263,6 +302,66 @@ def slot_weight_rows(inv):
     w[:, 1:, :] = inv
     w[:, 0, :] = -inv.sum(axis=1)
     return w
+
+
+def build_system_ex(tet_bodies, spring_bodies=(), fixed=(), subspace=(), boxes=()):
+    """_system.py:204-303 with spring nets and constraints (compile_constraints,
+    _system.py:172-201).  tet_bodies: (Mesh, (mu, lam, kd)); spring_bodies:
+    (particles (P,3), masses (P,), indices (S,2), rest_length (S,), stiffness (S,), kd);
+    fixed: vertex ids; subspace: (vertex, basis (3,L), anchor (3,)); boxes:
+    (vertex, lo (3,), hi (3,), k_b).  Vertices are numbered tet bodies first, then
+    spring bodies, in the given order (as Body order in the reference)."""
+    base = build_system(tet_bodies, fixed=()) if tet_bodies else None
+    n_t = base.num_vertices if base else 0
+    pos = [base.rest_positions] if base else []
+    mass = [base.masses] if base else []
+    sp, l0, k, kd = [], [], [], []
+    off = n_t
+    for parts, masses, idx, rest, stiff, damp in spring_bodies:
+        pos.append(np.asarray(parts, dtype=np.float64))
+        mass.append(np.asarray(masses, dtype=np.float64))
+        sp.append(np.asarray(idx, dtype=np.int64) + off)
+        l0.append(np.asarray(rest, dtype=np.float64))
+        k.append(np.asarray(stiff, dtype=np.float64))
+        kd.append(np.full(len(idx), float(damp)))
+        off += len(parts)
+    N = off
+    cat = lambda parts, shape, dt=np.float64: (np.ascontiguousarray(np.concatenate(parts).astype(dt))
+                                               if parts else np.zeros(shape, dtype=dt))
+    springs = cat(sp, (0, 2), np.int64)
+    tets = base.tets if base else np.zeros((0, 4), dtype=np.int64)
+    t_off, t_id, t_slot = incidence_from_elements(tets, N)
+    s_off, s_id, s_slot = incidence_from_elements(springs, N)
+    noff, nids = merged_adjacency(N, [tets, springs])
+    col, groups = greedy_color(noff, nids)
+    color_off = np.zeros(len(groups) + 1, dtype=np.int64)
+    np.cumsum([len(g) for g in groups], out=color_off[1:])
+    kind = np.zeros(N, dtype=np.uint8)
+    sub_dim = np.zeros(N, dtype=np.int64)
+    sub_basis = np.zeros((N, 3, 2))
+    sub_anchor = np.zeros((N, 3))
+    box_k, box_lo, box_hi = np.zeros(N), np.zeros((N, 3)), np.zeros((N, 3))
+    for v in fixed:
+        kind[int(v)] = FIXED
+    for v, basis, anchor in subspace:
+        b = np.asarray(basis, dtype=np.float64).reshape(3, -1)
+        if kind[v] == FIXED:
+            continue
+        kind[v] = SUBSPACE
+        sub_dim[v] = b.shape[1]
+        sub_basis[v, :, :b.shape[1]] = b
+        sub_anchor[v] = anchor
+    for v, lo, hi, kb in boxes:
+        box_k[v], box_lo[v], box_hi[v] = kb, lo, hi
+    z = lambda shape: np.zeros(shape)
+    return System(N, cat(mass, (0,)), cat(pos, (0, 3)), tets,
+                  base.tet_w if base else z((0, 4, 3)), base.tet_vol if base else z(0),
+                  base.tet_mu if base else z(0), base.tet_lam if base else z(0),
+                  base.tet_kd if base else z(0), t_off, t_id, t_slot, col, color_off,
+                  np.ascontiguousarray(np.concatenate(groups)) if groups else np.zeros(0, np.int64),
+                  kind, base.body_slices if base else (), springs, cat(l0, (0,)), cat(k, (0,)),
+                  cat(kd, (0,)), s_off, s_id, s_slot, sub_dim, sub_basis, sub_anchor,
+                  box_k, box_lo, box_hi)
 
 
 def build_system(bodies, fixed=()):
@@ -306,6 +405,17 @@ def color_pass(system, x, x_t, y, h, group, mode=0, line_search=False, eps_det=1
         raise TypeError("x must be C-contiguous float64")
     g = np.ascontiguousarray(group, dtype=np.int64)
     s = system
+    if s.has_extras:
+        rc = lib().oracle_color_pass_ex(
+            s.num_vertices, _p(x), _p(np.ascontiguousarray(x_t)), _p(np.ascontiguousarray(y)),
+            _p(s.masses), _p(s.tets), _p(s.tet_w), _p(s.tet_vol), _p(s.tet_mu), _p(s.tet_lam),
+            _p(s.tet_kd), _p(s.t_off), _p(s.t_id), _p(s.t_slot), _p(s.kind), float(h), _p(g),
+            len(g), int(mode), int(bool(line_search)), float(eps_det), int(n_threads),
+            _p(s.springs), _p(s.sp_l0), _p(s.sp_k), _p(s.sp_kd), _p(s.s_off), _p(s.s_id),
+            _p(s.s_slot), _p(s.sub_dim), _p(s.sub_basis), _p(s.box_k), _p(s.box_lo), _p(s.box_hi))
+        if rc != 0:
+            raise MemoryError("oracle colour pass failed")
+        return
     rc = lib().oracle_color_pass(
         s.num_vertices, _p(x), _p(np.ascontiguousarray(x_t)), _p(np.ascontiguousarray(y)),
         _p(s.masses), _p(s.tets), _p(s.tet_w), _p(s.tet_vol), _p(s.tet_mu), _p(s.tet_lam),
@@ -353,21 +463,16 @@ class RefSystemView:
         self.t_off, self.t_id, self.t_slot = s.t_off, s.t_id, s.t_slot
         self.color_off, self.color_verts = s.color_off, s.color_verts
         self.rest_positions = s.rest_positions
-        self.springs = np.zeros((0, 2), dtype=np.int64)
-        self.sp_l0 = self.sp_k = self.sp_kd = np.zeros(0)
-        self.s_off = np.zeros(n + 1, dtype=np.int64)
-        self.s_id, self.s_slot = z, z.copy()
+        self.springs, self.sp_l0, self.sp_k, self.sp_kd = s.springs, s.sp_l0, s.sp_k, s.sp_kd
+        self.s_off, self.s_id, self.s_slot = s.s_off, s.s_id, s.s_slot
+        del z
 
         class _Cons:
             pass
         c = _Cons()
         c.kind = s.kind
-        c.sub_dim = np.zeros(n, dtype=np.int64)
-        c.sub_basis = np.zeros((n, 3, 2))
-        c.sub_anchor = np.zeros((n, 3))
-        c.box_k = np.zeros(n)
-        c.box_lo = np.zeros((n, 3))
-        c.box_hi = np.zeros((n, 3))
+        c.sub_dim, c.sub_basis, c.sub_anchor = s.sub_dim, s.sub_basis, s.sub_anchor
+        c.box_k, c.box_lo, c.box_hi = s.box_k, s.box_lo, s.box_hi
         self.cons = c
         self.carr = _EmptyContacts(n)
 
@@ -409,7 +514,7 @@ def make_state(system, x0=None, v0=None):
 
 
 def initialize(system, st, h, a_ext, init_mode="adaptive"):
-    """solver.py:125-164 (no subspace constraints)."""
+    """solver.py:125-164."""
     a = np.asarray(a_ext, dtype=np.float64)
     st.y = inertia_target(st.x_t, st.v_t, a, h)
     if init_mode == "prev_pos":
@@ -429,6 +534,11 @@ def initialize(system, st, h, a_ext, init_mode="adaptive"):
             x = st.x_t + h * st.v_t + (h * h) * a_tilde[:, None] * a
     fixed = system.kind == FIXED
     x[fixed] = st.x_t[fixed]
+    for i in np.flatnonzero(system.kind == SUBSPACE):  # solver.py:158-162
+        dim = system.sub_dim[i]
+        b = system.sub_basis[i][:, :dim]
+        anchor = system.sub_anchor[i]
+        x[i] = anchor + b @ (b.T @ (x[i] - anchor))
     st.x = np.ascontiguousarray(x)
     return st.x
 

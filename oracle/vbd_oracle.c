@@ -3,17 +3,19 @@
  * never called by the product path).  Only tests/, __graft_entry__.smoke() and
  * bench.py's cpu_baseline / --impl reference leg may load this library.
  *
- * Plain-C fp64 restatement of the reference VBD colour pass for the hot-path
- * subset (tets + fixed vertices, mode 0 block-Newton, mode 1 diagonal GD,
- * optional 17-trial local line search), written so that its floating-point
+ * Plain-C fp64 restatement of the reference VBD colour pass without contacts
+ * (tets, springs, fixed / subspace / world-box constraints, mode 0 block-Newton,
+ * mode 1 diagonal GD, optional 17-trial local line search), written so that its floating-point
  * operation order is the reference's, hence bit-identical to the reference's
  * compiled kernel when built without FP contraction:
  *
  *   _tet_fc          <- /root/reference/pkg/src/vbdsim/_native.pyx:175-198
- *   _local_energy    <- _native.pyx:201-258 (tet + inertia terms)
- *   _assemble        <- _native.pyx:261-317 (inertia + SNH tets + damping)
- *   _solve_vertex    <- _native.pyx:412-494 (fixed skip, mode 1, adjugate
- *                       solve with relative det guard, line search)
+ *   _local_energy    <- _native.pyx:201-258 (inertia, tet, spring, box terms)
+ *   _assemble        <- _native.pyx:261-317 (inertia + SNH tets + damping),
+ *                       319-349 (springs), 401-409 (world box)
+ *   _solve_vertex    <- _native.pyx:412-494 (fixed skip, mode 1, subspace
+ *                       1D/2D solve, adjugate solve with relative det guard,
+ *                       line search)
  *   color_pass       <- _native.pyx:513-589 (aux buffer + serial merge)
  *   greedy_color     <- /root/reference/pkg/src/vbdsim/mesh.py:270-302
  *   beam connectivity<- /root/reference/pkg/src/vbdsim/harness.py:28-67
@@ -36,6 +38,7 @@ typedef double f64;
 typedef int64_t i64;
 
 #define KIND_FIXED 1
+#define KIND_SUBSPACE 2
 
 typedef struct {
     const f64 *x, *xt, *y, *masses;
@@ -45,6 +48,11 @@ typedef struct {
     const uint8_t *kind;
     f64 h, eps_det;
     int mode, line_search;
+    /* springs (_system.py:117-123) and constraints (_system.py:76-83); NULL = none */
+    const i64 *springs, *s_off, *s_id, *s_slot;
+    const f64 *sp_l0, *sp_k, *sp_kd;
+    const i64 *sub_dim;
+    const f64 *sub_basis, *box_k, *box_lo, *box_hi;
 } osys;
 
 /* F = sum_k x_k w_k^T with vertex i at p; cofactor; det by column-0 expansion
@@ -89,6 +97,30 @@ static f64 local_energy(const osys *s, i64 i, const f64 *p)
         f64 psi = ((0.5 * mu) * (ic - 3.0)) + (((0.5 * lam) * (J - g)) * (J - g));
         e = e + s->tet_vol[t] * psi;
     }
+    if (s->springs)
+        for (i64 kk = s->s_off[i]; kk < s->s_off[i + 1]; ++kk) {
+            i64 sp = s->s_id[kk];
+            i64 oth = s->springs[sp * 2 + (1 - s->s_slot[kk])];
+            f64 length = 0.0, d;
+            for (int a = 0; a < 3; ++a) {
+                d = p[a] - s->x[oth * 3 + a];
+                length = length + d * d;
+            }
+            length = sqrt(length);
+            if (length < 1e-12 * s->sp_l0[sp])
+                e = e + ((0.5 * s->sp_k[sp]) * s->sp_l0[sp]) * s->sp_l0[sp];
+            else {
+                d = length - s->sp_l0[sp];
+                e = e + ((0.5 * s->sp_k[sp]) * d) * d;
+            }
+        }
+    if (s->box_k && s->box_k[i] > 0.0)
+        for (int a = 0; a < 3; ++a) {
+            f64 d = s->box_lo[i * 3 + a] - p[a];
+            if (d > 0.0) e = e + ((0.5 * s->box_k[i]) * d) * d;
+            d = p[a] - s->box_hi[i * 3 + a];
+            if (d > 0.0) e = e + ((0.5 * s->box_k[i]) * d) * d;
+        }
     return e;
 }
 
@@ -136,9 +168,52 @@ static void assemble(const osys *s, i64 i, f64 *f, f64 *H)
         for (int a = 0; a < 3; ++a)
             for (int b = 0; b < 3; ++b) H[a * 3 + b] = H[a * 3 + b] + (1.0 + dsc) * He[a * 3 + b];
     }
+    if (s->springs) /* _native.pyx:319-349 */
+        for (i64 kk = s->s_off[i]; kk < s->s_off[i + 1]; ++kk) {
+            i64 sp = s->s_id[kk];
+            i64 oth = s->springs[sp * 2 + (1 - s->s_slot[kk])];
+            f64 dvec[3], length = 0.0;
+            for (int a = 0; a < 3; ++a) {
+                dvec[a] = s->x[i * 3 + a] - s->x[oth * 3 + a];
+                length = length + dvec[a] * dvec[a];
+            }
+            length = sqrt(length);
+            f64 k = s->sp_k[sp], l0 = s->sp_l0[sp];
+            if (length < 1e-12 * l0) {
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b) He[a * 3 + b] = (a == b) ? k : 0.0;
+            } else {
+                for (int a = 0; a < 3; ++a) dvec[a] = dvec[a] / length;
+                f64 coef = 1.0 - l0 / length;
+                for (int a = 0; a < 3; ++a) {
+                    f[a] = f[a] - (k * (length - l0)) * dvec[a];
+                    for (int b = 0; b < 3; ++b)
+                        He[a * 3 + b] = k * (dvec[a] * dvec[b] + coef * (((a == b) ? 1.0 : 0.0) - dvec[a] * dvec[b]));
+                }
+            }
+            f64 dsc = s->sp_kd[sp] / s->h;
+            for (int a = 0; a < 3; ++a) {
+                f64 tmp = 0.0;
+                for (int b = 0; b < 3; ++b) tmp = tmp + He[a * 3 + b] * (s->x[i * 3 + b] - s->xt[i * 3 + b]);
+                f[a] = f[a] - dsc * tmp;
+            }
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) H[a * 3 + b] = H[a * 3 + b] + (1.0 + dsc) * He[a * 3 + b];
+        }
+    if (s->box_k && s->box_k[i] > 0.0) /* _native.pyx:401-409 */
+        for (int a = 0; a < 3; ++a) {
+            f64 tmp = s->x[i * 3 + a];
+            if (tmp < s->box_lo[i * 3 + a]) {
+                f[a] = f[a] - s->box_k[i] * (tmp - s->box_lo[i * 3 + a]);
+                H[a * 4] = H[a * 4] + s->box_k[i];
+            } else if (tmp > s->box_hi[i * 3 + a]) {
+                f[a] = f[a] - s->box_k[i] * (tmp - s->box_hi[i * 3 + a]);
+                H[a * 4] = H[a * 4] + s->box_k[i];
+            }
+        }
 }
 
-/* one vertex solve into out[3], _native.pyx:412-494 (no subspace kind). */
+/* one vertex solve into out[3], _native.pyx:412-494. */
 static void solve_vertex(const osys *s, i64 i, f64 *out)
 {
     f64 f[3], H[9], d[3] = {0.0, 0.0, 0.0}, adj[9];
@@ -148,6 +223,38 @@ static void solve_vertex(const osys *s, i64 i, f64 *out)
     if (s->mode == 1) {
         for (int a = 0; a < 3; ++a)
             if (H[a * 3 + a] != 0.0) d[a] = f[a] / H[a * 3 + a];
+    } else if (s->kind && s->kind[i] == KIND_SUBSPACE) { /* _native.pyx:435-463 */
+        const f64 *B = &s->sub_basis[i * 6];
+        i64 dim = s->sub_dim[i];
+        f64 rhs[2], amat[4], det, tr, q0, q1;
+        for (int a = 0; a < dim; ++a) {
+            rhs[a] = 0.0;
+            for (int k = 0; k < 3; ++k) rhs[a] = rhs[a] + B[k * 2 + a] * f[k];
+            for (int b = 0; b < dim; ++b) {
+                amat[a * 2 + b] = 0.0;
+                for (int k = 0; k < 3; ++k) {
+                    q0 = 0.0;
+                    for (int t = 0; t < 3; ++t) q0 = q0 + H[k * 3 + t] * B[t * 2 + b];
+                    amat[a * 2 + b] = amat[a * 2 + b] + B[k * 2 + a] * q0;
+                }
+            }
+        }
+        if (dim == 1) {
+            det = amat[0];
+            tr = amat[0];
+            if (fabs(det) > s->eps_det * fabs(tr)) {
+                q0 = rhs[0] / amat[0];
+                for (int a = 0; a < 3; ++a) d[a] = B[a * 2] * q0;
+            }
+        } else {
+            det = amat[0] * amat[3] - amat[1] * amat[2];
+            tr = 0.5 * (amat[0] + amat[3]);
+            if (fabs(det) > (s->eps_det * tr) * tr) {
+                q0 = (amat[3] * rhs[0] - amat[1] * rhs[1]) / det;
+                q1 = (amat[0] * rhs[1] - amat[2] * rhs[0]) / det;
+                for (int a = 0; a < 3; ++a) d[a] = B[a * 2] * q0 + B[a * 2 + 1] * q1;
+            }
+        }
     } else {
         adj[0] = H[4] * H[8] - H[5] * H[7];
         adj[1] = H[2] * H[7] - H[1] * H[8];
@@ -190,8 +297,46 @@ int oracle_color_pass(i64 n_vertices, f64 *x, const f64 *xt, const f64 *y, const
 {
     (void)n_vertices;
     if (ng <= 0) return 0;
+    osys s;
+    memset(&s, 0, sizeof s);
+    s.x = x; s.xt = xt; s.y = y; s.masses = masses; s.tets = tets; s.tet_w = tet_w;
+    s.tet_vol = tet_vol; s.tet_mu = tet_mu; s.tet_lam = tet_lam; s.tet_kd = tet_kd;
+    s.t_off = t_off; s.t_id = t_id; s.t_slot = t_slot; s.kind = kind; s.h = h;
+    s.eps_det = eps_det; s.mode = mode; s.line_search = line_search;
+    f64 *out = (f64 *)malloc((size_t)ng * 3 * sizeof(f64));
+    if (!out) return -1;
+#ifdef _OPENMP
+    int nt = n_threads > 0 ? n_threads : omp_get_max_threads();
+#pragma omp parallel for schedule(static) num_threads(nt)
+#endif
+    for (i64 k = 0; k < ng; ++k) solve_vertex(&s, group[k], &out[k * 3]);
+    for (i64 k = 0; k < ng; ++k) {
+        i64 v = group[k];
+        x[v * 3 + 0] = out[k * 3 + 0];
+        x[v * 3 + 1] = out[k * 3 + 1];
+        x[v * 3 + 2] = out[k * 3 + 2];
+    }
+    free(out);
+    (void)n_threads;
+    return 0;
+}
+
+/* The same pass with springs and constraints (any pointer may be NULL). */
+int oracle_color_pass_ex(i64 n_vertices, f64 *x, const f64 *xt, const f64 *y, const f64 *masses,
+                         const i64 *tets, const f64 *tet_w, const f64 *tet_vol, const f64 *tet_mu,
+                         const f64 *tet_lam, const f64 *tet_kd, const i64 *t_off, const i64 *t_id,
+                         const i64 *t_slot, const uint8_t *kind, f64 h, const i64 *group, i64 ng,
+                         int mode, int line_search, f64 eps_det, int n_threads,
+                         const i64 *springs, const f64 *sp_l0, const f64 *sp_k, const f64 *sp_kd,
+                         const i64 *s_off, const i64 *s_id, const i64 *s_slot, const i64 *sub_dim,
+                         const f64 *sub_basis, const f64 *box_k, const f64 *box_lo, const f64 *box_hi)
+{
+    (void)n_vertices;
+    if (ng <= 0) return 0;
     osys s = {x, xt, y, masses, tets, tet_w, tet_vol, tet_mu, tet_lam, tet_kd,
-              t_off, t_id, t_slot, kind, h, eps_det, mode, line_search};
+              t_off, t_id, t_slot, kind, h, eps_det, mode, line_search,
+              springs, s_off, s_id, s_slot, sp_l0, sp_k, sp_kd, sub_dim, sub_basis,
+              box_k, box_lo, box_hi};
     f64 *out = (f64 *)malloc((size_t)ng * 3 * sizeof(f64));
     if (!out) return -1;
 #ifdef _OPENMP

@@ -159,8 +159,86 @@ def step_fixtures():
     save("steps_extreme_cube6.npz", x0=x0, x=np.array(xs))
 
 
+def extras_scene():
+    """A beam + a spring cloth + a spring chain, with fixed, subspace and world-box
+    constraints: the non-tet terms of _assemble / _solve_vertex (_native.pyx:319-349,
+    401-409, 435-463) and _local_energy (:226-257)."""
+    from vbdsim import SubspaceConstraint, WorldBoxConstraint, build_spring_net, generate_chain
+    m = generate_beam(7, 3, 3, 0.05, density=1000.0)
+    P = 5
+    xs_, ys_ = np.meshgrid(np.arange(P), np.arange(P), indexing="ij")
+    parts = np.stack([0.5 + 0.05 * xs_.ravel(), 0.05 * ys_.ravel(), np.full(P * P, 0.2)], 1)
+    rows = []
+    for i in range(P):
+        for j in range(P):
+            v = i * P + j
+            for w in ([v + P] if i + 1 < P else []) + ([v + 1] if j + 1 < P else []) + \
+                     ([v + P + 1] if i + 1 < P and j + 1 < P else []):
+                rows.append([v, w, float(np.linalg.norm(parts[v] - parts[w])), 500.0])
+    cloth = build_spring_net(parts, rows, np.full(P * P, 0.01))
+    chain = generate_chain(6, 0.04, 300.0, mass=0.02)
+    nb, nc = m.num_vertices, cloth.num_vertices
+    fixed = [int(v) for v in np.flatnonzero(m.rest_positions[:, 0] < 1e-9)] + [nb, nb + nc]
+    cons = [FixedConstraint(v) for v in fixed]
+    cons.append(SubspaceConstraint(nb - 1, np.array([[0.0], [0.0], [1.0]]), m.rest_positions[-1]))
+    cons.append(SubspaceConstraint(nb - 2, np.array([[1.0, 0.0], [0.0, 1.0], [0.0, 0.0]]),
+                                   m.rest_positions[-2]))
+    boxes = [(nb + v, (-1.0, -1.0, 0.185), (2.0, 2.0, 1.0), 1e4) for v in range(nc)]
+    cons += [WorldBoxConstraint(v, lo, hi, k) for v, lo, hi, k in boxes]
+    s = build_system([Body(m, MaterialParams(1e6, 1e7, 1e-6)),
+                      Body(cloth, k_d=1e-3), Body(chain, k_d=5e-4)], cons)
+    sub = [(nb - 1, [[0.0], [0.0], [1.0]], m.rest_positions[-1]),
+           (nb - 2, [[1.0, 0.0], [0.0, 1.0], [0.0, 0.0]], m.rest_positions[-2])]
+    return m, cloth, chain, fixed, sub, boxes, s
+
+
+def extras_fixture():
+    m, cloth, chain, fixed, sub, boxes, s = extras_scene()
+    st = make_state(s)
+    rng = np.random.default_rng(11)
+    st.v_t = 0.2 * rng.standard_normal(st.x.shape)
+    p = SolverParams(h=1.0 / 60.0, a_ext=G, threads=1)
+    st.y = inertia_target(st.x_t, st.v_t, p.a_ext_vec, p.h)
+    initialize(st, p)
+    st.x = np.ascontiguousarray(st.x + 0.004 * rng.standard_normal(st.x.shape))
+    x0 = st.x.copy()
+    outs = {}
+    off = s.color_off
+    x = x0.copy()
+    for g in range(s.colors.num_colors):
+        st.x = x
+        color_pass(st, s.color_verts[off[g]:off[g + 1]], p)
+        outs[f"after_color{g}"] = st.x.copy()
+        x = st.x.copy()
+    allv = np.arange(s.num_vertices, dtype=np.int64)
+    for mode in (0, 1):
+        st.x = x0.copy()
+        color_pass(st, allv, p, mode=mode)
+        outs[f"jacobi_mode{mode}"] = st.x.copy()
+    st.x = x0.copy()
+    color_pass(st, allv, SolverParams(h=1.0 / 60.0, a_ext=G, threads=1, line_search=True))
+    outs["jacobi_linesearch"] = st.x.copy()
+    # trajectories: the cloth falls onto the box floor, the chain swings
+    trajs = {}
+    for rho in (0.0, 0.9):
+        st2 = make_state(s)
+        p2 = SolverParams(h=1.0 / 60.0, n_max=15, rho=rho, a_ext=G, threads=1)
+        xs = []
+        for _ in range(8):
+            step(st2, p2)
+            xs.append(st2.x.copy())
+        trajs[f"steps_rho{int(rho * 100):02d}"] = np.array(xs)
+    save("extras_scene.npz", x0=x0, x_t=st.x_t, y=st.y, h=np.float64(p.h),
+         cloth_parts=cloth.particles, cloth_idx=cloth.indices, cloth_l0=cloth.rest_length,
+         cloth_k=cloth.stiffness, cloth_m=cloth.masses, chain_parts=chain.particles,
+         chain_idx=chain.indices, chain_l0=chain.rest_length, chain_k=chain.stiffness,
+         chain_m=chain.masses, fixed=np.array(fixed), color_of=s.colors.color_of,
+         **outs, **trajs)
+
+
 if __name__ == "__main__":
-    mesh_fixture()
-    coloring_fixtures()
-    pass_fixture()
-    step_fixtures()
+    which = set(sys.argv[1:]) or {"mesh", "coloring", "pass", "steps", "extras"}
+    for name, fn in (("mesh", mesh_fixture), ("coloring", coloring_fixtures), ("pass", pass_fixture),
+                     ("steps", step_fixtures), ("extras", extras_fixture)):
+        if name in which:
+            fn()

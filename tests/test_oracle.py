@@ -135,3 +135,42 @@ def test_oracle_matches_reference_kernel_live(O):
         O.step(s, a, 1 / 30, 20, 0.95, G)
         O.step(s, b, 1 / 30, 20, 0.95, G, kernel=ref, n_threads=1)
         assert np.array_equal(a.x, b.x)
+
+
+# ------------------------------------------------------------------------------------
+# springs, subspace and world-box constraints (_native.pyx:319-349, 401-409, 435-463)
+
+def test_extras_passes_bit_exact(O, golden):
+    from extras import extras_system
+    g = golden("extras_scene.npz")
+    m, s = extras_system(O, g)
+    h = float(g["h"])
+    x = g["x0"].copy()
+    for c, grp in enumerate(s.groups()):
+        O.color_pass(s, x, g["x_t"], g["y"], h, grp)
+        assert np.array_equal(x, g[f"after_color{c}"]), c
+    allv = np.arange(s.num_vertices)
+    for mode in (0, 1):
+        x = g["x0"].copy()
+        O.color_pass(s, x, g["x_t"], g["y"], h, allv, mode=mode)
+        assert np.array_equal(x, g[f"jacobi_mode{mode}"]), mode
+    x = g["x0"].copy()
+    O.color_pass(s, x, g["x_t"], g["y"], h, allv, line_search=True)
+    assert np.array_equal(x, g["jacobi_linesearch"])
+
+
+@pytest.mark.parametrize("rho", [0.0, 0.9])
+def test_extras_steps_bit_exact(O, golden, rho):
+    from extras import extras_system
+    g = golden("extras_scene.npz")
+    m, s = extras_system(O, g)
+    st = O.make_state(s)
+    xs = g[f"steps_rho{int(rho * 100):02d}"]
+    for k in range(len(xs)):
+        O.step(s, st, 1.0 / 60.0, 15, rho, G)
+        assert np.array_equal(st.x, xs[k]), k
+    # the cloth reached the box floor and the subspace vertices stayed on their subspaces
+    nb = m.num_vertices
+    assert (st.x[nb:nb + 25, 2] < 0.185).any()
+    assert abs(st.x[nb - 1, 0] - m.rest_positions[-1, 0]) < 1e-12
+    assert abs(st.x[nb - 2, 2] - m.rest_positions[-2, 2]) < 1e-12
