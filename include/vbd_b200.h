@@ -43,7 +43,7 @@ extern "C" {
 
 #define VBD_KIND_FREE 0
 #define VBD_KIND_FIXED 1 /* _system.py:17 FIXED */
-#define VBD_KIND_SUBSPACE 2 /* rejected: not on the hot path */
+#define VBD_KIND_SUBSPACE 2 /* SubspaceConstraint (_system.py:38-53) */
 
 #define VBD_INIT_PREV_POS 0 /* solver.py:25 INIT_MODES */
 #define VBD_INIT_INERTIA 1
@@ -71,6 +71,20 @@ typedef struct {
     const int64_t* color_off;   /* (C+1,) */
     const int64_t* color_verts; /* (N,) colour groups, concatenated */
     const double* rest_positions; /* (N,3) optional: spatial (Morton) order inside colours */
+    /* spring nets (_system.py:117-123; NULL / 0 = none) */
+    int64_t num_springs;
+    const int64_t* springs;     /* (S,2) */
+    const double* sp_l0;        /* (S,) */
+    const double* sp_k;         /* (S,) */
+    const double* sp_kd;        /* (S,) */
+    /* constraints (_system.py:76-83; NULL = none): kind[v] == VBD_KIND_SUBSPACE marks
+     * SubspaceConstraint vertices; box_k[v] > 0 an active WorldBoxConstraint */
+    const int64_t* sub_dim;     /* (N,) */
+    const double* sub_basis;    /* (N,3,2) */
+    const double* sub_anchor;   /* (N,3) */
+    const double* box_k;        /* (N,) */
+    const double* box_lo;       /* (N,3) */
+    const double* box_hi;       /* (N,3) */
 } vbd_system_desc;
 
 /* A procedural generate_beam(nx, ny, nz, spacing, density) body, rigidly translated. */

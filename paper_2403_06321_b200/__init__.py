@@ -9,9 +9,9 @@ from .backend import NAME as BACKEND_NAME
 from .context import Beam, DeviceContext
 from .errors import DegenerateTet, IndexOutOfRange, NonFiniteState, VbdError
 from .materials import MaterialParams
-from .mesh import (ColorPartition, SpringNet, TetMesh, VertexAdjacency, build_tet_mesh,
-                   generate_beam, generate_cube, greedy_color, incidence,
-                   incidence_from_elements)
+from .mesh import (ColorPartition, SpringNet, TetMesh, VertexAdjacency, build_spring_net,
+                   build_tet_mesh, generate_beam, generate_chain, generate_cube, greedy_color,
+                   incidence, incidence_from_elements)
 from .solver import (ContactParams, SimState, SolverParams, accelerate, chebyshev_omega,
                      color_pass, device_context, inertia_target, initialize, local_solve,
                      make_state, step)

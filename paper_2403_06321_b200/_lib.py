@@ -37,7 +37,10 @@ class SystemDesc(ctypes.Structure):
     _fields_ = [("num_vertices", i64), ("num_tets", i64), ("tets", P), ("tet_w", P),
                 ("tet_vol", P), ("tet_mu", P), ("tet_lam", P), ("tet_kd", P), ("masses", P),
                 ("kind", P), ("t_off", P), ("t_id", P), ("t_slot", P), ("num_colors", i64),
-                ("color_off", P), ("color_verts", P), ("rest_positions", P)]
+                ("color_off", P), ("color_verts", P), ("rest_positions", P),
+                ("num_springs", i64), ("springs", P), ("sp_l0", P), ("sp_k", P), ("sp_kd", P),
+                ("sub_dim", P), ("sub_basis", P), ("sub_anchor", P), ("box_k", P),
+                ("box_lo", P), ("box_hi", P)]
 
 
 class BeamDesc(ctypes.Structure):

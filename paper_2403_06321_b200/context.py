@@ -53,14 +53,22 @@ class Beam:
         return 5 * (self.nx - 1) * (self.ny - 1) * (self.nz - 1)
 
 
-def _unsupported_terms(system):
-    if len(getattr(system, "springs", ())):
-        raise NotImplementedError("springs are not on the B200 hot path")
+def _extra_terms(system, n):
+    """Spring and constraint arrays of a System (reference or mirrored) for the C ABI:
+    springs (_system.py:117-123), subspace and world-box constraints (_system.py:76-83)."""
+    out = {}
+    springs = getattr(system, "springs", None)
+    if springs is not None and len(springs):
+        out.update(springs=_lib.i64c(springs).reshape(-1, 2), sp_l0=_lib.f64c(system.sp_l0),
+                   sp_k=_lib.f64c(system.sp_k), sp_kd=_lib.f64c(system.sp_kd))
     cons = system.cons
-    if np.any(cons.kind == SUBSPACE):
-        raise NotImplementedError("SubspaceConstraint is not on the B200 hot path")
+    if np.any(np.asarray(cons.kind) == SUBSPACE):
+        out.update(sub_dim=_lib.i64c(cons.sub_dim), sub_basis=_lib.f64c(cons.sub_basis, (n, 3, 2)),
+                   sub_anchor=_lib.f64c(cons.sub_anchor, (n, 3)))
     if np.any(np.asarray(cons.box_k) > 0.0):
-        raise NotImplementedError("WorldBoxConstraint is not on the B200 hot path")
+        out.update(box_k=_lib.f64c(cons.box_k), box_lo=_lib.f64c(cons.box_lo, (n, 3)),
+                   box_hi=_lib.f64c(cons.box_hi, (n, 3)))
+    return out
 
 
 class DeviceContext:
@@ -73,7 +81,6 @@ class DeviceContext:
     # -- construction -----------------------------------------------------------------
     @classmethod
     def from_system(cls, system, precision="fp64", device=0):
-        _unsupported_terms(system)
         n = int(system.num_vertices)
         arrs = dict(
             tets=_lib.i64c(system.tets).reshape(-1, 4),
@@ -88,12 +95,14 @@ class DeviceContext:
         rp = getattr(system, "rest_positions", None)
         if rp is not None:
             arrs["rest_positions"] = _lib.f64c(rp, (n, 3))
+        arrs.update(_extra_terms(system, n))
         d = _lib.SystemDesc()
         d.num_vertices = n
         d.num_tets = len(arrs["tets"])
         for k, v in arrs.items():
             setattr(d, k, _lib.ptr(v))
         d.num_colors = len(arrs["color_off"]) - 1
+        d.num_springs = len(arrs["springs"]) if "springs" in arrs else 0
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().vbd_ctx_create(ctypes.byref(d), device, _lib.PREC[precision],
                                              ctypes.byref(h)))

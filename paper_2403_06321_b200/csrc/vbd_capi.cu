@@ -158,6 +158,9 @@ struct vbd_ctx {
     int nkinds = 0;
     int max_deg = 0;
     DBuf kinds, kind_keys;
+    // non-tet terms (springs, world box, subspace): host-built systems only; global K1
+    bool has_extras = false;
+    DBuf soff, sp_oth, sp_par, box, sub_idx, sub;
     // K1T tile pipeline (compact layout, in-place range passes): tiles of 64 vertices per
     // colour, their neighbour lists and 8-byte entries
     bool tiles = false;
@@ -483,7 +486,9 @@ template <typename R> void build_tiles(vbd_ctx* c)
 {
     c->tiles = false;
     const char* e = getenv("VBD_TILES");
-    if ((e && *e == '0') || !c->compact || !c->inplace || c->nsolve == 0 || c->nkinds >= 65535) return;
+    if ((e && *e == '0') || !c->compact || !c->inplace || c->nsolve == 0 || c->nkinds >= 65535 ||
+        c->has_extras)
+        return;
     const char* we = getenv("VBD_TILE_W");
     const int W = we && *we ? atoi(we) : 4;
     if (W != 4) fail(VBD_ERR_ARG, "VBD_TILE_W: only 4 lanes per vertex are compiled");
@@ -766,6 +771,14 @@ K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
     a.E = c->E;
     a.kinds = c->compact ? c->kinds.as<typename PlaneT<R>::T>() : nullptr;
     a.max_deg = c->max_deg;
+    typedef typename Vec4<R>::T R4;
+    a.soff = c->has_extras ? c->soff.as<long long>() : nullptr;
+    a.sp_oth = c->sp_oth.as<int>();
+    a.sp_par = c->sp_par.as<R4>();
+    a.box = c->has_extras && c->box.p ? c->box.as<R4>() : nullptr;
+    a.sub_idx = c->sub_idx.as<int>();
+    a.sub = c->sub.as<R4>();
+    a.h = (R)c->mat_h;
     a.off = c->eoff.as<long long>();
     a.pos = c->pos.as<typename Vec4<R>::T>();
     a.xt = c->xt.as<typename Vec4<R>::T>();
@@ -968,6 +981,8 @@ template <typename R> StepArgs<R> step_args(vbd_ctx* c)
     a.flag = c->flag.as<unsigned long long>();
     a.perm = c->perm.as<int>();
     a.stepctr = c->stepctr.as<int>();
+    a.sub_idx = c->has_extras ? c->sub_idx.as<int>() : nullptr;
+    a.sub = c->sub.as<R4>();
     return a;
 }
 
@@ -1062,6 +1077,7 @@ template <typename R> void enqueue_step_p2p(vbd_ctx* c)
 bool use_persistent(const vbd_ctx* c)
 {
     const char* e = getenv("VBD_PERSIST");
+    if (c->has_extras) return false;
     if (e && *e) return atoi(e) != 0 && c->inplace && c->ncolors <= VBD_PERSIST_MAX_COLORS;
     // measured on B200: grid.sync() costs more than a graph-node launch (C1 0.36 vs 0.25
     // ms/step), so the per-colour graph is the default everywhere
@@ -1228,6 +1244,108 @@ void do_color_pass(vbd_ctx* c, double* x, const double* x_t, const double* y, do
     }
 }
 
+// Springs, world boxes and subspace constraints of a host-built system, in colour-major order
+// over the solved vertices (the global K1 adds them in its per-vertex epilogue).
+template <typename R> void attach_extras(vbd_ctx* c, const vbd_system_desc* d, const std::vector<int>& color)
+{
+    typedef typename Vec4<R>::T R4;
+    cudaStream_t s = c->stream;
+    const long long N = d->num_vertices, S = d->springs ? d->num_springs : 0;
+    std::vector<int> perm(N), inv(N);
+    CK(cudaMemcpy(perm.data(), c->perm.p, N * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(inv.data(), c->inv.p, N * 4, cudaMemcpyDeviceToHost));
+    const long long ns = c->nsolve;
+    // vertex -> spring CSR, ascending spring id per vertex (incidence_from_elements order)
+    std::vector<long long> deg(N + 1, 0);
+    for (long long k = 0; k < S; ++k)
+        for (int e = 0; e < 2; ++e) {
+            const int64_t v = d->springs[2 * k + e];
+            if (v < 0 || v >= N) fail(VBD_ERR_ARG, "spring index out of range");
+            deg[v + 1]++;
+        }
+    for (long long v = 0; v < N; ++v) deg[v + 1] += deg[v];
+    std::vector<long long> fill(deg.begin(), deg.end() - 1);
+    std::vector<long long> vsp(2 * S);
+    std::vector<int> vslot(2 * S);
+    for (long long k = 0; k < S; ++k)
+        for (int e = 0; e < 2; ++e) {
+            const int64_t v = d->springs[2 * k + e];
+            vsp[fill[v]] = k;
+            vslot[fill[v]++] = e;
+        }
+    std::vector<long long> soff(ns + 1, 0);
+    for (long long i = 0; i < ns; ++i) soff[i + 1] = soff[i] + (deg[perm[i] + 1] - deg[perm[i]]);
+    std::vector<int> oth(std::max<long long>(soff[ns], 1));
+    std::vector<R4> par(std::max<long long>(soff[ns], 1));
+    for (long long i = 0; i < ns; ++i) {
+        const int o = perm[i];
+        long long w = soff[i];
+        for (long long k = deg[o]; k < deg[o + 1]; ++k, ++w) {
+            const long long sp = vsp[k];
+            oth[w] = inv[d->springs[2 * sp + (1 - vslot[k])]];
+            R4 q;
+            q.x = (R)d->sp_l0[sp];
+            q.y = (R)d->sp_k[sp];
+            q.z = (R)d->sp_kd[sp];
+            q.w = R(0);
+            par[w] = q;
+        }
+    }
+    upload(c->soff, soff.data(), soff.size(), s);
+    upload(c->sp_oth, oth.data(), oth.size(), s);
+    upload(c->sp_par, par.data(), par.size(), s);
+    // springs join vertices of different colours (the in-place sweep relies on it)
+    for (long long k = 0; k < S; ++k) {
+        const int64_t a = d->springs[2 * k], b = d->springs[2 * k + 1];
+        if (color[a] >= 0 && color[a] == color[b]) c->inplace = false;
+    }
+    // world boxes
+    bool any_box = false;
+    if (d->box_k)
+        for (long long v = 0; v < N; ++v) any_box |= d->box_k[v] > 0.0;
+    if (any_box) {
+        std::vector<R4> bx(2 * std::max<long long>(ns, 1));
+        for (long long i = 0; i < ns; ++i) {
+            const int o = perm[i];
+            R4 lo, hi;
+            lo.x = (R)d->box_lo[3 * o]; lo.y = (R)d->box_lo[3 * o + 1]; lo.z = (R)d->box_lo[3 * o + 2];
+            lo.w = (R)(d->box_k[o] > 0.0 ? d->box_k[o] : 0.0);
+            hi.x = (R)d->box_hi[3 * o]; hi.y = (R)d->box_hi[3 * o + 1]; hi.z = (R)d->box_hi[3 * o + 2];
+            hi.w = R(0);
+            bx[2 * i] = lo;
+            bx[2 * i + 1] = hi;
+        }
+        upload(c->box, bx.data(), bx.size(), s);
+    } else {
+        c->box.release();
+    }
+    // subspace constraints
+    std::vector<int> sidx(std::max<long long>(ns, 1), -1);
+    std::vector<R4> sub;
+    if (d->kind)
+        for (long long i = 0; i < ns; ++i) {
+            const int o = perm[i];
+            if (d->kind[o] != VBD_KIND_SUBSPACE) continue;
+            if (!d->sub_dim || !d->sub_basis || !d->sub_anchor) fail(VBD_ERR_ARG, "subspace arrays missing");
+            const int dim = (int)d->sub_dim[o];
+            if (dim != 1 && dim != 2) fail(VBD_ERR_ARG, "subspace dimension must be 1 or 2");
+            const double* B = d->sub_basis + 6 * o;
+            const double* an = d->sub_anchor + 3 * o;
+            sidx[i] = (int)(sub.size() / 3);
+            R4 a, b, e;
+            a.x = (R)B[0]; a.y = (R)B[1]; a.z = (R)B[2]; a.w = (R)B[3];
+            b.x = (R)B[4]; b.y = (R)B[5]; b.z = (R)an[0]; b.w = (R)an[1];
+            e.x = (R)an[2]; e.y = (R)dim; e.z = R(0); e.w = R(0);
+            sub.push_back(a);
+            sub.push_back(b);
+            sub.push_back(e);
+        }
+    if (sub.empty()) sub.resize(3);
+    upload(c->sub_idx, sidx.data(), sidx.size(), s);
+    upload(c->sub, sub.data(), sub.size(), s);
+    CK(cudaStreamSynchronize(s));
+}
+
 int material_id(vbd_ctx* c, std::map<MaterialKey, int>& ids, const MaterialKey& k)
 {
     auto it = ids.find(k);
@@ -1352,12 +1470,15 @@ int vbd_ctx_create(const vbd_system_desc* d, int device, int precision, vbd_ctx*
         upload(sc.vol, d->tet_vol, T, s);
         upload(sc.mass, d->masses, N, s);
         std::vector<unsigned char> kind(N, 0);
+        bool extras = d->springs && d->num_springs > 0;
         if (d->kind)
             for (long long v = 0; v < N; ++v) {
-                if (d->kind[v] == VBD_KIND_SUBSPACE)
-                    fail(VBD_ERR_UNSUPPORTED, "SubspaceConstraint is not on the B200 hot path");
+                if (d->kind[v] == VBD_KIND_SUBSPACE) extras = true;  // solved, in its subspace
                 kind[v] = d->kind[v] == VBD_KIND_FIXED ? 1 : 0;
             }
+        if (d->box_k)
+            for (long long v = 0; v < N && !extras; ++v) extras = d->box_k[v] > 0.0;
+        c->has_extras = extras;
         upload(sc.kind, kind.data(), N, s);
         // incidence exactly as given (ascending tet id per vertex, mesh.py:243-250)
         if (d->t_off[0] != 0 || d->t_off[N] != 4 * T) fail(VBD_ERR_ARG, "t_off inconsistent with tets");
@@ -1393,6 +1514,10 @@ int vbd_ctx_create(const vbd_system_desc* d, int device, int precision, vbd_ctx*
         }
         CK(cudaStreamSynchronize(s));
         finish_pack(c, sc);
+        if (c->has_extras) {
+            if (c->precision == VBD_PREC_F64) attach_extras<double>(c, d, color);
+            else attach_extras<float>(c, d, color);
+        }
         *out = c;
     });
     if (rc != VBD_OK) delete c;
@@ -1598,7 +1723,8 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         info->num_colors = c->ncolors;
         for (int k = 0; k < c->ncolors && k < 64; ++k) info->color_count[k] = c->ccnt[k];
         long long b = 0;
-        for (DBuf* d : {&c->perm, &c->inv, &c->eoff, &c->ent, &c->mat, &c->pos, &c->xt, &c->vt, &c->vprev,
+        for (DBuf* d : {&c->soff, &c->sp_oth, &c->sp_par, &c->box, &c->sub_idx, &c->sub,
+                        &c->perm, &c->inv, &c->eoff, &c->ent, &c->mat, &c->pos, &c->xt, &c->vt, &c->vprev,
                         &c->y, &c->ha, &c->hb, &c->mass, &c->out, &c->stage, &c->color_orig, &c->kinds,
                         &c->kind_keys, &c->vmat, &c->tv0, &c->tnv, &c->loff, &c->tnbr, &c->tent,
                         &c->tdesc})

@@ -37,6 +37,16 @@ template <typename R> struct K1Args {
     int pf_dist;             // L2 prefetch distance in CTAs (one residency wave)
     const int* vmat;         // per-vertex material when every vertex has one material, else null
     int line_search;         // 17-trial local backtracking (mode 0 only)
+    // non-tet terms (host-built systems only; nullptr = none), solved vertices, colour-major:
+    // spring CSR (other end, {l0, k, k_d}), world box {lo.xyz, k} {hi.xyz}, subspace index into
+    // sub (3 R4: {b00 b01 b10 b11} {b20 b21 ax ay} {az dim})
+    const long long* soff;
+    const int* sp_oth;
+    const R4* sp_par;
+    const R4* box;
+    const int* sub_idx;
+    const R4* sub;
+    R h;
     // fused slab halo push (multi-GPU, peer memory): the first nb[0] vertices of the colour
     // range face the left neighbour, the next nb[1] the right one; their new positions are
     // also stored into the neighbour's ghost block (peer_pos[s] + peer_off[s])
@@ -49,9 +59,132 @@ template <typename R> struct K1Args {
 // v = vbeg + g (or group[g]).  UM: one material per vertex (damping hoisted out of the loop).
 // Local energy G_i of vertex v at position p (_native.pyx:201-258, tet + inertia terms),
 // summed over the W lanes of the group (identical in every lane).
+// spring and world-box terms of G_i (_native.pyx:226-237, 250-257), vertex at p
+template <typename R>
+__device__ R extras_energy(const K1Args<R>& a, int v, const R* p)
+{
+    R e = R(0);
+    for (long long k = a.soff[v]; k < a.soff[v + 1]; ++k) {
+        const typename Vec4<R>::T q = a.pos[a.sp_oth[k]], sp = a.sp_par[k];
+        const R d0 = p[0] - q.x, d1 = p[1] - q.y, d2 = p[2] - q.z;
+        const R len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+        if (len < R(1e-12) * sp.x) {
+            e += R(0.5) * sp.y * sp.x * sp.x;
+        } else {
+            const R t = len - sp.x;
+            e += R(0.5) * sp.y * t * t;
+        }
+    }
+    if (a.box) {
+        const typename Vec4<R>::T lo = a.box[2 * v], hi = a.box[2 * v + 1];
+        if (lo.w > R(0)) {
+            const R l[3] = {lo.x, lo.y, lo.z}, u[3] = {hi.x, hi.y, hi.z};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                R t = l[c] - p[c];
+                if (t > R(0)) e += R(0.5) * lo.w * t * t;
+                t = p[c] - u[c];
+                if (t > R(0)) e += R(0.5) * lo.w * t * t;
+            }
+        }
+    }
+    return e;
+}
+
+// spring (_native.pyx:319-349, per-spring Rayleigh damping) and world-box (:401-409) terms
+template <typename R>
+__device__ void extras_terms(const K1Args<R>& a, int v, const R* xi, const R* dx, R* f, R* H)
+{
+    for (long long k = a.soff[v]; k < a.soff[v + 1]; ++k) {
+        const typename Vec4<R>::T q = a.pos[a.sp_oth[k]], sp = a.sp_par[k];
+        R dv[3] = {xi[0] - q.x, xi[1] - q.y, xi[2] - q.z};
+        const R len = sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
+        R he[6];
+        if (len < R(1e-12) * sp.x) {
+            he[0] = he[3] = he[5] = sp.y;
+            he[1] = he[2] = he[4] = R(0);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) dv[c] = dv[c] / len;
+            const R coef = R(1) - sp.x / len;
+            const R fs = sp.y * (len - sp.x);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) f[c] -= fs * dv[c];
+            he[0] = sp.y * (dv[0] * dv[0] + coef * (R(1) - dv[0] * dv[0]));
+            he[1] = sp.y * (dv[0] * dv[1] - coef * dv[0] * dv[1]);
+            he[2] = sp.y * (dv[0] * dv[2] - coef * dv[0] * dv[2]);
+            he[3] = sp.y * (dv[1] * dv[1] + coef * (R(1) - dv[1] * dv[1]));
+            he[4] = sp.y * (dv[1] * dv[2] - coef * dv[1] * dv[2]);
+            he[5] = sp.y * (dv[2] * dv[2] + coef * (R(1) - dv[2] * dv[2]));
+        }
+        const R dsc = sp.z / a.h;
+        f[0] -= dsc * (he[0] * dx[0] + he[1] * dx[1] + he[2] * dx[2]);
+        f[1] -= dsc * (he[1] * dx[0] + he[3] * dx[1] + he[4] * dx[2]);
+        f[2] -= dsc * (he[2] * dx[0] + he[4] * dx[1] + he[5] * dx[2]);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) H[c] += (R(1) + dsc) * he[c];
+    }
+    if (a.box) {
+        const typename Vec4<R>::T lo = a.box[2 * v], hi = a.box[2 * v + 1];
+        if (lo.w > R(0)) {
+            const R l[3] = {lo.x, lo.y, lo.z}, u[3] = {hi.x, hi.y, hi.z};
+            const int dg[3] = {0, 3, 5};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (xi[c] < l[c]) {
+                    f[c] -= lo.w * (xi[c] - l[c]);
+                    H[dg[c]] += lo.w;
+                } else if (xi[c] > u[c]) {
+                    f[c] -= lo.w * (xi[c] - u[c]);
+                    H[dg[c]] += lo.w;
+                }
+            }
+        }
+    }
+}
+
+// SubspaceConstraint solve (_native.pyx:435-463): delta = B (B^T H B)^-1 B^T f, 1- or 2-D,
+// with the reference's relative determinant guards.  H is symmetric (6 unique entries).
+template <typename R>
+__device__ void subspace_solve(const typename Vec4<R>::T* sub3, const R* f, const R* H, R eps_det, R* d)
+{
+    const typename Vec4<R>::T s0 = sub3[0], s1 = sub3[1], s2 = sub3[2];
+    const R B[3][2] = {{s0.x, s0.y}, {s0.z, s0.w}, {s1.x, s1.y}};
+    const int dim = (int)s2.y;
+    const R Hm[3][3] = {{H[0], H[1], H[2]}, {H[1], H[3], H[4]}, {H[2], H[4], H[5]}};
+    R rhs[2], am[2][2];
+    for (int p = 0; p < dim; ++p) {
+        rhs[p] = B[0][p] * f[0] + B[1][p] * f[1] + B[2][p] * f[2];
+        for (int q = 0; q < dim; ++q) {
+            R acc = R(0);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                acc += B[k][p] * (Hm[k][0] * B[0][q] + Hm[k][1] * B[1][q] + Hm[k][2] * B[2][q]);
+            am[p][q] = acc;
+        }
+    }
+    d[0] = d[1] = d[2] = R(0);
+    if (dim == 1) {
+        if (fabs(am[0][0]) > eps_det * fabs(am[0][0])) {
+            const R q0 = rhs[0] / am[0][0];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) d[c] = B[c][0] * q0;
+        }
+    } else {
+        const R det = am[0][0] * am[1][1] - am[0][1] * am[1][0];
+        const R tr = R(0.5) * (am[0][0] + am[1][1]);
+        if (fabs(det) > eps_det * tr * tr) {
+            const R q0 = (am[1][1] * rhs[0] - am[0][1] * rhs[1]) / det;
+            const R q1 = (am[0][0] * rhs[1] - am[1][0] * rhs[0]) / det;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) d[c] = B[c][0] * q0 + B[c][1] * q1;
+        }
+    }
+}
+
 template <typename R, int W>
 __device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int lane, unsigned gmask,
-                          const R* p, const typename Vec4<R>::T& y4)
+                          const R* p, const typename Vec4<R>::T& y4, int v)
 {
     typedef typename Vec4<R>::T R4;
     R e = R(0);
@@ -93,6 +226,7 @@ __device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int 
     }
 #pragma unroll
     for (int o = W / 2; o > 0; o >>= 1) e += __shfl_xor_sync(gmask, e, o, W);
+    if (a.soff) e += extras_energy<R>(a, v, p);
     R ein = R(0);
     const R d0 = p[0] - y4.x, d1 = p[1] - y4.y, d2 = p[2] - y4.z;
     ein = ein + ((R(0.5) * y4.w) * d0) * d0;
@@ -250,16 +384,23 @@ __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int la
     if (!LS && lane != 0) return;
     vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM && end > beg, mv.dsc, mv.opd);
     R d[3];
-    block_solve<R>(f, H, a.eps_det, a.mode, d);
+    if (a.soff) {
+        extras_terms<R>(a, v, xi, dx, f, H);
+        const int si = a.sub_idx[v];
+        if (si >= 0 && a.mode == 0) subspace_solve<R>(a.sub + 3 * si, f, H, a.eps_det, d);
+        else block_solve<R>(f, H, a.eps_det, a.mode, d);
+    } else {
+        block_solve<R>(f, H, a.eps_det, a.mode, d);
+    }
     R4 nx = xi4;
     if (LS && a.mode == 0) {
         // 17-trial backtracking on G_i (_native.pyx:481-492); every lane of the group runs
         // the same trials on the same reduced energies
-        const R e0 = local_energy<R, W>(a, beg, end, lane, gmask, xi, y4);
+        const R e0 = local_energy<R, W>(a, beg, end, lane, gmask, xi, y4, v);
         R alpha = R(1);
         for (int trial = 0; trial < 17; ++trial) {
             const R cand[3] = {xi[0] + alpha * d[0], xi[1] + alpha * d[1], xi[2] + alpha * d[2]};
-            if (local_energy<R, W>(a, beg, end, lane, gmask, cand, y4) <= e0) {
+            if (local_energy<R, W>(a, beg, end, lane, gmask, cand, y4, v) <= e0) {
                 nx.x = cand[0];
                 nx.y = cand[1];
                 nx.z = cand[2];
@@ -413,6 +554,8 @@ template <typename R> struct StepArgs {
     unsigned long long* flag;
     const int* perm;
     int* stepctr;
+    const int* sub_idx;  // SubspaceConstraint projection of the warm start (nullptr = none)
+    const R4* sub;
 };
 
 template <typename R>
@@ -449,6 +592,19 @@ __device__ __forceinline__ void k2_vertex(const StepArgs<R>& s, int i)
         }
     } else if (s.flag && !finite3(x.x, x.y, x.z)) {  // fixed vertices never pass through K1
         atomicMin(s.flag, StepFlag::key((unsigned)*s.stepctr, 1u, (unsigned)s.perm[i]));
+    }
+    if (s.sub_idx && i < s.nsolve && s.sub_idx[i] >= 0) {  // solver.py:158-162
+        const R4* b = s.sub + 3 * s.sub_idx[i];
+        const R4 s0 = b[0], s1 = b[1], s2 = b[2];
+        const R B[3][2] = {{s0.x, s0.y}, {s0.z, s0.w}, {s1.x, s1.y}};
+        const R an[3] = {s1.z, s1.w, s2.x};
+        const R r[3] = {x.x - an[0], x.y - an[1], x.z - an[2]};
+        R c[2] = {R(0), R(0)};
+        const int dim = (int)s2.y;
+        for (int q = 0; q < dim; ++q) c[q] = B[0][q] * r[0] + B[1][q] * r[1] + B[2][q] * r[2];
+        x.x = an[0] + B[0][0] * c[0] + B[0][1] * c[1];
+        x.y = an[1] + B[1][0] * c[0] + B[1][1] * c[1];
+        x.z = an[2] + B[2][0] * c[0] + B[2][1] * c[1];
     }
     s.y[i] = y;
     s.pos[i] = x;

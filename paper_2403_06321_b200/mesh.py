@@ -50,7 +50,8 @@ class TetMesh:
 
 @dataclass(frozen=True)
 class SpringNet:
-    """Particles (springs are not on the B200 hot path: only spring-free nets are accepted)."""
+    """Particles joined by linear springs (mesh.py:60-79): row s is (indices[s],
+    rest_length[s], stiffness[s])."""
 
     particles: np.ndarray
     indices: np.ndarray
@@ -172,6 +173,40 @@ def generate_cube(n: int, edge: float, density: float = 1000.0) -> TetMesh:
     if edge <= 0.0:
         raise ValueError("edge must be positive")
     return generate_beam(n, n, n, edge / (n - 1), density)
+
+
+def build_spring_net(particles, springs, masses) -> SpringNet:
+    """mesh.py:192-215: springs rows are (i, j, rest_length, stiffness)."""
+    particles = np.ascontiguousarray(particles, dtype=np.float64)
+    masses = np.ascontiguousarray(masses, dtype=np.float64)
+    springs = np.asarray(springs, dtype=np.float64).reshape(-1, 4)
+    idx = np.ascontiguousarray(springs[:, :2].astype(np.int64))
+    l0 = np.ascontiguousarray(springs[:, 2])
+    k = np.ascontiguousarray(springs[:, 3])
+    n = len(particles)
+    if idx.size and (idx.min() < 0 or idx.max() >= n):
+        raise IndexOutOfRange(f"spring index outside [0,{n})")
+    if np.any(idx[:, 0] == idx[:, 1]):
+        raise ValueError("spring endpoints must be distinct")
+    if np.any(l0 <= 0.0):
+        raise ValueError("rest lengths must be positive")
+    if np.any(k < 0.0):
+        raise ValueError("stiffness must be >= 0")
+    if np.any(masses <= 0.0):
+        raise ValueError("masses must be positive")
+    return SpringNet(particles, idx, l0, k, masses)
+
+
+def generate_chain(count: int, spacing: float, stiffness: float, mass: float = 1.0) -> SpringNet:
+    """harness.py:79-90: `count` particles hanging along -y, linked by serial springs."""
+    if count < 2:
+        raise ValueError("chain needs at least 2 particles")
+    if spacing <= 0.0 or stiffness <= 0.0 or mass <= 0.0:
+        raise ValueError("spacing, stiffness and mass must be positive")
+    particles = np.zeros((count, 3))
+    particles[:, 1] = -spacing * np.arange(count)
+    springs = [[i, i + 1, spacing, stiffness] for i in range(count - 1)]
+    return build_spring_net(particles, springs, np.full(count, mass))
 
 
 def incidence_from_elements(elements, num_vertices: int) -> VertexAdjacency:

@@ -215,8 +215,6 @@ def chebyshev_omega(rho: float, n: int) -> float:
 def _check_supported(state, params):
     if params.contact is not None:
         raise NotImplementedError("contact handling is not on the B200 hot path")
-    if np.any(state.system.cons.kind == SUBSPACE):
-        raise NotImplementedError("SubspaceConstraint is not on the B200 hot path")
 
 
 def _dparams(params):

@@ -31,13 +31,37 @@ def test_library_exports_every_declared_symbol():
     assert _lib.lib().vbd_version().decode().startswith("vbd_b200")
 
 
-def test_struct_layouts_match_header():
+def test_struct_layouts_match_header(tmp_path):
+    """Every ctypes mirror has the size and field offsets the C compiler gives the header."""
     import ctypes
+    import shutil
+    import subprocess
     from paper_2403_06321_b200 import _lib
-    assert ctypes.sizeof(_lib.StepParams) == 8 + 4 + 4 + 8 + 8 + 24 + 8
-    assert ctypes.sizeof(_lib.StepResult) == 24
-    assert ctypes.sizeof(_lib.BeamDesc) == 3 * 8 + 2 * 8 + 24 + 24 + 8
-    assert ctypes.sizeof(_lib.SystemDesc) == 17 * 8
+    mirrors = {"vbd_system_desc": _lib.SystemDesc, "vbd_beam_desc": _lib.BeamDesc,
+               "vbd_step_params": _lib.StepParams, "vbd_step_result": _lib.StepResult,
+               "vbd_ctx_info": _lib.CtxInfo}
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "vbd_b200.h"', "int main(void) {"]
+    for cname, py in mirrors.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n"):
+        if ln:
+            c, f, v = ln.split()
+            got[(c, f)] = int(v)
+    for cname, py in mirrors.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
 
 
 def test_no_cpu_fallback_without_gpu():

@@ -108,14 +108,34 @@ def test_reference_system_on_fast_path(ref):
         assert np.abs(x - st.x).max() / m.bbox_diagonal() <= tol, precision
 
 
-def test_out_of_scope_terms_raise(ref, with_b200):
+def test_springs_through_the_plugin_match_native(ref, with_b200):
+    """A tet cube hanging from a spring chain: the unmodified reference solver with the b200
+    colour pass against the reference's own native backend."""
     vbdsim, _ = ref
-    chain = vbdsim.generate_chain(3, 0.2, stiffness=900.0, mass=0.1)
-    cube = vbdsim.generate_cube(2, 0.4, density=1000.0)
+    chain = vbdsim.generate_chain(4, 0.2, stiffness=900.0, mass=0.1)
+    cube = vbdsim.generate_cube(3, 0.4, density=1000.0)
     s = vbdsim.build_system([vbdsim.Body(cube, vbdsim.MaterialParams(2e5, 8e5)),
-                             vbdsim.Body(chain, None, k_d=0.001)])
-    st = vbdsim.make_state(s)
-    p = vbdsim.SolverParams(h=1 / 60, a_ext=G)
+                             vbdsim.Body(chain, None, k_d=0.001)],
+                            [vbdsim.FixedConstraint(cube.num_vertices)])
+    p = vbdsim.SolverParams(h=1 / 60, n_max=10, a_ext=G)
+    a, b = vbdsim.make_state(s), vbdsim.make_state(s)
+    for _ in range(5):
+        vbdsim.step(a, p)
     with with_b200():
-        with pytest.raises(NotImplementedError):
-            vbdsim.step(st, p)
+        for _ in range(5):
+            vbdsim.step(b, p)
+    diag = float(np.linalg.norm(s.rest_positions.max(0) - s.rest_positions.min(0)))
+    assert np.abs(a.x - b.x).max() / diag <= 1e-10
+
+
+def test_contacts_raise(ref, with_b200):
+    vbdsim, _ = ref
+    import paper_2403_06321_b200.backend as B
+    cube = vbdsim.generate_cube(2, 0.4, density=1000.0)
+    s = vbdsim.build_system([vbdsim.Body(cube, vbdsim.MaterialParams(2e5, 8e5))])
+
+    class _Contacts:
+        count = 1
+    x = np.ascontiguousarray(s.rest_positions.copy())
+    with pytest.raises(NotImplementedError):
+        B.color_pass(s, _Contacts(), x, x, x, 1 / 60, np.arange(s.num_vertices))
