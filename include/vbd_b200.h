@@ -196,6 +196,12 @@ int vbd_step_p2p_finish(vbd_ctx* ctx, vbd_step_result* res);
 int vbd_greedy_color(int64_t n, const int64_t* noff, const int64_t* nids, const int64_t* order,
                      int device, int64_t* color_of, int64_t* num_colors);
 
+/* ---- metrics ------------------------------------------------------------------------------ */
+/* G(x) = 1/(2h^2) |x - y|_M^2 + E(x) at the current iterate (tets, springs, world boxes; no
+ * contacts) -- baselines.energy / _assembly.variational_energy (_assembly.py:78-82), the
+ * per-iteration metric of harness.run_simulation (harness.py:664-678).  Synchronous. */
+int vbd_energy(vbd_ctx* ctx, double h, double* G);
+
 /* ---- measurement ------------------------------------------------------------------------ */
 /* average device time of one colour-pass launch per colour over `reps` sweeps (CUDA events on
  * the context stream); ms has room for num_colors values */

@@ -585,3 +585,35 @@ def step(system, st, h, n_max, rho=0.0, a_ext=(0.0, 0.0, 0.0), eps_det=1e-10,
     st.x_t = st.x.copy()
     st.step_index += 1
     return st
+
+
+# --------------------------------------------------------------------------
+# incremental potential G (metrics path, _assembly.py:29-82 restated, no contacts)
+
+def variational_energy(system, x, y, h):
+    """G(x) = 1/(2 h^2) |x - y|_M^2 + E(x) with E = tets + springs + box
+    (_assembly.py:29-38, 41-46, 59-67, 70-82), the same NumPy operations."""
+    s = system
+    x = np.asarray(x)
+    dx = x - np.asarray(y)
+    inertia = 0.5 / (h * h) * float((s.masses[:, None] * dx * dx).sum())
+    e = 0.0
+    if len(s.tets):
+        f = np.einsum("tsa,tsb->tab", x[s.tets], s.tet_w)
+        i_c = np.einsum("tab,tab->t", f, f)
+        j = np.linalg.det(f)
+        gamma = 1.0 + s.tet_mu / s.tet_lam
+        psi = 0.5 * s.tet_mu * (i_c - 3.0) + 0.5 * s.tet_lam * (j - gamma) ** 2
+        e += float((s.tet_vol * psi).sum())
+    if len(s.springs):
+        d = x[s.springs[:, 0]] - x[s.springs[:, 1]]
+        length = np.linalg.norm(d, axis=1)
+        e += float((0.5 * s.sp_k * (length - s.sp_l0) ** 2).sum())
+    k = s.box_k
+    active = k > 0.0
+    if active.any():
+        xa = x[active]
+        below = np.maximum(s.box_lo[active] - xa, 0.0)
+        above = np.maximum(xa - s.box_hi[active], 0.0)
+        e += float(0.5 * (k[active][:, None] * (below ** 2 + above ** 2)).sum())
+    return inertia + e

@@ -13,7 +13,7 @@ from .mesh import (ColorPartition, SpringNet, TetMesh, VertexAdjacency, build_sp
                    build_tet_mesh, generate_beam, generate_chain, generate_cube, greedy_color,
                    incidence, incidence_from_elements)
 from .solver import (ContactParams, SimState, SolverParams, accelerate, chebyshev_omega,
-                     color_pass, device_context, inertia_target, initialize, local_solve,
+                     color_pass, device_context, energy, inertia_target, initialize, local_solve,
                      make_state, step)
 from .system import (Body, ConstraintArrays, FixedConstraint, SubspaceConstraint, System,
                      WorldBoxConstraint, build_system, compile_constraints)

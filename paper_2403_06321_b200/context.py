@@ -117,6 +117,12 @@ class DeviceContext:
                                                    _lib.PREC[precision], ctypes.byref(h)))
         return cls(h.value, keepalive=list(beams))
 
+    def energy(self, h):
+        """G(x) = 1/(2h^2)|x - y|_M^2 + E(x) at the device iterate (_assembly.py:78-82)."""
+        g = ctypes.c_double()
+        _lib.check(_lib.lib().vbd_energy(self._h, float(h), ctypes.byref(g)))
+        return g.value
+
     def close(self):
         if self._h and self._h.value:
             _lib.check(_lib.lib().vbd_ctx_destroy(self._h))

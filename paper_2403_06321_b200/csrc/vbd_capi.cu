@@ -1303,9 +1303,9 @@ template <typename R> void attach_extras(vbd_ctx* c, const vbd_system_desc* d, c
     bool any_box = false;
     if (d->box_k)
         for (long long v = 0; v < N; ++v) any_box |= d->box_k[v] > 0.0;
-    if (any_box) {
-        std::vector<R4> bx(2 * std::max<long long>(ns, 1));
-        for (long long i = 0; i < ns; ++i) {
+    if (any_box) {  // over all vertices (the energy counts fixed vertices' boxes too)
+        std::vector<R4> bx(2 * std::max<long long>(N, 1));
+        for (long long i = 0; i < N; ++i) {
             const int o = perm[i];
             R4 lo, hi;
             lo.x = (R)d->box_lo[3 * o]; lo.y = (R)d->box_lo[3 * o + 1]; lo.z = (R)d->box_lo[3 * o + 2];
@@ -2213,6 +2213,35 @@ int vbd_greedy_color(int64_t n, const int64_t* noff, const int64_t* nids, const 
             mx = std::max<long long>(mx, hc[v]);
         }
         if (num_colors) *num_colors = mx + 1;
+    });
+}
+
+int vbd_energy(vbd_ctx* c, double h, double* G)
+{
+    return guarded([&] {
+        if (!c || !G) fail(VBD_ERR_ARG, "NULL argument");
+        if (!(h > 0.0)) fail(VBD_ERR_ARG, "h must be positive");
+        cudaStream_t s = c->stream;
+        const unsigned b1 = blocks_for(std::max<long long>(c->nsolve, 1) * 4), b2 = blocks_for(std::max<long long>(c->n, 1));
+        DBuf part;
+        part.alloc((size_t)(b1 + b2) * sizeof(double));
+        auto run = [&](auto tag) {
+            typedef decltype(tag) R;
+            if (std::isnan(c->mat_h)) ensure_materials<R>(c, 1.0);  // rest data only
+            K1Args<R> a = k1_args<R>(c, 1e-10, 0, false, 0);
+            k_energy_elastic<R, 4><<<b1, 256, 0, s>>>(a, (int)c->nsolve, part.as<double>());
+            k_energy_vertex<R><<<b2, 256, 0, s>>>(a, c->mass.as<R>(), (int)c->n, 1.0 / (h * h),
+                                                 part.as<double>() + b1);
+        };
+        if (c->precision == VBD_PREC_F64) run(double{});
+        else run(float{});
+        CK(cudaGetLastError());
+        std::vector<double> h(b1 + b2);
+        CK(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double acc = 0.0;
+        for (double v : h) acc += v;
+        *G = acc;
     });
 }
 

@@ -527,6 +527,112 @@ __global__ void __launch_bounds__(256, MINB) k1_color_pass_bulk(const K1Args<R> 
     if (g < a.count) k1_vertex_impl<R, W, U, UM, false, true, true>(a, g, lane, sent, e0, bar);
 }
 
+// ---------------------------------------------------------------------------------------
+// Incremental potential G(x) = 1/(2h^2)|x - y|_M^2 + E(x) (_assembly.py:29-82, no contacts):
+// the metrics path of harness.run_simulation (harness.py:664-678) on the device.  Each tet is
+// counted once, from the entry of its smallest solved colour-major vertex; each spring from
+// its smaller solved end.  Per-block sums in double, summed in order on the host.
+template <typename R, int W>
+__global__ void __launch_bounds__(256) k_energy_elastic(const K1Args<R> a, int nsolve, double* partial)
+{
+    typedef typename Vec4<R>::T R4;
+    __shared__ double red[256];
+    const int g = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) / W);
+    const int lane = threadIdx.x & (W - 1);
+    double e = 0.0;
+    if (g < nsolve) {
+        const int v = g;
+        const R4 xi4 = a.pos[v];
+        for (long long k = a.off[v] + lane; k < a.off[v + 1]; k += W) {
+            int n[3];
+            R w[9], V, mu, lam, gamma;
+            if (a.kinds) {
+                const EntryK ek = EntryK::load(reinterpret_cast<const int4*>(a.ent), k);
+                R r[KindRec<R>::NR];
+                load_kind<R, KindRec<R>::Q>(a.kinds, ek.kind, r);
+                for (int j = 0; j < 3; ++j) n[j] = ek.n[j];
+                for (int j = 0; j < 9; ++j) w[j] = r[12 + j];
+                V = r[21]; mu = r[22]; lam = r[23]; gamma = r[11];
+            } else {
+                const Entry<R> en = Entry<R>::load(a.ent, a.E, k);
+                for (int j = 0; j < 3; ++j) n[j] = en.n[j];
+                for (int j = 0; j < 9; ++j) w[j] = en.w[j];
+                V = en.V;
+                const Material<R> m = a.mat[en.mat];
+                mu = m.mu; lam = m.lam; gamma = m.gamma;
+            }
+            bool own = true;
+            for (int j = 0; j < 3; ++j) own = own && (n[j] > v || n[j] >= nsolve);
+            if (!own) continue;
+            R ed[3][3];
+            for (int j = 0; j < 3; ++j) {
+                const R4 q = a.pos[n[j]];
+                ed[j][0] = q.x - xi4.x; ed[j][1] = q.y - xi4.y; ed[j][2] = q.z - xi4.z;
+            }
+            R F[9];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c)
+                    F[r * 3 + c] = ed[0][r] * w[c] + ed[1][r] * w[3 + c] + ed[2][r] * w[6 + c];
+            R ic = R(0);
+            for (int q = 0; q < 9; ++q) ic += F[q] * F[q];
+            const R J = F[0] * (F[4] * F[8] - F[7] * F[5]) + F[3] * (F[7] * F[2] - F[1] * F[8]) +
+                        F[6] * (F[1] * F[5] - F[4] * F[2]);
+            e += (double)V * (0.5 * (double)mu * ((double)ic - 3.0) +
+                              0.5 * (double)lam * ((double)J - (double)gamma) * ((double)J - (double)gamma));
+        }
+        if (lane == 0 && a.soff) {
+            for (long long k = a.soff[v]; k < a.soff[v + 1]; ++k) {
+                const int o = a.sp_oth[k];
+                if (o < v && o < nsolve) continue;  // counted from the other end
+                const R4 q = a.pos[o], sp = a.sp_par[k];
+                const double d0 = (double)xi4.x - q.x, d1 = (double)xi4.y - q.y, d2 = (double)xi4.z - q.z;
+                const double t = sqrt(d0 * d0 + d1 * d1 + d2 * d2) - (double)sp.x;
+                e += 0.5 * (double)sp.y * t * t;
+            }
+        }
+    }
+    red[threadIdx.x] = e;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// inertia of every vertex and the world-box penalty
+template <typename R>
+__global__ void __launch_bounds__(256) k_energy_vertex(const K1Args<R> a, const R* __restrict__ mass, int n,
+                                                       double inv_h2, double* partial)
+{
+    typedef typename Vec4<R>::T R4;
+    __shared__ double red[256];
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    double e = 0.0;
+    if (v < n) {
+        const R4 x = a.pos[v], y = a.y[v];
+        const double d0 = (double)x.x - y.x, d1 = (double)x.y - y.y, d2 = (double)x.z - y.z;
+        e = 0.5 * inv_h2 * (double)mass[v] * (d0 * d0 + d1 * d1 + d2 * d2);
+        if (a.box) {
+            const R4 lo = a.box[2 * v], hi = a.box[2 * v + 1];
+            if (lo.w > R(0)) {
+                const double xv[3] = {x.x, x.y, x.z}, l[3] = {lo.x, lo.y, lo.z}, u[3] = {hi.x, hi.y, hi.z};
+                for (int c = 0; c < 3; ++c) {
+                    const double b = fmax(l[c] - xv[c], 0.0), t = fmax(xv[c] - u[c], 0.0);
+                    e += 0.5 * (double)lo.w * (b * b + t * t);
+                }
+            }
+        }
+    }
+    red[threadIdx.x] = e;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
 template <typename R>
 __global__ void k_scatter_group(const typename Vec4<R>::T* __restrict__ out, const int* __restrict__ group,
                                 int ng, typename Vec4<R>::T* pos)

@@ -271,6 +271,17 @@ def step(state, params, on_iteration=None):
     return state
 
 
+def energy(state, params) -> float:
+    """baselines.energy (baselines.py:42-44): G(x) = 1/(2h^2)|x - y|_M^2 + E(x)
+    (_assembly.py:78-82) evaluated on the device.  Inside ``step(on_iteration=...)`` the
+    iterate is already resident, so the per-iteration metric of harness.run_simulation
+    (harness.py:664-678) costs no host transfer of x."""
+    ctx = device_context(state.system, params.precision, params.device)
+    state._bind(ctx)
+    state._upload(("x", "y"))
+    return ctx.energy(params.h)
+
+
 def color_pass(state, color_group, params, mode: int = 0) -> None:
     """One aux-buffer colour pass through the b200 backend (solver.py:191-201)."""
     from . import backend

@@ -236,9 +236,32 @@ def extras_fixture():
          **outs, **trajs)
 
 
+def energy_fixture():
+    """G = baselines.energy (_assembly.py:78-82) at a few iterates of the extras scene and
+    of the beam (metrics path of harness.run_simulation, harness.py:664-678)."""
+    from vbdsim import baselines
+    out = {}
+    for name, scene in (("extras", lambda: extras_scene()[-1]), ("beam", lambda: beam_system()[2])):
+        s = scene()
+        st = make_state(s)
+        p = SolverParams(h=1.0 / 60.0, n_max=10, rho=0.5, a_ext=G, threads=1)
+        xs, ys, gs = [], [], []
+
+        def rec(state, n):
+            xs.append(state.x.copy())
+            ys.append(state.y.copy())
+            gs.append(baselines.energy(state, p))
+        for _ in range(2):
+            step(st, p, on_iteration=rec)
+        out[f"{name}_x"] = np.array(xs[::5])
+        out[f"{name}_y"] = np.array(ys[::5])
+        out[f"{name}_G"] = np.array(gs[::5])
+    save("energy.npz", **out)
+
+
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"mesh", "coloring", "pass", "steps", "extras"}
+    which = set(sys.argv[1:]) or {"mesh", "coloring", "pass", "steps", "extras", "energy"}
     for name, fn in (("mesh", mesh_fixture), ("coloring", coloring_fixtures), ("pass", pass_fixture),
-                     ("steps", step_fixtures), ("extras", extras_fixture)):
+                     ("steps", step_fixtures), ("extras", extras_fixture), ("energy", energy_fixture)):
         if name in which:
             fn()

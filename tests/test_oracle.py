@@ -174,3 +174,16 @@ def test_extras_steps_bit_exact(O, golden, rho):
     assert (st.x[nb:nb + 25, 2] < 0.185).any()
     assert abs(st.x[nb - 1, 0] - m.rest_positions[-1, 0]) < 1e-12
     assert abs(st.x[nb - 2, 2] - m.rest_positions[-2, 2]) < 1e-12
+
+
+def test_energy_bit_exact(O, golden):
+    """G = 1/(2h^2)|x - y|_M^2 + E(x) (_assembly.py:78-82) at iterates recorded by the
+    reference's own baselines.energy."""
+    from extras import extras_system
+    g = golden("energy.npz")
+    m, s = extras_system(O, golden("extras_scene.npz"))
+    for k in range(len(g["extras_G"])):
+        assert O.variational_energy(s, g["extras_x"][k], g["extras_y"][k], 1 / 60) == g["extras_G"][k]
+    m, fixed, sb = _beam_system(O)
+    for k in range(len(g["beam_G"])):
+        assert O.variational_energy(sb, g["beam_x"][k], g["beam_y"][k], 1 / 60) == g["beam_G"][k]
