@@ -67,7 +67,8 @@ def lib():
                                     f64, P, i64, c_int, c_int, f64, c_int]
     L.oracle_color_pass.restype = c_int
     L.oracle_color_pass_ex.argtypes = ([i64, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
-                                        f64, P, i64, c_int, c_int, f64, c_int] + [P] * 12)
+                                        f64, P, i64, c_int, c_int, f64, c_int] + [P] * 21
+                                       + [f64, f64])
     L.oracle_color_pass_ex.restype = c_int
     L.oracle_local_energy.argtypes = [P, P, P, P, P, P, P, P, P, P, f64, i64, P]
     L.oracle_local_energy.restype = f64
@@ -399,20 +400,30 @@ def build_system(bodies, fixed=()):
 # colour pass + time step
 
 def color_pass(system, x, x_t, y, h, group, mode=0, line_search=False, eps_det=1e-10,
-               n_threads=0):
-    """_native.pyx:513-589 (tets + fixed subset), in place on x (C, fp64)."""
+               n_threads=0, carr=None, mu_c=0.0, eps_v=1e-2):
+    """_native.pyx:513-589, in place on x (C, fp64).  ``carr``: a ContactArrays look-alike
+    (count, idx, gamma, refresh, normal, tangent, k_c, cv_off, cv_cid, cv_slot)."""
     if x.dtype != np.float64 or not x.flags["C_CONTIGUOUS"]:
         raise TypeError("x must be C-contiguous float64")
     g = np.ascontiguousarray(group, dtype=np.int64)
     s = system
-    if s.has_extras:
+    has_c = carr is not None and carr.count > 0
+    if s.has_extras or has_c:
+        c = carr if has_c else None
+        dts = (np.int64, np.float64, np.uint8, np.float64, np.float64, np.float64, np.int64, np.int64,
+               np.int64)
+        keep = [np.ascontiguousarray(getattr(c, k), dtype=dt) for k, dt in zip(
+            ("idx", "gamma", "refresh", "normal", "tangent", "k_c", "cv_off", "cv_cid", "cv_slot"),
+            dts)] if c else []
         rc = lib().oracle_color_pass_ex(
             s.num_vertices, _p(x), _p(np.ascontiguousarray(x_t)), _p(np.ascontiguousarray(y)),
             _p(s.masses), _p(s.tets), _p(s.tet_w), _p(s.tet_vol), _p(s.tet_mu), _p(s.tet_lam),
             _p(s.tet_kd), _p(s.t_off), _p(s.t_id), _p(s.t_slot), _p(s.kind), float(h), _p(g),
             len(g), int(mode), int(bool(line_search)), float(eps_det), int(n_threads),
             _p(s.springs), _p(s.sp_l0), _p(s.sp_k), _p(s.sp_kd), _p(s.s_off), _p(s.s_id),
-            _p(s.s_slot), _p(s.sub_dim), _p(s.sub_basis), _p(s.box_k), _p(s.box_lo), _p(s.box_hi))
+            _p(s.s_slot), _p(s.sub_dim), _p(s.sub_basis), _p(s.box_k), _p(s.box_lo), _p(s.box_hi),
+            *([_p(a) for a in keep] if c else [None] * 9), float(mu_c), float(eps_v))
+        del keep
         if rc != 0:
             raise MemoryError("oracle colour pass failed")
         return

@@ -3,8 +3,8 @@
  * never called by the product path).  Only tests/, __graft_entry__.smoke() and
  * bench.py's cpu_baseline / --impl reference leg may load this library.
  *
- * Plain-C fp64 restatement of the reference VBD colour pass without contacts
- * (tets, springs, fixed / subspace / world-box constraints, mode 0 block-Newton,
+ * Plain-C fp64 restatement of the reference VBD colour pass (tets, springs,
+ * contacts with friction, fixed / subspace / world-box constraints, mode 0 block-Newton,
  * mode 1 diagonal GD, optional 17-trial local line search), written so that its floating-point
  * operation order is the reference's, hence bit-identical to the reference's
  * compiled kernel when built without FP contraction:
@@ -12,7 +12,9 @@
  *   _tet_fc          <- /root/reference/pkg/src/vbdsim/_native.pyx:175-198
  *   _local_energy    <- _native.pyx:201-258 (inertia, tet, spring, box terms)
  *   _assemble        <- _native.pyx:261-317 (inertia + SNH tets + damping),
- *                       319-349 (springs), 401-409 (world box)
+ *                       319-349 (springs), 351-399 (contacts + friction),
+ *                       401-409 (world box)
+ *   _contact_gamma   <- _native.pyx:134-172, _closest_bary <- :79-131
  *   _solve_vertex    <- _native.pyx:412-494 (fixed skip, mode 1, subspace
  *                       1D/2D solve, adjugate solve with relative det guard,
  *                       line search)
@@ -53,7 +55,85 @@ typedef struct {
     const f64 *sp_l0, *sp_k, *sp_kd;
     const i64 *sub_dim;
     const f64 *sub_basis, *box_k, *box_lo, *box_hi;
+    /* contacts (ContactArrays, _system.py:86-96); cv_off NULL = none */
+    const i64 *c_idx, *cv_off, *cv_cid, *cv_slot;
+    const f64 *c_gamma, *c_n, *c_t, *c_kc;
+    const uint8_t *c_refresh;
+    f64 mu_c, eps_u;
 } osys;
+
+/* Voronoi-region closest point on triangle abc, barycentric (_native.pyx:79-131). */
+static void closest_bary(const f64 *p, const f64 *a, const f64 *b, const f64 *c, f64 *bary)
+{
+    f64 ab[3], ac[3], ap[3], bp[3], cp[3];
+    for (int k = 0; k < 3; ++k) {
+        ab[k] = b[k] - a[k];
+        ac[k] = c[k] - a[k];
+        ap[k] = p[k] - a[k];
+    }
+    f64 d1 = ab[0] * ap[0] + ab[1] * ap[1] + ab[2] * ap[2];
+    f64 d2 = ac[0] * ap[0] + ac[1] * ap[1] + ac[2] * ap[2];
+    if (d1 <= 0.0 && d2 <= 0.0) { bary[0] = 1.0; bary[1] = 0.0; bary[2] = 0.0; return; }
+    for (int k = 0; k < 3; ++k) bp[k] = p[k] - b[k];
+    f64 d3 = ab[0] * bp[0] + ab[1] * bp[1] + ab[2] * bp[2];
+    f64 d4 = ac[0] * bp[0] + ac[1] * bp[1] + ac[2] * bp[2];
+    if (d3 >= 0.0 && d4 <= d3) { bary[0] = 0.0; bary[1] = 1.0; bary[2] = 0.0; return; }
+    f64 vc = d1 * d4 - d3 * d2, v, w;
+    if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+        v = d1 / (d1 - d3);
+        bary[0] = 1.0 - v; bary[1] = v; bary[2] = 0.0;
+        return;
+    }
+    for (int k = 0; k < 3; ++k) cp[k] = p[k] - c[k];
+    f64 d5 = ab[0] * cp[0] + ab[1] * cp[1] + ab[2] * cp[2];
+    f64 d6 = ac[0] * cp[0] + ac[1] * cp[1] + ac[2] * cp[2];
+    if (d6 >= 0.0 && d5 <= d6) { bary[0] = 0.0; bary[1] = 0.0; bary[2] = 1.0; return; }
+    f64 vb = d5 * d2 - d1 * d6;
+    if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+        w = d2 / (d2 - d6);
+        bary[0] = 1.0 - w; bary[1] = 0.0; bary[2] = w;
+        return;
+    }
+    f64 va = d3 * d6 - d5 * d4;
+    if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+        w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        bary[0] = 0.0; bary[1] = 1.0 - w; bary[2] = w;
+        return;
+    }
+    f64 denom = 1.0 / (va + vb + vc);
+    v = vb * denom;
+    w = vc * denom;
+    bary[0] = 1.0 - v - w; bary[1] = v; bary[2] = w;
+}
+
+/* Signed contact weights; DCD vertex-triangle anchors follow the current closest point
+ * (_native.pyx:134-172). */
+static void contact_gamma(const osys *s, i64 cid, f64 *gam)
+{
+    for (int k = 0; k < 4; ++k) gam[k] = s->c_gamma[cid * 4 + k];
+    if (!s->c_refresh[cid]) return;
+    i64 v = s->c_idx[cid * 4 + 0], t0 = s->c_idx[cid * 4 + 1], t1 = s->c_idx[cid * 4 + 2],
+        t2 = s->c_idx[cid * 4 + 3];
+    f64 e1[3], e2[3], nrm[3], bary[3], l1 = 0.0, l2 = 0.0, nn, scale;
+    for (int k = 0; k < 3; ++k) {
+        e1[k] = s->x[t1 * 3 + k] - s->x[t0 * 3 + k];
+        e2[k] = s->x[t2 * 3 + k] - s->x[t0 * 3 + k];
+        l1 = l1 + e1[k] * e1[k];
+        l2 = l2 + e2[k] * e2[k];
+    }
+    nrm[0] = e1[1] * e2[2] - e1[2] * e2[1];
+    nrm[1] = e1[2] * e2[0] - e1[0] * e2[2];
+    nrm[2] = e1[0] * e2[1] - e1[1] * e2[0];
+    nn = sqrt(nrm[0] * nrm[0] + nrm[1] * nrm[1] + nrm[2] * nrm[2]);
+    scale = l1 > l2 ? sqrt(l1) : sqrt(l2);
+    if (scale < 1e-30) scale = 1e-30;
+    if (nn < (1e-12 * scale) * scale) return;
+    closest_bary(&s->x[v * 3], &s->x[t0 * 3], &s->x[t1 * 3], &s->x[t2 * 3], bary);
+    gam[0] = 1.0;
+    gam[1] = -bary[0];
+    gam[2] = -bary[1];
+    gam[3] = -bary[2];
+}
 
 /* F = sum_k x_k w_k^T with vertex i at p; cofactor; det by column-0 expansion
  * (_native.pyx:175-198). */
@@ -113,6 +193,20 @@ static f64 local_energy(const osys *s, i64 i, const f64 *p)
                 d = length - s->sp_l0[sp];
                 e = e + ((0.5 * s->sp_k[sp]) * d) * d;
             }
+        }
+    if (s->cv_off) /* _native.pyx:239-249 */
+        for (i64 kk = s->cv_off[i]; kk < s->cv_off[i + 1]; ++kk) {
+            i64 cid = s->cv_cid[kk];
+            f64 gam[4], d = 0.0;
+            contact_gamma(s, cid, gam);
+            for (int k = 0; k < 4; ++k) {
+                i64 oth = s->c_idx[cid * 4 + k];
+                for (int a = 0; a < 3; ++a) {
+                    f64 tmp = (oth == i && k == s->cv_slot[kk]) ? p[a] : s->x[oth * 3 + a];
+                    d = d - (gam[k] * s->c_n[cid * 3 + a]) * tmp;
+                }
+            }
+            if (d > 0.0) e = e + ((0.5 * s->c_kc[cid]) * d) * d;
         }
     if (s->box_k && s->box_k[i] > 0.0)
         for (int a = 0; a < 3; ++a) {
@@ -199,6 +293,53 @@ static void assemble(const osys *s, i64 i, f64 *f, f64 *H)
             }
             for (int a = 0; a < 3; ++a)
                 for (int b = 0; b < 3; ++b) H[a * 3 + b] = H[a * 3 + b] + (1.0 + dsc) * He[a * 3 + b];
+        }
+    if (s->cv_off) /* _native.pyx:351-399 */
+        for (i64 kk = s->cv_off[i]; kk < s->cv_off[i + 1]; ++kk) {
+            i64 cid = s->cv_cid[kk], slot = s->cv_slot[kk];
+            f64 gam[4], d = 0.0, dvec[3], u[2], tvec[3];
+            contact_gamma(s, cid, gam);
+            for (int k = 0; k < 4; ++k) {
+                i64 oth = s->c_idx[cid * 4 + k];
+                for (int a = 0; a < 3; ++a) d = d - (gam[k] * s->c_n[cid * 3 + a]) * s->x[oth * 3 + a];
+            }
+            if (d <= 0.0) continue;
+            const f64 *n = &s->c_n[cid * 3], *ct = &s->c_t[cid * 6];
+            f64 kc = s->c_kc[cid];
+            f64 coef = (kc * d) * gam[slot];
+            for (int a = 0; a < 3; ++a) f[a] = f[a] + coef * n[a];
+            coef = (kc * gam[slot]) * gam[slot];
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) H[a * 3 + b] = H[a * 3 + b] + (coef * n[a]) * n[b];
+            if (s->mu_c > 0.0) {
+                f64 lamc = kc * d, ratio;
+                for (int a = 0; a < 3; ++a) dvec[a] = 0.0;
+                for (int k = 0; k < 4; ++k) {
+                    i64 oth = s->c_idx[cid * 4 + k];
+                    for (int a = 0; a < 3; ++a) dvec[a] = dvec[a] + gam[k] * (s->x[oth * 3 + a] - s->xt[oth * 3 + a]);
+                }
+                for (int k = 0; k < 2; ++k) {
+                    u[k] = 0.0;
+                    for (int a = 0; a < 3; ++a) u[k] = u[k] + ct[a * 2 + k] * dvec[a];
+                }
+                f64 unorm = sqrt(u[0] * u[0] + u[1] * u[1]);
+                if (unorm < 1e-14) {
+                    ratio = 2.0 / s->eps_u;
+                } else {
+                    f64 r = unorm / s->eps_u;
+                    f64 f1 = unorm >= s->eps_u ? 1.0 : 2.0 * r - r * r;
+                    ratio = f1 / unorm;
+                    coef = ((-s->mu_c * lamc) * gam[slot]) * ratio;
+                    for (int a = 0; a < 3; ++a) {
+                        tvec[a] = ct[a * 2 + 0] * u[0] + ct[a * 2 + 1] * u[1];
+                        f[a] = f[a] + coef * tvec[a];
+                    }
+                }
+                coef = (((s->mu_c * lamc) * gam[slot]) * gam[slot]) * ratio;
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b)
+                        H[a * 3 + b] = H[a * 3 + b] + coef * (ct[a * 2 + 0] * ct[b * 2 + 0] + ct[a * 2 + 1] * ct[b * 2 + 1]);
+            }
         }
     if (s->box_k && s->box_k[i] > 0.0) /* _native.pyx:401-409 */
         for (int a = 0; a < 3; ++a) {
@@ -329,14 +470,18 @@ int oracle_color_pass_ex(i64 n_vertices, f64 *x, const f64 *xt, const f64 *y, co
                          int mode, int line_search, f64 eps_det, int n_threads,
                          const i64 *springs, const f64 *sp_l0, const f64 *sp_k, const f64 *sp_kd,
                          const i64 *s_off, const i64 *s_id, const i64 *s_slot, const i64 *sub_dim,
-                         const f64 *sub_basis, const f64 *box_k, const f64 *box_lo, const f64 *box_hi)
+                         const f64 *sub_basis, const f64 *box_k, const f64 *box_lo, const f64 *box_hi,
+                         const i64 *c_idx, const f64 *c_gamma, const uint8_t *c_refresh, const f64 *c_n,
+                         const f64 *c_t, const f64 *c_kc, const i64 *cv_off, const i64 *cv_cid,
+                         const i64 *cv_slot, f64 mu_c, f64 eps_v)
 {
     (void)n_vertices;
     if (ng <= 0) return 0;
     osys s = {x, xt, y, masses, tets, tet_w, tet_vol, tet_mu, tet_lam, tet_kd,
               t_off, t_id, t_slot, kind, h, eps_det, mode, line_search,
               springs, s_off, s_id, s_slot, sp_l0, sp_k, sp_kd, sub_dim, sub_basis,
-              box_k, box_lo, box_hi};
+              box_k, box_lo, box_hi, c_idx, cv_off, cv_cid, cv_slot, c_gamma, c_n, c_t, c_kc,
+              c_refresh, mu_c, eps_v * h};
     f64 *out = (f64 *)malloc((size_t)ng * 3 * sizeof(f64));
     if (!out) return -1;
 #ifdef _OPENMP

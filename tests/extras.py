@@ -19,3 +19,24 @@ def extras_system(O, g):
         fixed=[int(v) for v in g["fixed"]], subspace=sub, boxes=boxes)
     assert np.array_equal(s.color_of, g["color_of"])
     return m, s
+
+
+class ContactCall:
+    """ContactArrays look-alike (_system.py:86-96) of one recorded colour pass."""
+
+    def __init__(self, g, k):
+        for name in ("idx", "gamma", "refresh", "normal", "tangent", "k_c", "cv_off", "cv_cid",
+                     "cv_slot"):
+            setattr(self, name, g[f"call{k}_{name}"])
+        self.count = len(self.idx)
+
+
+def contact_system(O):
+    """tests/golden/make_golden.contact_scene rebuilt with the oracle's builder."""
+    import numpy as np
+    n = 4
+    light = O.generate_beam(n, n, n, 0.3 / (n - 1), density=10.0)
+    heavy0 = O.generate_beam(n, n, n, 0.2 / (n - 1), density=2000.0)
+    heavy = O.build_tet_mesh(heavy0.rest_positions + [0.05, 0.05, 0.3005], heavy0.tets, 2000.0)
+    bottom = [i for i in range(light.num_vertices) if light.rest_positions[i, 2] < 1e-9]
+    return O.build_system([(light, (1e6, 1e7, 0.0)), (heavy, (1e6, 1e7, 0.0))], bottom)

@@ -259,9 +259,68 @@ def energy_fixture():
     save("energy.npz", **out)
 
 
+def contact_scene():
+    """A heavy cube resting on a light cube with a fixed base (a small version of the
+    reference's extreme-mass-ratio acceptance scene, test_acceptance.py:419-433)."""
+    from vbdsim import ContactParams, build_tet_mesh
+    n = 4
+    light = generate_beam(n, n, n, 0.3 / (n - 1), density=10.0)
+    heavy0 = generate_beam(n, n, n, 0.2 / (n - 1), density=2000.0)
+    heavy = build_tet_mesh(heavy0.rest_positions + [0.05, 0.05, 0.3005], heavy0.tets, 2000.0)
+    bottom = [i for i in range(light.num_vertices) if light.rest_positions[i, 2] < 1e-9]
+    s = build_system([Body(light, MaterialParams(1e6, 1e7), k_d=0.01),
+                      Body(heavy, MaterialParams(1e6, 1e7), k_d=0.01)],
+                     [FixedConstraint(i) for i in bottom])
+    p = SolverParams(h=1.0 / 120.0, n_max=10, threads=1, a_ext=G,
+                     contact=ContactParams(k_c=1e6, mu_c=0.5, eps_v=1e-3))
+    return s, p
+
+
+def contact_fixture():
+    """Colour passes with contacts (_native.pyx:351-399) recorded at the kernel seam, and the
+    trajectory of the reference's own step() (DCD/CCD, solver.py:241-324)."""
+    from vbdsim import _backend
+    s, p = contact_scene()
+    native = _backend._impl
+    calls = []
+    seen = [0]
+
+    class Rec:
+        NAME = native.NAME
+
+        @staticmethod
+        def color_pass(system, carr, x, x_t, y, h, group, mode=0, **kw):
+            before = x.copy()
+            native.color_pass(system, carr, x, x_t, y, h, group, mode, **kw)
+            seen[0] += 1
+            if carr is not None and carr.count and len(calls) < 8 and len(group) > 20 and seen[0] % 19 == 1:
+                calls.append(dict(x0=before, x_t=x_t.copy(), y=y.copy(), group=np.array(group),
+                                  x1=x.copy(), mu_c=kw["mu_c"], eps_v=kw["eps_v"], idx=carr.idx,
+                                  gamma=carr.gamma, refresh=carr.refresh, normal=carr.normal,
+                                  tangent=carr.tangent, k_c=carr.k_c, cv_off=carr.cv_off,
+                                  cv_cid=carr.cv_cid, cv_slot=carr.cv_slot))
+    _backend._impl = Rec
+    try:
+        st = make_state(s)
+        xs, counts, flags = [], [], []
+        for _ in range(4):
+            step(st, p)
+            xs.append(st.x.copy())
+            counts.append(len(st.contact_set))
+    finally:
+        _backend._impl = native
+    out = {"steps": np.array(xs), "contact_counts": np.array(counts), "h": np.float64(p.h)}
+    for k, c in enumerate(calls):
+        for name, v in c.items():
+            out[f"call{k}_{name}"] = np.asarray(v)
+    out["num_calls"] = np.int64(len(calls))
+    save("contact_scene.npz", **out)
+
+
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"mesh", "coloring", "pass", "steps", "extras", "energy"}
+    which = set(sys.argv[1:]) or {"mesh", "coloring", "pass", "steps", "extras", "energy", "contact"}
     for name, fn in (("mesh", mesh_fixture), ("coloring", coloring_fixtures), ("pass", pass_fixture),
-                     ("steps", step_fixtures), ("extras", extras_fixture), ("energy", energy_fixture)):
+                     ("steps", step_fixtures), ("extras", extras_fixture), ("energy", energy_fixture),
+                     ("contact", contact_fixture)):
         if name in which:
             fn()

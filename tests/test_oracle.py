@@ -187,3 +187,19 @@ def test_energy_bit_exact(O, golden):
     m, fixed, sb = _beam_system(O)
     for k in range(len(g["beam_G"])):
         assert O.variational_energy(sb, g["beam_x"][k], g["beam_y"][k], 1 / 60) == g["beam_G"][k]
+
+
+def test_contact_passes_bit_exact(O, golden):
+    """Colour passes with contact + friction terms (_native.pyx:351-399, gammas refreshed
+    for DCD vertex-triangle anchors, :134-172) recorded at the reference's kernel seam."""
+    from extras import ContactCall, contact_system
+    g = golden("contact_scene.npz")
+    s = contact_system(O)
+    h = float(g["h"])
+    for k in range(int(g["num_calls"])):
+        x = g[f"call{k}_x0"].copy()
+        O.color_pass(s, x, g[f"call{k}_x_t"], g[f"call{k}_y"], h, g[f"call{k}_group"],
+                     carr=ContactCall(g, k), mu_c=float(g[f"call{k}_mu_c"]),
+                     eps_v=float(g[f"call{k}_eps_v"]))
+        assert np.array_equal(x, g[f"call{k}_x1"]), k
+        assert not np.array_equal(x, g[f"call{k}_x0"])
