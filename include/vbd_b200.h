@@ -196,6 +196,18 @@ int vbd_step_p2p_finish(vbd_ctx* ctx, vbd_step_result* res);
 int vbd_greedy_color(int64_t n, const int64_t* noff, const int64_t* nids, const int64_t* order,
                      int device, int64_t* color_of, int64_t* num_colors);
 
+/* ---- contacts ----------------------------------------------------------------------------- */
+/* The contact set of subsequent colour passes / steps: the reference's ContactArrays
+ * (_system.py:86-96, compile_contacts :306-333) in original numbering -- idx (C,4), gamma (C,4),
+ * refresh (C,), normal (C,3), tangent (C,3,2), k_c (C,), cv_off (N+1), cv_cid, cv_slot -- and
+ * the friction parameters mu_c, eps_v (eps_u = eps_v h).  count 0 clears it.  The colour pass
+ * adds the penalty and friction terms of _native.pyx:351-399 (DCD anchors refreshed,
+ * :134-172).  Detection (broad phase, DCD, CCD) stays with the caller. */
+int vbd_set_contacts(vbd_ctx* ctx, int64_t count, const int64_t* idx, const double* gamma,
+                     const uint8_t* refresh, const double* normal, const double* tangent,
+                     const double* k_c, const int64_t* cv_off, const int64_t* cv_cid,
+                     const int64_t* cv_slot, double mu_c, double eps_v);
+
 /* ---- metrics ------------------------------------------------------------------------------ */
 /* G(x) = 1/(2h^2) |x - y|_M^2 + E(x) at the current iterate (tets, springs, world boxes; no
  * contacts) -- baselines.energy / _assembly.variational_energy (_assembly.py:78-82), the

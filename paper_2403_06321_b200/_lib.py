@@ -107,6 +107,7 @@ SIGNATURES = {
     "vbd_greedy_color": (ctypes.c_int, [i64, P, P, P, ctypes.c_int, P, ctypes.POINTER(i64)]),
     "vbd_profile_color_pass": (ctypes.c_int, [P, f64, i32, P]),
     "vbd_energy": (ctypes.c_int, [P, f64, ctypes.POINTER(f64)]),
+    "vbd_set_contacts": (ctypes.c_int, [P, i64, P, P, P, P, P, P, P, P, P, f64, f64]),
     "vbd_last_error": (ctypes.c_char_p, []),
     "vbd_version": (ctypes.c_char_p, []),
 }

@@ -117,6 +117,23 @@ class DeviceContext:
                                                    _lib.PREC[precision], ctypes.byref(h)))
         return cls(h.value, keepalive=list(beams))
 
+    def set_contacts(self, carr=None, mu_c=0.0, eps_v=1e-2):
+        """Contact set for subsequent colour passes (a ContactArrays, _system.py:86-96)."""
+        L = _lib.lib()
+        if carr is None or not getattr(carr, "count", 0):
+            _lib.check(L.vbd_set_contacts(self._h, 0, *([None] * 9), 0.0, 1e-2))
+            self._contacts = None
+            return
+        keep = dict(idx=_lib.i64c(carr.idx), gamma=_lib.f64c(carr.gamma),
+                    refresh=np.ascontiguousarray(carr.refresh, dtype=np.uint8),
+                    normal=_lib.f64c(carr.normal), tangent=_lib.f64c(carr.tangent),
+                    k_c=_lib.f64c(carr.k_c), cv_off=_lib.i64c(carr.cv_off),
+                    cv_cid=_lib.i64c(carr.cv_cid), cv_slot=_lib.i64c(carr.cv_slot))
+        _lib.check(L.vbd_set_contacts(self._h, int(carr.count), *[_lib.ptr(keep[k]) for k in (
+            "idx", "gamma", "refresh", "normal", "tangent", "k_c", "cv_off", "cv_cid", "cv_slot")],
+            float(mu_c), float(eps_v)))
+        self._contacts = carr
+
     def energy(self, h):
         """G(x) = 1/(2h^2)|x - y|_M^2 + E(x) at the device iterate (_assembly.py:78-82)."""
         g = ctypes.c_double()

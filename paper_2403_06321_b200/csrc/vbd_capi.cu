@@ -141,6 +141,7 @@ struct vbd_ctx {
     std::vector<BeamDev> beams;
     DBuf beams_dev;
     std::vector<int> hinv;  // host copy of inv (protocol colour pass)
+    std::vector<int> hperm; // host copy of perm (contact sets)
     K1Variant k1 = k1_variant_from_env();
     // P2P slab halo: flags[0..1] written by the neighbours, [2] epoch, [3] error word
     DBuf p2p_flags;
@@ -161,6 +162,10 @@ struct vbd_ctx {
     // non-tet terms (springs, world box, subspace): host-built systems only; global K1
     bool has_extras = false;
     DBuf soff, sp_oth, sp_par, box, sub_idx, sub;
+    // contact set (vbd_set_contacts; 0 = none)
+    long long ncontacts = 0;
+    double mu_c = 0.0, eps_v = 1e-2;
+    DBuf coff, ccid, cslot, cidx, creal;
     // K1T tile pipeline (compact layout, in-place range passes): tiles of 64 vertices per
     // colour, their neighbour lists and 8-byte entries
     bool tiles = false;
@@ -779,6 +784,13 @@ K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
     a.sub_idx = c->sub_idx.as<int>();
     a.sub = c->sub.as<R4>();
     a.h = (R)c->mat_h;
+    a.coff = c->ncontacts ? c->coff.as<long long>() : nullptr;
+    a.ccid = c->ccid.as<int>();
+    a.cslot = c->cslot.as<int>();
+    a.cidx = c->cidx.as<int4>();
+    a.creal = c->creal.as<R4>();
+    a.mu_c = (R)c->mu_c;
+    a.eps_u = (R)(c->eps_v * c->mat_h);
     a.off = c->eoff.as<long long>();
     a.pos = c->pos.as<typename Vec4<R>::T>();
     a.xt = c->xt.as<typename Vec4<R>::T>();
@@ -882,7 +894,7 @@ void launch_k1_tiles_w(const K1TArgs<R>& ta, int W, int stages, int occ, size_t 
 
 template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
 {
-    if (!c->tiles || a.group || a.out || a.line_search || !a.kinds) return false;
+    if (!c->tiles || a.group || a.out || a.line_search || !a.kinds || a.coff) return false;
     int col = -1;
     for (int k = 0; k < c->ncolors; ++k)
         if (c->cbeg[k] == a.vbeg && c->ccnt[k] == a.count) col = k;
@@ -1077,7 +1089,7 @@ template <typename R> void enqueue_step_p2p(vbd_ctx* c)
 bool use_persistent(const vbd_ctx* c)
 {
     const char* e = getenv("VBD_PERSIST");
-    if (c->has_extras) return false;
+    if (c->has_extras || c->ncontacts) return false;
     if (e && *e) return atoi(e) != 0 && c->inplace && c->ncolors <= VBD_PERSIST_MAX_COLORS;
     // measured on B200: grid.sync() costs more than a graph-node launch (C1 0.36 vs 0.25
     // ms/step), so the per-colour graph is the default everywhere
@@ -2213,6 +2225,86 @@ int vbd_greedy_color(int64_t n, const int64_t* noff, const int64_t* nids, const 
             mx = std::max<long long>(mx, hc[v]);
         }
         if (num_colors) *num_colors = mx + 1;
+    });
+}
+
+int vbd_set_contacts(vbd_ctx* c, int64_t count, const int64_t* idx, const double* gamma,
+                     const uint8_t* refresh, const double* normal, const double* tangent,
+                     const double* k_c, const int64_t* cv_off, const int64_t* cv_cid,
+                     const int64_t* cv_slot, double mu_c, double eps_v)
+{
+    return guarded([&] {
+        if (!c) fail(VBD_ERR_ARG, "NULL context");
+        if (count < 0) fail(VBD_ERR_ARG, "negative contact count");
+        c->ncontacts = 0;
+        if (count == 0) return;
+        if (!idx || !gamma || !refresh || !normal || !tangent || !k_c || !cv_off || !cv_cid || !cv_slot)
+            fail(VBD_ERR_ARG, "missing contact arrays");
+        if (!(eps_v > 0.0) || mu_c < 0.0) fail(VBD_ERR_ARG, "bad friction parameters");
+        if (c->hinv.empty()) {
+            c->hinv.resize(c->n);
+            CK(cudaMemcpy(c->hinv.data(), c->inv.p, c->n * 4, cudaMemcpyDeviceToHost));
+        }
+        const long long N = c->n;
+        if ((long long)c->hperm.size() != N) {
+            c->hperm.resize(N);
+            for (long long o = 0; o < N; ++o) c->hperm[c->hinv[o]] = (int)o;
+        }
+        const std::vector<int>& perm = c->hperm;
+        const bool f64p = c->precision == VBD_PREC_F64;
+        std::vector<int4> ci(count);
+        std::vector<double> cr(16 * count);
+        for (long long k = 0; k < count; ++k) {
+            int ids[4];
+            for (int q = 0; q < 4; ++q) {
+                const int64_t v = idx[4 * k + q];
+                if (v < 0 || v >= N) fail(VBD_ERR_ARG, "contact index out of range");
+                ids[q] = c->hinv[v];
+            }
+            ci[k] = make_int4(ids[0], ids[1], ids[2], ids[3]);
+            double* r = &cr[16 * k];
+            for (int q = 0; q < 4; ++q) r[q] = gamma[4 * k + q];
+            r[4] = normal[3 * k]; r[5] = normal[3 * k + 1]; r[6] = normal[3 * k + 2]; r[7] = k_c[k];
+            for (int q = 0; q < 4; ++q) r[8 + q] = tangent[6 * k + q];
+            r[12] = tangent[6 * k + 4]; r[13] = tangent[6 * k + 5];
+            r[14] = refresh[k] ? 1.0 : 0.0; r[15] = 0.0;
+        }
+        const long long ns = c->nsolve;
+        std::vector<long long> off(ns + 1, 0);
+        for (long long i = 0; i < ns; ++i) {
+            const int o = perm[i];
+            off[i + 1] = off[i] + (cv_off[o + 1] - cv_off[o]);
+        }
+        std::vector<int> cc(std::max<long long>(off[ns], 1)), cs(std::max<long long>(off[ns], 1));
+        for (long long i = 0; i < ns; ++i) {
+            const int o = perm[i];
+            long long w = off[i];
+            for (long long kk = cv_off[o]; kk < cv_off[o + 1]; ++kk, ++w) {
+                if (cv_cid[kk] < 0 || cv_cid[kk] >= count || cv_slot[kk] < 0 || cv_slot[kk] > 3)
+                    fail(VBD_ERR_ARG, "bad contact incidence");
+                cc[w] = (int)cv_cid[kk];
+                cs[w] = (int)cv_slot[kk];
+            }
+        }
+        cudaStream_t s = c->stream;
+        upload(c->coff, off.data(), off.size(), s);
+        upload(c->ccid, cc.data(), cc.size(), s);
+        upload(c->cslot, cs.data(), cs.size(), s);
+        upload(c->cidx, ci.data(), ci.size(), s);
+        if (f64p) {
+            upload(c->creal, cr.data(), cr.size(), s);
+        } else {
+            std::vector<float> crf(cr.begin(), cr.end());
+            upload(c->creal, crf.data(), crf.size(), s);
+        }
+        CK(cudaStreamSynchronize(s));
+        c->mu_c = mu_c;
+        c->eps_v = eps_v;
+        c->ncontacts = count;
+        if (c->gexec) {  // captured step graphs hold the old contact pointers
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
     });
 }
 

@@ -47,6 +47,15 @@ template <typename R> struct K1Args {
     const int* sub_idx;
     const R4* sub;
     R h;
+    // contacts (ContactArrays, _system.py:86-96; nullptr = none): per solved vertex CSR of
+    // (contact, slot); per contact cidx = 4 colour-major ids and creal = 4 R4:
+    // {gamma0..3} {n.xyz, k_c} {t00 t01 t10 t11} {t20 t21 refresh 0}
+    const long long* coff;
+    const int* ccid;
+    const int* cslot;
+    const int4* cidx;
+    const R4* creal;
+    R mu_c, eps_u;
     // fused slab halo push (multi-GPU, peer memory): the first nb[0] vertices of the colour
     // range face the left neighbour, the next nb[1] the right one; their new positions are
     // also stored into the neighbour's ghost block (peer_pos[s] + peer_off[s])
@@ -59,11 +68,170 @@ template <typename R> struct K1Args {
 // v = vbeg + g (or group[g]).  UM: one material per vertex (damping hoisted out of the loop).
 // Local energy G_i of vertex v at position p (_native.pyx:201-258, tet + inertia terms),
 // summed over the W lanes of the group (identical in every lane).
+// Voronoi-region closest point on triangle abc, barycentric (_native.pyx:79-131)
+template <typename R>
+__device__ void closest_bary(const R* p, const R* a, const R* b, const R* c, R* bary)
+{
+    R ab[3], ac[3], ap[3], bp[3], cp[3];
+    for (int k = 0; k < 3; ++k) {
+        ab[k] = b[k] - a[k];
+        ac[k] = c[k] - a[k];
+        ap[k] = p[k] - a[k];
+    }
+    const R d1 = ab[0] * ap[0] + ab[1] * ap[1] + ab[2] * ap[2];
+    const R d2 = ac[0] * ap[0] + ac[1] * ap[1] + ac[2] * ap[2];
+    if (d1 <= R(0) && d2 <= R(0)) { bary[0] = R(1); bary[1] = R(0); bary[2] = R(0); return; }
+    for (int k = 0; k < 3; ++k) bp[k] = p[k] - b[k];
+    const R d3 = ab[0] * bp[0] + ab[1] * bp[1] + ab[2] * bp[2];
+    const R d4 = ac[0] * bp[0] + ac[1] * bp[1] + ac[2] * bp[2];
+    if (d3 >= R(0) && d4 <= d3) { bary[0] = R(0); bary[1] = R(1); bary[2] = R(0); return; }
+    const R vc = d1 * d4 - d3 * d2;
+    if (vc <= R(0) && d1 >= R(0) && d3 <= R(0)) {
+        const R v = d1 / (d1 - d3);
+        bary[0] = R(1) - v; bary[1] = v; bary[2] = R(0);
+        return;
+    }
+    for (int k = 0; k < 3; ++k) cp[k] = p[k] - c[k];
+    const R d5 = ab[0] * cp[0] + ab[1] * cp[1] + ab[2] * cp[2];
+    const R d6 = ac[0] * cp[0] + ac[1] * cp[1] + ac[2] * cp[2];
+    if (d6 >= R(0) && d5 <= d6) { bary[0] = R(0); bary[1] = R(0); bary[2] = R(1); return; }
+    const R vb = d5 * d2 - d1 * d6;
+    if (vb <= R(0) && d2 >= R(0) && d6 <= R(0)) {
+        const R w = d2 / (d2 - d6);
+        bary[0] = R(1) - w; bary[1] = R(0); bary[2] = w;
+        return;
+    }
+    const R va = d3 * d6 - d5 * d4;
+    if (va <= R(0) && (d4 - d3) >= R(0) && (d5 - d6) >= R(0)) {
+        const R w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        bary[0] = R(0); bary[1] = R(1) - w; bary[2] = w;
+        return;
+    }
+    const R denom = R(1) / (va + vb + vc);
+    const R v = vb * denom, w = vc * denom;
+    bary[0] = R(1) - v - w; bary[1] = v; bary[2] = w;
+}
+
+// signed contact weights; DCD vertex-triangle anchors track the current closest point
+// (_native.pyx:134-172)
+template <typename R>
+__device__ void contact_gamma(const K1Args<R>& a, int cid, R* gam)
+{
+    typedef typename Vec4<R>::T R4;
+    const R4 g = a.creal[4 * cid], t3 = a.creal[4 * cid + 3];
+    gam[0] = g.x; gam[1] = g.y; gam[2] = g.z; gam[3] = g.w;
+    if (t3.z == R(0)) return;
+    const int4 id = a.cidx[cid];
+    const R4 pv = a.pos[id.x], p0 = a.pos[id.y], p1 = a.pos[id.z], p2 = a.pos[id.w];
+    const R e1[3] = {p1.x - p0.x, p1.y - p0.y, p1.z - p0.z};
+    const R e2[3] = {p2.x - p0.x, p2.y - p0.y, p2.z - p0.z};
+    const R l1 = e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2];
+    const R l2 = e2[0] * e2[0] + e2[1] * e2[1] + e2[2] * e2[2];
+    const R nr[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+    const R nn = sqrt(nr[0] * nr[0] + nr[1] * nr[1] + nr[2] * nr[2]);
+    R scale = l1 > l2 ? sqrt(l1) : sqrt(l2);
+    if (scale < R(1e-30)) scale = R(1e-30);
+    if (nn < R(1e-12) * scale * scale) return;
+    const R P[3] = {pv.x, pv.y, pv.z}, A[3] = {p0.x, p0.y, p0.z}, B[3] = {p1.x, p1.y, p1.z},
+            C[3] = {p2.x, p2.y, p2.z};
+    R bary[3];
+    closest_bary<R>(P, A, B, C, bary);
+    gam[0] = R(1);
+    gam[1] = -bary[0];
+    gam[2] = -bary[1];
+    gam[3] = -bary[2];
+}
+
+// contact penalty of G_i with vertex v at p (_native.pyx:239-249)
+template <typename R>
+__device__ R contact_energy(const K1Args<R>& a, int v, const R* p)
+{
+    typedef typename Vec4<R>::T R4;
+    R e = R(0);
+    for (long long kk = a.coff[v]; kk < a.coff[v + 1]; ++kk) {
+        const int cid = a.ccid[kk], slot = a.cslot[kk];
+        R gam[4];
+        contact_gamma<R>(a, cid, gam);
+        const int4 id = a.cidx[cid];
+        const int ids[4] = {id.x, id.y, id.z, id.w};
+        const R4 nk = a.creal[4 * cid + 1];
+        R d = R(0);
+        for (int k = 0; k < 4; ++k) {
+            const R4 q = a.pos[ids[k]];
+            const bool me = ids[k] == v && k == slot;
+            d -= gam[k] * (nk.x * (me ? p[0] : q.x) + nk.y * (me ? p[1] : q.y) + nk.z * (me ? p[2] : q.z));
+        }
+        if (d > R(0)) e += R(0.5) * nk.w * d * d;
+    }
+    return e;
+}
+
+// contact penalty + friction force / Hessian of vertex v (_native.pyx:351-399)
+template <typename R>
+__device__ void contact_terms(const K1Args<R>& a, int v, R* f, R* H)
+{
+    typedef typename Vec4<R>::T R4;
+    for (long long kk = a.coff[v]; kk < a.coff[v + 1]; ++kk) {
+        const int cid = a.ccid[kk], slot = a.cslot[kk];
+        R gam[4];
+        contact_gamma<R>(a, cid, gam);
+        const int4 id = a.cidx[cid];
+        const int ids[4] = {id.x, id.y, id.z, id.w};
+        const R4 nk = a.creal[4 * cid + 1];
+        R d = R(0);
+        for (int k = 0; k < 4; ++k) {
+            const R4 q = a.pos[ids[k]];
+            d -= gam[k] * (nk.x * q.x + nk.y * q.y + nk.z * q.z);
+        }
+        if (d <= R(0)) continue;
+        const R n[3] = {nk.x, nk.y, nk.z};
+        const R gs = gam[slot];
+        R coef = nk.w * d * gs;
+        for (int c = 0; c < 3; ++c) f[c] += coef * n[c];
+        coef = nk.w * gs * gs;
+        H[0] += coef * n[0] * n[0]; H[1] += coef * n[0] * n[1]; H[2] += coef * n[0] * n[2];
+        H[3] += coef * n[1] * n[1]; H[4] += coef * n[1] * n[2]; H[5] += coef * n[2] * n[2];
+        if (a.mu_c > R(0)) {
+            const R4 ta = a.creal[4 * cid + 2], tb = a.creal[4 * cid + 3];
+            const R T[3][2] = {{ta.x, ta.y}, {ta.z, ta.w}, {tb.x, tb.y}};
+            const R lamc = nk.w * d;
+            R dv[3] = {R(0), R(0), R(0)};
+            for (int k = 0; k < 4; ++k) {
+                const R4 q = a.pos[ids[k]], qt = a.xt[ids[k]];
+                dv[0] += gam[k] * (q.x - qt.x);
+                dv[1] += gam[k] * (q.y - qt.y);
+                dv[2] += gam[k] * (q.z - qt.z);
+            }
+            const R u0 = T[0][0] * dv[0] + T[1][0] * dv[1] + T[2][0] * dv[2];
+            const R u1 = T[0][1] * dv[0] + T[1][1] * dv[1] + T[2][1] * dv[2];
+            const R un = sqrt(u0 * u0 + u1 * u1);
+            R ratio;
+            if (un < R(1e-14)) {
+                ratio = R(2) / a.eps_u;
+            } else {
+                const R r = un / a.eps_u;
+                const R f1 = un >= a.eps_u ? R(1) : R(2) * r - r * r;
+                ratio = f1 / un;
+                const R cf = -a.mu_c * lamc * gs * ratio;
+                for (int c = 0; c < 3; ++c) f[c] += cf * (T[c][0] * u0 + T[c][1] * u1);
+            }
+            const R ch = a.mu_c * lamc * gs * gs * ratio;
+            H[0] += ch * (T[0][0] * T[0][0] + T[0][1] * T[0][1]);
+            H[1] += ch * (T[0][0] * T[1][0] + T[0][1] * T[1][1]);
+            H[2] += ch * (T[0][0] * T[2][0] + T[0][1] * T[2][1]);
+            H[3] += ch * (T[1][0] * T[1][0] + T[1][1] * T[1][1]);
+            H[4] += ch * (T[1][0] * T[2][0] + T[1][1] * T[2][1]);
+            H[5] += ch * (T[2][0] * T[2][0] + T[2][1] * T[2][1]);
+        }
+    }
+}
+
 // spring and world-box terms of G_i (_native.pyx:226-237, 250-257), vertex at p
 template <typename R>
 __device__ R extras_energy(const K1Args<R>& a, int v, const R* p)
 {
     R e = R(0);
+    if (a.soff)
     for (long long k = a.soff[v]; k < a.soff[v + 1]; ++k) {
         const typename Vec4<R>::T q = a.pos[a.sp_oth[k]], sp = a.sp_par[k];
         const R d0 = p[0] - q.x, d1 = p[1] - q.y, d2 = p[2] - q.z;
@@ -75,6 +243,7 @@ __device__ R extras_energy(const K1Args<R>& a, int v, const R* p)
             e += R(0.5) * sp.y * t * t;
         }
     }
+    if (a.coff) e += contact_energy<R>(a, v, p);
     if (a.box) {
         const typename Vec4<R>::T lo = a.box[2 * v], hi = a.box[2 * v + 1];
         if (lo.w > R(0)) {
@@ -95,6 +264,7 @@ __device__ R extras_energy(const K1Args<R>& a, int v, const R* p)
 template <typename R>
 __device__ void extras_terms(const K1Args<R>& a, int v, const R* xi, const R* dx, R* f, R* H)
 {
+    if (a.soff)
     for (long long k = a.soff[v]; k < a.soff[v + 1]; ++k) {
         const typename Vec4<R>::T q = a.pos[a.sp_oth[k]], sp = a.sp_par[k];
         R dv[3] = {xi[0] - q.x, xi[1] - q.y, xi[2] - q.z};
@@ -124,6 +294,7 @@ __device__ void extras_terms(const K1Args<R>& a, int v, const R* xi, const R* dx
 #pragma unroll
         for (int c = 0; c < 6; ++c) H[c] += (R(1) + dsc) * he[c];
     }
+    if (a.coff) contact_terms<R>(a, v, f, H);
     if (a.box) {
         const typename Vec4<R>::T lo = a.box[2 * v], hi = a.box[2 * v + 1];
         if (lo.w > R(0)) {
@@ -226,7 +397,7 @@ __device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int 
     }
 #pragma unroll
     for (int o = W / 2; o > 0; o >>= 1) e += __shfl_xor_sync(gmask, e, o, W);
-    if (a.soff) e += extras_energy<R>(a, v, p);
+    if (a.soff || a.coff || a.box) e += extras_energy<R>(a, v, p);
     R ein = R(0);
     const R d0 = p[0] - y4.x, d1 = p[1] - y4.y, d2 = p[2] - y4.z;
     ein = ein + ((R(0.5) * y4.w) * d0) * d0;
@@ -384,9 +555,9 @@ __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int la
     if (!LS && lane != 0) return;
     vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM && end > beg, mv.dsc, mv.opd);
     R d[3];
-    if (a.soff) {
+    if (a.soff || a.coff || a.box) {
         extras_terms<R>(a, v, xi, dx, f, H);
-        const int si = a.sub_idx[v];
+        const int si = a.sub_idx ? a.sub_idx[v] : -1;
         if (si >= 0 && a.mode == 0) subspace_solve<R>(a.sub + 3 * si, f, H, a.eps_det, d);
         else block_solve<R>(f, H, a.eps_det, a.mode, d);
     } else {

@@ -128,14 +128,26 @@ def test_springs_through_the_plugin_match_native(ref, with_b200):
     assert np.abs(a.x - b.x).max() / diag <= 1e-10
 
 
-def test_contacts_raise(ref, with_b200):
+def test_contact_scene_through_the_plugin_matches_native(ref, with_b200):
+    """A heavy cube dropped onto a light one: the reference's own detection (broad phase,
+    DCD, CCD, friction) with the b200 colour pass, against the native backend."""
     vbdsim, _ = ref
-    import paper_2403_06321_b200.backend as B
-    cube = vbdsim.generate_cube(2, 0.4, density=1000.0)
-    s = vbdsim.build_system([vbdsim.Body(cube, vbdsim.MaterialParams(2e5, 8e5))])
-
-    class _Contacts:
-        count = 1
-    x = np.ascontiguousarray(s.rest_positions.copy())
-    with pytest.raises(NotImplementedError):
-        B.color_pass(s, _Contacts(), x, x, x, 1 / 60, np.arange(s.num_vertices))
+    n = 4
+    light = vbdsim.generate_beam(n, n, n, 0.3 / (n - 1), density=10.0)
+    heavy0 = vbdsim.generate_beam(n, n, n, 0.2 / (n - 1), density=2000.0)
+    heavy = vbdsim.build_tet_mesh(heavy0.rest_positions + [0.05, 0.05, 0.3005], heavy0.tets, 2000.0)
+    bottom = [i for i in range(light.num_vertices) if light.rest_positions[i, 2] < 1e-9]
+    s = vbdsim.build_system([vbdsim.Body(light, vbdsim.MaterialParams(1e6, 1e7), k_d=0.01),
+                             vbdsim.Body(heavy, vbdsim.MaterialParams(1e6, 1e7), k_d=0.01)],
+                            [vbdsim.FixedConstraint(i) for i in bottom])
+    p = vbdsim.SolverParams(h=1 / 120, n_max=10, threads=1, a_ext=G,
+                            contact=vbdsim.ContactParams(k_c=1e6, mu_c=0.5, eps_v=1e-3))
+    a, b = vbdsim.make_state(s), vbdsim.make_state(s)
+    for _ in range(4):
+        vbdsim.step(a, p)
+    with with_b200():
+        for _ in range(4):
+            vbdsim.step(b, p)
+    assert len(b.contact_set) > 0
+    diag = float(np.linalg.norm(s.rest_positions.max(0) - s.rest_positions.min(0)))
+    assert np.abs(a.x - b.x).max() / diag <= 1e-10
