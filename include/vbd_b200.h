@@ -208,6 +208,20 @@ int vbd_set_contacts(vbd_ctx* ctx, int64_t count, const int64_t* idx, const doub
                      const double* k_c, const int64_t* cv_off, const int64_t* cv_cid,
                      const int64_t* cv_slot, double mu_c, double eps_v);
 
+/* Contact detection on the device for vbd_step (solver.py:241-324, contact.py): the collision
+ * surface (outward triangles (S,3) and unique edges (E,2) of the merged tet bodies, original
+ * ids), the hash cell (1.5 x median rest surface edge, contact.py:205-215) and ContactParams.
+ * Each step then runs DCD at x_t, CCD every n_col iterations, aux-buffer colour passes and K3
+ * without blending colliding vertices.  ntri 0 disables it. */
+int vbd_set_collision(vbd_ctx* ctx, int64_t ntri, const int64_t* tris, int64_t nedge, const int64_t* edges,
+                      double cell, double k_c, double mu_c, double eps_v, double dcd_radius,
+                      int32_t has_max_depth, double max_depth, int32_t n_col);
+/* one detection pass on the current state (which 0: DCD at x_t; 1: CCD x_t -> x), for tests:
+ * count, and up to cap records (original ids, signed weights, normal, 1 = CCD) */
+int vbd_detect_contacts(vbd_ctx* ctx, int32_t which, int64_t cap, int64_t* count, int64_t* idx,
+                        double* gamma, double* normal, int32_t* ccd);
+int vbd_get_colliding(vbd_ctx* ctx, uint8_t* flags); /* (N,) sticky colliding flags of the step */
+
 /* ---- metrics ------------------------------------------------------------------------------ */
 /* G(x) = 1/(2h^2) |x - y|_M^2 + E(x) at the current iterate (tets, springs, world boxes; no
  * contacts) -- baselines.energy / _assembly.variational_energy (_assembly.py:78-82), the

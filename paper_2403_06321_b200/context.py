@@ -134,6 +134,45 @@ class DeviceContext:
             float(mu_c), float(eps_v)))
         self._contacts = carr
 
+    def set_collision(self, system=None, contact=None, n_col=4):
+        """Device contact detection for step(): the collision surface of ``system`` (its
+        collision mesh, mapped to global ids) and ContactParams ``contact``; None disables."""
+        L = _lib.lib()
+        mesh = getattr(system, "collision_mesh", None) if system is not None else None
+        if contact is None or mesh is None or len(mesh.surface_tris) == 0:
+            _lib.check(L.vbd_set_collision(self._h, 0, None, 0, None, 1.0, 1.0, 0.0, 1e-2, 0.0, 0, 0.0, 1))
+            return
+        cmap = np.asarray(system.collision_map, dtype=np.int64)
+        tris = _lib.i64c(cmap[mesh.surface_tris])
+        edges = _lib.i64c(cmap[mesh.surface_edges]).reshape(-1, 2)
+        if len(mesh.surface_edges):  # contact.py:205-215: 1.5 x the median rest surface edge
+            e = mesh.rest_positions[mesh.surface_edges]
+            cell = 1.5 * float(np.median(np.linalg.norm(e[:, 1] - e[:, 0], axis=1)))
+        else:
+            cell = float(mesh.bbox_diagonal()) or 1.0
+        md = contact.max_depth
+        _lib.check(L.vbd_set_collision(self._h, len(tris), _lib.ptr(tris), len(edges), _lib.ptr(edges),
+                                       cell, float(contact.k_c), float(contact.mu_c), float(contact.eps_v),
+                                       float(contact.dcd_radius), 0 if md is None else 1,
+                                       0.0 if md is None else float(md), int(n_col)))
+
+    def detect_contacts(self, which, cap=100000):
+        """One detection pass (0: DCD at x_t, 1: CCD x_t -> x): (idx, gamma, normal, is_ccd)."""
+        n = ctypes.c_int64()
+        idx = np.zeros((cap, 4), np.int64)
+        gam = np.zeros((cap, 4))
+        nrm = np.zeros((cap, 3))
+        ccd = np.zeros(cap, np.int32)
+        _lib.check(_lib.lib().vbd_detect_contacts(self._h, int(which), cap, ctypes.byref(n), _lib.ptr(idx),
+                                                  _lib.ptr(gam), _lib.ptr(nrm), _lib.ptr(ccd)))
+        k = min(n.value, cap)
+        return idx[:k], gam[:k], nrm[:k], ccd[:k].astype(bool)
+
+    def colliding(self):
+        out = np.zeros(self.n, np.uint8)
+        _lib.check(_lib.lib().vbd_get_colliding(self._h, _lib.ptr(out)))
+        return out.astype(bool)
+
     def energy(self, h):
         """G(x) = 1/(2h^2)|x - y|_M^2 + E(x) at the device iterate (_assembly.py:78-82)."""
         g = ctypes.c_double()

@@ -17,6 +17,7 @@
 #include "vbd_common.cuh"
 #include "vbd_kernels.cuh"
 #include "vbd_tiles.cuh"
+#include "vbd_contact.cuh"
 
 // K1 launch variant (lanes per vertex W, entries per lane per iteration U, min blocks/SM);
 // selected per context from VBD_K1 (e.g. "8x1", "4x2", "4x2b3"), default below.
@@ -162,10 +163,19 @@ struct vbd_ctx {
     // non-tet terms (springs, world box, subspace): host-built systems only; global K1
     bool has_extras = false;
     DBuf soff, sp_oth, sp_par, box, sub_idx, sub;
-    // contact set (vbd_set_contacts; 0 = none)
+    // contact set (vbd_set_contacts, or the device detection below; 0 = none)
     long long ncontacts = 0;
     double mu_c = 0.0, eps_v = 1e-2;
     DBuf coff, ccid, cslot, cidx, creal;
+    // device contact detection for step() (vbd_set_collision): surface primitives
+    // (colour-major ids, original order), per-vertex active mask, sticky colliding flags, the
+    // DCD records of the step (and their codes) and the CCD records of the last pass
+    bool coll_on = false;
+    DBuf csv, ctri, cedge, cactive, ccoll, dcd_recs, dcd_codes, ccd_recs;
+    int nsv = 0, ntri = 0, nedge = 0;
+    long long ndcd = 0, nccd = 0;
+    double coll_cell = 1.0, coll_kc = 1.0, coll_dcd_r = 1e-3, coll_max_depth = 0.0;
+    int coll_has_max_depth = 0, coll_ncol = 4;
     // K1T tile pipeline (compact layout, in-place range passes): tiles of 64 vertices per
     // colour, their neighbour lists and 8-byte entries
     bool tiles = false;
@@ -940,8 +950,9 @@ template <typename R> void color_sweep(vbd_ctx* c, int color, int iter, bool che
     a.line_search = c->cur.line_search ? 1 : 0;
     a.vbeg = (int)c->cbeg[color];
     a.count = (int)c->ccnt[color];
-    if (!c->inplace) {
-        // aux-buffer semantics over the contiguous colour range: compute into `out`, then copy
+    if (!c->inplace || c->ncontacts) {
+        // aux-buffer semantics over the contiguous colour range (invalid colouring, or contacts
+        // coupling vertices of one colour): compute into `out`, then copy
         a.out = c->out.as<typename Vec4<R>::T>();
         launch_k1<R>(c, a, s);
         CK(cudaMemcpyAsync(c->pos.as<char>() + c->cbeg[color] * c->r4(), c->out.p,
@@ -1013,7 +1024,7 @@ template <typename R> void enqueue_iter_end(vbd_ctx* c, int n)
     int blend = (n >= 2 && w != 1.0) ? 1 : 0;
     k3_chebyshev<R><<<blocks_for(c->n), 256, 0, c->stream>>>(
         c->pos.as<R4>(), hist, (int)c->n, w, blend, c->flag.as<unsigned long long>(),
-        c->perm.as<int>(), c->stepctr.as<int>(), n);
+        c->perm.as<int>(), c->stepctr.as<int>(), n, c->coll_on ? c->ccoll.as<unsigned char>() : nullptr);
 }
 
 template <typename R> void enqueue_end(vbd_ctx* c)
@@ -1147,6 +1158,230 @@ void read_result(vbd_ctx* c, vbd_step_result* res)
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// device contact detection (vbd_contact.cuh) and the contact step
+
+template <typename R> CollArgs<R> coll_args(vbd_ctx* c, const DBuf& xs, const DBuf& xe, double margin)
+{
+    CollArgs<R> a;
+    a.sv = c->csv.as<int>();
+    a.tri = c->ctri.as<int4>();
+    a.edge = c->cedge.as<int2>();
+    a.nsv = c->nsv;
+    a.ntri = c->ntri;
+    a.nedge = c->nedge;
+    a.active = c->cactive.as<unsigned char>();
+    a.xs = xs.as<typename Vec4<R>::T>();
+    a.xe = xe.as<typename Vec4<R>::T>();
+    a.cell = c->coll_cell;
+    a.pad = margin + 1e-12 * c->coll_cell;
+    return a;
+}
+
+// cells of primitives `what` (0 vertex, 1 triangle, 2 edge), sorted by key
+template <typename R> long long grid_cells(vbd_ctx* c, const CollArgs<R>& a, int what, int n, DBuf& key, DBuf& own)
+{
+    cudaStream_t s = c->stream;
+    DBuf cnt, off;
+    cnt.alloc((size_t)std::max(n, 1) * 8);
+    if (n) k_cell_count<R><<<blocks_for(n), 256, 0, s>>>(a, what, n, cnt.as<long long>());
+    CK(cudaGetLastError());
+    exclusive_offsets(cnt.as<long long>(), n, off, s);
+    const long long m = read_scalar<long long>(off.as<long long>() + n, s);
+    key.alloc((size_t)std::max<long long>(m, 1) * 8);
+    own.alloc((size_t)std::max<long long>(m, 1) * 4);
+    if (n) k_cell_emit<R><<<blocks_for(n), 256, 0, s>>>(a, what, n, off.as<long long>(), key.as<unsigned long long>(),
+                                                        own.as<int>());
+    CK(cudaGetLastError());
+    if (m) sort_pairs_u64_i32(key, own, m, s);
+    return m;
+}
+
+void unique_u64(DBuf& keys, long long& n, cudaStream_t s)
+{
+    if (n == 0) return;
+    DBuf out, nsel, tmp;
+    out.alloc((size_t)n * 8);
+    nsel.alloc(8);
+    size_t tb = 0;
+    CK(cub::DeviceSelect::Unique(nullptr, tb, keys.as<unsigned long long>(), out.as<unsigned long long>(),
+                                 nsel.as<long long>(), (int64_t)n, s));
+    tmp.alloc(tb);
+    CK(cub::DeviceSelect::Unique(tmp.p, tb, keys.as<unsigned long long>(), out.as<unsigned long long>(),
+                                 nsel.as<long long>(), (int64_t)n, s));
+    n = read_scalar<long long>(nsel.p, s);
+    keys.swap(out);
+}
+
+// candidate codes (ascending, unique): vertex-triangle k * ntri + t, or edge-edge e * nedge + o
+template <typename R> long long broad_phase(vbd_ctx* c, const CollArgs<R>& a, bool ee, DBuf& codes)
+{
+    cudaStream_t s = c->stream;
+    DBuf qk, qo, tk, to;
+    long long nq, nt;
+    if (ee) {
+        nt = grid_cells<R>(c, a, 2, a.nedge, tk, to);
+        nq = nt;
+    } else {
+        nt = grid_cells<R>(c, a, 1, a.ntri, tk, to);
+        nq = grid_cells<R>(c, a, 0, a.nsv, qk, qo);
+    }
+    const unsigned long long* qkey = ee ? tk.as<unsigned long long>() : qk.as<unsigned long long>();
+    const int* qown = ee ? to.as<int>() : qo.as<int>();
+    const long long width = ee ? a.nedge : a.ntri;
+    DBuf cnt, off;
+    cnt.alloc((size_t)std::max<long long>(nq, 1) * 8);
+    if (nq) {
+        if (ee) k_cell_join<false, true><<<blocks_for(nq), 256, 0, s>>>(qkey, qown, nq, tk.as<unsigned long long>(), to.as<int>(), nt, width, cnt.as<long long>(), nullptr, nullptr);
+        else k_cell_join<false, false><<<blocks_for(nq), 256, 0, s>>>(qkey, qown, nq, tk.as<unsigned long long>(), to.as<int>(), nt, width, cnt.as<long long>(), nullptr, nullptr);
+    }
+    CK(cudaGetLastError());
+    exclusive_offsets(cnt.as<long long>(), nq, off, s);
+    long long m = read_scalar<long long>(off.as<long long>() + nq, s);
+    codes.alloc((size_t)std::max<long long>(m, 1) * 8);
+    if (nq && m) {
+        if (ee) k_cell_join<true, true><<<blocks_for(nq), 256, 0, s>>>(qkey, qown, nq, tk.as<unsigned long long>(), to.as<int>(), nt, width, nullptr, off.as<long long>(), codes.as<unsigned long long>());
+        else k_cell_join<true, false><<<blocks_for(nq), 256, 0, s>>>(qkey, qown, nq, tk.as<unsigned long long>(), to.as<int>(), nt, width, nullptr, off.as<long long>(), codes.as<unsigned long long>());
+    }
+    CK(cudaGetLastError());
+    if (m) {
+        sort_keys_u64(codes, m, s);
+        unique_u64(codes, m, s);
+    }
+    return m;
+}
+
+__global__ void k_drop_known(const unsigned long long* __restrict__ codes, long long n,
+                             const unsigned long long* __restrict__ known, long long nk, int* acc)
+{
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n || !acc[i] || nk == 0) return;
+    const long long j = lower_key(known, nk, codes[i]);
+    if (j < nk && known[j] == codes[i]) acc[i] = 0;  // already tracked by DCD (update_ccd)
+}
+
+template <typename T>
+__global__ void k_compact(const T* __restrict__ in, const int* __restrict__ acc, const long long* __restrict__ off,
+                          long long n, T* __restrict__ out)
+{
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n && acc[i]) out[off[i]] = in[i];
+}
+
+// keep the accepted records (and codes) in candidate order
+long long compact_recs(vbd_ctx* c, const DBuf& recs, const DBuf& codes, const DBuf& acc, long long n, DBuf& out_recs,
+                       DBuf* out_codes)
+{
+    cudaStream_t s = c->stream;
+    DBuf off;
+    exclusive_offsets(acc.as<int>(), n, off, s);
+    const long long m = read_scalar<long long>(off.as<long long>() + n, s);
+    out_recs.alloc((size_t)std::max<long long>(m, 1) * sizeof(ContactRec));
+    if (n) k_compact<ContactRec><<<blocks_for(n), 256, 0, s>>>(recs.as<ContactRec>(), acc.as<int>(), off.as<long long>(), n, out_recs.as<ContactRec>());
+    if (out_codes) {
+        out_codes->alloc((size_t)std::max<long long>(m, 1) * 8);
+        if (n) k_compact<unsigned long long><<<blocks_for(n), 256, 0, s>>>(codes.as<unsigned long long>(), acc.as<int>(), off.as<long long>(), n, out_codes->as<unsigned long long>());
+    }
+    CK(cudaGetLastError());
+    return m;
+}
+
+// DCD at x_t (solver.py:241-260): the step's DCD records; clears the colliding flags
+template <typename R> void detect_dcd(vbd_ctx* c)
+{
+    cudaStream_t s = c->stream;
+    const CollArgs<R> a = coll_args<R>(c, c->xt, c->xt, c->coll_dcd_r);
+    DBuf codes, recs, acc;
+    const long long n = broad_phase<R>(c, a, false, codes);
+    recs.alloc((size_t)std::max<long long>(n, 1) * sizeof(ContactRec));
+    acc.alloc((size_t)std::max<long long>(n, 1) * 4);
+    if (n) k_dcd_vt<R><<<blocks_for(n, 128), 128, 0, s>>>(a, codes.as<unsigned long long>(), n, c->coll_dcd_r, c->coll_kc,
+                                                     c->coll_has_max_depth, c->coll_max_depth, recs.as<ContactRec>(),
+                                                     acc.as<int>());
+    CK(cudaGetLastError());
+    c->ndcd = compact_recs(c, recs, codes, acc, n, c->dcd_recs, &c->dcd_codes);
+    c->nccd = 0;
+    CK(cudaMemsetAsync(c->ccoll.p, 0, c->n, s));
+}
+
+// CCD between x_t and the current iterate (solver.py:263-279): vertex-triangle then edge-edge
+template <typename R> void detect_ccd(vbd_ctx* c)
+{
+    cudaStream_t s = c->stream;
+    const CollArgs<R> a = coll_args<R>(c, c->xt, c->pos, 0.0);
+    DBuf vcodes, vrecs, vacc, ecodes, erecs, eacc, vt_out, ee_out;
+    const long long nv = broad_phase<R>(c, a, false, vcodes);
+    vrecs.alloc((size_t)std::max<long long>(nv, 1) * sizeof(ContactRec));
+    vacc.alloc((size_t)std::max<long long>(nv, 1) * 4);
+    if (nv) {
+        k_ccd_vt<R><<<blocks_for(nv, 128), 128, 0, s>>>(a, vcodes.as<unsigned long long>(), nv, c->coll_kc, vrecs.as<ContactRec>(), vacc.as<int>());
+        k_drop_known<<<blocks_for(nv), 256, 0, s>>>(vcodes.as<unsigned long long>(), nv, c->dcd_codes.as<unsigned long long>(), c->ndcd, vacc.as<int>());
+    }
+    CK(cudaGetLastError());
+    const long long mv = compact_recs(c, vrecs, vcodes, vacc, nv, vt_out, nullptr);
+    const long long ne = a.nedge ? broad_phase<R>(c, a, true, ecodes) : 0;
+    erecs.alloc((size_t)std::max<long long>(ne, 1) * sizeof(ContactRec));
+    eacc.alloc((size_t)std::max<long long>(ne, 1) * 4);
+    if (ne) k_ccd_ee<R><<<blocks_for(ne, 128), 128, 0, s>>>(a, ecodes.as<unsigned long long>(), ne, c->coll_kc, erecs.as<ContactRec>(), eacc.as<int>());
+    CK(cudaGetLastError());
+    const long long me = compact_recs(c, erecs, ecodes, eacc, ne, ee_out, nullptr);
+    c->nccd = mv + me;
+    c->ccd_recs.alloc((size_t)std::max<long long>(c->nccd, 1) * sizeof(ContactRec));
+    if (mv) CK(cudaMemcpyAsync(c->ccd_recs.p, vt_out.p, mv * sizeof(ContactRec), cudaMemcpyDeviceToDevice, s));
+    if (me) CK(cudaMemcpyAsync(c->ccd_recs.as<ContactRec>() + mv, ee_out.p, me * sizeof(ContactRec), cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+// mark_flags at `x` and compile the DCD + CCD records into the K1 contact arrays
+template <typename R> void compile_contact_set(vbd_ctx* c, const DBuf& x)
+{
+    typedef typename Vec4<R>::T R4;
+    cudaStream_t s = c->stream;
+    const long long n = c->ndcd + c->nccd;
+    DBuf all;
+    all.alloc((size_t)std::max<long long>(n, 1) * sizeof(ContactRec));
+    if (c->ndcd) CK(cudaMemcpyAsync(all.p, c->dcd_recs.p, c->ndcd * sizeof(ContactRec), cudaMemcpyDeviceToDevice, s));
+    if (c->nccd) CK(cudaMemcpyAsync(all.as<ContactRec>() + c->ndcd, c->ccd_recs.p, c->nccd * sizeof(ContactRec), cudaMemcpyDeviceToDevice, s));
+    c->ncontacts = n;
+    if (n == 0) return;
+    k_mark_flags<R><<<blocks_for(n), 256, 0, s>>>(all.as<ContactRec>(), (int)n, x.as<R4>(), c->ccoll.as<unsigned char>());
+    c->cidx.alloc((size_t)n * sizeof(int4));
+    c->creal.alloc((size_t)n * 4 * sizeof(R4));
+    DBuf inc, dummy;
+    inc.alloc((size_t)n * 4 * 8);
+    k_pack_contacts<R><<<blocks_for(n), 256, 0, s>>>(all.as<ContactRec>(), (int)n, c->cidx.as<int4>(), c->creal.as<R4>(),
+                                                     inc.as<unsigned long long>());
+    CK(cudaGetLastError());
+    sort_keys_u64(inc, 4 * n, s);
+    // incidence of solved vertices only (keys of fixed / ghost vertices sort last)
+    c->coff.alloc((size_t)(c->nsolve + 1) * 8);
+    c->ccid.alloc((size_t)4 * n * 4);
+    c->cslot.alloc((size_t)4 * n * 4);
+    k_contact_csr<<<blocks_for(4 * n), 256, 0, s>>>(inc.as<unsigned long long>(), 4 * n, c->nsolve, c->coff.as<long long>(),
+                                                   c->ccid.as<int>(), c->cslot.as<int>());
+    CK(cudaGetLastError());
+    c->mu_c = c->mu_c;
+}
+
+// one step with contacts: DCD at x_t, CCD every n_col iterations, aux-buffer colour passes
+// (contacts couple vertices of one colour), K3 keeping colliding vertices unblended
+template <typename R> void do_step_contacts(vbd_ctx* c, vbd_step_result* res)
+{
+    detect_dcd<R>(c);
+    compile_contact_set<R>(c, c->xt);
+    enqueue_begin<R>(c);
+    for (int n = 1; n <= c->cur.n_max; ++n) {
+        if ((n - 1) % c->coll_ncol == 0) {
+            detect_ccd<R>(c);
+            compile_contact_set<R>(c, c->pos);
+        }
+        for (int col = 0; col < c->ncolors; ++col) color_sweep<R>(c, col, n, c->cur.rho == 0.0);
+        enqueue_iter_end<R>(c, n);
+    }
+    enqueue_end<R>(c);
+    read_result(c, res);
+}
+
 template <typename R> void do_step(vbd_ctx* c, const vbd_step_params* p, int n_steps, vbd_step_result* res)
 {
     validate_params(p);
@@ -1157,6 +1392,10 @@ template <typename R> void do_step(vbd_ctx* c, const vbd_step_params* p, int n_s
     cudaStream_t s = c->stream;
     CK(cudaMemsetAsync(c->flag.p, 0xff, 8, s));
     CK(cudaMemsetAsync(c->stepctr.p, 0, 4, s));
+    if (c->coll_on) {
+        for (int k = 0; k < n_steps; ++k) do_step_contacts<R>(c, res);
+        return;
+    }
     if (use_persistent(c) && !p->line_search) {
         c->omega_dev.alloc((p->n_max + 1) * sizeof(double));
         CK(cudaMemcpyAsync(c->omega_dev.p, c->omegas.data(), (p->n_max + 1) * sizeof(double),
@@ -2305,6 +2544,116 @@ int vbd_set_contacts(vbd_ctx* c, int64_t count, const int64_t* idx, const double
             cudaGraphExecDestroy(c->gexec);
             c->gexec = nullptr;
         }
+    });
+}
+
+int vbd_set_collision(vbd_ctx* c, int64_t ntri, const int64_t* tris, int64_t nedge, const int64_t* edges,
+                      double cell, double k_c, double mu_c, double eps_v, double dcd_radius,
+                      int32_t has_max_depth, double max_depth, int32_t n_col)
+{
+    return guarded([&] {
+        if (!c) fail(VBD_ERR_ARG, "NULL context");
+        c->coll_on = false;
+        c->ncontacts = 0;
+        if (c->gexec) {
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+        if (ntri <= 0) return;
+        if (!tris || (nedge > 0 && !edges)) fail(VBD_ERR_ARG, "missing surface arrays");
+        if (!(cell > 0.0) || !(k_c > 0.0) || mu_c < 0.0 || !(eps_v > 0.0) || dcd_radius < 0.0 || n_col < 1)
+            fail(VBD_ERR_ARG, "bad contact parameters");
+        if (c->hinv.empty()) {
+            c->hinv.resize(c->n);
+            CK(cudaMemcpy(c->hinv.data(), c->inv.p, c->n * 4, cudaMemcpyDeviceToHost));
+        }
+        const long long N = c->n;
+        auto map = [&](int64_t v) {
+            if (v < 0 || v >= N) fail(VBD_ERR_ARG, "surface index out of range");
+            return c->hinv[v];
+        };
+        std::vector<int64_t> sv(tris, tris + 3 * ntri);
+        std::sort(sv.begin(), sv.end());
+        sv.erase(std::unique(sv.begin(), sv.end()), sv.end());
+        std::vector<int> svm(sv.size());
+        for (size_t k = 0; k < sv.size(); ++k) svm[k] = map(sv[k]);
+        std::vector<int4> tr(ntri);
+        for (long long k = 0; k < ntri; ++k) tr[k] = make_int4(map(tris[3 * k]), map(tris[3 * k + 1]), map(tris[3 * k + 2]), 0);
+        std::vector<int2> ed(std::max<int64_t>(nedge, 1));
+        for (long long k = 0; k < nedge; ++k) ed[k] = make_int2(map(edges[2 * k]), map(edges[2 * k + 1]));
+        std::vector<unsigned char> act(N);
+        for (long long v = 0; v < N; ++v) act[v] = v < c->nfree_all ? 1 : 0;
+        cudaStream_t s = c->stream;
+        upload(c->csv, svm.data(), svm.size(), s);
+        upload(c->ctri, tr.data(), tr.size(), s);
+        upload(c->cedge, ed.data(), ed.size(), s);
+        upload(c->cactive, act.data(), act.size(), s);
+        c->ccoll.alloc((size_t)std::max<long long>(N, 1));
+        CK(cudaMemsetAsync(c->ccoll.p, 0, N, s));
+        CK(cudaStreamSynchronize(s));
+        c->nsv = (int)sv.size();
+        c->ntri = (int)ntri;
+        c->nedge = (int)std::max<int64_t>(nedge, 0);
+        c->coll_cell = cell;
+        c->coll_kc = k_c;
+        c->mu_c = mu_c;
+        c->eps_v = eps_v;
+        c->coll_dcd_r = dcd_radius;
+        c->coll_has_max_depth = has_max_depth;
+        c->coll_max_depth = max_depth;
+        c->coll_ncol = n_col;
+        c->coll_on = true;
+    });
+}
+
+int vbd_detect_contacts(vbd_ctx* c, int32_t which, int64_t cap, int64_t* count, int64_t* idx, double* gamma,
+                        double* normal, int32_t* ccd)
+{
+    return guarded([&] {
+        if (!c || !count) fail(VBD_ERR_ARG, "NULL argument");
+        if (!c->coll_on) fail(VBD_ERR_ARG, "no collision surface (vbd_set_collision)");
+        auto run = [&](auto tag) {
+            typedef decltype(tag) R;
+            if (which == 0) {
+                detect_dcd<R>(c);
+                compile_contact_set<R>(c, c->xt);
+            } else {
+                detect_ccd<R>(c);
+                compile_contact_set<R>(c, c->pos);
+            }
+        };
+        if (c->precision == VBD_PREC_F64) run(double{});
+        else run(float{});
+        const long long n = which == 0 ? c->ndcd : c->nccd;
+        *count = n;
+        if (!idx || cap <= 0) return;
+        std::vector<ContactRec> h((size_t)n);
+        if (n) CK(cudaMemcpy(h.data(), (which == 0 ? c->dcd_recs : c->ccd_recs).p, n * sizeof(ContactRec),
+                             cudaMemcpyDeviceToHost));
+        if (c->hperm.size() != (size_t)c->n) {
+            c->hperm.resize(c->n);
+            for (long long o = 0; o < c->n; ++o) c->hperm[c->hinv[o]] = (int)o;
+        }
+        for (long long k = 0; k < std::min<long long>(n, cap); ++k) {
+            const int ids[4] = {h[k].idx.x, h[k].idx.y, h[k].idx.z, h[k].idx.w};
+            for (int q = 0; q < 4; ++q) {
+                idx[4 * k + q] = c->hperm[ids[q]];
+                if (gamma) gamma[4 * k + q] = h[k].g[q];
+            }
+            if (normal)
+                for (int q = 0; q < 3; ++q) normal[3 * k + q] = h[k].n[q];
+            if (ccd) ccd[k] = h[k].ccd;
+        }
+    });
+}
+
+int vbd_get_colliding(vbd_ctx* c, uint8_t* flags)
+{
+    return guarded([&] {
+        if (!c || !flags) fail(VBD_ERR_ARG, "NULL argument");
+        std::vector<unsigned char> h(c->n, 0);
+        if (c->coll_on) CK(cudaMemcpy(h.data(), c->ccoll.p, c->n, cudaMemcpyDeviceToHost));
+        for (long long o = 0; o < c->n; ++o) flags[o] = h[c->hinv.empty() ? o : c->hinv[o]];
     });
 }
 

@@ -901,11 +901,12 @@ __global__ void k2_step_init(const StepArgs<R> s)
 template <typename R>
 __device__ __forceinline__ void k3_vertex(typename Vec4<R>::T* pos, typename Vec4<R>::T* hist,
                                           double omega, int blend, unsigned long long* flag,
-                                          const int* perm, const int* stepctr, int iter, int i)
+                                          const int* perm, const int* stepctr, int iter, int i,
+                                          const unsigned char* coll = nullptr)
 {
     typedef typename Vec4<R>::T R4;
     R4 x = pos[i];
-    if (blend) {
+    if (blend && !(coll && coll[i])) {  // colliding vertices keep x (solver.py:229-230)
         const R4 pp = hist[i];
         const R w = (R)omega;
         x.x = w * (x.x - pp.x) + pp.x;
@@ -921,10 +922,11 @@ __device__ __forceinline__ void k3_vertex(typename Vec4<R>::T* pos, typename Vec
 template <typename R>
 __global__ void k3_chebyshev(typename Vec4<R>::T* pos, typename Vec4<R>::T* hist, int n,
                              double omega, int blend, unsigned long long* flag,
-                             const int* perm, const int* stepctr, int iter)
+                             const int* perm, const int* stepctr, int iter,
+                             const unsigned char* coll = nullptr)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) k3_vertex<R>(pos, hist, omega, blend, flag, perm, stepctr, iter, i);
+    if (i < n) k3_vertex<R>(pos, hist, omega, blend, flag, perm, stepctr, iter, i, coll);
 }
 
 // K4: velocity commit (solver.py:319-323); skipped when the step reported a non-finite state.

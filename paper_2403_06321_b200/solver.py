@@ -213,8 +213,8 @@ def chebyshev_omega(rho: float, n: int) -> float:
 
 
 def _check_supported(state, params):
-    if params.contact is not None:
-        raise NotImplementedError("contact handling is not on the B200 hot path")
+    """Contacts: detection runs on the device (vbd_set_collision) when the system has a
+    collision surface (solver.py:235-238)."""
 
 
 def _dparams(params):
@@ -236,10 +236,20 @@ def initialize(state, params) -> np.ndarray:
     return state._h["x"]
 
 
+def _collision(ctx, system, params):
+    key = (params.contact, params.n_col)
+    if getattr(ctx, "_coll_key", None) != key:
+        ctx.set_collision(system if params.contact is not None else None, params.contact, params.n_col)
+        ctx._coll_key = key
+
+
 def step(state, params, on_iteration=None):
     """Advance one step of size params.h on the GPU (solver.py:291-324)."""
     _check_supported(state, params)
     ctx = device_context(state.system, params.precision, params.device)
+    _collision(ctx, state.system, params)
+    if params.contact is not None and on_iteration is not None:
+        raise NotImplementedError("on_iteration with contacts: use step() without the callback")
     state._bind(ctx)
     state._upload(_INPUTS)
     if on_iteration is None:

@@ -315,6 +315,47 @@ def contact_fixture():
             out[f"call{k}_{name}"] = np.asarray(v)
     out["num_calls"] = np.int64(len(calls))
     save("contact_scene.npz", **out)
+    contact_detection_fixture()
+
+
+def contact_detection_fixture():
+    """The reference's own contact sets right after each DCD / CCD pass of the contact scene
+    (solver.py:241-279, contact.py): inputs x_t, x and the records in order."""
+    from vbdsim import solver as S
+    s, p = contact_scene()
+    rec = []
+    dcd0, ccd0 = S._detect_dcd, S._detect_ccd
+
+    def snap(tag, state):
+        cs = state.contact_set
+        lst = cs.dcd if tag == "dcd" else cs.ccd
+        rec.append(dict(kind=tag, x_t=state.x_t.copy(), x=state.x.copy(),
+                        idx=np.array([c.indices for c in lst], dtype=np.int64).reshape(-1, 4),
+                        gamma=np.array([c.gammas() for c in lst]).reshape(-1, 4),
+                        normal=np.array([c.normal for c in lst]).reshape(-1, 3),
+                        ee=np.array([c.kind == "ee" for c in lst], dtype=bool),
+                        flags=cs.colliding_flag.copy()))
+
+    def dcd(state, params):
+        dcd0(state, params)
+        snap("dcd", state)
+
+    def ccd(state, params):
+        ccd0(state, params)
+        snap("ccd", state)
+    S._detect_dcd, S._detect_ccd = dcd, ccd
+    try:
+        st = make_state(s)
+        for _ in range(4):
+            step(st, p)
+    finally:
+        S._detect_dcd, S._detect_ccd = dcd0, ccd0
+    out = {"num": np.int64(len(rec))}
+    for k, r in enumerate(rec):
+        out[f"r{k}_which"] = np.int64(0 if r["kind"] == "dcd" else 1)
+        for name in ("x_t", "x", "idx", "gamma", "normal", "ee", "flags"):
+            out[f"r{k}_{name}"] = r[name]
+    save("contact_detection.npz", **out)
 
 
 if __name__ == "__main__":

@@ -176,7 +176,8 @@ def test_local_solve_and_color_pass(V):
         state.x = ref
 
 
-def test_unsupported_raise(V):
+def test_contacts_with_iteration_callback_raise(V):
     system, state = beam_state(V)
     with pytest.raises(NotImplementedError):
-        V.step(state, V.SolverParams(h=0.01, contact=V.ContactParams(k_c=1e5)))
+        V.step(state, V.SolverParams(h=0.01, contact=V.ContactParams(k_c=1e5)),
+               on_iteration=lambda st, n: None)
