@@ -32,7 +32,8 @@ _INPUTS = ("x_t", "v_t", "v_prev")
 
 @dataclass(frozen=True)
 class ContactParams:
-    """Accepted for API compatibility; contact is not on the B200 hot path."""
+    """solver.py ContactParams: penalty stiffness, friction, DCD radius and depth bound;
+    detection and contact terms run on the device."""
 
     k_c: float
     mu_c: float = 0.0
