@@ -2194,13 +2194,17 @@ int vbd_step_begin(vbd_ctx* c, const vbd_step_params* p)
         c->in_step = true;
         CK(cudaMemsetAsync(c->flag.p, 0xff, 8, c->stream));
         CK(cudaMemsetAsync(c->stepctr.p, 0, 4, c->stream));
-        if (c->precision == VBD_PREC_F64) {
-            ensure_materials<double>(c, p->h);
-            enqueue_begin<double>(c);
-        } else {
-            ensure_materials<float>(c, p->h);
-            enqueue_begin<float>(c);
-        }
+        auto begin = [&](auto tag) {
+            typedef decltype(tag) R;
+            ensure_materials<R>(c, p->h);
+            if (c->coll_on) {  // DCD at x_t (solver.py:298-300)
+                detect_dcd<R>(c);
+                compile_contact_set<R>(c, c->xt);
+            }
+            enqueue_begin<R>(c);
+        };
+        if (c->precision == VBD_PREC_F64) begin(double{});
+        else begin(float{});
         CK(cudaGetLastError());
     });
 }
@@ -2210,6 +2214,15 @@ int vbd_step_color(vbd_ctx* c, int32_t color, int32_t iter)
     return guarded([&] {
         if (!c || !c->in_step) fail(VBD_ERR_ARG, "no step in progress");
         if (color < 0 || color >= c->ncolors) fail(VBD_ERR_ARG, "bad colour");
+        if (c->coll_on && color == 0 && (iter - 1) % c->coll_ncol == 0) {  // CCD (solver.py:308-309)
+            if (c->precision == VBD_PREC_F64) {
+                detect_ccd<double>(c);
+                compile_contact_set<double>(c, c->pos);
+            } else {
+                detect_ccd<float>(c);
+                compile_contact_set<float>(c, c->pos);
+            }
+        }
         bool check = c->cur.rho == 0.0;
         if (c->precision == VBD_PREC_F64) color_sweep<double>(c, color, iter, check);
         else color_sweep<float>(c, color, iter, check);
@@ -2664,8 +2677,9 @@ int vbd_energy(vbd_ctx* c, double h, double* G)
         if (!(h > 0.0)) fail(VBD_ERR_ARG, "h must be positive");
         cudaStream_t s = c->stream;
         const unsigned b1 = blocks_for(std::max<long long>(c->nsolve, 1) * 4), b2 = blocks_for(std::max<long long>(c->n, 1));
+        const unsigned b3 = c->ncontacts ? blocks_for(c->ncontacts) : 0;
         DBuf part;
-        part.alloc((size_t)(b1 + b2) * sizeof(double));
+        part.alloc((size_t)(b1 + b2 + b3) * sizeof(double));
         auto run = [&](auto tag) {
             typedef decltype(tag) R;
             if (std::isnan(c->mat_h)) ensure_materials<R>(c, 1.0);  // rest data only
@@ -2673,11 +2687,14 @@ int vbd_energy(vbd_ctx* c, double h, double* G)
             k_energy_elastic<R, 4><<<b1, 256, 0, s>>>(a, (int)c->nsolve, part.as<double>());
             k_energy_vertex<R><<<b2, 256, 0, s>>>(a, c->mass.as<R>(), (int)c->n, 1.0 / (h * h),
                                                  part.as<double>() + b1);
+            if (c->ncontacts)
+                k_energy_contact<R><<<b3, 256, 0, s>>>(c->cidx.as<int4>(), c->creal.as<typename Vec4<R>::T>(),
+                                                       (int)c->ncontacts, a.pos, part.as<double>() + b1 + b2);
         };
         if (c->precision == VBD_PREC_F64) run(double{});
         else run(float{});
         CK(cudaGetLastError());
-        std::vector<double> h(b1 + b2);
+        std::vector<double> h(b1 + b2 + b3);
         CK(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         double acc = 0.0;

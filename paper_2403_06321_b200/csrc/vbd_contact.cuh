@@ -574,3 +574,32 @@ __global__ void k_contact_csr(const unsigned long long* __restrict__ keys, long 
         for (long long u = v + 1; u <= nsolve; ++u) off[u] = m;
 }
 
+
+// contact penalty energy sum_c 1/2 k_c max(0, d)^2 with the detection-time weights
+// (_assembly.py:49-56, Contact.gap contact.py:70-74)
+template <typename R>
+__global__ void __launch_bounds__(256) k_energy_contact(const int4* __restrict__ cidx,
+                                                        const typename Vec4<R>::T* __restrict__ creal, int n,
+                                                        const typename Vec4<R>::T* __restrict__ x, double* partial)
+{
+    __shared__ double red[256];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double e = 0.0;
+    if (i < n) {
+        const int4 id = cidx[i];
+        const int ids[4] = {id.x, id.y, id.z, id.w};
+        const typename Vec4<R>::T g = creal[4 * i], nk = creal[4 * i + 1];
+        const double gam[4] = {g.x, g.y, g.z, g.w};
+        D3 acc = gam[0] * ld3<R>(x, ids[0]);
+        for (int k = 1; k < 4; ++k) acc = acc + gam[k] * ld3<R>(x, ids[k]);
+        const double d = fmax(0.0, -(acc.x * nk.x + acc.y * nk.y + acc.z * nk.z));
+        e = 0.5 * (double)nk.w * d * d;
+    }
+    red[threadIdx.x] = e;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}

@@ -249,8 +249,6 @@ def step(state, params, on_iteration=None):
     _check_supported(state, params)
     ctx = device_context(state.system, params.precision, params.device)
     _collision(ctx, state.system, params)
-    if params.contact is not None and on_iteration is not None:
-        raise NotImplementedError("on_iteration with contacts: use step() without the callback")
     state._bind(ctx)
     state._upload(_INPUTS)
     if on_iteration is None:

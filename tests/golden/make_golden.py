@@ -241,10 +241,13 @@ def energy_fixture():
     of the beam (metrics path of harness.run_simulation, harness.py:664-678)."""
     from vbdsim import baselines
     out = {}
-    for name, scene in (("extras", lambda: extras_scene()[-1]), ("beam", lambda: beam_system()[2])):
+    for name, scene in (("extras", lambda: extras_scene()[-1]), ("beam", lambda: beam_system()[2]),
+                        ("contact", lambda: contact_scene()[0])):
         s = scene()
         st = make_state(s)
         p = SolverParams(h=1.0 / 60.0, n_max=10, rho=0.5, a_ext=G, threads=1)
+        if name == "contact":
+            p = contact_scene()[1]
         xs, ys, gs = [], [], []
 
         def rec(state, n):

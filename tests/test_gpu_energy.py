@@ -58,3 +58,25 @@ def test_energy_per_iteration_metric(V, O):
     assert len(rows) == 10
     assert np.allclose(rows, want, rtol=1e-11, atol=0)
     assert rows[-1] < rows[0]  # VBD decreases G within the step
+
+
+def test_energy_per_iteration_with_contacts(V, golden):
+    """The metrics path of a contact scene: device detection inside step(on_iteration=...),
+    G including the contact penalty (_assembly.py:49-56), against the reference's values."""
+    g = golden("energy.npz")
+    n = 4
+    light = V.generate_beam(n, n, n, 0.3 / (n - 1), density=10.0)
+    heavy0 = V.generate_beam(n, n, n, 0.2 / (n - 1), density=2000.0)
+    heavy = V.build_tet_mesh(heavy0.rest_positions + [0.05, 0.05, 0.3005], heavy0.tets, 2000.0)
+    bottom = [i for i in range(light.num_vertices) if light.rest_positions[i, 2] < 1e-9]
+    system = V.build_system([V.Body(light, V.MaterialParams(1e6, 1e7), k_d=0.01),
+                             V.Body(heavy, V.MaterialParams(1e6, 1e7), k_d=0.01)],
+                            [V.FixedConstraint(i) for i in bottom])
+    params = V.SolverParams(h=1 / 120, n_max=10, a_ext=G, precision="fp64",
+                            contact=V.ContactParams(k_c=1e6, mu_c=0.5, eps_v=1e-3))
+    state = V.make_state(system)
+    rows = []
+    for _ in range(2):
+        V.step(state, params, on_iteration=lambda st, k: rows.append(V.energy(st, params)))
+    got = np.array(rows[::5])
+    assert np.allclose(got, g["contact_G"], rtol=1e-8, atol=0), (got, g["contact_G"])
