@@ -223,10 +223,15 @@ int vbd_detect_contacts(vbd_ctx* ctx, int32_t which, int64_t cap, int64_t* count
 int vbd_get_colliding(vbd_ctx* ctx, uint8_t* flags); /* (N,) sticky colliding flags of the step */
 
 /* ---- metrics ------------------------------------------------------------------------------ */
-/* G(x) = 1/(2h^2) |x - y|_M^2 + E(x) at the current iterate (tets, springs, world boxes; no
- * contacts) -- baselines.energy / _assembly.variational_energy (_assembly.py:78-82), the
- * per-iteration metric of harness.run_simulation (harness.py:664-678).  Synchronous. */
+/* G(x) = 1/(2h^2) |x - y|_M^2 + E(x) at the current iterate (tets, springs, world boxes and the
+ * penalty of the active contact set) -- baselines.energy / _assembly.variational_energy
+ * (_assembly.py:78-82), the per-iteration metric of harness.run_simulation
+ * (harness.py:664-678).  Synchronous. */
 int vbd_energy(vbd_ctx* ctx, double h, double* G);
+/* vbd_energy plus the other two per-iteration metric columns of harness.py:664-670 in the same
+ * reduction: the active contact count (len(state.contact_set)) and the largest contact gap at
+ * the iterate (max_penetration, solver.py:327-332; 0 without contacts).  Either may be NULL. */
+int vbd_energy_metrics(vbd_ctx* ctx, double h, double* G, int64_t* contacts, double* max_gap);
 
 /* ---- measurement ------------------------------------------------------------------------ */
 /* average device time of one colour-pass launch per colour over `reps` sweeps (CUDA events on

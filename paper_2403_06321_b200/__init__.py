@@ -7,14 +7,16 @@ vertex sweep for Stable Neo-Hookean tets: hand-written sm_100a CUDA kernels in
 
 from .backend import NAME as BACKEND_NAME
 from .context import Beam, DeviceContext
-from .errors import DegenerateTet, IndexOutOfRange, NonFiniteState, VbdError
+from .errors import DegenerateTet, IndexOutOfRange, NonFiniteState, SchemaError, VbdError
+from .harness import (METRICS_HEADER, ObjectConfig, OutputConfig, SceneConfig, export_frame,
+                      load_frame, parse_scene, run_simulation, scene_build, serialize_scene)
 from .materials import MaterialParams
 from .mesh import (ColorPartition, SpringNet, TetMesh, VertexAdjacency, build_spring_net,
                    build_tet_mesh, generate_beam, generate_chain, generate_cube, greedy_color,
-                   incidence, incidence_from_elements)
+                   incidence, incidence_from_elements, load_node_ele)
 from .solver import (ContactParams, SimState, SolverParams, accelerate, chebyshev_omega,
                      color_pass, device_context, energy, inertia_target, initialize, local_solve,
-                     make_state, step)
+                     make_state, max_penetration, metrics, step)
 from .system import (Body, ConstraintArrays, FixedConstraint, SubspaceConstraint, System,
                      WorldBoxConstraint, build_system, compile_constraints)
 

@@ -107,6 +107,8 @@ SIGNATURES = {
     "vbd_greedy_color": (ctypes.c_int, [i64, P, P, P, ctypes.c_int, P, ctypes.POINTER(i64)]),
     "vbd_profile_color_pass": (ctypes.c_int, [P, f64, i32, P]),
     "vbd_energy": (ctypes.c_int, [P, f64, ctypes.POINTER(f64)]),
+    "vbd_energy_metrics": (ctypes.c_int, [P, f64, ctypes.POINTER(f64), ctypes.POINTER(i64),
+                                          ctypes.POINTER(f64)]),
     "vbd_set_contacts": (ctypes.c_int, [P, i64, P, P, P, P, P, P, P, P, P, f64, f64]),
     "vbd_set_collision": (ctypes.c_int, [P, i64, P, i64, P, f64, f64, f64, f64, f64, i32, f64, i32]),
     "vbd_detect_contacts": (ctypes.c_int, [P, i32, i64, ctypes.POINTER(i64), P, P, P, P]),

@@ -179,6 +179,14 @@ class DeviceContext:
         _lib.check(_lib.lib().vbd_energy(self._h, float(h), ctypes.byref(g)))
         return g.value
 
+    def metrics(self, h):
+        """(G, active contact count, max contact gap) at the device iterate in one reduction
+        (the per-iteration columns of harness.py:664-670)."""
+        g, n, d = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+        _lib.check(_lib.lib().vbd_energy_metrics(self._h, float(h), ctypes.byref(g), ctypes.byref(n),
+                                                 ctypes.byref(d)))
+        return g.value, int(n.value), d.value
+
     def close(self):
         if self._h and self._h.value:
             _lib.check(_lib.lib().vbd_ctx_destroy(self._h))

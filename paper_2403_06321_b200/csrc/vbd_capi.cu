@@ -2670,7 +2670,7 @@ int vbd_get_colliding(vbd_ctx* c, uint8_t* flags)
     });
 }
 
-int vbd_energy(vbd_ctx* c, double h, double* G)
+int vbd_energy_metrics(vbd_ctx* c, double h, double* G, int64_t* contacts, double* max_gap)
 {
     return guarded([&] {
         if (!c || !G) fail(VBD_ERR_ARG, "NULL argument");
@@ -2679,7 +2679,7 @@ int vbd_energy(vbd_ctx* c, double h, double* G)
         const unsigned b1 = blocks_for(std::max<long long>(c->nsolve, 1) * 4), b2 = blocks_for(std::max<long long>(c->n, 1));
         const unsigned b3 = c->ncontacts ? blocks_for(c->ncontacts) : 0;
         DBuf part;
-        part.alloc((size_t)(b1 + b2 + b3) * sizeof(double));
+        part.alloc((size_t)(b1 + b2 + 2 * b3) * sizeof(double));
         auto run = [&](auto tag) {
             typedef decltype(tag) R;
             if (std::isnan(c->mat_h)) ensure_materials<R>(c, 1.0);  // rest data only
@@ -2689,19 +2689,25 @@ int vbd_energy(vbd_ctx* c, double h, double* G)
                                                  part.as<double>() + b1);
             if (c->ncontacts)
                 k_energy_contact<R><<<b3, 256, 0, s>>>(c->cidx.as<int4>(), c->creal.as<typename Vec4<R>::T>(),
-                                                       (int)c->ncontacts, a.pos, part.as<double>() + b1 + b2);
+                                                       (int)c->ncontacts, a.pos, part.as<double>() + b1 + b2,
+                                                       part.as<double>() + b1 + b2 + b3);
         };
         if (c->precision == VBD_PREC_F64) run(double{});
         else run(float{});
         CK(cudaGetLastError());
-        std::vector<double> h(b1 + b2 + b3);
+        std::vector<double> h(b1 + b2 + 2 * b3);
         CK(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        double acc = 0.0;
-        for (double v : h) acc += v;
+        double acc = 0.0, mx = 0.0;
+        for (unsigned i = 0; i < b1 + b2 + b3; ++i) acc += h[i];
+        for (unsigned i = b1 + b2 + b3; i < h.size(); ++i) mx = std::max(mx, h[i]);
         *G = acc;
+        if (contacts) *contacts = c->ncontacts;
+        if (max_gap) *max_gap = mx;
     });
 }
+
+int vbd_energy(vbd_ctx* c, double h, double* G) { return vbd_energy_metrics(c, h, G, nullptr, nullptr); }
 
 int vbd_profile_color_pass(vbd_ctx* c, double h, int32_t reps, double* ms)
 {

@@ -576,15 +576,17 @@ __global__ void k_contact_csr(const unsigned long long* __restrict__ keys, long 
 
 
 // contact penalty energy sum_c 1/2 k_c max(0, d)^2 with the detection-time weights
-// (_assembly.py:49-56, Contact.gap contact.py:70-74)
+// (_assembly.py:49-56, Contact.gap contact.py:70-74); gap_max[block] = the block's largest
+// gap d, for the max_penetration metric (solver.py:327-332)
 template <typename R>
 __global__ void __launch_bounds__(256) k_energy_contact(const int4* __restrict__ cidx,
                                                         const typename Vec4<R>::T* __restrict__ creal, int n,
-                                                        const typename Vec4<R>::T* __restrict__ x, double* partial)
+                                                        const typename Vec4<R>::T* __restrict__ x, double* partial,
+                                                        double* gap_max)
 {
-    __shared__ double red[256];
+    __shared__ double red[256], mx[256];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    double e = 0.0;
+    double e = 0.0, d = 0.0;
     if (i < n) {
         const int4 id = cidx[i];
         const int ids[4] = {id.x, id.y, id.z, id.w};
@@ -592,14 +594,21 @@ __global__ void __launch_bounds__(256) k_energy_contact(const int4* __restrict__
         const double gam[4] = {g.x, g.y, g.z, g.w};
         D3 acc = gam[0] * ld3<R>(x, ids[0]);
         for (int k = 1; k < 4; ++k) acc = acc + gam[k] * ld3<R>(x, ids[k]);
-        const double d = fmax(0.0, -(acc.x * nk.x + acc.y * nk.y + acc.z * nk.z));
+        d = fmax(0.0, -(acc.x * nk.x + acc.y * nk.y + acc.z * nk.z));
         e = 0.5 * (double)nk.w * d * d;
     }
     red[threadIdx.x] = e;
+    mx[threadIdx.x] = d;
     __syncthreads();
     for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        if (threadIdx.x < o) {
+            red[threadIdx.x] += red[threadIdx.x + o];
+            mx[threadIdx.x] = fmax(mx[threadIdx.x], mx[threadIdx.x + o]);
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+    if (threadIdx.x == 0) {
+        partial[blockIdx.x] = red[0];
+        gap_max[blockIdx.x] = mx[0];
+    }
 }

@@ -209,6 +209,30 @@ def generate_chain(count: int, spacing: float, stiffness: float, mass: float = 1
     return build_spring_net(particles, springs, np.full(count, mass))
 
 
+def load_node_ele(node_path, ele_path) -> tuple:
+    """mesh.py:305-333: ``.node`` rows ``index x y z`` (indices 0..N-1 in order) and ``.ele``
+    rows ``index v0 v1 v2 v3``, 0-based; blank and ``#`` lines skipped; extra columns
+    ignored.  Returns (positions (N,3) float64, tets (T,4) int64) for build_tet_mesh."""
+
+    def table(path, cols):
+        rows = []
+        with open(path, encoding="utf-8") as fh:
+            for no, raw in enumerate(fh, 1):
+                line = raw.strip()
+                if line and not line.startswith("#"):
+                    fields = line.split()
+                    if len(fields) < cols:
+                        raise ValueError(f"{path}:{no}: expected {cols} columns")
+                    rows.append(fields[:cols])
+        return np.array(rows, dtype=np.float64).reshape(-1, cols)
+
+    nodes = table(node_path, 4)
+    if not np.array_equal(nodes[:, 0].astype(np.int64), np.arange(len(nodes))):
+        raise ValueError(f"{node_path}: node indices must be 0..N-1 in order")
+    eles = table(ele_path, 5)
+    return np.ascontiguousarray(nodes[:, 1:]), np.ascontiguousarray(eles[:, 1:].astype(np.int64))
+
+
 def incidence_from_elements(elements, num_vertices: int) -> VertexAdjacency:
     """mesh.py:232-267."""
     elements = np.asarray(elements, dtype=np.int64)

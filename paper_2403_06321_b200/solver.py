@@ -291,6 +291,25 @@ def energy(state, params) -> float:
     return ctx.energy(params.h)
 
 
+def metrics(state, params):
+    """(G, active contact count, max contact gap) at the iterate in one device reduction:
+    the per-iteration columns of harness.run_simulation (harness.py:664-670)."""
+    ctx = device_context(state.system, params.precision, params.device)
+    state._bind(ctx)
+    state._upload(("x", "y"))
+    return ctx.metrics(params.h)
+
+
+def max_penetration(state, params=None) -> float:
+    """solver.py:327-332: the largest gap d = max(0, (x_b - x_a) . n) over the active contact
+    set at state.x (0 without contacts), from the device contact set."""
+    ctx = state._ctx
+    if ctx is None:
+        return 0.0
+    state._upload(("x", "y"))
+    return ctx.metrics(params.h if params is not None else 1.0)[2]
+
+
 def color_pass(state, color_group, params, mode: int = 0) -> None:
     """One aux-buffer colour pass through the b200 backend (solver.py:191-201)."""
     from . import backend

@@ -361,10 +361,197 @@ def contact_detection_fixture():
     save("contact_detection.npz", **out)
 
 
+# --------------------------------------------------------------------------------------------
+# harness: scene schema, scene_build, frames, run_simulation, CLI (harness.py, cli.py)
+
+HARNESS_BASE = {
+    "objects": [{"generator": {"kind": "beam", "nx": 3, "ny": 2, "nz": 2, "spacing": 0.1},
+                 "material": {"mu": 1e5, "lambda": 4e5, "k_d": 0.001}, "density": 1000.0}],
+    "gravity": [0.0, 0.0, -9.8],
+    "constraints": [{"kind": "fixed", "object": 0, "box": [[-1e-6, -1e-6, -1e-6], [1e-6, 0.2, 0.2]]}],
+    "solver": {"h": 0.005, "n_max": 6},
+    "frames": 2,
+    "output": {"format": "bin", "every": 1},
+}
+
+
+def harness_scenes():
+    """Scenes run through the reference's run_simulation (small enough for its CPU path)."""
+    import copy
+    import json
+    base = copy.deepcopy(HARNESS_BASE)
+    placed = {
+        "objects": [{"generator": {"kind": "beam", "nx": 6, "ny": 3, "nz": 3, "spacing": 0.05},
+                     "material": {"mu": 2e5, "lambda": 1e6, "k_d": 1e-4}, "density": 800.0,
+                     "translate": [0.5, -0.2, 1.0], "rotate_deg": [10.0, 20.0, 30.0],
+                     "scale": [1.2, 1.0, 0.9], "velocity": [0.1, 0.0, -0.3],
+                     "initial_stretch": [1.05, 0.98, 1.0]}],
+        "gravity": [0.0, -9.8, 0.0],
+        "constraints": [{"kind": "fixed", "object": 0, "vertices": [0, 1, 2]}],
+        "solver": {"S": 2, "n_max": 5, "rho": 0.5, "line_search": "local_backtracking"},
+        "frames": 2, "output": {"format": "obj", "every": 1}}
+    mixed = {
+        "objects": [{"generator": {"kind": "beam", "nx": 5, "ny": 3, "nz": 3, "spacing": 0.05},
+                     "material": {"mu": 1e5, "lambda": 5e5}},
+                    {"generator": {"kind": "chain", "count": 6, "spacing": 0.04, "stiffness": 800.0,
+                                   "mass": 0.05},
+                     "material": {"mu": 1.0, "lambda": 1.0, "k_d": 1e-3},
+                     "translate": [0.0, 0.5, 0.3], "scale": 1.5},
+                    {"generator": {"kind": "cube", "n": 3, "edge": 0.1}, "material":
+                     {"mu": 3e5, "lambda": 1e6}, "translate": [0.5, 0.0, 0.0]}],
+        "gravity": [0.0, 0.0, -9.8],
+        "constraints": [{"kind": "fixed", "object": 0, "box": [[-1, -1, -1], [1e-9, 1, 1]]},
+                        {"kind": "fixed", "object": 1, "vertices": [0]},
+                        {"kind": "subspace", "object": 0, "vertex": 44, "basis": [[0, 0, 1]]},
+                        {"kind": "subspace", "object": 2, "vertex": 26,
+                         "basis": [[1, 0, 0], [0, 1, 0]], "anchor": [0.6, 0.1, 0.1]},
+                        {"kind": "world_box", "lo": [-5, -5, -0.02], "hi": [5, 5, 5], "k_b": 1e4},
+                        {"kind": "world_box", "object": 2, "lo": [-5, -5, 0.0], "hi": [5, 5, 5],
+                         "k_b": 5e3}],
+        "solver": {"h": 1 / 120, "n_max": 8, "init_mode": "inertia", "eps_det": 1e-9},
+        "frames": 3, "output": {"format": "bin", "every": 2}}
+    contact = {
+        "objects": [{"generator": {"kind": "cube", "n": 4, "edge": 0.3},
+                     "material": {"mu": 5e4, "lambda": 2e5, "k_d": 1e-4}, "density": 10.0},
+                    {"generator": {"kind": "cube", "n": 4, "edge": 0.2},
+                     "material": {"mu": 5e5, "lambda": 2e6, "k_d": 1e-4}, "density": 2000.0,
+                     "translate": [0.05, 0.05, 0.3005], "velocity": [0.0, 0.0, -0.5]}],
+        "gravity": [0.0, 0.0, -9.8],
+        "constraints": [{"kind": "fixed", "object": 0, "box": [[-1, -1, -1], [1, 1, 1e-9]]}],
+        "contact": {"k_c": 1e6, "mu_c": 0.3, "eps_v": 1e-2, "dcd_radius": 2e-3},
+        "solver": {"h": 1 / 120, "n_max": 8, "n_col": 3},
+        "frames": 3, "output": {"format": "bin", "every": 1}}
+    return {"base": json.dumps(base), "placed": json.dumps(placed), "mixed": json.dumps(mixed),
+            "contact": json.dumps(contact)}
+
+
+HARNESS_BAD = [
+    '{nope',
+    '{"objects": []}',
+    '{"objects": [{"generator": {"kind": "beam", "nx": 3, "ny": 2, "nz": 2, "spacing": 0.1}}]}',
+    '{"objects": [{"generator": {"kind": "tube"}, "material": {"mu": 1, "lambda": 1}}]}',
+    '{"objects": [{"generator": {"kind": "beam", "nx": 1, "ny": 2, "nz": 2, "spacing": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}]}',
+    '{"objects": [{"generator": {"kind": "beam", "nx": 3, "ny": 2, "nz": 2, "spacing": "a"}, '
+    '"material": {"mu": 1, "lambda": 1}}]}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": -1}}]}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}, "scale": [1, 0, 1]}]}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}, "translate": [1, 2]}]}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "solver": {"h": "fast"}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "solver": {"h": -0.5}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "solver": {"rho": 1.0}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "solver": {"S": 0}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "solver": {"n_max": 2.5}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "solver": {"line_search": "on"}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "solver": {"init_mode": "zero"}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "solver": {"dt": 0.1}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "contact": {"mu_c": 0.1}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "contact": {"k_c": 1e7, "mu_c": -2.0}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "constraints": [{"kind": "fixed", "object": 0}]}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "constraints": [{"kind": "fixed", "object": 3, '
+    '"vertices": [0]}]}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "constraints": [{"kind": "subspace", "object": 0, '
+    '"vertex": 0, "basis": [[1, 0]]}]}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "constraints": [{"kind": "world_box", '
+    '"lo": [0, 0, 0], "hi": [1, 1, 1]}]}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "frames": -1}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "output": {"format": "vtk"}}',
+    '{"objects": [{"generator": {"kind": "cube", "n": 3, "edge": 0.1}, '
+    '"material": {"mu": 1, "lambda": 1}}], "warp_speed": 9}',
+    '[1, 2]',
+]
+
+
+def harness_fixture():
+    """Reference outputs of parse_scene/serialize_scene (incl. the error for each bad document),
+    scene_build, export_frame and run_simulation (metrics rows minus wall_ms and the last
+    frame) -- harness.py:95-691 -- plus the `color` command's JSON (cli.py:94-118)."""
+    import json
+    import tempfile
+    from click.testing import CliRunner
+    from vbdsim import harness as H
+    from vbdsim.cli import main as cli_main
+    from vbdsim.errors import SchemaError
+    out = {}
+    for name, text in harness_scenes().items():
+        cfg = H.parse_scene(text)
+        out[f"{name}_scene"] = np.str_(text)
+        out[f"{name}_ser"] = np.str_(H.serialize_scene(cfg))
+        system, state, params = H.scene_build(cfg)
+        for f in ("rest_positions", "masses", "tets", "springs", "sp_l0", "sp_k", "sp_kd",
+                  "color_verts", "color_off"):
+            out[f"{name}_{f}"] = np.asarray(getattr(system, f))
+        for f in system.cons._fields:
+            out[f"{name}_cons_{f}"] = np.asarray(getattr(system.cons, f))
+        out[f"{name}_x0"] = state.x.copy()
+        out[f"{name}_v0"] = state.v_t.copy()
+        out[f"{name}_faces"] = H._surface_faces(system)
+        with tempfile.TemporaryDirectory() as d:
+            H.run_simulation(cfg, d)
+            rows = [ln.split(",") for ln in open(f"{d}/metrics.csv").read().splitlines()[1:]]
+            out[f"{name}_metrics"] = np.array([[float(c) for c in r[:-1]] for r in rows])
+            files = sorted(p.name for p in Path(d).glob("frame_*"))
+            out[f"{name}_frame_files"] = np.array(files)
+            pos, fac = H.load_frame(Path(d) / files[-1])
+            out[f"{name}_last_x"] = pos
+            out[f"{name}_last_faces"] = fac
+    errs = []
+    for text in HARNESS_BAD:
+        try:
+            H.parse_scene(text)
+            errs.append(("none", ""))
+        except SchemaError as e:
+            errs.append(("SchemaError", str(e)))
+        except ValueError as e:
+            errs.append(("ValueError", str(e)))
+    out["bad_scenes"] = np.array(HARNESS_BAD)
+    out["bad_kind"] = np.array([e[0] for e in errs])
+    out["bad_msg"] = np.array([e[1] for e in errs])
+    rng = np.random.default_rng(5)
+    pos = rng.standard_normal((11, 3))
+    fac = rng.integers(0, 11, (7, 3))
+    with tempfile.TemporaryDirectory() as d:
+        H.export_frame(pos, fac, f"{d}/f.bin")
+        H.export_frame(pos, fac, f"{d}/f.obj")
+        out["frame_pos"], out["frame_faces"] = pos, fac
+        out["frame_bin"] = np.frombuffer(Path(f"{d}/f.bin").read_bytes(), dtype=np.uint8)
+        out["frame_obj"] = np.str_(Path(f"{d}/f.obj").read_text())
+        m = generate_beam(4, 3, 3, 0.1, density=1000.0)
+        Path(f"{d}/m.node").write_text("# nodes\n" + "\n".join(
+            f"{i} {float(p[0])!r} {float(p[1])!r} {float(p[2])!r}" for i, p in enumerate(m.rest_positions)))
+        Path(f"{d}/m.ele").write_text("\n".join(f"{i} {t[0]} {t[1]} {t[2]} {t[3]} 0"
+                                                for i, t in enumerate(m.tets)) + "\n\n")
+        out["mesh_node"] = np.str_(Path(f"{d}/m.node").read_text())
+        out["mesh_ele"] = np.str_(Path(f"{d}/m.ele").read_text())
+        res = CliRunner().invoke(cli_main, ["color", "--nodes", f"{d}/m.node", "--eles", f"{d}/m.ele"])
+        assert res.exit_code == 0, res.output
+        out["color_json"] = np.str_(json.dumps(json.loads(res.output), sort_keys=True))
+    save("harness.npz", **out)
+
+
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"mesh", "coloring", "pass", "steps", "extras", "energy", "contact"}
+    which = set(sys.argv[1:]) or {"mesh", "coloring", "pass", "steps", "extras", "energy", "contact", "harness"}
     for name, fn in (("mesh", mesh_fixture), ("coloring", coloring_fixtures), ("pass", pass_fixture),
                      ("steps", step_fixtures), ("extras", extras_fixture), ("energy", energy_fixture),
-                     ("contact", contact_fixture)):
+                     ("contact", contact_fixture), ("harness", harness_fixture)):
         if name in which:
             fn()
