@@ -137,6 +137,8 @@ typedef struct {
     int64_t tile_nbr_refs;     /* K1T: neighbour-list entries over all tiles */
     int32_t tile_lanes;        /* K1T: lanes per vertex */
     int32_t tile_stages;       /* K1T: shared-memory pipeline stages */
+    int32_t tile_ent_cap;      /* K1T: entry slots of the largest tile (per-stage capacity) */
+    int32_t tile_smem_bytes;   /* K1T: dynamic shared memory per CTA */
 } vbd_ctx_info;
 
 /* ---- context ---------------------------------------------------------------------------- */

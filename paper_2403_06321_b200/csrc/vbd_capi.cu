@@ -183,6 +183,7 @@ struct vbd_ctx {
     int ent_cap = 0, nbr_cap = 0;
     DBuf tv0, tnv, loff, tnbr, tent, tdesc;
     int tile_stages = 2, tile_w = 4, tile_occ = 2;
+    bool tile_defer = true;  // K1T deferred block solves (VBD_TILE_DEFER=0 disables)
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -540,10 +541,16 @@ template <typename R> void build_tiles(vbd_ctx* c)
     CK(cudaGetLastError());
     if (read_scalar<int>(err.p, s)) return;
     std::vector<long long> hc(2 * (size_t)nt), nls(nt), nss(nt);
+    std::vector<int> nl_real(nt);
     CK(cudaMemcpy(hc.data(), cnt.p, (size_t)nt * 16, cudaMemcpyDeviceToHost));
+    // bank-aware placement (k_tile_banks): lists padded by VBD_TILE_BANK_SLACK percent (default
+    // 25; 0 keeps the sorted list) to a multiple of the 8 bank groups
+    const char* be = getenv("VBD_TILE_BANK_SLACK");
+    const int slack = be && *be ? atoi(be) : 25;
     long long mx = 0, ms = 0;
     for (int t = 0; t < nt; ++t) {
-        nls[t] = hc[2 * t];
+        nl_real[t] = (int)hc[2 * t];
+        nls[t] = slack > 0 ? (hc[2 * t] * (100 + slack) / 100 + 8 + 7) / 8 * 8 : hc[2 * t];
         nss[t] = hc[2 * t + 1];
         mx = std::max(mx, nls[t]);
         ms = std::max(ms, nss[t]);
@@ -557,6 +564,8 @@ template <typename R> void build_tiles(vbd_ctx* c)
     // as many stages (2..4) as fit two CTAs per SM
     const char* oe = getenv("VBD_TILE_OCC");
     c->tile_occ = oe && *oe == '2' ? 2 : 3;  // 3 CTAs per SM (one entry per lane in flight) measured faster
+    const char* de = getenv("VBD_TILE_DEFER");
+    c->tile_defer = !(de && *de == '0');
     const size_t cap = c->tile_occ == 3 ? 75 * 1024 : VBD_TILE_SMEM_MAX;
     int stages = 0;
     for (int st = 4; st >= 2 && !stages; --st)
@@ -585,6 +594,20 @@ template <typename R> void build_tiles(vbd_ctx* c)
                                                 (unsigned)(c->nkinds * KindRec<R>::HOT * sizeof(R)), err.as<int>());
     CK(cudaGetLastError());
     if (read_scalar<int>(err.p, s)) fail(VBD_ERR_INTERNAL, "tile build failed");
+    if (slack > 0) {
+        DBuf dnl, ids, asg;
+        upload(dnl, nl_real.data(), nl_real.size(), s);
+        ids.alloc((size_t)std::max<long long>(total, 1) * 4);
+        asg.alloc((size_t)std::max<long long>(total, 1) * 4);
+        k_tile_banks<<<blocks_for(nt, 64), 64, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
+                                                      c->loff.as<long long>(), sbase.as<long long>(), dnl.as<int>(),
+                                                      nt, W, (unsigned)sizeof(typename Vec4<R>::T),
+                                                      (unsigned)(c->nbr_cap * sizeof(typename Vec4<R>::T)),
+                                                      c->tnbr.as<int>(), c->tent.as<uint2>(), ids.as<int>(),
+                                                      asg.as<int>());
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+    }
     c->tdesc.alloc((size_t)nt * sizeof(TileDesc));
     k_tile_desc<<<blocks_for(nt), 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
                                               c->loff.as<long long>(), sbase.as<long long>(), nt, W,
@@ -862,44 +885,46 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     else k1_color_pass<R, W, U, B, false, false><<<nb, 256, 0, s>>>(a);
 }
 
-template <typename R, bool UM, int S, int W, int OCC>
+template <typename R, bool UM, int S, int W, int OCC, int DEF>
 void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
 {
     static size_t attr = 0;
     static int per_sm = 0, sms = 148;
     if (smem > attr) {
-        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC, DEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = smem;
         int dev = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, S, W, OCC>, 288, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, S, W, OCC, DEF>, 288, smem));
         per_sm = std::max(1, per_sm);
     }
     const int grid = std::min(ta.tcount, per_sm * sms);
-    k1_tiles<R, UM, S, W, OCC><<<grid, 288, smem, s>>>(ta);
+    k1_tiles<R, UM, S, W, OCC, DEF><<<grid, 288, smem, s>>>(ta);
 }
 
 template <typename R, bool UM, int W>
-void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, int occ, size_t smem, cudaStream_t s)
+void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, int occ, bool defer, size_t smem, cudaStream_t s)
 {
     if (occ == 3) {
-        if (stages >= 3) launch_k1_tiles_v<R, UM, 3, W, 3>(ta, smem, s);
-        else launch_k1_tiles_v<R, UM, 2, W, 3>(ta, smem, s);
+        if (stages >= 3) launch_k1_tiles_v<R, UM, 3, W, 3, 1>(ta, smem, s);
+        else if (defer) launch_k1_tiles_v<R, UM, 2, W, 3, W>(ta, smem, s);
+        else launch_k1_tiles_v<R, UM, 2, W, 3, 1>(ta, smem, s);
         return;
     }
-    if (stages >= 4) launch_k1_tiles_v<R, UM, 4, W, 2>(ta, smem, s);
-    else if (stages == 3) launch_k1_tiles_v<R, UM, 3, W, 2>(ta, smem, s);
-    else launch_k1_tiles_v<R, UM, 2, W, 2>(ta, smem, s);
+    if (stages >= 4) launch_k1_tiles_v<R, UM, 4, W, 2, 1>(ta, smem, s);
+    else if (stages == 3) launch_k1_tiles_v<R, UM, 3, W, 2, 1>(ta, smem, s);
+    else launch_k1_tiles_v<R, UM, 2, W, 2, 1>(ta, smem, s);
 }
 
 template <typename R, bool UM>
-void launch_k1_tiles_w(const K1TArgs<R>& ta, int W, int stages, int occ, size_t smem, cudaStream_t s)
+void launch_k1_tiles_w(const K1TArgs<R>& ta, int W, int stages, int occ, bool defer, size_t smem,
+                       cudaStream_t s)
 {
     // 4 lanes per vertex (1 and 2 were measured slower); the kernel and the
     // tile build stay generic in W
     (void)W;
-    launch_k1_tiles_s<R, UM, 4>(ta, stages, occ, smem, s);
+    launch_k1_tiles_s<R, UM, 4>(ta, stages, occ, defer, smem, s);
 }
 
 template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
@@ -922,8 +947,8 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     ta.nkinds = c->nkinds;
     const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds, 256 / c->tile_w};
     const int S = c->tile_stages;
-    if (a.vmat) launch_k1_tiles_w<R, true>(ta, c->tile_w, S, c->tile_occ, L.total(S), s);
-    else launch_k1_tiles_w<R, false>(ta, c->tile_w, S, c->tile_occ, L.total(S), s);
+    if (a.vmat) launch_k1_tiles_w<R, true>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, L.total(S), s);
+    else launch_k1_tiles_w<R, false>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, L.total(S), s);
     return true;
 }
 
@@ -1993,6 +2018,13 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         info->tile_nbr_refs = c->tiles ? c->tnbr.bytes / 4 : 0;
         info->tile_lanes = c->tiles ? c->tile_w : 0;
         info->tile_stages = c->tiles ? c->tile_stages : 0;
+        info->tile_ent_cap = c->tiles ? c->ent_cap : 0;
+        if (c->tiles) {
+            const TileSmem<float> L32{c->ent_cap, c->nbr_cap, (int)c->nkinds, 256 / c->tile_w};
+            const TileSmem<double> L64{c->ent_cap, c->nbr_cap, (int)c->nkinds, 256 / c->tile_w};
+            info->tile_smem_bytes = (int)(c->precision == VBD_PREC_F64 ? L64.total(c->tile_stages)
+                                                                       : L32.total(c->tile_stages));
+        }
         info->entry_bytes = c->compact ? 16 : EntryPlanesBytes(c->precision);
     });
 }

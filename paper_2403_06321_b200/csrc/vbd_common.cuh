@@ -332,16 +332,21 @@ template <typename R> __device__ __forceinline__ bool finite3(R a, R b, R c)
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
+// the waiting warp is suspended (not spinning on issue slots) until the phase completes or
+// the hint expires
+#ifndef VBD_MBAR_SUSPEND_NS
+#define VBD_MBAR_SUSPEND_NS 1000000u
+#endif
 __device__ __forceinline__ void mbar_wait_parity(unsigned bar, unsigned phase)
 {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@P1 bra DONE;\n"
         "bra LAB_WAIT;\n"
         "DONE:\n"
-        "}\n" ::"r"(bar), "r"(phase) : "memory");
+        "}\n" ::"r"(bar), "r"(phase), "r"(VBD_MBAR_SUSPEND_NS) : "memory");
 }
 

@@ -166,6 +166,86 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
     }
 }
 
+// Bank-aware placement of a tile's neighbour positions (one thread per tile, after FILL).
+// A consumer LDS.128 is served per quarter-warp: its 8 lanes (8 vertices, same entry
+// position, same tet corner k) take one wavefront only if their positions lie in 8 distinct
+// 16-byte bank groups (slot index mod 8) or coincide.  The sorted list leaves that to chance
+// (~2.1 wavefronts per quarter measured on C5).  Here every quarter-warp group, in sweep
+// order, places its not-yet-placed neighbours into bank groups its placed members do not
+// use, least-filled first, inside a list padded to nlp = 8 * (slots per bank); then each bank
+// group is filled in sorted-id order.  The list is rewritten in position order (-1 = hole,
+// skipped by the producer) and the slots' offsets remapped; positions only move in shared
+// memory, so results are bitwise unchanged.
+__global__ void k_tile_banks(const int* __restrict__ tv0, const int* __restrict__ tnv,
+                             const long long* __restrict__ eoff, const long long* __restrict__ lbase,
+                             const long long* __restrict__ sbase, const int* __restrict__ nls, int nt, int W,
+                             unsigned r4b, unsigned pad_pos, int* __restrict__ tnbr, uint2* __restrict__ tent,
+                             int* __restrict__ ids, int* __restrict__ asg)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const long long l0 = lbase[t], s0 = sbase[t];
+    const int nl = nls[t], nlp = (int)(lbase[t + 1] - l0), cap = nlp / 8;
+    const int pad_bank = (int)((pad_pos / r4b) & 7u);
+    for (int u = 0; u < nl; ++u) {
+        ids[l0 + u] = tnbr[l0 + u];
+        asg[l0 + u] = -1;
+    }
+    int fill[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int vpw = 32 / W, v0 = tv0[t], nv = tnv[t];
+    long long slot = s0;
+    for (int w = 0; w < 8; ++w) {
+        const int rounds = tile_warp_rounds(eoff, v0, nv, w, W);
+        for (int i = 0; i < rounds; ++i, slot += 32) {
+            uint2 e[32];
+            for (int l = 0; l < 32; ++l) e[l] = tent[slot + l];
+            for (int k = 0; k < 3; ++k)
+                for (int q = 0; q < 32; q += vpw) {  // one quarter-warp group
+                    int u[8];
+                    unsigned used = 0;
+                    for (int l = 0; l < vpw; ++l) {
+                        const uint2 s = e[q + l];
+                        const unsigned off = (k == 0 ? s.x : k == 1 ? s.x >> 16 : s.y) & 0xffffu;
+                        u[l] = off == pad_pos ? -2 : (int)(off / r4b);
+                        if (u[l] == -2) used |= 1u << pad_bank;
+                        else if (asg[l0 + u[l]] >= 0) used |= 1u << asg[l0 + u[l]];
+                    }
+                    for (int l = 0; l < vpw; ++l) {
+                        if (u[l] < 0 || asg[l0 + u[l]] >= 0) continue;
+                        int best = -1;
+                        for (int b = 0; b < 8; ++b)  // a free bank group the group does not use yet
+                            if (!(used >> b & 1u) && fill[b] < cap && (best < 0 || fill[b] < fill[best])) best = b;
+                        if (best < 0)
+                            for (int b = 0; b < 8; ++b)  // none: least-filled (a conflict)
+                                if (fill[b] < cap && (best < 0 || fill[b] < fill[best])) best = b;
+                        asg[l0 + u[l]] = best;
+                        ++fill[best];
+                        used |= 1u << best;
+                    }
+                }
+        }
+    }
+    // positions: within each bank group in sorted-id order, so the producer's gather (lane i ->
+    // position i) still walks nearly sorted ids (coalesced cp.async sources)
+    int next[8] = {0, 1, 2, 3, 4, 5, 6, 7};
+    for (int u = 0; u < nl; ++u) {
+        const int b = asg[l0 + u];
+        asg[l0 + u] = next[b];
+        next[b] += 8;
+    }
+    for (int p = 0; p < nlp; ++p) tnbr[l0 + p] = -1;
+    for (int u = 0; u < nl; ++u) tnbr[l0 + asg[l0 + u]] = ids[l0 + u];
+    auto remap = [&](unsigned off) {
+        return off == pad_pos ? off : (unsigned)asg[l0 + off / r4b] * r4b;
+    };
+    for (long long sl = s0; sl < slot; ++sl) {
+        uint2 s = tent[sl];
+        s.x = remap(s.x & 0xffffu) | (remap(s.x >> 16) << 16);
+        s.y = remap(s.y & 0xffffu) | (s.y & 0xffff0000u);
+        tent[sl] = s;
+    }
+}
+
 // per-tile descriptor (64 B): the producer loads the first 32 B; the whole record is
 // bulk-copied into the stage header for the consumers
 struct __align__(16) TileDesc {
@@ -287,9 +367,33 @@ __device__ __forceinline__ uint2 lds_u2(unsigned a)
     return v;
 }
 
+// the vertex update after the block solve: in-place store, NVLink ghost store, finite check
+template <typename R>
+__device__ __forceinline__ void k1t_store(const K1Args<R>& a, int v, typename Vec4<R>::T nx)
+{
+    a.pos[v] = nx;
+    if (a.peer_pos[0] || a.peer_pos[1]) {
+        const int jj = v - a.vbeg;
+        if (jj < a.nb[0]) {
+            a.peer_pos[0][a.peer_off[0] + jj] = nx;  // NVLink store into the left ghost
+            __threadfence_system();
+        } else if (jj < a.nb[0] + a.nb[1]) {
+            a.peer_pos[1][a.peer_off[1] + (jj - a.nb[0])] = nx;
+            __threadfence_system();
+        }
+    }
+    if (a.flag && !finite3(nx.x, nx.y, nx.z))
+        atomicMin(a.flag, StepFlag::key((unsigned)*a.stepctr, (unsigned)a.iter, (unsigned)a.perm[v]));
+}
+
 // OCC = CTAs per SM the kernel is compiled for (register budget); OCC >= 3 sweeps one entry
 // per lane at a time (fewer live registers), else two.
-template <typename R, bool UM, int S, int W, int OCC>
+// DEF = W: deferred block solves.  After a tile's butterfly every lane of a vertex holds its
+// sums; the vertex terms run on all of them and lane j = (tile count mod W) keeps (f, H, v).
+// Every W tiles the warp solves and stores 32 vertices with all lanes active, instead of
+// 32 / W vertices per tile with a quarter of the lanes.  Vertices of one colour do not read
+// each other, so deferring their stores inside the launch changes nothing (bitwise).
+template <typename R, bool UM, int S, int W, int OCC, int DEF>
 __global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
 {
     typedef typename Vec4<R>::T R4;
@@ -397,6 +501,23 @@ __global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
     const int lv = warp * VPW + vi;
     int stage = 0;
     unsigned ph = 0;
+    static_assert(DEF == 1 || DEF == W, "deferral batches one tile per lane of a vertex");
+    int tc = 0, qv = -1;  // DEF > 1: tiles since the last flush; the deferred vertex of this lane
+    R qf[DEF > 1 ? 3 : 1], qH[DEF > 1 ? 6 : 1];
+    auto flush = [&]() {
+        if constexpr (DEF > 1) {
+            if (qv >= 0) {
+                R d[3];
+                block_solve<R>(qf, qH, a.eps_det, a.mode, d);
+                R4 nx = a.pos[qv];  // own colour: not written by anyone else in this launch
+                nx.x = nx.x + d[0];
+                nx.y = nx.y + d[1];
+                nx.z = nx.z + d[2];
+                k1t_store<R>(a, qv, nx);
+            }
+            qv = -1;
+        }
+    };
     for (int t = blockIdx.x; t < ta.tcount; t += gridDim.x) {
         mbar_wait_parity(smem_u32(&full[stage]), ph);
         const unsigned char* st = stages + stage * L.stage_bytes();
@@ -465,7 +586,24 @@ __global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
 #pragma unroll
             for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(0xffffffffu, H[q], o);
         }
-        if (act && j == 0) {  // j = 0 processed the vertex's first entry (UM: dsc/opd)
+        if constexpr (DEF > 1) {
+            if (UM) {  // the vertex's first entry (position 0) is on lane j = 0
+                dsc = __shfl_sync(0xffffffffu, dsc, vi);
+                opd = __shfl_sync(0xffffffffu, opd, vi);
+            }
+            vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM, dsc, opd);
+            if (j == tc) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) qf[q] = f[q];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) qH[q] = H[q];
+                qv = act ? hv0 + lv : -1;
+            }
+            if (++tc == DEF) {
+                tc = 0;
+                flush();
+            }
+        } else if (act && j == 0) {  // j = 0 processed the vertex's first entry (UM: dsc/opd)
             const int v = hv0 + lv;
             vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM, dsc, opd);  // no entries: dsc = opd = 0, H = 0
             R d[3];
@@ -474,23 +612,12 @@ __global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
             nx.x = xi[0] + d[0];
             nx.y = xi[1] + d[1];
             nx.z = xi[2] + d[2];
-            a.pos[v] = nx;
-            if (a.peer_pos[0] || a.peer_pos[1]) {
-                const int jj = v - a.vbeg;
-                if (jj < a.nb[0]) {
-                    a.peer_pos[0][a.peer_off[0] + jj] = nx;  // NVLink store into the left ghost
-                    __threadfence_system();
-                } else if (jj < a.nb[0] + a.nb[1]) {
-                    a.peer_pos[1][a.peer_off[1] + (jj - a.nb[0])] = nx;
-                    __threadfence_system();
-                }
-            }
-            if (a.flag && !finite3(nx.x, nx.y, nx.z))
-                atomicMin(a.flag, StepFlag::key((unsigned)*a.stepctr, (unsigned)a.iter, (unsigned)a.perm[v]));
+            k1t_store<R>(a, v, nx);
         }
         if (++stage == S) {
             stage = 0;
             ph ^= 1;
         }
     }
+    if constexpr (DEF > 1) flush();
 }

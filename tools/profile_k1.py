@@ -17,5 +17,8 @@ from paper_2403_06321_b200.scenes import build, config  # noqa: E402
 
 cfg = config(a.config, a.scale)
 ctx, _ = build(cfg, precision=a.precision)
+inf = ctx._info()
+print("tiles", inf.tiles, "ent_cap", inf.tile_ent_cap, "nbr_cap", inf.tile_nbr_cap, "stages",
+      inf.tile_stages, "smem/CTA", inf.tile_smem_bytes, "kinds", inf.num_entry_kinds)
 ctx.step(cfg.step_params())
 print("k1 ms per colour:", ctx.profile_color_pass(cfg.h, reps=a.reps))
