@@ -506,9 +506,9 @@ template <typename R> void build_tiles(vbd_ctx* c)
         c->has_extras)
         return;
     const char* we = getenv("VBD_TILE_W");
-    const int W = we && *we ? atoi(we) : 4;
-    if (W != 4) fail(VBD_ERR_ARG, "VBD_TILE_W: only 4 lanes per vertex are compiled");
-    const int VPT = 256 / W;
+    const int W = we && *we ? atoi(we) : 2;  // 2 lanes x 16 vertices per warp measured fastest
+    if (W != 4 && W != 2) fail(VBD_ERR_ARG, "VBD_TILE_W: 4 or 2 lanes per vertex are compiled");
+    const int VPT = 64;  // 2 W consumer warps x 32 / W vertices
     if ((long long)VPT * c->max_deg * 3 > VBD_TILE_SORT) return;
     c->tile_w = W;
     cudaStream_t s = c->stream;
@@ -896,11 +896,11 @@ void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
         int dev = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, S, W, OCC, DEF>, 288, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, S, W, OCC, DEF>, 64 * W + 32, smem));
         per_sm = std::max(1, per_sm);
     }
     const int grid = std::min(ta.tcount, per_sm * sms);
-    k1_tiles<R, UM, S, W, OCC, DEF><<<grid, 288, smem, s>>>(ta);
+    k1_tiles<R, UM, S, W, OCC, DEF><<<grid, 64 * W + 32, smem, s>>>(ta);
 }
 
 template <typename R, bool UM, int W>
@@ -912,19 +912,22 @@ void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, int occ, bool defer, si
         else launch_k1_tiles_v<R, UM, 2, W, 3, 1>(ta, smem, s);
         return;
     }
-    if (stages >= 4) launch_k1_tiles_v<R, UM, 4, W, 2, 1>(ta, smem, s);
-    else if (stages == 3) launch_k1_tiles_v<R, UM, 3, W, 2, 1>(ta, smem, s);
-    else launch_k1_tiles_v<R, UM, 2, W, 2, 1>(ta, smem, s);
+    if constexpr (W == 4) {
+        if (stages >= 4) launch_k1_tiles_v<R, UM, 4, W, 2, 1>(ta, smem, s);
+        else if (stages == 3) launch_k1_tiles_v<R, UM, 3, W, 2, 1>(ta, smem, s);
+        else launch_k1_tiles_v<R, UM, 2, W, 2, 1>(ta, smem, s);
+    } else {
+        fail(VBD_ERR_ARG, "VBD_TILE_W=2 is compiled for 3 CTAs per SM only");
+    }
 }
 
 template <typename R, bool UM>
 void launch_k1_tiles_w(const K1TArgs<R>& ta, int W, int stages, int occ, bool defer, size_t smem,
                        cudaStream_t s)
 {
-    // 4 lanes per vertex (1 and 2 were measured slower); the kernel and the
-    // tile build stay generic in W
-    (void)W;
-    launch_k1_tiles_s<R, UM, 4>(ta, stages, occ, defer, smem, s);
+    // W lanes per vertex in 2 W consumer warps (64-vertex tiles); 1 lane was measured slower
+    if (W == 2) launch_k1_tiles_s<R, UM, 2>(ta, stages, occ, defer, smem, s);
+    else launch_k1_tiles_s<R, UM, 4>(ta, stages, occ, defer, smem, s);
 }
 
 template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
@@ -945,7 +948,10 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     ta.ent_cap = c->ent_cap;
     ta.nbr_cap = c->nbr_cap;
     ta.nkinds = c->nkinds;
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds, 256 / c->tile_w};
+    const char* dbg = getenv("VBD_TILE_DBG");
+    ta.dbg = dbg && *dbg ? atoi(dbg) : 0;
+    if (ta.dbg) ta.a.flag = nullptr;  // garbage positions in the timing experiments
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds, 64};
     const int S = c->tile_stages;
     if (a.vmat) launch_k1_tiles_w<R, true>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, L.total(S), s);
     else launch_k1_tiles_w<R, false>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, L.total(S), s);
@@ -2020,8 +2026,8 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         info->tile_stages = c->tiles ? c->tile_stages : 0;
         info->tile_ent_cap = c->tiles ? c->ent_cap : 0;
         if (c->tiles) {
-            const TileSmem<float> L32{c->ent_cap, c->nbr_cap, (int)c->nkinds, 256 / c->tile_w};
-            const TileSmem<double> L64{c->ent_cap, c->nbr_cap, (int)c->nkinds, 256 / c->tile_w};
+            const TileSmem<float> L32{c->ent_cap, c->nbr_cap, (int)c->nkinds, 64};
+            const TileSmem<double> L64{c->ent_cap, c->nbr_cap, (int)c->nkinds, 64};
             info->tile_smem_bytes = (int)(c->precision == VBD_PREC_F64 ? L64.total(c->tile_stages)
                                                                        : L32.total(c->tile_stages));
         }

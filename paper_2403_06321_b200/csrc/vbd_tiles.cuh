@@ -192,7 +192,7 @@ __global__ void k_tile_banks(const int* __restrict__ tv0, const int* __restrict_
         asg[l0 + u] = -1;
     }
     int fill[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const int vpw = 32 / W, v0 = tv0[t], nv = tnv[t];
+    const int v0 = tv0[t], nv = tnv[t];
     long long slot = s0;
     for (int w = 0; w < 8; ++w) {
         const int rounds = tile_warp_rounds(eoff, v0, nv, w, W);
@@ -200,17 +200,17 @@ __global__ void k_tile_banks(const int* __restrict__ tv0, const int* __restrict_
             uint2 e[32];
             for (int l = 0; l < 32; ++l) e[l] = tent[slot + l];
             for (int k = 0; k < 3; ++k)
-                for (int q = 0; q < 32; q += vpw) {  // one quarter-warp group
+                for (int q = 0; q < 32; q += 8) {  // one quarter-warp group (8 lanes)
                     int u[8];
                     unsigned used = 0;
-                    for (int l = 0; l < vpw; ++l) {
+                    for (int l = 0; l < 8; ++l) {
                         const uint2 s = e[q + l];
                         const unsigned off = (k == 0 ? s.x : k == 1 ? s.x >> 16 : s.y) & 0xffffu;
                         u[l] = off == pad_pos ? -2 : (int)(off / r4b);
                         if (u[l] == -2) used |= 1u << pad_bank;
                         else if (asg[l0 + u[l]] >= 0) used |= 1u << asg[l0 + u[l]];
                     }
-                    for (int l = 0; l < vpw; ++l) {
+                    for (int l = 0; l < 8; ++l) {
                         if (u[l] < 0 || asg[l0 + u[l]] >= 0) continue;
                         int best = -1;
                         for (int b = 0; b < 8; ++b)  // a free bank group the group does not use yet
@@ -292,6 +292,8 @@ template <typename R> struct K1TArgs {
     int tbeg, tcount;          // tiles of this colour
     int ent_cap, nbr_cap;      // per-stage capacity (entries incl. pad, neighbours)
     int nkinds;
+    int dbg;  // timing experiments only (VBD_TILE_DBG): 1 consumers skip the entry sweep,
+              // 2 the producer skips the neighbour gathers; results are wrong in both
 };
 
 typedef TileDesc TileHdr;  // the stage header is a copy of the tile's descriptor
@@ -393,15 +395,19 @@ __device__ __forceinline__ void k1t_store(const K1Args<R>& a, int v, typename Ve
 // Every W tiles the warp solves and stores 32 vertices with all lanes active, instead of
 // 32 / W vertices per tile with a quarter of the lanes.  Vertices of one colour do not read
 // each other, so deferring their stores inside the launch changes nothing (bitwise).
+// Tiles are 64 vertices: NCW = 2 W consumer warps of 32 / W vertices (W = 4: 8 warps, W = 2:
+// 4 warps of 16 vertices with twice the rounds -- half the per-vertex reduction and solve
+// overhead per entry).
 template <typename R, bool UM, int S, int W, int OCC, int DEF>
-__global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
+__global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta)
 {
     typedef typename Vec4<R>::T R4;
     constexpr int VPW = 32 / W;  // vertices per consumer warp
+    constexpr int NCW = 2 * W;   // consumer warps
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long full[S], empty[S];
     const K1Args<R>& a = ta.a;
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds, 8 * VPW};
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds, NCW * VPW};
     typedef typename PlaneT<R>::T PL;
     PL* skind = reinterpret_cast<PL*>(smem);
     unsigned char* stages = smem + ((L.kinds_bytes() + 127) & ~(size_t)127);
@@ -414,13 +420,13 @@ __global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(smem_u32(&full[s]), 33);  // expect_tx arrive + 32 cp.async arrivals
-            mbar_init(smem_u32(&empty[s]), 8);  // one per consumer warp
+            mbar_init(smem_u32(&empty[s]), NCW);  // one per consumer warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    if (warp == 8) {  // ---------------- producer
+    if (warp == NCW) {  // ---------------- producer
         // Software-pipelined, unrolled by two with named buffers (no register copies that would
         // expose load latency): while tile t is issued, the neighbour ids of tile t + grid and
         // the descriptor of tile t + 2 grid are in flight.
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
                 bulk_g2s(st + L.off_y(), a.y + d.v0, vby, bar);
             }
             R4* np = reinterpret_cast<R4*>(st + L.off_npos());
-            for (int base = 0;;) {
+            for (int base = 0; ta.dbg != 2;) {
 #pragma unroll
                 for (int q = 0; q < B; ++q) {
                     if (ids[q] < 0) continue;
@@ -523,7 +529,7 @@ __global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
         const unsigned char* st = stages + stage * L.stage_bytes();
         const TileHdr* hp = reinterpret_cast<const TileHdr*>(st + L.off_hdr());
         const int hv0 = hp->v0, hnv = hp->nv, wr = hp->wr[warp];
-        const int rounds = wr & 0xffff, sb = wr >> 16;
+        const int rounds = ta.dbg == 1 ? 0 : wr & 0xffff, sb = wr >> 16;
         const uint2* sent = reinterpret_cast<const uint2*>(st + L.off_ent()) + 32 * sb + lane;
         const R4* np = reinterpret_cast<const R4*>(st + L.off_npos());
         const bool act = lv < hnv;
@@ -533,10 +539,22 @@ __global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
         const R4 y4 = reinterpret_cast<const R4*>(st + L.off_y())[lvc];
         const R xi[3] = {xi4.x, xi4.y, xi4.z};
         const R dx[3] = {xi[0] - xt4.x, xi[1] - xt4.y, xi[2] - xt4.z};
-        R f[3] = {R(0), R(0), R(0)};
-        R H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
-        R sv = R(0), dsc = R(0), opd = R(1);
-        constexpr int U = OCC >= 3 ? 1 : VBD_TILE_U;
+        // NA = 4 / W accumulator sets: with W = 2, lane j sums entry positions j mod 4 (even
+        // rounds) and j + 2 mod 4 (odd rounds) apart and adds them before the butterfly --
+        // exactly the partial sums and pairing of the 4-lane variants (bitwise equal)
+        constexpr int NA = 4 / W;
+        R fa[NA][3], Ha[NA][6], sva[NA];
+#pragma unroll
+        for (int b = 0; b < NA; ++b) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) fa[b][q] = R(0);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) Ha[b][q] = R(0);
+            sva[b] = R(0);
+        }
+        R dsc = R(0), opd = R(1);
+        constexpr int U = OCC >= 3 && W == 4 ? 1 : VBD_TILE_U;  // register budget
+        static_assert(U % NA == 0, "rounds per iteration must cover the accumulator sets");
         const unsigned npb = smem_u32(np);
         const unsigned kb = smem_u32(skind);
         const unsigned sb32 = smem_u32(sent);
@@ -565,16 +583,25 @@ __global__ void __launch_bounds__(288, OCC) k1_tiles(const K1TArgs<R> ta)
                 const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
                 const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
                 const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
-                tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], dx, f, H, sv);
+                const int b = u % NA;  // i0 is a multiple of U, so (i0 + u) % NA == u % NA (unrolled)
+                tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], dx, fa[b], Ha[b], sva[b]);
                 if (UM && i0 + u == 0) {  // position j: lane j = 0 holds the vertex's first entry
                     dsc = r[9];
                     opd = r[10];
                 }
             }
         }
-        H[0] = H[0] + sv;
-        H[3] = H[3] + sv;
-        H[5] = H[5] + sv;
+        R f[3], H[6];
+#pragma unroll
+        for (int b = 0; b < NA; ++b) {
+            Ha[b][0] = Ha[b][0] + sva[b];
+            Ha[b][3] = Ha[b][3] + sva[b];
+            Ha[b][5] = Ha[b][5] + sva[b];
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) f[q] = NA == 2 ? fa[0][q] + fa[NA - 1][q] : fa[0][q];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) H[q] = NA == 2 ? Ha[0][q] + Ha[NA - 1][q] : Ha[0][q];
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));  // stage's smem no longer read
         // the W lanes of a vertex are vi + VPW j: same butterfly order as the other K1
