@@ -175,7 +175,7 @@ __device__ __forceinline__ void ec_terms(const R* __restrict__ w, R V, R mu, R l
 
 // DAMP = false: one material per vertex -- the undamped block is accumulated (H and the
 // scalar sum sv of V mu |w|^2) and the caller applies damping once per vertex.
-// ~53 FP instructions per entry (the F-form needs ~130).
+// ~50 FP instructions per entry (the F-form needs ~130).
 template <typename R, bool DAMP>
 __device__ __forceinline__ void tet_contrib_ec(const R* __restrict__ e0, const R* __restrict__ e1,
                                                const R* __restrict__ e2, const R* __restrict__ t, R dsc, R opd,
@@ -190,11 +190,11 @@ __device__ __forceinline__ void tet_contrib_ec(const R* __restrict__ e0, const R
 #pragma unroll
     for (int a = 0; a < 3; ++a) cw[a] = fma(t[5], c[a], k[a]);  // r C w
     const R vc = fma(t[6], dot3(e2, c), -t[7]);                  // r (J - gamma)
-    R g[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)  // V (mu F w + lam (J - gamma) C w)
-        g[a] = fma(vc, cw[a], fma(t[2], e2[a], fma(t[1], e1[a], mul_rn(t[0], e0[a]))));
     if (DAMP) {
+        R g[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)  // V (mu F w + lam (J - gamma) C w)
+            g[a] = fma(vc, cw[a], fma(t[2], e2[a], fma(t[1], e1[a], mul_rn(t[0], e0[a]))));
         R he[6];
         he[0] = fma(cw[0], cw[0], t[8]);
         he[1] = mul_rn(cw[0], cw[1]);
@@ -211,7 +211,8 @@ __device__ __forceinline__ void tet_contrib_ec(const R* __restrict__ e0, const R
         for (int q = 0; q < 6; ++q) H[q] = fma(opd, he[q], H[q]);
     } else {
 #pragma unroll
-        for (int a = 0; a < 3; ++a) f[a] = f[a] - g[a];
+        for (int a = 0; a < 3; ++a)  // f -= V (mu F w + lam (J - gamma) C w), one FFMA per term
+            f[a] = fma(-vc, cw[a], fma(-t[2], e2[a], fma(-t[1], e1[a], fma(-t[0], e0[a], f[a]))));
         H[0] = fma(cw[0], cw[0], H[0]);
         H[1] = fma(cw[0], cw[1], H[1]);
         H[2] = fma(cw[0], cw[2], H[2]);
