@@ -351,3 +351,59 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned bar, unsigned phase)
         "}\n" ::"r"(bar), "r"(phase), "r"(VBD_MBAR_SUSPEND_NS) : "memory");
 }
 
+
+// ---------------------------------------------------------------------------------------
+// tet_contrib_ec<float, false> with the x/y components of each 3-vector packed as fp32x2
+// (FFMA2 / FMUL2 / FADD2 on sm_100; a scalar operand is broadcast to both halves).  The x/y
+// pair of a position comes straight from its 16-byte shared-memory load; each component
+// executes exactly the scalar operation sequence (round-to-nearest per component;
+// x - a b == x + (-a) b), so results are bitwise those of tet_contrib_ec.  Cross products and
+// the volume term stay scalar.  f is (f0, f1) + f2; H is (H0, H3), (H2, H4), H1, H5.
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+
+struct AccXY {
+    float2 f01;    // f0, f1
+    float f2;
+    float2 h03;    // H0, H3
+    float2 h24;    // H2, H4
+    float h1, h5, sv;
+    __device__ __forceinline__ void zero()
+    {
+        f01 = h03 = h24 = make_float2(0.f, 0.f);
+        f2 = h1 = h5 = sv = 0.f;
+    }
+};
+
+__device__ __forceinline__ void tet_contrib_ec_xy(float4 p0, float4 p1, float4 p2, float2 nxy, float nz,
+                                                  const float* __restrict__ t, AccXY& A)
+{
+    // edges e_k = p_k - x_i
+    const float2 e0 = add2(make_float2(p0.x, p0.y), nxy), e1 = add2(make_float2(p1.x, p1.y), nxy),
+                 e2 = add2(make_float2(p2.x, p2.y), nxy);
+    const float e0z = p0.z + nz, e1z = p1.z + nz, e2z = p2.z + nz;
+    // u = t3 e1 - t4 e0
+    const float2 u = fma2(bc2(t[3]), e1, mul2(bc2(-t[4]), e0));
+    const float uz = __fmaf_rn(t[3], e1z, -__fmul_rn(t[4], e0z));
+    // c = e0 x e1, k = u x e2 (scalar, as cross3)
+    const float c0 = __fmaf_rn(e0.y, e1z, -__fmul_rn(e0z, e1.y));
+    const float c1 = __fmaf_rn(e0z, e1.x, -__fmul_rn(e0.x, e1z));
+    const float c2 = __fmaf_rn(e0.x, e1.y, -__fmul_rn(e0.y, e1.x));
+    const float k0 = __fmaf_rn(u.y, e2z, -__fmul_rn(uz, e2.y));
+    const float k1 = __fmaf_rn(uz, e2.x, -__fmul_rn(u.x, e2z));
+    const float k2 = __fmaf_rn(u.x, e2.y, -__fmul_rn(u.y, e2.x));
+    // r C w
+    const float2 cw = fma2(bc2(t[5]), make_float2(c0, c1), make_float2(k0, k1));
+    const float cwz = __fmaf_rn(t[5], c2, k2);
+    // r (J - gamma)
+    const float vc = __fmaf_rn(t[6], __fmaf_rn(e2z, c2, __fmaf_rn(e2.y, c1, __fmul_rn(e2.x, c0))), -t[7]);
+    A.f01 = fma2(bc2(-vc), cw, fma2(bc2(-t[2]), e2, fma2(bc2(-t[1]), e1, fma2(bc2(-t[0]), e0, A.f01))));
+    A.f2 = __fmaf_rn(-vc, cwz, __fmaf_rn(-t[2], e2z, __fmaf_rn(-t[1], e1z, __fmaf_rn(-t[0], e0z, A.f2))));
+    A.h03 = fma2(cw, cw, A.h03);
+    A.h24 = fma2(cw, bc2(cwz), A.h24);
+    A.h1 = __fmaf_rn(cw.x, cw.y, A.h1);
+    A.h5 = __fmaf_rn(cwz, cwz, A.h5);
+    A.sv = A.sv + t[8];
+}

@@ -555,6 +555,13 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
         R dsc = R(0), opd = R(1);
         constexpr int U = OCC >= 3 && W == 4 ? 1 : VBD_TILE_U;  // register budget
         static_assert(U % NA == 0, "rounds per iteration must cover the accumulator sets");
+        // fp32 with one material per vertex: packed fp32x2 arithmetic (tet_contrib_ec_xy)
+        constexpr bool PACK = sizeof(R) == 4 && UM;
+        AccXY acc[NA];
+#pragma unroll
+        for (int b = 0; b < NA; ++b) acc[b].zero();
+        const float2 nxy = make_float2(-(float)xi[0], -(float)xi[1]);
+        const float nz = -(float)xi[2];
         const unsigned npb = smem_u32(np);
         const unsigned kb = smem_u32(skind);
         const unsigned sb32 = smem_u32(sent);
@@ -568,27 +575,64 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                 lds_v(npb + (e[u].x >> 16), p[u][1]);
                 lds_v(npb + (e[u].y & 0xffffu), p[u][2]);
             }
+            if constexpr (PACK) {  // x/y of every 3-vector packed as fp32x2 (FFMA2)
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                R r[KindRec<R>::HOT];
-                const unsigned rp = kb + (e[u].y >> 16);
+                for (int u = 0; u < U; ++u) {
+                    float r[KindRec<R>::HOT];
+                    const unsigned rp = kb + (e[u].y >> 16);
 #pragma unroll
-                for (int q = 0; q < QH; ++q) {
-                    PL v;
-                    lds_v(rp + 16u * q, v);
-                    const R* vr = reinterpret_cast<const R*>(&v);
-#pragma unroll
-                    for (int z = 0; z < 16 / (int)sizeof(R); ++z) r[q * (16 / (int)sizeof(R)) + z] = vr[z];
+                    for (int q = 0; q < QH; ++q) {
+                        PL v;
+                        lds_v(rp + 16u * q, v);
+                        r[4 * q] = v.x;
+                        r[4 * q + 1] = v.y;
+                        r[4 * q + 2] = v.z;
+                        r[4 * q + 3] = v.w;
+                    }
+                    tet_contrib_ec_xy(p[u][0], p[u][1], p[u][2], nxy, nz, r, acc[u % NA]);
+                    if (i0 + u == 0) {  // position j: lane j = 0 holds the vertex's first entry
+                        dsc = r[9];
+                        opd = r[10];
+                    }
                 }
-                const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
-                const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
-                const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
-                const int b = u % NA;  // i0 is a multiple of U, so (i0 + u) % NA == u % NA (unrolled)
-                tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], dx, fa[b], Ha[b], sva[b]);
-                if (UM && i0 + u == 0) {  // position j: lane j = 0 holds the vertex's first entry
-                    dsc = r[9];
-                    opd = r[10];
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    R r[KindRec<R>::HOT];
+                    const unsigned rp = kb + (e[u].y >> 16);
+#pragma unroll
+                    for (int q = 0; q < QH; ++q) {
+                        PL v;
+                        lds_v(rp + 16u * q, v);
+                        const R* vr = reinterpret_cast<const R*>(&v);
+#pragma unroll
+                        for (int z = 0; z < 16 / (int)sizeof(R); ++z) r[q * (16 / (int)sizeof(R)) + z] = vr[z];
+                    }
+                    const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
+                    const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
+                    const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
+                    const int b = u % NA;  // i0 is a multiple of U, so (i0 + u) % NA == u % NA (unrolled)
+                    tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], dx, fa[b], Ha[b], sva[b]);
+                    if (UM && i0 + u == 0) {  // position j: lane j = 0 holds the vertex's first entry
+                        dsc = r[9];
+                        opd = r[10];
+                    }
                 }
+            }
+        }
+        if constexpr (PACK) {
+#pragma unroll
+            for (int b = 0; b < NA; ++b) {
+                fa[b][0] = acc[b].f01.x;
+                fa[b][1] = acc[b].f01.y;
+                fa[b][2] = acc[b].f2;
+                Ha[b][0] = acc[b].h03.x;
+                Ha[b][1] = acc[b].h1;
+                Ha[b][2] = acc[b].h24.x;
+                Ha[b][3] = acc[b].h03.y;
+                Ha[b][4] = acc[b].h24.y;
+                Ha[b][5] = acc[b].h5;
+                sva[b] = acc[b].sv;
             }
         }
         R f[3], H[6];
