@@ -318,7 +318,18 @@ def run_ours(args):
     if world > 1 and cfg.sharding == "slabs":
         if args.halo == "p2p":  # fused K1 push into the neighbour's ghosts over NVLink
             from paper_2403_06321_b200.dist import SlabP2P
-            exch = SlabP2P.distributed(ctx, rank, world, device=local)
+            ok = 1.0
+            try:
+                exch = SlabP2P.distributed(ctx, rank, world, device=local)
+            except Exception as e:  # e.g. no peer access between these GPUs
+                print(f"rank {rank}: P2P halo setup failed ({e}); using the NCCL halo", file=sys.stderr)
+                ok = 0.0
+            flag = torch.tensor([ok], device=red_dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank takes the same path
+            if flag.item() < 1.0:
+                args.halo = "nccl"
+                ctx.p2p_disconnect()
+                exch = SlabExchange.distributed(ctx, rank, world)
         else:                   # NCCL send/recv per colour
             exch = SlabExchange.distributed(ctx, rank, world)
     stream = torch.cuda.ExternalStream(ctx.stream) if ctx.stream else torch.cuda.current_stream()

@@ -191,6 +191,7 @@ int vbd_ipc_open(int device, const void* handle64, void** ptr);
 int vbd_ipc_close(void* ptr);
 int vbd_halo_p2p_connect(vbd_ctx* ctx, int32_t side, void* peer_pos, void* peer_flags,
                          const int64_t* peer_ghost_begin, const int64_t* peer_ghost_count);
+                         /* peer_pos == NULL disconnects `side` (the other arguments are ignored) */
 int vbd_step_p2p_launch(vbd_ctx* ctx, const vbd_step_params* params); /* asynchronous */
 int vbd_step_p2p_finish(vbd_ctx* ctx, vbd_step_result* res);
 

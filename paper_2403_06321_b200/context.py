@@ -344,6 +344,11 @@ class DeviceContext:
                                                    ctypes.c_void_p(peer_flags), _lib.ptr(b),
                                                    _lib.ptr(n)))
 
+    def p2p_disconnect(self):
+        """Drop both peer mappings (the K1 epilogue stops pushing into neighbour ghosts)."""
+        for side in (0, 1):
+            _lib.check(_lib.lib().vbd_halo_p2p_connect(self._h, side, None, None, None, None))
+
     def step_p2p_launch(self, params):
         _lib.check(_lib.lib().vbd_step_p2p_launch(self._h, ctypes.byref(params)))
 

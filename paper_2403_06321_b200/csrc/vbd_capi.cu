@@ -863,11 +863,14 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     static const bool bulk_on = !getenv("VBD_K1_BULK") || atoi(getenv("VBD_K1_BULK")) != 0;
     const size_t smem = (size_t)(256 / W) * (size_t)std::max(a.max_deg, 1) * 16;
     if (a.kinds && !a.group && !a.out && bulk_on && smem <= 64 * 1024) {
-        static bool attr[2] = {false, false};
+        static bool attr[64][2] = {};  // per device
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        dev &= 63;
         auto kb = um ? k1_color_pass_bulk<R, W, U, B, true> : k1_color_pass_bulk<R, W, U, B, false>;
-        if (!attr[um]) {
+        if (!attr[dev][um]) {
             CK(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-            attr[um] = true;
+            attr[dev][um] = true;
         }
         kb<<<nb, 256, smem, s>>>(a);
         return;
@@ -888,18 +891,20 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
 template <typename R, bool UM, int S, int W, int OCC, int DEF>
 void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
 {
-    static size_t attr = 0;
-    static int per_sm = 0, sms = 148;
-    if (smem > attr) {
+    // the shared-memory opt-in and the occupancy are per device
+    static size_t attr[64] = {};
+    static int per_sm[64] = {}, sms[64] = {};
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    dev &= 63;
+    if (smem > attr[dev]) {
         CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC, DEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
-        int dev = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tiles<R, UM, S, W, OCC, DEF>, 64 * W + 32, smem));
-        per_sm = std::max(1, per_sm);
+        attr[dev] = smem;
+        CK(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k1_tiles<R, UM, S, W, OCC, DEF>, 64 * W + 32, smem));
+        per_sm[dev] = std::max(1, per_sm[dev]);
     }
-    const int grid = std::min(ta.tcount, per_sm * sms);
+    const int grid = std::min(ta.tcount, per_sm[dev] * sms[dev]);
     k1_tiles<R, UM, S, W, OCC, DEF><<<grid, 64 * W + 32, smem, s>>>(ta);
 }
 
@@ -2404,8 +2409,17 @@ int vbd_halo_p2p_connect(vbd_ctx* c, int32_t side, void* peer_pos, void* peer_fl
                          const int64_t* peer_ghost_begin, const int64_t* peer_ghost_count)
 {
     return guarded([&] {
-        if (!c || side < 0 || side > 1 || !peer_pos || !peer_flags || !peer_ghost_begin || !peer_ghost_count)
-            fail(VBD_ERR_ARG, "NULL argument");
+        if (!c || side < 0 || side > 1) fail(VBD_ERR_ARG, "NULL argument");
+        if (!peer_pos) {  // disconnect this side (e.g. falling back to the NCCL halo)
+            c->peer_pos[side] = nullptr;
+            c->peer_flag_slot[side] = nullptr;
+            if (c->p2p_gexec) {
+                cudaGraphExecDestroy(c->p2p_gexec);
+                c->p2p_gexec = nullptr;
+            }
+            return;
+        }
+        if (!peer_flags || !peer_ghost_begin || !peer_ghost_count) fail(VBD_ERR_ARG, "NULL argument");
         if (c->bnd_cnt[side].empty()) fail(VBD_ERR_ARG, "context is not a slab");
         CK(cudaSetDevice(c->device));
         ensure_p2p_flags(c);

@@ -354,3 +354,29 @@ def test_slab_p2p_bitwise_equals_single_context(V):
             lo = max(cuts[r] - 1, 0)
             own = slice((cuts[r] - lo) * plane, (cuts[r + 1] - lo) * plane)
             assert np.array_equal(xs[own], xf[cuts[r] * plane:cuts[r + 1] * plane]), (rho, r)
+
+
+def test_slab_p2p_disconnect_then_nccl_style_exchange(V):
+    """bench.py's fallback: slabs connected for the P2P halo, then disconnected and stepped with
+    the host-driven exchange -- no stale peer stores, still bitwise equal to one context."""
+    beam = V.Beam(24, 7, 6, 0.02, 1e6, 1e7, 1e-6, fix_min_x=True)
+    full = V.DeviceContext.from_beams([beam], precision="fp32")
+    cuts = [0, 7, 15, beam.nx]
+    slabs = [V.DeviceContext.from_beams([beam], precision="fp32", slab=(cuts[r], cuts[r + 1]))
+             for r in range(3)]
+    from paper_2403_06321_b200.dist import SlabExchange, SlabP2P
+    SlabP2P.local(slabs)
+    for sctx in slabs:
+        sctx.p2p_disconnect()
+    ex = SlabExchange.local(slabs)
+    p = full.step_params(1 / 120, 8, 0.9, 1e-10, "adaptive", G)
+    for _ in range(3):
+        full.step(p)
+        ex.step(p)
+    xf = full.get_state(x=True)["x"]
+    plane = beam.ny * beam.nz
+    for r, sctx in enumerate(slabs):
+        xs = sctx.get_state(x=True)["x"]
+        lo = max(cuts[r] - 1, 0)
+        own = slice((cuts[r] - lo) * plane, (cuts[r + 1] - lo) * plane)
+        assert np.array_equal(xs[own], xf[cuts[r] * plane:cuts[r + 1] * plane]), r
