@@ -284,6 +284,15 @@ def ncu_traffic(cfg_name, precision, variant):
     return d.get(f"{cfg_name}_{precision}_{variant}")
 
 
+def ncu_limiter(cfg_name, precision, variant):
+    """The measured limiter of the colour pass from the committed ncu capture
+    (profiles/k1_limiter.json): SOL percentages of the pipes that bound it."""
+    p = ROOT / "profiles" / "k1_limiter.json"
+    if not p.exists():
+        return None
+    return json.loads(p.read_text()).get(f"{cfg_name}_{precision}_{variant}")
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -481,7 +490,9 @@ def run_ours(args):
                          "layout_achieved": layout_achieved, "layout_frac": layout_achieved / peak,
                          "note": "frac > 1 is the lossless entry compression (DESIGN 2): the kernel "
                                  "moves layout_bytes, not the reference layout's bytes; layout_frac "
-                                 "is its HBM share, and its limiter is SM issue (profiles/)",
+                                 "is its HBM share; its limiter is the L1/shared-memory wavefront "
+                                 "pipe (limiter, profiles/r01_k1t_c5_analysis.md)",
+                         "limiter": ncu_limiter(cfg.name, args.precision, variant),
                          "traffic_unit": "DRAM bytes per k1 launch (ncu, profiles/k1_traffic.json)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
