@@ -125,3 +125,20 @@ def test_cli_color_matches_reference(tmp_path):
                                         "--eles", str(tmp_path / "m.ele")])
     assert res.exit_code == 0, res.output
     assert json.dumps(json.loads(res.output), sort_keys=True) == str(GOLD["color_json"])
+
+
+@pytest.mark.parametrize("name", ("base", "mixed"))
+def test_run_simulation_fp32_within_tolerance(name, tmp_path):
+    """solver.precision = "fp32" (the performance build): same frames within 1e-5 x bbox
+    diagonal of the reference's fp64 run (BASELINE north_star tolerance)."""
+    doc = json.loads(str(GOLD[f"{name}_scene"]))
+    doc.setdefault("solver", {})["precision"] = "fp32"
+    run_simulation(parse_scene(json.dumps(doc)), tmp_path)
+    files = sorted(p.name for p in tmp_path.glob("frame_*"))
+    assert files == list(GOLD[f"{name}_frame_files"])
+    pos, _ = load_frame(tmp_path / files[-1])
+    rest = GOLD[f"{name}_rest_positions"]
+    diag = np.linalg.norm(rest.max(0) - rest.min(0))
+    assert np.abs(pos - GOLD[f"{name}_last_x"]).max() <= 1e-5 * diag
+    got = _metrics(tmp_path)
+    np.testing.assert_allclose(got[:, 2], GOLD[f"{name}_metrics"][:, 2], rtol=1e-4)
