@@ -599,12 +599,26 @@ template <typename R> void build_tiles(vbd_ctx* c)
         upload(dnl, nl_real.data(), nl_real.size(), s);
         ids.alloc((size_t)std::max<long long>(total, 1) * 4);
         asg.alloc((size_t)std::max<long long>(total, 1) * 4);
+        // bank groups: DSATUR colouring per tile (VBD_TILE_BANKS=greedy: the sweep-order greedy)
+        const char* bm = getenv("VBD_TILE_BANKS");
+        const bool dsatur = !(bm && std::string(bm) == "greedy");
+        const unsigned pad_pos = (unsigned)(c->nbr_cap * sizeof(typename Vec4<R>::T));
+        if (dsatur) {
+            int vmax = 1;
+            for (int t = 0; t < nt; ++t) vmax = std::max(vmax, nl_real[t]);
+            const int mmax = 3 * c->ent_cap;
+            const size_t smem = (size_t)vmax * 12 + (size_t)(vmax + 1) * 4 + (size_t)mmax * 2 + 16;
+            CK(cudaFuncSetAttribute(k_tile_banks_dsatur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_tile_banks_dsatur<<<nt, 32, smem, s>>>(c->loff.as<long long>(), sbase.as<long long>(), dnl.as<int>(), nt,
+                                                    (unsigned)sizeof(typename Vec4<R>::T), pad_pos,
+                                                    c->tent.as<uint2>(), asg.as<int>(), vmax, mmax);
+            CK(cudaGetLastError());
+        }
         k_tile_banks<<<blocks_for(nt, 64), 64, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
                                                       c->loff.as<long long>(), sbase.as<long long>(), dnl.as<int>(),
-                                                      nt, W, (unsigned)sizeof(typename Vec4<R>::T),
-                                                      (unsigned)(c->nbr_cap * sizeof(typename Vec4<R>::T)),
+                                                      nt, W, (unsigned)sizeof(typename Vec4<R>::T), pad_pos,
                                                       c->tnbr.as<int>(), c->tent.as<uint2>(), ids.as<int>(),
-                                                      asg.as<int>());
+                                                      asg.as<int>(), dsatur ? 1 : 0);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s));
     }
