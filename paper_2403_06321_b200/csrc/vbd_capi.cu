@@ -184,6 +184,7 @@ struct vbd_ctx {
     DBuf tv0, tnv, loff, tnbr, tent, tdesc;
     int tile_stages = 2, tile_w = 4, tile_occ = 2;
     bool tile_defer = true;  // K1T deferred block solves (VBD_TILE_DEFER=0 disables)
+    bool tile_kg = false;    // K1T kind records read from global (table too large for shared memory)
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -478,7 +479,9 @@ template <typename R> void compact_entries(vbd_ctx* c)
     CK(cudaStreamSynchronize(s));
     if (hc[2]) fail(VBD_ERR_INTERNAL, "entry dictionary lookup failed");
     c->ent.swap(cent);  // the explicit planes are released with `cent`
-    c->kinds.alloc((size_t)nk * KindRec<R>::Q * 16);
+    // nk records + one zero record (index nk: the padding slots of K1T with global kinds)
+    c->kinds.alloc((size_t)(nk + 1) * KindRec<R>::Q * 16);
+    CK(cudaMemsetAsync(c->kinds.p, 0, (size_t)(nk + 1) * KindRec<R>::Q * 16, s));
     c->compact = true;
     c->nkinds = nk;
 }
@@ -555,22 +558,29 @@ template <typename R> void build_tiles(vbd_ctx* c)
         mx = std::max(mx, nls[t]);
         ms = std::max(ms, nss[t]);
     }
-    // slots hold 16-bit shared-memory byte offsets (+1 zero position, +1 zero kind record)
+    // slots hold 16-bit shared-memory byte offsets (+1 zero position) and a 16-bit kind: the
+    // record's byte offset in the shared-memory table, or (KG: tables over 32 KB, e.g. fp64
+    // grids whose rest shapes differ in the last bits) its index in the global table
     if ((mx + 1) * (long long)sizeof(typename Vec4<R>::T) > 65535) return;
-    if ((long long)(c->nkinds + 1) * KindRec<R>::HOT * sizeof(R) > 65535) return;
+    if (c->nkinds >= 65535) return;
+    const char* kge = getenv("VBD_TILE_KG");
+    c->tile_kg = (long long)(c->nkinds + 1) * KindRec<R>::HOT * sizeof(R) > 32768 || (kge && *kge == '1');
+    if (c->tile_kg && W != 2) return;  // compiled for the 2-lane kernel
     c->nbr_cap = (int)mx;
     c->ent_cap = (int)ms;
-    TileSmem<R> L{c->ent_cap, c->nbr_cap, c->nkinds, VPT};
-    // as many stages (2..4) as fit two CTAs per SM
+    TileSmem<R> L{c->ent_cap, c->nbr_cap, c->tile_kg ? -1 : (int)c->nkinds, VPT};
+    // as many stages (2..4) as fit three CTAs per SM, else two (2-lane: 2 stages)
     const char* oe = getenv("VBD_TILE_OCC");
     c->tile_occ = oe && *oe == '2' ? 2 : 3;  // 3 CTAs per SM (one entry per lane in flight) measured faster
     const char* de = getenv("VBD_TILE_DEFER");
     c->tile_defer = !(de && *de == '0');
-    const size_t cap = c->tile_occ == 3 ? 75 * 1024 : VBD_TILE_SMEM_MAX;
     int stages = 0;
-    for (int st = 4; st >= 2 && !stages; --st)
-        if (L.total(st) <= cap) stages = st;
-    for (int st = 3; st >= 2 && !stages && c->tile_occ == 2; --st)  // else one CTA per SM
+    for (int st = 4; st >= 2 && !stages && c->tile_occ == 3; --st)
+        if (L.total(st) <= 75 * 1024) stages = st;
+    if (!stages) c->tile_occ = 2;  // e.g. fp64: 32-byte positions
+    for (int st = W == 2 ? 2 : 4; st >= 2 && !stages; --st)
+        if (L.total(st) <= VBD_TILE_SMEM_MAX) stages = st;
+    for (int st = 3; st >= 2 && !stages && W == 4; --st)  // else one CTA per SM
         if (L.total(st) <= 2 * VBD_TILE_SMEM_MAX) stages = st;
     const char* se = getenv("VBD_TILE_STAGES");
     if (se && *se) stages = std::min(stages, atoi(se));
@@ -590,8 +600,10 @@ template <typename R> void build_tiles(vbd_ctx* c)
                                                 c->tnbr.as<int>(), c->tent.as<uint2>(), W,
                                                 (unsigned)sizeof(typename Vec4<R>::T),
                                                 (unsigned)(c->nbr_cap * sizeof(typename Vec4<R>::T)),
-                                                (unsigned)(KindRec<R>::HOT * sizeof(R)),
-                                                (unsigned)(c->nkinds * KindRec<R>::HOT * sizeof(R)), err.as<int>());
+                                                c->tile_kg ? 1u : (unsigned)(KindRec<R>::HOT * sizeof(R)),
+                                                c->tile_kg ? (unsigned)c->nkinds
+                                                           : (unsigned)(c->nkinds * KindRec<R>::HOT * sizeof(R)),
+                                                err.as<int>());
     CK(cudaGetLastError());
     if (read_scalar<int>(err.p, s)) fail(VBD_ERR_INTERNAL, "tile build failed");
     if (slack > 0) {
@@ -902,7 +914,7 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     else k1_color_pass<R, W, U, B, false, false><<<nb, 256, 0, s>>>(a);
 }
 
-template <typename R, bool UM, int S, int W, int OCC, int DEF>
+template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false>
 void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
 {
     // the shared-memory opt-in and the occupancy are per device
@@ -912,19 +924,26 @@ void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
     CK(cudaGetDevice(&dev));
     dev &= 63;
     if (smem > attr[dev]) {
-        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC, DEF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC, DEF, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[dev] = smem;
         CK(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k1_tiles<R, UM, S, W, OCC, DEF>, 64 * W + 32, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k1_tiles<R, UM, S, W, OCC, DEF, KG>, 64 * W + 32, smem));
         per_sm[dev] = std::max(1, per_sm[dev]);
     }
     const int grid = std::min(ta.tcount, per_sm[dev] * sms[dev]);
-    k1_tiles<R, UM, S, W, OCC, DEF><<<grid, 64 * W + 32, smem, s>>>(ta);
+    k1_tiles<R, UM, S, W, OCC, DEF, KG><<<grid, 64 * W + 32, smem, s>>>(ta);
 }
 
 template <typename R, bool UM, int W>
-void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, int occ, bool defer, size_t smem, cudaStream_t s)
+void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, int occ, bool defer, bool kg, size_t smem,
+                       cudaStream_t s)
 {
+    if constexpr (W == 2) {  // 2 stages; global kind records or 2 CTAs per SM
+        if (kg && occ == 3) return launch_k1_tiles_v<R, UM, 2, W, 3, W, true>(ta, smem, s);
+        if (kg) return launch_k1_tiles_v<R, UM, 2, W, 2, W, true>(ta, smem, s);
+        if (occ == 2) return launch_k1_tiles_v<R, UM, 2, W, 2, W>(ta, smem, s);
+    }
+    if (kg) fail(VBD_ERR_INTERNAL, "global kind records are compiled for 2 lanes per vertex");
     if (occ == 3) {
         if (stages >= 3) launch_k1_tiles_v<R, UM, 3, W, 3, 1>(ta, smem, s);
         else if (defer) launch_k1_tiles_v<R, UM, 2, W, 3, W>(ta, smem, s);
@@ -935,18 +954,16 @@ void launch_k1_tiles_s(const K1TArgs<R>& ta, int stages, int occ, bool defer, si
         if (stages >= 4) launch_k1_tiles_v<R, UM, 4, W, 2, 1>(ta, smem, s);
         else if (stages == 3) launch_k1_tiles_v<R, UM, 3, W, 2, 1>(ta, smem, s);
         else launch_k1_tiles_v<R, UM, 2, W, 2, 1>(ta, smem, s);
-    } else {
-        fail(VBD_ERR_ARG, "VBD_TILE_W=2 is compiled for 3 CTAs per SM only");
     }
 }
 
 template <typename R, bool UM>
-void launch_k1_tiles_w(const K1TArgs<R>& ta, int W, int stages, int occ, bool defer, size_t smem,
+void launch_k1_tiles_w(const K1TArgs<R>& ta, int W, int stages, int occ, bool defer, bool kg, size_t smem,
                        cudaStream_t s)
 {
     // W lanes per vertex in 2 W consumer warps (64-vertex tiles); 1 lane was measured slower
-    if (W == 2) launch_k1_tiles_s<R, UM, 2>(ta, stages, occ, defer, smem, s);
-    else launch_k1_tiles_s<R, UM, 4>(ta, stages, occ, defer, smem, s);
+    if (W == 2) launch_k1_tiles_s<R, UM, 2>(ta, stages, occ, defer, kg, smem, s);
+    else launch_k1_tiles_s<R, UM, 4>(ta, stages, occ, defer, kg, smem, s);
 }
 
 template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
@@ -970,10 +987,10 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     const char* dbg = getenv("VBD_TILE_DBG");
     ta.dbg = dbg && *dbg ? atoi(dbg) : 0;
     if (ta.dbg) ta.a.flag = nullptr;  // garbage positions in the timing experiments
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds, 64};
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, c->tile_kg ? -1 : ta.nkinds, 64};
     const int S = c->tile_stages;
-    if (a.vmat) launch_k1_tiles_w<R, true>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, L.total(S), s);
-    else launch_k1_tiles_w<R, false>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, L.total(S), s);
+    if (a.vmat) launch_k1_tiles_w<R, true>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, c->tile_kg, L.total(S), s);
+    else launch_k1_tiles_w<R, false>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, c->tile_kg, L.total(S), s);
     return true;
 }
 
@@ -2045,8 +2062,8 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         info->tile_stages = c->tiles ? c->tile_stages : 0;
         info->tile_ent_cap = c->tiles ? c->ent_cap : 0;
         if (c->tiles) {
-            const TileSmem<float> L32{c->ent_cap, c->nbr_cap, (int)c->nkinds, 64};
-            const TileSmem<double> L64{c->ent_cap, c->nbr_cap, (int)c->nkinds, 64};
+            const TileSmem<float> L32{c->ent_cap, c->nbr_cap, c->tile_kg ? -1 : (int)c->nkinds, 64};
+            const TileSmem<double> L64{c->ent_cap, c->nbr_cap, c->tile_kg ? -1 : (int)c->nkinds, 64};
             info->tile_smem_bytes = (int)(c->precision == VBD_PREC_F64 ? L64.total(c->tile_stages)
                                                                        : L32.total(c->tile_stages));
         }

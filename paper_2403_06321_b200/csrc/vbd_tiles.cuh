@@ -526,7 +526,9 @@ __device__ __forceinline__ void k1t_store(const K1Args<R>& a, int v, typename Ve
 // Tiles are 64 vertices: NCW = 2 W consumer warps of 32 / W vertices (W = 4: 8 warps, W = 2:
 // 4 warps of 16 vertices with twice the rounds -- half the per-vertex reduction and solve
 // overhead per entry).
-template <typename R, bool UM, int S, int W, int OCC, int DEF>
+// KG: the kind table is too large for shared memory (e.g. fp64 grids whose rest shapes differ
+// in the last bits): slots carry the kind index and the records are read through L1 from global.
+template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false>
 __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta)
 {
     typedef typename Vec4<R>::T R4;
@@ -535,14 +537,16 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long full[S], empty[S];
     const K1Args<R>& a = ta.a;
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, ta.nkinds, NCW * VPW};
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, KG ? -1 : ta.nkinds, NCW * VPW};
     typedef typename PlaneT<R>::T PL;
     PL* skind = reinterpret_cast<PL*>(smem);
     unsigned char* stages = smem + ((L.kinds_bytes() + 127) & ~(size_t)127);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int QH = KindRec<R>::QH, Q = KindRec<R>::Q;
-    for (int i = tid; i < ta.nkinds * QH; i += blockDim.x) skind[i] = ta.kinds[(i / QH) * Q + i % QH];
-    for (int i = tid; i < QH; i += blockDim.x) skind[ta.nkinds * QH + i] = PL{};  // padding: zero record
+    if (!KG) {
+        for (int i = tid; i < ta.nkinds * QH; i += blockDim.x) skind[i] = ta.kinds[(i / QH) * Q + i % QH];
+        for (int i = tid; i < QH; i += blockDim.x) skind[ta.nkinds * QH + i] = PL{};  // padding: zero record
+    }
     for (int s = 0; s < S; ++s)  // padding: zero position after the largest neighbour list
         if (tid == 0) *reinterpret_cast<R4*>(stages + s * L.stage_bytes() + L.off_npos() + ta.nbr_cap * sizeof(R4)) = R4{};
     if (tid == 0) {
@@ -711,7 +715,8 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
 #pragma unroll
                     for (int q = 0; q < QH; ++q) {
                         PL v;
-                        lds_v(rp + 16u * q, v);
+                        if constexpr (KG) v = __ldg(ta.kinds + (size_t)(e[u].y >> 16) * Q + q);
+                        else lds_v(rp + 16u * q, v);
                         r[4 * q] = v.x;
                         r[4 * q + 1] = v.y;
                         r[4 * q + 2] = v.z;
@@ -731,7 +736,8 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
 #pragma unroll
                     for (int q = 0; q < QH; ++q) {
                         PL v;
-                        lds_v(rp + 16u * q, v);
+                        if constexpr (KG) v = __ldg(ta.kinds + (size_t)(e[u].y >> 16) * Q + q);
+                        else lds_v(rp + 16u * q, v);
                         const R* vr = reinterpret_cast<const R*>(&v);
 #pragma unroll
                         for (int z = 0; z < 16 / (int)sizeof(R); ++z) r[q * (16 / (int)sizeof(R)) + z] = vr[z];
