@@ -642,12 +642,13 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
     static_assert(DEF == 1 || DEF == W, "deferral batches one tile per lane of a vertex");
     int tc = 0, qv = -1;  // DEF > 1: tiles since the last flush; the deferred vertex of this lane
     R qf[DEF > 1 ? 3 : 1], qH[DEF > 1 ? 6 : 1];
+    typename Vec4<R>::T qx{};  // its x (from the stage; a reload from global stalled the flush)
     auto flush = [&]() {
         if constexpr (DEF > 1) {
             if (qv >= 0) {
                 R d[3];
                 block_solve<R>(qf, qH, a.eps_det, a.mode, d);
-                R4 nx = a.pos[qv];  // own colour: not written by anyone else in this launch
+                R4 nx = qx;
                 nx.x = nx.x + d[0];
                 nx.y = nx.y + d[1];
                 nx.z = nx.z + d[2];
@@ -803,6 +804,7 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
 #pragma unroll
                 for (int q = 0; q < 6; ++q) qH[q] = H[q];
                 qv = act ? hv0 + lv : -1;
+                qx = xi4;
             }
             if (++tc == DEF) {
                 tc = 0;
