@@ -150,3 +150,36 @@ def test_device_generated_c5_like_block_is_compact(V):
     ctx = V.DeviceContext.from_beams([V.Beam(40, 40, 40, 0.01, 2e6, 2e7, 1e-7, fix_min_x=True)],
                                      precision="fp32")
     assert ctx.info.layout == 1 and ctx.info.num_entry_kinds <= 64
+
+
+def hub_system(O, n_spokes=240):
+    """A beam plus one hub vertex shared by n_spokes tets (degree far above a 5-tet grid's 32):
+    the tile build must decline or handle it, and every layout must still agree bitwise."""
+    m = O.generate_beam(9, 5, 5, 0.05)
+    rng = np.random.default_rng(3)
+    pos = m.rest_positions
+    hub = np.array([[0.2, 0.1, 0.35]])
+    pts = np.concatenate([pos, hub])
+    hub_id = len(pos)
+    tets = [list(t) for t in m.tets]
+    top = np.flatnonzero(pos[:, 2] > 0.19)
+    for _ in range(n_spokes):
+        a, b, c = rng.choice(top, 3, replace=False)
+        t = [hub_id, a, b, c]
+        d = np.linalg.det(np.stack([pts[t[1]] - pts[t[0]], pts[t[2]] - pts[t[0]], pts[t[3]] - pts[t[0]]]))
+        if abs(d) < 1e-7:
+            continue
+        tets.append(t if d > 0 else [t[0], t[2], t[1], t[3]])
+    mesh = O.build_tet_mesh(pts, np.asarray(tets, dtype=np.int64), 1000.0)
+    fixed = np.flatnonzero(pts[:, 0] < 1e-9)
+    return O.build_system([(mesh, (1e5, 1e6, 1e-6))], fixed)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_high_degree_vertex_all_layouts_bitwise(V, O, precision, monkeypatch):
+    s = hub_system(O)
+    a = steps(make_ctx(V, O, s, precision, "auto", monkeypatch), s, 3, rho=0.5, n_max=6)
+    b = steps(make_ctx(V, O, s, precision, "explicit", monkeypatch), s, 3, rho=0.5, n_max=6)
+    c = steps(make_ctx(V, O, s, precision, "compact", monkeypatch), s, 3, rho=0.5, n_max=6)
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["x"], c["x"])
+    assert np.isfinite(a["x"]).all()
