@@ -75,6 +75,8 @@ inline unsigned blocks_for(long long n, int bs = 256) { return (unsigned)((n + b
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaStream_t st = nullptr;  // pooled buffers: the stream they were allocated (and are freed) on
+    bool pooled = false;
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
@@ -86,17 +88,35 @@ struct DBuf {
         CK(cudaMalloc(&p, b));
         bytes = b;
     }
+    // stream-ordered allocation from the device's memory pool (no device-wide synchronisation
+    // on allocate / free; for the many short-lived scratch buffers of contact detection, sorts
+    // and scans)
+    void alloc_on(size_t b, cudaStream_t s)
+    {
+        release();
+        if (b == 0) b = 16;
+        CK(cudaMallocAsync(&p, b, s));
+        bytes = b;
+        st = s;
+        pooled = true;
+    }
     void release()
     {
-        if (p) cudaFree(p);
+        if (p) {
+            if (pooled) cudaFreeAsync(p, st);
+            else cudaFree(p);
+        }
         p = nullptr;
         bytes = 0;
+        pooled = false;
     }
     template <typename T> T* as() const { return static_cast<T*>(p); }
     void swap(DBuf& o)
     {
         std::swap(p, o.p);
         std::swap(bytes, o.bytes);
+        std::swap(st, o.st);
+        std::swap(pooled, o.pooled);
     }
 };
 
@@ -124,6 +144,17 @@ struct GraphKey {
 }  // namespace
 
 struct vbd_ctx {
+    // first member, destroyed last: pooled buffers are freed on this stream by their destructors
+    struct OwnedStream {
+        cudaStream_t s = nullptr;
+        ~OwnedStream()
+        {
+            if (s) {
+                cudaStreamSynchronize(s);
+                cudaStreamDestroy(s);
+            }
+        }
+    } owned;
     int device = 0;
     int precision = VBD_PREC_F32;
     cudaStream_t stream = nullptr;
@@ -205,7 +236,7 @@ struct vbd_ctx {
             for (auto& v : halo_recv[s])
                 for (auto* b : v) delete b;
         }
-        if (own_stream) cudaStreamDestroy(own_stream);
+        if (stream) cudaStreamSynchronize(stream);  // own_stream is destroyed by `owned`, last
     }
     size_t r4() const { return precision == VBD_PREC_F64 ? 32 : 16; }
     size_t rs() const { return precision == VBD_PREC_F64 ? 8 : 4; }
@@ -239,49 +270,46 @@ void sort_pairs_i32(DBuf& keys, DBuf& vals, long long n, int end_bit, cudaStream
 void sort_pairs_u64_i32(DBuf& keys, DBuf& vals, long long n, cudaStream_t s)
 {
     DBuf k2, v2, tmp;
-    k2.alloc(n * 8);
-    v2.alloc(n * 4);
+    k2.alloc_on(n * 8, s);
+    v2.alloc_on(n * 4, s);
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<unsigned long long>(),
                                        k2.as<unsigned long long>(), vals.as<int>(), v2.as<int>(),
                                        (int64_t)n, 0, 64, s));
-    tmp.alloc(tb);
+    tmp.alloc_on(tb, s);
     CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<unsigned long long>(),
                                        k2.as<unsigned long long>(), vals.as<int>(), v2.as<int>(),
                                        (int64_t)n, 0, 64, s));
     CK(cudaStreamSynchronize(s));
-    std::swap(keys.p, k2.p);
-    std::swap(keys.bytes, k2.bytes);
-    std::swap(vals.p, v2.p);
-    std::swap(vals.bytes, v2.bytes);
+    keys.swap(k2);
+    vals.swap(v2);
 }
 
 void sort_keys_u64(DBuf& keys, long long n, cudaStream_t s)
 {
     DBuf k2, tmp;
-    k2.alloc(n * 8);
+    k2.alloc_on(n * 8, s);
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.as<unsigned long long>(),
                                       k2.as<unsigned long long>(), (int64_t)n, 0, 64, s));
-    tmp.alloc(tb);
+    tmp.alloc_on(tb, s);
     CK(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.as<unsigned long long>(),
                                       k2.as<unsigned long long>(), (int64_t)n, 0, 64, s));
     CK(cudaStreamSynchronize(s));
-    std::swap(keys.p, k2.p);
-    std::swap(keys.bytes, k2.bytes);
+    keys.swap(k2);
 }
 
 // out[0] = 0, out[i+1] = sum(in[0..i]); in has n entries of type In
 template <typename In>
 void exclusive_offsets(const In* in, long long n, DBuf& out, cudaStream_t s)
 {
-    out.alloc((n + 1) * sizeof(long long));
+    out.alloc_on((n + 1) * sizeof(long long), s);
     CK(cudaMemsetAsync(out.p, 0, sizeof(long long), s));
     if (n == 0) return;
     DBuf tmp;
     size_t tb = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out.as<long long>() + 1, (int64_t)n, s));
-    tmp.alloc(tb);
+    tmp.alloc_on(tb, s);
     CK(cub::DeviceScan::InclusiveSum(tmp.p, tb, in, out.as<long long>() + 1, (int64_t)n, s));
     CK(cudaStreamSynchronize(s));
 }
@@ -1250,13 +1278,13 @@ template <typename R> long long grid_cells(vbd_ctx* c, const CollArgs<R>& a, int
 {
     cudaStream_t s = c->stream;
     DBuf cnt, off;
-    cnt.alloc((size_t)std::max(n, 1) * 8);
+    cnt.alloc_on((size_t)std::max(n, 1) * 8, s);
     if (n) k_cell_count<R><<<blocks_for(n), 256, 0, s>>>(a, what, n, cnt.as<long long>());
     CK(cudaGetLastError());
     exclusive_offsets(cnt.as<long long>(), n, off, s);
     const long long m = read_scalar<long long>(off.as<long long>() + n, s);
-    key.alloc((size_t)std::max<long long>(m, 1) * 8);
-    own.alloc((size_t)std::max<long long>(m, 1) * 4);
+    key.alloc_on((size_t)std::max<long long>(m, 1) * 8, s);
+    own.alloc_on((size_t)std::max<long long>(m, 1) * 4, s);
     if (n) k_cell_emit<R><<<blocks_for(n), 256, 0, s>>>(a, what, n, off.as<long long>(), key.as<unsigned long long>(),
                                                         own.as<int>());
     CK(cudaGetLastError());
@@ -1268,12 +1296,12 @@ void unique_u64(DBuf& keys, long long& n, cudaStream_t s)
 {
     if (n == 0) return;
     DBuf out, nsel, tmp;
-    out.alloc((size_t)n * 8);
-    nsel.alloc(8);
+    out.alloc_on((size_t)n * 8, s);
+    nsel.alloc_on(8, s);
     size_t tb = 0;
     CK(cub::DeviceSelect::Unique(nullptr, tb, keys.as<unsigned long long>(), out.as<unsigned long long>(),
                                  nsel.as<long long>(), (int64_t)n, s));
-    tmp.alloc(tb);
+    tmp.alloc_on(tb, s);
     CK(cub::DeviceSelect::Unique(tmp.p, tb, keys.as<unsigned long long>(), out.as<unsigned long long>(),
                                  nsel.as<long long>(), (int64_t)n, s));
     n = read_scalar<long long>(nsel.p, s);
@@ -1297,7 +1325,7 @@ template <typename R> long long broad_phase(vbd_ctx* c, const CollArgs<R>& a, bo
     const int* qown = ee ? to.as<int>() : qo.as<int>();
     const long long width = ee ? a.nedge : a.ntri;
     DBuf cnt, off;
-    cnt.alloc((size_t)std::max<long long>(nq, 1) * 8);
+    cnt.alloc_on((size_t)std::max<long long>(nq, 1) * 8, s);
     if (nq) {
         if (ee) k_cell_join<false, true><<<blocks_for(nq), 256, 0, s>>>(qkey, qown, nq, tk.as<unsigned long long>(), to.as<int>(), nt, width, cnt.as<long long>(), nullptr, nullptr);
         else k_cell_join<false, false><<<blocks_for(nq), 256, 0, s>>>(qkey, qown, nq, tk.as<unsigned long long>(), to.as<int>(), nt, width, cnt.as<long long>(), nullptr, nullptr);
@@ -1305,7 +1333,7 @@ template <typename R> long long broad_phase(vbd_ctx* c, const CollArgs<R>& a, bo
     CK(cudaGetLastError());
     exclusive_offsets(cnt.as<long long>(), nq, off, s);
     long long m = read_scalar<long long>(off.as<long long>() + nq, s);
-    codes.alloc((size_t)std::max<long long>(m, 1) * 8);
+    codes.alloc_on((size_t)std::max<long long>(m, 1) * 8, s);
     if (nq && m) {
         if (ee) k_cell_join<true, true><<<blocks_for(nq), 256, 0, s>>>(qkey, qown, nq, tk.as<unsigned long long>(), to.as<int>(), nt, width, nullptr, off.as<long long>(), codes.as<unsigned long long>());
         else k_cell_join<true, false><<<blocks_for(nq), 256, 0, s>>>(qkey, qown, nq, tk.as<unsigned long long>(), to.as<int>(), nt, width, nullptr, off.as<long long>(), codes.as<unsigned long long>());
@@ -1343,7 +1371,7 @@ long long compact_recs(vbd_ctx* c, const DBuf& recs, const DBuf& codes, const DB
     DBuf off;
     exclusive_offsets(acc.as<int>(), n, off, s);
     const long long m = read_scalar<long long>(off.as<long long>() + n, s);
-    out_recs.alloc((size_t)std::max<long long>(m, 1) * sizeof(ContactRec));
+    out_recs.alloc_on((size_t)std::max<long long>(m, 1) * sizeof(ContactRec), s);
     if (n) k_compact<ContactRec><<<blocks_for(n), 256, 0, s>>>(recs.as<ContactRec>(), acc.as<int>(), off.as<long long>(), n, out_recs.as<ContactRec>());
     if (out_codes) {
         out_codes->alloc((size_t)std::max<long long>(m, 1) * 8);
@@ -1360,8 +1388,8 @@ template <typename R> void detect_dcd(vbd_ctx* c)
     const CollArgs<R> a = coll_args<R>(c, c->xt, c->xt, c->coll_dcd_r);
     DBuf codes, recs, acc;
     const long long n = broad_phase<R>(c, a, false, codes);
-    recs.alloc((size_t)std::max<long long>(n, 1) * sizeof(ContactRec));
-    acc.alloc((size_t)std::max<long long>(n, 1) * 4);
+    recs.alloc_on((size_t)std::max<long long>(n, 1) * sizeof(ContactRec), s);
+    acc.alloc_on((size_t)std::max<long long>(n, 1) * 4, s);
     if (n) k_dcd_vt<R><<<blocks_for(n, 128), 128, 0, s>>>(a, codes.as<unsigned long long>(), n, c->coll_dcd_r, c->coll_kc,
                                                      c->coll_has_max_depth, c->coll_max_depth, recs.as<ContactRec>(),
                                                      acc.as<int>());
@@ -1378,8 +1406,8 @@ template <typename R> void detect_ccd(vbd_ctx* c)
     const CollArgs<R> a = coll_args<R>(c, c->xt, c->pos, 0.0);
     DBuf vcodes, vrecs, vacc, ecodes, erecs, eacc, vt_out, ee_out;
     const long long nv = broad_phase<R>(c, a, false, vcodes);
-    vrecs.alloc((size_t)std::max<long long>(nv, 1) * sizeof(ContactRec));
-    vacc.alloc((size_t)std::max<long long>(nv, 1) * 4);
+    vrecs.alloc_on((size_t)std::max<long long>(nv, 1) * sizeof(ContactRec), s);
+    vacc.alloc_on((size_t)std::max<long long>(nv, 1) * 4, s);
     if (nv) {
         k_ccd_vt<R><<<blocks_for(nv, 128), 128, 0, s>>>(a, vcodes.as<unsigned long long>(), nv, c->coll_kc, vrecs.as<ContactRec>(), vacc.as<int>());
         k_drop_known<<<blocks_for(nv), 256, 0, s>>>(vcodes.as<unsigned long long>(), nv, c->dcd_codes.as<unsigned long long>(), c->ndcd, vacc.as<int>());
@@ -1387,13 +1415,13 @@ template <typename R> void detect_ccd(vbd_ctx* c)
     CK(cudaGetLastError());
     const long long mv = compact_recs(c, vrecs, vcodes, vacc, nv, vt_out, nullptr);
     const long long ne = a.nedge ? broad_phase<R>(c, a, true, ecodes) : 0;
-    erecs.alloc((size_t)std::max<long long>(ne, 1) * sizeof(ContactRec));
-    eacc.alloc((size_t)std::max<long long>(ne, 1) * 4);
+    erecs.alloc_on((size_t)std::max<long long>(ne, 1) * sizeof(ContactRec), s);
+    eacc.alloc_on((size_t)std::max<long long>(ne, 1) * 4, s);
     if (ne) k_ccd_ee<R><<<blocks_for(ne, 128), 128, 0, s>>>(a, ecodes.as<unsigned long long>(), ne, c->coll_kc, erecs.as<ContactRec>(), eacc.as<int>());
     CK(cudaGetLastError());
     const long long me = compact_recs(c, erecs, ecodes, eacc, ne, ee_out, nullptr);
     c->nccd = mv + me;
-    c->ccd_recs.alloc((size_t)std::max<long long>(c->nccd, 1) * sizeof(ContactRec));
+    c->ccd_recs.alloc_on((size_t)std::max<long long>(c->nccd, 1) * sizeof(ContactRec), s);
     if (mv) CK(cudaMemcpyAsync(c->ccd_recs.p, vt_out.p, mv * sizeof(ContactRec), cudaMemcpyDeviceToDevice, s));
     if (me) CK(cudaMemcpyAsync(c->ccd_recs.as<ContactRec>() + mv, ee_out.p, me * sizeof(ContactRec), cudaMemcpyDeviceToDevice, s));
     CK(cudaStreamSynchronize(s));
@@ -1406,24 +1434,24 @@ template <typename R> void compile_contact_set(vbd_ctx* c, const DBuf& x)
     cudaStream_t s = c->stream;
     const long long n = c->ndcd + c->nccd;
     DBuf all;
-    all.alloc((size_t)std::max<long long>(n, 1) * sizeof(ContactRec));
+    all.alloc_on((size_t)std::max<long long>(n, 1) * sizeof(ContactRec), s);
     if (c->ndcd) CK(cudaMemcpyAsync(all.p, c->dcd_recs.p, c->ndcd * sizeof(ContactRec), cudaMemcpyDeviceToDevice, s));
     if (c->nccd) CK(cudaMemcpyAsync(all.as<ContactRec>() + c->ndcd, c->ccd_recs.p, c->nccd * sizeof(ContactRec), cudaMemcpyDeviceToDevice, s));
     c->ncontacts = n;
     if (n == 0) return;
     k_mark_flags<R><<<blocks_for(n), 256, 0, s>>>(all.as<ContactRec>(), (int)n, x.as<R4>(), c->ccoll.as<unsigned char>());
-    c->cidx.alloc((size_t)n * sizeof(int4));
-    c->creal.alloc((size_t)n * 4 * sizeof(R4));
+    c->cidx.alloc_on((size_t)n * sizeof(int4), s);
+    c->creal.alloc_on((size_t)n * 4 * sizeof(R4), s);
     DBuf inc, dummy;
-    inc.alloc((size_t)n * 4 * 8);
+    inc.alloc_on((size_t)n * 4 * 8, s);
     k_pack_contacts<R><<<blocks_for(n), 256, 0, s>>>(all.as<ContactRec>(), (int)n, c->cidx.as<int4>(), c->creal.as<R4>(),
                                                      inc.as<unsigned long long>());
     CK(cudaGetLastError());
     sort_keys_u64(inc, 4 * n, s);
     // incidence of solved vertices only (keys of fixed / ghost vertices sort last)
-    c->coff.alloc((size_t)(c->nsolve + 1) * 8);
-    c->ccid.alloc((size_t)4 * n * 4);
-    c->cslot.alloc((size_t)4 * n * 4);
+    c->coff.alloc_on((size_t)(c->nsolve + 1) * 8, s);
+    c->ccid.alloc_on((size_t)4 * n * 4, s);
+    c->cslot.alloc_on((size_t)4 * n * 4, s);
     k_contact_csr<<<blocks_for(4 * n), 256, 0, s>>>(inc.as<unsigned long long>(), 4 * n, c->nsolve, c->coff.as<long long>(),
                                                    c->ccid.as<int>(), c->cslot.as<int>());
     CK(cudaGetLastError());
@@ -1690,7 +1718,15 @@ void init_ctx(vbd_ctx* c, int device, int precision)
     if (prop.major < 10)
         fail(VBD_ERR_NODEVICE, std::string("device ") + prop.name + " is not sm_100 (Blackwell)");
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->owned.s = c->own_stream;
     c->stream = c->own_stream;
+    {  // keep up to 1 GB of freed pool memory cached (stream-ordered scratch allocations)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+            unsigned long long thr = 1ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
 }
 
 void finish_pack(vbd_ctx* c, Scene& sc)
