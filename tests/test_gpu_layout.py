@@ -183,3 +183,19 @@ def test_high_degree_vertex_all_layouts_bitwise(V, O, precision, monkeypatch):
     c = steps(make_ctx(V, O, s, precision, "compact", monkeypatch), s, 3, rho=0.5, n_max=6)
     assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["x"], c["x"])
     assert np.isfinite(a["x"]).all()
+
+
+@pytest.mark.parametrize("kg", ["0", "1"])
+def test_fp64_tiles_exact_grid_bitwise(V, O, kg, monkeypatch):
+    """An fp64 grid with exactly representable spacing has few kinds: the 2-lane tiles run with
+    the kind table in shared memory at 2 CTAs/SM (32-byte positions), or with VBD_TILE_KG=1
+    from global memory -- both bitwise equal to the explicit layout."""
+    m = O.generate_beam(11, 5, 5, 0.25)
+    s = O.build_system([(m, (1e6, 1e7, 1e-6))], np.flatnonzero(m.rest_positions[:, 0] < 1e-9))
+    monkeypatch.setenv("VBD_TILE_KG", kg)
+    ctx = make_ctx(V, O, s, "fp64", "auto", monkeypatch)
+    monkeypatch.delenv("VBD_TILE_KG")
+    assert ctx.info.tiles > 0 and ctx.info.num_entry_kinds < 100
+    a = steps(ctx, s, 4, rho=0.9)
+    b = steps(make_ctx(V, O, s, "fp64", "explicit", monkeypatch), s, 4, rho=0.9)
+    assert np.array_equal(a["x"], b["x"])
