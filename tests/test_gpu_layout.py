@@ -199,3 +199,27 @@ def test_fp64_tiles_exact_grid_bitwise(V, O, kg, monkeypatch):
     a = steps(ctx, s, 4, rho=0.9)
     b = steps(make_ctx(V, O, s, "fp64", "explicit", monkeypatch), s, 4, rho=0.9)
     assert np.array_equal(a["x"], b["x"])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_irregular_mesh_tiles_bitwise(V, O, precision, seed, monkeypatch):
+    """Jittered rest shapes with the default kind cap: thousands of kinds, so the tiles read
+    their records from global memory (KG) and every tile's bank placement (DSATUR) sees an
+    irregular conflict graph.  Tiles == explicit layout bitwise; both within the north-star
+    bar of the oracle."""
+    m = O.generate_beam(10, 5, 4, 0.05)
+    rng = np.random.default_rng(seed)
+    pos = m.rest_positions + rng.uniform(-0.01, 0.01, m.rest_positions.shape)
+    mj = O.build_tet_mesh(pos, m.tets, 1000.0)
+    s = O.build_system([(mj, (1e6, 1e7, 1e-6))], np.flatnonzero(pos[:, 0] < 0.01))
+    t = make_ctx(V, O, s, precision, "auto", monkeypatch)
+    assert t.info.tiles > 0 and t.info.num_entry_kinds > 1000
+    a = steps(t, s, 4, rho=0.9)
+    b = steps(make_ctx(V, O, s, precision, "explicit", monkeypatch), s, 4, rho=0.9)
+    assert np.array_equal(a["x"], b["x"])
+    st = O.make_state(s)
+    for _ in range(4):
+        O.step(s, st, H, 10, 0.9, G)
+    tol = 1e-10 if precision == "fp64" else 1e-5
+    assert np.abs(a["x"] - st.x).max() / mj.bbox_diagonal() <= tol
