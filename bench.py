@@ -490,8 +490,9 @@ def run_ours(args):
                          "layout_achieved": layout_achieved, "layout_frac": layout_achieved / peak,
                          "note": "frac > 1 is the lossless entry compression (DESIGN 2): the kernel "
                                  "moves layout_bytes, not the reference layout's bytes; layout_frac "
-                                 "is its HBM share; its limiter is the L1/shared-memory wavefront "
-                                 "pipe (limiter, profiles/r01_k1t_c5_analysis.md)",
+                                 "is its HBM share; no single pipe saturates (roofline.limiter: "
+                                 "latency-bound at the shared-memory-limited occupancy, "
+                                 "profiles/r01_k1t_c5_analysis.md)",
                          "limiter": ncu_limiter(cfg.name, args.precision, variant),
                          "traffic_unit": "DRAM bytes per k1 launch (ncu, profiles/k1_traffic.json)"},
             "cpu_baseline": cpu,
