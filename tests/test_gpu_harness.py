@@ -142,3 +142,19 @@ def test_run_simulation_fp32_within_tolerance(name, tmp_path):
     assert np.abs(pos - GOLD[f"{name}_last_x"]).max() <= 1e-5 * diag
     got = _metrics(tmp_path)
     np.testing.assert_allclose(got[:, 2], GOLD[f"{name}_metrics"][:, 2], rtol=1e-4)
+
+
+def test_chain_only_scene_obj_frames(tmp_path):
+    """A spring-net-only scene has no collision surface: frames carry vertices and no faces."""
+    doc = {"objects": [{"generator": {"kind": "chain", "count": 8, "spacing": 0.05, "stiffness": 500.0}}],
+           "gravity": [0.0, 0.0, -9.8],
+           "constraints": [{"kind": "fixed", "object": 0, "vertices": [0]}],
+           "solver": {"h": 0.01, "n_max": 5}, "frames": 3, "output": {"format": "obj", "every": 1}}
+    s = run_simulation(parse_scene(json.dumps(doc)), tmp_path)
+    assert s["frame_files"] == 4 and s["steps"] == 3
+    pos, fac = load_frame(tmp_path / "frame_00003.obj")
+    assert pos.shape == (8, 3) and fac.shape == (0, 3) and np.isfinite(pos).all()
+    assert np.array_equal(pos[0], [0.0, 0.0, 0.0])      # the fixed end stays put
+    assert pos[-1, 2] < 0.0                              # the free end falls under gravity
+    rows = _metrics(tmp_path)
+    assert rows.shape == (3 * 5, 6) and (rows[:, 4] == 0).all()
