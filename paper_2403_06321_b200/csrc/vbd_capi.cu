@@ -213,6 +213,7 @@ struct vbd_ctx {
     std::vector<int> tile_beg;  // first tile of colour c (size ncolors + 1)
     int ent_cap = 0, nbr_cap = 0;
     DBuf tv0, tnv, loff, tnbr, tent, tdesc;
+    DBuf vsv;  // per solved vertex: sum of V mu |w|^2 over its entries (one material per vertex)
     int tile_stages = 2, tile_w = 4, tile_occ = 2;
     bool tile_defer = true;  // K1T deferred block solves (VBD_TILE_DEFER=0 disables)
     bool tile_kg = false;    // K1T kind records read from global (table too large for shared memory)
@@ -838,6 +839,8 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
 }
 
 // material table for step size h
+template <typename R> K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter);
+
 template <typename R> void ensure_materials(vbd_ctx* c, double h)
 {
     if (c->mat_h == h && c->mat.p) return;
@@ -853,6 +856,12 @@ template <typename R> void ensure_materials(vbd_ctx* c, double h)
     CK(cudaMemcpy(c->mat.p, m.data(), m.size() * sizeof(Material<R>), cudaMemcpyHostToDevice));
     c->mat_h = h;
     refresh_kinds<R>(c);
+    if (c->uniform_mat && c->nsolve) {  // per-vertex sum of V mu |w|^2 (k_vertex_sv)
+        if (c->vsv.bytes < (size_t)c->nsolve * sizeof(R)) c->vsv.alloc((size_t)c->nsolve * sizeof(R));
+        K1Args<R> a = k1_args<R>(c, 1e-10, 0, false, 0);
+        k_vertex_sv<R><<<blocks_for(c->nsolve), 256, 0, c->stream>>>(a, (int)c->nsolve, c->vsv.as<R>());
+        CK(cudaGetLastError());
+    }
 }
 
 template <typename R>
@@ -896,6 +905,7 @@ K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
     a.iter = iter;
     a.pf_dist = 0;
     a.vmat = c->uniform_mat ? c->vmat.as<int>() : nullptr;
+    a.vsv = c->uniform_mat ? c->vsv.as<R>() : nullptr;
     a.line_search = 0;
     a.peer_pos[0] = a.peer_pos[1] = nullptr;
     a.peer_off[0] = a.peer_off[1] = 0;

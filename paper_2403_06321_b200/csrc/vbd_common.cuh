@@ -219,7 +219,7 @@ __device__ __forceinline__ void tet_contrib_ec(const R* __restrict__ e0, const R
         H[3] = fma(cw[1], cw[1], H[3]);
         H[4] = fma(cw[1], cw[2], H[4]);
         H[5] = fma(cw[2], cw[2], H[5]);
-        sv = sv + t[8];
+        (void)sv;  // V mu |w|^2 (t[8]) is summed once per vertex at pack time (k_vertex_sv)
     }
 }
 
@@ -369,11 +369,11 @@ struct AccXY {
     float f2;
     float2 h03;    // H0, H3
     float2 h24;    // H2, H4
-    float h1, h5, sv;
+    float h1, h5;
     __device__ __forceinline__ void zero()
     {
         f01 = h03 = h24 = make_float2(0.f, 0.f);
-        f2 = h1 = h5 = sv = 0.f;
+        f2 = h1 = h5 = 0.f;
     }
 };
 
@@ -405,5 +405,4 @@ __device__ __forceinline__ void tet_contrib_ec_xy(float4 p0, float4 p1, float4 p
     A.h24 = fma2(cw, bc2(cwz), A.h24);
     A.h1 = __fmaf_rn(cw.x, cw.y, A.h1);
     A.h5 = __fmaf_rn(cwz, cwz, A.h5);
-    A.sv = A.sv + t[8];
 }

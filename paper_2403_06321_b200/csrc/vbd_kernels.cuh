@@ -18,6 +18,7 @@ template <typename R> struct K1Args {
     const PL* ent;           // entry planes (explicit layout) or int4 entries (compact)
     long long E;             // plane stride (entries)
     const PL* kinds;         // compact layout: kind table (KindRec); nullptr = explicit
+    const R* vsv;            // one material per vertex: sum of V mu |w|^2 over its entries
     int max_deg;             // (host) max entries of one vertex: bulk-staging smem bound
     const long long* off;    // entry offsets of free vertices (nfree + 1)
     R4* pos;                 // current iterate x (in place)
@@ -447,9 +448,6 @@ __device__ __forceinline__ void k1_accumulate_explicit(const K1Args<R>& a, long 
             }
         }
     }
-    H[0] = H[0] + sv;
-    H[3] = H[3] + sv;
-    H[5] = H[5] + sv;
 }
 
 // compact layout: one 16-byte entry per (vertex, tet); the per-kind constants come from the
@@ -505,9 +503,6 @@ __device__ __forceinline__ void k1_accumulate_compact(const K1Args<R>& a, long l
             }
         }
     }
-    H[0] = H[0] + sv;
-    H[3] = H[3] + sv;
-    H[5] = H[5] + sv;
 }
 
 template <typename R, int W, int U, bool UM, bool LS = false, bool KC = false, bool SENT = false>
@@ -551,6 +546,12 @@ __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int la
         for (int q = 0; q < 3; ++q) f[q] += __shfl_xor_sync(gmask, f[q], o, W);
 #pragma unroll
         for (int q = 0; q < 6; ++q) H[q] += __shfl_xor_sync(gmask, H[q], o, W);
+    }
+    if (UM) {  // sum over the vertex's entries of V mu |w|^2, precomputed in entry order
+        const R s = a.vsv[v];
+        H[0] = H[0] + s;
+        H[3] = H[3] + s;
+        H[5] = H[5] + s;
     }
     if (!LS && lane != 0) return;
     vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM && end > beg, mv.dsc, mv.opd);
@@ -1121,4 +1122,35 @@ __global__ void k_halo_unpack(typename Vec4<R>::T* pos, const int* __restrict__ 
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) pos[ids[i]] = buf[i];
+}
+
+
+// Per-vertex sum over its entries (CSR order) of V mu |w|^2 -- the constant diagonal Hessian
+// term of every entry (ec_terms t[8]) -- for one material per vertex (UM).  Summed here once in
+// entry order and added after the lane reduction by every K1 variant, so all of them stay
+// bitwise equal; the sweep no longer loads or adds it per entry.
+template <typename R>
+__global__ void k_vertex_sv(const K1Args<R> a, int nsolve, R* __restrict__ out)
+{
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nsolve) return;
+    R s = R(0);
+    const long long beg = a.off[v], end = a.off[v + 1];
+    if (a.kinds) {
+        for (long long k = beg; k < end; ++k) {
+            const int kind = reinterpret_cast<const int4*>(a.ent)[k].w;
+            R r[KindRec<R>::HOT];
+            load_kind<R, KindRec<R>::QH>(a.kinds, kind, r);
+            s = s + r[8];
+        }
+    } else {
+        const Material<R> m = a.mat[a.vmat[v]];
+        for (long long k = beg; k < end; ++k) {
+            const Entry<R> e = Entry<R>::load(a.ent, a.E, k);
+            R t[9];
+            ec_terms<R>(e.w, e.V, m.mu, m.lam, m.gamma, t);
+            s = s + t[8];
+        }
+    }
+    out[v] = s;
 }

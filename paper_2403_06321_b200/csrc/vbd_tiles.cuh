@@ -685,6 +685,7 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
             for (int q = 0; q < 6; ++q) Ha[b][q] = R(0);
             sva[b] = R(0);
         }
+        const R svv = UM && act ? a.vsv[hv0 + lv] : R(0);  // added after the lane reduction
         R dsc = R(0), opd = R(1);
         constexpr int U = OCC >= 3 && W == 4 ? 1 : VBD_TILE_U;  // register budget
         static_assert(U % NA == 0, "rounds per iteration must cover the accumulator sets");
@@ -767,16 +768,9 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                 Ha[b][3] = acc[b].h03.y;
                 Ha[b][4] = acc[b].h24.y;
                 Ha[b][5] = acc[b].h5;
-                sva[b] = acc[b].sv;
             }
         }
         R f[3], H[6];
-#pragma unroll
-        for (int b = 0; b < NA; ++b) {
-            Ha[b][0] = Ha[b][0] + sva[b];
-            Ha[b][3] = Ha[b][3] + sva[b];
-            Ha[b][5] = Ha[b][5] + sva[b];
-        }
 #pragma unroll
         for (int q = 0; q < 3; ++q) f[q] = NA == 2 ? fa[0][q] + fa[NA - 1][q] : fa[0][q];
 #pragma unroll
@@ -797,6 +791,11 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                 dsc = __shfl_sync(0xffffffffu, dsc, vi);
                 opd = __shfl_sync(0xffffffffu, opd, vi);
             }
+            if (UM) {
+                H[0] = H[0] + svv;
+                H[3] = H[3] + svv;
+                H[5] = H[5] + svv;
+            }
             vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM, dsc, opd);
             if (j == tc) {
 #pragma unroll
@@ -812,6 +811,11 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
             }
         } else if (act && j == 0) {  // j = 0 processed the vertex's first entry (UM: dsc/opd)
             const int v = hv0 + lv;
+            if (UM) {
+                H[0] = H[0] + svv;
+                H[3] = H[3] + svv;
+                H[5] = H[5] + svv;
+            }
             vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM, dsc, opd);  // no entries: dsc = opd = 0, H = 0
             R d[3];
             block_solve<R>(f, H, a.eps_det, a.mode, d);
