@@ -725,10 +725,6 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                         r[4 * q + 3] = v.w;
                     }
                     tet_contrib_ec_xy(p[u][0], p[u][1], p[u][2], nxy, nz, r, acc[u % NA]);
-                    if (i0 + u == 0) {  // position j: lane j = 0 holds the vertex's first entry
-                        dsc = r[9];
-                        opd = r[10];
-                    }
                 }
             } else {
 #pragma unroll
@@ -749,11 +745,30 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                     const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
                     const int b = u % NA;  // i0 is a multiple of U, so (i0 + u) % NA == u % NA (unrolled)
                     tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], dx, fa[b], Ha[b], sva[b]);
-                    if (UM && i0 + u == 0) {  // position j: lane j = 0 holds the vertex's first entry
-                        dsc = r[9];
-                        opd = r[10];
-                    }
                 }
+            }
+        }
+        if (UM && rounds > 0) {  // the record of this lane's round-0 slot (position j; lane j = 0
+                                 // holds the vertex's first entry), read once, not per iteration
+            const uint2 e0s = lds_u2(sb32);
+            PL v;
+            if constexpr (KG) v = __ldg(ta.kinds + (size_t)(e0s.y >> 16) * Q + 2);
+            else lds_v(kb + (e0s.y >> 16) + 32u, v);
+            const R* vr = reinterpret_cast<const R*>(&v);
+            if constexpr (sizeof(R) == 4) {  // r[8..11] = chunk 2
+                dsc = vr[1];
+                opd = vr[2];
+            } else {  // double2 chunks: r[8..9] = chunk 4, r[10..11] = chunk 5
+                PL v5;
+                if constexpr (KG) {
+                    v = __ldg(ta.kinds + (size_t)(e0s.y >> 16) * Q + 4);
+                    v5 = __ldg(ta.kinds + (size_t)(e0s.y >> 16) * Q + 5);
+                } else {
+                    lds_v(kb + (e0s.y >> 16) + 64u, v);
+                    lds_v(kb + (e0s.y >> 16) + 80u, v5);
+                }
+                dsc = reinterpret_cast<const R*>(&v)[1];
+                opd = reinterpret_cast<const R*>(&v5)[0];
             }
         }
         if constexpr (PACK) {

@@ -193,8 +193,10 @@ def test_fp64_tiles_exact_grid_bitwise(V, O, kg, monkeypatch):
     m = O.generate_beam(11, 5, 5, 0.25)
     s = O.build_system([(m, (1e6, 1e7, 1e-6))], np.flatnonzero(m.rest_positions[:, 0] < 1e-9))
     monkeypatch.setenv("VBD_TILE_KG", kg)
+    monkeypatch.setenv("VBD_TILE_W", "2")  # global kinds are compiled for the 2-lane kernel
     ctx = make_ctx(V, O, s, "fp64", "auto", monkeypatch)
     monkeypatch.delenv("VBD_TILE_KG")
+    monkeypatch.delenv("VBD_TILE_W")
     assert ctx.info.tiles > 0 and ctx.info.num_entry_kinds < 100
     a = steps(ctx, s, 4, rho=0.9)
     b = steps(make_ctx(V, O, s, "fp64", "explicit", monkeypatch), s, 4, rho=0.9)
@@ -213,7 +215,9 @@ def test_irregular_mesh_tiles_bitwise(V, O, precision, seed, monkeypatch):
     pos = m.rest_positions + rng.uniform(-0.01, 0.01, m.rest_positions.shape)
     mj = O.build_tet_mesh(pos, m.tets, 1000.0)
     s = O.build_system([(mj, (1e6, 1e7, 1e-6))], np.flatnonzero(pos[:, 0] < 0.01))
+    monkeypatch.setenv("VBD_TILE_W", "2")  # global kinds are compiled for the 2-lane kernel
     t = make_ctx(V, O, s, precision, "auto", monkeypatch)
+    monkeypatch.delenv("VBD_TILE_W")
     assert t.info.tiles > 0 and t.info.num_entry_kinds > 1000
     a = steps(t, s, 4, rho=0.9)
     b = steps(make_ctx(V, O, s, precision, "explicit", monkeypatch), s, 4, rho=0.9)
