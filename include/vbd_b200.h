@@ -236,6 +236,18 @@ int vbd_energy(vbd_ctx* ctx, double h, double* G);
  * the iterate (max_penetration, solver.py:327-332; 0 without contacts).  Either may be NULL. */
 int vbd_energy_metrics(vbd_ctx* ctx, double h, double* G, int64_t* contacts, double* max_gap);
 
+/* ---- convergence traces ------------------------------------------------------------------- */
+/* baselines.descend (baselines.py:152-189) for the sweep methods, on the device, on the frozen
+ * objective of the current x and y (vbd_set_state; no detection updates): method 0 "vbd" (colour
+ * sweeps), 1 "vbd-cheb" (colour sweeps + Chebyshev blend at rho), 2 "jacobi" (block_jacobi_step,
+ * baselines.py:92-97: every vertex against the previous iterate) and 3 "gd" (gd_step, :100-104,
+ * mode 1); jacobi and gd take the global backtracking line search toward the last checkpoint every
+ * 8 iterations (:139-149, 180-183).  g[0..n_iters] = G per iteration (vbd_energy's value),
+ * wall_ms[0..n_iters] (may be NULL) = cumulative device time since after G_0 (CUDA events).
+ * x is left at the final iterate. */
+int vbd_descend(vbd_ctx* ctx, int32_t method, int32_t n_iters, double h, double rho, double eps_det,
+                int32_t line_search, double* g, double* wall_ms);
+
 /* ---- measurement ------------------------------------------------------------------------ */
 /* average device time of one colour-pass launch per colour over `reps` sweeps (CUDA events on
  * the context stream); ms has room for num_colors values */

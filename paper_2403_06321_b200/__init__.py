@@ -7,9 +7,9 @@ vertex sweep for Stable Neo-Hookean tets: hand-written sm_100a CUDA kernels in
 
 from .backend import NAME as BACKEND_NAME
 from .context import Beam, DeviceContext
-from .errors import DegenerateTet, IndexOutOfRange, NonFiniteState, SchemaError, VbdError
-from .harness import (METRICS_HEADER, ObjectConfig, OutputConfig, SceneConfig, export_frame,
-                      load_frame, parse_scene, run_simulation, scene_build, serialize_scene)
+from .errors import DegenerateTet, EmptyDescentRange, IndexOutOfRange, NonFiniteState, SchemaError, VbdError
+from .harness import (CONVERGENCE_HEADER, METRICS_HEADER, ObjectConfig, OutputConfig, SceneConfig, export_frame,
+                      load_frame, parse_scene, run_convergence, run_simulation, scene_build, serialize_scene)
 from .materials import MaterialParams
 from .mesh import (ColorPartition, SpringNet, TetMesh, VertexAdjacency, build_spring_net,
                    build_tet_mesh, generate_beam, generate_chain, generate_cube, greedy_color,
@@ -19,6 +19,8 @@ from .solver import (ContactParams, SimState, SolverParams, accelerate, chebyshe
                      make_state, max_penetration, metrics, step)
 from .system import (Body, ConstraintArrays, FixedConstraint, SubspaceConstraint, System,
                      WorldBoxConstraint, build_system, compile_constraints)
+
+from . import baselines  # noqa: E402
 
 __version__ = "0.1.0"
 

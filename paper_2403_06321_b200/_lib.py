@@ -109,6 +109,7 @@ SIGNATURES = {
     "vbd_energy": (ctypes.c_int, [P, f64, ctypes.POINTER(f64)]),
     "vbd_energy_metrics": (ctypes.c_int, [P, f64, ctypes.POINTER(f64), ctypes.POINTER(i64),
                                           ctypes.POINTER(f64)]),
+    "vbd_descend": (ctypes.c_int, [P, i32, i32, f64, f64, f64, i32, P, P]),
     "vbd_set_contacts": (ctypes.c_int, [P, i64, P, P, P, P, P, P, P, P, P, f64, f64]),
     "vbd_set_collision": (ctypes.c_int, [P, i64, P, i64, P, f64, f64, f64, f64, f64, i32, f64, i32]),
     "vbd_detect_contacts": (ctypes.c_int, [P, i32, i64, ctypes.POINTER(i64), P, P, P, P]),

@@ -187,6 +187,20 @@ class DeviceContext:
                                                  ctypes.byref(d)))
         return g.value, int(n.value), d.value
 
+    DESCEND_METHODS = {"vbd": 0, "vbd-cheb": 1, "jacobi": 2, "gd": 3}
+
+    def descend(self, method, n_iters, h, rho=0.0, eps_det=1e-10, line_search=False):
+        """baselines.descend (baselines.py:152-189) on the device from the resident x and y:
+        returns (G per iteration (n_iters+1,), cumulative device ms (n_iters+1,))."""
+        if method not in self.DESCEND_METHODS:
+            raise ValueError(f"unknown solver {method!r}")
+        g = np.zeros(int(n_iters) + 1)
+        w = np.zeros(int(n_iters) + 1)
+        _lib.check(_lib.lib().vbd_descend(self._h, self.DESCEND_METHODS[method], int(n_iters), float(h),
+                                          float(rho), float(eps_det), 1 if line_search else 0,
+                                          _lib.ptr(g), _lib.ptr(w)))
+        return g, w
+
     def close(self):
         if self._h and self._h.value:
             _lib.check(_lib.lib().vbd_ctx_destroy(self._h))

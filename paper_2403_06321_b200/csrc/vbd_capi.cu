@@ -2799,44 +2799,191 @@ int vbd_get_colliding(vbd_ctx* c, uint8_t* flags)
     });
 }
 
+}  // extern "C"
+
+// G(x) partial sums of the current iterate: b1 + b2 + b3 block partials to add (ascending) and
+// b3 contact-gap maxima after them.  Enqueued only; the caller reduces on the host.
+struct EnergyLayout {
+    unsigned b1, b2, b3;
+    unsigned sums() const { return b1 + b2 + b3; }
+    unsigned total() const { return b1 + b2 + 2 * b3; }
+};
+
+EnergyLayout energy_layout(const vbd_ctx* c)
+{
+    return {blocks_for(std::max<long long>(c->nsolve, 1) * 4), blocks_for(std::max<long long>(c->n, 1)),
+            c->ncontacts ? blocks_for(c->ncontacts) : 0u};
+}
+
+void enqueue_energy(vbd_ctx* c, double h, const EnergyLayout& L, double* part)
+{
+    cudaStream_t s = c->stream;
+    auto run = [&](auto tag) {
+        typedef decltype(tag) R;
+        if (std::isnan(c->mat_h)) ensure_materials<R>(c, 1.0);  // rest data only
+        K1Args<R> a = k1_args<R>(c, 1e-10, 0, false, 0);
+        k_energy_elastic<R, 4><<<L.b1, 256, 0, s>>>(a, (int)c->nsolve, part);
+        k_energy_vertex<R><<<L.b2, 256, 0, s>>>(a, c->mass.as<R>(), (int)c->n, 1.0 / (h * h), part + L.b1);
+        if (c->ncontacts)
+            k_energy_contact<R><<<L.b3, 256, 0, s>>>(c->cidx.as<int4>(), c->creal.as<typename Vec4<R>::T>(),
+                                                     (int)c->ncontacts, a.pos, part + L.b1 + L.b2,
+                                                     part + L.b1 + L.b2 + L.b3);
+    };
+    if (c->precision == VBD_PREC_F64) run(double{});
+    else run(float{});
+    CK(cudaGetLastError());
+}
+
+double reduce_energy(const EnergyLayout& L, const double* h, double* max_gap = nullptr)
+{
+    double acc = 0.0, mx = 0.0;
+    for (unsigned i = 0; i < L.sums(); ++i) acc += h[i];
+    for (unsigned i = L.sums(); i < L.total(); ++i) mx = std::max(mx, h[i]);
+    if (max_gap) *max_gap = mx;
+    return acc;
+}
+
+double energy_now(vbd_ctx* c, double h, double* max_gap = nullptr)
+{
+    const EnergyLayout L = energy_layout(c);
+    DBuf part;
+    part.alloc_on((size_t)L.total() * sizeof(double), c->stream);
+    enqueue_energy(c, h, L, part.as<double>());
+    std::vector<double> hp(L.total());
+    CK(cudaMemcpyAsync(hp.data(), part.p, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return reduce_energy(L, hp.data(), max_gap);
+}
+
+extern "C" {
+
 int vbd_energy_metrics(vbd_ctx* c, double h, double* G, int64_t* contacts, double* max_gap)
 {
     return guarded([&] {
         if (!c || !G) fail(VBD_ERR_ARG, "NULL argument");
         if (!(h > 0.0)) fail(VBD_ERR_ARG, "h must be positive");
-        cudaStream_t s = c->stream;
-        const unsigned b1 = blocks_for(std::max<long long>(c->nsolve, 1) * 4), b2 = blocks_for(std::max<long long>(c->n, 1));
-        const unsigned b3 = c->ncontacts ? blocks_for(c->ncontacts) : 0;
-        DBuf part;
-        part.alloc((size_t)(b1 + b2 + 2 * b3) * sizeof(double));
-        auto run = [&](auto tag) {
-            typedef decltype(tag) R;
-            if (std::isnan(c->mat_h)) ensure_materials<R>(c, 1.0);  // rest data only
-            K1Args<R> a = k1_args<R>(c, 1e-10, 0, false, 0);
-            k_energy_elastic<R, 4><<<b1, 256, 0, s>>>(a, (int)c->nsolve, part.as<double>());
-            k_energy_vertex<R><<<b2, 256, 0, s>>>(a, c->mass.as<R>(), (int)c->n, 1.0 / (h * h),
-                                                 part.as<double>() + b1);
-            if (c->ncontacts)
-                k_energy_contact<R><<<b3, 256, 0, s>>>(c->cidx.as<int4>(), c->creal.as<typename Vec4<R>::T>(),
-                                                       (int)c->ncontacts, a.pos, part.as<double>() + b1 + b2,
-                                                       part.as<double>() + b1 + b2 + b3);
-        };
-        if (c->precision == VBD_PREC_F64) run(double{});
-        else run(float{});
-        CK(cudaGetLastError());
-        std::vector<double> h(b1 + b2 + 2 * b3);
-        CK(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        double acc = 0.0, mx = 0.0;
-        for (unsigned i = 0; i < b1 + b2 + b3; ++i) acc += h[i];
-        for (unsigned i = b1 + b2 + b3; i < h.size(); ++i) mx = std::max(mx, h[i]);
-        *G = acc;
+        CK(cudaSetDevice(c->device));
+        double mx = 0.0;
+        *G = energy_now(c, h, &mx);
         if (contacts) *contacts = c->ncontacts;
         if (max_gap) *max_gap = mx;
     });
 }
 
 int vbd_energy(vbd_ctx* c, double h, double* G) { return vbd_energy_metrics(c, h, G, nullptr, nullptr); }
+
+}  // extern "C"
+
+// ---- baselines.descend on the device (baselines.py:152-189) ---------------------------------
+
+template <typename R>
+void descend_impl(vbd_ctx* c, int method, int n_iters, double h, double rho, double eps_det, int ls,
+                  double* g, double* wall_ms)
+{
+    typedef typename Vec4<R>::T R4;
+    cudaStream_t s = c->stream;
+    const size_t vb = (size_t)c->n * c->r4();
+    ensure_materials<R>(c, h);
+    k_fill_mih2<R><<<blocks_for(std::max<long long>(c->n, 1)), 256, 0, s>>>(c->y.as<R4>(), c->mass.as<R>(),
+                                                                          (int)c->n, h * h);
+    vbd_step_params p{};
+    p.h = h;
+    p.n_max = n_iters;
+    p.rho = method == 1 ? rho : 0.0;  // plain vbd never blends (omega_n == 1 for rho == 0)
+    p.eps_det = eps_det;
+    p.line_search = ls;
+    c->cur = p;
+    c->omegas = omega_table(p.rho, n_iters);
+    CK(cudaMemsetAsync(c->flag.p, 0xff, 8, s));
+    CK(cudaMemsetAsync(c->stepctr.p, 0, 4, s));
+    // x_prev1 = x, x_pp = None (baselines.py:165-166): K3's history at iteration 2 reads ha
+    if (p.rho != 0.0) CK(cudaMemcpyAsync(c->ha.p, c->pos.p, vb, cudaMemcpyDeviceToDevice, s));
+    const EnergyLayout L = energy_layout(c);
+    DBuf part, ckpt, xn;
+    part.alloc_on((size_t)(n_iters + 1) * L.total() * sizeof(double), s);
+    double* pp = part.as<double>();
+    const bool sweep = method <= 1;
+    double g_check = 0.0;
+    std::vector<double> hp(L.total());
+    auto sync_energy = [&](double* slot) {
+        CK(cudaMemcpyAsync(hp.data(), slot, L.total() * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return reduce_energy(L, hp.data());
+    };
+    enqueue_energy(c, h, L, pp);
+    if (!sweep) {
+        ckpt.alloc_on(vb, s);
+        xn.alloc_on(vb, s);
+        CK(cudaMemcpyAsync(ckpt.p, c->pos.p, vb, cudaMemcpyDeviceToDevice, s));
+        g_check = sync_energy(pp);
+    }
+    std::vector<cudaEvent_t> ev(n_iters + 1);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(ev[0], s));
+    for (int n = 1; n <= n_iters; ++n) {
+        if (sweep) {
+            for (int col = 0; col < c->ncolors; ++col) color_sweep<R>(c, col, n, false);
+            enqueue_iter_end<R>(c, n);
+        } else {
+            // block_jacobi_step / gd_step (baselines.py:92-104): every vertex against the previous
+            // iterate, mode 0 block solves or mode 1 preconditioned gradient steps
+            K1Args<R> a = k1_args<R>(c, eps_det, method == 3 ? 1 : 0, false, n);
+            a.line_search = ls;
+            a.vbeg = 0;
+            a.count = (int)c->nsolve;
+            a.out = c->out.as<R4>();
+            launch_k1<R>(c, a, s);
+            CK(cudaMemcpyAsync(c->pos.p, c->out.p, (size_t)c->nsolve * c->r4(), cudaMemcpyDeviceToDevice, s));
+            if (n % 8 == 0) {  // _LS_PERIOD (baselines.py:22, 180-183)
+                CK(cudaMemcpyAsync(xn.p, c->pos.p, vb, cudaMemcpyDeviceToDevice, s));
+                double alpha = 1.0;
+                bool ok = false;
+                for (int k = 0; k <= 16 && !ok; ++k) {  // _MAX_HALVINGS (baselines.py:23, 139-149)
+                    k_ls_blend<R><<<blocks_for(c->n), 256, 0, s>>>(c->pos.as<R4>(), ckpt.as<R4>(),
+                                                                 xn.as<R4>(), alpha, (int)c->n);
+                    enqueue_energy(c, h, L, pp + (size_t)n * L.total());
+                    ok = sync_energy(pp + (size_t)n * L.total()) <= g_check;
+                    alpha *= 0.5;
+                }
+                if (!ok) CK(cudaMemcpyAsync(c->pos.p, ckpt.p, vb, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(ckpt.p, c->pos.p, vb, cudaMemcpyDeviceToDevice, s));
+                enqueue_energy(c, h, L, pp + (size_t)n * L.total());
+                g_check = sync_energy(pp + (size_t)n * L.total());
+            }
+        }
+        enqueue_energy(c, h, L, pp + (size_t)n * L.total());
+        CK(cudaEventRecord(ev[n], s));
+    }
+    CK(cudaGetLastError());
+    std::vector<double> all((size_t)(n_iters + 1) * L.total());
+    CK(cudaMemcpyAsync(all.data(), pp, all.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int n = 0; n <= n_iters; ++n) {
+        g[n] = reduce_energy(L, all.data() + (size_t)n * L.total());
+        float ms = 0.f;
+        if (n) CK(cudaEventElapsedTime(&ms, ev[0], ev[n]));
+        if (wall_ms) wall_ms[n] = ms;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+}
+
+extern "C" {
+
+int vbd_descend(vbd_ctx* c, int32_t method, int32_t n_iters, double h, double rho, double eps_det,
+                int32_t line_search, double* g, double* wall_ms)
+{
+    return guarded([&] {
+        if (!c || !g) fail(VBD_ERR_ARG, "NULL argument");
+        if (c->in_step) fail(VBD_ERR_ARG, "a fine-grained step is in progress");
+        if (method < 0 || method > 3) fail(VBD_ERR_ARG, "method must be 0 vbd, 1 vbd-cheb, 2 jacobi or 3 gd");
+        if (n_iters < 0) fail(VBD_ERR_ARG, "n_iters must be >= 0");
+        if (!(h > 0.0)) fail(VBD_ERR_ARG, "h must be positive");
+        if (!(rho >= 0.0 && rho < 1.0)) fail(VBD_ERR_ARG, "rho must be in [0, 1)");
+        CK(cudaSetDevice(c->device));
+        if (c->precision == VBD_PREC_F64) descend_impl<double>(c, method, n_iters, h, rho, eps_det, line_search, g, wall_ms);
+        else descend_impl<float>(c, method, n_iters, h, rho, eps_det, line_search, g, wall_ms);
+    });
+}
 
 int vbd_profile_color_pass(vbd_ctx* c, double h, int32_t reps, double* ms)
 {

@@ -1064,6 +1064,32 @@ __global__ void k_fill_mih2(typename Vec4<R>::T* y, const R* mass, int n, double
     if (i < n) y[i].w = mass[i] / (R)hh;
 }
 
+// Global backtracking trial of baselines._global_line_search (baselines.py:139-149):
+// x = checkpoint + alpha * (x_new - checkpoint), each operation rounded on its own as NumPy
+// evaluates it (no contraction into an FMA).
+__device__ __forceinline__ double ls_axpy(double c, double xn, double alpha)
+{
+    return __dadd_rn(c, __dmul_rn(alpha, __dsub_rn(xn, c)));
+}
+__device__ __forceinline__ float ls_axpy(float c, float xn, double alpha)
+{
+    return __fadd_rn(c, __fmul_rn((float)alpha, __fsub_rn(xn, c)));
+}
+
+template <typename R>
+__global__ void k_ls_blend(typename Vec4<R>::T* pos, const typename Vec4<R>::T* ckpt,
+                           const typename Vec4<R>::T* xn, double alpha, int n)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    typename Vec4<R>::T x = xn[i];
+    const typename Vec4<R>::T c = ckpt[i];
+    x.x = ls_axpy(c.x, x.x, alpha);
+    x.y = ls_axpy(c.y, x.y, alpha);
+    x.z = ls_axpy(c.z, x.z, alpha);
+    pos[i] = x;
+}
+
 // halo exchange for slab-decomposed scenes: gather/scatter the positions of a vertex list
 // Neighbour phase barrier over peer memory (slab P2P halo).  flags[0] of a context is
 // written by its left neighbour, flags[1] by its right one; values are monotonically

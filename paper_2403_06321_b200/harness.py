@@ -585,3 +585,64 @@ def run_simulation(config: SceneConfig, out_dir, threads=None, frames=None, metr
     return {"frames": n_frames, "steps": state.step_index, "frame_files": written,
             "backend": _BACKEND, "metrics": str(csv_path),
             "wall_s": round(time.perf_counter() - t_start, 3)}
+
+
+CONVERGENCE_HEADER = "solver,iteration,G,relative_loss,wall_ms"
+
+
+def run_convergence(config: SceneConfig, solvers, n_iters: int, out_csv=None, threads=None,
+                    g_star=None):
+    """Convergence study on the frozen first-step objective (harness.py:702-743) on the GPU.
+
+    Builds the scene, runs DCD at x_t and the warm start once (device), then records a G trace
+    per requested solver from the same start (``baselines.descend``: one device call per
+    solver).  The reference's G* comes from Newton (harness.py:721-722), which is not provided:
+    pass ``g_star``, else the lowest G of the recorded traces stands in for it
+    (``g_star_method`` "min-trace"; VBD's fixed point is not G's minimiser, since damping is a
+    force-level term, so a long VBD run is no substitute for Newton).  Writes
+    solver,iteration,G,relative_loss,wall_ms rows when out_csv is given."""
+    from . import baselines
+    from .solver import _collision, _INPUTS, device_context, initialize
+    names = list(solvers)
+    if "newton" in names:
+        raise NotImplementedError("newton is not provided by the b200 backend")
+    bad = [n for n in names if n not in baselines.METHODS]
+    if bad:
+        raise ValueError(f"unknown solver {bad[0]!r}")
+    system, state, params = scene_build(config)
+    if threads is not None:
+        params = replace(params, threads=threads)
+    ctx = device_context(system, params.precision, params.device)
+    _collision(ctx, system, params)
+    state._bind(ctx)
+    state._upload(_INPUTS)
+    mesh = getattr(system, "collision_mesh", None)
+    if params.contact is not None and mesh is not None and len(mesh.surface_tris):
+        ctx.detect_contacts(0, cap=1)  # DCD at x_t -> the active contact set (harness.py:718)
+    initialize(state, params)
+    x0, y0 = state.x.copy(), state.y.copy()
+    traces, losses = {}, {}
+    for name in names:
+        state.x, state.y = x0.copy(), y0.copy()
+        p = params
+        if name == "vbd-cheb" and p.rho == 0.0:
+            p = replace(p, rho=0.95)
+        traces[name] = baselines.descend(state, p, name, n_iters)
+    method = "given"
+    if g_star is None:
+        g_star = min(float(np.nanmin(t.g)) for t in traces.values()) if traces else 0.0
+        method = "min-trace"
+    for name in names:
+        try:
+            losses[name] = baselines.relative_loss(traces[name].g, g_star)
+        except Exception:
+            losses[name] = np.zeros_like(traces[name].g)
+
+    if out_csv is not None:
+        with open(out_csv, "w") as fh:
+            fh.write(CONVERGENCE_HEADER + "\n")
+            for name in names:
+                tr = traces[name]
+                for k in range(len(tr.g)):
+                    fh.write(f"{name},{k},{_g(tr.g[k])},{_g(losses[name][k])},{tr.wall_ms[k]:.3f}\n")
+    return {"g_star": g_star, "g_star_method": method, "traces": traces, "relative_loss": losses}

@@ -548,10 +548,44 @@ def harness_fixture():
     save("harness.npz", **out)
 
 
+def convergence_fixture():
+    """Reference run_convergence (harness.py:702-743: the Newton optimum G* and a G trace per
+    solver through baselines.descend, baselines.py:152-189) on the harness scenes, with the
+    frozen start (x, y after DCD and the warm start) and each solver's final iterate."""
+    from dataclasses import replace
+    from vbdsim import baselines as B
+    from vbdsim import harness as H
+    from vbdsim.solver import _detect_dcd
+    out = {}
+    iters = 24  # three global line searches for jacobi / gd
+    for name, text in harness_scenes().items():
+        cfg = H.parse_scene(text)
+        res = H.run_convergence(cfg, ["vbd", "vbd-cheb", "jacobi", "gd", "newton"], iters)
+        out[f"{name}_g_star"] = np.float64(res["g_star"])
+        system, state, params = H.scene_build(cfg)
+        state.y = inertia_target(state.x_t, state.v_t, params.a_ext_vec, params.h)
+        _detect_dcd(state, params)
+        initialize(state, params)
+        out[f"{name}_x0"], out[f"{name}_y0"] = state.x.copy(), state.y.copy()
+        for m in ("vbd", "vbd-cheb", "jacobi", "gd"):
+            tr = res["traces"][m]
+            out[f"{name}_{m}_g"] = tr.g
+            out[f"{name}_{m}_x"] = tr.x_final
+            out[f"{name}_{m}_loss"] = res["relative_loss"][m]
+            # the same trace again from the stored start (the trace is deterministic)
+            st = H._clone_state(state)
+            p = replace(params, rho=0.95) if m == "vbd-cheb" and params.rho == 0.0 else params
+            assert np.array_equal(B.descend(st, p, m, iters).g, tr.g), (name, m)
+    out["iters"] = np.int64(iters)
+    save("convergence.npz", **out)
+
+
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"mesh", "coloring", "pass", "steps", "extras", "energy", "contact", "harness"}
+    which = set(sys.argv[1:]) or {"mesh", "coloring", "pass", "steps", "extras", "energy", "contact", "harness",
+                                 "convergence"}
     for name, fn in (("mesh", mesh_fixture), ("coloring", coloring_fixtures), ("pass", pass_fixture),
                      ("steps", step_fixtures), ("extras", extras_fixture), ("energy", energy_fixture),
-                     ("contact", contact_fixture), ("harness", harness_fixture)):
+                     ("contact", contact_fixture), ("harness", harness_fixture),
+                     ("convergence", convergence_fixture)):
         if name in which:
             fn()

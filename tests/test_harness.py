@@ -113,11 +113,36 @@ def test_cli_bad_scene_exits_2(tmp_path):
     assert res.exit_code == 2 and "material" in res.output
 
 
-def test_cli_converge_is_out_of_scope(tmp_path):
+def test_cli_converge_rejects_newton_and_unknown_solvers(tmp_path):
+    """cli.py:68-77: unknown solver names exit 2; newton is not provided here (exit 2 too)."""
     p = tmp_path / "s.json"
     p.write_text(str(GOLD["base_scene"]))
-    res = _cli(["converge", "--scene", str(p), "--out", str(tmp_path / "c.csv")])
-    assert res.exit_code == 2 and "out of scope" in res.output
+    res = _cli(["converge", "--scene", str(p), "--out", str(tmp_path / "c.csv"), "--solvers", "vbd,cg"])
+    assert res.exit_code == 2 and "unknown solvers" in res.output
+    res = _cli(["converge", "--scene", str(p), "--out", str(tmp_path / "c.csv"), "--solvers", "newton"])
+    assert res.exit_code == 2 and "newton" in res.output
+    p.write_text("{broken")
+    assert _cli(["converge", "--scene", str(p), "--out", str(tmp_path / "c.csv")]).exit_code == 2
+
+
+def test_convergence_header_and_relative_loss():
+    """harness.py:36 and baselines.py:107-115 (EmptyDescentRange without a descent range)."""
+    from paper_2403_06321_b200 import CONVERGENCE_HEADER, EmptyDescentRange
+    from paper_2403_06321_b200.baselines import relative_loss
+    assert CONVERGENCE_HEADER == "solver,iteration,G,relative_loss,wall_ms"
+    np.testing.assert_array_equal(relative_loss([3.0, 2.0, 1.0], 1.0), [1.0, 0.5, 0.0])
+    with pytest.raises(EmptyDescentRange):
+        relative_loss([1.0, 0.5], 1.0)
+
+
+def test_convergence_fixture_self_consistent():
+    """The reference's relative_loss column is (G - G*)/(G_0 - G*) of its own traces."""
+    conv = np.load(Path(__file__).parent / "golden" / "convergence.npz")
+    from paper_2403_06321_b200.baselines import relative_loss
+    for name in SCENES:
+        for m in ("vbd", "vbd-cheb", "jacobi", "gd"):
+            np.testing.assert_array_equal(relative_loss(conv[f"{name}_{m}_g"], float(conv[f"{name}_g_star"])),
+                                          conv[f"{name}_{m}_loss"])
 
 
 def test_cli_color_missing_mesh_exits_2(tmp_path):
