@@ -249,8 +249,8 @@ int vbd_descend(vbd_ctx* ctx, int32_t method, int32_t n_iters, double h, double 
                 int32_t line_search, double* g, double* wall_ms);
 
 /* ---- measurement ------------------------------------------------------------------------ */
-/* average device time of one colour-pass launch per colour over `reps` sweeps (CUDA events on
- * the context stream); ms has room for num_colors values */
+/* average device time of one colour-pass launch per colour over `reps` sweeps, colours in step
+ * order (one CUDA event pair per launch on the context stream); ms has room for num_colors values */
 int vbd_profile_color_pass(vbd_ctx* ctx, double h, int32_t reps, double* ms);
 
 const char* vbd_last_error(void);

@@ -2991,29 +2991,38 @@ int vbd_profile_color_pass(vbd_ctx* c, double h, int32_t reps, double* ms)
         if (!c || !ms || reps < 1) fail(VBD_ERR_ARG, "bad argument");
         CK(cudaSetDevice(c->device));
         cudaStream_t s = c->stream;
-        cudaEvent_t e0, e1;
-        CK(cudaEventCreate(&e0));
-        CK(cudaEventCreate(&e1));
         c->cur.eps_det = c->cur.eps_det > 0 ? c->cur.eps_det : 1e-10;
-        for (int col = 0; col < c->ncolors; ++col) {
-            if (c->precision == VBD_PREC_F64) ensure_materials<double>(c, h);
-            else ensure_materials<float>(c, h);
-            // warm-up launch
+        if (c->precision == VBD_PREC_F64) ensure_materials<double>(c, h);
+        else ensure_materials<float>(c, h);
+        auto sweep = [&](int col) {
             if (c->precision == VBD_PREC_F64) color_sweep<double>(c, col, 1, false);
             else color_sweep<float>(c, col, 1, false);
-            CK(cudaEventRecord(e0, s));
-            for (int r = 0; r < reps; ++r) {
-                if (c->precision == VBD_PREC_F64) color_sweep<double>(c, col, 1, false);
-                else color_sweep<float>(c, col, 1, false);
+        };
+        // colours in step order (each launch reads what the previous colours wrote, as in
+        // the step); one event pair per launch
+        const int nc = c->ncolors;
+        std::vector<cudaEvent_t> ev(2 * (size_t)nc * reps);
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        for (int col = 0; col < nc; ++col) sweep(col);  // warm-up sweep
+        for (int r = 0; r < reps; ++r)
+            for (int col = 0; col < nc; ++col) {
+                const size_t k = 2 * ((size_t)r * nc + col);
+                CK(cudaEventRecord(ev[k], s));
+                sweep(col);
+                CK(cudaEventRecord(ev[k + 1], s));
             }
-            CK(cudaEventRecord(e1, s));
-            CK(cudaEventSynchronize(e1));
-            float t = 0;
-            CK(cudaEventElapsedTime(&t, e0, e1));
-            ms[col] = (double)t / reps;
+        CK(cudaStreamSynchronize(s));
+        for (int col = 0; col < nc; ++col) {
+            double acc = 0.0;
+            for (int r = 0; r < reps; ++r) {
+                const size_t k = 2 * ((size_t)r * nc + col);
+                float t = 0;
+                CK(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
+                acc += t;
+            }
+            ms[col] = acc / reps;
         }
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+        for (auto& e : ev) cudaEventDestroy(e);
     });
 }
 
