@@ -128,6 +128,14 @@ template <typename T> void upload(DBuf& b, const T* host, size_t n, cudaStream_t
     if (n) CK(cudaMemcpyAsync(b.p, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
 }
 
+// the same into a stream-ordered pooled buffer (per-step scratch: no cudaMalloc / cudaFree,
+// whose free synchronises the whole device)
+template <typename T> void upload_on(DBuf& b, const T* host, size_t n, cudaStream_t s)
+{
+    b.alloc_on(n * sizeof(T), s);
+    if (n) CK(cudaMemcpyAsync(b.p, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
 struct MaterialKey {
     double mu, lam, kd, density;
     bool operator<(const MaterialKey& o) const
@@ -913,6 +921,31 @@ K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
     return a;
 }
 
+// Launch with programmatic stream serialisation (PDL) for the kernels that begin with
+// pdl_wait(): the next colour pass / blend is scheduled while the previous one drains, which
+// hides most of the per-node launch latency of small scenes' step graphs.  VBD_PDL=0 disables.
+bool pdl_enabled()
+{
+    static const bool on = !getenv("VBD_PDL") || atoi(getenv("VBD_PDL")) != 0;
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, Args&&... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
+
 template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, bool pf, cudaStream_t s)
 {
     long long threads = (long long)a0.count * W;
@@ -969,7 +1002,7 @@ void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
         per_sm[dev] = std::max(1, per_sm[dev]);
     }
     const int grid = std::min(ta.tcount, per_sm[dev] * sms[dev]);
-    k1_tiles<R, UM, S, W, OCC, DEF, KG><<<grid, 64 * W + 32, smem, s>>>(ta);
+    launch_pdl(k1_tiles<R, UM, S, W, OCC, DEF, KG>, (unsigned)grid, 64 * W + 32, smem, s, ta);
 }
 
 template <typename R, bool UM, int W>
@@ -1127,9 +1160,9 @@ template <typename R> void enqueue_iter_end(vbd_ctx* c, int n)
     R4* hist = (n % 2 == 1) ? c->hb.as<R4>() : c->ha.as<R4>();
     double w = c->omegas[n];
     int blend = (n >= 2 && w != 1.0) ? 1 : 0;
-    k3_chebyshev<R><<<blocks_for(c->n), 256, 0, c->stream>>>(
-        c->pos.as<R4>(), hist, (int)c->n, w, blend, c->flag.as<unsigned long long>(),
-        c->perm.as<int>(), c->stepctr.as<int>(), n, c->coll_on ? c->ccoll.as<unsigned char>() : nullptr);
+    launch_pdl(k3_chebyshev<R>, blocks_for(c->n), 256, 0, c->stream, c->pos.as<R4>(), hist, (int)c->n, w,
+               blend, c->flag.as<unsigned long long>(), c->perm.as<int>(), c->stepctr.as<int>(), n,
+               c->coll_on ? (const unsigned char*)c->ccoll.as<unsigned char>() : nullptr);
 }
 
 template <typename R> void enqueue_end(vbd_ctx* c)
@@ -2249,8 +2282,8 @@ int vbd_set_fixed_targets(vbd_ctx* c, int64_t n, const int64_t* idx, const doubl
             if (ids[k] < c->nfree_all) fail(VBD_ERR_ARG, "kinematic targets apply to fixed vertices only");
         }
         DBuf did, dxyz;
-        upload(did, ids.data(), n, c->stream);
-        upload(dxyz, xyz, 3 * n, c->stream);
+        upload_on(did, ids.data(), n, c->stream);
+        upload_on(dxyz, xyz, 3 * n, c->stream);
         if (c->precision == VBD_PREC_F64)
             k_set_targets<double><<<blocks_for(n), 256, 0, c->stream>>>(did.as<int>(), dxyz.as<double>(), (int)n,
                                                                        c->xt.as<double4>(), c->pos.as<double4>());

@@ -329,6 +329,14 @@ template <typename R> __device__ __forceinline__ bool finite3(R a, R b, R c)
 }
 
 // ---------------------------------------------------------------------------------------
+// Programmatic dependent launch (sm_90+): a kernel launched with the programmatic-stream-
+// serialization attribute may start while its predecessor drains; griddepcontrol.wait blocks
+// until the predecessor grid has completed and its writes are visible, so everything before it
+// must read constant data only.  Both are no-ops for a plain launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------------------
 // shared-memory address / mbarrier helpers (bulk-copy staging)
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }

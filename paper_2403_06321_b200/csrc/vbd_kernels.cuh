@@ -926,6 +926,8 @@ __global__ void k3_chebyshev(typename Vec4<R>::T* pos, typename Vec4<R>::T* hist
                              const int* perm, const int* stepctr, int iter,
                              const unsigned char* coll = nullptr)
 {
+    pdl_wait();
+    pdl_launch_dependents();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) k3_vertex<R>(pos, hist, omega, blend, flag, perm, stepctr, iter, i, coll);
 }

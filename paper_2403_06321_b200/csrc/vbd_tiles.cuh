@@ -557,6 +557,9 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // the kind table and the barriers above are step constants; positions are not
+    pdl_wait();
+    pdl_launch_dependents();
 
     if (warp == NCW) {  // ---------------- producer
         // Software-pipelined, unrolled by two with named buffers (no register copies that would
