@@ -969,20 +969,20 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
             CK(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
             attr[dev][um] = true;
         }
-        kb<<<nb, 256, smem, s>>>(a);
+        launch_pdl(kb, nb, 256, smem, s, a);
         return;
     }
     if (a.kinds) {
-        if (pf && um) k1_color_pass<R, W, U, B, true, true, true><<<nb, 256, 0, s>>>(a);
-        else if (pf) k1_color_pass<R, W, U, B, true, false, true><<<nb, 256, 0, s>>>(a);
-        else if (um) k1_color_pass<R, W, U, B, false, true, true><<<nb, 256, 0, s>>>(a);
-        else k1_color_pass<R, W, U, B, false, false, true><<<nb, 256, 0, s>>>(a);
+        if (pf && um) launch_pdl(k1_color_pass<R, W, U, B, true, true, true>, nb, 256, 0, s, a);
+        else if (pf) launch_pdl(k1_color_pass<R, W, U, B, true, false, true>, nb, 256, 0, s, a);
+        else if (um) launch_pdl(k1_color_pass<R, W, U, B, false, true, true>, nb, 256, 0, s, a);
+        else launch_pdl(k1_color_pass<R, W, U, B, false, false, true>, nb, 256, 0, s, a);
         return;
     }
-    if (pf && um) k1_color_pass<R, W, U, B, true, true><<<nb, 256, 0, s>>>(a);
-    else if (pf) k1_color_pass<R, W, U, B, true, false><<<nb, 256, 0, s>>>(a);
-    else if (um) k1_color_pass<R, W, U, B, false, true><<<nb, 256, 0, s>>>(a);
-    else k1_color_pass<R, W, U, B, false, false><<<nb, 256, 0, s>>>(a);
+    if (pf && um) launch_pdl(k1_color_pass<R, W, U, B, true, true>, nb, 256, 0, s, a);
+    else if (pf) launch_pdl(k1_color_pass<R, W, U, B, true, false>, nb, 256, 0, s, a);
+    else if (um) launch_pdl(k1_color_pass<R, W, U, B, false, true>, nb, 256, 0, s, a);
+    else launch_pdl(k1_color_pass<R, W, U, B, false, false>, nb, 256, 0, s, a);
 }
 
 template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false>

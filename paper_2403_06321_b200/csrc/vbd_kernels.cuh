@@ -659,6 +659,8 @@ __global__ void __launch_bounds__(256, MINB) k1_color_pass(const K1Args<R> a)
                 }
         }
     }
+    pdl_wait();  // entries are step constants (prefetched above); positions are not
+    pdl_launch_dependents();
     if (g < a.count) k1_vertex_impl<R, W, U, UM, false, KC>(a, g, lane);
 }
 
@@ -694,6 +696,8 @@ __global__ void __launch_bounds__(256, MINB) k1_color_pass_bulk(const K1Args<R> 
                 : "memory");
     }
     __syncthreads();  // barrier initialised before anyone waits on it
+    pdl_wait();       // the entry copy above reads step constants only
+    pdl_launch_dependents();
     const int g = (int)(g0 + threadIdx.x / W);
     const int lane = threadIdx.x & (W - 1);
     if (g < a.count) k1_vertex_impl<R, W, U, UM, false, true, true>(a, g, lane, sent, e0, bar);

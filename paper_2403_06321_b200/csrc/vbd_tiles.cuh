@@ -557,7 +557,10 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // the kind table and the barriers above are step constants; positions are not
+    // programmatic dependent launch: everything above reads step constants only (the kind
+    // table is rewritten only by refresh_kinds, which synchronises the stream before any
+    // colour pass is enqueued); positions are read after the predecessor grid has finished.
+    // Overlapping this prologue with the previous pass is worth ~10 % on C1 / C2.
     pdl_wait();
     pdl_launch_dependents();
 

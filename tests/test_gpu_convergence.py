@@ -115,3 +115,26 @@ def test_cli_converge_writes_traces(tmp_path):
         g = np.array([float(r[2]) for r in rows if r[0] == m])
         np.testing.assert_allclose(g, CONV[f"base_{m}_g"], rtol=G_RTOL, atol=0)
         assert summary["final_G"][m] == pytest.approx(float(g[-1]), rel=1e-15)
+
+
+def test_descend_zero_iterations_and_fp32():
+    """n_iters = 0 records G_0 only and leaves x alone; an fp32 context follows the fp64
+    reference trace to fp32 accuracy."""
+    from dataclasses import replace
+    system, state, params = scene_build(_cfg("base"))
+    x0, y0 = CONV["base_x0"], CONV["base_y0"]
+    state.x, state.y = x0.copy(), y0.copy()
+    tr = baselines.descend(state, params, "vbd", 0)
+    assert tr.g.shape == (1,) and tr.wall_ms.tolist() == [0.0]
+    np.testing.assert_allclose(tr.g[0], CONV["base_vbd_g"][0], rtol=G_RTOL)
+    assert np.array_equal(tr.x_final, x0)
+    # fp32 build: the colour-sweep traces end within the north-star fp32 bar of the reference's
+    # fp64 iterate (jacobi / gd accept-or-reject line searches on fp32 G are not compared)
+    p32 = replace(params, precision="fp32")
+    diag = _diag(x0)
+    for m in ("vbd", "vbd-cheb"):
+        state.x, state.y = x0.copy(), y0.copy()
+        p = replace(p32, rho=0.95) if m == "vbd-cheb" and p32.rho == 0.0 else p32
+        tr = baselines.descend(state, p, m, ITERS)
+        err = np.abs(tr.x_final - CONV[f"base_{m}_x"]).max() / diag
+        assert err <= 1e-5, (m, err)
