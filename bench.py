@@ -48,6 +48,11 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
                     help="slab halo transport for N>1: fused peer-memory push or NCCL send/recv")
+    ap.add_argument("--checksum", action="store_true",
+                    help="add the sha256 of the owned positions after warm-up + timed steps "
+                         "(rank order = vertex order) -- for the 1-rank vs N-rank bitwise test")
+    ap.add_argument("--no-fp64-record", action="store_true",
+                    help="skip the fp64 sub-record (the reference's precision) of the fp32 run")
     return ap.parse_args()
 
 
@@ -68,19 +73,32 @@ def _stock_reference():
     return vbdsim if vbdsim.backend_name() == "native" else None
 
 
-def _sample_meshes(cfg_name, cfg):
+def _sample_meshes(cfg_name, cfg, shrink=1.0):
     b = cfg.beams[0]
     if cfg_name == "c4":
-        return [(b.nx, b.ny, b.nz, b.spacing)] * 8, "8 of the 10,368 generate_cube(15,0.3) objects"
+        k = max(1, int(round(8 * shrink)))
+        return [(b.nx, b.ny, b.nz, b.spacing)] * k, f"{k} of the 10,368 generate_cube(15,0.3) objects"
     if cfg_name == "c5":
-        n = 31
+        n = max(8, int(round(31 * shrink ** (1 / 3))))
         return [(n, n, n, b.spacing)], f"generate_beam({n},{n},{n},0.01) block (same material/h/n_max/BCs)"
     if cfg_name == "c3":
-        return [(300, 4, 4, b.spacing)], "generate_beam(300,4,4,0.01) (1/10 of one C3 beam)"
+        n = max(8, int(round(300 * shrink)))
+        return [(n, 4, 4, b.spacing)], f"generate_beam({n},4,4,0.01) (part of one C3 beam)"
     return [(bb.nx, bb.ny, bb.nz, bb.spacing) for bb in cfg.beams], "full scene"
 
 
-def cpu_reference_sample(cfg_name, budget_s=15.0):
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_reference_sample(cfg_name, budget_s=15.0, steps=None, warmup=1):
     """Time the reference on a bounded sample of the workload, on this box's host cores.
 
     Preferred: the UNMODIFIED reference package from baseline/_ref through its own public
@@ -89,17 +107,24 @@ def cpu_reference_sample(cfg_name, budget_s=15.0):
     else the oracle's C port.  The sample is a scaled-down scene of the same kind (same
     generator, material, h, n_max, rho, constraints); vertex-iterations/s is
     size-independent to first order.  The as-shipped kernel takes the GIL per tet inside its
-    OpenMP loop, so 1 thread and all host threads are probed and the faster
-    setting is reported with its core count.
+    OpenMP loop, so 1 thread and all host threads are both timed (one step
+    each) and the faster setting is used for the timed steps; both rates are reported.
+
+    steps=None: as many steps as fit in budget_s (>= 3); else exactly `steps` timed steps
+    after `warmup` untimed ones, on a sample shrunk so that they take about budget_s.
     """
     from paper_2403_06321_b200.scenes import config
     cfg = config(cfg_name)
     b = cfg.beams[0]
-    dims, sample = _sample_meshes(cfg_name, cfg)
+    shrink = 1.0
+    if steps is not None and cfg_name in ("c3", "c4", "c5"):
+        # the 31^3 C5 sample takes ~1.8 s per step on one core
+        shrink = min(1.0, budget_s / (1.8 * max(1, steps + warmup)))
+    dims, sample = _sample_meshes(cfg_name, cfg, shrink)
     ncores = len(os.sched_getaffinity(0))
     vb = _stock_reference()
     if vb is not None:
-        kind, how = "reference", "vbdsim.step (baseline/_ref, native backend)"
+        kind, how = "reference", "vbdsim.step (baseline/_ref, unmodified, native backend)"
         meshes = []
         for k, (nx, ny, nz, sp) in enumerate(dims):
             m = vb.generate_beam(nx, ny, nz, sp, density=b.density)
@@ -132,8 +157,8 @@ def cpu_reference_sample(cfg_name, budget_s=15.0):
         meshes = []
         for k, (nx, ny, nz, sp) in enumerate(dims):
             m = O.generate_beam(nx, ny, nz, sp, b.density)
-            meshes.append(O.Mesh(m.rest_positions + np.array([0.0, 0.0, 2.0 * k]), m.tets,
-                                 m.rest_volumes, m.inv_rest_shape, m.masses))
+            meshes.append(O.build_tet_mesh(m.rest_positions + np.array([0.0, 0.0, 2.0 * k]),
+                                           m.tets, b.density))
         fixed, off = [], 0
         for m in meshes:
             if b.fix_min_x:
@@ -151,27 +176,34 @@ def cpu_reference_sample(cfg_name, budget_s=15.0):
             O.step(s, st, cfg.h, cfg.n_max, cfg.rho, cfg.a_ext, kernel=ref, n_threads=threads)
             return time.perf_counter() - t0
 
-    best = None
+    vit = n_total * cfg.n_max
+    probe = {}
     for threads in sorted({1, ncores}):
-        dt = one_step(make(), threads)
-        if best is None or dt < best[1]:
-            best = (threads, dt)
-    threads = best[0]
+        probe[threads] = vit / one_step(make(), threads)
+    threads = max(probe, key=probe.get)
     st = make()
-    one_step(st, threads)  # warm-up
+    for _ in range(max(0, warmup)):
+        one_step(st, threads)
     times = []
     t_start = time.perf_counter()
-    while len(times) < 3 or (time.perf_counter() - t_start < budget_s and len(times) < 20):
-        times.append(one_step(st, threads))
-        if time.perf_counter() - t_start > 2 * budget_s:
-            break
+    if steps is not None:
+        for _ in range(steps):
+            times.append(one_step(st, threads))
+    else:
+        while len(times) < 3 or (time.perf_counter() - t_start < budget_s and len(times) < 20):
+            times.append(one_step(st, threads))
+            if time.perf_counter() - t_start > 2 * budget_s:
+                break
     ms = 1e3 * statistics.mean(times)
-    rate = n_total * cfg.n_max / (ms / 1e3)
+    rate = vit / (ms / 1e3)
     return {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{sample}: {n_total} vertices, {n_tets} tets, n_max={cfg.n_max}; {how}; "
-                      f"mean of {len(times)} steps after 1 warm-up, {ms:.1f} ms/step; "
-                      f"threads probed 1 and {ncores}, best={threads}",
-            "ms_per_step_sample": ms}
+                      f"mean of {len(times)} steps after {warmup} warm-up, {ms:.1f} ms/step at "
+                      f"{threads} thread(s)",
+            "threads_probe": {f"{t}_threads": r for t, r in probe.items()},
+            "host_threads": ncores, "cpu_model": cpu_model(),
+            "sample_vertices": n_total, "sample_tets": n_tets, "sample_steps": len(times),
+            "sample_warmup": warmup, "ms_per_step_sample": ms}
 
 
 def _x0(rest):
@@ -276,6 +308,33 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
+def fma_peak_tflops(device, precision, seconds=1.0):
+    """Measured FMA-pipe peak of this GPU (vbd_fma_peak: independent FMA chains on every SM,
+    packed fp32x2 FFMA2 for fp32, DFMA for fp64) run for `seconds` -- the denominator of the
+    FP32 / FP64 roofline (MEASURED_PEAKS.json has no FP32 figure)."""
+    import ctypes
+    from paper_2403_06321_b200 import _lib
+    out = ctypes.c_double(0.0)
+    prec = 1 if precision == "fp64" else 0
+    _lib.check(_lib.lib().vbd_fma_peak(int(device), prec, 1, float(seconds), ctypes.byref(out)))
+    return out.value
+
+
+def ncu_flops(cfg_name, precision, variant):
+    """Executed floating-point operations of one K1 launch, from ncu SASS counters
+    (profiles/k1_flops.json; FFMA / DFMA = 2, FFMA2 = 4, FADD2 / FMUL2 = 2)."""
+    p = ROOT / "profiles" / "k1_flops.json"
+    if not p.exists():
+        return None
+    return json.loads(p.read_text()).get(f"{cfg_name}_{precision}_{variant}")
+
+
+def reference_model_flops_per_iteration(info):
+    """~259 flops per (vertex, tet) entry in the reference's formulation
+    (_native.pyx:181-198, 292-317) + ~75 per vertex (inertia, adjugate solve, update)."""
+    return 75 * int(info.num_vertices) + 259 * 4 * int(info.num_tets)
+
+
 def ncu_traffic(cfg_name, precision, variant):
     p = ROOT / "profiles" / "k1_traffic.json"
     if not p.exists():
@@ -304,6 +363,9 @@ def run_ours(args):
         args.gpus = world
     # one process per GPU; VBD_DIST_BACKEND=gloo (tests only) lets several ranks share a GPU
     backend = os.environ.get("VBD_DIST_BACKEND", "nccl")
+    if world > 1 and backend == "nccl":   # communicator init lines (nranks) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
@@ -372,15 +434,17 @@ def run_ours(args):
         dist.all_reduce(tot)
     n_total = int(tot.item())
 
-    def timed(fn):
+    def timed(fn, strm=None):
+        """CUDA-event time of fn() on the stream its kernels run on, max over ranks."""
+        strm = stream if strm is None else strm
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        e0.record(strm)
         fn()
-        e1.record(stream)
+        e1.record(strm)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         t = torch.tensor([ms], device=red_dev)
@@ -394,20 +458,15 @@ def run_ours(args):
     ms_step = ms_total / args.steps
     vit_per_step = n_total * cfg.n_max
     value = vit_per_step * args.steps / (ms_total / 1e3)
+    checksum = state_checksum(ctx, cfg, part, exch, rank, world) if args.checksum else None
 
     # dominant kernel (K1) live timing on the same stream: average per-colour launch time
     # n_max sweeps in step order straight after the timed region: one step's worth of launches,
     # so the kernel runs at the same power-capped sustained clock as inside the step (a short
     # burst of 10 sweeps reads about 6 % faster on C5)
-    k1_ms = ctx.profile_color_pass(cfg.h, reps=max(10, cfg.n_max))
-    bytes_iter = algorithmic_bytes_per_iteration(info, args.precision)
-    layout_iter = layout_bytes_per_iteration(info, args.precision)
-    k1_iter_ms = float(np.sum(k1_ms))
-    peak, peak_kind = load_peaks()
-    achieved = bytes_iter / (k1_iter_ms / 1e3) / 1e9
-    layout_achieved = layout_iter / (k1_iter_ms / 1e3) / 1e9
-    kname = "k1_tiles" if int(info.tiles) else "k1_color_pass"
-    variant = "tiles" if int(info.tiles) else ("compact" if int(info.layout) == 1 else "explicit")
+    k1_reps = max(10, cfg.n_max)
+    k1_ms = ctx.profile_color_pass(cfg.h, reps=k1_reps)
+    roof = roofline_record(cfg, info, args.precision, k1_ms, k1_reps, local)
     phases = 1 + cfg.n_max * (int(info.num_colors) + (1 if cfg.rho else 0)) + 1
     launches_per_step = phases
     if exch is not None and args.halo == "p2p":
@@ -420,8 +479,8 @@ def run_ours(args):
     n_loc = int(info.num_vertices)
     pin = lambda: torch.empty((n_loc, 3), dtype=torch.float64, pin_memory=True).numpy()
     hx, hxt, hv, hvp = pin(), pin(), pin(), pin()
-    got = ctx.get_state(x=True, x_t=True, v_t=True, v_prev=True,
-                        out={"x": hx, "x_t": hxt, "v_t": hv, "v_prev": hvp})
+    ctx.get_state(x=True, x_t=True, v_t=True, v_prev=True,
+                  out={"x": hx, "x_t": hxt, "v_t": hv, "v_prev": hvp})
 
     bufs = {"x_t": hxt, "v_t": hv, "v_prev": hvp, "spare": hx}
 
@@ -446,6 +505,20 @@ def run_ours(args):
     e2e_value = vit_per_step / (e2e_ms / 1e3)
     h2d = 3 * 24 * n_total
     d2h = 2 * 24 * n_total
+    del hx, hxt, hv, hvp, bufs
+
+    # the reference's precision (fp64), timed in the same run on the same scene
+    fp64 = None
+    if (world == 1 and args.precision == "fp32" and not args.no_fp64_record
+            and cfg.name in ("c4", "c5")):
+        if exch is not None:
+            exch = None
+        ctx.close()
+        ctx = None
+        try:
+            fp64 = fp64_record(cfg, local, timed)
+        except Exception as e:  # pragma: no cover - reported, not fatal
+            fp64 = {"error": str(e)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -458,7 +531,6 @@ def run_ours(args):
 
     clocks = clk.summary() if rank == 0 else None
     if rank == 0:
-        b0 = cfg.beams[0]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -472,78 +544,218 @@ def run_ours(args):
                 "colors": int(info.num_colors),
                 "parallelism": (f"{cfg.sharding}x{world}" + (f" ({args.halo} halo)" if cfg.sharding == "slabs" else "")
                                 if world > 1 else "single GPU"),
-                "layout": ("K1T tiles (%d lanes/vertex, %d stages): 8 B entry slots + %d entry kinds"
-                           % (info.tile_lanes, info.tile_stages, info.num_entry_kinds) if int(info.tiles) else
-                           "compact: 16 B entries + %d entry kinds" % info.num_entry_kinds
-                           if info.layout == 1 else "explicit: %d B entries" % info.entry_bytes),
-                "l2": "inputs larger than L2 (%.1f GB of entries per GPU)"
-                      % (layout_iter / 1e9) if layout_iter > 4 * 126e6 else "scene fits in L2 (no flush)",
+                "dist_backend": backend if world > 1 else None,
+                "layout": layout_name(info),
+                "l2": ("inputs larger than L2: %.1f GB of layout bytes (slots, neighbour lists, "
+                       "tile descriptors, per-vertex state) read per iteration per GPU, no flush"
+                       % (roof["_layout_iter"] / 1e9)) if roof["_layout_iter"] > 4 * 126e6
+                      else "scene fits in L2 (no flush)",
                 "build_s": round(t_build, 2),
             },
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         "traffic": ncu_traffic(cfg.name, args.precision, variant),
-                         "kernel": kname, "peak_source": peak_kind,
-                         "k1_ms_per_color": [round(float(x), 4) for x in k1_ms],
-                         "k1_timing": f"CUDA events per launch, colours in step order, {max(10, cfg.n_max)} "
-                                      "sweeps right after the timed region (sustained clocks)",
-                         "algorithmic_bytes_per_iteration": bytes_iter,
-                         "algorithmic_bytes_per_launch": bytes_iter / max(1, int(info.num_colors)),
-                         "algorithmic_model": "SURVEY 8(d): 92 N + 208 T bytes per iteration (fp32), "
-                                              "the reference data layout (Dm^-1 per entry)",
-                         "layout_bytes_per_launch": layout_iter / max(1, int(info.num_colors)),
-                         "layout_achieved": layout_achieved, "layout_frac": layout_achieved / peak,
-                         "note": "frac > 1 is the lossless entry compression (DESIGN 2): the kernel "
-                                 "moves layout_bytes, not the reference layout's bytes; layout_frac "
-                                 "is its HBM share; no single pipe saturates (roofline.limiter: "
-                                 "latency-bound at the shared-memory-limited occupancy, "
-                                 "profiles/r01_k1t_c5_analysis.md)",
-                         "limiter": ncu_limiter(cfg.name, args.precision, variant),
-                         "traffic_unit": "DRAM bytes per k1 launch (ncu, profiles/k1_traffic.json)"},
+            "roofline": {k: v for k, v in roof.items() if not k.startswith("_")},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
         }
+        if fp64 is not None:
+            line["fp64"] = fp64
+        if checksum is not None:
+            line["state_sha256"] = checksum
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if ctx is not None:
+        ctx.close()
+
+
+def state_checksum(ctx, cfg, part, exch, rank, world):
+    """sha256 of the positions this run owns, concatenated in rank order (= original vertex
+    order for slabs and object shards), after warm-up + timed steps."""
+    import hashlib
+
+    import torch.distributed as dist
+    x = ctx.get_state(x=True)["x"]
+    if exch is not None and cfg.sharding == "slabs":
+        plane = cfg.beams[0].ny * cfg.beams[0].nz
+        lo = max(part[0] - 1, 0)
+        x = x[(part[0] - lo) * plane:(part[1] - lo) * plane]
+    x = np.ascontiguousarray(x)
+    if world > 1:
+        allx = [None] * world
+        dist.all_gather_object(allx, x)
+        x = np.concatenate(allx)
+    return hashlib.sha256(x.tobytes()).hexdigest() if rank == 0 else None
+
+
+def layout_name(info):
+    if int(info.tiles):
+        return ("K1T tiles (%d lanes/vertex, %d stages): 8 B entry slots + %d entry kinds"
+                % (info.tile_lanes, info.tile_stages, info.num_entry_kinds))
+    if info.layout == 1:
+        return "compact: 16 B entries + %d entry kinds" % info.num_entry_kinds
+    return "explicit: %d B entries" % info.entry_bytes
+
+
+def roofline_record(cfg, info, precision, k1_ms, k1_reps, device):
+    """The HBM roofline of the dominant kernel (K1, one colour pass per launch) and its FP32 /
+    FP64 roofline.
+
+    HBM: `achieved` = the compulsory bytes of the layout actually used (DESIGN.md §4:
+    slots, neighbour lists, tile descriptors, own-vertex state, other-colour positions) per
+    launch / the live CUDA-event launch time; `peak` = MEASURED_PEAKS.json hbm_gbs.  The
+    SURVEY §8(d) figure (the reference's data model, Dm^-1 stored per entry) is reported
+    separately as `reference_model` -- it exceeds the peak because the entry dictionary
+    replaces those bytes losslessly.
+    FP: executed flops per launch from ncu SASS counters (profiles/k1_flops.json) / the same
+    launch time, against the FMA peak measured live (vbd_fma_peak) after the timed region."""
+    bytes_iter = algorithmic_bytes_per_iteration(info, precision)
+    layout_iter = layout_bytes_per_iteration(info, precision)
+    ncol = max(1, int(info.num_colors))
+    k1_iter_ms = float(np.sum(k1_ms))
+    peak, peak_kind = load_peaks()
+    layout_achieved = layout_iter / (k1_iter_ms / 1e3) / 1e9
+    ref_achieved = bytes_iter / (k1_iter_ms / 1e3) / 1e9
+    kname = "k1_tiles" if int(info.tiles) else "k1_color_pass"
+    variant = "tiles" if int(info.tiles) else ("compact" if int(info.layout) == 1 else "explicit")
+    rec = {"bound": "hbm", "achieved": layout_achieved, "peak": peak, "unit": "GB/s",
+           "frac": layout_achieved / peak,
+           "traffic": ncu_traffic(cfg.name, precision, variant),
+           "kernel": kname, "peak_source": peak_kind,
+           "bytes_per_launch": layout_iter / ncol,
+           "bytes_model": "layout bytes (DESIGN.md §4): 8 B per entry slot + 4 B per neighbour-list "
+                          "entry + 64 B per tile + x, x_t, y read and x written per solved vertex + "
+                          "one read of every other-colour position" if int(info.tiles) else
+                          "layout bytes: entry_bytes per entry + CSR offset + per-vertex state + "
+                          "other-colour positions",
+           "k1_ms_per_color": [round(float(x), 4) for x in k1_ms],
+           "k1_timing": f"CUDA events per launch on the context stream, colours in step order, "
+                        f"{k1_reps} sweeps right after the timed region (sustained clocks)",
+           "reference_model": {
+               "bytes_per_launch": bytes_iter / ncol, "achieved": ref_achieved,
+               "frac": ref_achieved / peak,
+               "model": "SURVEY 8(d): 92 N + 208 T bytes per iteration (fp32) / 180 N + 368 T (fp64), "
+                        "the reference's data layout (Dm^-1 + V + 3 ids per entry); above 1 because "
+                        "the entry dictionary and 8-byte tile slots remove those bytes losslessly"},
+           "limiter": ncu_limiter(cfg.name, precision, variant),
+           "traffic_unit": "DRAM bytes per k1 launch (ncu dram__bytes_read+write, profiles/k1_traffic.json)",
+           "_layout_iter": layout_iter}
+    fl = ncu_flops(cfg.name, precision, variant)
+    try:
+        fpk = fma_peak_tflops(device, precision, 1.0)
+    except Exception:  # pragma: no cover
+        fpk = None
+    fp = {"unit": "TFLOP/s", "peak": fpk,
+          "peak_source": "measured live: vbd_fma_peak, %s chains on every SM for 1 s after the "
+                         "timed region" % ("FFMA2 (fp32x2)" if precision == "fp32" else "DFMA"),
+          "reference_model_flops_per_launch": reference_model_flops_per_iteration(info) / ncol}
+    if fl:
+        per = float(fl["flops_per_launch"])
+        fp.update({"flops_per_launch": per, "achieved": per / (k1_iter_ms / ncol / 1e3) / 1e12,
+                   "flops_source": "ncu SASS thread-instruction counters of one launch "
+                                   "(profiles/k1_flops.json: %s)" % fl.get("source", "")})
+        if fpk:
+            fp["frac"] = fp["achieved"] / fpk
+    ra = fp["reference_model_flops_per_launch"] / (k1_iter_ms / ncol / 1e3) / 1e12
+    fp["reference_model_achieved"] = ra
+    rec["fp32" if precision == "fp32" else "fp64"] = fp
+    return rec
+
+
+def fp64_record(cfg, device, timed, steps=3, warmup=2):
+    """The same scene at the reference's precision (fp64 build), timed in this run."""
+    from paper_2403_06321_b200.scenes import build
+    t0 = time.perf_counter()
+    ctx, _ = build(cfg, 0, 1, "fp64", device=device)
+    t_build = time.perf_counter() - t0
+    import torch
+    p = cfg.step_params()
+    ctx.step(p, n_steps=warmup)
+    strm = torch.cuda.ExternalStream(ctx.stream) if ctx.stream else torch.cuda.current_stream()
+    ms = timed(lambda: ctx.step(p, n_steps=steps), strm) / steps
+    info = ctx.info
+    reps = max(10, cfg.n_max)
+    k1 = ctx.profile_color_pass(cfg.h, reps=reps)
+    roof = roofline_record(cfg, info, "fp64", k1, reps, device)
+    vit = int(info.num_solved + info.num_fixed) * cfg.n_max
     ctx.close()
+    return {"dtype": "f64", "ms_per_step": ms, "value": vit / (ms / 1e3), "unit": UNIT,
+            "steps": steps, "warmup": warmup, "build_s": round(t_build, 2),
+            "layout": layout_name(info),
+            "k1_ms_per_color": roof["k1_ms_per_color"], "layout_frac": roof["frac"],
+            "roofline": {k: v for k, v in roof.items() if not k.startswith("_")}}
 
 
 def run_reference(args):
+    """The reference arm: the unmodified reference (baseline/_ref, else oracle/_ref) on this
+    box's host cores.  It runs exactly --warmup untimed and --steps timed steps of a bounded
+    sample of the workload (same generator, material, h, n_max, BCs; shrunk so the whole run
+    takes about a minute); ms_per_step is the sample's own, value its vertex-iterations/s
+    (the metric is size-independent to first order), and the full-scene ms/step it implies is
+    reported separately as an extrapolation."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2403_06321_b200.scenes import config
     cfg = config(args.config)
-    budget = max(10.0, min(60.0, args.cpu_seconds))
-    r = cpu_reference_sample(args.config, budget)
+    budget = max(20.0, min(90.0, 4 * args.cpu_seconds))
+    r = cpu_reference_sample(args.config, budget, steps=args.steps, warmup=args.warmup)
     ms_sample = r.pop("ms_per_step_sample")
-    vit = cfg.num_vertices * cfg.n_max
+    vit_full = cfg.num_vertices * cfg.n_max
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": vit / r["value"] * 1e3, "higher_is_better": True,
+        "steps": r["sample_steps"], "warmup": r["sample_warmup"],
+        "ms_per_step": ms_sample, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generators), bounded sample; ms_per_step extrapolated "
-                "linearly from the sample's vertex-iterations/s",
-        "config": {"workload": f"{cfg.name}: {cfg.description}", "num_vertices": cfg.num_vertices,
-                   "num_tets": cfg.num_tets, "h": cfg.h, "n_max": cfg.n_max, "rho": cfg.rho},
+        "data": "synthetic (reference generators), bounded sample of the workload",
+        "config": {"workload": f"{cfg.name} sample: {r['sample']}",
+                   "full_workload": f"{cfg.name}: {cfg.description}",
+                   "sample_vertices": r["sample_vertices"], "sample_tets": r["sample_tets"],
+                   "num_vertices": cfg.num_vertices, "num_tets": cfg.num_tets,
+                   "h": cfg.h, "n_max": cfg.n_max, "rho": cfg.rho},
+        "extrapolated": True,
+        "extrapolated_full_scene_ms_per_step": vit_full / r["value"] * 1e3,
         "impl": "reference",
         "cpu_baseline": r,
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    line["config"]["sample_ms_per_step"] = ms_sample
     print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` outside torchrun: start the N ranks ourselves, exactly as
+    `python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py ...`
+    would.  With fewer GPUs than ranks (tests, 1-GPU boxes) the ranks share the GPUs and the
+    control-plane collectives run over gloo (NCCL refuses two ranks on one device); the halo
+    itself stays the fused peer-memory push."""
+    import socket
+    try:
+        import torch
+        ngpu = torch.cuda.device_count()
+    except Exception:
+        ngpu = 0
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    if ngpu < args.gpus:
+        env.setdefault("VBD_DIST_BACKEND", "gloo")
+    env.setdefault("NCCL_DEBUG", "INFO")            # communicator init lines (nranks) on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(ROOT / "bench.py")] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 if __name__ == "__main__":
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(a))
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -253,6 +253,13 @@ int vbd_descend(vbd_ctx* ctx, int32_t method, int32_t n_iters, double h, double 
  * order (one CUDA event pair per launch on the context stream); ms has room for num_colors values */
 int vbd_profile_color_pass(vbd_ctx* ctx, double h, int32_t reps, double* ms);
 
+/* FMA-pipe peak of this device (the denominator of the FP32 / FP64 roofline): a kernel of
+ * independent fused multiply-add chains on every SM (precision VBD_PREC_F32: packed fp32x2
+ * FFMA2 when packed != 0, else scalar FFMA; VBD_PREC_F64: DFMA), run back to back for about
+ * `seconds` (a burst when short, the power-capped sustained rate when long).  *tflops = 2 x FMAs
+ * per second / 1e12 over the timed launches (CUDA events). */
+int vbd_fma_peak(int device, int precision, int packed, double seconds, double* tflops);
+
 const char* vbd_last_error(void);
 const char* vbd_version(void);
 

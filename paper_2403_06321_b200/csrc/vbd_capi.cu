@@ -1810,6 +1810,47 @@ __global__ void k_beam_velocity(const BeamDev* __restrict__ beams, int nb, const
     v[3 * i + 2] = q[2] + (q[3] * ry - q[4] * rx);
 }
 
+// FMA-pipe peak microbenchmark (vbd_fma_peak): 8 independent FMA chains per thread (enough
+// to cover the 4-cycle pipe latency at full occupancy); the sum is stored only under an
+// impossible condition so the chains stay live.
+template <int MODE>  // 0 FFMA, 1 FFMA2 (fp32x2), 2 DFMA
+__global__ void __launch_bounds__(256) k_fma_peak(float* sink, int iters, float a, float b)
+{
+    constexpr int CH = 8;
+    if constexpr (MODE == 1) {
+        float2 acc[CH];
+        for (int j = 0; j < CH; ++j) acc[j] = make_float2(threadIdx.x * 1e-3f + j, j * 0.5f);
+        const float2 A = make_float2(a, a), B = make_float2(b, b);
+#pragma unroll 16
+        for (int i = 0; i < iters; ++i)
+#pragma unroll
+            for (int j = 0; j < CH; ++j) acc[j] = __ffma2_rn(acc[j], A, B);
+        float t = 0.f;
+        for (int j = 0; j < CH; ++j) t += acc[j].x + acc[j].y;
+        if (t == 1234.5f) sink[threadIdx.x] = t;
+    } else if constexpr (MODE == 0) {
+        float acc[CH];
+        for (int j = 0; j < CH; ++j) acc[j] = threadIdx.x * 1e-3f + j;
+#pragma unroll 16
+        for (int i = 0; i < iters; ++i)
+#pragma unroll
+            for (int j = 0; j < CH; ++j) acc[j] = __fmaf_rn(acc[j], a, b);
+        float t = 0.f;
+        for (int j = 0; j < CH; ++j) t += acc[j];
+        if (t == 1234.5f) sink[threadIdx.x] = t;
+    } else {
+        double acc[CH];
+        for (int j = 0; j < CH; ++j) acc[j] = threadIdx.x * 1e-3 + j;
+#pragma unroll 16
+        for (int i = 0; i < iters; ++i)
+#pragma unroll
+            for (int j = 0; j < CH; ++j) acc[j] = __fma_rn(acc[j], (double)a, (double)b);
+        double t = 0.0;
+        for (int j = 0; j < CH; ++j) t += acc[j];
+        if (t == 1234.5) sink[threadIdx.x] = (float)t;
+    }
+}
+
 }  // namespace
 
 // =========================================================================================
@@ -3056,6 +3097,53 @@ int vbd_profile_color_pass(vbd_ctx* c, double h, int32_t reps, double* ms)
             ms[col] = acc / reps;
         }
         for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
+int vbd_fma_peak(int device, int precision, int packed, double seconds, double* tflops)
+{
+    return guarded([&] {
+        if (!tflops || seconds <= 0) fail(VBD_ERR_ARG, "bad argument");
+        CK(cudaSetDevice(device));
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        const int mode = precision == VBD_PREC_F64 ? 2 : (packed ? 1 : 0);
+        auto launch = [&](int iters, cudaStream_t s) {
+            const unsigned grid = 8u * (unsigned)sms;  // 8 x 256 threads = 64 warps per SM
+            if (mode == 0) k_fma_peak<0><<<grid, 256, 0, s>>>(nullptr, iters, 0.999f, 1e-3f);
+            else if (mode == 1) k_fma_peak<1><<<grid, 256, 0, s>>>(nullptr, iters, 0.999f, 1e-3f);
+            else k_fma_peak<2><<<grid, 256, 0, s>>>(nullptr, iters, 0.999f, 1e-3f);
+            CK(cudaGetLastError());
+        };
+        const double fma_per_iter = 8.0 * sms * 256.0 * 8.0 * (mode == 1 ? 2.0 : 1.0);
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        // calibrate one launch to ~20 ms, then repeat for `seconds`
+        int iters = 1 << 12;
+        float ms = 0.f;
+        for (;;) {
+            CK(cudaEventRecord(e0, s));
+            launch(iters, s);
+            CK(cudaEventRecord(e1, s));
+            CK(cudaEventSynchronize(e1));
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            if (ms >= 5.0f || iters >= (1 << 26)) break;
+            iters *= 4;
+        }
+        iters = (int)std::min<double>((double)(1 << 28), iters * (20.0 / std::max(ms, 1e-3f)));
+        const int reps = std::max(1, (int)(seconds * 1e3 / 20.0));
+        CK(cudaEventRecord(e0, s));
+        for (int r = 0; r < reps; ++r) launch(iters, s);
+        CK(cudaEventRecord(e1, s));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        *tflops = 2.0 * fma_per_iter * (double)iters * reps / (ms * 1e-3) / 1e12;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(s);
     });
 }
 

@@ -594,10 +594,8 @@ __device__ __forceinline__ void k1_vertex_impl(const K1Args<R>& a, int g, int la
             const int j = v - a.vbeg;
             if (j < a.nb[0]) {
                 a.peer_pos[0][a.peer_off[0] + j] = nx;  // NVLink store into the left ghost
-                __threadfence_system();
             } else if (j < a.nb[0] + a.nb[1]) {
                 a.peer_pos[1][a.peer_off[1] + (j - a.nb[0])] = nx;
-                __threadfence_system();
             }
         }
     }
@@ -1101,6 +1099,12 @@ __global__ void k_ls_blend(typename Vec4<R>::T* pos, const typename Vec4<R>::T* 
 // written by its left neighbour, flags[1] by its right one; values are monotonically
 // increasing phase stamps base + phase, base = phases of all previous steps (identical on
 // every rank because every rank runs the same phase sequence).
+// The release of a phase.  The colour pass before it stored its slab-boundary vertices
+// straight into the neighbours' ghost slots (plain st.global through the cudaIpc mapping, no
+// per-store fence).  This kernel is stream-ordered after that grid has completed, so those
+// stores happen-before this thread; the system-scope fence + st.release.sys below publishes
+// all of them with one release per phase, and the neighbour's k_phase_wait (ld.acquire.sys)
+// synchronises with it before its next phase reads a ghost.
 __global__ void k_phase_signal(unsigned long long* left_slot, unsigned long long* right_slot,
                                const unsigned long long* epoch, unsigned long long pps, int phase)
 {

@@ -506,10 +506,8 @@ __device__ __forceinline__ void k1t_store(const K1Args<R>& a, int v, typename Ve
         const int jj = v - a.vbeg;
         if (jj < a.nb[0]) {
             a.peer_pos[0][a.peer_off[0] + jj] = nx;  // NVLink store into the left ghost
-            __threadfence_system();
         } else if (jj < a.nb[0] + a.nb[1]) {
             a.peer_pos[1][a.peer_off[1] + (jj - a.nb[0])] = nx;
-            __threadfence_system();
         }
     }
     if (a.flag && !finite3(nx.x, nx.y, nx.z))
@@ -543,6 +541,9 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
     unsigned char* stages = smem + ((L.kinds_bytes() + 127) & ~(size_t)127);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int QH = KindRec<R>::QH, Q = KindRec<R>::Q;
+    // chunks the entry loop reads: with one material per vertex the sweep needs t[0..7] only
+    // (t[8] = V mu |w|^2 is summed per vertex at pack time, dsc / opd are read once per vertex)
+    constexpr int QS = UM ? 8 * (int)sizeof(R) / 16 : QH;
     if (!KG) {
         for (int i = tid; i < ta.nkinds * QH; i += blockDim.x) skind[i] = ta.kinds[(i / QH) * Q + i % QH];
         for (int i = tid; i < QH; i += blockDim.x) skind[ta.nkinds * QH + i] = PL{};  // padding: zero record
@@ -721,7 +722,7 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                     float r[KindRec<R>::HOT];
                     const unsigned rp = kb + (e[u].y >> 16);
 #pragma unroll
-                    for (int q = 0; q < QH; ++q) {
+                    for (int q = 0; q < QS; ++q) {
                         PL v;
                         if constexpr (KG) v = __ldg(ta.kinds + (size_t)(e[u].y >> 16) * Q + q);
                         else lds_v(rp + 16u * q, v);
@@ -738,7 +739,7 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                     R r[KindRec<R>::HOT];
                     const unsigned rp = kb + (e[u].y >> 16);
 #pragma unroll
-                    for (int q = 0; q < QH; ++q) {
+                    for (int q = 0; q < QS; ++q) {
                         PL v;
                         if constexpr (KG) v = __ldg(ta.kinds + (size_t)(e[u].y >> 16) * Q + q);
                         else lds_v(rp + 16u * q, v);
@@ -750,7 +751,8 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                     const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
                     const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
                     const int b = u % NA;  // i0 is a multiple of U, so (i0 + u) % NA == u % NA (unrolled)
-                    tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], dx, fa[b], Ha[b], sva[b]);
+                    tet_contrib_ec<R, !UM>(e0, e1, e2, r, UM ? R(0) : r[9], UM ? R(1) : r[10], dx, fa[b], Ha[b],
+                                           sva[b]);
                 }
             }
         }

@@ -580,12 +580,105 @@ def convergence_fixture():
     save("convergence.npz", **out)
 
 
+def config_fixtures():
+    """Parity at the BASELINE configs' own settings.
+
+    * c2_full.npz -- C2 at full size: generate_cube(37, 0.5), mu=2e6 lam=1e7 kd=1e-6,
+      x0 = default_rng(0).uniform(bbox) (regenerated by the tests from the mesh), h=1/60,
+      no gravity.  Per-colour-pass outputs of the first iteration of the first step on
+      identical inputs (x = x_t = y = x0; only the colour's own rows are stored) and x after
+      the first step at n_max=100, rho=0.95.
+    * c4obj_steps.npz -- the first C4 object: generate_cube(15, 0.3) translated to z=1,
+      mu=1e6 lam=1e7 kd=1e-7, h=1/120, n_max=60, gravity, seeded rigid velocity
+      v = lin + ang x (x - centre); x after steps 1, 5, 10.
+    * c5block_steps.npz -- a 32^3 block with C5's material, h, n_max and BCs:
+      generate_beam(32,32,32,0.01), x=0 face fixed, mu=2e6 lam=2e7 kd=1e-7, h=1/240,
+      n_max=40, gravity; x after steps 1 and 10.
+    """
+    from vbdsim import build_tet_mesh
+    # C2
+    m = generate_cube(37, 0.5, density=1000.0)
+    s = build_system([Body(m, MaterialParams(2e6, 1e7, 1e-6))])
+    lo, hi = m.rest_positions.min(0), m.rest_positions.max(0)
+    x0 = np.random.default_rng(0).uniform(lo, hi, size=m.rest_positions.shape)
+    st = make_state(s, x0=x0)
+    p = SolverParams(h=1.0 / 60.0, n_max=100, rho=0.95, threads=1)
+    out = {}
+    off = s.color_off
+    x = x0.copy()
+    for g in range(s.colors.num_colors):
+        grp = s.color_verts[off[g]:off[g + 1]]
+        st.x = x.copy()
+        color_pass(st, grp, p)
+        out[f"after_color{g}"] = st.x[grp].copy()
+        x = st.x.copy()
+    st = make_state(s, x0=x0)
+    step(st, p)
+    # the reference's own noise floor on these inputs: its NumPy backend (same algorithm,
+    # different rounding) against its native backend, per pass and after the first step
+    from vbdsim import _backend
+    from vbdsim import _numpy_core
+    native = _backend._impl
+    _backend._impl = _numpy_core
+    try:
+        fmax, fq = [], []
+        x = x0.copy()
+        for g in range(s.colors.num_colors):
+            grp = s.color_verts[off[g]:off[g + 1]]
+            stn = make_state(s, x0=x0)
+            stn.x = x.copy()
+            color_pass(stn, grp, p)
+            d = np.abs(stn.x[grp] - out[f"after_color{g}"])
+            fmax.append(d.max())
+            fq.append(np.quantile(d, 0.999))
+            x[grp] = out[f"after_color{g}"]
+        stn = make_state(s, x0=x0)
+        step(stn, p)
+        diag = np.linalg.norm(st.x.max(0) - st.x.min(0))
+        floor_step1 = np.abs(stn.x - st.x).max() / diag
+    finally:
+        _backend._impl = native
+    save("c2_full.npz", x_step1=st.x, floor_pass_max=np.array(fmax),
+         floor_pass_p999=np.array(fq), floor_step1=np.float64(floor_step1), **out)
+    # one C4 object
+    rng = np.random.default_rng(0)
+    lin = rng.uniform(-1, 1, (10368, 3))[0]
+    ang = 4.0 * rng.uniform(-1, 1, (10368, 3))[0]
+    m0 = generate_cube(15, 0.3, density=1000.0)
+    m = build_tet_mesh(m0.rest_positions + np.array([0.0, 0.0, 1.0]), m0.tets, 1000.0)
+    c = np.array([0.0, 0.0, 1.0]) + 0.5 * (0.3 / 14) * 14
+    r = m.rest_positions - c
+    v0 = np.stack([lin[0] + (ang[1] * r[:, 2] - ang[2] * r[:, 1]),
+                   lin[1] + (ang[2] * r[:, 0] - ang[0] * r[:, 2]),
+                   lin[2] + (ang[0] * r[:, 1] - ang[1] * r[:, 0])], 1)
+    s = build_system([Body(m, MaterialParams(1e6, 1e7, 1e-7))])
+    st = make_state(s, v0=v0)
+    p = SolverParams(h=1.0 / 120.0, n_max=60, a_ext=G, threads=1)
+    xs = []
+    for k in range(10):
+        step(st, p)
+        if k in (0, 4, 9):
+            xs.append(st.x.copy())
+    save("c4obj_steps.npz", la=np.concatenate([lin, ang]), v0=v0, x=np.array(xs),
+         steps=np.array([1, 5, 10]))
+    # C5 material / h / BCs on a 32^3 block
+    m, fixed, s = beam_system(32, 32, 32, 0.01, mat=(2e6, 2e7, 1e-7))
+    st = make_state(s)
+    p = SolverParams(h=1.0 / 240.0, n_max=40, a_ext=G, threads=1)
+    xs = []
+    for k in range(10):
+        step(st, p)
+        if k in (0, 9):
+            xs.append(st.x.copy())
+    save("c5block_steps.npz", x=np.array(xs), steps=np.array([1, 10]), fixed=fixed)
+
+
 if __name__ == "__main__":
     which = set(sys.argv[1:]) or {"mesh", "coloring", "pass", "steps", "extras", "energy", "contact", "harness",
-                                 "convergence"}
+                                 "convergence", "configs"}
     for name, fn in (("mesh", mesh_fixture), ("coloring", coloring_fixtures), ("pass", pass_fixture),
                      ("steps", step_fixtures), ("extras", extras_fixture), ("energy", energy_fixture),
                      ("contact", contact_fixture), ("harness", harness_fixture),
-                     ("convergence", convergence_fixture)):
+                     ("convergence", convergence_fixture), ("configs", config_fixtures)):
         if name in which:
             fn()

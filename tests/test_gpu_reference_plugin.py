@@ -22,8 +22,8 @@ def ref():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
-    if not (REF / "vbdsim").exists():
-        pytest.skip("reference not installed in baseline/_ref")
+    # build() installs the unmodified reference here; its absence is a failure, not a skip
+    assert (REF / "vbdsim").exists(), "reference not installed in baseline/_ref (run build())"
     sys.path.insert(0, str(REF))
     import vbdsim
     from vbdsim import _backend

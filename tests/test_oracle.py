@@ -203,3 +203,57 @@ def test_contact_passes_bit_exact(O, golden):
                      eps_v=float(g[f"call{k}_eps_v"]))
         assert np.array_equal(x, g[f"call{k}_x1"]), k
         assert not np.array_equal(x, g[f"call{k}_x0"])
+
+
+# --------------------------------------------------------------------------------------
+# BASELINE configs' own settings (tests/golden/make_golden.py::config_fixtures)
+
+
+def c2_full_system(O):
+    m = O.generate_cube(37, 0.5)
+    s = O.build_system([(m, (2e6, 1e7, 1e-6))])
+    lo, hi = m.rest_positions.min(0), m.rest_positions.max(0)
+    x0 = np.random.default_rng(0).uniform(lo, hi, size=m.rest_positions.shape)
+    return m, s, x0
+
+
+def test_c2_full_color_passes_bit_exact(O, golden):
+    """C2 at full size (37^3): the first iteration's colour passes on identical inputs."""
+    g = golden("c2_full.npz")
+    m, s, x0 = c2_full_system(O)
+    x = x0.copy()
+    for c, grp in enumerate(s.groups()):
+        O.color_pass(s, x, x0, x0, 1.0 / 60.0, grp)
+        assert np.array_equal(x[grp], g[f"after_color{c}"]), c
+
+
+def test_c2_full_first_step_bit_exact(O, golden):
+    g = golden("c2_full.npz")
+    m, s, x0 = c2_full_system(O)
+    st = O.make_state(s, x0=x0)
+    O.step(s, st, 1.0 / 60.0, 100, 0.95, (0.0, 0.0, 0.0))
+    assert np.array_equal(st.x, g["x_step1"])
+
+
+def test_c4_object_steps_bit_exact(O, golden):
+    """The first C4 object (cube 15, z=1, rigid velocity) at C4's material/h/n_max."""
+    g = golden("c4obj_steps.npz")
+    m0 = O.generate_cube(15, 0.3)
+    m = O.build_tet_mesh(m0.rest_positions + np.array([0.0, 0.0, 1.0]), m0.tets, 1000.0)
+    s = O.build_system([(m, (1e6, 1e7, 1e-7))], [])
+    st = O.make_state(s, v0=g["v0"])
+    want = dict(zip(g["steps"].tolist(), g["x"]))
+    for k in range(1, 11):
+        O.step(s, st, 1.0 / 120.0, 60, 0.0, G)
+        if k in want:
+            assert np.array_equal(st.x, want[k]), k
+
+
+def test_c5_block_first_step_bit_exact(O, golden):
+    """32^3 block with C5's material, h, n_max and fixed face."""
+    g = golden("c5block_steps.npz")
+    m, fixed, s = _beam_system(O, 32, 32, 32, 0.01, mat=(2e6, 2e7, 1e-7))
+    assert np.array_equal(fixed, g["fixed"])
+    st = O.make_state(s)
+    O.step(s, st, 1.0 / 240.0, 40, 0.0, G)
+    assert np.array_equal(st.x, g["x"][0])
