@@ -139,6 +139,9 @@ typedef struct {
     int32_t tile_stages;       /* K1T: shared-memory pipeline stages */
     int32_t tile_ent_cap;      /* K1T: entry slots of the largest tile (per-stage capacity) */
     int32_t tile_smem_bytes;   /* K1T: dynamic shared memory per CTA */
+    int32_t resident;          /* K1R whole-step kernel (decided at the first step): 0 none,
+                                  1 one cluster with position replicas, 2 grid-resident */
+    int32_t resident_ctas;     /* K1R: CTAs (cluster size for 1, SMs for 2) */
 } vbd_ctx_info;
 
 /* ---- context ---------------------------------------------------------------------------- */

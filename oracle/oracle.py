@@ -436,6 +436,74 @@ def color_pass(system, x, x_t, y, h, group, mode=0, line_search=False, eps_det=1
         raise MemoryError("oracle colour pass failed")
 
 
+_lib32 = None
+
+
+def color_pass_fp32(system, x, x_t, y, h, group, eps_det=1e-10):
+    """The same colour pass with every real in binary32 (liboracle_f32.so, tets only): the
+    reference ALGORITHM in fp32 arithmetic.  Used only as the fp32 sensitivity yardstick on
+    ill-conditioned inputs; returns the group's new rows (float64 copy of the fp32 result)."""
+    global _lib32
+    if _lib32 is None:
+        path = HERE / "liboracle_f32.so"
+        if not path.exists():
+            subprocess.run(["make", "-C", str(HERE), "liboracle_f32.so"], check=True, capture_output=True)
+        L = ctypes.CDLL(str(path))
+        P = ctypes.c_void_p
+        L.oracle_color_pass.argtypes = [ctypes.c_int64, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
+                                        ctypes.c_float, P, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_float, ctypes.c_int]
+        L.oracle_color_pass.restype = ctypes.c_int
+        _lib32 = L
+    s = system
+    if s.has_extras:
+        raise NotImplementedError("color_pass_fp32: tets only")
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float32)
+    keep = [f(x), f(x_t), f(y), f(s.masses), f(s.tet_w), f(s.tet_vol), f(s.tet_mu), f(s.tet_lam),
+            f(s.tet_kd)]
+    x32, xt32, y32, m32, w32, v32, mu32, la32, kd32 = keep
+    g = np.ascontiguousarray(group, dtype=np.int64)
+    rc = _lib32.oracle_color_pass(s.num_vertices, _p(x32), _p(xt32), _p(y32), _p(m32), _p(s.tets), _p(w32),
+                                  _p(v32), _p(mu32), _p(la32), _p(kd32), _p(s.t_off), _p(s.t_id),
+                                  _p(s.t_slot), _p(s.kind), float(h), _p(g), len(g), 0, 0, float(eps_det), 0)
+    if rc != 0:
+        raise MemoryError("oracle fp32 colour pass failed")
+    return x32[g].astype(np.float64)
+
+
+def step_fp32(system, st, h, n_max, rho=0.0, a_ext=(0.0, 0.0, 0.0), eps_det=1e-10):
+    """step() with every real in binary32: float32 state and K2 / blend / velocity arithmetic,
+    colour passes through color_pass_fp32 (tets only, adaptive init, no contact).  The fp32
+    sensitivity yardstick for chaotic scenes (C2 extreme init), never a parity reference."""
+    f = np.float32
+    a = np.asarray(a_ext, dtype=f)
+    h32 = f(h)
+    xt, vt, vp = (np.asarray(v, dtype=f) for v in (st.x_t, st.v_t, st.v_prev))
+    y = xt + h32 * vt + (h32 * h32) * a
+    norm = f(np.linalg.norm(a))
+    if norm == 0:
+        x = xt + h32 * vt
+    else:
+        at = (vt - vp) / h32
+        comp = at @ (a / norm)
+        x = xt + h32 * vt + ((h32 * h32) * np.clip(comp / norm, 0, 1).astype(f))[:, None] * a
+    x[system.kind == 1] = xt[system.kind == 1]
+    x = np.ascontiguousarray(x, dtype=f)
+    prev1, pp = x.copy(), None
+    for n in range(1, n_max + 1):
+        for g in system.groups():
+            x[g] = color_pass_fp32(system, x, xt, y, h, g, eps_det).astype(f)
+        omega = chebyshev_omega(rho, n)
+        if omega != 1.0 and pp is not None:
+            x[...] = f(omega) * (x - pp) + pp
+        pp = prev1
+        prev1 = x.copy()
+    v = (x - xt) / h32
+    st.v_prev, st.v_t, st.x_t, st.x = st.v_t, v.astype(np.float64), x.astype(np.float64), x.astype(np.float64)
+    st.step_index += 1
+    return st
+
+
 def local_energy(system, x, y, h, i, p):
     s = system
     p = np.ascontiguousarray(p, dtype=np.float64)

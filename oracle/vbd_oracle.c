@@ -36,7 +36,15 @@
 #include <omp.h>
 #endif
 
+/* ORACLE_F32 (liboracle_f32.so): the same restatement with every real -- arrays, scalars and
+ * literals (-fsingle-precision-constant) -- in binary32.  It is the fp32-arithmetic SENSITIVITY
+ * yardstick for ill-conditioned inputs (tests/test_gpu_configs.py, C2 extreme init), never a
+ * parity reference. */
+#ifdef ORACLE_F32
+typedef float f64;
+#else
 typedef double f64;
+#endif
 typedef int64_t i64;
 
 #define KIND_FIXED 1

@@ -67,7 +67,8 @@ class CtxInfo(ctypes.Structure):
                 ("num_materials", i32), ("layout", i32), ("entry_bytes", i32),
                 ("num_entry_kinds", i64), ("tiles", i32), ("tile_nbr_cap", i32),
                 ("tile_slots", i64), ("tile_nbr_refs", i64), ("tile_lanes", i32),
-                ("tile_stages", i32), ("tile_ent_cap", i32), ("tile_smem_bytes", i32)]
+                ("tile_stages", i32), ("tile_ent_cap", i32), ("tile_smem_bytes", i32),
+                ("resident", i32), ("resident_ctas", i32)]
 
 
 # name -> (restype, argtypes); must match include/vbd_b200.h (checked by tests)

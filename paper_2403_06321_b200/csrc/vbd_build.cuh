@@ -640,6 +640,17 @@ __global__ void k_kind_records(const unsigned* __restrict__ keys, int nk, const 
     for (int j = 0; j < KindRec<R>::NR; ++j) o[j] = r[j];
 }
 
+// rest edges of every kind (fp32 displacement state): W^-1 of the key's three fp32 rows
+__global__ void k_kind_edges(const unsigned* __restrict__ keys, int nk, float4* __restrict__ out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nk) return;
+    const unsigned* key = keys + (long long)i * KindKey<float>::KW;
+    float w[9];
+    for (int j = 0; j < 9; ++j) w[j] = __uint_as_float(key[j]);
+    rest_edges_from_rows(w, out + 3LL * i);
+}
+
 __global__ void k_max_degree(const long long* __restrict__ eoff, long long n, int* out)
 {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;

@@ -1,6 +1,7 @@
 // vbd_capi.cu -- the C ABI (include/vbd_b200.h): device context, scene packing, the
 // CUDA-graph step pipeline and the protocol-compatible colour pass.
 #include <cub/cub.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -18,6 +19,7 @@
 #include "vbd_kernels.cuh"
 #include "vbd_tiles.cuh"
 #include "vbd_contact.cuh"
+#include "vbd_resident.cuh"
 
 // K1 launch variant (lanes per vertex W, entries per lane per iteration U, min blocks/SM);
 // selected per context from VBD_K1 (e.g. "8x1", "4x2", "4x2b3"), default below.
@@ -54,6 +56,21 @@ struct VbdError {
             fail(VBD_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + " (" + \
                                    __FILE__ + ":" + std::to_string(__LINE__) + ")");      \
     } while (0)
+
+// NVTX ranges (header-only nvtx3; free when no tool is attached).  Host-driven paths mark
+// every step / iteration / colour pass; the graph path marks each step's graph launch.
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    template <typename... A> Nvtx(const char* fmt, A... a)
+    {
+        char buf[96];
+        snprintf(buf, sizeof buf, fmt, a...);
+        nvtxRangePushA(buf);
+    }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 template <typename F> int guarded(F&& f)
 {
@@ -199,6 +216,11 @@ struct vbd_ctx {
     int nkinds = 0;
     int max_deg = 0;
     DBuf kinds, kind_keys;
+    // fp32 displacement state: position-like vectors (x, x_t, y, Chebyshev history)
+    // are stored as x - X with the rest positions X kept in double (rest, colour-major); the
+    // kernels add the kinds' rest edges (kedge, 3 float4 per kind + a zero record)
+    bool disp = false;
+    DBuf rest, kedge;
     // non-tet terms (springs, world box, subspace): host-built systems only; global K1
     bool has_extras = false;
     DBuf soff, sp_oth, sp_par, box, sub_idx, sub;
@@ -225,6 +247,13 @@ struct vbd_ctx {
     int tile_stages = 2, tile_w = 4, tile_occ = 2;
     bool tile_defer = true;  // K1T deferred block solves (VBD_TILE_DEFER=0 disables)
     bool tile_kg = false;    // K1T kind records read from global (table too large for shared memory)
+    // K1R resident whole-step kernel (small scenes): 0 off, 1 REPL (one cluster, position
+    // replicas in shared memory), 2 GLOB (one CTA per SM, grid barrier); -1 not decided yet
+    int res_mode = -1;
+    std::string res_want;  // VBD_RESIDENT at context creation
+    int res_ncta = 0, res_slot_cap = 0, res_grp_cap = 0;
+    size_t res_smem = 0;
+    DBuf res_slots, res_slot_beg, res_groups, res_grp_beg, res_col_grp, res_bar;
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -426,6 +455,7 @@ int run_jp(const long long* noff, const int* nids, const long long* rank, long l
 // neighbour CSR from the incidence, then K5
 void color_scene(Scene& sc, cudaStream_t s)
 {
+    Nvtx nv_("colouring (K5)");
     DBuf cnt, overflow, noff, nids;
     cnt.alloc(sc.n * 4);
     overflow.alloc(4);
@@ -521,6 +551,12 @@ template <typename R> void compact_entries(vbd_ctx* c)
     CK(cudaMemsetAsync(c->kinds.p, 0, (size_t)(nk + 1) * KindRec<R>::Q * 16, s));
     c->compact = true;
     c->nkinds = nk;
+    if constexpr (sizeof(R) == 4) {  // rest edges per kind (+ the zero record at index nk)
+        c->kedge.alloc((size_t)(nk + 1) * 48);
+        CK(cudaMemsetAsync(c->kedge.p, 0, (size_t)(nk + 1) * 48, s));
+        k_kind_edges<<<blocks_for(nk), 256, 0, s>>>(c->kind_keys.as<unsigned>(), nk, c->kedge.as<float4>());
+        CK(cudaGetLastError());
+    }
 }
 
 // kind records for the current material table
@@ -540,6 +576,7 @@ constexpr size_t VBD_TILE_SMEM_MAX = 112 * 1024;  // two CTAs per SM
 
 template <typename R> void build_tiles(vbd_ctx* c)
 {
+    Nvtx nv_("tile build");
     c->tiles = false;
     const char* e = getenv("VBD_TILES");
     if ((e && *e == '0') || !c->compact || !c->inplace || c->nsolve == 0 || c->nkinds >= 65535 ||
@@ -598,7 +635,8 @@ template <typename R> void build_tiles(vbd_ctx* c)
     // slots hold 16-bit shared-memory byte offsets (+1 zero position) and a 16-bit kind: the
     // record's byte offset in the shared-memory table, or (KG: tables over 32 KB, e.g. fp64
     // grids whose rest shapes differ in the last bits) its index in the global table
-    if ((mx + 1) * (long long)sizeof(typename Vec4<R>::T) > 65535) return;
+    constexpr unsigned PU = TileSmem<R>::PU;  // slot offsets address 16-byte position units
+    if ((mx + 1) * (long long)PU > 65535) return;
     if (c->nkinds >= 65535) return;
     const char* kge = getenv("VBD_TILE_KG");
     c->tile_kg = (long long)(c->nkinds + 1) * KindRec<R>::HOT * sizeof(R) > 32768 || (kge && *kge == '1');
@@ -635,8 +673,7 @@ template <typename R> void build_tiles(vbd_ctx* c)
     k_tile_nbrs<true><<<nt, 256, sort_smem, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
                                                 cent, nullptr, c->loff.as<long long>(), sbase.as<long long>(),
                                                 c->tnbr.as<int>(), c->tent.as<uint2>(), W,
-                                                (unsigned)sizeof(typename Vec4<R>::T),
-                                                (unsigned)(c->nbr_cap * sizeof(typename Vec4<R>::T)),
+                                                PU, (unsigned)(c->nbr_cap * PU),
                                                 c->tile_kg ? 1u : (unsigned)(KindRec<R>::HOT * sizeof(R)),
                                                 c->tile_kg ? (unsigned)c->nkinds
                                                            : (unsigned)(c->nkinds * KindRec<R>::HOT * sizeof(R)),
@@ -651,7 +688,7 @@ template <typename R> void build_tiles(vbd_ctx* c)
         // bank groups: DSATUR colouring per tile (VBD_TILE_BANKS=greedy: the sweep-order greedy)
         const char* bm = getenv("VBD_TILE_BANKS");
         const bool dsatur = !(bm && std::string(bm) == "greedy");
-        const unsigned pad_pos = (unsigned)(c->nbr_cap * sizeof(typename Vec4<R>::T));
+        const unsigned pad_pos = (unsigned)(c->nbr_cap * PU);
         if (dsatur) {
             int vmax = 1;
             for (int t = 0; t < nt; ++t) vmax = std::max(vmax, nl_real[t]);
@@ -659,13 +696,12 @@ template <typename R> void build_tiles(vbd_ctx* c)
             const size_t smem = (size_t)vmax * 12 + (size_t)(vmax + 1) * 4 + (size_t)mmax * 2 + 16;
             CK(cudaFuncSetAttribute(k_tile_banks_dsatur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             k_tile_banks_dsatur<<<nt, 32, smem, s>>>(c->loff.as<long long>(), sbase.as<long long>(), dnl.as<int>(), nt,
-                                                    (unsigned)sizeof(typename Vec4<R>::T), pad_pos,
-                                                    c->tent.as<uint2>(), asg.as<int>(), vmax, mmax);
+                                                    PU, pad_pos, c->tent.as<uint2>(), asg.as<int>(), vmax, mmax);
             CK(cudaGetLastError());
         }
         k_tile_banks<<<blocks_for(nt, 64), 64, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
                                                       c->loff.as<long long>(), sbase.as<long long>(), dnl.as<int>(),
-                                                      nt, W, (unsigned)sizeof(typename Vec4<R>::T), pad_pos,
+                                                      nt, W, PU, pad_pos,
                                                       c->tnbr.as<int>(), c->tent.as<uint2>(), ids.as<int>(),
                                                       asg.as<int>(), dsatur ? 1 : 0);
         CK(cudaGetLastError());
@@ -698,6 +734,7 @@ template <typename R> void sort_incidence_by_kind(Scene& sc, cudaStream_t s)
 // K6 + context finalisation
 template <typename R> void pack(vbd_ctx* c, Scene& sc)
 {
+    Nvtx nv_("pack (K6)");
     cudaStream_t s = c->stream;
     c->n = sc.n;
     c->T = sc.T;
@@ -843,6 +880,16 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
     c->color_orig.alloc(sc.n * 4);
     CK(cudaMemcpyAsync(c->color_orig.p, sc.color.p, sc.n * 4, cudaMemcpyDeviceToDevice, s));
     alloc_state<R>(c);
+    // rest positions (colour-major, double) and the fp32 displacement state
+    if (sc.pos.p && sc.n) {
+        c->rest.alloc((size_t)sc.n * sizeof(double4));
+        k_rest_positions<<<blocks_for(sc.n), 256, 0, s>>>(sc.pos.as<double>(), c->perm.as<int>(), (int)sc.n,
+                                                          c->rest.as<double4>());
+        CK(cudaGetLastError());
+        const char* de = getenv("VBD_DISP");
+        c->disp = sizeof(R) == 4 && !c->has_extras && !(de && *de == '0');
+    }
+    if (sizeof(R) == 4 && !c->disp) c->tiles = false;  // K1T / K1R are compiled for the fp32 displacement state
     CK(cudaStreamSynchronize(s));
 }
 
@@ -914,6 +961,8 @@ K1Args<R> k1_args(vbd_ctx* c, double eps_det, int mode, bool check, int iter)
     a.pf_dist = 0;
     a.vmat = c->uniform_mat ? c->vmat.as<int>() : nullptr;
     a.vsv = c->uniform_mat ? c->vsv.as<R>() : nullptr;
+    a.kedge = (c->disp && c->compact) ? c->kedge.as<float4>() : nullptr;
+    a.disp = c->disp ? 1 : 0;
     a.line_search = 0;
     a.peer_pos[0] = a.peer_pos[1] = nullptr;
     a.peer_off[0] = a.peer_off[1] = 0;
@@ -1173,8 +1222,14 @@ template <typename R> void enqueue_end(vbd_ctx* c)
         c->flag.as<unsigned long long>(), c->stepctr.as<int>());
 }
 
+template <typename R> void launch_resident(vbd_ctx* c);
+
 template <typename R> void enqueue_step(vbd_ctx* c)
 {
+    if (c->res_mode > 0 && !c->cur.line_search) {  // the whole step in one resident launch
+        launch_resident<R>(c);
+        return;
+    }
     enqueue_begin<R>(c);
     bool check_in_k1 = c->cur.rho == 0.0;  // otherwise K3 checks every vertex
     for (int n = 1; n <= c->cur.n_max; ++n) {
@@ -1232,6 +1287,230 @@ template <typename R> void enqueue_step_p2p(vbd_ctx* c)
     enqueue_end<R>(c);
     signal();
     k_epoch_advance<<<1, 32, 0, s>>>(fl + 2, pps);
+}
+
+// Contacts (DCD / CCD and the K1 contact terms) work on absolute positions: leave the fp32
+// displacement state for good -- x = fl32(X + u) for every position-like vector -- and drop
+// the paths compiled for it (K1T tiles, K1R) and the cached step graph.
+void to_absolute(vbd_ctx* c)
+{
+    if (!c->disp) return;
+    cudaStream_t s = c->stream;
+    for (DBuf* d : {&c->pos, &c->xt, &c->y, &c->ha, &c->hb})
+        if (d->p) k_disp_to_abs<<<blocks_for(std::max<long long>(c->n, 1)), 256, 0, s>>>(d->as<float4>(),
+                                                                                     c->rest.as<double4>(), (int)c->n);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    c->disp = false;
+    c->tiles = false;
+    c->res_mode = 0;
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+}
+
+// ---- K1R: resident whole-step kernel for small scenes (vbd_resident.cuh) ----------------
+
+// Decide (once per context, at its first step) whether the step runs as one resident launch,
+// and build its per-CTA layout on the host from the compact entries: per colour, 8-vertex
+// groups (4 lanes per vertex, rounds = max ceil(d / 4), even) are cut into contiguous runs of
+// equal slot work, one run per CTA; each group's slots are [round][lane] int4 {n0, n1, n2,
+// kind}, padding = {n, n, n, nkinds} (zero position, zero record).
+// VBD_RESIDENT: unset = REPL when the replica fits one cluster, "0" off, "repl" / "glob" force.
+template <typename R> void ensure_resident(vbd_ctx* c)
+{
+    if (c->res_mode >= 0) return;
+    c->res_mode = 0;
+    const std::string want = c->res_want;
+    if (want == "0" || !c->compact || !c->inplace || c->has_extras || c->ncontacts || c->coll_on || c->nsolve == 0 ||
+        c->ncolors > VBD_RES_MAX_COLORS || c->nkinds >= 65535 || c->n >= (1LL << 30))
+        return;
+    Nvtx nv_("resident layout");
+    typedef typename Vec4<R>::T R4;
+    cudaStream_t s = c->stream;
+    std::vector<long long> eoff(c->nsolve + 1);
+    std::vector<int4> ent((size_t)c->E);
+    CK(cudaMemcpyAsync(eoff.data(), c->eoff.p, eoff.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ent.data(), c->ent.p, ent.size() * 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int dev = 0, sms = 148, smem_max = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    struct G { int v0, nv, rounds; };
+    std::vector<std::vector<G>> cg(c->ncolors);
+    for (int col = 0; col < c->ncolors; ++col)
+        for (long long o = 0; o < c->ccnt[col]; o += 8) {
+            G g{(int)(c->cbeg[col] + o), (int)std::min<long long>(8, c->ccnt[col] - o), 0};
+            for (int k = 0; k < g.nv; ++k) {
+                const long long d = eoff[g.v0 + k + 1] - eoff[g.v0 + k];
+                g.rounds = std::max(g.rounds, (int)((d + 3) / 4));
+            }
+            g.rounds = (g.rounds + 1) / 2 * 2;
+            cg[col].push_back(g);
+        }
+    // runs of equal work per CTA and colour
+    auto plan = [&](int ncta, std::vector<std::vector<int>>& cut, int& slot_cap, int& grp_cap) {
+        cut.assign(c->ncolors, std::vector<int>(ncta + 1, 0));
+        std::vector<long long> slots(ncta, 0), grps(ncta, 0);
+        for (int col = 0; col < c->ncolors; ++col) {
+            const auto& gs = cg[col];
+            long long tot = 0;
+            for (const G& g : gs) tot += g.rounds + 2;
+            long long acc = 0;
+            int k = 0;
+            for (int i = 0; i < (int)gs.size(); ++i) {
+                while (k < ncta - 1 && acc * ncta >= tot * (k + 1)) cut[col][++k] = i;
+                acc += gs[i].rounds + 2;
+                slots[k] += 32LL * gs[i].rounds;
+                grps[k] += 1;
+            }
+            while (k < ncta - 1) cut[col][++k] = (int)gs.size();
+            cut[col][ncta] = (int)gs.size();
+        }
+        slot_cap = (int)*std::max_element(slots.begin(), slots.end());
+        grp_cap = (int)std::max<long long>(1, *std::max_element(grps.begin(), grps.end()));
+    };
+    auto smem_of = [&](bool repl, int slot_cap, int grp_cap) {
+        ResSmem<R> L{(int)c->nkinds, (int)c->n, slot_cap, grp_cap, c->ncolors, repl};
+        return L.total();
+    };
+    std::vector<std::vector<int>> cut;
+    int slot_cap = 0, grp_cap = 0, mode = 0, ncta = 0;
+    const size_t budget = (size_t)smem_max - 2048;
+    if (want != "glob") {
+        for (int cl : {16, 8}) {
+            plan(cl, cut, slot_cap, grp_cap);
+            if (smem_of(true, slot_cap, grp_cap) > budget) continue;
+            auto k = (c->vmat.p && c->uniform_mat) ? k_step_resident<R, true, true> : k_step_resident<R, false, true>;
+            const size_t sm = smem_of(true, slot_cap, grp_cap);
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            if (cl > 8) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(cl);
+            cfg.blockDim = dim3(VBD_RES_THREADS);
+            cfg.dynamicSmemBytes = sm;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, k, &cfg) != cudaSuccess || nclusters < 1) {
+                cudaGetLastError();
+                continue;
+            }
+            mode = 1;
+            ncta = cl;
+            break;
+        }
+    }
+    if (!mode && (want == "glob")) {
+        ncta = sms;
+        plan(ncta, cut, slot_cap, grp_cap);
+        const size_t sm = smem_of(false, slot_cap, grp_cap);
+        if (sm <= budget) {
+            auto k = (c->vmat.p && c->uniform_mat) ? k_step_resident<R, true, false> : k_step_resident<R, false, false>;
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            int per = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, VBD_RES_THREADS, sm));
+            if (per >= 1) mode = 2;
+        }
+    }
+    if (!mode) return;
+    // per-CTA arrays
+    std::vector<int4> slots;
+    std::vector<long long> slot_beg(ncta + 1, 0);
+    std::vector<ResGroup> groups;
+    std::vector<int> grp_beg(ncta + 1, 0), col_grp((size_t)ncta * (c->ncolors + 1), 0);
+    const int nk = (int)c->nkinds, npad = (int)c->n;
+    for (int k = 0; k < ncta; ++k) {
+        slot_beg[k] = (long long)slots.size();
+        grp_beg[k] = (int)groups.size();
+        int sb = 0;
+        for (int col = 0; col < c->ncolors; ++col) {
+            col_grp[(size_t)k * (c->ncolors + 1) + col] = (int)groups.size() - grp_beg[k];
+            for (int i = cut[col][k]; i < cut[col][k + 1]; ++i) {
+                const G& g = cg[col][i];
+                groups.push_back(ResGroup{g.v0, g.nv, sb, g.rounds});
+                for (int r = 0; r < g.rounds; ++r)
+                    for (int lane = 0; lane < 32; ++lane) {
+                        const int vi = lane & 7, j = lane >> 3, pos = 4 * r + j;
+                        int4 sl = make_int4(npad, npad, npad, nk);
+                        if (vi < g.nv) {
+                            const long long e0 = eoff[g.v0 + vi], d = eoff[g.v0 + vi + 1] - e0;
+                            if (pos < d) sl = ent[(size_t)(e0 + pos)];
+                        }
+                        slots.push_back(sl);
+                    }
+                sb += 32 * g.rounds;
+            }
+        }
+        col_grp[(size_t)k * (c->ncolors + 1) + c->ncolors] = (int)groups.size() - grp_beg[k];
+    }
+    slot_beg[ncta] = (long long)slots.size();
+    grp_beg[ncta] = (int)groups.size();
+    if (slots.empty()) slots.push_back(make_int4(npad, npad, npad, nk));
+    upload(c->res_slots, slots.data(), slots.size(), s);
+    upload(c->res_slot_beg, slot_beg.data(), slot_beg.size(), s);
+    upload(c->res_groups, groups.data(), std::max<size_t>(groups.size(), 1), s);
+    upload(c->res_grp_beg, grp_beg.data(), grp_beg.size(), s);
+    upload(c->res_col_grp, col_grp.data(), col_grp.size(), s);
+    c->res_bar.alloc(16);
+    CK(cudaMemsetAsync(c->res_bar.p, 0, 16, s));
+    CK(cudaStreamSynchronize(s));
+    c->res_mode = mode;
+    c->res_ncta = ncta;
+    c->res_slot_cap = slot_cap;
+    c->res_grp_cap = grp_cap;
+    c->res_smem = smem_of(mode == 1, slot_cap, grp_cap);
+}
+
+template <typename R> void launch_resident(vbd_ctx* c)
+{
+    ResArgs<R> ra;
+    ra.a = k1_args<R>(c, c->cur.eps_det, 0, c->cur.rho == 0.0, 0);
+    ra.s = step_args<R>(c);
+    ra.slots = c->res_slots.as<int4>();
+    ra.slot_beg = c->res_slot_beg.as<long long>();
+    ra.groups = c->res_groups.as<ResGroup>();
+    ra.grp_beg = c->res_grp_beg.as<int>();
+    ra.col_grp = c->res_col_grp.as<int>();
+    ra.ncolors = c->ncolors;
+    ra.n_max = c->cur.n_max;
+    ra.cheb = c->cur.rho != 0.0;
+    ra.omega[0] = ra.omega[1] = 1.0;
+    ra.omegas = c->omega_dev.as<double>();
+    ra.nkinds = (int)c->nkinds;
+    ra.slot_cap = c->res_slot_cap;
+    ra.grp_cap = c->res_grp_cap;
+    ra.bar = c->res_bar.as<unsigned>();
+    ra.ncta = c->res_ncta;
+    const bool um = c->vmat.p && c->uniform_mat;
+    const bool repl = c->res_mode == 1;
+    void (*k)(const ResArgs<R>) = repl ? (um ? k_step_resident<R, true, true> : k_step_resident<R, false, true>)
+                                       : (um ? k_step_resident<R, true, false> : k_step_resident<R, false, false>);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->res_ncta);
+    cfg.blockDim = dim3(VBD_RES_THREADS);
+    cfg.dynamicSmemBytes = c->res_smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    if (repl) {
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = c->res_ncta;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+    } else {
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k, ra));
 }
 
 // one cooperative launch per step (small scenes); see k_step_persistent
@@ -1505,15 +1784,24 @@ template <typename R> void compile_contact_set(vbd_ctx* c, const DBuf& x)
 // (contacts couple vertices of one colour), K3 keeping colliding vertices unblended
 template <typename R> void do_step_contacts(vbd_ctx* c, vbd_step_result* res)
 {
-    detect_dcd<R>(c);
-    compile_contact_set<R>(c, c->xt);
+    Nvtx r0("vbd_step (contacts)");
+    {
+        Nvtx r1("dcd");
+        detect_dcd<R>(c);
+        compile_contact_set<R>(c, c->xt);
+    }
     enqueue_begin<R>(c);
     for (int n = 1; n <= c->cur.n_max; ++n) {
+        Nvtx r1("iteration %d", n);
         if ((n - 1) % c->coll_ncol == 0) {
+            Nvtx r2("ccd");
             detect_ccd<R>(c);
             compile_contact_set<R>(c, c->pos);
         }
-        for (int col = 0; col < c->ncolors; ++col) color_sweep<R>(c, col, n, c->cur.rho == 0.0);
+        for (int col = 0; col < c->ncolors; ++col) {
+            Nvtx r2("colour %d", col);
+            color_sweep<R>(c, col, n, c->cur.rho == 0.0);
+        }
         enqueue_iter_end<R>(c, n);
     }
     enqueue_end<R>(c);
@@ -1542,12 +1830,19 @@ template <typename R> void do_step(vbd_ctx* c, const vbd_step_params* p, int n_s
         read_result(c, res);
         return;
     }
+    ensure_resident<R>(c);
+    if (c->res_mode > 0 && !p->line_search) {  // K1R reads the omega table from the device
+        if (c->omega_dev.bytes < (p->n_max + 1) * sizeof(double)) c->omega_dev.alloc((p->n_max + 1) * sizeof(double));
+        CK(cudaMemcpyAsync(c->omega_dev.p, c->omegas.data(), (p->n_max + 1) * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+    }
     GraphKey key{*p};
     if (!c->gexec || !(key == c->gkey)) {
         if (c->gexec) {
             cudaGraphExecDestroy(c->gexec);
             c->gexec = nullptr;
         }
+        Nvtx r("vbd_step capture");
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         enqueue_step<R>(c);
@@ -1557,29 +1852,38 @@ template <typename R> void do_step(vbd_ctx* c, const vbd_step_params* p, int n_s
         cudaGraphDestroy(g);
         c->gkey = key;
     }
-    for (int k = 0; k < n_steps; ++k) CK(cudaGraphLaunch(c->gexec, s));
+    for (int k = 0; k < n_steps; ++k) {
+        Nvtx r("vbd_step graph (n_max %d, %d colours)", p->n_max, c->ncolors);
+        CK(cudaGraphLaunch(c->gexec, s));
+    }
     read_result(c, res);
 }
 
 // ---------------------------------------------------------------------------------------
 // state transfer
 
-template <typename R> void load_vec(vbd_ctx* c, const double* host, DBuf& dst)
+// rest positions to subtract / add for a position-like vector (fp32 displacement state)
+inline const double4* rest_for(const vbd_ctx* c, bool position)
+{
+    return c->disp && position ? const_cast<DBuf&>(c->rest).as<double4>() : nullptr;
+}
+
+template <typename R> void load_vec(vbd_ctx* c, const double* host, DBuf& dst, bool position)
 {
     cudaStream_t s = c->stream;
     CK(cudaMemcpyAsync(c->stage.p, host, c->n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
     k_load_vec<R><<<blocks_for(c->n), 256, 0, s>>>(c->stage.as<double>(),
                                                    dst.as<typename Vec4<R>::T>(),
-                                                   c->perm.as<int>(), (int)c->n);
+                                                   c->perm.as<int>(), (int)c->n, rest_for(c, position));
     CK(cudaGetLastError());
 }
 
-template <typename R> void store_vec(vbd_ctx* c, const DBuf& src, double* host)
+template <typename R> void store_vec(vbd_ctx* c, const DBuf& src, double* host, bool position)
 {
     cudaStream_t s = c->stream;
     k_store_vec<R><<<blocks_for(c->n), 256, 0, s>>>(src.as<typename Vec4<R>::T>(),
                                                     c->stage.as<double>(), c->inv.as<int>(),
-                                                    (int)c->n);
+                                                    (int)c->n, rest_for(c, position));
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(host, c->stage.p, c->n * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1592,10 +1896,11 @@ void do_color_pass(vbd_ctx* c, double* x, const double* x_t, const double* y, do
     typedef typename Vec4<R>::T R4;
     cudaStream_t s = c->stream;
     if (ng <= 0) return;  // _native.pyx:520-521
+    Nvtx r("vbd_color_pass (%lld vertices)", (long long)ng);
     ensure_materials<R>(c, h);
-    load_vec<R>(c, x, c->pos);
-    load_vec<R>(c, x_t, c->xt);
-    load_vec<R>(c, y, c->y);
+    load_vec<R>(c, x, c->pos, true);
+    load_vec<R>(c, x_t, c->xt, true);
+    load_vec<R>(c, y, c->y, true);
     k_fill_mih2<R><<<blocks_for(c->n), 256, 0, s>>>(c->y.as<R4>(), c->mass.as<R>(), (int)c->n, h * h);
     // group (original ids) -> colour-major ids
     std::vector<int> gi(ng);
@@ -1621,15 +1926,21 @@ void do_color_pass(vbd_ctx* c, double* x, const double* x_t, const double* y, do
     a.out = odev.as<R4>();
     launch_k1<R>(c, a, s);
     CK(cudaGetLastError());
-    std::vector<R4> ho(ng);
-    CK(cudaMemcpyAsync(ho.data(), odev.p, ng * c->r4(), cudaMemcpyDeviceToHost, s));
+    // the group's new rows in double (+ the rest positions in the displacement state)
+    DBuf o64;
+    o64.alloc((size_t)ng * 24);
+    k_group_abs<R><<<blocks_for(ng), 256, 0, s>>>(odev.as<R4>(), gdev.as<int>(), rest_for(c, true), (int)ng,
+                                                  o64.as<double>());
+    CK(cudaGetLastError());
+    std::vector<double> ho(3 * ng);
+    CK(cudaMemcpyAsync(ho.data(), o64.p, ng * 24, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     // merge (_native.pyx:585-589): only the group's rows change
     for (int64_t k = 0; k < ng; ++k) {
         int64_t v = group[k];
-        x[3 * v] = (double)ho[k].x;
-        x[3 * v + 1] = (double)ho[k].y;
-        x[3 * v + 2] = (double)ho[k].z;
+        x[3 * v] = ho[3 * k];
+        x[3 * v + 1] = ho[3 * k + 1];
+        x[3 * v + 2] = ho[3 * k + 2];
     }
 }
 
@@ -1748,6 +2059,7 @@ int material_id(vbd_ctx* c, std::map<MaterialKey, int>& ids, const MaterialKey& 
 
 void init_ctx(vbd_ctx* c, int device, int precision)
 {
+    if (const char* e = getenv("VBD_RESIDENT")) c->res_want = e;
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
         fail(VBD_ERR_NODEVICE, "no CUDA device available (the B200 path has no CPU fallback)");
@@ -1788,7 +2100,7 @@ template <typename R> void set_rest_state(vbd_ctx* c, const Scene& sc)
     for (DBuf* d : {&c->pos, &c->xt, &c->y})
         k_load_vec<R><<<blocks_for(c->n), 256, 0, s>>>(c->stage.as<double>(),
                                                        d->as<typename Vec4<R>::T>(),
-                                                       c->perm.as<int>(), (int)c->n);
+                                                       c->perm.as<int>(), (int)c->n, rest_for(c, true));
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
 }
@@ -2188,6 +2500,8 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
                                                                        : L32.total(c->tile_stages));
         }
         info->entry_bytes = c->compact ? 16 : EntryPlanesBytes(c->precision);
+        info->resident = c->res_mode > 0 ? c->res_mode : 0;
+        info->resident_ctas = c->res_mode > 0 ? c->res_ncta : 0;
     });
 }
 
@@ -2232,17 +2546,17 @@ int vbd_set_state(vbd_ctx* c, const double* x, const double* x_t, const double* 
         if (!c) fail(VBD_ERR_ARG, "NULL ctx");
         CK(cudaSetDevice(c->device));
         if (c->precision == VBD_PREC_F64) {
-            if (x) load_vec<double>(c, x, c->pos);
-            if (x_t) load_vec<double>(c, x_t, c->xt);
-            if (v_t) load_vec<double>(c, v_t, c->vt);
-            if (v_prev) load_vec<double>(c, v_prev, c->vprev);
-            if (y) load_vec<double>(c, y, c->y);
+            if (x) load_vec<double>(c, x, c->pos, true);
+            if (x_t) load_vec<double>(c, x_t, c->xt, true);
+            if (v_t) load_vec<double>(c, v_t, c->vt, false);
+            if (v_prev) load_vec<double>(c, v_prev, c->vprev, false);
+            if (y) load_vec<double>(c, y, c->y, true);
         } else {
-            if (x) load_vec<float>(c, x, c->pos);
-            if (x_t) load_vec<float>(c, x_t, c->xt);
-            if (v_t) load_vec<float>(c, v_t, c->vt);
-            if (v_prev) load_vec<float>(c, v_prev, c->vprev);
-            if (y) load_vec<float>(c, y, c->y);
+            if (x) load_vec<float>(c, x, c->pos, true);
+            if (x_t) load_vec<float>(c, x_t, c->xt, true);
+            if (v_t) load_vec<float>(c, v_t, c->vt, false);
+            if (v_prev) load_vec<float>(c, v_prev, c->vprev, false);
+            if (y) load_vec<float>(c, y, c->y, true);
         }
         CK(cudaStreamSynchronize(c->stream));
     });
@@ -2254,17 +2568,17 @@ int vbd_get_state(vbd_ctx* c, double* x, double* x_t, double* v_t, double* v_pre
         if (!c) fail(VBD_ERR_ARG, "NULL ctx");
         CK(cudaSetDevice(c->device));
         if (c->precision == VBD_PREC_F64) {
-            if (x) store_vec<double>(c, c->pos, x);
-            if (x_t) store_vec<double>(c, c->xt, x_t);
-            if (v_t) store_vec<double>(c, c->vt, v_t);
-            if (v_prev) store_vec<double>(c, c->vprev, v_prev);
-            if (y) store_vec<double>(c, c->y, y);
+            if (x) store_vec<double>(c, c->pos, x, true);
+            if (x_t) store_vec<double>(c, c->xt, x_t, true);
+            if (v_t) store_vec<double>(c, c->vt, v_t, false);
+            if (v_prev) store_vec<double>(c, c->vprev, v_prev, false);
+            if (y) store_vec<double>(c, c->y, y, true);
         } else {
-            if (x) store_vec<float>(c, c->pos, x);
-            if (x_t) store_vec<float>(c, c->xt, x_t);
-            if (v_t) store_vec<float>(c, c->vt, v_t);
-            if (v_prev) store_vec<float>(c, c->vprev, v_prev);
-            if (y) store_vec<float>(c, c->y, y);
+            if (x) store_vec<float>(c, c->pos, x, true);
+            if (x_t) store_vec<float>(c, c->xt, x_t, true);
+            if (v_t) store_vec<float>(c, c->vt, v_t, false);
+            if (v_prev) store_vec<float>(c, c->vprev, v_prev, false);
+            if (y) store_vec<float>(c, c->y, y, true);
         }
     });
 }
@@ -2286,7 +2600,7 @@ int vbd_set_beam_velocities(vbd_ctx* c, const double* la)
                                                                  c->inv.as<int>(), (int)c->n);
         else
             k_store_vec<float><<<blocks_for(c->n), 256, 0, s>>>(c->xt.as<float4>(), posd.as<double>(),
-                                                                c->inv.as<int>(), (int)c->n);
+                                                                c->inv.as<int>(), (int)c->n, rest_for(c, true));
         k_beam_velocity<<<blocks_for(c->n), 256, 0, s>>>(c->beams_dev.as<BeamDev>(), (int)c->beams.size(),
                                                          dla.as<double>(), posd.as<double>(), c->n,
                                                          vd.as<double>());
@@ -2330,7 +2644,8 @@ int vbd_set_fixed_targets(vbd_ctx* c, int64_t n, const int64_t* idx, const doubl
                                                                        c->xt.as<double4>(), c->pos.as<double4>());
         else
             k_set_targets<float><<<blocks_for(n), 256, 0, c->stream>>>(did.as<int>(), dxyz.as<double>(), (int)n,
-                                                                      c->xt.as<float4>(), c->pos.as<float4>());
+                                                                      c->xt.as<float4>(), c->pos.as<float4>(),
+                                                                      rest_for(c, true));
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(c->stream));
     });
@@ -2406,6 +2721,7 @@ int vbd_step_begin(vbd_ctx* c, const vbd_step_params* p)
 int vbd_step_color(vbd_ctx* c, int32_t color, int32_t iter)
 {
     return guarded([&] {
+        Nvtx nv_("colour %d (iteration %d)", (int)color, (int)iter);
         if (!c || !c->in_step) fail(VBD_ERR_ARG, "no step in progress");
         if (color < 0 || color >= c->ncolors) fail(VBD_ERR_ARG, "bad colour");
         if (c->coll_on && color == 0 && (iter - 1) % c->coll_ncol == 0) {  // CCD (solver.py:308-309)
@@ -2693,6 +3009,7 @@ int vbd_set_contacts(vbd_ctx* c, int64_t count, const int64_t* idx, const double
         if (count < 0) fail(VBD_ERR_ARG, "negative contact count");
         c->ncontacts = 0;
         if (count == 0) return;
+        to_absolute(c);
         if (!idx || !gamma || !refresh || !normal || !tangent || !k_c || !cv_off || !cv_cid || !cv_slot)
             fail(VBD_ERR_ARG, "missing contact arrays");
         if (!(eps_v > 0.0) || mu_c < 0.0) fail(VBD_ERR_ARG, "bad friction parameters");
@@ -2776,6 +3093,7 @@ int vbd_set_collision(vbd_ctx* c, int64_t ntri, const int64_t* tris, int64_t ned
             c->gexec = nullptr;
         }
         if (ntri <= 0) return;
+        to_absolute(c);
         if (!tris || (nedge > 0 && !edges)) fail(VBD_ERR_ARG, "missing surface arrays");
         if (!(cell > 0.0) || !(k_c > 0.0) || mu_c < 0.0 || !(eps_v > 0.0) || dcd_radius < 0.0 || n_col < 1)
             fail(VBD_ERR_ARG, "bad contact parameters");
@@ -2955,6 +3273,7 @@ void descend_impl(vbd_ctx* c, int method, int n_iters, double h, double rho, dou
                   double* g, double* wall_ms)
 {
     typedef typename Vec4<R>::T R4;
+    Nvtx nv_("vbd_descend (method %d, %d iterations)", method, n_iters);
     cudaStream_t s = c->stream;
     const size_t vb = (size_t)c->n * c->r4();
     ensure_materials<R>(c, h);

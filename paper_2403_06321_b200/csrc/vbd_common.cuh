@@ -64,8 +64,53 @@ __device__ __forceinline__ float volume_from_rows(const float* w)
     return __fdividef(1.0f / 6.0f, fabsf(d));
 }
 
+// fp32 displacement state: positions are stored as u = x - X (rest), so an
+// edge is e_j = E_j + (u_nj - u_i) with the REST edges E = W^-1 (F = E W = I at rest; column
+// j of W^-1 is (w_{j+1} x w_{j+2}) / det W over the entry's three other slot rows).  E is a
+// function of the fp32 rows only -- computed in double, rounded once, with every operation
+// pinned -- so the kind table (k_kind_edges) and the explicit layout (per entry) agree bitwise.
+// out: E_0 (xyz), E_1, E_2 as 3 float4 (w = 0).
+__device__ __forceinline__ void rest_edges_from_rows(const float* w, float4* out)
+{
+    double r[3][3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) r[j][c] = (double)w[3 * j + c];
+    double cr[3][3];  // cr[j] = r[j+1] x r[j+2]
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const double* a = r[(j + 1) % 3];
+        const double* b = r[(j + 2) % 3];
+        cr[j][0] = __fma_rn(a[1], b[2], -__dmul_rn(a[2], b[1]));
+        cr[j][1] = __fma_rn(a[2], b[0], -__dmul_rn(a[0], b[2]));
+        cr[j][2] = __fma_rn(a[0], b[1], -__dmul_rn(a[1], b[0]));
+    }
+    const double det = __fma_rn(r[0][2], cr[0][2], __fma_rn(r[0][1], cr[0][1], __dmul_rn(r[0][0], cr[0][0])));
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+        out[j] = make_float4(__double2float_rn(__ddiv_rn(cr[j][0], det)), __double2float_rn(__ddiv_rn(cr[j][1], det)),
+                             __double2float_rn(__ddiv_rn(cr[j][2], det)), 0.0f);
+}
+
+// e_j = E_j + (p_j - x_i) (displacement state, has) or p_j - x_i (absolute state)
+template <typename R>
+__device__ __forceinline__ void edge3(const typename Vec4<R>::T& p, const R* xi, const float4& ex, bool has, R* e)
+{
+    e[0] = p.x - xi[0];
+    e[1] = p.y - xi[1];
+    e[2] = p.z - xi[2];
+    if (has) {
+        e[0] = (R)ex.x + e[0];
+        e[1] = (R)ex.y + e[1];
+        e[2] = (R)ex.z + e[2];
+    }
+}
+
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 
 template <typename R> struct Entry;
 
@@ -386,12 +431,15 @@ struct AccXY {
 };
 
 __device__ __forceinline__ void tet_contrib_ec_xy(float4 p0, float4 p1, float4 p2, float2 nxy, float nz,
+                                                  float4 x0, float4 x1, float4 x2,
                                                   const float* __restrict__ t, AccXY& A)
 {
-    // edges e_k = p_k - x_i
-    const float2 e0 = add2(make_float2(p0.x, p0.y), nxy), e1 = add2(make_float2(p1.x, p1.y), nxy),
-                 e2 = add2(make_float2(p2.x, p2.y), nxy);
-    const float e0z = p0.z + nz, e1z = p1.z + nz, e2z = p2.z + nz;
+    // edges e_k = E_k + (u_k - u_i): rest edge x0..x2 plus the displacement difference (the
+    // fp32 displacement state, edge3 / rest_edges_from_rows)
+    const float2 e0 = add2(make_float2(x0.x, x0.y), add2(make_float2(p0.x, p0.y), nxy)),
+                 e1 = add2(make_float2(x1.x, x1.y), add2(make_float2(p1.x, p1.y), nxy)),
+                 e2 = add2(make_float2(x2.x, x2.y), add2(make_float2(p2.x, p2.y), nxy));
+    const float e0z = x0.z + (p0.z + nz), e1z = x1.z + (p1.z + nz), e2z = x2.z + (p2.z + nz);
     // u = t3 e1 - t4 e0
     const float2 u = fma2(bc2(t[3]), e1, mul2(bc2(-t[4]), e0));
     const float uz = __fmaf_rn(t[3], e1z, -__fmul_rn(t[4], e0z));

@@ -19,6 +19,11 @@ template <typename R> struct K1Args {
     long long E;             // plane stride (entries)
     const PL* kinds;         // compact layout: kind table (KindRec); nullptr = explicit
     const R* vsv;            // one material per vertex: sum of V mu |w|^2 over its entries
+    // fp32 displacement state (positions are x - X_rest): compact layout, the rest
+    // edges of each kind (3 float4, k_kind_edges); explicit layout (disp), from the rows per
+    // entry.  nullptr / 0: absolute positions (fp64, or fp32 after contacts were enabled)
+    const float4* kedge;
+    int disp;
     int max_deg;             // (host) max entries of one vertex: bulk-staging smem bound
     const long long* off;    // entry offsets of free vertices (nfree + 1)
     R4* pos;                 // current iterate x (in place)
@@ -354,6 +359,28 @@ __device__ void subspace_solve(const typename Vec4<R>::T* sub3, const R* f, cons
     }
 }
 
+// rest edges of an entry in the fp32 displacement state (kind table, or from the rows of an
+// explicit entry); false = absolute positions
+template <typename R>
+__device__ __forceinline__ bool rest_edges_of(const K1Args<R>& a, int kind, const R* w, float4* ex)
+{
+    if constexpr (sizeof(R) == 4) {
+        if (a.kedge && kind >= 0) {
+            const float4* p = a.kedge + 3LL * kind;
+            ex[0] = __ldg(p);
+            ex[1] = __ldg(p + 1);
+            ex[2] = __ldg(p + 2);
+            return true;
+        }
+        if (a.disp && kind < 0) {
+            rest_edges_from_rows(reinterpret_cast<const float*>(w), ex);
+            return true;
+        }
+    }
+    (void)a; (void)kind; (void)w; (void)ex;
+    return false;
+}
+
 template <typename R, int W>
 __device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int lane, unsigned gmask,
                           const R* p, const typename Vec4<R>::T& y4, int v)
@@ -363,8 +390,10 @@ __device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int 
     for (long long k = beg + lane; k < end; k += W) {
         Entry<R> en;
         R mu, lam, gamma;
+        int ek_kind = -1;
         if (a.kinds) {
             const EntryK ek = EntryK::load(reinterpret_cast<const int4*>(a.ent), k);
+            ek_kind = ek.kind;
             R r[KindRec<R>::NR];
             load_kind<R, KindRec<R>::Q>(a.kinds, ek.kind, r);
 #pragma unroll
@@ -379,9 +408,12 @@ __device__ R local_energy(const K1Args<R>& a, long long beg, long long end, int 
             mu = m.mu; lam = m.lam; gamma = m.gamma;
         }
         const R4 q0 = a.pos[en.n[0]], q1 = a.pos[en.n[1]], q2 = a.pos[en.n[2]];
-        const R e0[3] = {q0.x - p[0], q0.y - p[1], q0.z - p[2]};
-        const R e1[3] = {q1.x - p[0], q1.y - p[1], q1.z - p[2]};
-        const R e2[3] = {q2.x - p[0], q2.y - p[1], q2.z - p[2]};
+        float4 ex[3];
+        const bool has = rest_edges_of<R>(a, ek_kind, en.w, ex);
+        R e0[3], e1[3], e2[3];
+        edge3<R>(q0, p, ex[0], has, e0);
+        edge3<R>(q1, p, ex[1], has, e1);
+        edge3<R>(q2, p, ex[2], has, e2);
         R F[9];
 #pragma unroll
         for (int r = 0; r < 3; ++r)
@@ -438,9 +470,12 @@ __device__ __forceinline__ void k1_accumulate_explicit(const K1Args<R>& a, long 
         for (int u = 0; u < U; ++u) {
             const long long k = k0 + (long long)u * W;
             if (u == 0 || k < end) {
-                const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
-                const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
-                const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
+                float4 ex[3];
+                const bool has = rest_edges_of<R>(a, -1, e[u].w, ex);
+                R e0[3], e1[3], e2[3];
+                edge3<R>(p[u][0], xi, ex[0], has, e0);
+                edge3<R>(p[u][1], xi, ex[1], has, e1);
+                edge3<R>(p[u][2], xi, ex[2], has, e2);
                 const Material<R> m = UM ? mv : a.mat[e[u].mat];
                 R t[9];
                 ec_terms<R>(e[u].w, e[u].V, m.mu, m.lam, m.gamma, t);
@@ -492,9 +527,12 @@ __device__ __forceinline__ void k1_accumulate_compact(const K1Args<R>& a, long l
             if (u == 0 || k < end) {
                 R r[KindRec<R>::HOT];
                 load_kind<R, KindRec<R>::QH>(a.kinds, e[u].kind, r);
-                const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
-                const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
-                const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
+                float4 ex[3];
+                const bool has = rest_edges_of<R>(a, e[u].kind, r, ex);
+                R e0[3], e1[3], e2[3];
+                edge3<R>(p[u][0], xi, ex[0], has, e0);
+                edge3<R>(p[u][1], xi, ex[1], has, e1);
+                edge3<R>(p[u][2], xi, ex[2], has, e2);
                 tet_contrib_ec<R, !UM>(e0, e1, e2, r, r[9], r[10], dx, f, H, sv);
                 if (UM) {
                     dsc = r[9];
@@ -718,10 +756,11 @@ __global__ void __launch_bounds__(256) k_energy_elastic(const K1Args<R> a, int n
         const int v = g;
         const R4 xi4 = a.pos[v];
         for (long long k = a.off[v] + lane; k < a.off[v + 1]; k += W) {
-            int n[3];
+            int n[3], kind = -1;
             R w[9], V, mu, lam, gamma;
             if (a.kinds) {
                 const EntryK ek = EntryK::load(reinterpret_cast<const int4*>(a.ent), k);
+                kind = ek.kind;
                 R r[KindRec<R>::NR];
                 load_kind<R, KindRec<R>::Q>(a.kinds, ek.kind, r);
                 for (int j = 0; j < 3; ++j) n[j] = ek.n[j];
@@ -739,10 +778,10 @@ __global__ void __launch_bounds__(256) k_energy_elastic(const K1Args<R> a, int n
             for (int j = 0; j < 3; ++j) own = own && (n[j] > v || n[j] >= nsolve);
             if (!own) continue;
             R ed[3][3];
-            for (int j = 0; j < 3; ++j) {
-                const R4 q = a.pos[n[j]];
-                ed[j][0] = q.x - xi4.x; ed[j][1] = q.y - xi4.y; ed[j][2] = q.z - xi4.z;
-            }
+            float4 ex[3];
+            const bool has = rest_edges_of<R>(a, kind, w, ex);
+            const R xi[3] = {xi4.x, xi4.y, xi4.z};
+            for (int j = 0; j < 3; ++j) edge3<R>(a.pos[n[j]], xi, ex[j], has, ed[j]);
             R F[9];
             for (int r = 0; r < 3; ++r)
                 for (int c = 0; c < 3; ++c)
@@ -845,30 +884,34 @@ __device__ __forceinline__ void k2_vertex(const StepArgs<R>& s, int i)
     const R4 xt = s.xt[i], vt = s.vt[i];
     const R h = (R)s.h, hh = (R)s.hh;
     const R ax = (R)s.a[0], ay = (R)s.a[1], az = (R)s.a[2];
+    // every operation rounded separately, in the reference's NumPy order (solver.py:120-164):
+    // no FMA contraction, so K2 gives the same bits wherever it is inlined (k2_step_init, the
+    // persistent and resident step kernels)
     R4 y;
-    y.x = xt.x + h * vt.x + hh * ax;
-    y.y = xt.y + h * vt.y + hh * ay;
-    y.z = xt.z + h * vt.z + hh * az;
+    const R xh[3] = {add_rn(xt.x, mul_rn(h, vt.x)), add_rn(xt.y, mul_rn(h, vt.y)), add_rn(xt.z, mul_rn(h, vt.z))};
+    y.x = add_rn(xh[0], mul_rn(hh, ax));
+    y.y = add_rn(xh[1], mul_rn(hh, ay));
+    y.z = add_rn(xh[2], mul_rn(hh, az));
     y.w = s.mass[i] / hh;
     R4 x = xt;
     x.w = R(0);
     if (i < s.nfree_all) {
         if (s.init_mode == 1 || (s.init_mode == 3 && s.anorm == 0.0)) {
-            x.x = xt.x + h * vt.x;
-            x.y = xt.y + h * vt.y;
-            x.z = xt.z + h * vt.z;
+            x.x = xh[0];
+            x.y = xh[1];
+            x.z = xh[2];
         } else if (s.init_mode == 2) {
             x.x = y.x; x.y = y.y; x.z = y.z;
         } else if (s.init_mode == 3) {
             const R4 vp = s.vprev[i];
             R atx = (vt.x - vp.x) / h, aty = (vt.y - vp.y) / h, atz = (vt.z - vp.z) / h;
-            R comp = atx * (R)s.an[0] + aty * (R)s.an[1] + atz * (R)s.an[2];
+            R comp = add_rn(add_rn(mul_rn(atx, (R)s.an[0]), mul_rn(aty, (R)s.an[1])), mul_rn(atz, (R)s.an[2]));
             R at = comp / (R)s.anorm;
             at = at < R(0) ? R(0) : (at > R(1) ? R(1) : at);
-            R sc = hh * at;
-            x.x = xt.x + h * vt.x + sc * ax;
-            x.y = xt.y + h * vt.y + sc * ay;
-            x.z = xt.z + h * vt.z + sc * az;
+            R sc = mul_rn(hh, at);
+            x.x = add_rn(xh[0], mul_rn(sc, ax));
+            x.y = add_rn(xh[1], mul_rn(sc, ay));
+            x.z = add_rn(xh[2], mul_rn(sc, az));
         }
     } else if (s.flag && !finite3(x.x, x.y, x.z)) {  // fixed vertices never pass through K1
         atomicMin(s.flag, StepFlag::key((unsigned)*s.stepctr, 1u, (unsigned)s.perm[i]));
@@ -898,6 +941,30 @@ __global__ void k2_step_init(const StepArgs<R> s)
     if (i < s.n) k2_vertex<R>(s, i);
 }
 
+// x <- omega (x - x_pp) + x_pp (solver.py:221-232); shared by K3 and the resident step kernel
+template <typename R>
+__device__ __forceinline__ typename Vec4<R>::T k3_blend(typename Vec4<R>::T x, typename Vec4<R>::T pp, double omega)
+{
+    const R w = (R)omega;  // omega (x - x_pp) + x_pp, rounded per operation (no contraction)
+    x.x = add_rn(mul_rn(w, x.x - pp.x), pp.x);
+    x.y = add_rn(mul_rn(w, x.y - pp.y), pp.y);
+    x.z = add_rn(mul_rn(w, x.z - pp.z), pp.z);
+    return x;
+}
+
+// v = (x - x_t) / h (solver.py:319-323); shared by K4 and the resident step kernel
+template <typename R>
+__device__ __forceinline__ typename Vec4<R>::T k4_velocity(typename Vec4<R>::T x, typename Vec4<R>::T x0, double h)
+{
+    const R hr = (R)h;
+    typename Vec4<R>::T v;
+    v.x = (x.x - x0.x) / hr;
+    v.y = (x.y - x0.y) / hr;
+    v.z = (x.z - x0.z) / hr;
+    v.w = R(0);
+    return v;
+}
+
 // K3: Chebyshev semi-iterative blend against the iterate two sweeps back, then copy the
 // blended iterate into the history buffer that becomes x_prev1 (solver.py:221-232, 312-315),
 // then the non-finite check of solver.py:282-288.
@@ -910,11 +977,7 @@ __device__ __forceinline__ void k3_vertex(typename Vec4<R>::T* pos, typename Vec
     typedef typename Vec4<R>::T R4;
     R4 x = pos[i];
     if (blend && !(coll && coll[i])) {  // colliding vertices keep x (solver.py:229-230)
-        const R4 pp = hist[i];
-        const R w = (R)omega;
-        x.x = w * (x.x - pp.x) + pp.x;
-        x.y = w * (x.y - pp.y) + pp.y;
-        x.z = w * (x.z - pp.z) + pp.z;
+        x = k3_blend<R>(x, hist[i], omega);
         pos[i] = x;
     }
     hist[i] = x;
@@ -942,12 +1005,7 @@ __device__ __forceinline__ void k4_vertex(typename Vec4<R>::T* pos, typename Vec
 {
     typedef typename Vec4<R>::T R4;
     const R4 x = pos[i], x0 = xt[i], v0 = vt[i];
-    const R hr = (R)h;
-    R4 v;
-    v.x = (x.x - x0.x) / hr;
-    v.y = (x.y - x0.y) / hr;
-    v.z = (x.z - x0.z) / hr;
-    v.w = R(0);
+    const R4 v = k4_velocity<R>(x, x0, h);
     vprev[i] = v0;
     vt[i] = v;
     xt[i] = x;
@@ -1019,46 +1077,111 @@ __global__ void __launch_bounds__(256, 3) k_step_persistent(const PersistArgs<R>
 // ---------------------------------------------------------------------------------------
 // state transfer: original-order (N,3) float64 <-> colour-major R4
 
+// rest: colour-major rest positions (fp32 displacement state: position-like vectors are
+// stored as x - X); nullptr for velocities and absolute states
 template <typename R>
 __global__ void k_load_vec(const double* __restrict__ src, typename Vec4<R>::T* dst,
-                           const int* __restrict__ perm, int n)
+                           const int* __restrict__ perm, int n, const double4* __restrict__ rest = nullptr)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     long long o = perm[i];
+    double x = src[3 * o], y = src[3 * o + 1], z = src[3 * o + 2];
+    if (rest) {
+        const double4 r = rest[i];
+        x -= r.x;
+        y -= r.y;
+        z -= r.z;
+    }
     typename Vec4<R>::T v;
-    v.x = (R)src[3 * o];
-    v.y = (R)src[3 * o + 1];
-    v.z = (R)src[3 * o + 2];
+    v.x = (R)x;
+    v.y = (R)y;
+    v.z = (R)z;
     v.w = R(0);
     dst[i] = v;
 }
 
 template <typename R>
 __global__ void k_store_vec(const typename Vec4<R>::T* __restrict__ src, double* dst,
-                            const int* __restrict__ inv, int n)
+                            const int* __restrict__ inv, int n, const double4* __restrict__ rest = nullptr)
 {
     int o = blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= n) return;
-    typename Vec4<R>::T v = src[inv[o]];
-    dst[3LL * o] = (double)v.x;
-    dst[3LL * o + 1] = (double)v.y;
-    dst[3LL * o + 2] = (double)v.z;
+    const int i = inv[o];
+    typename Vec4<R>::T v = src[i];
+    double x = (double)v.x, y = (double)v.y, z = (double)v.z;
+    if (rest) {
+        const double4 r = rest[i];
+        x += r.x;
+        y += r.y;
+        z += r.z;
+    }
+    dst[3LL * o] = x;
+    dst[3LL * o + 1] = y;
+    dst[3LL * o + 2] = z;
 }
 
 template <typename R>
 __global__ void k_set_targets(const int* __restrict__ ids, const double* __restrict__ xyz, int n,
-                              typename Vec4<R>::T* xt, typename Vec4<R>::T* pos)
+                              typename Vec4<R>::T* xt, typename Vec4<R>::T* pos,
+                              const double4* __restrict__ rest = nullptr)
 {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
+    double x = xyz[3 * k], y = xyz[3 * k + 1], z = xyz[3 * k + 2];
+    if (rest) {
+        const double4 r = rest[ids[k]];
+        x -= r.x;
+        y -= r.y;
+        z -= r.z;
+    }
     typename Vec4<R>::T v;
-    v.x = (R)xyz[3 * k];
-    v.y = (R)xyz[3 * k + 1];
-    v.z = (R)xyz[3 * k + 2];
+    v.x = (R)x;
+    v.y = (R)y;
+    v.z = (R)z;
     v.w = R(0);
     xt[ids[k]] = v;
     pos[ids[k]] = v;
+}
+
+// aux-buffer results of a group pass in double, absolute (+ rest in the displacement state)
+template <typename R>
+__global__ void k_group_abs(const typename Vec4<R>::T* __restrict__ out, const int* __restrict__ g,
+                            const double4* __restrict__ rest, int ng, double* __restrict__ dst)
+{
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ng) return;
+    const typename Vec4<R>::T v = out[k];
+    double x = (double)v.x, y = (double)v.y, z = (double)v.z;
+    if (rest) {
+        const double4 r = rest[g[k]];
+        x += r.x;
+        y += r.y;
+        z += r.z;
+    }
+    dst[3LL * k] = x;
+    dst[3LL * k + 1] = y;
+    dst[3LL * k + 2] = z;
+}
+
+// colour-major rest positions (double4) from original-order (N, 3)
+__global__ void k_rest_positions(const double* __restrict__ src, const int* __restrict__ perm, int n,
+                                 double4* __restrict__ rest)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long o = perm[i];
+    rest[i] = make_double4(src[3 * o], src[3 * o + 1], src[3 * o + 2], 0.0);
+}
+
+// fp32 displacement state -> absolute (contacts need absolute positions): x = fl32(X + u)
+__global__ void k_disp_to_abs(float4* v, const double4* __restrict__ rest, int n)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 u = v[i];
+    const double4 r = rest[i];
+    v[i] = make_float4((float)(r.x + (double)u.x), (float)(r.y + (double)u.y), (float)(r.z + (double)u.z), u.w);
 }
 
 template <typename R>

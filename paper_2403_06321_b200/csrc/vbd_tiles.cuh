@@ -464,10 +464,18 @@ __device__ __forceinline__ void cp_async_mbar_arrive(unsigned bar)
 template <typename R> struct TileSmem {
     typedef typename Vec4<R>::T R4;
     int ent_cap, nbr_cap, nk, vpt;  // vpt: vertices per tile
-    __host__ __device__ size_t kinds_bytes() const { return (size_t)(nk + 1) * KindRec<R>::HOT * sizeof(R); }
+    // kind records (HOT R each), then for fp32 (displacement state) the kinds' rest edges
+    // (3 float4 = 48 B each: the same byte offset as the fp32 record, in the second table)
+    __host__ __device__ size_t recs_bytes() const { return (size_t)(nk + 1) * KindRec<R>::HOT * sizeof(R); }
+    __host__ __device__ size_t kinds_bytes() const { return recs_bytes() * (sizeof(R) == 4 ? 2 : 1); }
     __host__ __device__ size_t off_hdr() const { return 0; }
     __host__ __device__ size_t off_ent() const { return sizeof(TileDesc); }
+    // neighbour positions, 16-byte units: fp32 one float4 per neighbour; fp64 the (x, y) halves of
+    // all neighbours, then the (z, w) halves (off_nzw), so a quarter-warp LDS.128 of 8 placed
+    // neighbours hits 8 distinct bank groups (a 32-byte double4 stride would reach only 4)
+    static constexpr unsigned PU = 16;
     __host__ __device__ size_t off_npos() const { return off_ent() + (size_t)ent_cap * 8; }
+    __host__ __device__ size_t off_nzw() const { return off_npos() + (size_t)(nbr_cap + 1) * PU; }
     __host__ __device__ size_t off_x() const { return off_npos() + (size_t)(nbr_cap + 1) * sizeof(R4); }
     __host__ __device__ size_t off_xt() const { return off_x() + vpt * sizeof(R4); }
     __host__ __device__ size_t off_y() const { return off_xt() + vpt * sizeof(R4); }
@@ -485,6 +493,14 @@ __device__ __forceinline__ void lds_v(unsigned a, double4& v)
 {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.z), "=d"(v.w) : "r"(a + 16));
+}
+// a staged neighbour position at byte offset a (16-byte units): fp64 reads the (z, w) half
+// from the second array, zw bytes further
+__device__ __forceinline__ void lds_pos(unsigned a, unsigned, float4& v) { lds_v(a, v); }
+__device__ __forceinline__ void lds_pos(unsigned a, unsigned zw, double4& v)
+{
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.z), "=d"(v.w) : "r"(a + zw));
 }
 __device__ __forceinline__ void lds_v(unsigned a, double2& v)
 {
@@ -544,12 +560,22 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
     // chunks the entry loop reads: with one material per vertex the sweep needs t[0..7] only
     // (t[8] = V mu |w|^2 is summed per vertex at pack time, dsc / opd are read once per vertex)
     constexpr int QS = UM ? 8 * (int)sizeof(R) / 16 : QH;
+    constexpr bool DISP = sizeof(R) == 4;  // fp32: displacement state, rest edges per kind
     if (!KG) {
         for (int i = tid; i < ta.nkinds * QH; i += blockDim.x) skind[i] = ta.kinds[(i / QH) * Q + i % QH];
         for (int i = tid; i < QH; i += blockDim.x) skind[ta.nkinds * QH + i] = PL{};  // padding: zero record
+        if constexpr (DISP) {  // 3 float4 per kind (QH == 3 for fp32), same offsets as the records
+            float4* sedge = reinterpret_cast<float4*>(smem + L.recs_bytes());
+            for (int i = tid; i < ta.nkinds * 3; i += blockDim.x) sedge[i] = ta.a.kedge[i];
+            for (int i = tid; i < 3; i += blockDim.x) sedge[ta.nkinds * 3 + i] = float4{};
+        }
     }
     for (int s = 0; s < S; ++s)  // padding: zero position after the largest neighbour list
-        if (tid == 0) *reinterpret_cast<R4*>(stages + s * L.stage_bytes() + L.off_npos() + ta.nbr_cap * sizeof(R4)) = R4{};
+        if (tid == 0) {
+            unsigned char* z = stages + s * L.stage_bytes() + L.off_npos() + (size_t)ta.nbr_cap * L.PU;
+            *reinterpret_cast<float4*>(z) = float4{};
+            if constexpr (sizeof(R4) == 32) *reinterpret_cast<float4*>(z + (L.off_nzw() - L.off_npos())) = float4{};
+        }
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(smem_u32(&full[s]), 33);  // expect_tx arrive + 32 cp.async arrivals
@@ -597,19 +623,16 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                 bulk_g2s(st + L.off_xt(), a.xt + d.v0, vby, bar);
                 bulk_g2s(st + L.off_y(), a.y + d.v0, vby, bar);
             }
-            R4* np = reinterpret_cast<R4*>(st + L.off_npos());
+            unsigned char* np = st + L.off_npos();
             for (int base = 0; ta.dbg != 2;) {
 #pragma unroll
                 for (int q = 0; q < B; ++q) {
                     if (ids[q] < 0) continue;
                     const int i = base + q * 32 + lane;
-                    if constexpr (sizeof(R4) == 16) {
-                        cp_async_n<16>(np + i, a.pos + ids[q]);
-                    } else {
-                        cp_async_n<16>(reinterpret_cast<char*>(np + i), reinterpret_cast<const char*>(a.pos + ids[q]));
-                        cp_async_n<16>(reinterpret_cast<char*>(np + i) + 16,
-                                       reinterpret_cast<const char*>(a.pos + ids[q]) + 16);
-                    }
+                    const char* src = reinterpret_cast<const char*>(a.pos + ids[q]);
+                    cp_async_n<16>(np + (size_t)i * L.PU, src);
+                    if constexpr (sizeof(R4) == 32)  // (z, w) half into the second array
+                        cp_async_n<16>(np + (L.off_nzw() - L.off_npos()) + (size_t)i * L.PU, src + 16);
                 }
                 base += 32 * B;
                 if (base >= d.nl) break;
@@ -704,7 +727,9 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
         const float2 nxy = make_float2(-(float)xi[0], -(float)xi[1]);
         const float nz = -(float)xi[2];
         const unsigned npb = smem_u32(np);
+        const unsigned nzw = (unsigned)(L.off_nzw() - L.off_npos());
         const unsigned kb = smem_u32(skind);
+        const unsigned keb = kb + (unsigned)L.recs_bytes();  // fp32: rest-edge table
         const unsigned sb32 = smem_u32(sent);
         for (int i0 = 0; i0 < rounds; i0 += U) {  // rounds is a multiple of U
             uint2 e[U];
@@ -712,9 +737,19 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 e[u] = lds_u2(sb32 + 256u * (unsigned)(i0 + u));
-                lds_v(npb + (e[u].x & 0xffffu), p[u][0]);
-                lds_v(npb + (e[u].x >> 16), p[u][1]);
-                lds_v(npb + (e[u].y & 0xffffu), p[u][2]);
+                lds_pos(npb + (e[u].x & 0xffffu), nzw, p[u][0]);
+                lds_pos(npb + (e[u].x >> 16), nzw, p[u][1]);
+                lds_pos(npb + (e[u].y & 0xffffu), nzw, p[u][2]);
+            }
+            float4 ex[U][3];  // fp32: the entries' rest edges
+            if constexpr (DISP) {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        if constexpr (KG) ex[u][q] = __ldg(ta.a.kedge + 3 * (size_t)(e[u].y >> 16) + q);
+                        else lds_v(keb + (e[u].y >> 16) + 16u * q, ex[u][q]);
+                    }
             }
             if constexpr (PACK) {  // x/y of every 3-vector packed as fp32x2 (FFMA2)
 #pragma unroll
@@ -731,7 +766,7 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                         r[4 * q + 2] = v.z;
                         r[4 * q + 3] = v.w;
                     }
-                    tet_contrib_ec_xy(p[u][0], p[u][1], p[u][2], nxy, nz, r, acc[u % NA]);
+                    tet_contrib_ec_xy(p[u][0], p[u][1], p[u][2], nxy, nz, ex[u][0], ex[u][1], ex[u][2], r, acc[u % NA]);
                 }
             } else {
 #pragma unroll
@@ -747,9 +782,10 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
 #pragma unroll
                         for (int z = 0; z < 16 / (int)sizeof(R); ++z) r[q * (16 / (int)sizeof(R)) + z] = vr[z];
                     }
-                    const R e0[3] = {p[u][0].x - xi[0], p[u][0].y - xi[1], p[u][0].z - xi[2]};
-                    const R e1[3] = {p[u][1].x - xi[0], p[u][1].y - xi[1], p[u][1].z - xi[2]};
-                    const R e2[3] = {p[u][2].x - xi[0], p[u][2].y - xi[1], p[u][2].z - xi[2]};
+                    R e0[3], e1[3], e2[3];
+                    edge3<R>(p[u][0], xi, ex[u][0], DISP, e0);
+                    edge3<R>(p[u][1], xi, ex[u][1], DISP, e1);
+                    edge3<R>(p[u][2], xi, ex[u][2], DISP, e2);
                     const int b = u % NA;  // i0 is a multiple of U, so (i0 + u) % NA == u % NA (unrolled)
                     tet_contrib_ec<R, !UM>(e0, e1, e2, r, UM ? R(0) : r[9], UM ? R(1) : r[10], dx, fa[b], Ha[b],
                                            sva[b]);

@@ -257,3 +257,20 @@ def test_c5_block_first_step_bit_exact(O, golden):
     st = O.make_state(s)
     O.step(s, st, 1.0 / 240.0, 40, 0.0, G)
     assert np.array_equal(st.x, g["x"][0])
+
+
+def test_fp32_oracle_is_the_same_algorithm_in_binary32(O):
+    """liboracle_f32.so (the fp32 sensitivity yardstick of test_gpu_configs) runs the same
+    restatement in binary32: on a well-conditioned beam pass it agrees with the fp64 oracle to
+    fp32 rounding, and its result is exactly representable in float32."""
+    m, fixed, s = _beam_system(O)
+    rng = np.random.default_rng(3)
+    x0 = s.rest_positions + rng.normal(scale=1e-3, size=s.rest_positions.shape)
+    diag = m.bbox_diagonal()
+    for grp in s.groups():
+        x = x0.copy()
+        O.color_pass(s, x, s.rest_positions, s.rest_positions, 1.0 / 60.0, grp)
+        r = O.color_pass_fp32(s, x0, s.rest_positions, s.rest_positions, 1.0 / 60.0, grp)
+        assert np.array_equal(r.astype(np.float32).astype(np.float64), r)
+        err = np.abs(r - x[grp]).max() / diag
+        assert 0 < err < 1e-5, err
