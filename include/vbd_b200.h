@@ -96,6 +96,9 @@ typedef struct {
     double mu, lam, kd;
     int32_t fix_min_x; /* FixedConstraint on every vertex with (x - origin.x) < 1e-9 */
     int32_t fix_max_x; /* ... and on every vertex of the last x plane (clamped far end) */
+    double jitter;     /* rest positions moved by a deterministic per-vertex offset in
+                          [-jitter, jitter] x spacing (0 = the reference grid; the x = 0 plane
+                          keeps x = 0): an irregular mesh with one rest shape per tet */
 } vbd_beam_desc;
 
 typedef struct {

@@ -46,7 +46,7 @@ class SystemDesc(ctypes.Structure):
 class BeamDesc(ctypes.Structure):
     _fields_ = [("nx", i64), ("ny", i64), ("nz", i64), ("spacing", f64), ("density", f64),
                 ("origin", f64 * 3), ("mu", f64), ("lam", f64), ("kd", f64),
-                ("fix_min_x", i32), ("fix_max_x", i32)]
+                ("fix_min_x", i32), ("fix_max_x", i32), ("jitter", f64)]
 
 
 class StepParams(ctypes.Structure):

@@ -33,6 +33,7 @@ class Beam:
     origin: tuple = (0.0, 0.0, 0.0)
     fix_min_x: bool = False
     fix_max_x: bool = False
+    jitter: float = 0.0  # rest-position jitter, fraction of spacing (irregular mesh; 0 = grid)
 
     def desc(self):
         d = _lib.BeamDesc()
@@ -42,6 +43,7 @@ class Beam:
         d.mu, d.lam, d.kd = self.mu, self.lam, self.kd
         d.fix_min_x = 1 if self.fix_min_x else 0
         d.fix_max_x = 1 if self.fix_max_x else 0
+        d.jitter = float(self.jitter)
         return d
 
     @property

@@ -23,7 +23,18 @@ struct BeamDev {
     int mat;
     int fix_min_x;
     int fix_max_x;
+    double jitter;  // fraction of spacing (vbd_beam_desc::jitter)
 };
+
+// deterministic jitter in [-1, 1) of (global vertex, axis): splitmix64 of the key
+__device__ __forceinline__ double vertex_jitter(unsigned long long key)
+{
+    unsigned long long z = key + 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
 
 __constant__ int c_cell_even[5][4] = {{0, 3, 5, 6}, {1, 0, 3, 5}, {2, 0, 3, 6}, {4, 0, 5, 6}, {7, 3, 5, 6}};
 __constant__ int c_cell_odd[5][4] = {{1, 2, 4, 7}, {0, 1, 2, 4}, {3, 1, 2, 7}, {5, 1, 4, 7}, {6, 2, 4, 7}};
@@ -49,6 +60,13 @@ __global__ void k_gen_vertices(const BeamDev* __restrict__ beams, int nb, long l
     long long az = l % B.nz, ay = (l / B.nz) % B.ny, ax = B.ax0 + l / (B.nz * B.ny);
     // harness.py:50-51: spacing * (ix, iy, iz), then the rigid translation
     double px = B.spacing * (double)ax, py = B.spacing * (double)ay, pz = B.spacing * (double)az;
+    if (B.jitter != 0.0) {  // irregular rest shapes; keyed by the global vertex (slabs agree)
+        const unsigned long long g = (unsigned long long)((ax * B.ny + ay) * B.nz + az) * 3ull;
+        const double a = B.jitter * B.spacing;
+        if (ax > 0) px += a * vertex_jitter(g);
+        py += a * vertex_jitter(g + 1);
+        pz += a * vertex_jitter(g + 2);
+    }
     pos[3 * v] = px + B.origin[0];
     pos[3 * v + 1] = py + B.origin[1];
     pos[3 * v + 2] = pz + B.origin[2];

@@ -253,7 +253,7 @@ struct vbd_ctx {
     std::string res_want;  // VBD_RESIDENT at context creation
     int res_ncta = 0, res_slot_cap = 0, res_grp_cap = 0;
     size_t res_smem = 0;
-    DBuf res_slots, res_slot_beg, res_groups, res_grp_beg, res_col_grp, res_bar;
+    DBuf res_slots, res_slot_beg, res_groups, res_grp_beg, res_col_grp, res_bar, res_push;
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -1379,8 +1379,10 @@ template <typename R> void ensure_resident(vbd_ctx* c)
     std::vector<std::vector<int>> cut;
     int slot_cap = 0, grp_cap = 0, mode = 0, ncta = 0;
     const size_t budget = (size_t)smem_max - 2048;
+    const char* cle = getenv("VBD_RES_CL");  // cluster size (16 or 8; tuning)
+    const int cl_first = cle && atoi(cle) == 8 ? 8 : 16;
     if (want != "glob") {
-        for (int cl : {16, 8}) {
+        for (int cl : {cl_first, 8}) {
             plan(cl, cut, slot_cap, grp_cap);
             if (smem_of(true, slot_cap, grp_cap) > budget) continue;
             auto k = (c->vmat.p && c->uniform_mat) ? k_step_resident<R, true, true> : k_step_resident<R, false, true>;
@@ -1453,12 +1455,34 @@ template <typename R> void ensure_resident(vbd_ctx* c)
     }
     slot_beg[ncta] = (long long)slots.size();
     grp_beg[ncta] = (int)groups.size();
+    // REPL push sets: CTA k reads v if v is one of its vertices, a neighbour of one of them, or
+    // in its K3 / K4 chunk [n k / ncta, n (k + 1) / ncta)  (VBD_RES_PUSH=all: every CTA)
+    std::vector<unsigned short> push((size_t)c->n, 0);
+    const char* pe = getenv("VBD_RES_PUSH");
+    const bool push_all = pe && std::string(pe) == "all";
+    for (int k = 0; k < ncta; ++k) {
+        const unsigned short bit = (unsigned short)(1u << k);
+        const long long lo = c->n * k / ncta, hi = c->n * (k + 1) / ncta;
+        for (long long v = lo; v < hi; ++v) push[v] |= bit;
+        for (int gi = grp_beg[k]; gi < grp_beg[k + 1]; ++gi) {
+            const ResGroup& g = groups[gi];
+            for (int vi = 0; vi < g.nv; ++vi) push[g.v0 + vi] |= bit;
+        }
+        for (long long q = slot_beg[k]; q < slot_beg[k + 1]; ++q) {
+            const int4 sl = slots[q];
+            for (int id : {sl.x, sl.y, sl.z})
+                if (id < npad) push[id] |= bit;
+        }
+    }
+    if (push_all || ncta > 16)
+        for (auto& m : push) m = (unsigned short)((1u << std::min(ncta, 16)) - 1);
     if (slots.empty()) slots.push_back(make_int4(npad, npad, npad, nk));
     upload(c->res_slots, slots.data(), slots.size(), s);
     upload(c->res_slot_beg, slot_beg.data(), slot_beg.size(), s);
     upload(c->res_groups, groups.data(), std::max<size_t>(groups.size(), 1), s);
     upload(c->res_grp_beg, grp_beg.data(), grp_beg.size(), s);
     upload(c->res_col_grp, col_grp.data(), col_grp.size(), s);
+    upload(c->res_push, push.data(), std::max<size_t>(push.size(), 1), s);
     c->res_bar.alloc(16);
     CK(cudaMemsetAsync(c->res_bar.p, 0, 16, s));
     CK(cudaStreamSynchronize(s));
@@ -1489,6 +1513,7 @@ template <typename R> void launch_resident(vbd_ctx* c)
     ra.grp_cap = c->res_grp_cap;
     ra.bar = c->res_bar.as<unsigned>();
     ra.ncta = c->res_ncta;
+    ra.push = c->res_push.as<unsigned short>();
     const bool um = c->vmat.p && c->uniform_mat;
     const bool repl = c->res_mode == 1;
     void (*k)(const ResArgs<R>) = repl ? (um ? k_step_resident<R, true, true> : k_step_resident<R, false, true>)
@@ -2302,6 +2327,8 @@ int vbd_ctx_create_beams(const vbd_beam_desc* beams, int64_t nb, int64_t slab_lo
                 for (int k = 0; k < 3; ++k) B.origin[k] = d.origin[k];
                 B.fix_min_x = d.fix_min_x;
                 B.fix_max_x = d.fix_max_x;
+                if (!(d.jitter >= 0.0 && d.jitter < 0.25)) fail(VBD_ERR_ARG, "beam jitter must be in [0, 0.25)");
+                B.jitter = d.jitter;
                 B.mat = material_id(c, ids, MaterialKey{d.mu, d.lam, d.kd, d.density});
                 if ((int)dens.size() <= B.mat) dens.resize(B.mat + 1, d.density);
                 if (full || !slab) {

@@ -67,30 +67,25 @@ __device__ __forceinline__ float volume_from_rows(const float* w)
 // fp32 displacement state: positions are stored as u = x - X (rest), so an
 // edge is e_j = E_j + (u_nj - u_i) with the REST edges E = W^-1 (F = E W = I at rest; column
 // j of W^-1 is (w_{j+1} x w_{j+2}) / det W over the entry's three other slot rows).  E is a
-// function of the fp32 rows only -- computed in double, rounded once, with every operation
-// pinned -- so the kind table (k_kind_edges) and the explicit layout (per entry) agree bitwise.
-// out: E_0 (xyz), E_1, E_2 as 3 float4 (w = 0).
+// function of the fp32 rows only, in fp32 with every operation pinned, so the kind table
+// (k_kind_edges, once) and the explicit layout (per entry, per pass: ~30 instructions) agree
+// bitwise.  out: E_0 (xyz), E_1, E_2 as 3 float4 (w = 0).
 __device__ __forceinline__ void rest_edges_from_rows(const float* w, float4* out)
 {
-    double r[3][3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) r[j][c] = (double)w[3 * j + c];
-    double cr[3][3];  // cr[j] = r[j+1] x r[j+2]
+    float cr[3][3];  // cr[j] = w_{j+1} x w_{j+2}
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        const double* a = r[(j + 1) % 3];
-        const double* b = r[(j + 2) % 3];
-        cr[j][0] = __fma_rn(a[1], b[2], -__dmul_rn(a[2], b[1]));
-        cr[j][1] = __fma_rn(a[2], b[0], -__dmul_rn(a[0], b[2]));
-        cr[j][2] = __fma_rn(a[0], b[1], -__dmul_rn(a[1], b[0]));
+        const float* a = w + 3 * ((j + 1) % 3);
+        const float* b = w + 3 * ((j + 2) % 3);
+        cr[j][0] = __fmaf_rn(a[1], b[2], -__fmul_rn(a[2], b[1]));
+        cr[j][1] = __fmaf_rn(a[2], b[0], -__fmul_rn(a[0], b[2]));
+        cr[j][2] = __fmaf_rn(a[0], b[1], -__fmul_rn(a[1], b[0]));
     }
-    const double det = __fma_rn(r[0][2], cr[0][2], __fma_rn(r[0][1], cr[0][1], __dmul_rn(r[0][0], cr[0][0])));
+    const float det = __fmaf_rn(w[2], cr[0][2], __fmaf_rn(w[1], cr[0][1], __fmul_rn(w[0], cr[0][0])));
+    const float inv = __fdiv_rn(1.0f, det);
 #pragma unroll
     for (int j = 0; j < 3; ++j)
-        out[j] = make_float4(__double2float_rn(__ddiv_rn(cr[j][0], det)), __double2float_rn(__ddiv_rn(cr[j][1], det)),
-                             __double2float_rn(__ddiv_rn(cr[j][2], det)), 0.0f);
+        out[j] = make_float4(__fmul_rn(cr[j][0], inv), __fmul_rn(cr[j][1], inv), __fmul_rn(cr[j][2], inv), 0.0f);
 }
 
 // e_j = E_j + (p_j - x_i) (displacement state, has) or p_j - x_i (absolute state)

@@ -46,6 +46,8 @@ template <typename R> struct ResArgs {
     int slot_cap, grp_cap;      // max slots / groups of one CTA (shared memory sizing)
     unsigned* bar;              // GLOB: {count, generation}
     int ncta;
+    const unsigned short* push; // REPL: per vertex, the CTAs whose replica must see its updates
+                                // (owners of its neighbours, its own CTA, its K3 / K4 chunk CTA)
 };
 
 // shared memory of one CTA (bytes; every region 16-byte aligned)
@@ -149,6 +151,17 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
     const int gb0 = ra.grp_beg[cta], ng = ra.grp_beg[cta + 1] - gb0;
     for (int i = tid; i < ng; i += blockDim.x) sgrp[i] = ra.groups[gb0 + i];
     for (int i = tid; i <= ra.ncolors; i += blockDim.x) scg[i] = ra.col_grp[cta * (ra.ncolors + 1) + i];
+
+    // push a new position of vertex v into the replicas of the CTAs in m (DSMEM stores); a
+    // colour pass ends with barrier.cluster (release / acquire)
+    auto push_to = [&](unsigned m, int v, const R4& x) {
+        cg::cluster_group cl = cg::this_cluster();
+        while (m) {
+            const int r = __ffs(m) - 1;
+            m &= m - 1;
+            cl.map_shared_rank(rep, r)[v] = x;
+        }
+    };
 
     // ---- K2 over this CTA's elementwise chunk
     const int lo = (int)((long long)n * cta / ncta), hi = (int)((long long)n * (cta + 1) / ncta);
@@ -287,39 +300,48 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
                 nx.x = __shfl_sync(0xffffffffu, nx.x, vi);
                 nx.y = __shfl_sync(0xffffffffu, nx.y, vi);
                 nx.z = __shfl_sync(0xffffffffu, nx.z, vi);
+                if constexpr (REPL) __syncwarp();  // inactive lanes read x of the group's first vertex
                 if (act) {
-                    if constexpr (REPL) {  // lane j pushes to CTAs j, j + 4, ... (DSMEM stores)
-                        cg::cluster_group cl = cg::this_cluster();
-                        for (int r = j; r < ncta; r += 4) cl.map_shared_rank(rep, r)[v] = nx;
+                    if constexpr (REPL) {  // lane j pushes to every 4th CTA of the reader set
+                        push_to(ra.push[v] & (0x1111u << j), v, nx);
                     } else if (j == 0) {
                         stcg4(s.pos + v, nx);
                     }
                 }
             }
-            barrier();
-        }
-        if (ra.cheb) {  // K3 over the elementwise chunk
+            // K3 of this iteration (after its last colour pass): the history copy and the
+            // finite check of the chunk; with a blend it is a pass of its own
             R4* hist = (it % 2 == 1) ? s.hb : s.ha;
-            const double w = ra.omegas[it];
-            const bool blend = it >= 2 && w != 1.0;
-            for (int i = lo + tid; i < hi; i += blockDim.x) {
-                R4 x = xget(i);
-                if (blend) {
-                    x = k3_blend<R>(x, hist[i], w);
-                    if constexpr (REPL) {
-                        cg::cluster_group cl = cg::this_cluster();
-                        for (int r = 0; r < ncta; ++r) cl.map_shared_rank(rep, r)[i] = x;
-                    } else {
-                        stcg4(s.pos + i, x);
-                    }
+            const double w = ra.cheb ? ra.omegas[it] : 1.0;
+            const bool blend = ra.cheb && it >= 2 && w != 1.0;
+            auto k3_copy = [&]() {
+                for (int i = lo + tid; i < hi; i += blockDim.x) {
+                    const R4 x = xget(i);
+                    hist[i] = x;
+                    if (s.flag && !finite3(x.x, x.y, x.z))
+                        atomicMin(s.flag, StepFlag::key((unsigned)*s.stepctr, (unsigned)it, (unsigned)s.perm[i]));
                 }
-                hist[i] = x;
-                if (s.flag && !finite3(x.x, x.y, x.z))
-                    atomicMin(s.flag, StepFlag::key((unsigned)*s.stepctr, (unsigned)it, (unsigned)s.perm[i]));
-            }
+            };
+            const bool copy_here = ra.cheb && !blend && c == ra.ncolors - 1;
             barrier();
+            if (copy_here) {
+                k3_copy();
+                barrier();
+            }
+            if (blend && c == ra.ncolors - 1) {  // K3 blend pass over the elementwise chunk
+                for (int i = lo + tid; i < hi; i += blockDim.x) {
+                    R4 x = k3_blend<R>(xget(i), hist[i], w);
+                    if constexpr (REPL) push_to(ra.push[i], i, x);
+                    else stcg4(s.pos + i, x);
+                    hist[i] = x;
+                    if (s.flag && !finite3(x.x, x.y, x.z))
+                        atomicMin(s.flag, StepFlag::key((unsigned)*s.stepctr, (unsigned)it, (unsigned)s.perm[i]));
+                }
+                barrier();
+            }
         }
     }
+    if constexpr (REPL) cg::this_cluster().sync();  // every flag report and remote store settled
     // ---- K4 (the final iterate is stored either way; the commit only without a non-finite report)
     const bool ok = *reinterpret_cast<volatile unsigned long long*>(s.flag) == StepFlag::NONE;
     for (int i = lo + tid; i < hi; i += blockDim.x) {

@@ -88,6 +88,12 @@ def config(name: str, scale: float = 1.0) -> Config:
         n = max(4, int(round(364 * scale ** (1 / 3))))
         return Config("c5", (Beam(n, n, n, 0.01, 2e6, 2e7, 1e-7, fix_min_x=True),), 1 / 240, 40,
                       sharding="slabs", description=f"generate_beam({n},{n},{n},0.01), x=0 fixed")
+    if name == "c5j":  # C5 with irregular rest shapes: one kind per entry, no entry dictionary
+        n = max(4, int(round(364 * scale ** (1 / 3))))
+        return Config("c5j", (Beam(n, n, n, 0.01, 2e6, 2e7, 1e-7, fix_min_x=True, jitter=0.1),),
+                      1 / 240, 40, sharding="slabs",
+                      description=f"generate_beam({n},{n},{n},0.01) with rest positions jittered "
+                                  "+-10% of the spacing (irregular mesh), x=0 fixed")
     raise ValueError(f"unknown config {name!r}")
 
 

@@ -227,3 +227,29 @@ def test_irregular_mesh_tiles_bitwise(V, O, precision, seed, monkeypatch):
         O.step(s, st, H, 10, 0.9, G)
     tol = 1e-10 if precision == "fp64" else 1e-5
     assert np.abs(a["x"] - st.x).max() / mj.bbox_diagonal() <= tol
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-10), ("fp32", 1e-5)])
+def test_device_generated_jittered_beam_vs_oracle(V, O, precision, tol):
+    """Beam.jitter (the c5j bench scene's irregular rest shapes): every tet its own rest shape,
+    so the entry dictionary overflows and the explicit layout runs (fp32: rest edges from the
+    rows per entry).  Five steps against the oracle built from the device's rest positions."""
+    b = V.Beam(12, 6, 6, 0.05, 2e6, 2e7, 1e-7, fix_min_x=True, jitter=0.1)
+    ctx = V.DeviceContext.from_beams([b], precision=precision)
+    rest = ctx.get_state(x=True)["x"]
+    grid = O.generate_beam(12, 6, 6, 0.05)
+    assert np.abs(rest - grid.rest_positions).max() <= 0.1 * 0.05 + 1e-15
+    assert (rest[:, 0][grid.rest_positions[:, 0] < 1e-9] == 0.0).all()
+    mesh = O.build_tet_mesh(rest, grid.tets, 1000.0)
+    fixed = np.flatnonzero(rest[:, 0] < 1e-9)
+    s = O.build_system([(mesh, (2e6, 2e7, 1e-7))], fixed)
+    assert np.array_equal(ctx.colors(), s.color_of)
+    st = O.make_state(s)
+    p = ctx.step_params(1 / 240, 10, 0.0, 1e-10, "adaptive", G)
+    for _ in range(5):
+        ctx.step(p)
+        O.step(s, st, 1 / 240, 10, 0.0, G)
+    assert ctx.info.layout == 0 or ctx.info.num_entry_kinds > 1000
+    err = np.abs(ctx.get_state(x=True)["x"] - st.x).max() / mesh.bbox_diagonal()
+    assert err <= tol, err
+    ctx.close()
