@@ -145,6 +145,8 @@ typedef struct {
     int32_t resident;          /* K1R whole-step kernel (decided at the first step): 0 none,
                                   1 one cluster with position replicas, 2 grid-resident */
     int32_t resident_ctas;     /* K1R: CTAs (cluster size for 1, SMs for 2) */
+    int64_t contact_graph_steps;     /* contact steps run as one captured graph */
+    int64_t contact_graph_fallbacks; /* ... rolled back and redone on the host path (capacity) */
 } vbd_ctx_info;
 
 /* ---- context ---------------------------------------------------------------------------- */

@@ -237,6 +237,19 @@ struct vbd_ctx {
     long long ndcd = 0, nccd = 0;
     double coll_cell = 1.0, coll_kc = 1.0, coll_dcd_r = 1e-3, coll_max_depth = 0.0;
     int coll_has_max_depth = 0, coll_ncol = 4;
+    // graph-mode contact step (step_contacts_graph): capacities sized from the largest counts
+    // seen on the host-synchronised path (mx_*), sentinel-padded buffers, one graph per step
+    long long mx_cell[3] = {0, 0, 0}, mx_join[2] = {0, 0}, mx_rec[3] = {0, 0, 0};
+    long long cap_cell[3] = {0, 0, 0}, cap_join[2] = {0, 0};
+    bool cg_ready = false, cg_pending = false;
+    bool cg_enabled = true;  // VBD_CONTACT_GRAPH=0 at context creation: host path only
+    long long cg_steps = 0;
+    int cg_fallbacks = 0;  // steps redone on the host path after a capacity overflow
+    cudaGraphExec_t cg_exec = nullptr;
+    GraphKey cg_key{};
+    DBuf cg_cnt, cg_off, cg_key_q, cg_own_q, cg_key_t, cg_own_t, cg_jcnt, cg_joff, cg_codes, cg_codes2,
+        cg_nsel, cg_recs, cg_acc, cg_aoff, cg_tmp, cg_dcd_codes, cg_vt, cg_ee, cg_all, cg_inc, cg_inc2, cg_flag,
+        cg_snap;
     // K1T tile pipeline (compact layout, in-place range passes): tiles of 64 vertices per
     // colour, their neighbour lists and 8-byte entries
     bool tiles = false;
@@ -268,6 +281,7 @@ struct vbd_ctx {
     {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (p2p_gexec) cudaGraphExecDestroy(p2p_gexec);
+        if (cg_exec) cudaGraphExecDestroy(cg_exec);
         for (int s = 0; s < 2; ++s) {
             for (auto& v : halo_send[s])
                 for (auto* b : v) delete b;
@@ -1636,6 +1650,7 @@ template <typename R> long long grid_cells(vbd_ctx* c, const CollArgs<R>& a, int
                                                         own.as<int>());
     CK(cudaGetLastError());
     if (m) sort_pairs_u64_i32(key, own, m, s);
+    c->mx_cell[what] = std::max(c->mx_cell[what], m);
     return m;
 }
 
@@ -1680,6 +1695,7 @@ template <typename R> long long broad_phase(vbd_ctx* c, const CollArgs<R>& a, bo
     CK(cudaGetLastError());
     exclusive_offsets(cnt.as<long long>(), nq, off, s);
     long long m = read_scalar<long long>(off.as<long long>() + nq, s);
+    c->mx_join[ee ? 1 : 0] = std::max(c->mx_join[ee ? 1 : 0], m);
     codes.alloc_on((size_t)std::max<long long>(m, 1) * 8, s);
     if (nq && m) {
         if (ee) k_cell_join<true, true><<<blocks_for(nq), 256, 0, s>>>(qkey, qown, nq, tk.as<unsigned long long>(), to.as<int>(), nt, width, nullptr, off.as<long long>(), codes.as<unsigned long long>());
@@ -1805,6 +1821,286 @@ template <typename R> void compile_contact_set(vbd_ctx* c, const DBuf& x)
     c->mu_c = c->mu_c;
 }
 
+// ---- graph-mode contact step ----------------------------------------------------------------
+// The host path above reads every data-dependent size back (about 8 synchronisations per
+// detection).  Graph mode runs the same kernels at fixed capacities with sentinel-padded
+// tails (vbd_contact.cuh), so DCD, every CCD, the contact-set compile, the colour passes, K3
+// and K4 of a step are ONE captured CUDA graph and the step costs one synchronisation (the
+// result read).  Capacities come from the largest counts the host path has seen (2x + 1024);
+// a step whose counts exceed them raises a device flag, is rolled back (x_t, v_t, v_prev,
+// the step counter) and redone on the host path, which then grows the capacities.
+// Records keep the host path's relative order (DCD, CCD vertex-triangle, CCD edge-edge, each
+// compacted in candidate order), so the per-vertex contact sums -- and the results -- are
+// bitwise those of the host path.  VBD_CONTACT_GRAPH=0 keeps the host path.
+
+struct CgLayout {
+    long long capQ, capT, capJ0, capJ1, capAll;  // sv cells, tri / edge cells, vt / ee candidates
+};
+inline CgLayout cg_layout(const vbd_ctx* c)
+{
+    CgLayout L;
+    L.capQ = std::max<long long>(c->cap_cell[0], 1);
+    L.capT = std::max<long long>(std::max(c->cap_cell[1], c->cap_cell[2]), 1);
+    L.capJ0 = std::max<long long>(c->cap_join[0], 1);
+    L.capJ1 = c->nedge ? std::max<long long>(c->cap_join[1], 1) : 0;
+    L.capAll = 2 * L.capJ0 + L.capJ1;
+    return L;
+}
+
+template <typename R> void cg_setup(vbd_ctx* c)
+{
+    for (int w = 0; w < 3; ++w) c->cap_cell[w] = 2 * c->mx_cell[w] + 1024;
+    for (int w = 0; w < 2; ++w) c->cap_join[w] = 2 * c->mx_join[w] + 1024;
+    const CgLayout L = cg_layout(c);
+    const long long capJ = std::max(L.capJ0, L.capJ1);
+    const long long nprim = std::max<long long>(std::max(c->nsv, c->ntri), std::max(c->nedge, 1));
+    c->cg_cnt.alloc((size_t)nprim * 8);
+    c->cg_off.alloc((size_t)(nprim + 1) * 8);
+    c->cg_key_q.alloc((size_t)L.capQ * 8);
+    c->cg_own_q.alloc((size_t)L.capQ * 4);
+    c->cg_key_t.alloc((size_t)L.capT * 8);
+    c->cg_own_t.alloc((size_t)L.capT * 4);
+    const long long capK = std::max(L.capQ, L.capT);
+    c->cg_jcnt.alloc((size_t)capK * 8);
+    c->cg_joff.alloc((size_t)(capK + 1) * 8);
+    c->cg_codes.alloc((size_t)capJ * 8);
+    c->cg_codes2.alloc((size_t)std::max(capJ, capK) * 8);  // unsorted codes / unsorted cell keys
+    c->cg_nsel.alloc(8);
+    c->cg_recs.alloc((size_t)capJ * sizeof(ContactRec));
+    c->cg_acc.alloc((size_t)std::max(capJ, capK) * 4);     // narrow-phase accept / unsorted owners
+    c->cg_aoff.alloc((size_t)(capJ + 1) * 8);
+    c->cg_dcd_codes.alloc((size_t)L.capJ0 * 8);
+    c->cg_all.alloc((size_t)L.capAll * sizeof(ContactRec));  // [DCD | CCD vt | CCD ee]
+    c->cg_inc.alloc((size_t)4 * L.capAll * 8);
+    c->cg_inc2.alloc((size_t)4 * L.capAll * 8);
+    c->cg_flag.alloc(16);
+    c->cidx.alloc((size_t)L.capAll * sizeof(int4));
+    c->creal.alloc((size_t)L.capAll * 4 * sizeof(typename Vec4<R>::T));
+    c->coff.alloc((size_t)(c->nsolve + 1) * 8);
+    c->ccid.alloc((size_t)4 * L.capAll * 4);
+    c->cslot.alloc((size_t)4 * L.capAll * 4);
+    c->cg_snap.alloc((size_t)3 * c->n * c->r4() + 16);
+    // CUB temporary storage: the largest of every scan / sort / unique of a step
+    size_t mx = 0, tb = 0;
+    const long long nscan = std::max(std::max(nprim, capK), capJ);
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, (const long long*)nullptr, (long long*)nullptr, (int64_t)nscan));
+    mx = std::max(mx, tb);
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, (const int*)nullptr, (long long*)nullptr, (int64_t)nscan));
+    mx = std::max(mx, tb);
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                       (const int*)nullptr, (int*)nullptr, (int64_t)capK, 0, 64));
+    mx = std::max(mx, tb);
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                      (int64_t)std::max(capJ, 4 * L.capAll), 0, 64));
+    mx = std::max(mx, tb);
+    CK(cub::DeviceSelect::Unique(nullptr, tb, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                 (long long*)nullptr, (int64_t)capJ));
+    mx = std::max(mx, tb);
+    c->cg_tmp.alloc(mx);
+    if (c->cg_exec) {
+        cudaGraphExecDestroy(c->cg_exec);
+        c->cg_exec = nullptr;
+    }
+    c->cg_ready = true;
+}
+
+// out[0] = 0, out[1..n] = inclusive sum (capture-safe: preallocated temp, no synchronisation)
+template <typename In> void cg_scan(vbd_ctx* c, const In* in, long long n, long long* out)
+{
+    CK(cudaMemsetAsync(out, 0, 8, c->stream));
+    if (n <= 0) return;
+    size_t tb = c->cg_tmp.bytes;
+    CK(cub::DeviceScan::InclusiveSum(c->cg_tmp.p, tb, in, out + 1, (int64_t)n, c->stream));
+}
+
+// sorted, sentinel-padded cells of primitives `what` (capacity cap) into key / own
+template <typename R>
+void cg_cells(vbd_ctx* c, const CollArgs<R>& a, int what, int n, long long cap, DBuf& key, DBuf& own)
+{
+    cudaStream_t s = c->stream;
+    unsigned long long* kt = c->cg_codes2.as<unsigned long long>();
+    int* ot = c->cg_acc.as<int>();
+    long long* off = c->cg_off.as<long long>();
+    if (n) k_cell_count<R><<<blocks_for(n), 256, 0, s>>>(a, what, n, c->cg_cnt.as<long long>());
+    cg_scan(c, c->cg_cnt.as<long long>(), n, off);
+    if (n) k_cell_emit<R><<<blocks_for(n), 256, 0, s>>>(a, what, n, off, kt, ot, cap);
+    k_sent_tail<<<blocks_for(cap), 256, 0, s>>>(kt, ot, off + n, cap, c->cg_flag.as<int>());
+    size_t tb = c->cg_tmp.bytes;
+    CK(cub::DeviceRadixSort::SortPairs(c->cg_tmp.p, tb, kt, key.as<unsigned long long>(), ot, own.as<int>(),
+                                       (int64_t)cap, 0, 64, s));
+}
+
+// candidate codes (sorted, unique, sentinel tail) of capacity capJ into c->cg_codes
+template <typename R> void cg_broad(vbd_ctx* c, const CollArgs<R>& a, bool ee, long long capJ, const CgLayout& L)
+{
+    cudaStream_t s = c->stream;
+    long long nq, nt;
+    if (ee) {
+        cg_cells<R>(c, a, 2, a.nedge, L.capT, c->cg_key_t, c->cg_own_t);
+        nq = nt = L.capT;
+    } else {
+        cg_cells<R>(c, a, 1, a.ntri, L.capT, c->cg_key_t, c->cg_own_t);
+        cg_cells<R>(c, a, 0, a.nsv, L.capQ, c->cg_key_q, c->cg_own_q);
+        nq = L.capQ;
+        nt = L.capT;
+    }
+    const unsigned long long* qk = (ee ? c->cg_key_t : c->cg_key_q).as<unsigned long long>();
+    const int* qo = (ee ? c->cg_own_t : c->cg_own_q).as<int>();
+    const unsigned long long* tk = c->cg_key_t.as<unsigned long long>();
+    const int* to = c->cg_own_t.as<int>();
+    const long long width = ee ? a.nedge : a.ntri;
+    long long* jc = c->cg_jcnt.as<long long>();
+    long long* jo = c->cg_joff.as<long long>();
+    unsigned long long* raw = c->cg_codes2.as<unsigned long long>();
+    if (ee) k_cell_join<false, true><<<blocks_for(nq), 256, 0, s>>>(qk, qo, nq, tk, to, nt, width, jc, nullptr, nullptr);
+    else k_cell_join<false, false><<<blocks_for(nq), 256, 0, s>>>(qk, qo, nq, tk, to, nt, width, jc, nullptr, nullptr);
+    cg_scan(c, jc, nq, jo);
+    if (ee) k_cell_join<true, true><<<blocks_for(nq), 256, 0, s>>>(qk, qo, nq, tk, to, nt, width, nullptr, jo, raw, capJ);
+    else k_cell_join<true, false><<<blocks_for(nq), 256, 0, s>>>(qk, qo, nq, tk, to, nt, width, nullptr, jo, raw, capJ);
+    k_sent_tail<<<blocks_for(capJ), 256, 0, s>>>(raw, nullptr, jo + nq, capJ, c->cg_flag.as<int>());
+    size_t tb = c->cg_tmp.bytes;
+    unsigned long long* sorted = c->cg_inc2.as<unsigned long long>();  // free until the compile
+    CK(cub::DeviceRadixSort::SortKeys(c->cg_tmp.p, tb, raw, sorted, (int64_t)capJ, 0, 64, s));
+    tb = c->cg_tmp.bytes;
+    CK(cub::DeviceSelect::Unique(c->cg_tmp.p, tb, sorted, c->cg_codes.as<unsigned long long>(),
+                                 c->cg_nsel.as<long long>(), (int64_t)capJ, s));
+    k_sent_tail<<<blocks_for(capJ), 256, 0, s>>>(c->cg_codes.as<unsigned long long>(), nullptr,
+                                                 c->cg_nsel.as<long long>(), capJ, nullptr);
+}
+
+// accepted records (and codes) in candidate order into out (capacity capJ, idx.x = -1 tail)
+inline void cg_compact(vbd_ctx* c, long long capJ, ContactRec* out, unsigned long long* out_codes)
+{
+    cudaStream_t s = c->stream;
+    CK(cudaMemsetAsync(out, 0xff, (size_t)capJ * sizeof(ContactRec), s));
+    cg_scan(c, c->cg_acc.as<int>(), capJ, c->cg_aoff.as<long long>());
+    k_compact<ContactRec><<<blocks_for(capJ), 256, 0, s>>>(c->cg_recs.as<ContactRec>(), c->cg_acc.as<int>(),
+                                                        c->cg_aoff.as<long long>(), capJ, out);
+    if (out_codes) {
+        CK(cudaMemsetAsync(out_codes, 0xff, (size_t)capJ * 8, s));
+        k_compact<unsigned long long><<<blocks_for(capJ), 256, 0, s>>>(c->cg_codes.as<unsigned long long>(),
+                                                                       c->cg_acc.as<int>(), c->cg_aoff.as<long long>(),
+                                                                       capJ, out_codes);
+    }
+}
+
+template <typename R> void cg_detect_dcd(vbd_ctx* c, const CgLayout& L)
+{
+    cudaStream_t s = c->stream;
+    const CollArgs<R> a = coll_args<R>(c, c->xt, c->xt, c->coll_dcd_r);
+    cg_broad<R>(c, a, false, L.capJ0, L);
+    CK(cudaMemsetAsync(c->cg_acc.p, 0, (size_t)L.capJ0 * 4, s));
+    k_dcd_vt<R><<<blocks_for(L.capJ0, 128), 128, 0, s>>>(a, c->cg_codes.as<unsigned long long>(), L.capJ0, c->coll_dcd_r,
+                                                       c->coll_kc, c->coll_has_max_depth, c->coll_max_depth,
+                                                       c->cg_recs.as<ContactRec>(), c->cg_acc.as<int>());
+    ContactRec* all = c->cg_all.as<ContactRec>();
+    cg_compact(c, L.capJ0, all, c->cg_dcd_codes.as<unsigned long long>());
+    CK(cudaMemsetAsync(all + L.capJ0, 0xff, (size_t)(L.capJ0 + L.capJ1) * sizeof(ContactRec), s));  // no CCD yet
+    CK(cudaMemsetAsync(c->ccoll.p, 0, c->n, s));
+}
+
+template <typename R> void cg_detect_ccd(vbd_ctx* c, const CgLayout& L)
+{
+    cudaStream_t s = c->stream;
+    const CollArgs<R> a = coll_args<R>(c, c->xt, c->pos, 0.0);
+    ContactRec* all = c->cg_all.as<ContactRec>();
+    cg_broad<R>(c, a, false, L.capJ0, L);
+    CK(cudaMemsetAsync(c->cg_acc.p, 0, (size_t)L.capJ0 * 4, s));
+    k_ccd_vt<R><<<blocks_for(L.capJ0, 128), 128, 0, s>>>(a, c->cg_codes.as<unsigned long long>(), L.capJ0, c->coll_kc,
+                                                       c->cg_recs.as<ContactRec>(), c->cg_acc.as<int>());
+    k_drop_known<<<blocks_for(L.capJ0), 256, 0, s>>>(c->cg_codes.as<unsigned long long>(), L.capJ0,
+                                                    c->cg_dcd_codes.as<unsigned long long>(), L.capJ0, c->cg_acc.as<int>());
+    cg_compact(c, L.capJ0, all + L.capJ0, nullptr);
+    if (L.capJ1) {
+        cg_broad<R>(c, a, true, L.capJ1, L);
+        CK(cudaMemsetAsync(c->cg_acc.p, 0, (size_t)L.capJ1 * 4, s));
+        k_ccd_ee<R><<<blocks_for(L.capJ1, 128), 128, 0, s>>>(a, c->cg_codes.as<unsigned long long>(), L.capJ1, c->coll_kc,
+                                                           c->cg_recs.as<ContactRec>(), c->cg_acc.as<int>());
+        cg_compact(c, L.capJ1, all + 2 * L.capJ0, nullptr);
+    }
+}
+
+// mark_flags at x and the K1 contact arrays of [DCD | CCD vt | CCD ee] (sentinel records skip)
+template <typename R> void cg_compile(vbd_ctx* c, const DBuf& x, const CgLayout& L)
+{
+    typedef typename Vec4<R>::T R4;
+    cudaStream_t s = c->stream;
+    const long long n = L.capAll;
+    const ContactRec* all = c->cg_all.as<ContactRec>();
+    k_mark_flags<R><<<blocks_for(n), 256, 0, s>>>(all, (int)n, x.as<R4>(), c->ccoll.as<unsigned char>());
+    CK(cudaMemsetAsync(c->cidx.p, 0xff, (size_t)n * sizeof(int4), s));
+    k_pack_contacts<R><<<blocks_for(n), 256, 0, s>>>(all, (int)n, c->cidx.as<int4>(), c->creal.as<R4>(),
+                                                     c->cg_inc.as<unsigned long long>());
+    size_t tb = c->cg_tmp.bytes;
+    CK(cub::DeviceRadixSort::SortKeys(c->cg_tmp.p, tb, c->cg_inc.as<unsigned long long>(),
+                                      c->cg_inc2.as<unsigned long long>(), (int64_t)(4 * n), 0, 64, s));
+    k_contact_csr<<<blocks_for(4 * n), 256, 0, s>>>(c->cg_inc2.as<unsigned long long>(), 4 * n, c->nsolve,
+                                                   c->coff.as<long long>(), c->ccid.as<int>(), c->cslot.as<int>());
+}
+
+template <typename R> void enqueue_step_contacts_graph(vbd_ctx* c)
+{
+    const CgLayout L = cg_layout(c);
+    c->ncontacts = L.capAll;  // padded arrays: K1 aux passes with the contact epilogue
+    cg_detect_dcd<R>(c, L);
+    cg_compile<R>(c, c->xt, L);
+    enqueue_begin<R>(c);
+    for (int n = 1; n <= c->cur.n_max; ++n) {
+        if ((n - 1) % c->coll_ncol == 0) {
+            cg_detect_ccd<R>(c, L);
+            cg_compile<R>(c, c->pos, L);
+        }
+        for (int col = 0; col < c->ncolors; ++col) color_sweep<R>(c, col, n, c->cur.rho == 0.0);
+        enqueue_iter_end<R>(c, n);
+    }
+    enqueue_end<R>(c);
+}
+
+template <typename R> void do_step_contacts(vbd_ctx* c, vbd_step_result* res);
+
+// one contact step as one graph launch; false = the capacities overflowed (state rolled back)
+template <typename R> bool step_contacts_graph(vbd_ctx* c, vbd_step_result* res)
+{
+    cudaStream_t s = c->stream;
+    const size_t vb = (size_t)c->n * c->r4();
+    char* snap = c->cg_snap.as<char>();
+    CK(cudaMemcpyAsync(snap, c->xt.p, vb, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(snap + vb, c->vt.p, vb, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(snap + 2 * vb, c->vprev.p, vb, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(snap + 3 * vb, c->stepctr.p, 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(c->cg_flag.p, 0, 16, s));
+    GraphKey key{c->cur};
+    if (!c->cg_exec || !(key == c->cg_key)) {
+        if (c->cg_exec) {
+            cudaGraphExecDestroy(c->cg_exec);
+            c->cg_exec = nullptr;
+        }
+        Nvtx r("contact step capture");
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        enqueue_step_contacts_graph<R>(c);
+        CK(cudaStreamEndCapture(s, &g));
+        CK(cudaGraphInstantiate(&c->cg_exec, g, 0));
+        cudaGraphDestroy(g);
+        c->cg_key = key;
+    }
+    {
+        Nvtx r("vbd_step contact graph");
+        CK(cudaGraphLaunch(c->cg_exec, s));
+    }
+    const int overflow = read_scalar<int>(c->cg_flag.p, s);
+    if (!overflow) {
+        read_result(c, res);
+        return true;
+    }
+    CK(cudaMemcpyAsync(c->xt.p, snap, vb, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->vt.p, snap + vb, vb, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->vprev.p, snap + 2 * vb, vb, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->stepctr.p, snap + 3 * vb, 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(c->flag.p, 0xff, 8, s));
+    return false;
+}
+
 // one step with contacts: DCD at x_t, CCD every n_col iterations, aux-buffer colour passes
 // (contacts couple vertices of one colour), K3 keeping colliding vertices unblended
 template <typename R> void do_step_contacts(vbd_ctx* c, vbd_step_result* res)
@@ -1844,7 +2140,20 @@ template <typename R> void do_step(vbd_ctx* c, const vbd_step_params* p, int n_s
     CK(cudaMemsetAsync(c->flag.p, 0xff, 8, s));
     CK(cudaMemsetAsync(c->stepctr.p, 0, 4, s));
     if (c->coll_on) {
-        for (int k = 0; k < n_steps; ++k) do_step_contacts<R>(c, res);
+        const bool graph_on = c->cg_enabled;
+        for (int k = 0; k < n_steps; ++k) {
+            if (graph_on && c->cg_pending) {  // (not right after the host step: its contact set
+                cg_setup<R>(c);               //  stays readable by the metrics until the next step)
+                c->cg_pending = false;
+            }
+            if (graph_on && c->cg_ready && step_contacts_graph<R>(c, res)) {
+                ++c->cg_steps;
+                continue;
+            }
+            if (graph_on && c->cg_ready) ++c->cg_fallbacks;
+            do_step_contacts<R>(c, res);  // host path; records the counts the capacities need
+            c->cg_pending = graph_on;
+        }
         return;
     }
     if (use_persistent(c) && !p->line_search) {
@@ -2085,6 +2394,7 @@ int material_id(vbd_ctx* c, std::map<MaterialKey, int>& ids, const MaterialKey& 
 void init_ctx(vbd_ctx* c, int device, int precision)
 {
     if (const char* e = getenv("VBD_RESIDENT")) c->res_want = e;
+    if (const char* e = getenv("VBD_CONTACT_GRAPH")) c->cg_enabled = *e != '0';
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
         fail(VBD_ERR_NODEVICE, "no CUDA device available (the B200 path has no CPU fallback)");
@@ -2529,6 +2839,8 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         info->entry_bytes = c->compact ? 16 : EntryPlanesBytes(c->precision);
         info->resident = c->res_mode > 0 ? c->res_mode : 0;
         info->resident_ctas = c->res_mode > 0 ? c->res_ncta : 0;
+        info->contact_graph_steps = c->cg_steps;
+        info->contact_graph_fallbacks = c->cg_fallbacks;
     });
 }
 
@@ -3118,6 +3430,13 @@ int vbd_set_collision(vbd_ctx* c, int64_t ntri, const int64_t* tris, int64_t ned
         if (c->gexec) {
             cudaGraphExecDestroy(c->gexec);
             c->gexec = nullptr;
+        }
+        c->cg_ready = c->cg_pending = false;
+        for (long long& m : c->mx_cell) m = 0;
+        for (long long& m : c->mx_join) m = 0;
+        if (c->cg_exec) {
+            cudaGraphExecDestroy(c->cg_exec);
+            c->cg_exec = nullptr;
         }
         if (ntri <= 0) return;
         to_absolute(c);

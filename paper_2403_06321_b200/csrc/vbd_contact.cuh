@@ -52,6 +52,12 @@ template <typename R> struct CollArgs {
     double cell, pad;
 };
 
+// Graph mode (one CUDA graph per contact step, vbd_capi.cu step_contacts_graph): every array
+// runs at a fixed capacity and its unused tail holds a SENTINEL (key / code ~0, record idx.x
+// < 0) instead of a host-read count; the kernels below skip sentinels, so the same kernels
+// serve the host-synchronised path (no sentinels) and the captured one.
+#define VBD_SENT 0xffffffffffffffffull
+
 // ---------------------------------------------------------------------------------------
 // broad phase
 
@@ -112,7 +118,7 @@ __global__ void k_cell_count(const CollArgs<R> c, int what, int n, long long* cn
 
 template <typename R>
 __global__ void k_cell_emit(const CollArgs<R> c, int what, int n, const long long* __restrict__ off,
-                            unsigned long long* __restrict__ key, int* __restrict__ own)
+                            unsigned long long* __restrict__ key, int* __restrict__ own, long long cap = 0)
 {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
@@ -127,6 +133,7 @@ __global__ void k_cell_emit(const CollArgs<R> c, int what, int n, const long lon
     for (long long ix = l[0]; ix <= h[0]; ++ix)
         for (long long iy = l[1]; iy <= h[1]; ++iy)
             for (long long iz = l[2]; iz <= h[2]; ++iz, ++w) {
+                if (cap && w >= cap) return;  // graph mode: overflow (flagged by k_sent_tail)
                 key[w] = cell_key(ix, iy, iz);
                 own[w] = p;
             }
@@ -151,21 +158,39 @@ __global__ void k_cell_join(const unsigned long long* __restrict__ qkey, const i
                             long long nq, const unsigned long long* __restrict__ tkey,
                             const int* __restrict__ town, long long nt, long long width,
                             long long* __restrict__ cnt, const long long* __restrict__ off,
-                            unsigned long long* __restrict__ codes)
+                            unsigned long long* __restrict__ codes, long long cap = 0)
 {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= nq) return;
     const unsigned long long k = qkey[i];
+    if (k == VBD_SENT) {  // padding (graph mode)
+        if (!FILL) cnt[i] = 0;
+        return;
+    }
     long long j = lower_key(tkey, nt, k);
     long long c = 0, w = FILL ? off[i] : 0;
     const long long q = qown[i];
     for (; j < nt && tkey[j] == k; ++j) {
         const long long t = town[j];
         if (SELF && !(q < t)) continue;
-        if (FILL) codes[w++] = (unsigned long long)(q * width + t);
+        if (FILL && (!cap || w < cap)) codes[w] = (unsigned long long)(q * width + t);
+        if (FILL) ++w;
         ++c;
     }
     if (!FILL) cnt[i] = c;
+}
+
+// graph mode: the tail [total, cap) of a key array gets the sentinel (and own = -1); a total
+// over the capacity raises the overflow flag (the step is redone on the host path)
+__global__ void k_sent_tail(unsigned long long* __restrict__ key, int* __restrict__ own,
+                            const long long* __restrict__ total, long long cap, int* __restrict__ overflow)
+{
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long t = *total;
+    if (i == 0 && t > cap) atomicExch(overflow, 1);
+    if (i >= cap || i < t) return;
+    key[i] = VBD_SENT;
+    if (own) own[i] = -1;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -258,6 +283,10 @@ __global__ void k_dcd_vt(const CollArgs<R> c, const unsigned long long* __restri
 {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (codes[i] == VBD_SENT) {  // padding (graph mode)
+        acc[i] = 0;
+        return;
+    }
     const long long k = (long long)(codes[i] / (unsigned long long)c.ntri);
     const int t = (int)(codes[i] % (unsigned long long)c.ntri);
     acc[i] = 0;
@@ -418,6 +447,10 @@ __global__ void k_ccd_vt(const CollArgs<R> c, const unsigned long long* __restri
 {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (codes[i] == VBD_SENT) {  // padding (graph mode)
+        acc[i] = 0;
+        return;
+    }
     acc[i] = 0;
     const long long k = (long long)(codes[i] / (unsigned long long)c.ntri);
     const int t = (int)(codes[i] % (unsigned long long)c.ntri);
@@ -469,6 +502,10 @@ __global__ void k_ccd_ee(const CollArgs<R> c, const unsigned long long* __restri
 {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (codes[i] == VBD_SENT) {  // padding (graph mode)
+        acc[i] = 0;
+        return;
+    }
     acc[i] = 0;
     const int e = (int)(codes[i] / (unsigned long long)c.nedge);
     const int o = (int)(codes[i] % (unsigned long long)c.nedge);
@@ -526,6 +563,7 @@ __global__ void k_mark_flags(const ContactRec* __restrict__ recs, int n, const t
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const ContactRec& r = recs[i];
+    if (r.idx.x < 0) return;  // padding (graph mode)
     const int ids[4] = {r.idx.x, r.idx.y, r.idx.z, r.idx.w};
     bool on = r.ccd != 0;
     if (!on) {  // Contact.gap: sep = -(sum_k gamma_k x_k), d = sep . n (contact.py:70-74)
@@ -546,6 +584,10 @@ __global__ void k_pack_contacts(const ContactRec* __restrict__ recs, int n, int4
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const ContactRec& r = recs[i];
+    if (r.idx.x < 0) {  // padding (graph mode): sorts after every real key
+        for (int k = 0; k < 4; ++k) inc[4 * i + k] = VBD_SENT;
+        return;
+    }
     cidx[i] = r.idx;
     typename Vec4<R>::T* o = creal + 4 * i;
     o[0].x = (R)r.g[0]; o[0].y = (R)r.g[1]; o[0].z = (R)r.g[2]; o[0].w = (R)r.g[3];
@@ -563,10 +605,14 @@ __global__ void k_contact_csr(const unsigned long long* __restrict__ keys, long 
 {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= m) return;
-    const long long v = (long long)(keys[i] >> 32);
+    const bool pad = keys[i] == VBD_SENT;  // graph mode: keys of padding records sort last
+    const long long v = pad ? nsolve + 1 : (long long)(keys[i] >> 32);
     const unsigned lo = (unsigned)(keys[i] & 0xffffffffu);
-    cid[i] = (int)(lo >> 2);
-    slot[i] = (int)(lo & 3u);
+    if (!pad) {
+        cid[i] = (int)(lo >> 2);
+        slot[i] = (int)(lo & 3u);
+    }
+    if (pad && i > 0 && keys[i - 1] == VBD_SENT) return;
     // off[v + 1] = index of the first key with vertex > v
     const long long vp = i > 0 ? (long long)(keys[i - 1] >> 32) : -1;
     for (long long u = vp + 1; u <= v && u <= nsolve; ++u) off[u] = i;
@@ -587,7 +633,7 @@ __global__ void __launch_bounds__(256) k_energy_contact(const int4* __restrict__
     __shared__ double red[256], mx[256];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     double e = 0.0, d = 0.0;
-    if (i < n) {
+    if (i < n && cidx[i].x >= 0) {  // (padding records of the graph-mode arrays: idx.x = -1)
         const int4 id = cidx[i];
         const int ids[4] = {id.x, id.y, id.z, id.w};
         const typename Vec4<R>::T g = creal[4 * i], nk = creal[4 * i + 1];

@@ -146,3 +146,38 @@ def test_criterion_10_line_search_descent(V):
     gs = np.array(gs)
     assert (np.diff(gs) <= 1e-9 * np.abs(gs[:-1])).all(), np.diff(gs).max()
     assert gs[-1] < gs[0]
+
+
+def _mass_ratio_scene(V):
+    n = 7
+    light = V.generate_beam(n, n, n, 0.5 / (n - 1), density=10.0)
+    rho_heavy = 2000.0 * light.masses.sum() / 0.4 ** 3
+    heavy0 = V.generate_beam(n, n, n, 0.4 / (n - 1), density=rho_heavy)
+    heavy = V.build_tet_mesh(heavy0.rest_positions + [0.05, 0.05, 0.5005], heavy0.tets, rho_heavy)
+    bottom = np.flatnonzero(light.rest_positions[:, 2] < 1e-9)
+    system = V.build_system([V.Body(light, stiff(V), k_d=0.01), V.Body(heavy, stiff(V), k_d=0.01)],
+                            [V.FixedConstraint(int(i)) for i in bottom])
+    params = V.SolverParams(h=1.0 / 120.0, n_max=25, a_ext=GRAV,
+                            contact=V.ContactParams(k_c=1e7, mu_c=1.0, eps_v=1e-3, dcd_radius=0.008))
+    return system, params
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_contact_step_graph_bitwise_equals_host_path(V, precision, monkeypatch):
+    """The graph-mode contact step (DCD, CCD, contact-set compile, passes, K3, K4 in one
+    captured graph at fixed capacities with sentinel padding) gives the host-synchronised
+    path's trajectory bit for bit, and runs as a graph after the first (capacity-sizing) step."""
+    out = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("VBD_CONTACT_GRAPH", mode)
+        system, params = _mass_ratio_scene(V)
+        params = V.SolverParams(h=params.h, n_max=params.n_max, a_ext=params.a_ext, contact=params.contact,
+                                precision=precision)
+        state = V.make_state(system)
+        for _ in range(60):
+            V.step(state, params)
+        info = state._ctx._info()
+        out.append((state.x.copy(), state.v_t.copy(), int(info.contact_graph_steps)))
+    monkeypatch.delenv("VBD_CONTACT_GRAPH")
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == 0 and out[1][2] >= 50, (out[0][2], out[1][2])
