@@ -471,6 +471,12 @@ def run_ours(args):
     roof = roofline_record(cfg, info, args.precision, k1_ms, k1_reps, local)
     phases = 1 + cfg.n_max * (int(info.num_colors) + (1 if cfg.rho else 0)) + 1
     launches_per_step = phases
+    resident = int(ctx._info().resident)  # decided at the first step (small scenes: K1R)
+    if resident:
+        launches_per_step = 1
+        roof["step_kernel"] = ("k_step_resident (K1R, %s, %d CTAs): the whole step is one launch; the "
+                               "k1 timing above is the per-colour K1T pass of the graph path"
+                               % ("cluster replicas" if resident == 1 else "grid", int(ctx._info().resident_ctas)))
     if exch is not None and args.halo == "p2p":
         launches_per_step = 3 * phases + 1   # + phase wait / signal kernels, epoch advance
     elif exch is not None:

@@ -91,14 +91,26 @@ __global__ void k_gen_tets(const BeamDev* __restrict__ beams, int nb, long long 
     long long cz = cell % ncz, cy = (cell / ncz) % ncy, cx = B.gcell0 + cell / (ncz * ncy);
     const int(*pat)[4] = ((cx + cy + cz) % 2 == 0) ? c_cell_even : c_cell_odd;
     long long vid[4];
+    int cof[4][3];  // the corners' integer cell offsets
     for (int k = 0; k < 4; ++k) {
         int c = pat[j][k];
         int dx = c >> 2, dy = (c >> 1) & 1, dz = c & 1;
+        cof[k][0] = dx;
+        cof[k][1] = dy;
+        cof[k][2] = dz;
         vid[k] = B.vbase + ((cx + dx - B.ax0) * B.ny + (cy + dy)) * B.nz + (cz + dz);
     }
-    double D[9];  // columns = edges x_{k} - x_0, D[a*3+k]
+    // columns = edges x_{k} - x_0, D[a*3+k].  On the regular grid the edges are formed from the
+    // corners' integer offsets times the spacing (exact), not from differences of rounded
+    // absolute positions: every cell of a shape then gets bitwise the same Dm^-1 and V, so an
+    // fp64 grid has 40 entry kinds like fp32 (not ~40,000 last-bit variants).  The reference
+    // differences positions (mesh.py:155-159); the two agree to ~1e-13 relative.  Jittered
+    // meshes (irregular) difference the positions.
+    double D[9];
     for (int k = 0; k < 3; ++k)
-        for (int a = 0; a < 3; ++a) D[a * 3 + k] = pos[3 * vid[k + 1] + a] - pos[3 * vid[0] + a];
+        for (int a = 0; a < 3; ++a)
+            D[a * 3 + k] = B.jitter == 0.0 ? (double)(cof[k + 1][a] - cof[0][a]) * B.spacing
+                                          : pos[3 * vid[k + 1] + a] - pos[3 * vid[0] + a];
     double det = D[0] * (D[4] * D[8] - D[5] * D[7]) - D[1] * (D[3] * D[8] - D[5] * D[6]) +
                  D[2] * (D[3] * D[7] - D[4] * D[6]);
     if (det < 0.0) {  // swap slots 1 and 2: [0, 2, 1, 3]

@@ -1361,7 +1361,7 @@ template <typename R> void ensure_resident(vbd_ctx* c)
                 const long long d = eoff[g.v0 + k + 1] - eoff[g.v0 + k];
                 g.rounds = std::max(g.rounds, (int)((d + 3) / 4));
             }
-            g.rounds = (g.rounds + 1) / 2 * 2;
+            g.rounds = (g.rounds + VBD_RES_U - 1) / VBD_RES_U * VBD_RES_U;
             cg[col].push_back(g);
         }
     // runs of equal work per CTA and colour
@@ -1528,6 +1528,8 @@ template <typename R> void launch_resident(vbd_ctx* c)
     ra.bar = c->res_bar.as<unsigned>();
     ra.ncta = c->res_ncta;
     ra.push = c->res_push.as<unsigned short>();
+    ra.dbg = getenv("VBD_RES_DBG") ? atoi(getenv("VBD_RES_DBG")) : 0;
+    if (ra.dbg) ra.a.flag = ra.s.flag = nullptr;  // (garbage positions in the timing experiments)
     const bool um = c->vmat.p && c->uniform_mat;
     const bool repl = c->res_mode == 1;
     void (*k)(const ResArgs<R>) = repl ? (um ? k_step_resident<R, true, true> : k_step_resident<R, false, true>)

@@ -22,7 +22,8 @@
 
 #include "vbd_kernels.cuh"
 
-#define VBD_RES_THREADS 512  // 16 warps: 16 groups of 8 vertices per round of the CTA's run
+#define VBD_RES_THREADS 512  // 16 warps: 16 groups of 8 vertices in flight per CTA
+#define VBD_RES_U 2          // entries per lane in flight per sweep iteration (rounds padded to it; 4 at 384 threads measured slower: 2.81 vs 2.50 us per C1 pass)
 #define VBD_RES_MAX_COLORS 16
 
 struct ResGroup {
@@ -48,6 +49,8 @@ template <typename R> struct ResArgs {
     int ncta;
     const unsigned short* push; // REPL: per vertex, the CTAs whose replica must see its updates
                                 // (owners of its neighbours, its own CTA, its K3 / K4 chunk CTA)
+    int dbg;                    // timing experiments only (VBD_RES_DBG, wrong results): 1 no DSMEM
+                                // pushes, 2 no entry sweep, 3 neither
 };
 
 // shared memory of one CTA (bytes; every region 16-byte aligned)
@@ -208,18 +211,19 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
                         return id < n ? p : zero4;
                     }
                 };
-                for (int i0 = 0; i0 < g.rounds; i0 += 2) {
-                    int4 e[2];
-                    R4 p[2][3];
+                const int grounds = (ra.dbg & 2) ? 0 : g.rounds;
+                for (int i0 = 0; i0 < grounds; i0 += VBD_RES_U) {
+                    int4 e[VBD_RES_U];
+                    R4 p[VBD_RES_U][3];
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
+                    for (int u = 0; u < VBD_RES_U; ++u) {
                         e[u] = sl[32 * (i0 + u)];
                         p[u][0] = pos_of(e[u].x);
                         p[u][1] = pos_of(e[u].y);
                         p[u][2] = pos_of(e[u].z);
                     }
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
+                    for (int u = 0; u < VBD_RES_U; ++u) {
                         R r[HOT];
                         const unsigned rp = kb + (unsigned)e[u].w * (unsigned)(HOT * sizeof(R));
                         float4 ex[3];
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
                 if constexpr (REPL) __syncwarp();  // inactive lanes read x of the group's first vertex
                 if (act) {
                     if constexpr (REPL) {  // lane j pushes to every 4th CTA of the reader set
-                        push_to(ra.push[v] & (0x1111u << j), v, nx);
+                        push_to((ra.dbg & 1) ? 0u : ra.push[v] & (0x1111u << j), v, nx);
                     } else if (j == 0) {
                         stcg4(s.pos + v, nx);
                     }
@@ -343,7 +347,7 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
     }
     if constexpr (REPL) cg::this_cluster().sync();  // every flag report and remote store settled
     // ---- K4 (the final iterate is stored either way; the commit only without a non-finite report)
-    const bool ok = *reinterpret_cast<volatile unsigned long long*>(s.flag) == StepFlag::NONE;
+    const bool ok = !s.flag || *reinterpret_cast<volatile unsigned long long*>(s.flag) == StepFlag::NONE;
     for (int i = lo + tid; i < hi; i += blockDim.x) {
         const R4 x = xget(i);
         if constexpr (REPL) s.pos[i] = x;

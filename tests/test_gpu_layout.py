@@ -146,9 +146,12 @@ def test_irregular_mesh_falls_back_to_explicit(V, O, monkeypatch):
         assert np.abs(x - st.x).max() / diag <= 1e-5
 
 
-def test_device_generated_c5_like_block_is_compact(V):
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_device_generated_c5_like_block_is_compact(V, precision):
+    """fp64 too: the generator forms grid edges from integer cell offsets, so every cell of a
+    shape has bitwise the same Dm^-1 (40 kinds, the kind table in shared memory)."""
     ctx = V.DeviceContext.from_beams([V.Beam(40, 40, 40, 0.01, 2e6, 2e7, 1e-7, fix_min_x=True)],
-                                     precision="fp32")
+                                     precision=precision)
     assert ctx.info.layout == 1 and ctx.info.num_entry_kinds <= 64
 
 

@@ -1,0 +1,15 @@
+#!/bin/bash
+# round-2 record: whole GPU suite, smoke, bench lines C1..C5 + C5j, ncu launch list of the C5 step,
+# ncu full captures (K1T fp32 C5, explicit K1 C5j, K1R C1)
+O=gpurun_out; mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q > $O/r2v_all.log 2>&1; echo rc=$? >> $O/r2v_all.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $O/r2v_smoke.log 2>&1
+timeout 600 python bench.py > $O/r2v_bench_c5.log 2>&1
+for cfg in c1 c2 c3; do timeout 300 python bench.py --config $cfg --steps 50 --warmup 5 --no-fp64-record > $O/r2v_bench_$cfg.log 2>&1; done
+timeout 900 python bench.py --config c4 --steps 10 --warmup 3 > $O/r2v_bench_c4.log 2>&1
+timeout 900 python bench.py --config c5j --steps 3 --warmup 3 --no-fp64-record > $O/r2v_bench_c5j.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/r2v_launches_c5.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-fp64-record --e2e-steps 1 > $O/r2v_launches_c5.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k1_tiles --launch-skip 4 -c 1 -o $O/r2v_k1t_c5_fp32 python tools/k1_once.py c5 fp32 > $O/r2v_ncu1.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k1_color_pass --launch-skip 4 -c 1 -o $O/r2v_k1_c5j python tools/k1_once.py c5j fp32 > $O/r2v_ncu2.log 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:k_step_resident -c 1 -o $O/r2v_k1r_c1 python bench.py --config c1 --steps 2 --warmup 1 --no-cpu-baseline --no-fp64-record > $O/r2v_ncu3.log 2>&1
+ls -la $O/r2v_* | head -40

@@ -5,8 +5,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2403_06321_b200.scenes import build, config
 
-for mode in ("repl", "0"):
+for mode, dbg in (("repl", "0"), ("repl", "1"), ("repl", "2"), ("0", "0")):
     os.environ["VBD_RESIDENT"] = mode
+    os.environ["VBD_RES_DBG"] = dbg
     cfg = config("c1")
     ctx, _ = build(cfg, precision="fp32")
     stream = torch.cuda.ExternalStream(ctx.stream)
@@ -24,5 +25,5 @@ for mode in ("repl", "0"):
         out.append((n_max, e0.elapsed_time(e1) / 50 * 1e3))
     ns, ts = np.array(out).T
     k, b = np.polyfit(ns, ts, 1)
-    print(mode, " ".join(f"n_max={int(n)}:{t:.1f}us" for n, t in out), f"| slope {k / 4:.2f} us/pass, intercept {b:.1f} us")
+    print(mode, "dbg", dbg, " ".join(f"n_max={int(n)}:{t:.1f}us" for n, t in out), f"| slope {k / 4:.2f} us/pass, intercept {b:.1f} us")
     ctx.close()
