@@ -661,11 +661,12 @@ template <typename R> void build_tiles(vbd_ctx* c)
     // as many stages (2..4) as fit three CTAs per SM, else two (2-lane: 2 stages)
     const char* oe = getenv("VBD_TILE_OCC");
     c->tile_occ = oe && *oe == '2' ? 2 : 3;  // 3 CTAs per SM (one entry per lane in flight) measured faster
+    const bool force_occ3 = oe && *oe == '3';  // (tuning: keep 3 CTAs/SM even above 75 KB)
     const char* de = getenv("VBD_TILE_DEFER");
     c->tile_defer = !(de && *de == '0');
     int stages = 0;
     for (int st = 4; st >= 2 && !stages && c->tile_occ == 3; --st)
-        if (L.total(st) <= 75 * 1024) stages = st;
+        if (L.total(st) <= 75 * 1024 || (force_occ3 && st == 2)) stages = st;
     if (!stages) c->tile_occ = 2;  // e.g. fp64: 32-byte positions
     for (int st = W == 2 ? 2 : 4; st >= 2 && !stages; --st)
         if (L.total(st) <= VBD_TILE_SMEM_MAX) stages = st;

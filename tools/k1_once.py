@@ -26,6 +26,9 @@ def main():
     cfg = config(name)
     ctx, _ = build(cfg, precision=prec)
     ctx.step(cfg.step_params())
+    i = ctx._info()
+    print("tiles", i.tiles, "stages", i.tile_stages, "smem/CTA", i.tile_smem_bytes, "nbr_cap", i.tile_nbr_cap,
+          "ent_cap", i.tile_ent_cap, "kinds", i.num_entry_kinds)
     print("k1 ms per colour:", ctx.profile_color_pass(cfg.h, reps=2))
     ctx.close()
 
