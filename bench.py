@@ -296,8 +296,9 @@ def layout_bytes_per_iteration(info, precision):
     n_all = int(info.num_vertices)
     C = int(info.num_colors)
     other = sum(r4 * (n_all - int(info.color_count[c])) for c in range(min(C, 64)))
-    if int(info.tiles):
-        return (8 * int(info.tile_slots) + 4 * int(info.tile_nbr_refs) + 64 * int(info.tiles)
+    if int(info.tiles):  # K1T; K1T-X (explicit layout) also streams 36 B of rows per slot
+        rows = 36 * int(info.tile_slots) if int(info.layout) == 0 else 0
+        return (8 * int(info.tile_slots) + rows + 4 * int(info.tile_nbr_refs) + 64 * int(info.tiles)
                 + 4 * r4 * n_solved + other)
     return n_solved * (8 + 4 * r4) + int(info.num_entries) * int(info.entry_bytes) + other
 
@@ -599,6 +600,9 @@ def state_checksum(ctx, cfg, part, exch, rank, world):
 
 
 def layout_name(info):
+    if int(info.tiles) and int(info.layout) == 0:
+        return ("K1T-X tiles (irregular mesh, %d lanes/vertex, %d stages): 8 B entry slots + 36 B of "
+                "slot-weight rows per slot streamed, constants derived per entry" % (info.tile_lanes, info.tile_stages))
     if int(info.tiles):
         return ("K1T tiles (%d lanes/vertex, %d stages): 8 B entry slots + %d entry kinds"
                 % (info.tile_lanes, info.tile_stages, info.num_entry_kinds))

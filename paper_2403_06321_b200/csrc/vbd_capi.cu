@@ -260,6 +260,11 @@ struct vbd_ctx {
     int tile_stages = 2, tile_w = 4, tile_occ = 2;
     bool tile_defer = true;  // K1T deferred block solves (VBD_TILE_DEFER=0 disables)
     bool tile_kg = false;    // K1T kind records read from global (table too large for shared memory)
+    // K1T-X (explicit layout, fp32, one material per vertex): the tiles' slots carry no kind;
+    // each slot's 9 slot-weight rows stream from xrows (9 planes of `slots` floats, slot order)
+    // and the per-entry constants and rest edges are derived on the fly (as the explicit K1 does)
+    bool tile_xr = false;
+    DBuf xrows;
     // K1R resident whole-step kernel (small scenes): 0 off, 1 REPL (one cluster, position
     // replicas in shared memory), 2 GLOB (one CTA per SM, grid barrier); -1 not decided yet
     int res_mode = -1;
@@ -593,7 +598,10 @@ template <typename R> void build_tiles(vbd_ctx* c)
     Nvtx nv_("tile build");
     c->tiles = false;
     const char* e = getenv("VBD_TILES");
-    if ((e && *e == '0') || !c->compact || !c->inplace || c->nsolve == 0 || c->nkinds >= 65535 ||
+    c->tile_xr = false;
+    const char* xe = getenv("VBD_TILES_X");
+    const bool xr = !c->compact && sizeof(R) == 4 && c->disp && c->uniform_mat && !(xe && *xe == '0');
+    if ((e && *e == '0') || !(c->compact || xr) || !c->inplace || c->nsolve == 0 || c->nkinds >= 65535 ||
         c->has_extras)
         return;
     const char* we = getenv("VBD_TILE_W");
@@ -620,7 +628,13 @@ template <typename R> void build_tiles(vbd_ctx* c)
     cnt.alloc((size_t)nt * 16);
     err.alloc(4);
     CK(cudaMemsetAsync(err.p, 0, 4, s));
-    const int4* cent = c->ent.as<int4>();
+    DBuf xids;  // XR: {n0, n1, n2, 0} of every explicit entry (the tile build's input)
+    if (xr) {
+        xids.alloc((size_t)std::max<long long>(c->E, 1) * 16);
+        if (c->E) k_plane_ids<<<blocks_for(c->E), 256, 0, s>>>(c->ent.as<float4>(), c->E, xids.as<int4>());
+        CK(cudaGetLastError());
+    }
+    const int4* cent = xr ? xids.as<int4>() : c->ent.as<int4>();
     int P = 256;
     while (P < VPT * c->max_deg * 3) P <<= 1;
     const size_t sort_smem = (size_t)P * 4;
@@ -653,11 +667,11 @@ template <typename R> void build_tiles(vbd_ctx* c)
     if ((mx + 1) * (long long)PU > 65535) return;
     if (c->nkinds >= 65535) return;
     const char* kge = getenv("VBD_TILE_KG");
-    c->tile_kg = (long long)(c->nkinds + 1) * KindRec<R>::HOT * sizeof(R) > 32768 || (kge && *kge == '1');
+    c->tile_kg = !xr && ((long long)(c->nkinds + 1) * TileSmem<R>::KSTRIDE > 32768 || (kge && *kge == '1'));
     if (c->tile_kg && W != 2) return;  // compiled for the 2-lane kernel
     c->nbr_cap = (int)mx;
     c->ent_cap = (int)ms;
-    TileSmem<R> L{c->ent_cap, c->nbr_cap, c->tile_kg ? -1 : (int)c->nkinds, VPT};
+    TileSmem<R> L{c->ent_cap, c->nbr_cap, (c->tile_kg || xr) ? -1 : (int)c->nkinds, VPT};
     // as many stages (2..4) as fit three CTAs per SM, else two (2-lane: 2 stages)
     const char* oe = getenv("VBD_TILE_OCC");
     c->tile_occ = oe && *oe == '2' ? 2 : 3;  // 3 CTAs per SM (one entry per lane in flight) measured faster
@@ -674,6 +688,11 @@ template <typename R> void build_tiles(vbd_ctx* c)
         if (L.total(st) <= 2 * VBD_TILE_SMEM_MAX) stages = st;
     const char* se = getenv("VBD_TILE_STAGES");
     if (se && *se) stages = std::min(stages, atoi(se));
+    if (xr && (W != 2 || stages < 2)) return;
+    if (xr) {  // K1T-X: 2 stages, 2 CTAs per SM (registers for the rows in flight; measured faster)
+        stages = 2;
+        if (!(oe && *oe == '3')) c->tile_occ = 2;
+    }
     if (stages < 2) return;
     c->tile_stages = stages;
     DBuf dl, ds, sbase;
@@ -685,14 +704,16 @@ template <typename R> void build_tiles(vbd_ctx* c)
     const long long slots = read_scalar<long long>(sbase.as<long long>() + nt, s);
     c->tnbr.alloc((size_t)std::max<long long>(total, 1) * 4);
     c->tent.alloc((size_t)std::max<long long>(slots, 1) * 8);
+    DBuf slot_entry;  // XR: the explicit entry of every slot (-1: padding)
+    if (xr) slot_entry.alloc((size_t)std::max<long long>(slots, 1) * 8);
     k_tile_nbrs<true><<<nt, 256, sort_smem, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
                                                 cent, nullptr, c->loff.as<long long>(), sbase.as<long long>(),
                                                 c->tnbr.as<int>(), c->tent.as<uint2>(), W,
                                                 PU, (unsigned)(c->nbr_cap * PU),
-                                                c->tile_kg ? 1u : (unsigned)(KindRec<R>::HOT * sizeof(R)),
-                                                c->tile_kg ? (unsigned)c->nkinds
-                                                           : (unsigned)(c->nkinds * KindRec<R>::HOT * sizeof(R)),
-                                                err.as<int>());
+                                                xr ? 0u : c->tile_kg ? 1u : TileSmem<R>::KSTRIDE,
+                                                xr ? 0u : c->tile_kg ? (unsigned)c->nkinds
+                                                                     : (unsigned)(c->nkinds * TileSmem<R>::KSTRIDE),
+                                                err.as<int>(), xr ? slot_entry.as<long long>() : nullptr);
     CK(cudaGetLastError());
     if (read_scalar<int>(err.p, s)) fail(VBD_ERR_INTERNAL, "tile build failed");
     if (slack > 0) {
@@ -721,6 +742,13 @@ template <typename R> void build_tiles(vbd_ctx* c)
                                                       asg.as<int>(), dsatur ? 1 : 0);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s));
+    }
+    if (xr) {  // the rows of every slot, 9 planes in slot order (padding: zeros)
+        c->xrows.alloc((size_t)std::max<long long>(slots, 1) * 9 * 4);
+        k_slot_rows<<<blocks_for(std::max<long long>(slots, 1)), 256, 0, s>>>(
+            slot_entry.as<long long>(), slots, c->ent.as<float4>(), c->E, c->xrows.as<float>());
+        CK(cudaGetLastError());
+        c->tile_xr = true;
     }
     c->tdesc.alloc((size_t)nt * sizeof(TileDesc));
     k_tile_desc<<<blocks_for(nt), 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
@@ -870,7 +898,6 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
              "fp32 layout recomputes tet volumes from |det W|; tet_vol disagrees with tet_w "
              "(use precision=fp64)");
     compact_entries<R>(c);
-    build_tiles<R>(c);
     // one material per vertex? (always true for bodies built by build_system)
     {
         DBuf mixed;
@@ -904,7 +931,7 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
         const char* de = getenv("VBD_DISP");
         c->disp = sizeof(R) == 4 && !c->has_extras && !(de && *de == '0');
     }
-    if (sizeof(R) == 4 && !c->disp) c->tiles = false;  // K1T / K1R are compiled for the fp32 displacement state
+    if (sizeof(R) == 4 ? c->disp : true) build_tiles<R>(c);  // fp32 K1T needs the displacement state
     CK(cudaStreamSynchronize(s));
 }
 
@@ -1049,7 +1076,7 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     else launch_pdl(k1_color_pass<R, W, U, B, false, false>, nb, 256, 0, s, a);
 }
 
-template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false>
+template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false, bool XR = false>
 void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
 {
     // the shared-memory opt-in and the occupancy are per device
@@ -1059,14 +1086,14 @@ void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
     CK(cudaGetDevice(&dev));
     dev &= 63;
     if (smem > attr[dev]) {
-        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC, DEF, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC, DEF, KG, XR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[dev] = smem;
         CK(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k1_tiles<R, UM, S, W, OCC, DEF, KG>, 64 * W + 32, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k1_tiles<R, UM, S, W, OCC, DEF, KG, XR>, 64 * W + 32, smem));
         per_sm[dev] = std::max(1, per_sm[dev]);
     }
     const int grid = std::min(ta.tcount, per_sm[dev] * sms[dev]);
-    launch_pdl(k1_tiles<R, UM, S, W, OCC, DEF, KG>, (unsigned)grid, 64 * W + 32, smem, s, ta);
+    launch_pdl(k1_tiles<R, UM, S, W, OCC, DEF, KG, XR>, (unsigned)grid, 64 * W + 32, smem, s, ta);
 }
 
 template <typename R, bool UM, int W>
@@ -1103,7 +1130,7 @@ void launch_k1_tiles_w(const K1TArgs<R>& ta, int W, int stages, int occ, bool de
 
 template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a, cudaStream_t s)
 {
-    if (!c->tiles || a.group || a.out || a.line_search || !a.kinds || a.coff) return false;
+    if (!c->tiles || a.group || a.out || a.line_search || (!a.kinds && !c->tile_xr) || a.coff) return false;
     int col = -1;
     for (int k = 0; k < c->ncolors; ++k)
         if (c->cbeg[k] == a.vbeg && c->ccnt[k] == a.count) col = k;
@@ -1122,8 +1149,18 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     const char* dbg = getenv("VBD_TILE_DBG");
     ta.dbg = dbg && *dbg ? atoi(dbg) : 0;
     if (ta.dbg) ta.a.flag = nullptr;  // garbage positions in the timing experiments
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, c->tile_kg ? -1 : ta.nkinds, 64};
+    ta.xrows = c->tile_xr ? c->xrows.as<float>() : nullptr;
+    ta.xstride = c->tile_xr ? (long long)(c->tent.bytes / 8) : 0;
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (c->tile_kg || c->tile_xr) ? -1 : ta.nkinds, 64};
     const int S = c->tile_stages;
+    if (c->tile_xr) {  // K1T-X: fp32, one material per vertex, 2 lanes, deferred solves
+        if constexpr (sizeof(R) == 4) {
+            if (!a.vmat || c->tile_w != 2 || S != 2) fail(VBD_ERR_INTERNAL, "K1T-X configuration");
+            if (c->tile_occ == 3) launch_k1_tiles_v<R, true, 2, 2, 3, 2, false, true>(ta, L.total(S), s);
+            else launch_k1_tiles_v<R, true, 2, 2, 2, 2, false, true>(ta, L.total(S), s);
+        }
+        return true;
+    }
     if (a.vmat) launch_k1_tiles_w<R, true>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, c->tile_kg, L.total(S), s);
     else launch_k1_tiles_w<R, false>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, c->tile_kg, L.total(S), s);
     return true;

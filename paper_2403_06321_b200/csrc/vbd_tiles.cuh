@@ -55,7 +55,8 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
                                                    const long long* __restrict__ lbase,
                                                    const long long* __restrict__ sbase, int* __restrict__ tnbr,
                                                    uint2* __restrict__ tent, int W, unsigned r4b,
-                                                   unsigned pad_pos, unsigned kstride, unsigned pad_kind, int* err)
+                                                   unsigned pad_pos, unsigned kstride, unsigned pad_kind, int* err,
+                                                   long long* __restrict__ slot_entry = nullptr)
 {
     extern __shared__ int keys[];  // next power of two >= max references per tile
     __shared__ int part[257];
@@ -143,9 +144,11 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
         const int vpw = 32 / W;
         const int lv = vpw * w + lane % vpw, pos = W * i + lane / vpw;
         uint2 out = make_uint2(pad_pos | (pad_pos << 16), pad_pos | (pad_kind << 16));
+        long long ent = -1;
         if (lv < nv) {
             const long long k = eoff[v0 + lv] + pos;
             if (k < eoff[v0 + lv + 1]) {
+                ent = k;
                 const int4 e = cent[k];
                 unsigned loc[3];
                 const int ids[3] = {e.x, e.y, e.z};
@@ -163,7 +166,33 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
             }
         }
         tent[s0 + sl] = out;
+        if (slot_entry) slot_entry[s0 + sl] = ent;
     }
+}
+
+// K1T-X: {n0, n1, n2, 0} of every explicit fp32 entry (ids without the material bits)
+__global__ void k_plane_ids(const float4* __restrict__ planes, long long E, int4* __restrict__ out)
+{
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= E) return;
+    const float4 a = planes[k];
+    out[k] = make_int4((int)(__float_as_uint(a.x) & VBD_ID_MASK), (int)(__float_as_uint(a.y) & VBD_ID_MASK),
+                       (int)(__float_as_uint(a.z) & VBD_ID_MASK), 0);
+}
+
+// K1T-X: the 9 slot-weight rows of every slot's entry, plane q at rows + q * S (padding: 0)
+__global__ void k_slot_rows(const long long* __restrict__ slot_entry, long long S, const float4* __restrict__ planes,
+                            long long E, float* __restrict__ rows)
+{
+    const long long sl = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (sl >= S) return;
+    const long long k = slot_entry[sl];
+    float w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (k >= 0) {
+        const Entry<float> e = Entry<float>::load(planes, E, k);
+        for (int q = 0; q < 9; ++q) w[q] = e.w[q];
+    }
+    for (int q = 0; q < 9; ++q) rows[q * S + sl] = w[q];
 }
 
 // Bank-aware placement of a tile's neighbour positions (one thread per tile, after FILL).
@@ -422,6 +451,8 @@ template <typename R> struct K1TArgs {
     int nkinds;
     int dbg;  // timing experiments only (VBD_TILE_DBG): 1 consumers skip the entry sweep,
               // 2 the producer skips the neighbour gathers; results are wrong in both
+    const float* xrows;  // K1T-X: slot-weight rows, 9 planes of xstride floats in slot order
+    long long xstride;
 };
 
 typedef TileDesc TileHdr;  // the stage header is a copy of the tile's descriptor
@@ -466,8 +497,12 @@ template <typename R> struct TileSmem {
     int ent_cap, nbr_cap, nk, vpt;  // vpt: vertices per tile
     // kind records (HOT R each), then for fp32 (displacement state) the kinds' rest edges
     // (3 float4 = 48 B each: the same byte offset as the fp32 record, in the second table)
-    __host__ __device__ size_t recs_bytes() const { return (size_t)(nk + 1) * KindRec<R>::HOT * sizeof(R); }
-    __host__ __device__ size_t kinds_bytes() const { return recs_bytes() * (sizeof(R) == 4 ? 2 : 1); }
+    // fp32 (displacement state): one packed 80-byte SWEEP record per kind, read with 4 LDS.128 +
+    // 1 LDS.32 per entry: [E0.xyz, t0] [E1.xyz, t1] [E2.xyz, t2] [t3 t4 t5 t6] [t7 t8 dsc opd]
+    // (E = rest edges, t = ec_terms); fp64: the HOT part of the kind record
+    static constexpr unsigned KSTRIDE = sizeof(R) == 4 ? 80u : (unsigned)(KindRec<R>::HOT * sizeof(R));
+    __host__ __device__ size_t recs_bytes() const { return (size_t)(nk + 1) * KSTRIDE; }
+    __host__ __device__ size_t kinds_bytes() const { return recs_bytes(); }
     __host__ __device__ size_t off_hdr() const { return 0; }
     __host__ __device__ size_t off_ent() const { return sizeof(TileDesc); }
     // neighbour positions, 16-byte units: fp32 one float4 per neighbour; fp64 the (x, y) halves of
@@ -506,6 +541,12 @@ __device__ __forceinline__ void lds_v(unsigned a, double2& v)
 {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
 }
+__device__ __forceinline__ float lds_f32(unsigned a)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint2 lds_u2(unsigned a)
 {
     uint2 v;
@@ -542,7 +583,11 @@ __device__ __forceinline__ void k1t_store(const K1Args<R>& a, int v, typename Ve
 // overhead per entry).
 // KG: the kind table is too large for shared memory (e.g. fp64 grids whose rest shapes differ
 // in the last bits): slots carry the kind index and the records are read through L1 from global.
-template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false>
+// XR (K1T-X, fp32, one material per vertex): explicit entries -- the slots carry no kind; each
+// entry's 9 slot-weight rows stream from ta.xrows (coalesced: a warp round reads 128 B per
+// plane) and its constants, volume and rest edges are derived exactly as the explicit K1 does
+// (ec_terms, volume_from_rows, rest_edges_from_rows), so results stay bitwise equal to it.
+template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false, bool XR = false>
 __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta)
 {
     typedef typename Vec4<R>::T R4;
@@ -551,7 +596,8 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long full[S], empty[S];
     const K1Args<R>& a = ta.a;
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, KG ? -1 : ta.nkinds, NCW * VPW};
+    static_assert(!XR || (sizeof(R) == 4 && UM && !KG), "K1T-X: fp32, one material per vertex");
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (KG || XR) ? -1 : ta.nkinds, NCW * VPW};
     typedef typename PlaneT<R>::T PL;
     PL* skind = reinterpret_cast<PL*>(smem);
     unsigned char* stages = smem + ((L.kinds_bytes() + 127) & ~(size_t)127);
@@ -561,13 +607,28 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
     // (t[8] = V mu |w|^2 is summed per vertex at pack time, dsc / opd are read once per vertex)
     constexpr int QS = UM ? 8 * (int)sizeof(R) / 16 : QH;
     constexpr bool DISP = sizeof(R) == 4;  // fp32: displacement state, rest edges per kind
-    if (!KG) {
-        for (int i = tid; i < ta.nkinds * QH; i += blockDim.x) skind[i] = ta.kinds[(i / QH) * Q + i % QH];
-        for (int i = tid; i < QH; i += blockDim.x) skind[ta.nkinds * QH + i] = PL{};  // padding: zero record
-        if constexpr (DISP) {  // 3 float4 per kind (QH == 3 for fp32), same offsets as the records
-            float4* sedge = reinterpret_cast<float4*>(smem + L.recs_bytes());
-            for (int i = tid; i < ta.nkinds * 3; i += blockDim.x) sedge[i] = ta.a.kedge[i];
-            for (int i = tid; i < 3; i += blockDim.x) sedge[ta.nkinds * 3 + i] = float4{};
+    if (!KG && !XR) {
+        if constexpr (DISP) {  // packed fp32 sweep records (TileSmem::KSTRIDE); padding: zero record
+            float4* sk = reinterpret_cast<float4*>(smem);
+            for (int i = tid; i < (ta.nkinds + 1) * 5; i += blockDim.x) {
+                const int k = i / 5, q = i % 5;
+                float4 v{};
+                if (k < ta.nkinds) {
+                    const float* t = reinterpret_cast<const float*>(ta.kinds + (size_t)k * Q);
+                    if (q < 3) {
+                        v = ta.a.kedge[3 * k + q];
+                        v.w = t[q];
+                    } else if (q == 3) {
+                        v = make_float4(t[3], t[4], t[5], t[6]);
+                    } else {
+                        v = make_float4(t[7], t[8], t[9], t[10]);
+                    }
+                }
+                sk[i] = v;
+            }
+        } else {
+            for (int i = tid; i < ta.nkinds * QH; i += blockDim.x) skind[i] = ta.kinds[(i / QH) * Q + i % QH];
+            for (int i = tid; i < QH; i += blockDim.x) skind[ta.nkinds * QH + i] = PL{};  // padding: zero record
         }
     }
     for (int s = 0; s < S; ++s)  // padding: zero position after the largest neighbour list
@@ -622,6 +683,15 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                 bulk_g2s(st + L.off_x(), a.pos + d.v0, vby, bar);
                 bulk_g2s(st + L.off_xt(), a.xt + d.v0, vby, bar);
                 bulk_g2s(st + L.off_y(), a.y + d.v0, vby, bar);
+                if constexpr (XR) {  // the tile's rows into L2 (the consumers stream them next)
+#pragma unroll 1
+                    for (int q = 0; q < 9; ++q)
+                        if (eby)
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                             ta.xrows + (size_t)q * ta.xstride + d.eb),
+                                         "r"(eby / 2u)
+                                         : "memory");
+                }
             }
             unsigned char* np = st + L.off_npos();
             for (int base = 0; ta.dbg != 2;) {
@@ -729,11 +799,43 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
         const unsigned npb = smem_u32(np);
         const unsigned nzw = (unsigned)(L.off_nzw() - L.off_npos());
         const unsigned kb = smem_u32(skind);
-        const unsigned keb = kb + (unsigned)L.recs_bytes();  // fp32: rest-edge table
         const unsigned sb32 = smem_u32(sent);
+        const long long hxeb = XR ? hp->eb : 0;  // K1T-X: the tile's first slot (rows index)
+        const unsigned padp = (unsigned)ta.nbr_cap * L.PU;
+        Material<R> xmat{};
+        if constexpr (XR) xmat = a.mat[a.vmat[hv0 + lvc]];
+        // K1T-X: the rows of the next XPF iterations are in flight (registers), a rotating window
+        constexpr int XPF = 1;  // (2 at 2 CTAs/SM spills: 3.54 vs 3.21 ms per C5j pass)
+        float wn[XR ? XPF : 1][XR ? U : 1][XR ? 9 : 1];
+        auto load_rows = [&](int i0n, float (&dst)[XR ? U : 1][XR ? 9 : 1]) {
+            if constexpr (XR) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const float* xp = ta.xrows + hxeb + 32ll * (sb + i0n + u) + lane;
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) dst[u][q] = i0n < rounds ? __ldcs(xp + q * ta.xstride) : 0.0f;
+                }
+            }
+        };
+#pragma unroll
+        for (int f = 0; f < (XR ? XPF : 0); ++f) load_rows(f * U, wn[f]);
         for (int i0 = 0; i0 < rounds; i0 += U) {  // rounds is a multiple of U
             uint2 e[U];
             R4 p[U][3];
+            float wc[XR ? U : 1][XR ? 9 : 1];
+            if constexpr (XR) {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) wc[u][q] = wn[0][u][q];
+#pragma unroll
+                for (int f = 0; f + 1 < XPF; ++f)
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int q = 0; q < 9; ++q) wn[f][u][q] = wn[f + 1][u][q];
+                load_rows(i0 + XPF * U, wn[XPF - 1]);
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 e[u] = lds_u2(sb32 + 256u * (unsigned)(i0 + u));
@@ -742,37 +844,44 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                 lds_pos(npb + (e[u].y & 0xffffu), nzw, p[u][2]);
             }
             float4 ex[U][3];  // fp32: the entries' rest edges
-            if constexpr (DISP) {
+            R r[U][KindRec<R>::HOT];
 #pragma unroll
-                for (int u = 0; u < U; ++u)
+            for (int u = 0; u < U; ++u) {
+                const unsigned rp = kb + (e[u].y >> 16);
+                if constexpr (XR) {  // rows streamed from global (one iteration ahead), constants here
+                    const float* w = wc[u];
+                    const bool valid = (e[u].x & 0xffffu) != padp;  // padding slot: contributes +0
+                    const float V = valid ? volume_from_rows(w) : 0.0f;
+                    ec_terms<float>(w, V, xmat.mu, xmat.lam, xmat.gamma, reinterpret_cast<float*>(r[u]));
+                    rest_edges_from_rows(w, ex[u]);
+                    if (!valid) ex[u][0] = ex[u][1] = ex[u][2] = float4{};
+                } else if constexpr (DISP && !KG) {  // packed sweep record: 4 LDS.128 + 1 LDS.32 (UM)
+                    float4 c3;
 #pragma unroll
                     for (int q = 0; q < 3; ++q) {
-                        if constexpr (KG) ex[u][q] = __ldg(ta.a.kedge + 3 * (size_t)(e[u].y >> 16) + q);
-                        else lds_v(keb + (e[u].y >> 16) + 16u * q, ex[u][q]);
+                        lds_v(rp + 16u * q, ex[u][q]);
+                        r[u][q] = ex[u][q].w;
                     }
-            }
-            if constexpr (PACK) {  // x/y of every 3-vector packed as fp32x2 (FFMA2)
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    float r[KindRec<R>::HOT];
-                    const unsigned rp = kb + (e[u].y >> 16);
-#pragma unroll
-                    for (int q = 0; q < QS; ++q) {
-                        PL v;
-                        if constexpr (KG) v = __ldg(ta.kinds + (size_t)(e[u].y >> 16) * Q + q);
-                        else lds_v(rp + 16u * q, v);
-                        r[4 * q] = v.x;
-                        r[4 * q + 1] = v.y;
-                        r[4 * q + 2] = v.z;
-                        r[4 * q + 3] = v.w;
+                    lds_v(rp + 48u, c3);
+                    r[u][3] = c3.x;
+                    r[u][4] = c3.y;
+                    r[u][5] = c3.z;
+                    r[u][6] = c3.w;
+                    if constexpr (UM) {
+                        r[u][7] = lds_f32(rp + 64u);
+                    } else {
+                        float4 c4;
+                        lds_v(rp + 64u, c4);
+                        r[u][7] = c4.x;
+                        r[u][8] = c4.y;
+                        r[u][9] = c4.z;
+                        r[u][10] = c4.w;
                     }
-                    tet_contrib_ec_xy(p[u][0], p[u][1], p[u][2], nxy, nz, ex[u][0], ex[u][1], ex[u][2], r, acc[u % NA]);
-                }
-            } else {
+                } else {
+                    if constexpr (DISP) {  // (KG: rest edges from the global table)
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    R r[KindRec<R>::HOT];
-                    const unsigned rp = kb + (e[u].y >> 16);
+                        for (int q = 0; q < 3; ++q) ex[u][q] = __ldg(ta.a.kedge + 3 * (size_t)(e[u].y >> 16) + q);
+                    }
 #pragma unroll
                     for (int q = 0; q < QS; ++q) {
                         PL v;
@@ -780,24 +889,41 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                         else lds_v(rp + 16u * q, v);
                         const R* vr = reinterpret_cast<const R*>(&v);
 #pragma unroll
-                        for (int z = 0; z < 16 / (int)sizeof(R); ++z) r[q * (16 / (int)sizeof(R)) + z] = vr[z];
+                        for (int z = 0; z < 16 / (int)sizeof(R); ++z) r[u][q * (16 / (int)sizeof(R)) + z] = vr[z];
                     }
+                }
+            }
+            if constexpr (PACK) {  // x/y of every 3-vector packed as fp32x2 (FFMA2)
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    tet_contrib_ec_xy(p[u][0], p[u][1], p[u][2], nxy, nz, ex[u][0], ex[u][1], ex[u][2],
+                                      reinterpret_cast<const float*>(r[u]), acc[u % NA]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
                     R e0[3], e1[3], e2[3];
                     edge3<R>(p[u][0], xi, ex[u][0], DISP, e0);
                     edge3<R>(p[u][1], xi, ex[u][1], DISP, e1);
                     edge3<R>(p[u][2], xi, ex[u][2], DISP, e2);
                     const int b = u % NA;  // i0 is a multiple of U, so (i0 + u) % NA == u % NA (unrolled)
-                    tet_contrib_ec<R, !UM>(e0, e1, e2, r, UM ? R(0) : r[9], UM ? R(1) : r[10], dx, fa[b], Ha[b],
-                                           sva[b]);
+                    tet_contrib_ec<R, !UM>(e0, e1, e2, r[u], UM ? R(0) : r[u][9], UM ? R(1) : r[u][10], dx, fa[b],
+                                           Ha[b], sva[b]);
                 }
             }
         }
-        if (UM && rounds > 0) {  // the record of this lane's round-0 slot (position j; lane j = 0
+        if constexpr (XR) {  // damping from the vertex's material (explicit K1: the same)
+            dsc = xmat.dsc;
+            opd = xmat.opd;
+        } else if (UM && rounds > 0) {  // the record of this lane's round-0 slot (position j; lane j = 0
                                  // holds the vertex's first entry), read once, not per iteration
             const uint2 e0s = lds_u2(sb32);
             PL v;
             if constexpr (KG) v = __ldg(ta.kinds + (size_t)(e0s.y >> 16) * Q + 2);
-            else lds_v(kb + (e0s.y >> 16) + 32u, v);
+            else if constexpr (DISP) {  // packed record chunk 4 = (t7, t8, dsc, opd): as chunk 2's (., dsc, opd)
+                float4 c4;
+                lds_v(kb + (e0s.y >> 16) + 64u, c4);
+                v = make_float4(c4.y, c4.z, c4.w, 0.0f);
+            } else lds_v(kb + (e0s.y >> 16) + 32u, v);
             const R* vr = reinterpret_cast<const R*>(&v);
             if constexpr (sizeof(R) == 4) {  // r[8..11] = chunk 2
                 dsc = vr[1];

@@ -50,3 +50,23 @@ def test_reference_arm_reports_what_it_ran():
     vit = cb["sample_vertices"] * line["config"]["n_max"]
     assert abs(vit / (line["ms_per_step"] / 1e3) / line["value"] - 1) < 1e-9
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_layout_bytes_model_per_layout():
+    """roofline.frac's numerator for the three kernels that carry a layout:
+    K1T (8 B slots), K1T-X (8 B slots + 36 B of streamed rows per slot) and the global K1
+    (entry_bytes per entry + CSR offset)."""
+    import types
+    import bench
+    base = dict(num_vertices=1000, num_solved=900, num_colors=4, color_count=[250, 250, 250, 250],
+                tile_slots=20000, tile_nbr_refs=5000, tiles=16, num_entries=18000, entry_bytes=48)
+    other = sum(16 * (1000 - 250) for _ in range(4))
+    k1t = types.SimpleNamespace(layout=1, **base)
+    k1tx = types.SimpleNamespace(layout=0, **base)
+    glob = types.SimpleNamespace(layout=0, **dict(base, tiles=0))
+    tiles = 8 * 20000 + 4 * 5000 + 64 * 16 + 4 * 16 * 900 + other
+    assert bench.layout_bytes_per_iteration(k1t, "fp32") == tiles
+    assert bench.layout_bytes_per_iteration(k1tx, "fp32") == tiles + 36 * 20000
+    assert bench.layout_bytes_per_iteration(glob, "fp32") == 900 * (8 + 64) + 18000 * 48 + other
+    k1tx.tile_lanes, k1tx.tile_stages = 2, 2
+    assert bench.layout_name(k1tx).startswith("K1T-X")

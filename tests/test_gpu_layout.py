@@ -256,3 +256,26 @@ def test_device_generated_jittered_beam_vs_oracle(V, O, precision, tol):
     err = np.abs(ctx.get_state(x=True)["x"] - st.x).max() / mesh.bbox_diagonal()
     assert err <= tol, err
     ctx.close()
+
+
+@pytest.mark.parametrize("rho", [0.0, 0.9])
+def test_k1t_explicit_rows_bitwise_equals_explicit_k1(V, monkeypatch, rho):
+    """K1T-X (irregular mesh through the tile pipeline, rows streamed per slot, constants and
+    rest edges derived on the fly) is bitwise the explicit-layout global K1 (VBD_TILES_X=0)."""
+    b = V.Beam(14, 9, 7, 0.05, 2e6, 2e7, 1e-7, fix_min_x=True, jitter=0.1)
+    out = []
+    for xr in ("1", "0"):
+        monkeypatch.setenv("VBD_TILES_X", xr)
+        monkeypatch.setenv("VBD_RESIDENT", "0")
+        monkeypatch.setenv("VBD_LAYOUT", "explicit")  # (a mesh this small fits the entry dictionary)
+        ctx = V.DeviceContext.from_beams([b], precision="fp32")
+        for k in ("VBD_TILES_X", "VBD_RESIDENT", "VBD_LAYOUT"):
+            monkeypatch.delenv(k)
+        assert ctx.info.layout == 0
+        assert (ctx.info.tiles > 0) == (xr == "1")
+        p = ctx.step_params(1 / 240, 10, rho, 1e-10, "adaptive", G)
+        for _ in range(3):
+            ctx.step(p)
+        out.append(ctx.get_state(x=True, v_t=True))
+        ctx.close()
+    assert np.array_equal(out[0]["x"], out[1]["x"]) and np.array_equal(out[0]["v_t"], out[1]["v_t"])
