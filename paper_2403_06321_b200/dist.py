@@ -20,11 +20,16 @@ from __future__ import annotations
 import numpy as np
 
 
-def slab_cuts(nx: int, world: int):
-    """Owned vertex-plane ranges [cuts[r], cuts[r+1]) of equal size along x."""
-    if world < 1 or world > nx:
-        raise ValueError("need 1 <= world <= nx")
-    return [int(round(r * nx / world)) for r in range(world + 1)]
+def slab_cuts(nx: int, world: int, fixed_lo: int = 0, fixed_hi: int = 0):
+    """Owned vertex-plane ranges [cuts[r], cuts[r+1]) along x, balanced by SOLVED planes: the
+    fixed_lo first / fixed_hi last planes (a clamped face: never solved, only copied by K2 /
+    K4) ride on the first / last rank instead of counting as a plane of work."""
+    if world < 1 or world > nx - fixed_lo - fixed_hi:
+        raise ValueError("need 1 <= world <= solved planes")
+    work = nx - fixed_lo - fixed_hi
+    cuts = [fixed_lo + int(round(r * work / world)) for r in range(world + 1)]
+    cuts[0], cuts[-1] = 0, nx
+    return cuts
 
 
 def object_shard(num_objects: int, rank: int, world: int):

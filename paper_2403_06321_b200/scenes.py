@@ -142,7 +142,8 @@ def rigid_velocities(num_beams: int, scale: float, seed: int = 0):
 def build(cfg: Config, rank: int = 0, world: int = 1, precision: str = "fp32", device: int = 0):
     """This rank's DeviceContext for ``cfg`` (object shard, slab, or full replica)."""
     if world > 1 and cfg.sharding == "slabs":
-        cuts = slab_cuts(cfg.beams[0].nx, world)
+        b = cfg.beams[0]
+        cuts = slab_cuts(b.nx, world, int(b.fix_min_x), int(b.fix_max_x))
         ctx = DeviceContext.from_beams(list(cfg.beams), precision, device,
                                        slab=(cuts[rank], cuts[rank + 1]))
         return ctx, (cuts[rank], cuts[rank + 1])

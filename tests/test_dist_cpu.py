@@ -169,3 +169,8 @@ def test_partition_helpers():
     assert {hi - lo for lo, hi in spans} == {1296}
     with pytest.raises(ValueError):
         slab_cuts(4, 5)
+    # the fixed x = 0 face of C5 is not work: the other 363 planes are split evenly
+    fc = slab_cuts(364, 8, 1, 0)
+    assert fc[0] == 0 and fc[-1] == 364
+    solved = np.diff(fc) - np.array([1] + [0] * 7)
+    assert max(solved) - min(solved) <= 1 and solved.sum() == 363
