@@ -107,6 +107,7 @@ SIGNATURES = {
     "vbd_step_p2p_launch": (ctypes.c_int, [P, ctypes.POINTER(StepParams)]),
     "vbd_step_p2p_finish": (ctypes.c_int, [P, ctypes.POINTER(StepResult)]),
     "vbd_greedy_color": (ctypes.c_int, [i64, P, P, P, ctypes.c_int, P, ctypes.POINTER(i64)]),
+    "vbd_resident_timeline": (ctypes.c_int, [P, ctypes.POINTER(i64), i64, ctypes.POINTER(i64)]),
     "vbd_profile_color_pass": (ctypes.c_int, [P, f64, i32, P]),
     "vbd_fma_peak": (ctypes.c_int, [i32, i32, i32, f64, P]),
     "vbd_energy": (ctypes.c_int, [P, f64, ctypes.POINTER(f64)]),

@@ -239,7 +239,7 @@ struct vbd_ctx {
     int coll_has_max_depth = 0, coll_ncol = 4;
     // graph-mode contact step (step_contacts_graph): capacities sized from the largest counts
     // seen on the host-synchronised path (mx_*), sentinel-padded buffers, one graph per step
-    long long mx_cell[3] = {0, 0, 0}, mx_join[2] = {0, 0}, mx_rec[3] = {0, 0, 0};
+    long long mx_cell[3] = {0, 0, 0}, mx_join[2] = {0, 0};
     long long cap_cell[3] = {0, 0, 0}, cap_join[2] = {0, 0};
     bool cg_ready = false, cg_pending = false;
     bool cg_enabled = true;  // VBD_CONTACT_GRAPH=0 at context creation: host path only
@@ -271,7 +271,7 @@ struct vbd_ctx {
     std::string res_want;  // VBD_RESIDENT at context creation
     int res_ncta = 0, res_slot_cap = 0, res_grp_cap = 0;
     size_t res_smem = 0;
-    DBuf res_slots, res_slot_beg, res_groups, res_grp_beg, res_col_grp, res_bar, res_push;
+    DBuf res_slots, res_slot_beg, res_groups, res_grp_beg, res_col_grp, res_bar, res_push, res_prof;
     // step state for the fine-grained path
     vbd_step_params cur{};
     std::vector<double> omegas;
@@ -1535,6 +1535,8 @@ template <typename R> void ensure_resident(vbd_ctx* c)
     upload(c->res_grp_beg, grp_beg.data(), grp_beg.size(), s);
     upload(c->res_col_grp, col_grp.data(), col_grp.size(), s);
     upload(c->res_push, push.data(), std::max<size_t>(push.size(), 1), s);
+    if (getenv("VBD_RES_DBG") && (atoi(getenv("VBD_RES_DBG")) & 8))  // diagnostics: pass timeline
+        c->res_prof.alloc((size_t)32 * (4096 * (c->ncolors + 1) + 1));
     c->res_bar.alloc(16);
     CK(cudaMemsetAsync(c->res_bar.p, 0, 16, s));
     CK(cudaStreamSynchronize(s));
@@ -1558,7 +1560,6 @@ template <typename R> void launch_resident(vbd_ctx* c)
     ra.ncolors = c->ncolors;
     ra.n_max = c->cur.n_max;
     ra.cheb = c->cur.rho != 0.0;
-    ra.omega[0] = ra.omega[1] = 1.0;
     ra.omegas = c->omega_dev.as<double>();
     ra.nkinds = (int)c->nkinds;
     ra.slot_cap = c->res_slot_cap;
@@ -1567,7 +1568,10 @@ template <typename R> void launch_resident(vbd_ctx* c)
     ra.ncta = c->res_ncta;
     ra.push = c->res_push.as<unsigned short>();
     ra.dbg = getenv("VBD_RES_DBG") ? atoi(getenv("VBD_RES_DBG")) : 0;
-    if (ra.dbg) ra.a.flag = ra.s.flag = nullptr;  // (garbage positions in the timing experiments)
+    if (ra.dbg & 3) ra.a.flag = ra.s.flag = nullptr;  // (garbage positions in the timing experiments)
+    ra.prof = nullptr;
+    if ((ra.dbg & 8) && c->res_prof.bytes >= (size_t)32 * (c->cur.n_max * (c->ncolors + 1) + 1))
+        ra.prof = c->res_prof.as<long long>();  // CTA 0's pass timeline (vbd_resident_timeline)
     const bool um = c->vmat.p && c->uniform_mat;
     const bool repl = c->res_mode == 1;
     void (*k)(const ResArgs<R>) = repl ? (um ? k_step_resident<R, true, true> : k_step_resident<R, false, true>)
@@ -3761,6 +3765,22 @@ int vbd_descend(vbd_ctx* c, int32_t method, int32_t n_iters, double h, double rh
         CK(cudaSetDevice(c->device));
         if (c->precision == VBD_PREC_F64) descend_impl<double>(c, method, n_iters, h, rho, eps_det, line_search, g, wall_ms);
         else descend_impl<float>(c, method, n_iters, h, rho, eps_det, line_search, g, wall_ms);
+    });
+}
+
+int vbd_resident_timeline(vbd_ctx* c, int64_t* out, int64_t cap, int64_t* n)
+{
+    return guarded([&] {
+        if (!c || !n) fail(VBD_ERR_ARG, "NULL argument");
+        *n = 0;
+        if (!c->res_prof.p || c->res_mode <= 0) return;
+        const int64_t have = (int64_t)(c->res_prof.bytes / 8);
+        const int64_t m = std::min<int64_t>(cap, have);
+        if (m > 0 && out) {
+            CK(cudaStreamSynchronize(c->stream));
+            CK(cudaMemcpy(out, c->res_prof.p, (size_t)m * 8, cudaMemcpyDeviceToHost));
+        }
+        *n = m;
     });
 }
 

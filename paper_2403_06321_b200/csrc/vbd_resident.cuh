@@ -41,7 +41,6 @@ template <typename R> struct ResArgs {
     const int* grp_beg;         // (ncta + 1)
     const int* col_grp;         // per CTA: (ncolors + 1) group offsets (relative to grp_beg[k])
     int ncolors, n_max, cheb;
-    double omega[2];            // unused slot (omegas from the table below)
     const double* omegas;       // (n_max + 1), device
     int nkinds;
     int slot_cap, grp_cap;      // max slots / groups of one CTA (shared memory sizing)
@@ -50,7 +49,9 @@ template <typename R> struct ResArgs {
     const unsigned short* push; // REPL: per vertex, the CTAs whose replica must see its updates
                                 // (owners of its neighbours, its own CTA, its K3 / K4 chunk CTA)
     int dbg;                    // timing experiments only (VBD_RES_DBG, wrong results): 1 no DSMEM
-                                // pushes, 2 no entry sweep, 3 neither
+                                // pushes, 2 no entry sweep, 3 neither; 8: CTA 0's pass timeline
+                                // (clock64, results unchanged) into prof
+    long long* prof;            // dbg & 8: per pass {start, last sweep end, last push end, barrier exit}
 };
 
 // shared memory of one CTA (bytes; every region 16-byte aligned)
@@ -188,8 +189,16 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
     const unsigned kb = smem_u32(skind);
     const int vi = lane & 7, j = lane >> 3;  // lane = 8 j + vi serves entry positions j, j + 4, ...
     const R4 zero4{};
+    __shared__ unsigned long long prof_t[2];
+    const bool prof = (ra.dbg & 8) && cta == 0 && ra.prof;
+    int pass = 0;
     for (int it = 1; it <= ra.n_max; ++it) {
         for (int c = 0; c < ra.ncolors; ++c) {
+            if (prof && tid == 0) {
+                prof_t[0] = prof_t[1] = 0;
+                ra.prof[4 * pass] = (long long)clock64();
+            }
+            if (prof) __syncthreads();
             for (int gi = scg[c] + warp; gi < scg[c + 1]; gi += NW) {
                 const ResGroup g = sgrp[gi];
                 const bool act = vi < g.nv;
@@ -277,6 +286,7 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
                     dsc = r[9];
                     opd = r[10];
                 }
+                if (prof && lane == 0) atomicMax(&prof_t[0], (unsigned long long)clock64());
                 // the 4 lanes of a vertex are vi + 8 j: butterfly j ^ 2, then j ^ 1 (4-lane K1 order)
 #pragma unroll
                 for (int o = 16; o >= 8; o >>= 1) {
@@ -327,7 +337,14 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
                 }
             };
             const bool copy_here = ra.cheb && !blend && c == ra.ncolors - 1;
+            if (prof && lane == 0) atomicMax(&prof_t[1], (unsigned long long)clock64());
             barrier();
+            if (prof && tid == 0) {
+                ra.prof[4 * pass + 1] = (long long)prof_t[0];
+                ra.prof[4 * pass + 2] = (long long)prof_t[1];
+                ra.prof[4 * pass + 3] = (long long)clock64();
+            }
+            ++pass;
             if (copy_here) {
                 k3_copy();
                 barrier();
