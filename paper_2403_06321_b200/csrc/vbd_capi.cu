@@ -1406,15 +1406,18 @@ template <typename R> void ensure_resident(vbd_ctx* c)
     auto plan = [&](int ncta, std::vector<std::vector<int>>& cut, int& slot_cap, int& grp_cap) {
         cut.assign(c->ncolors, std::vector<int>(ncta + 1, 0));
         std::vector<long long> slots(ncta, 0), grps(ncta, 0);
+        const char* pe = getenv("VBD_RES_PLAN");  // "count": equal group counts (tuning)
+        const bool by_count = pe && std::string(pe) == "count";
+        auto cost = [&](const G& g) { return by_count ? 1LL : (long long)g.rounds + 2; };
         for (int col = 0; col < c->ncolors; ++col) {
             const auto& gs = cg[col];
             long long tot = 0;
-            for (const G& g : gs) tot += g.rounds + 2;
+            for (const G& g : gs) tot += cost(g);
             long long acc = 0;
             int k = 0;
             for (int i = 0; i < (int)gs.size(); ++i) {
                 while (k < ncta - 1 && acc * ncta >= tot * (k + 1)) cut[col][++k] = i;
-                acc += gs[i].rounds + 2;
+                acc += cost(gs[i]);
                 slots[k] += 32LL * gs[i].rounds;
                 grps[k] += 1;
             }

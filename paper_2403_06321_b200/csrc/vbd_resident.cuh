@@ -159,11 +159,24 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
     // push a new position of vertex v into the replicas of the CTAs in m (DSMEM stores); a
     // colour pass ends with barrier.cluster (release / acquire)
     auto push_to = [&](unsigned m, int v, const R4& x) {
-        cg::cluster_group cl = cg::this_cluster();
+        const unsigned la = smem_u32(rep + v);
         while (m) {
             const int r = __ffs(m) - 1;
             m &= m - 1;
-            cl.map_shared_rank(rep, r)[v] = x;
+            unsigned ca;  // the rank's copy of this address (mapa), stored with st.shared::cluster
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ca) : "r"(la), "r"(r));
+            if constexpr (sizeof(R) == 4) {
+                asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ca), "f"((float)x.x),
+                             "f"((float)x.y), "f"((float)x.z), "f"((float)x.w)
+                             : "memory");
+            } else {
+                asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ca), "d"((double)x.x),
+                             "d"((double)x.y)
+                             : "memory");
+                asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ca + 16), "d"((double)x.z),
+                             "d"((double)x.w)
+                             : "memory");
+            }
         }
     };
 
@@ -205,6 +218,8 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
                 const int v = g.v0 + (act ? vi : 0);
                 const int k = gi * 8 + vi;
                 const R4 xi4 = xget(v), xt4 = sxt[k], y4 = sy[k];
+                // the vertex's push set, loaded before the sweep (its latency off the critical path)
+                const unsigned pmask = REPL ? (unsigned)__ldg(ra.push + v) : 0u;
                 const R xi[3] = {xi4.x, xi4.y, xi4.z};
                 const R dx[3] = {xi[0] - xt4.x, xi[1] - xt4.y, xi[2] - xt4.z};
                 R f[3] = {R(0), R(0), R(0)}, H[6] = {R(0), R(0), R(0), R(0), R(0), R(0)}, sv = R(0);
@@ -317,7 +332,7 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
                 if constexpr (REPL) __syncwarp();  // inactive lanes read x of the group's first vertex
                 if (act) {
                     if constexpr (REPL) {  // lane j pushes to every 4th CTA of the reader set
-                        push_to((ra.dbg & 1) ? 0u : ra.push[v] & (0x1111u << j), v, nx);
+                        push_to((ra.dbg & 1) ? 0u : pmask & (0x1111u << j), v, nx);
                     } else if (j == 0) {
                         stcg4(s.pos + v, nx);
                     }
