@@ -380,3 +380,31 @@ def test_slab_p2p_disconnect_then_nccl_style_exchange(V):
         lo = max(cuts[r] - 1, 0)
         own = slice((cuts[r] - lo) * plane, (cuts[r + 1] - lo) * plane)
         assert np.array_equal(xs[own], xf[cuts[r] * plane:cuts[r + 1] * plane]), r
+
+
+def test_slab_p2p_irregular_mesh_k1t_x_bitwise(V, monkeypatch):
+    """An irregular mesh (jittered rest positions, explicit layout -> K1T-X) decomposed into
+    three slabs with the fused peer-memory halo: bitwise equal to one context."""
+    monkeypatch.setenv("VBD_LAYOUT", "explicit")
+    monkeypatch.setenv("VBD_RESIDENT", "0")
+    beam = V.Beam(26, 7, 6, 0.02, 1e6, 1e7, 1e-6, fix_min_x=True, jitter=0.1)
+    full = V.DeviceContext.from_beams([beam], precision="fp32")
+    cuts = [0, 8, 17, beam.nx]
+    slabs = [V.DeviceContext.from_beams([beam], precision="fp32", slab=(cuts[r], cuts[r + 1]))
+             for r in range(3)]
+    monkeypatch.delenv("VBD_LAYOUT")
+    monkeypatch.delenv("VBD_RESIDENT")
+    assert full.info.layout == 0 and full.info.tiles > 0
+    from paper_2403_06321_b200.dist import SlabP2P
+    ex = SlabP2P.local(slabs)
+    p = full.step_params(1 / 120, 6, 0.9, 1e-10, "adaptive", G)
+    for _ in range(3):
+        full.step(p)
+        ex.step(p)
+    xf = full.get_state(x=True)["x"]
+    plane = beam.ny * beam.nz
+    for r, sctx in enumerate(slabs):
+        xs = sctx.get_state(x=True)["x"]
+        lo = max(cuts[r] - 1, 0)
+        own = slice((cuts[r] - lo) * plane, (cuts[r + 1] - lo) * plane)
+        assert np.array_equal(xs[own], xf[cuts[r] * plane:cuts[r + 1] * plane]), r
