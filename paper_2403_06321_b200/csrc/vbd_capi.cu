@@ -1181,6 +1181,8 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     const char* dbg = getenv("VBD_TILE_DBG");
     ta.dbg = dbg && *dbg ? atoi(dbg) : 0;
     if (ta.dbg) ta.a.flag = nullptr;  // garbage positions in the timing experiments
+    static const bool early = !(getenv("VBD_PDL_EARLY") && *getenv("VBD_PDL_EARLY") == '0');
+    ta.early = early ? 1 : 0;
     ta.xrows = c->tile_xr ? c->xrows.as<float>() : nullptr;
     ta.xstride = c->tile_xr ? (long long)(c->tent.bytes / 8) : 0;
     const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (c->tile_kg || c->tile_xr) ? -1 : ta.nkinds, 64};

@@ -453,6 +453,7 @@ template <typename R> struct K1TArgs {
               // 2 the producer skips the neighbour gathers; results are wrong in both
     const float* xrows;  // K1T-X: slot-weight rows, 9 planes of xstride floats in slot order
     long long xstride;
+    int early;           // producer loads its first descriptors / ids before the PDL wait
 };
 
 typedef TileDesc TileHdr;  // the stage header is a copy of the tile's descriptor
@@ -648,8 +649,10 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
     // programmatic dependent launch: everything above reads step constants only (the kind
     // table is rewritten only by refresh_kinds, which synchronises the stream before any
     // colour pass is enqueued); positions are read after the predecessor grid has finished.
-    // Overlapping this prologue with the previous pass is worth ~10 % on C1 / C2.
-    pdl_wait();
+    // Overlapping this prologue with the previous pass is worth ~10 % on C1 / C2.  The
+    // producer also loads its first tiles' descriptors and neighbour ids (step constants)
+    // before it waits; the consumers wait here.
+    if (warp != NCW || !ta.early) pdl_wait();
     pdl_launch_dependents();
 
     if (warp == NCW) {  // ---------------- producer
@@ -718,6 +721,7 @@ __global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
         TileDescHead d0 = head(blockIdx.x), d1 = head(blockIdx.x + g);
         int i0[B], i1[B];
         load_ids(d0, 0, i0);
+        if (ta.early) pdl_wait();  // positions and x / x_t / y are the predecessor's output
         for (int t = blockIdx.x; t < ta.tcount; t += 2 * g) {
             load_ids(d1, 0, i1);                       // tile t + g
             const TileDescHead d0n = head(t + 2 * g);  // tile t + 2g
