@@ -217,3 +217,38 @@ def test_full_size_fp32_vs_fp64_ten_steps(V, name):
         msg += f", {d.max() / obj:.3e} x object diag"
     print(msg)
     assert err <= 1e-5, err
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-10), ("fp32", 1e-5)])
+def test_c3_full_size_twisting_beams_vs_oracle(V, O, precision, tol):
+    """BASELINE config 3 at FULL size (two generate_beam(3032,4,4,0.01) beams, both ends
+    clamped and twisted +-0.5 rev/s by rewriting x_t of the fixed vertices every step, rho 0.95,
+    n_max 100), the bench's own device-generated scene, against the oracle over 5 steps."""
+    from paper_2403_06321_b200.scenes import build, config, end_planes, twist_targets
+    cfg = config("c3")
+    ctx, _ = build(cfg, precision=precision)
+    rest = ctx.get_state(x=True)["x"]
+    bodies, off, fixed = [], 0, np.concatenate(end_planes(cfg))
+    for b in cfg.beams:
+        g = O.generate_beam(b.nx, b.ny, b.nz, b.spacing)
+        mesh = O.build_tet_mesh(rest[off:off + g.num_vertices], g.tets, 1000.0)
+        bodies.append((mesh, (b.mu, b.lam, b.kd)))
+        off += g.num_vertices
+    s = O.build_system(bodies, fixed)
+    assert np.array_equal(ctx.colors(), s.color_of)
+    st = O.make_state(s)
+    p = cfg.step_params()
+    for k in range(1, 6):
+        idx, xyz = twist_targets(cfg, rest, k * cfg.h)
+        ctx.set_fixed_targets(idx, xyz)
+        ctx.step(p)
+        st.x_t[idx] = xyz
+        st.x[idx] = xyz
+        O.step(s, st, cfg.h, cfg.n_max, cfg.rho, cfg.a_ext)
+    x = ctx.get_state(x=True)["x"]
+    diag = float(np.linalg.norm(rest.max(0) - rest.min(0)))
+    err = np.abs(x - st.x).max() / diag
+    print(f"C3 full size {precision}: {err:.3e} x diag after 5 steps")
+    assert err <= tol, err
+    assert np.abs(x[idx] - rest[idx]).max() > 5e-4  # the clamped ends really turned (0.05 rad)
+    ctx.close()
