@@ -252,3 +252,31 @@ def test_c3_full_size_twisting_beams_vs_oracle(V, O, precision, tol):
     assert err <= tol, err
     assert np.abs(x[idx] - rest[idx]).max() > 5e-4  # the clamped ends really turned (0.05 rad)
     ctx.close()
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-10), ("fp32", 1e-5)])
+def test_c4_full_scene_objects_vs_oracle(V, O, precision, tol):
+    """The FULL C4 bench scene (10,368 objects, seeded rigid velocities, built and stepped as
+    the bench does): three of its objects -- first, middle, last -- against the oracle run on
+    each object alone from the same start (objects never interact), 10 steps."""
+    from paper_2403_06321_b200.scenes import build, config
+    cfg = config("c4")
+    ctx, _ = build(cfg, precision=precision)
+    st0 = ctx.get_state(x=True, v_t=True)
+    p = cfg.step_params()
+    ctx.step(p, n_steps=10)
+    x = ctx.get_state(x=True)["x"]
+    nv = cfg.beams[0].num_vertices
+    for k in (0, len(cfg.beams) // 2, len(cfg.beams) - 1):
+        b = cfg.beams[k]
+        sl = slice(k * nv, (k + 1) * nv)
+        g = O.generate_beam(b.nx, b.ny, b.nz, b.spacing)
+        mesh = O.build_tet_mesh(st0["x"][sl], g.tets, b.density)
+        s = O.build_system([(mesh, (b.mu, b.lam, b.kd))])
+        st = O.make_state(s, x0=st0["x"][sl], v0=st0["v_t"][sl])
+        for _ in range(10):
+            O.step(s, st, cfg.h, cfg.n_max, cfg.rho, cfg.a_ext)
+        err = np.abs(x[sl] - st.x).max() / mesh.bbox_diagonal()
+        print(f"C4 full scene object {k} {precision}: {err:.3e} x object diag")
+        assert err <= tol, (k, err)
+    ctx.close()
