@@ -296,6 +296,7 @@ struct vbd_ctx {
     // each slot's 9 slot-weight rows stream from xrows (9 planes of `slots` floats, slot order)
     // and the per-entry constants and rest edges are derived on the fly (as the explicit K1 does)
     bool tile_xr = false;
+    int tile_vpt = 64;  // K1T vertices per tile (64, or 32 for small scenes)
     DBuf xrows;
     // K1R resident whole-step kernel (small scenes): 0 off, 1 REPL (one cluster, position
     // replicas in shared memory), 2 GLOB (one CTA per SM, grid barrier); -1 not decided yet
@@ -639,7 +640,20 @@ template <typename R> void build_tiles(vbd_ctx* c)
     const char* we = getenv("VBD_TILE_W");
     const int W = we && *we ? atoi(we) : 2;  // 2 lanes x 16 vertices per warp measured fastest
     if (W != 4 && W != 2) fail(VBD_ERR_ARG, "VBD_TILE_W: 4 or 2 lanes per vertex are compiled");
-    const int VPT = 64;  // 2 W consumer warps x 32 / W vertices
+    // vertices per tile: 64 (2 W consumer warps x 32 / W); 32 when the largest colour would not
+    // fill the SMs twice over with 64-vertex tiles (small scenes; W = 2 only)
+    long long cmax = 0;
+    for (int col = 0; col < c->ncolors; ++col) cmax = std::max(cmax, c->ccnt[col]);
+    int dev_ = 0, sms_ = 148;
+    CK(cudaGetDevice(&dev_));
+    CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev_));
+    const char* tve = getenv("VBD_TILE_V");
+    const char* kg_e = getenv("VBD_TILE_KG");
+    const char* de_e = getenv("VBD_TILE_DEFER");
+    const bool small_ok = W == 2 && !xr && (long long)(c->nkinds + 1) * TileSmem<R>::KSTRIDE <= 32768 &&
+                          !(kg_e && *kg_e == '1') && !(de_e && *de_e == '0');
+    const int VPT = small_ok && (tve && *tve ? atoi(tve) == 32 : cmax < 64LL * 2 * sms_) ? 32 : 64;
+    c->tile_vpt = VPT;
     if ((long long)VPT * c->max_deg * 3 > VBD_TILE_SORT) return;
     c->tile_w = W;
     cudaStream_t s = c->stream;
@@ -721,6 +735,11 @@ template <typename R> void build_tiles(vbd_ctx* c)
     const char* se = getenv("VBD_TILE_STAGES");
     if (se && *se) stages = std::min(stages, atoi(se));
     if (xr && (W != 2 || stages < 2)) return;
+    if (VPT == 32) {  // compiled for 2 stages at 3 CTAs per SM (the stages are half as large)
+        if (stages < 2) return;
+        stages = 2;
+        c->tile_occ = 3;
+    }
     if (xr) {  // K1T-X: 2 stages, 2 CTAs per SM (registers for the rows in flight; measured faster)
         stages = 2;
         if (!(oe && *oe == '3')) c->tile_occ = 2;
@@ -1108,7 +1127,7 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     else launch_pdl(k1_color_pass<R, W, U, B, false, false>, nb, 256, 0, s, a);
 }
 
-template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false, bool XR = false>
+template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false, bool XR = false, int TV = 64>
 void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
 {
     // the shared-memory opt-in and the occupancy are per device
@@ -1118,14 +1137,14 @@ void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
     CK(cudaGetDevice(&dev));
     dev &= 63;
     if (smem > attr[dev]) {
-        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC, DEF, KG, XR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC, DEF, KG, XR, TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[dev] = smem;
         CK(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k1_tiles<R, UM, S, W, OCC, DEF, KG, XR>, 64 * W + 32, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k1_tiles<R, UM, S, W, OCC, DEF, KG, XR, TV>, TV * W + 32, smem));
         per_sm[dev] = std::max(1, per_sm[dev]);
     }
     const int grid = std::min(ta.tcount, per_sm[dev] * sms[dev]);
-    launch_pdl(k1_tiles<R, UM, S, W, OCC, DEF, KG, XR>, (unsigned)grid, 64 * W + 32, smem, s, ta);
+    launch_pdl(k1_tiles<R, UM, S, W, OCC, DEF, KG, XR, TV>, (unsigned)grid, TV * W + 32, smem, s, ta);
 }
 
 template <typename R, bool UM, int W>
@@ -1185,8 +1204,15 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     ta.early = early ? 1 : 0;
     ta.xrows = c->tile_xr ? c->xrows.as<float>() : nullptr;
     ta.xstride = c->tile_xr ? (long long)(c->tent.bytes / 8) : 0;
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (c->tile_kg || c->tile_xr) ? -1 : ta.nkinds, 64};
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (c->tile_kg || c->tile_xr) ? -1 : ta.nkinds, c->tile_vpt};
     const int S = c->tile_stages;
+    if (c->tile_vpt == 32) {  // small scenes: 32-vertex tiles (2 lanes, 2 stages, deferred solves)
+        if (c->tile_w != 2 || S != 2 || c->tile_kg || c->tile_xr || c->tile_occ != 3 || !c->tile_defer)
+            fail(VBD_ERR_INTERNAL, "32-vertex tiles: configuration");
+        if (a.vmat) launch_k1_tiles_v<R, true, 2, 2, 3, 2, false, false, 32>(ta, L.total(S), s);
+        else launch_k1_tiles_v<R, false, 2, 2, 3, 2, false, false, 32>(ta, L.total(S), s);
+        return true;
+    }
     if (c->tile_xr) {  // K1T-X: fp32, one material per vertex, 2 lanes, deferred solves
         if constexpr (sizeof(R) == 4) {
             if (!a.vmat || c->tile_w != 2 || S != 2) fail(VBD_ERR_INTERNAL, "K1T-X configuration");
@@ -2987,8 +3013,9 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         info->tile_stages = c->tiles ? c->tile_stages : 0;
         info->tile_ent_cap = c->tiles ? c->ent_cap : 0;
         if (c->tiles) {
-            const TileSmem<float> L32{c->ent_cap, c->nbr_cap, c->tile_kg ? -1 : (int)c->nkinds, 64};
-            const TileSmem<double> L64{c->ent_cap, c->nbr_cap, c->tile_kg ? -1 : (int)c->nkinds, 64};
+            const int kn = (c->tile_kg || c->tile_xr) ? -1 : (int)c->nkinds;
+            const TileSmem<float> L32{c->ent_cap, c->nbr_cap, kn, c->tile_vpt};
+            const TileSmem<double> L64{c->ent_cap, c->nbr_cap, kn, c->tile_vpt};
             info->tile_smem_bytes = (int)(c->precision == VBD_PREC_F64 ? L64.total(c->tile_stages)
                                                                        : L32.total(c->tile_stages));
         }

@@ -588,12 +588,14 @@ __device__ __forceinline__ void k1t_store(const K1Args<R>& a, int v, typename Ve
 // entry's 9 slot-weight rows stream from ta.xrows (coalesced: a warp round reads 128 B per
 // plane) and its constants, volume and rest edges are derived exactly as the explicit K1 does
 // (ec_terms, volume_from_rows, rest_edges_from_rows), so results stay bitwise equal to it.
-template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false, bool XR = false>
-__global__ void __launch_bounds__(64 * W + 32, OCC) k1_tiles(const K1TArgs<R> ta)
+// TV: vertices per tile (64; 32 for small scenes: twice the CTAs per colour pass, half the
+// gather and sweep per CTA).
+template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false, bool XR = false, int TV = 64>
+__global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta)
 {
     typedef typename Vec4<R>::T R4;
     constexpr int VPW = 32 / W;  // vertices per consumer warp
-    constexpr int NCW = 2 * W;   // consumer warps
+    constexpr int NCW = TV * W / 32;  // consumer warps
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long full[S], empty[S];
     const K1Args<R>& a = ta.a;

@@ -86,13 +86,21 @@ def test_compact_bitwise_equals_explicit(V, O, precision, rho, layout, monkeypat
     assert np.array_equal(a["v_t"], b["v_t"])
 
 
-def test_tiles_cover_every_colour(V, O, monkeypatch):
-    """64-vertex tiles per colour; every neighbour list fits the 16-bit local index."""
+@pytest.mark.parametrize("tv", [64, 32])
+def test_tiles_cover_every_colour(V, O, monkeypatch, tv):
+    """64-vertex tiles per colour (32 for small scenes); every neighbour list fits the 16-bit
+    local index; and the two tile sizes give bitwise the same steps."""
     m, s = beam_sys(O, 21, 9, 7)
+    monkeypatch.setenv("VBD_TILE_V", str(tv))
+    monkeypatch.setenv("VBD_RESIDENT", "0")
     ctx = make_ctx(V, O, s, "fp32", "auto", monkeypatch)
     counts = ctx.color_counts()
-    assert ctx.info.tiles == sum((c + 63) // 64 for c in counts)
+    assert ctx.info.tiles == sum((c + tv - 1) // tv for c in counts)
     assert 0 < ctx.info.tile_nbr_cap < 65536
+    b_ctx = make_ctx(V, O, s, "fp32", "explicit", monkeypatch)
+    monkeypatch.delenv("VBD_TILE_V")
+    monkeypatch.delenv("VBD_RESIDENT")
+    assert np.array_equal(steps(ctx, s, 3)["x"], steps(b_ctx, s, 3)["x"])
 
 
 def test_compact_bitwise_equals_explicit_line_search(V, O, monkeypatch):
