@@ -260,7 +260,8 @@ int vbd_descend(vbd_ctx* ctx, int32_t method, int32_t n_iters, double h, double 
 /* average device time of one colour-pass launch per colour over `reps` sweeps, colours in step
  * order (one CUDA event pair per launch on the context stream); ms has room for num_colors values */
 /* Diagnostics (VBD_RES_DBG=8 at context creation): K1R's pass timeline of CTA 0 in the last
-   step, 4 clock64 stamps per pass {start, last sweep end, last push end, barrier exit}. */
+   step, 5 clock64 values per pass {start, last sweep end, last push end, barrier exit, the
+   longest single group's sweep end -> push end}. */
 int vbd_resident_timeline(vbd_ctx* ctx, int64_t* out, int64_t cap, int64_t* n);
 int vbd_profile_color_pass(vbd_ctx* ctx, double h, int32_t reps, double* ms);
 

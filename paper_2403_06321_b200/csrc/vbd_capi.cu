@@ -1599,7 +1599,7 @@ template <typename R> void ensure_resident(vbd_ctx* c)
     upload(c->res_col_grp, col_grp.data(), col_grp.size(), s);
     upload(c->res_push, push.data(), std::max<size_t>(push.size(), 1), s);
     if (getenv("VBD_RES_DBG") && (atoi(getenv("VBD_RES_DBG")) & 8))  // diagnostics: pass timeline
-        c->res_prof.alloc((size_t)32 * (4096 * (c->ncolors + 1) + 1));
+        c->res_prof.alloc((size_t)40 * (4096 * (c->ncolors + 1) + 1));
     c->res_bar.alloc(16);
     CK(cudaMemsetAsync(c->res_bar.p, 0, 16, s));
     CK(cudaStreamSynchronize(s));
@@ -1633,7 +1633,7 @@ template <typename R> void launch_resident(vbd_ctx* c)
     ra.dbg = getenv("VBD_RES_DBG") ? atoi(getenv("VBD_RES_DBG")) : 0;
     if (ra.dbg & 3) ra.a.flag = ra.s.flag = nullptr;  // (garbage positions in the timing experiments)
     ra.prof = nullptr;
-    if ((ra.dbg & 8) && c->res_prof.bytes >= (size_t)32 * (c->cur.n_max * (c->ncolors + 1) + 1))
+    if ((ra.dbg & 8) && c->res_prof.bytes >= (size_t)40 * (c->cur.n_max * (c->ncolors + 1) + 1))
         ra.prof = c->res_prof.as<long long>();  // CTA 0's pass timeline (vbd_resident_timeline)
     const bool um = c->vmat.p && c->uniform_mat;
     const bool repl = c->res_mode == 1;

@@ -51,7 +51,8 @@ template <typename R> struct ResArgs {
     int dbg;                    // timing experiments only (VBD_RES_DBG, wrong results): 1 no DSMEM
                                 // pushes, 2 no entry sweep, 3 neither; 8: CTA 0's pass timeline
                                 // (clock64, results unchanged) into prof
-    long long* prof;            // dbg & 8: per pass {start, last sweep end, last push end, barrier exit}
+    long long* prof;            // dbg & 8: per pass {start, last sweep end, last push end, barrier exit,
+                                // longest single group's sweep end -> push end}
 };
 
 // shared memory of one CTA (bytes; every region 16-byte aligned)
@@ -202,14 +203,14 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
     const unsigned kb = smem_u32(skind);
     const int vi = lane & 7, j = lane >> 3;  // lane = 8 j + vi serves entry positions j, j + 4, ...
     const R4 zero4{};
-    __shared__ unsigned long long prof_t[2];
+    __shared__ unsigned long long prof_t[3];
     const bool prof = (ra.dbg & 8) && cta == 0 && ra.prof;
     int pass = 0;
     for (int it = 1; it <= ra.n_max; ++it) {
         for (int c = 0; c < ra.ncolors; ++c) {
             if (prof && tid == 0) {
-                prof_t[0] = prof_t[1] = 0;
-                ra.prof[4 * pass] = (long long)clock64();
+                prof_t[0] = prof_t[1] = prof_t[2] = 0;
+                ra.prof[5 * pass] = (long long)clock64();
             }
             if (prof) __syncthreads();
             for (int gi = scg[c] + warp; gi < scg[c + 1]; gi += NW) {
@@ -301,7 +302,8 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
                     dsc = r[9];
                     opd = r[10];
                 }
-                if (prof && lane == 0) atomicMax(&prof_t[0], (unsigned long long)clock64());
+                const unsigned long long t_sw = prof ? (unsigned long long)clock64() : 0ull;
+                if (prof && lane == 0) atomicMax(&prof_t[0], t_sw);
                 // the 4 lanes of a vertex are vi + 8 j: butterfly j ^ 2, then j ^ 1 (4-lane K1 order)
 #pragma unroll
                 for (int o = 16; o >= 8; o >>= 1) {
@@ -337,6 +339,10 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
                         stcg4(s.pos + v, nx);
                     }
                 }
+                if (prof) {
+                    __syncwarp();
+                    if (lane == 0) atomicMax(&prof_t[2], (unsigned long long)clock64() - t_sw);
+                }
             }
             // K3 of this iteration (after its last colour pass): the history copy and the
             // finite check of the chunk; with a blend it is a pass of its own
@@ -355,9 +361,10 @@ __global__ void __launch_bounds__(VBD_RES_THREADS, 1) k_step_resident(const ResA
             if (prof && lane == 0) atomicMax(&prof_t[1], (unsigned long long)clock64());
             barrier();
             if (prof && tid == 0) {
-                ra.prof[4 * pass + 1] = (long long)prof_t[0];
-                ra.prof[4 * pass + 2] = (long long)prof_t[1];
-                ra.prof[4 * pass + 3] = (long long)clock64();
+                ra.prof[5 * pass + 1] = (long long)prof_t[0];
+                ra.prof[5 * pass + 2] = (long long)prof_t[1];
+                ra.prof[5 * pass + 3] = (long long)clock64();
+                ra.prof[5 * pass + 4] = (long long)prof_t[2];
             }
             ++pass;
             if (copy_here) {
