@@ -147,6 +147,10 @@ typedef struct {
     int32_t resident_ctas;     /* K1R: CTAs (cluster size for 1, SMs for 2) */
     int64_t contact_graph_steps;     /* contact steps run as one captured graph */
     int64_t contact_graph_fallbacks; /* ... rolled back and redone on the host path (capacity) */
+    int64_t class_vertices;    /* K1T: solved vertices swept in grid-class tiles */
+    int32_t class_tiles;       /* K1T: grid-class tiles (one lane per vertex, register-resident
+                                  neighbours) */
+    int32_t class_records;     /* K1T: kind records staged per class position */
 } vbd_ctx_info;
 
 /* ---- context ---------------------------------------------------------------------------- */

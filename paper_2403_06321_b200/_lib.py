@@ -69,7 +69,8 @@ class CtxInfo(ctypes.Structure):
                 ("tile_slots", i64), ("tile_nbr_refs", i64), ("tile_lanes", i32),
                 ("tile_stages", i32), ("tile_ent_cap", i32), ("tile_smem_bytes", i32),
                 ("resident", i32), ("resident_ctas", i32),
-                ("contact_graph_steps", i64), ("contact_graph_fallbacks", i64)]
+                ("contact_graph_steps", i64), ("contact_graph_fallbacks", i64),
+                ("class_vertices", i64), ("class_tiles", i32), ("class_records", i32)]
 
 
 # name -> (restype, argtypes); must match include/vbd_b200.h (checked by tests)

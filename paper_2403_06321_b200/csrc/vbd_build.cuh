@@ -8,6 +8,7 @@
 //   * K6: the colour-major re-pack into the entry planes consumed by K1.
 #pragma once
 #include "vbd_common.cuh"
+#include "vbd_grid_classes.cuh"
 
 // ---------------------------------------------------------------------------------------
 // procedural beams
@@ -335,12 +336,14 @@ __global__ void k_iota(int* __restrict__ a, long long n)
 // solved: class 0 / 1 = slab boundary vertex facing the left / right neighbour, 2 = interior;
 // ghost: class 0 / 1 = ghost plane on the left / right.  Boundary and ghost blocks are ordered
 // by vertex id (so a rank's boundary block matches the neighbour's ghost block element for
-// element); interior vertices by (rounds = ceil(d/W), spatial rank i -> order0[i]).
+// element); interior vertices by (rounds = ceil(d/W), spatial rank i -> order0[i]); vertices of
+// a grid-class instance (vinst, K1T class tiles) by (0x80 | instance, spatial rank), so each
+// (colour, instance) is one contiguous run.
 // halo: 0 none, 1 boundary-left, 2 boundary-right, 3 ghost-left, 4 ghost-right (may be null)
 __global__ void k_order_keys(const long long* __restrict__ off, const unsigned char* __restrict__ kind,
                              const unsigned char* __restrict__ halo, const int* __restrict__ color,
                              const int* __restrict__ order0, long long n, int W,
-                             unsigned long long* __restrict__ keys)
+                             unsigned long long* __restrict__ keys, const signed char* __restrict__ vinst = nullptr)
 {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -353,7 +356,8 @@ __global__ void k_order_keys(const long long* __restrict__ off, const unsigned c
         cls = hv == 1 ? 0ull : (hv == 2 ? 1ull : 2ull);
         if (cls == 2) {
             long long d = off[v + 1] - off[v];
-            r = (unsigned long long)((d + W - 1) / W) & 0xffull;
+            r = (unsigned long long)min((d + W - 1) / W, 0x7fLL);
+            if (vinst && vinst[v] >= 0) r = 0x80ull | (unsigned long long)vinst[v];  // K1T class tiles
             low = (unsigned long long)i;
         } else {
             low = (unsigned long long)v;
@@ -687,15 +691,79 @@ __global__ void k_max_degree(const long long* __restrict__ eoff, long long n, in
     if (i < n) atomicMax(out, (int)(eoff[i + 1] - eoff[i]));
 }
 
-// Entry order within a vertex: sorted by a hash of the entry's kind key (the exact rest data
-// the layouts deduplicate), ties in ascending (tet, slot) order.  Vertices of one class of a
-// structured grid then list the same kinds in the same order, so the lanes of a K1T
-// quarter-warp (same entry position, 8 vertices) read the same kind record (smem broadcast).
-// Every layout is packed from this one order, so they stay bitwise equal.
+// Rest-edge sign pattern of an entry (vertex role sl of tet t): E = W^-1 over the other three
+// slot rows, column j = (w_{j+1} x w_{j+2}) / det W; each component's sign {-, 0, +} -> digit
+// {0, 1, 2}, code = sum digit(E_j[k]) 3^(3 j + k) (< 3^9).  Zero below 1e-9 of the largest
+// cofactor (a structured grid's axis-aligned edges).  tools/gen_grid_classes.py computes the
+// same code from rest positions.
+__device__ __forceinline__ unsigned entry_code(const double* __restrict__ w12, int sl)
+{
+    double w[9];
+    int j = 0;
+    for (int q = 0; q < 4; ++q) {
+        if (q == sl) continue;
+        for (int b = 0; b < 3; ++b) w[3 * j + b] = w12[3 * q + b];
+        ++j;
+    }
+    double cr[9], m = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        const double* a = w + 3 * ((c + 1) % 3);
+        const double* b = w + 3 * ((c + 2) % 3);
+        cr[3 * c + 0] = a[1] * b[2] - a[2] * b[1];
+        cr[3 * c + 1] = a[2] * b[0] - a[0] * b[2];
+        cr[3 * c + 2] = a[0] * b[1] - a[1] * b[0];
+    }
+    for (int i = 0; i < 9; ++i) m = fmax(m, fabs(cr[i]));
+    const double det = w[0] * cr[0] + w[1] * cr[1] + w[2] * cr[2];
+    const double tol = 1e-9 * m;
+    unsigned code = 0, p = 1;
+    for (int i = 0; i < 9; ++i, p *= 3) {
+        const unsigned d = fabs(cr[i]) <= tol ? 1u : ((cr[i] > 0.0) == (det > 0.0) ? 2u : 0u);
+        code += d * p;
+    }
+    return code;
+}
+
+// the kind hash of an entry (the exact rest data + material the layouts deduplicate)
+template <typename R>
+__device__ __forceinline__ unsigned entry_kind_hash(const double* __restrict__ tet_w, const double* __restrict__ vol,
+                                                    const int* __restrict__ tmat, long long t, int sl)
+{
+    unsigned key[KindKey<R>::KW];
+    int j = 0;
+    for (int q = 0; q < 4; ++q) {
+        if (q == sl) continue;
+        for (int b = 0; b < 3; ++b) {
+            const double w = tet_w[12 * t + 3 * q + b];
+            if constexpr (sizeof(R) == 4) {
+                key[3 * j + b] = __float_as_uint((float)w);
+            } else {
+                key[2 * (3 * j + b)] = (unsigned)__double2loint(w);
+                key[2 * (3 * j + b) + 1] = (unsigned)__double2hiint(w);
+            }
+        }
+        ++j;
+    }
+    if constexpr (sizeof(R) == 8) {
+        key[18] = (unsigned)__double2loint(vol[t]);
+        key[19] = (unsigned)__double2hiint(vol[t]);
+    }
+    key[KindKey<R>::KW - 1] = (unsigned)tmat[t];
+    return kind_hash<KindKey<R>::KW>(key);
+}
+
+// Entry order within a vertex: by the entry's rest-edge sign pattern (entry_code), then by a
+// hash of its kind key (the exact rest data the layouts deduplicate), ties in ascending (tet,
+// slot) order.  Interior vertices of one class of a structured grid then list the same kinds
+// in the same order -- independent of spacing and material -- so the lanes of a K1T
+// quarter-warp (same entry position, 8 vertices) read the same kind record (smem broadcast),
+// and K1T's class tiles can address the entries' neighbours by compile-time indices
+// (vbd_grid_classes.cuh).  Every layout is packed from this one order, so they stay bitwise equal.
 template <typename R>
 __global__ void k_inc_kind_keys(const long long* __restrict__ off, const unsigned* __restrict__ inc,
                                 const double* __restrict__ tet_w, const double* __restrict__ vol,
-                                const int* __restrict__ tmat, long long n, unsigned long long* __restrict__ keys)
+                                const int* __restrict__ tmat, long long n, unsigned long long* __restrict__ keys,
+                                int by_code = 1)
 {
     const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (v >= n) return;
@@ -703,26 +771,92 @@ __global__ void k_inc_kind_keys(const long long* __restrict__ off, const unsigne
         const unsigned val = inc[k];
         const long long t = val >> 2;
         const int sl = (int)(val & 3u);
-        unsigned key[KindKey<R>::KW];
-        int j = 0;
-        for (int q = 0; q < 4; ++q) {
-            if (q == sl) continue;
-            for (int b = 0; b < 3; ++b) {
-                const double w = tet_w[12 * t + 3 * q + b];
-                if constexpr (sizeof(R) == 4) {
-                    key[3 * j + b] = __float_as_uint((float)w);
-                } else {
-                    key[2 * (3 * j + b)] = (unsigned)__double2loint(w);
-                    key[2 * (3 * j + b) + 1] = (unsigned)__double2hiint(w);
-                }
-            }
-            ++j;
+        const unsigned h = entry_kind_hash<R>(tet_w, vol, tmat, t, sl);
+        if (!by_code) {  // (VBD_ENTRY_ORDER=hash: the kind hash alone; no class tiles)
+            keys[k] = ((unsigned long long)v << 32) | h;
+            continue;
         }
-        if constexpr (sizeof(R) == 8) {
-            key[18] = (unsigned)__double2loint(vol[t]);
-            key[19] = (unsigned)__double2hiint(vol[t]);
-        }
-        key[KindKey<R>::KW - 1] = (unsigned)tmat[t];
-        keys[k] = ((unsigned long long)v << 32) | kind_hash<KindKey<R>::KW>(key);
+        const unsigned code = entry_code(tet_w + 12 * t, sl);
+        keys[k] = ((unsigned long long)v << 32) | ((unsigned long long)code << 17) | (h & 0x1ffffu);
     }
+}
+
+// Grid-class detection (original vertex order, after the entry sort): a vertex is of class c
+// (vbd_grid_classes.cuh) when its entry count, every entry's pattern code and the neighbour
+// identity implied by the class's local indices all match.  out_key = (c + 1) << 32 | a hash of
+// its entries' kind hashes (the class instance: the same kinds at every position), else 0.
+template <typename R>
+__global__ void k_vertex_class(const long long* __restrict__ off, const unsigned* __restrict__ inc,
+                               const int* __restrict__ tets, const double* __restrict__ tet_w,
+                               const double* __restrict__ vol, const int* __restrict__ tmat, long long n,
+                               unsigned long long* __restrict__ out_key)
+{
+    const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const long long e0 = off[v];
+    const int d = (int)(off[v + 1] - e0);
+    unsigned long long res = 0ull;
+    for (int c = 0; c < VBD_GC_N && !res; ++c) {
+        const int b = vbd_gc_beg[c];
+        if (d != vbd_gc_beg[c + 1] - b) continue;
+        int loc[VBD_GC_MAXNL];
+        for (int i = 0; i < VBD_GC_MAXNL; ++i) loc[i] = -1;
+        bool ok = true;
+        unsigned h = 0x811c9dc5u;
+        for (int q = 0; q < d && ok; ++q) {
+            const unsigned val = inc[e0 + q];
+            const long long t = val >> 2;
+            const int sl = (int)(val & 3u);
+            if (entry_code(tet_w + 12 * t, sl) != vbd_gc_code[b + q]) {
+                ok = false;
+                break;
+            }
+            int r = 0;
+            for (int q4 = 0; q4 < 4; ++q4) {
+                if (q4 == sl) continue;
+                const int id = tets[4 * t + q4];
+                const int li = vbd_gc_nbr[3 * (b + q) + r];
+                if (loc[li] < 0) loc[li] = id;
+                else if (loc[li] != id) ok = false;
+                ++r;
+            }
+            h = (h ^ entry_kind_hash<R>(tet_w, vol, tmat, t, sl)) * 0x01000193u;
+        }
+        if (ok) res = ((unsigned long long)(c + 1) << 32) | h;
+    }
+    out_key[v] = res;
+}
+
+// the distinct nonzero class keys into a small open-addressing table (cap slots, 0 = empty);
+// *overflow set when more than cap distinct keys
+__global__ void k_class_keys_insert(const unsigned long long* __restrict__ key, long long n,
+                                    unsigned long long* __restrict__ table, int cap, int* __restrict__ overflow)
+{
+    const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const unsigned long long k = key[v];
+    if (!k) return;
+    unsigned s = (unsigned)((k * 0x9e3779b97f4a7c15ull) >> 40) % (unsigned)cap;
+    for (int p = 0; p < cap; ++p, s = (s + 1) % (unsigned)cap) {
+        unsigned long long cur = *(volatile unsigned long long*)(table + s);
+        if (cur == k) return;
+        if (cur == 0ull) {
+            cur = atomicCAS(table + s, 0ull, k);
+            if (cur == 0ull || cur == k) return;
+        }
+    }
+    atomicExch(overflow, 1);
+}
+
+// per vertex: its class instance (index of its key in the host-sorted key list), or -1
+__global__ void k_class_instance(const unsigned long long* __restrict__ key, long long n,
+                                 const unsigned long long* __restrict__ sorted, int nkeys, signed char* __restrict__ inst)
+{
+    const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const unsigned long long k = key[v];
+    int r = -1;
+    for (int i = 0; i < nkeys && k; ++i)
+        if (sorted[i] == k) r = i;
+    inst[v] = (signed char)r;
 }

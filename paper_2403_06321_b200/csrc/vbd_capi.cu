@@ -297,6 +297,21 @@ struct vbd_ctx {
     // and the per-entry constants and rest edges are derived on the fly (as the explicit K1 does)
     bool tile_xr = false;
     int tile_vpt = 64;  // K1T vertices per tile (64, or 32 for small scenes)
+    // K1T class tiles (fp32 grids, vbd_grid_classes.cuh): the solved vertices of one grid-class
+    // instance (class + the kinds at every entry position) form one run per colour
+    struct ClassRun {
+        long long beg, cnt;
+        int inst;
+    };
+    std::vector<ClassRun> crun;
+    std::vector<int> cinst_tpl;  // class of instance i
+    int tile_svpt = 64;          // stage capacity for x / x_t / y (128 with class tiles)
+    bool tile_xtg = false;       // class tiles: x_t / y not staged (read by the consumers)
+    int ncrec = 0;               // class records after the kind table's zero record
+    DBuf ckind;                  // kind id of every class record
+    long long class_vertices = 0;
+    int class_tiles = 0;
+    std::vector<int> tile_cls_beg;  // first class tile of colour c (after its plain tiles)
     DBuf xrows;
     // K1R resident whole-step kernel (small scenes): 0 off, 1 REPL (one cluster, position
     // replicas in shared memory), 2 GLOB (one CTA per SM, grid barrier); -1 not decided yet
@@ -657,19 +672,94 @@ template <typename R> void build_tiles(vbd_ctx* c)
     if ((long long)VPT * c->max_deg * 3 > VBD_TILE_SORT) return;
     c->tile_w = W;
     cudaStream_t s = c->stream;
-    std::vector<int> v0, nv;
+    // K1T class tiles (fp32 displacement state, one material per vertex, 2-lane 64-vertex tiles):
+    // the runs of grid-class instances (pack) are cut into 128-vertex tiles of one lane per
+    // vertex whose slots are the vertices' neighbour offsets in class order (k_class_pseudo)
+    const char* cle = getenv("VBD_TILE_CLASS");
+    const char* kge0 = getenv("VBD_TILE_KG");
+    bool cls = sizeof(R) == 4 && c->disp && c->uniform_mat && !xr && W == 2 && VPT == 64 && !c->crun.empty() &&
+               !(cle && *cle == '0') && !(kge0 && *kge0 == '1');
+    c->ncrec = 0;
+    c->class_tiles = 0;
+    c->class_vertices = 0;
+    std::vector<int> irec;  // first class record of instance i
+    if (cls) {
+        const int ninst = (int)c->cinst_tpl.size();
+        std::vector<int> ck;
+        for (int i = 0; i < ninst && cls; ++i) {
+            irec.push_back((int)ck.size());
+            const int ne = vbd_gc_ne_host[c->cinst_tpl[i]];
+            long long vb = -1;
+            for (const auto& r : c->crun)
+                if (r.inst == i) {
+                    vb = r.beg;
+                    break;
+                }
+            if (vb < 0) {  // an instance without solved vertices (fixed only): no records needed
+                for (int q = 0; q < ne; ++q) ck.push_back((int)c->nkinds);
+                continue;
+            }
+            const long long e0 = read_scalar<long long>(c->eoff.as<long long>() + vb, s);
+            std::vector<int4> ents(ne);
+            CK(cudaMemcpy(ents.data(), c->ent.as<int4>() + e0, ne * sizeof(int4), cudaMemcpyDeviceToHost));
+            for (int q = 0; q < ne; ++q) ck.push_back(ents[q].w);
+        }
+        c->ncrec = (int)ck.size();
+        if ((long long)(c->nkinds + 1 + c->ncrec) * TileSmem<R>::KSTRIDE > 32768) cls = false;
+        if (cls) upload(c->ckind, ck.data(), ck.size(), s);
+        else c->ncrec = 0;
+    }
+    std::vector<int> v0, nv, tcw;
+    std::vector<signed char> tw;
+    auto cut = [&](long long from, long long to, int per, int inst) {
+        for (long long o = from; o < to; o += per) {
+            v0.push_back((int)o);
+            nv.push_back((int)std::min<long long>(per, to - o));
+            tw.push_back((signed char)(inst >= 0 ? 1 : W));
+            tcw.push_back(inst >= 0 ? (c->cinst_tpl[inst] + 1) |
+                                          ((int)((c->nkinds + 1 + irec[inst]) * TileSmem<R>::KSTRIDE) << 16)
+                                    : 0);
+            if (inst >= 0) {
+                c->class_tiles++;
+                c->class_vertices += std::min<long long>(per, to - o);
+            }
+        }
+    };
     c->tile_beg.assign(c->ncolors + 1, 0);
     for (int col = 0; col < c->ncolors; ++col) {
         c->tile_beg[col] = (int)v0.size();
-        for (long long o = 0; o < c->ccnt[col]; o += VPT) {
-            v0.push_back((int)(c->cbeg[col] + o));
-            nv.push_back((int)std::min<long long>(VPT, c->ccnt[col] - o));
+        const long long b = c->cbeg[col], e = b + c->ccnt[col];
+        long long p = b;
+        for (const auto& r : c->crun) {
+            if (!cls || r.beg < b || r.beg >= e) continue;
+            cut(p, r.beg, VPT, -1);
+            cut(r.beg, r.beg + r.cnt, 128, r.inst);
+            p = r.beg + r.cnt;
         }
+        cut(p, e, VPT, -1);
     }
+
     const int nt = (int)v0.size();
     c->tile_beg[c->ncolors] = nt;
+    // per colour: its plain tiles, then its class runs (instances sort after every plain vertex)
+    c->tile_cls_beg.assign(c->ncolors, 0);
+    for (int col = 0; col < c->ncolors; ++col) {
+        int t = c->tile_beg[col];
+        while (t < c->tile_beg[col + 1] && tcw[t] == 0) ++t;
+        c->tile_cls_beg[col] = t;
+        for (int u = t; u < c->tile_beg[col + 1]; ++u)
+            if (!tcw[u]) fail(VBD_ERR_INTERNAL, "class tiles: a plain tile after a class run");
+    }
+    c->tile_svpt = cls ? 128 : VPT;
+    c->tile_xtg = cls;
     upload(c->tv0, v0.data(), v0.size(), s);
     upload(c->tnv, nv.data(), nv.size(), s);
+    DBuf dtw, dtcw;
+    if (cls) {
+        upload(dtw, tw.data(), tw.size(), s);
+        upload(dtcw, tcw.data(), tcw.size(), s);
+    }
+    const signed char* tWp = cls ? dtw.as<signed char>() : nullptr;
     DBuf cnt, err;
     cnt.alloc((size_t)nt * 16);
     err.alloc(4);
@@ -681,14 +771,50 @@ template <typename R> void build_tiles(vbd_ctx* c)
         CK(cudaGetLastError());
     }
     const int4* cent = xr ? xids.as<int4>() : c->ent.as<int4>();
+    const long long* eoffb = c->eoff.as<long long>();
+    DBuf eoff2, cent2;  // class tiles: pseudo entries (k_class_pseudo)
+    if (cls) {
+        DBuf vtpl, vins, deg2, cerr;
+        vtpl.alloc(c->nsolve);
+        vins.alloc(c->nsolve);
+        CK(cudaMemsetAsync(vtpl.p, 0xff, c->nsolve, s));
+        CK(cudaMemsetAsync(vins.p, 0xff, c->nsolve, s));
+        for (const auto& r : c->crun) {
+            CK(cudaMemsetAsync(vtpl.as<char>() + r.beg, c->cinst_tpl[r.inst], r.cnt, s));
+            CK(cudaMemsetAsync(vins.as<char>() + r.beg, r.inst, r.cnt, s));
+        }
+        deg2.alloc(c->nsolve * 8);
+        k_class_deg<<<blocks_for(c->nsolve), 256, 0, s>>>(c->eoff.as<long long>(), vtpl.as<signed char>(), c->nsolve,
+                                                          deg2.as<long long>());
+        CK(cudaGetLastError());
+        exclusive_offsets(deg2.as<long long>(), c->nsolve, eoff2, s);
+        const long long E2 = read_scalar<long long>(eoff2.as<long long>() + c->nsolve, s);
+        cent2.alloc((size_t)std::max<long long>(E2, 1) * 16);
+        DBuf direc;
+        upload(direc, irec.data(), irec.size(), s);
+        cerr.alloc(4);
+        CK(cudaMemsetAsync(cerr.p, 0, 4, s));
+        k_class_pseudo<<<blocks_for(c->nsolve), 256, 0, s>>>(
+            c->eoff.as<long long>(), cent, c->nsolve, vtpl.as<signed char>(), vins.as<signed char>(),
+            eoff2.as<long long>(), cent2.as<int4>(), direc.as<int>(), c->ckind.as<int>(), (int)c->nkinds,
+            cerr.as<int>());
+        CK(cudaGetLastError());
+        if (read_scalar<int>(cerr.p, s)) {  // (cannot happen for detected classes) -- plain tiles
+            c->crun.clear();
+            build_tiles<R>(c);
+            return;
+        }
+        eoffb = eoff2.as<long long>();
+        cent = cent2.as<int4>();
+    }
     int P = 256;
-    while (P < VPT * c->max_deg * 3) P <<= 1;
+    while (P < std::max(VPT * c->max_deg, cls ? 128 * VBD_GC_MAXNL : 0) * 3) P <<= 1;
     const size_t sort_smem = (size_t)P * 4;
     CK(cudaFuncSetAttribute(k_tile_nbrs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
     CK(cudaFuncSetAttribute(k_tile_nbrs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
-    k_tile_nbrs<false><<<nt, 256, sort_smem, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
+    k_tile_nbrs<false><<<nt, 256, sort_smem, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), eoffb,
                                                  cent, cnt.as<long long>(), nullptr, nullptr, nullptr, nullptr, W,
-                                                 0u, 0u, 0u, 0u, err.as<int>());
+                                                 0u, 0u, 0u, 0u, err.as<int>(), nullptr, tWp);
     CK(cudaGetLastError());
     if (read_scalar<int>(err.p, s)) return;
     std::vector<long long> hc(2 * (size_t)nt), nls(nt), nss(nt);
@@ -717,7 +843,8 @@ template <typename R> void build_tiles(vbd_ctx* c)
     if (c->tile_kg && W != 2) return;  // compiled for the 2-lane kernel
     c->nbr_cap = (int)mx;
     c->ent_cap = (int)ms;
-    TileSmem<R> L{c->ent_cap, c->nbr_cap, (c->tile_kg || xr) ? -1 : (int)c->nkinds, VPT};
+    TileSmem<R> L{c->ent_cap, c->nbr_cap, (c->tile_kg || xr) ? -1 : (int)c->nkinds + c->ncrec, c->tile_svpt,
+                  c->tile_xtg ? 1 : 3};
     // as many stages (2..4) as fit three CTAs per SM, else two (2-lane: 2 stages)
     const char* oe = getenv("VBD_TILE_OCC");
     c->tile_occ = oe && *oe == '2' ? 2 : 3;  // 3 CTAs per SM (one entry per lane in flight) measured faster
@@ -740,6 +867,7 @@ template <typename R> void build_tiles(vbd_ctx* c)
         stages = 2;
         c->tile_occ = 3;
     }
+    if (cls) stages = std::min(stages, 2);  // the class loop is compiled for the 2-stage ring
     if (xr) {  // K1T-X: 2 stages, 2 CTAs per SM (registers for the rows in flight; measured faster)
         stages = 2;
         if (!(oe && *oe == '3')) c->tile_occ = 2;
@@ -757,14 +885,14 @@ template <typename R> void build_tiles(vbd_ctx* c)
     c->tent.alloc((size_t)std::max<long long>(slots, 1) * 8);
     DBuf slot_entry;  // XR: the explicit entry of every slot (-1: padding)
     if (xr) slot_entry.alloc((size_t)std::max<long long>(slots, 1) * 8);
-    k_tile_nbrs<true><<<nt, 256, sort_smem, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
+    k_tile_nbrs<true><<<nt, 256, sort_smem, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), eoffb,
                                                 cent, nullptr, c->loff.as<long long>(), sbase.as<long long>(),
                                                 c->tnbr.as<int>(), c->tent.as<uint2>(), W,
                                                 PU, (unsigned)(c->nbr_cap * PU),
                                                 xr ? 0u : c->tile_kg ? 1u : TileSmem<R>::KSTRIDE,
                                                 xr ? 0u : c->tile_kg ? (unsigned)c->nkinds
                                                                      : (unsigned)(c->nkinds * TileSmem<R>::KSTRIDE),
-                                                err.as<int>(), xr ? slot_entry.as<long long>() : nullptr);
+                                                err.as<int>(), xr ? slot_entry.as<long long>() : nullptr, tWp);
     CK(cudaGetLastError());
     if (read_scalar<int>(err.p, s)) fail(VBD_ERR_INTERNAL, "tile build failed");
     if (slack > 0) {
@@ -786,11 +914,11 @@ template <typename R> void build_tiles(vbd_ctx* c)
                                                     PU, pad_pos, c->tent.as<uint2>(), asg.as<int>(), vmax, mmax);
             CK(cudaGetLastError());
         }
-        k_tile_banks<<<blocks_for(nt, 64), 64, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
+        k_tile_banks<<<blocks_for(nt, 64), 64, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), eoffb,
                                                       c->loff.as<long long>(), sbase.as<long long>(), dnl.as<int>(),
                                                       nt, W, PU, pad_pos,
                                                       c->tnbr.as<int>(), c->tent.as<uint2>(), ids.as<int>(),
-                                                      asg.as<int>(), dsatur ? 1 : 0);
+                                                      asg.as<int>(), dsatur ? 1 : 0, tWp);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s));
     }
@@ -802,12 +930,18 @@ template <typename R> void build_tiles(vbd_ctx* c)
         c->tile_xr = true;
     }
     c->tdesc.alloc((size_t)nt * sizeof(TileDesc));
-    k_tile_desc<<<blocks_for(nt), 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), c->eoff.as<long long>(),
+    k_tile_desc<<<blocks_for(nt), 256, 0, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), eoffb,
                                               c->loff.as<long long>(), sbase.as<long long>(), nt, W,
-                                              c->tdesc.as<TileDesc>());
+                                              c->tdesc.as<TileDesc>(), tWp, cls ? dtcw.as<int>() : nullptr);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     c->tiles = true;
+}
+
+static bool entry_order_by_code()
+{
+    const char* e = getenv("VBD_ENTRY_ORDER");
+    return !(e && std::string(e) == "hash");
 }
 
 // per-vertex entry order by kind (k_inc_kind_keys): one stable 64-bit radix sort of
@@ -820,7 +954,8 @@ template <typename R> void sort_incidence_by_kind(Scene& sc, cudaStream_t s)
     keys.alloc(n4 * 8);
     k_inc_kind_keys<R><<<blocks_for(sc.n), 256, 0, s>>>(sc.inc_off.as<long long>(), sc.inc.as<unsigned>(),
                                                         sc.tet_w.as<double>(), sc.vol.as<double>(),
-                                                        sc.tmat.as<int>(), sc.n, keys.as<unsigned long long>());
+                                                        sc.tmat.as<int>(), sc.n, keys.as<unsigned long long>(),
+                                                        entry_order_by_code() ? 1 : 0);
     CK(cudaGetLastError());
     sort_pairs_u64_i32(keys, sc.inc, n4, s);
 }
@@ -862,12 +997,57 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
         k_iota<<<blocks_for(sc.n), 256, 0, s>>>(order0.as<int>(), sc.n);
         CK(cudaGetLastError());
     }
+    // grid-class instances (K1T class tiles, fp32): per original vertex its instance or -1
+    DBuf vinst;
+    std::vector<unsigned long long> ikeys;
+    c->crun.clear();
+    c->cinst_tpl.clear();
+    {
+        const char* ce = getenv("VBD_TILE_CLASS");
+        const bool on = sizeof(R) == 4 && sc.n && sc.T && sc.tet_w.p && !(ce && *ce == '0') && entry_order_by_code() &&
+                        !(getenv("VBD_KIND_ORDER") && *getenv("VBD_KIND_ORDER") == '0');
+        if (on) {
+            DBuf ck, table, ovf, sorted;
+            ck.alloc(sc.n * 8);
+            k_vertex_class<R><<<blocks_for(sc.n), 256, 0, s>>>(sc.inc_off.as<long long>(), sc.inc.as<unsigned>(),
+                                                               sc.tets.as<int>(), sc.tet_w.as<double>(),
+                                                               sc.vol.as<double>(), sc.tmat.as<int>(), sc.n,
+                                                               ck.as<unsigned long long>());
+            CK(cudaGetLastError());
+            constexpr int CAP = 256;
+            table.alloc(CAP * 8);
+            ovf.alloc(4);
+            CK(cudaMemsetAsync(table.p, 0, CAP * 8, s));
+            CK(cudaMemsetAsync(ovf.p, 0, 4, s));
+            k_class_keys_insert<<<blocks_for(sc.n), 256, 0, s>>>(ck.as<unsigned long long>(), sc.n,
+                                                                table.as<unsigned long long>(), CAP, ovf.as<int>());
+            CK(cudaGetLastError());
+            std::vector<unsigned long long> ht(CAP);
+            CK(cudaMemcpyAsync(ht.data(), table.p, CAP * 8, cudaMemcpyDeviceToHost, s));
+            const int of = read_scalar<int>(ovf.p, s);
+            for (unsigned long long k : ht)
+                if (k) ikeys.push_back(k);
+            std::sort(ikeys.begin(), ikeys.end());
+            if (of || ikeys.size() > 64) ikeys.clear();  // too many instances: no class tiles
+            if (!ikeys.empty()) {
+                upload(sorted, ikeys.data(), ikeys.size(), s);
+                vinst.alloc(sc.n);
+                k_class_instance<<<blocks_for(sc.n), 256, 0, s>>>(ck.as<unsigned long long>(), sc.n,
+                                                                 sorted.as<unsigned long long>(), (int)ikeys.size(),
+                                                                 vinst.as<signed char>());
+                CK(cudaGetLastError());
+                CK(cudaStreamSynchronize(s));
+                for (unsigned long long k : ikeys) c->cinst_tpl.push_back((int)(k >> 32) - 1);
+            }
+        }
+    }
     DBuf keys;
     keys.alloc(sc.n * 8);
     k_order_keys<<<blocks_for(sc.n), 256, 0, s>>>(sc.inc_off.as<long long>(), sc.kind.as<unsigned char>(),
                                                   sc.halo.p ? sc.halo.as<unsigned char>() : nullptr,
                                                   sc.color.as<int>(), order0.as<int>(), sc.n, c->k1.W,
-                                                  keys.as<unsigned long long>());
+                                                  keys.as<unsigned long long>(),
+                                                  vinst.p ? vinst.as<signed char>() : nullptr);
     CK(cudaGetLastError());
     sort_keys_u64(keys, sc.n, s);
     c->perm.alloc(sc.n * 4);
@@ -897,6 +1077,18 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
         int col = (int)((hk[i] >> 44) & 0xfff);
         c->cbeg[col] = i;
         c->ccnt[col]++;
+    }
+    // class-instance runs: (cat 0, interior class 2, rounds field 0x80 | instance)
+    for (long long i = 0; i < c->nsolve && !c->cinst_tpl.empty(); ++i) {
+        const unsigned cl = (unsigned)((hk[i] >> 40) & 0xf), r = (unsigned)((hk[i] >> 32) & 0xff);
+        if (cl != 2 || !(r & 0x80u)) continue;
+        const int col = (int)((hk[i] >> 44) & 0xfff), inst = (int)(r & 0x7fu);
+        auto& v = c->crun;
+        if (!v.empty() && v.back().inst == inst && v.back().beg + v.back().cnt == i &&
+            (int)((hk[v.back().beg] >> 44) & 0xfff) == col)
+            v.back().cnt++;
+        else
+            v.push_back({i, 1, inst});
     }
     // slab boundary blocks (head of each colour range) and ghost blocks per (side, colour)
     for (int sd = 0; sd < 2; ++sd) {
@@ -1127,7 +1319,8 @@ template <typename R, int W, int U, int B> void launch_k1v(const K1Args<R>& a0, 
     else launch_pdl(k1_color_pass<R, W, U, B, false, false>, nb, 256, 0, s, a);
 }
 
-template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false, bool XR = false, int TV = 64>
+template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false, bool XR = false, int TV = 64,
+          bool CL = false>
 void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
 {
     // the shared-memory opt-in and the occupancy are per device
@@ -1137,14 +1330,14 @@ void launch_k1_tiles_v(const K1TArgs<R>& ta, size_t smem, cudaStream_t s)
     CK(cudaGetDevice(&dev));
     dev &= 63;
     if (smem > attr[dev]) {
-        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC, DEF, KG, XR, TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k1_tiles<R, UM, S, W, OCC, DEF, KG, XR, TV, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[dev] = smem;
         CK(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k1_tiles<R, UM, S, W, OCC, DEF, KG, XR, TV>, TV * W + 32, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k1_tiles<R, UM, S, W, OCC, DEF, KG, XR, TV, CL>, TV * W + 32, smem));
         per_sm[dev] = std::max(1, per_sm[dev]);
     }
     const int grid = std::min(ta.tcount, per_sm[dev] * sms[dev]);
-    launch_pdl(k1_tiles<R, UM, S, W, OCC, DEF, KG, XR, TV>, (unsigned)grid, TV * W + 32, smem, s, ta);
+    launch_pdl(k1_tiles<R, UM, S, W, OCC, DEF, KG, XR, TV, CL>, (unsigned)grid, TV * W + 32, smem, s, ta);
 }
 
 template <typename R, bool UM, int W>
@@ -1202,9 +1395,15 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
     if (ta.dbg) ta.a.flag = nullptr;  // garbage positions in the timing experiments
     static const bool early = !(getenv("VBD_PDL_EARLY") && *getenv("VBD_PDL_EARLY") == '0');
     ta.early = early ? 1 : 0;
+    ta.ckind = c->ncrec ? c->ckind.as<int>() : nullptr;
+    ta.ncrec = c->ncrec;
+    ta.svpt = c->tile_svpt;
     ta.xrows = c->tile_xr ? c->xrows.as<float>() : nullptr;
     ta.xstride = c->tile_xr ? (long long)(c->tent.bytes / 8) : 0;
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (c->tile_kg || c->tile_xr) ? -1 : ta.nkinds, c->tile_vpt};
+    ta.xtg = c->tile_xtg ? 1 : 0;
+    ta.tcls = c->class_tiles ? c->tile_cls_beg[col] - ta.tbeg : ta.tcount;
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (c->tile_kg || c->tile_xr) ? -1 : ta.nkinds + ta.ncrec,
+                        c->tile_svpt, c->tile_xtg ? 1 : 3};
     const int S = c->tile_stages;
     if (c->tile_vpt == 32) {  // small scenes: 32-vertex tiles (2 lanes, 2 stages, deferred solves)
         if (c->tile_w != 2 || S != 2 || c->tile_kg || c->tile_xr || c->tile_occ != 3 || !c->tile_defer)
@@ -1220,6 +1419,16 @@ template <typename R> bool launch_k1_tiles(const vbd_ctx* c, const K1Args<R>& a,
             else launch_k1_tiles_v<R, true, 2, 2, 2, 2, false, true>(ta, L.total(S), s);
         }
         return true;
+    }
+    if (c->class_tiles) {  // (build_tiles: fp32, one material per vertex, 2 lanes, 2 stages)
+        if constexpr (sizeof(R) == 4) {
+            if (!a.vmat || c->tile_w != 2 || c->tile_kg || S != 2) fail(VBD_ERR_INTERNAL, "class tiles: configuration");
+            const size_t sm = L.total(S);
+            if (c->tile_occ == 2) launch_k1_tiles_v<R, true, 2, 2, 2, 2, false, false, 64, true>(ta, sm, s);
+            else if (c->tile_defer) launch_k1_tiles_v<R, true, 2, 2, 3, 2, false, false, 64, true>(ta, sm, s);
+            else launch_k1_tiles_v<R, true, 2, 2, 3, 1, false, false, 64, true>(ta, sm, s);
+            return true;
+        }
     }
     if (a.vmat) launch_k1_tiles_w<R, true>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, c->tile_kg, L.total(S), s);
     else launch_k1_tiles_w<R, false>(ta, c->tile_w, S, c->tile_occ, c->tile_defer, c->tile_kg, L.total(S), s);
@@ -3013,9 +3222,9 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         info->tile_stages = c->tiles ? c->tile_stages : 0;
         info->tile_ent_cap = c->tiles ? c->ent_cap : 0;
         if (c->tiles) {
-            const int kn = (c->tile_kg || c->tile_xr) ? -1 : (int)c->nkinds;
-            const TileSmem<float> L32{c->ent_cap, c->nbr_cap, kn, c->tile_vpt};
-            const TileSmem<double> L64{c->ent_cap, c->nbr_cap, kn, c->tile_vpt};
+            const int kn = (c->tile_kg || c->tile_xr) ? -1 : (int)c->nkinds + c->ncrec;
+            const TileSmem<float> L32{c->ent_cap, c->nbr_cap, kn, c->tile_svpt, c->tile_xtg ? 1 : 3};
+            const TileSmem<double> L64{c->ent_cap, c->nbr_cap, kn, c->tile_svpt, c->tile_xtg ? 1 : 3};
             info->tile_smem_bytes = (int)(c->precision == VBD_PREC_F64 ? L64.total(c->tile_stages)
                                                                        : L32.total(c->tile_stages));
         }
@@ -3024,6 +3233,9 @@ int vbd_ctx_get_info(vbd_ctx* c, vbd_ctx_info* info)
         info->resident_ctas = c->res_mode > 0 ? c->res_ncta : 0;
         info->contact_graph_steps = c->cg_steps;
         info->contact_graph_fallbacks = c->cg_fallbacks;
+        info->class_vertices = c->tiles ? c->class_vertices : 0;
+        info->class_tiles = c->tiles ? c->class_tiles : 0;
+        info->class_records = c->tiles ? c->ncrec : 0;
     });
 }
 

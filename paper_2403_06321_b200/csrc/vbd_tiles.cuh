@@ -21,6 +21,7 @@
 // every other K1 variant.
 #pragma once
 #include "vbd_kernels.cuh"
+#include "vbd_grid_classes.cuh"
 
 #define VBD_TILE_SORT 32768  // max neighbour references (3 per entry) per tile for the build
 
@@ -56,12 +57,14 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
                                                    const long long* __restrict__ sbase, int* __restrict__ tnbr,
                                                    uint2* __restrict__ tent, int W, unsigned r4b,
                                                    unsigned pad_pos, unsigned kstride, unsigned pad_kind, int* err,
-                                                   long long* __restrict__ slot_entry = nullptr)
+                                                   long long* __restrict__ slot_entry = nullptr,
+                                                   const signed char* __restrict__ tw = nullptr)
 {
     extern __shared__ int keys[];  // next power of two >= max references per tile
     __shared__ int part[257];
     __shared__ int wslot[9];
     const int t = blockIdx.x, tid = threadIdx.x;
+    if (tw) W = tw[t];  // class tiles: one lane per vertex
     const int v0 = tv0[t], nv = tnv[t];
     const long long e0 = eoff[v0], e1 = eoff[v0 + nv];
     const int nref = (int)(3 * (e1 - e0));
@@ -170,6 +173,59 @@ __global__ void __launch_bounds__(256) k_tile_nbrs(const int* __restrict__ tv0, 
     }
 }
 
+// K1T class tiles: the tile build's input for a grid-class vertex (vtpl >= 0) is R = ceil(NL / 3)
+// pseudo entries {loc[3r], loc[3r + 1], loc[3r + 2], pad kind} -- its NL distinct neighbours in
+// the class's local order (vbd_grid_classes.cuh), so the slots a lane reads are the shared-memory
+// offsets of its neighbours (bank-placed like any slot); other vertices keep their entries.
+// err: 1 a vertex does not match its class, 2 its kinds differ from its instance's records.
+__global__ void k_class_pseudo(const long long* __restrict__ eoff, const int4* __restrict__ cent, long long nsolve,
+                               const signed char* __restrict__ vtpl, const signed char* __restrict__ vins,
+                               const long long* __restrict__ eoff2, int4* __restrict__ cent2,
+                               const int* __restrict__ irec, const int* __restrict__ ckind, int pad_kind,
+                               int* __restrict__ err)
+{
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nsolve) return;
+    const long long k0 = eoff[i], o = eoff2[i];
+    const int d = (int)(eoff[i + 1] - k0), tpl = vtpl[i];
+    if (tpl < 0) {
+        for (int q = 0; q < d; ++q) cent2[o + q] = cent[k0 + q];
+        return;
+    }
+    const int b = vbd_gc_beg[tpl], ne = vbd_gc_beg[tpl + 1] - b, nl = vbd_gc_nl[tpl];
+    if (d != ne) {
+        atomicExch(err, 1);
+        return;
+    }
+    int loc[VBD_GC_MAXNL];
+    for (int q = 0; q < VBD_GC_MAXNL; ++q) loc[q] = -1;
+    const int* kr = ckind + irec[vins[i]];
+    for (int q = 0; q < ne; ++q) {
+        const int4 e = cent[k0 + q];
+        const int ids[3] = {e.x, e.y, e.z};
+        for (int r = 0; r < 3; ++r) {
+            const int li = vbd_gc_nbr[3 * (b + q) + r];
+            if (loc[li] < 0) loc[li] = ids[r];
+            else if (loc[li] != ids[r]) atomicExch(err, 1);
+        }
+        if (e.w != kr[q]) atomicExch(err, 2);
+    }
+    for (int r = 0; 3 * r < nl; ++r) {
+        const int a = loc[3 * r];
+        cent2[o + r] = make_int4(a, 3 * r + 1 < nl ? loc[3 * r + 1] : a, 3 * r + 2 < nl ? loc[3 * r + 2] : a, pad_kind);
+    }
+}
+
+// class tiles: the tile build's degree of every solved vertex (pseudo rows for class vertices)
+__global__ void k_class_deg(const long long* __restrict__ eoff, const signed char* __restrict__ vtpl, long long n,
+                            long long* __restrict__ deg)
+{
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int t = vtpl[i];
+    deg[i] = t < 0 ? eoff[i + 1] - eoff[i] : (long long)((vbd_gc_nl[t] + 2) / 3);
+}
+
 // K1T-X: {n0, n1, n2, 0} of every explicit fp32 entry (ids without the material bits)
 __global__ void k_plane_ids(const float4* __restrict__ planes, long long E, int4* __restrict__ out)
 {
@@ -209,10 +265,12 @@ __global__ void k_tile_banks(const int* __restrict__ tv0, const int* __restrict_
                              const long long* __restrict__ eoff, const long long* __restrict__ lbase,
                              const long long* __restrict__ sbase, const int* __restrict__ nls, int nt, int W,
                              unsigned r4b, unsigned pad_pos, int* __restrict__ tnbr, uint2* __restrict__ tent,
-                             int* __restrict__ ids, int* __restrict__ asg, int given)
+                             int* __restrict__ ids, int* __restrict__ asg, int given,
+                             const signed char* __restrict__ tw = nullptr)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nt) return;
+    if (tw) W = tw[t];
     const long long l0 = lbase[t], s0 = sbase[t];
     const int nl = nls[t], nlp = (int)(lbase[t + 1] - l0), cap = nlp / 8;
     const int pad_bank = (int)((pad_pos / r4b) & 7u);
@@ -420,10 +478,12 @@ struct __align__(16) TileDescHead {
 
 __global__ void k_tile_desc(const int* __restrict__ tv0, const int* __restrict__ tnv,
                             const long long* __restrict__ eoff, const long long* __restrict__ lbase,
-                            const long long* __restrict__ sbase, int nt, int W, TileDesc* __restrict__ out)
+                            const long long* __restrict__ sbase, int nt, int W, TileDesc* __restrict__ out,
+                            const signed char* __restrict__ tw = nullptr, const int* __restrict__ tcw = nullptr)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nt) return;
+    if (tw) W = tw[t];
     TileDesc d;
     d.v0 = tv0[t];
     d.nv = tnv[t];
@@ -437,6 +497,9 @@ __global__ void k_tile_desc(const int* __restrict__ tv0, const int* __restrict__
         d.wr[w] = r | (pre << 16);
         pre += r;
     }
+    // class tiles (4 consumer warps of 32 vertices, so warp 7 has no rounds): wr[7] =
+    // (class + 1) | (byte offset of the instance's records in the shared table) << 16
+    if (tcw && tcw[t]) d.wr[7] = tcw[t];
     out[t] = d;
 }
 
@@ -454,6 +517,11 @@ template <typename R> struct K1TArgs {
     const float* xrows;  // K1T-X: slot-weight rows, 9 planes of xstride floats in slot order
     long long xstride;
     int early;           // producer loads its first descriptors / ids before the PDL wait
+    const int* ckind;    // class tiles: kind id of every class record (after the zero record)
+    int ncrec;
+    int svpt;            // stage capacity for x / x_t / y (vertices; 128 with class tiles)
+    int xtg;             // x_t / y read from global by the consumers, not staged (class tiles)
+    int tcls;            // class tiles of this colour are [tcls, tcount) (tcount: none)
 };
 
 typedef TileDesc TileHdr;  // the stage header is a copy of the tile's descriptor
@@ -496,6 +564,7 @@ __device__ __forceinline__ void cp_async_mbar_arrive(unsigned bar)
 template <typename R> struct TileSmem {
     typedef typename Vec4<R>::T R4;
     int ent_cap, nbr_cap, nk, vpt;  // vpt: vertices per tile
+    int nxv = 3;  // vertex arrays staged: x, x_t, y (3) or x only (1: x_t / y read from global)
     // kind records (HOT R each), then for fp32 (displacement state) the kinds' rest edges
     // (3 float4 = 48 B each: the same byte offset as the fp32 record, in the second table)
     // fp32 (displacement state): one packed 80-byte SWEEP record per kind, read with 4 LDS.128 +
@@ -513,9 +582,12 @@ template <typename R> struct TileSmem {
     __host__ __device__ size_t off_npos() const { return off_ent() + (size_t)ent_cap * 8; }
     __host__ __device__ size_t off_nzw() const { return off_npos() + (size_t)(nbr_cap + 1) * PU; }
     __host__ __device__ size_t off_x() const { return off_npos() + (size_t)(nbr_cap + 1) * sizeof(R4); }
-    __host__ __device__ size_t off_xt() const { return off_x() + vpt * sizeof(R4); }
-    __host__ __device__ size_t off_y() const { return off_xt() + vpt * sizeof(R4); }
-    __host__ __device__ size_t stage_bytes() const { return (off_y() + vpt * sizeof(R4) + 127) & ~(size_t)127; }
+    __host__ __device__ size_t off_xt() const { return off_x() + (nxv == 3 ? vpt * sizeof(R4) : 0); }
+    __host__ __device__ size_t off_y() const { return off_xt() + (nxv == 3 ? vpt * sizeof(R4) : 0); }
+    __host__ __device__ size_t stage_bytes() const
+    {
+        return (off_x() + (size_t)nxv * vpt * sizeof(R4) + 127) & ~(size_t)127;
+    }
     __host__ __device__ size_t total(int stages) const { return ((kinds_bytes() + 127) & ~(size_t)127) + stages * stage_bytes(); }
 };
 
@@ -572,6 +644,53 @@ __device__ __forceinline__ void k1t_store(const K1Args<R>& a, int v, typename Ve
         atomicMin(a.flag, StepFlag::key((unsigned)*a.stepctr, (unsigned)a.iter, (unsigned)a.perm[v]));
 }
 
+// read-only global loads issued where they stand (volatile: not sunk to their first use)
+__device__ __forceinline__ void ldg_nc(const float4* p, float4& v)
+{
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+}
+__device__ __forceinline__ void ldg_nc(const double4* p, double4& v)
+{
+    v = *p;
+}
+__device__ __forceinline__ float ldg_nc(const float* p)
+{
+    float v;
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ldg_nc(const double* p) { return *p; }
+
+// K1T class tile sweep (one lane per vertex of grid class C, vbd_grid_classes.cuh).  The lane's
+// slots are its vertex's distinct neighbours in class order, 3 per row (bank-placed offsets);
+// each position is loaded once, at its first use, and the class's entries run in position order
+// q from registers with the record at recs + 80 q (the instance's block in the shared table:
+// the same address on every lane, a broadcast).  Entry q goes to accumulator set q mod 4 in
+// increasing q, so (s0 + s2) + (s1 + s3) is exactly the 2-lane path's lane sums + butterfly.
+template <int C>
+__device__ __forceinline__ void class_sweep(const unsigned char* slots, const unsigned char* npos,
+                                            const unsigned char* recs, float2 nxy, float nz, AccXY (&acc)[4])
+{
+    using G = GridClass<C>;
+    float4 P[G::NL];
+    uint2 row[G::R];
+#pragma unroll
+    for (int q = 0; q < G::NE; ++q) {
+#pragma unroll
+        for (int k = 0; k < G::NL; ++k) {
+            if (G::first(k) != q) continue;
+            if (k % 3 == 0) row[k / 3] = *reinterpret_cast<const uint2*>(slots + 256 * (k / 3));
+            const unsigned off = k % 3 == 0 ? (row[k / 3].x & 0xffffu)
+                                            : (k % 3 == 1 ? (row[k / 3].x >> 16) : (row[k / 3].y & 0xffffu));
+            P[k] = *reinterpret_cast<const float4*>(npos + off);
+        }
+        const float4* rec = reinterpret_cast<const float4*>(recs + 80 * q);
+        const float4 e0 = rec[0], e1 = rec[1], e2 = rec[2], c3 = rec[3];
+        const float t[8] = {e0.w, e1.w, e2.w, c3.x, c3.y, c3.z, c3.w, reinterpret_cast<const float*>(rec + 4)[0]};
+        tet_contrib_ec_xy(P[G::nbr(q, 0)], P[G::nbr(q, 1)], P[G::nbr(q, 2)], nxy, nz, e0, e1, e2, t, acc[q & 3]);
+    }
+}
+
 // OCC = CTAs per SM the kernel is compiled for (register budget); OCC >= 3 sweeps one entry
 // per lane at a time (fewer live registers), else two.
 // DEF = W: deferred block solves.  After a tile's butterfly every lane of a vertex holds its
@@ -590,7 +709,10 @@ __device__ __forceinline__ void k1t_store(const K1Args<R>& a, int v, typename Ve
 // (ec_terms, volume_from_rows, rest_edges_from_rows), so results stay bitwise equal to it.
 // TV: vertices per tile (64; 32 for small scenes: twice the CTAs per colour pass, half the
 // gather and sweep per CTA).
-template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false, bool XR = false, int TV = 64>
+// CL: the colour's class tiles run in a second loop (class_sweep); instantiated only for
+// contexts that have class tiles, so the plain kernel keeps its register allocation.
+template <typename R, bool UM, int S, int W, int OCC, int DEF, bool KG = false, bool XR = false, int TV = 64,
+          bool CL = false>
 __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta)
 {
     typedef typename Vec4<R>::T R4;
@@ -600,7 +722,7 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
     __shared__ __align__(8) unsigned long long full[S], empty[S];
     const K1Args<R>& a = ta.a;
     static_assert(!XR || (sizeof(R) == 4 && UM && !KG), "K1T-X: fp32, one material per vertex");
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (KG || XR) ? -1 : ta.nkinds, NCW * VPW};
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (KG || XR) ? -1 : ta.nkinds + ta.ncrec, ta.svpt, ta.xtg ? 1 : 3};
     typedef typename PlaneT<R>::T PL;
     PL* skind = reinterpret_cast<PL*>(smem);
     unsigned char* stages = smem + ((L.kinds_bytes() + 127) & ~(size_t)127);
@@ -612,11 +734,14 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
     constexpr bool DISP = sizeof(R) == 4;  // fp32: displacement state, rest edges per kind
     if (!KG && !XR) {
         if constexpr (DISP) {  // packed fp32 sweep records (TileSmem::KSTRIDE); padding: zero record
+            // (class tiles: the instances' records follow the zero record, ckind[i] for record
+            // nkinds + 1 + i)
             float4* sk = reinterpret_cast<float4*>(smem);
-            for (int i = tid; i < (ta.nkinds + 1) * 5; i += blockDim.x) {
-                const int k = i / 5, q = i % 5;
+            for (int i = tid; i < (ta.nkinds + 1 + ta.ncrec) * 5; i += blockDim.x) {
+                const int k0 = i / 5, q = i % 5;
+                const int k = k0 < ta.nkinds ? k0 : (k0 == ta.nkinds ? -1 : ta.ckind[k0 - ta.nkinds - 1]);
                 float4 v{};
-                if (k < ta.nkinds) {
+                if (k >= 0) {
                     const float* t = reinterpret_cast<const float*>(ta.kinds + (size_t)k * Q);
                     if (q < 3) {
                         v = ta.a.kedge[3 * k + q];
@@ -682,12 +807,23 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
             const unsigned bar = smem_u32(&full[stage]);
             if (lane == 0) {
                 const unsigned eby = (unsigned)d.ne * 8u, vby = (unsigned)(d.nv * sizeof(R4));
-                mbar_expect_tx(bar, (unsigned)sizeof(TileDesc) + eby + 3 * vby);
+                mbar_expect_tx(bar, (unsigned)sizeof(TileDesc) + eby + (unsigned)L.nxv * vby);
                 bulk_g2s(st + L.off_hdr(), ta.desc + ta.tbeg + t, (unsigned)sizeof(TileDesc), bar);
                 if (eby) bulk_g2s(st + L.off_ent(), ta.tent + d.eb, eby, bar);
                 bulk_g2s(st + L.off_x(), a.pos + d.v0, vby, bar);
-                bulk_g2s(st + L.off_xt(), a.xt + d.v0, vby, bar);
-                bulk_g2s(st + L.off_y(), a.y + d.v0, vby, bar);
+                if (L.nxv == 3) {
+                    bulk_g2s(st + L.off_xt(), a.xt + d.v0, vby, bar);
+                    bulk_g2s(st + L.off_y(), a.y + d.v0, vby, bar);
+                } else {  // x_t / y (and the vertices' V mu |w|^2 sums) into L2 for the consumers
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.xt + d.v0), "r"(vby) : "memory");
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.y + d.v0), "r"(vby) : "memory");
+                    if (UM && a.vsv) {  // (16-byte aligned range covering the tile's sums)
+                        const size_t b0 = reinterpret_cast<size_t>(a.vsv + d.v0) & ~(size_t)15;
+                        const size_t b1 = (reinterpret_cast<size_t>(a.vsv + d.v0 + d.nv) + 15) & ~(size_t)15;
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0), "r"((unsigned)(b1 - b0))
+                                     : "memory");
+                    }
+                }
                 if constexpr (XR) {  // the tile's rows into L2 (the consumers stream them next)
 #pragma unroll 1
                     for (int q = 0; q < 9; ++q)
@@ -763,7 +899,14 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
             qv = -1;
         }
     };
-    for (int t = blockIdx.x; t < ta.tcount; t += gridDim.x) {
+    // class tiles (fp32, one material per vertex, 2-lane 64-vertex tiles): wr[7] = (class + 1) |
+    // record block offset << 16; one lane per vertex, 32 vertices per consumer warp
+    constexpr bool CLS = CL && sizeof(R) == 4 && UM && W == 2 && !KG && !XR && TV == 64;
+    static_assert(!CL || CLS, "class tiles: fp32, one material per vertex, 2-lane 64-vertex tiles");
+    // the colour's plain tiles first, then (CLS) its class tiles [tcls, tcount) in a second loop
+    // over the same grid-stride sequence, so the deferral state is dead in the class sweep
+    int t = blockIdx.x;
+    for (; t < (CLS ? ta.tcls : ta.tcount); t += gridDim.x) {
         mbar_wait_parity(smem_u32(&full[stage]), ph);
         const unsigned char* st = stages + stage * L.stage_bytes();
         const TileHdr* hp = reinterpret_cast<const TileHdr*>(st + L.off_hdr());
@@ -774,8 +917,8 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
         const bool act = lv < hnv;
         const int lvc = act ? lv : 0;
         const R4 xi4 = reinterpret_cast<const R4*>(st + L.off_x())[lvc];
-        const R4 xt4 = reinterpret_cast<const R4*>(st + L.off_xt())[lvc];
-        const R4 y4 = reinterpret_cast<const R4*>(st + L.off_y())[lvc];
+        const R4 xt4 = ta.xtg ? a.xt[hv0 + lvc] : reinterpret_cast<const R4*>(st + L.off_xt())[lvc];
+        const R4 y4 = ta.xtg ? a.y[hv0 + lvc] : reinterpret_cast<const R4*>(st + L.off_y())[lvc];
         const R xi[3] = {xi4.x, xi4.y, xi4.z};
         const R dx[3] = {xi[0] - xt4.x, xi[1] - xt4.y, xi[2] - xt4.z};
         // NA = 4 / W accumulator sets: with W = 2, lane j sums entry positions j mod 4 (even
@@ -1022,4 +1165,73 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
         }
     }
     if constexpr (DEF > 1) flush();
+    if constexpr (CLS) {
+        for (; t < ta.tcount; t += gridDim.x) {
+            mbar_wait_parity(smem_u32(&full[stage]), ph);
+            const unsigned char* st = stages + stage * L.stage_bytes();
+            const TileHdr* hp = reinterpret_cast<const TileHdr*>(st + L.off_hdr());
+            const int cw = hp->wr[7], hv0 = hp->v0, hnv = hp->nv, sbw = hp->wr[warp] >> 16;
+            const int lq = warp * 32 + lane;
+            const bool act = lq < hnv;
+            const int lc = act ? lq : 0;
+            if (warp * 32 < hnv) {  // (a warp without vertices has no slots)
+                const R4 xi4 = reinterpret_cast<const R4*>(st + L.off_x())[lc];
+                R4 xt4, y4;
+                R svv = R(0);
+                if (ta.xtg) {  // issued before the sweep (used after it)
+                    ldg_nc(a.xt + hv0 + lc, xt4);
+                    ldg_nc(a.y + hv0 + lc, y4);
+                    svv = ldg_nc(a.vsv + hv0 + lc);
+                } else {
+                    xt4 = reinterpret_cast<const R4*>(st + L.off_xt())[lc];
+                    y4 = reinterpret_cast<const R4*>(st + L.off_y())[lc];
+                    svv = a.vsv[hv0 + lc];
+                }
+                const unsigned char* recs = smem + (cw >> 16);
+                AccXY acc[4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[b].zero();
+                const float2 nxy = make_float2(-(float)xi4.x, -(float)xi4.y);
+                const float nz = -(float)xi4.z;
+                const unsigned char* slots = st + L.off_ent() + 8 * (32 * sbw + lane);
+                const unsigned char* npos = st + L.off_npos();
+                if ((cw & 0xff) == 1) class_sweep<0>(slots, npos, recs, nxy, nz, acc);
+                else class_sweep<1>(slots, npos, recs, nxy, nz, acc);
+                const float4 c4 = reinterpret_cast<const float4*>(recs)[4];  // position 0: (t7, t8, dsc, opd)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));  // stage's smem no longer read
+                R f[3] = {(acc[0].f01.x + acc[2].f01.x) + (acc[1].f01.x + acc[3].f01.x),
+                          (acc[0].f01.y + acc[2].f01.y) + (acc[1].f01.y + acc[3].f01.y),
+                          (acc[0].f2 + acc[2].f2) + (acc[1].f2 + acc[3].f2)};
+                R H[6] = {(acc[0].h03.x + acc[2].h03.x) + (acc[1].h03.x + acc[3].h03.x),
+                          (acc[0].h1 + acc[2].h1) + (acc[1].h1 + acc[3].h1),
+                          (acc[0].h24.x + acc[2].h24.x) + (acc[1].h24.x + acc[3].h24.x),
+                          (acc[0].h03.y + acc[2].h03.y) + (acc[1].h03.y + acc[3].h03.y),
+                          (acc[0].h24.y + acc[2].h24.y) + (acc[1].h24.y + acc[3].h24.y),
+                          (acc[0].h5 + acc[2].h5) + (acc[1].h5 + acc[3].h5)};
+                if (act) {
+                    H[0] = H[0] + svv;
+                    H[3] = H[3] + svv;
+                    H[5] = H[5] + svv;
+                    const R xi[3] = {xi4.x, xi4.y, xi4.z};
+                    const R dx[3] = {xi[0] - xt4.x, xi[1] - xt4.y, xi[2] - xt4.z};
+                    vertex_terms<R>(f, H, dx, xi, y4.x, y4.y, y4.z, y4.w, UM, (R)c4.z, (R)c4.w);
+                    R d[3];
+                    block_solve<R>(f, H, a.eps_det, a.mode, d);
+                    R4 nx = xi4;
+                    nx.x = xi[0] + d[0];
+                    nx.y = xi[1] + d[1];
+                    nx.z = xi[2] + d[2];
+                    k1t_store<R>(a, hv0 + lq, nx);
+                }
+            } else {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));
+            }
+            if (++stage == S) {
+                stage = 0;
+                ph ^= 1;
+            }
+        }
+    }
 }

@@ -93,7 +93,9 @@ def test_tiles_cover_every_colour(V, O, monkeypatch, tv):
     m, s = beam_sys(O, 21, 9, 7)
     monkeypatch.setenv("VBD_TILE_V", str(tv))
     monkeypatch.setenv("VBD_RESIDENT", "0")
+    monkeypatch.setenv("VBD_TILE_CLASS", "0")  # (class tiles hold 128 vertices: own test below)
     ctx = make_ctx(V, O, s, "fp32", "auto", monkeypatch)
+    monkeypatch.delenv("VBD_TILE_CLASS")
     counts = ctx.color_counts()
     assert ctx.info.tiles == sum((c + tv - 1) // tv for c in counts)
     assert 0 < ctx.info.tile_nbr_cap < 65536
@@ -287,3 +289,74 @@ def test_k1t_explicit_rows_bitwise_equals_explicit_k1(V, monkeypatch, rho):
         out.append(ctx.get_state(x=True, v_t=True))
         ctx.close()
     assert np.array_equal(out[0]["x"], out[1]["x"]) and np.array_equal(out[0]["v_t"], out[1]["v_t"])
+
+
+def class_run(V, monkeypatch, beams, mode, n=3, rho=0.9, n_max=10, h=1 / 240):
+    """mode: "class" (K1T with grid-class tiles), "plain" (K1T, VBD_TILE_CLASS=0), "global"
+    (the compact global K1)."""
+    monkeypatch.setenv("VBD_TILE_CLASS", "0" if mode == "plain" else "1")
+    monkeypatch.setenv("VBD_TILE_V", "64")  # class tiles ride on the 64-vertex tile configuration
+    monkeypatch.setenv("VBD_RESIDENT", "0")
+    monkeypatch.setenv("VBD_TILES", "0" if mode == "global" else "1")
+    ctx = V.DeviceContext.from_beams(beams, precision="fp32")
+    for k in ("VBD_TILE_CLASS", "VBD_TILE_V", "VBD_RESIDENT", "VBD_TILES"):
+        monkeypatch.delenv(k)
+    info = ctx._info()
+    p = ctx.step_params(h, n_max, rho, 1e-10, "adaptive", G)
+    for _ in range(n):
+        ctx.step(p)
+    out = ctx.get_state(x=True, v_t=True, v_prev=True)
+    ctx.close()
+    return out, info
+
+
+@pytest.mark.parametrize("rho", [0.0, 0.9])
+def test_class_tiles_bitwise_equal_plain_tiles(V, monkeypatch, rho):
+    """K1T class tiles (interior vertices of the 5-tet grid, one lane per vertex, each distinct
+    neighbour loaded once into registers, entries from compile-time indices) are bitwise the
+    2-lane tiles (VBD_TILE_CLASS=0) and the global compact K1."""
+    beams = [V.Beam(40, 17, 15, 0.01, 2e6, 2e7, 1e-7, fix_min_x=True)]
+    a, ia = class_run(V, monkeypatch, beams, "class", rho=rho)
+    b, ib = class_run(V, monkeypatch, beams, "plain", rho=rho)
+    c, _ = class_run(V, monkeypatch, beams, "global", rho=rho)
+    assert ia.class_tiles > 0 and ia.class_records == 40
+    # interior vertices: (40 - 1) x 15 x 13 solved interior of 39 x 17 x 15 solved
+    assert ia.class_vertices == 38 * 15 * 13
+    assert ib.class_tiles == 0
+    for k in ("x", "v_t", "v_prev"):
+        assert np.array_equal(a[k], b[k]), k
+        assert np.array_equal(a[k], c[k]), k
+
+
+def test_class_tiles_several_instances_and_beams(V, monkeypatch):
+    """two beams with different materials and spacings (two instances per class), a twisted
+    start (large strains), rho 0.95: still bitwise the plain tiles"""
+    beams = [V.Beam(33, 12, 12, 0.01, 2e6, 2e7, 1e-7, fix_min_x=True),
+             V.Beam(29, 14, 11, 0.013, 5e5, 4e6, 3e-7, fix_min_x=True, origin=(0.0, 0.3, 0.0))]
+    a, ia = class_run(V, monkeypatch, beams, "class", n=4, rho=0.95, h=1 / 120)
+    b, _ = class_run(V, monkeypatch, beams, "plain", n=4, rho=0.95, h=1 / 120)
+    assert ia.class_tiles > 0 and ia.class_records == 80
+    for k in ("x", "v_t", "v_prev"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_class_tiles_from_system_vs_oracle(V, O, monkeypatch):
+    """through build_system (the reference's API): class tiles on, 3 steps within the fp32 bar
+    of the fp64 oracle, and bitwise the plain tiles"""
+    m, s = beam_sys(O, 41, 15, 13, 0.01, (2e6, 2e7, 1e-7))
+    xs = []
+    for mode in ("1", "0"):
+        monkeypatch.setenv("VBD_TILE_CLASS", mode)
+        monkeypatch.setenv("VBD_TILE_V", "64")
+        monkeypatch.setenv("VBD_RESIDENT", "0")
+        ctx = V.DeviceContext.from_system(O.RefSystemView(s), precision="fp32")
+        for k in ("VBD_TILE_CLASS", "VBD_TILE_V", "VBD_RESIDENT"):
+            monkeypatch.delenv(k)
+        assert (ctx._info().class_tiles > 0) == (mode == "1")
+        xs.append(steps(ctx, s, 3)["x"])
+        ctx.close()
+    assert np.array_equal(xs[0], xs[1])
+    st = O.make_state(s)
+    for _ in range(3):
+        O.step(s, st, H, 10, 0.9, G)
+    assert np.abs(xs[0] - st.x).max() / m.bbox_diagonal() <= 1e-5

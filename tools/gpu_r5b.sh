@@ -1,0 +1,7 @@
+#!/bin/bash
+O=gpurun_out
+timeout 900 python -m pytest tests/test_gpu_layout.py -x -q -k "class or cover or bitwise" > $O/r5b_tests.log 2>&1
+for m in 1 0 1; do
+  echo "== fp32 VBD_TILE_CLASS=$m" >> $O/r5b.log
+  VBD_TILE_CLASS=$m timeout 300 python tools/k1_once.py c5 fp32 2>&1 | tail -3 >> $O/r5b.log
+done

@@ -1,0 +1,7 @@
+#!/bin/bash
+O=gpurun_out
+timeout 900 python -m pytest tests/test_gpu_layout.py -x -q -k "class or cover or bitwise" > $O/r5d_tests.log 2>&1
+for cfg in "VBD_TILE_CLASS=1" "VBD_TILE_CLASS=0" "VBD_TILE_CLASS=1"; do
+  echo "== fp32 $cfg" >> $O/r5d.log
+  env $cfg timeout 300 python tools/k1_once.py c5 fp32 2>&1 | tail -3 >> $O/r5d.log
+done

@@ -28,7 +28,8 @@ def main():
     ctx.step(cfg.step_params())
     i = ctx._info()
     print("tiles", i.tiles, "stages", i.tile_stages, "smem/CTA", i.tile_smem_bytes, "nbr_cap", i.tile_nbr_cap,
-          "ent_cap", i.tile_ent_cap, "kinds", i.num_entry_kinds)
+          "ent_cap", i.tile_ent_cap, "kinds", i.num_entry_kinds, "class_tiles", i.class_tiles,
+          "class_vertices", i.class_vertices, "of", i.num_solved)
     print("k1 ms per colour:", ctx.profile_color_pass(cfg.h, reps=2))
     ctx.close()
 
