@@ -609,6 +609,12 @@ def layout_name(info):
     if int(info.tiles) and int(info.layout) == 0:
         return ("K1T-X tiles (irregular mesh, %d lanes/vertex, %d stages): 8 B entry slots + 36 B of "
                 "slot-weight rows per slot streamed, constants derived per entry" % (info.tile_lanes, info.tile_stages))
+    if int(info.tiles) and int(info.class_tiles):
+        return ("K1T tiles (%d stages) with grid-class tiles: %d of %d solved vertices one lane per vertex, "
+                "8 B neighbour-offset rows, neighbours in registers, %d class records; the rest 2 lanes/vertex, "
+                "8 B entry slots + %d entry kinds"
+                % (info.tile_stages, info.class_vertices, info.num_solved, info.class_records,
+                   info.num_entry_kinds))
     if int(info.tiles):
         return ("K1T tiles (%d lanes/vertex, %d stages): 8 B entry slots + %d entry kinds"
                 % (info.tile_lanes, info.tile_stages, info.num_entry_kinds))
@@ -637,7 +643,8 @@ def roofline_record(cfg, info, precision, k1_ms, k1_reps, device):
     layout_achieved = layout_iter / (k1_iter_ms / 1e3) / 1e9
     ref_achieved = bytes_iter / (k1_iter_ms / 1e3) / 1e9
     kname = "k1_tiles" if int(info.tiles) else "k1_color_pass"
-    variant = "tiles" if int(info.tiles) else ("compact" if int(info.layout) == 1 else "explicit")
+    variant = ("classtiles" if int(info.class_tiles) else "tiles") if int(info.tiles) else (
+        "compact" if int(info.layout) == 1 else "explicit")
     rec = {"bound": "hbm", "achieved": layout_achieved, "peak": peak, "unit": "GB/s",
            "frac": layout_achieved / peak,
            "traffic": ncu_traffic(cfg.name, precision, variant),

@@ -709,8 +709,9 @@ template <typename R> void build_tiles(vbd_ctx* c)
         if (cls) upload(c->ckind, ck.data(), ck.size(), s);
         else c->ncrec = 0;
     }
-    std::vector<int> v0, nv, tcw;
+    std::vector<int> v0, nv, tcw, tcol;
     std::vector<signed char> tw;
+    int cur_col = 0;
     auto cut = [&](long long from, long long to, int per, int inst) {
         for (long long o = from; o < to; o += per) {
             v0.push_back((int)o);
@@ -719,14 +720,12 @@ template <typename R> void build_tiles(vbd_ctx* c)
             tcw.push_back(inst >= 0 ? (c->cinst_tpl[inst] + 1) |
                                           ((int)((c->nkinds + 1 + irec[inst]) * TileSmem<R>::KSTRIDE) << 16)
                                     : 0);
-            if (inst >= 0) {
-                c->class_tiles++;
-                c->class_vertices += std::min<long long>(per, to - o);
-            }
+            tcol.push_back(cur_col);
         }
     };
     c->tile_beg.assign(c->ncolors + 1, 0);
     for (int col = 0; col < c->ncolors; ++col) {
+        cur_col = col;
         c->tile_beg[col] = (int)v0.size();
         const long long b = c->cbeg[col], e = b + c->ccnt[col];
         long long p = b;
@@ -739,27 +738,39 @@ template <typename R> void build_tiles(vbd_ctx* c)
         cut(p, e, VPT, -1);
     }
 
-    const int nt = (int)v0.size();
-    c->tile_beg[c->ncolors] = nt;
-    // per colour: its plain tiles, then its class runs (instances sort after every plain vertex)
-    c->tile_cls_beg.assign(c->ncolors, 0);
-    for (int col = 0; col < c->ncolors; ++col) {
-        int t = c->tile_beg[col];
-        while (t < c->tile_beg[col + 1] && tcw[t] == 0) ++t;
-        c->tile_cls_beg[col] = t;
-        for (int u = t; u < c->tile_beg[col + 1]; ++u)
-            if (!tcw[u]) fail(VBD_ERR_INTERNAL, "class tiles: a plain tile after a class run");
-    }
+    int nt = 0;
+    DBuf dtw, dtcw;
+    // tile arrays -> device, colour ranges, the class tile split of each colour
+    auto commit_tiles = [&]() {
+        nt = (int)v0.size();
+        c->tile_beg.assign(c->ncolors + 1, nt);
+        for (int t = nt - 1; t >= 0; --t) c->tile_beg[tcol[t]] = t;
+        for (int col = c->ncolors - 1; col >= 0; --col)  // (colours without tiles)
+            if (c->tile_beg[col] > c->tile_beg[col + 1]) c->tile_beg[col] = c->tile_beg[col + 1];
+        // per colour: its plain tiles, then its class runs (instances sort after every plain vertex)
+        c->tile_cls_beg.assign(c->ncolors, 0);
+        c->class_tiles = 0;
+        c->class_vertices = 0;
+        for (int col = 0; col < c->ncolors; ++col) {
+            int t = c->tile_beg[col];
+            while (t < c->tile_beg[col + 1] && tcw[t] == 0) ++t;
+            c->tile_cls_beg[col] = t;
+            for (int u = t; u < c->tile_beg[col + 1]; ++u) {
+                if (!tcw[u]) fail(VBD_ERR_INTERNAL, "class tiles: a plain tile after a class run");
+                c->class_tiles++;
+                c->class_vertices += nv[u];
+            }
+        }
+        upload(c->tv0, v0.data(), v0.size(), s);
+        upload(c->tnv, nv.data(), nv.size(), s);
+        if (cls) {
+            upload(dtw, tw.data(), tw.size(), s);
+            upload(dtcw, tcw.data(), tcw.size(), s);
+        }
+    };
+    commit_tiles();
     c->tile_svpt = cls ? 128 : VPT;
     c->tile_xtg = cls;
-    upload(c->tv0, v0.data(), v0.size(), s);
-    upload(c->tnv, nv.data(), nv.size(), s);
-    DBuf dtw, dtcw;
-    if (cls) {
-        upload(dtw, tw.data(), tw.size(), s);
-        upload(dtcw, tcw.data(), tcw.size(), s);
-    }
-    const signed char* tWp = cls ? dtw.as<signed char>() : nullptr;
     DBuf cnt, err;
     cnt.alloc((size_t)nt * 16);
     err.alloc(4);
@@ -812,18 +823,56 @@ template <typename R> void build_tiles(vbd_ctx* c)
     const size_t sort_smem = (size_t)P * 4;
     CK(cudaFuncSetAttribute(k_tile_nbrs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
     CK(cudaFuncSetAttribute(k_tile_nbrs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
-    k_tile_nbrs<false><<<nt, 256, sort_smem, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), eoffb,
-                                                 cent, cnt.as<long long>(), nullptr, nullptr, nullptr, nullptr, W,
-                                                 0u, 0u, 0u, 0u, err.as<int>(), nullptr, tWp);
-    CK(cudaGetLastError());
-    if (read_scalar<int>(err.p, s)) return;
-    std::vector<long long> hc(2 * (size_t)nt), nls(nt), nss(nt);
-    std::vector<int> nl_real(nt);
-    CK(cudaMemcpy(hc.data(), cnt.p, (size_t)nt * 16, cudaMemcpyDeviceToHost));
     // bank-aware placement (k_tile_banks): lists padded by VBD_TILE_BANK_SLACK percent (default
     // 25; 0 keeps the sorted list) to a multiple of the 8 bank groups
     const char* be = getenv("VBD_TILE_BANK_SLACK");
     const int slack = be && *be ? atoi(be) : 25;
+    auto padded = [&](long long n) { return slack > 0 ? (n * (100 + slack) / 100 + 8 + 7) / 8 * 8 : n; };
+    std::vector<long long> hc;
+    const signed char* tWp = nullptr;
+    for (int round = 0;; ++round) {
+        tWp = cls ? dtw.as<signed char>() : nullptr;
+        cnt.alloc((size_t)nt * 16);
+        k_tile_nbrs<false><<<nt, 256, sort_smem, s>>>(c->tv0.as<int>(), c->tnv.as<int>(), eoffb,
+                                                     cent, cnt.as<long long>(), nullptr, nullptr, nullptr, nullptr, W,
+                                                     0u, 0u, 0u, 0u, err.as<int>(), nullptr, tWp);
+        CK(cudaGetLastError());
+        if (read_scalar<int>(err.p, s)) return;
+        hc.assign(2 * (size_t)nt, 0);
+        CK(cudaMemcpy(hc.data(), cnt.p, (size_t)nt * 16, cudaMemcpyDeviceToHost));
+        if (!cls || round == 4) break;
+        // class tiles whose neighbour list would keep two stages from fitting 3 CTAs per SM are
+        // cut in two (C4's small cubes: a class run spans several cubes)
+        long long ms0 = 0;
+        for (int t = 0; t < nt; ++t) ms0 = std::max(ms0, hc[2 * t + 1]);
+        const long long fixed = ((long long)(c->nkinds + 1 + c->ncrec) * TileSmem<R>::KSTRIDE + 127) / 128 * 128 +
+                                2 * ((long long)sizeof(TileDesc) + ms0 * 8 + 128LL * (long long)sizeof(typename Vec4<R>::T) + 256);
+        const long long budget = (75 * 1024 - fixed) / 2 / (long long)TileSmem<R>::PU - 1;
+        std::vector<int> v0b, nvb, tcwb, tcolb;
+        std::vector<signed char> twb;
+        bool any = false;
+        for (int t = 0; t < nt; ++t) {
+            const bool split = tcw[t] && nv[t] > 32 && padded(hc[2 * t]) > budget;
+            const int h = split ? (nv[t] / 2 + 31) / 32 * 32 : nv[t];
+            for (int part = 0; part < (split ? 2 : 1); ++part) {
+                v0b.push_back(part ? v0[t] + h : v0[t]);
+                nvb.push_back(split ? (part ? nv[t] - h : h) : nv[t]);
+                tcwb.push_back(tcw[t]);
+                tcolb.push_back(tcol[t]);
+                twb.push_back(tw[t]);
+            }
+            any |= split;
+        }
+        if (!any) break;
+        v0.swap(v0b);
+        nv.swap(nvb);
+        tcw.swap(tcwb);
+        tcol.swap(tcolb);
+        tw.swap(twb);
+        commit_tiles();
+    }
+    std::vector<long long> nls(nt), nss(nt);
+    std::vector<int> nl_real(nt);
     long long mx = 0, ms = 0;
     for (int t = 0; t < nt; ++t) {
         nl_real[t] = (int)hc[2 * t];
