@@ -2,7 +2,7 @@
 
     compute-sanitizer --tool racecheck python tools/sanitize.py [case ...]
 
-cases: k1t (K1T tiles, per-colour graph), k1r (K1R cluster-resident step), k1r_glob (grid-
+cases: k1t (K1T tiles, per-colour graph), k1t_class (K1T with grid-class tiles), k1r (K1R cluster-resident step), k1r_glob (grid-
 resident), k1 (global-memory K1, compact), explicit (48-byte entries), slabs (3 slabs, host-
 driven halo pack / unpack), p2p (3 slabs on 3 streams with the fused NVLink-style halo stores
 and phase flags: needs concurrent kernels, so it cannot run under a sanitizer, which
@@ -42,6 +42,17 @@ def main():
             env(VBD_RESIDENT="0")
             i = beam_case(V)
             assert i.tiles > 0 and i.resident == 0
+        elif c == "k1t_class":  # grid-class tiles (one lane per vertex, neighbours in registers)
+            env(VBD_RESIDENT="0", VBD_TILE_V="64")
+            beam = V.Beam(40, 10, 9, 0.02, 1e6, 1e7, 1e-6, fix_min_x=True)
+            ctx = V.DeviceContext.from_beams([beam], precision="fp32")
+            p = ctx.step_params(1 / 120, 4, 0.9, 1e-10, "adaptive", G)
+            for _ in range(2):
+                ctx.step(p)
+            assert np.isfinite(ctx.get_state(x=True)["x"]).all()
+            assert ctx._info().class_tiles > 0
+            ctx.close()
+            os.environ.pop("VBD_TILE_V", None)
         elif c == "k1r":
             env(VBD_RESIDENT="repl")
             assert beam_case(V).resident == 1
