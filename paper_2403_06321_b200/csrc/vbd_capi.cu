@@ -682,6 +682,13 @@ template <typename R> void build_tiles(vbd_ctx* c)
     c->ncrec = 0;
     c->class_tiles = 0;
     c->class_vertices = 0;
+    if (cls) {  // worth it only when class vertices carry most of the sweep (C3: 25 %, slower)
+        long long cv = 0;
+        for (const auto& r : c->crun) cv += r.cnt;
+        const char* me = getenv("VBD_TILE_CLASS_MIN");
+        const double mn = me && *me ? atof(me) : 0.5;
+        if ((double)cv < mn * (double)c->nsolve) cls = false;
+    }
     std::vector<int> irec;  // first class record of instance i
     if (cls) {
         const int ninst = (int)c->cinst_tpl.size();
@@ -987,10 +994,15 @@ template <typename R> void build_tiles(vbd_ctx* c)
     c->tiles = true;
 }
 
-static bool entry_order_by_code()
+// per-vertex entry order: by rest-edge sign pattern (fp32 scenes large enough for class tiles,
+// or VBD_ENTRY_ORDER=code) else by kind hash alone (the small scenes measured ~2 % faster with
+// it on C2; fp64 has no class tiles)
+template <typename R> static bool entry_order_by_code(long long n)
 {
     const char* e = getenv("VBD_ENTRY_ORDER");
-    return !(e && std::string(e) == "hash");
+    if (e && std::string(e) == "code") return true;
+    if (e && std::string(e) == "hash") return false;
+    return sizeof(R) == 4 && n >= 200000;
 }
 
 // per-vertex entry order by kind (k_inc_kind_keys): one stable 64-bit radix sort of
@@ -1004,7 +1016,7 @@ template <typename R> void sort_incidence_by_kind(Scene& sc, cudaStream_t s)
     k_inc_kind_keys<R><<<blocks_for(sc.n), 256, 0, s>>>(sc.inc_off.as<long long>(), sc.inc.as<unsigned>(),
                                                         sc.tet_w.as<double>(), sc.vol.as<double>(),
                                                         sc.tmat.as<int>(), sc.n, keys.as<unsigned long long>(),
-                                                        entry_order_by_code() ? 1 : 0);
+                                                        entry_order_by_code<R>(sc.n) ? 1 : 0);
     CK(cudaGetLastError());
     sort_pairs_u64_i32(keys, sc.inc, n4, s);
 }
@@ -1053,7 +1065,7 @@ template <typename R> void pack(vbd_ctx* c, Scene& sc)
     c->cinst_tpl.clear();
     {
         const char* ce = getenv("VBD_TILE_CLASS");
-        const bool on = sizeof(R) == 4 && sc.n && sc.T && sc.tet_w.p && !(ce && *ce == '0') && entry_order_by_code() &&
+        const bool on = sizeof(R) == 4 && sc.n && sc.T && sc.tet_w.p && !(ce && *ce == '0') && entry_order_by_code<R>(sc.n) &&
                         !(getenv("VBD_KIND_ORDER") && *getenv("VBD_KIND_ORDER") == '0');
         if (on) {
             DBuf ck, table, ovf, sorted;

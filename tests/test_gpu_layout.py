@@ -296,10 +296,11 @@ def class_run(V, monkeypatch, beams, mode, n=3, rho=0.9, n_max=10, h=1 / 240):
     (the compact global K1)."""
     monkeypatch.setenv("VBD_TILE_CLASS", "0" if mode == "plain" else "1")
     monkeypatch.setenv("VBD_TILE_V", "64")  # class tiles ride on the 64-vertex tile configuration
+    monkeypatch.setenv("VBD_ENTRY_ORDER", "code")  # (small scenes keep the kind-hash order)
     monkeypatch.setenv("VBD_RESIDENT", "0")
     monkeypatch.setenv("VBD_TILES", "0" if mode == "global" else "1")
     ctx = V.DeviceContext.from_beams(beams, precision="fp32")
-    for k in ("VBD_TILE_CLASS", "VBD_TILE_V", "VBD_RESIDENT", "VBD_TILES"):
+    for k in ("VBD_TILE_CLASS", "VBD_TILE_V", "VBD_RESIDENT", "VBD_TILES", "VBD_ENTRY_ORDER"):
         monkeypatch.delenv(k)
     info = ctx._info()
     p = ctx.step_params(h, n_max, rho, 1e-10, "adaptive", G)
@@ -349,8 +350,9 @@ def test_class_tiles_from_system_vs_oracle(V, O, monkeypatch):
         monkeypatch.setenv("VBD_TILE_CLASS", mode)
         monkeypatch.setenv("VBD_TILE_V", "64")
         monkeypatch.setenv("VBD_RESIDENT", "0")
+        monkeypatch.setenv("VBD_ENTRY_ORDER", "code")
         ctx = V.DeviceContext.from_system(O.RefSystemView(s), precision="fp32")
-        for k in ("VBD_TILE_CLASS", "VBD_TILE_V", "VBD_RESIDENT"):
+        for k in ("VBD_TILE_CLASS", "VBD_TILE_V", "VBD_RESIDENT", "VBD_ENTRY_ORDER"):
             monkeypatch.delenv(k)
         assert (ctx._info().class_tiles > 0) == (mode == "1")
         xs.append(steps(ctx, s, 3)["x"])
@@ -360,3 +362,21 @@ def test_class_tiles_from_system_vs_oracle(V, O, monkeypatch):
     for _ in range(3):
         O.step(s, st, H, 10, 0.9, G)
     assert np.abs(xs[0] - st.x).max() / m.bbox_diagonal() <= 1e-5
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_entry_orders_bitwise_across_layouts(V, O, precision, monkeypatch):
+    """both per-vertex entry orders (rest-edge sign pattern / kind hash) give layouts that agree
+    bitwise with each other's explicit layout, and stay within the oracle bars"""
+    m, s = beam_sys(O)
+    st = O.make_state(s)
+    for _ in range(3):
+        O.step(s, st, H, 10, 0.9, G)
+    tol = 1e-10 if precision == "fp64" else 1e-5
+    for order in ("code", "hash"):
+        monkeypatch.setenv("VBD_ENTRY_ORDER", order)
+        a = steps(make_ctx(V, O, s, precision, "auto", monkeypatch), s, 3)["x"]
+        b = steps(make_ctx(V, O, s, precision, "explicit", monkeypatch), s, 3)["x"]
+        monkeypatch.delenv("VBD_ENTRY_ORDER")
+        assert np.array_equal(a, b), order
+        assert np.abs(a - st.x).max() / m.bbox_diagonal() <= tol

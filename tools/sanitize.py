@@ -43,7 +43,7 @@ def main():
             i = beam_case(V)
             assert i.tiles > 0 and i.resident == 0
         elif c == "k1t_class":  # grid-class tiles (one lane per vertex, neighbours in registers)
-            env(VBD_RESIDENT="0", VBD_TILE_V="64")
+            env(VBD_RESIDENT="0", VBD_TILE_V="64", VBD_ENTRY_ORDER="code")
             beam = V.Beam(40, 10, 9, 0.02, 1e6, 1e7, 1e-6, fix_min_x=True)
             ctx = V.DeviceContext.from_beams([beam], precision="fp32")
             p = ctx.step_params(1 / 120, 4, 0.9, 1e-10, "adaptive", G)
@@ -53,6 +53,7 @@ def main():
             assert ctx._info().class_tiles > 0
             ctx.close()
             os.environ.pop("VBD_TILE_V", None)
+            os.environ.pop("VBD_ENTRY_ORDER", None)
         elif c == "k1r":
             env(VBD_RESIDENT="repl")
             assert beam_case(V).resident == 1
