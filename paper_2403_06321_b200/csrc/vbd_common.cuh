@@ -425,16 +425,35 @@ struct AccXY {
     }
 };
 
+// the displacement difference u_k - u_i of one neighbour (x/y packed), formed once per
+// neighbour by the class-tile sweep (the same operation tet_contrib_ec_xy does per use)
+struct DiffXY {
+    float2 xy;
+    float z;
+};
+__device__ __forceinline__ DiffXY diff_xy(float4 p, float2 nxy, float nz)
+{
+    return DiffXY{add2(make_float2(p.x, p.y), nxy), p.z + nz};
+}
+
+__device__ __forceinline__ void tet_contrib_ec_xy_d(DiffXY d0, DiffXY d1, DiffXY d2, float4 x0, float4 x1, float4 x2,
+                                                    const float* __restrict__ t, AccXY& A);
+
 __device__ __forceinline__ void tet_contrib_ec_xy(float4 p0, float4 p1, float4 p2, float2 nxy, float nz,
                                                   float4 x0, float4 x1, float4 x2,
                                                   const float* __restrict__ t, AccXY& A)
 {
+    tet_contrib_ec_xy_d(diff_xy(p0, nxy, nz), diff_xy(p1, nxy, nz), diff_xy(p2, nxy, nz), x0, x1, x2, t, A);
+}
+
+__device__ __forceinline__ void tet_contrib_ec_xy_d(DiffXY d0, DiffXY d1, DiffXY d2, float4 x0, float4 x1, float4 x2,
+                                                    const float* __restrict__ t, AccXY& A)
+{
     // edges e_k = E_k + (u_k - u_i): rest edge x0..x2 plus the displacement difference (the
     // fp32 displacement state, edge3 / rest_edges_from_rows)
-    const float2 e0 = add2(make_float2(x0.x, x0.y), add2(make_float2(p0.x, p0.y), nxy)),
-                 e1 = add2(make_float2(x1.x, x1.y), add2(make_float2(p1.x, p1.y), nxy)),
-                 e2 = add2(make_float2(x2.x, x2.y), add2(make_float2(p2.x, p2.y), nxy));
-    const float e0z = x0.z + (p0.z + nz), e1z = x1.z + (p1.z + nz), e2z = x2.z + (p2.z + nz);
+    const float2 e0 = add2(make_float2(x0.x, x0.y), d0.xy), e1 = add2(make_float2(x1.x, x1.y), d1.xy),
+                 e2 = add2(make_float2(x2.x, x2.y), d2.xy);
+    const float e0z = x0.z + d0.z, e1z = x1.z + d1.z, e2z = x2.z + d2.z;
     // u = t3 e1 - t4 e0
     const float2 u = fma2(bc2(t[3]), e1, mul2(bc2(-t[4]), e0));
     const float uz = __fmaf_rn(t[3], e1z, -__fmul_rn(t[4], e0z));

@@ -672,7 +672,7 @@ __device__ __forceinline__ void class_sweep(const unsigned char* slots, const un
                                             const unsigned char* recs, float2 nxy, float nz, AccXY (&acc)[4])
 {
     using G = GridClass<C>;
-    float4 P[G::NL];
+    DiffXY P[G::NL];  // u_k - u_i of every neighbour, formed once (each is used ~5 times)
     uint2 row[G::R];
 #pragma unroll
     for (int q = 0; q < G::NE; ++q) {
@@ -682,12 +682,12 @@ __device__ __forceinline__ void class_sweep(const unsigned char* slots, const un
             if (k % 3 == 0) row[k / 3] = *reinterpret_cast<const uint2*>(slots + 256 * (k / 3));
             const unsigned off = k % 3 == 0 ? (row[k / 3].x & 0xffffu)
                                             : (k % 3 == 1 ? (row[k / 3].x >> 16) : (row[k / 3].y & 0xffffu));
-            P[k] = *reinterpret_cast<const float4*>(npos + off);
+            P[k] = diff_xy(*reinterpret_cast<const float4*>(npos + off), nxy, nz);
         }
         const float4* rec = reinterpret_cast<const float4*>(recs + 80 * q);
         const float4 e0 = rec[0], e1 = rec[1], e2 = rec[2], c3 = rec[3];
         const float t[8] = {e0.w, e1.w, e2.w, c3.x, c3.y, c3.z, c3.w, reinterpret_cast<const float*>(rec + 4)[0]};
-        tet_contrib_ec_xy(P[G::nbr(q, 0)], P[G::nbr(q, 1)], P[G::nbr(q, 2)], nxy, nz, e0, e1, e2, t, acc[q & 3]);
+        tet_contrib_ec_xy_d(P[G::nbr(q, 0)], P[G::nbr(q, 1)], P[G::nbr(q, 2)], e0, e1, e2, t, acc[q & 3]);
     }
 }
 
