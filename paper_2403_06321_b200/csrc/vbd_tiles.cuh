@@ -1195,7 +1195,8 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                 const float nz = -(float)xi4.z;
                 const unsigned char* slots = st + L.off_ent() + 8 * (32 * sbw + lane);
                 const unsigned char* npos = st + L.off_npos();
-                if ((cw & 0xff) == 1) class_sweep<0>(slots, npos, recs, nxy, nz, acc);
+                if (ta.dbg == 1) {  // (timing experiment: no sweep)
+                } else if ((cw & 0xff) == 1) class_sweep<0>(slots, npos, recs, nxy, nz, acc);
                 else class_sweep<1>(slots, npos, recs, nxy, nz, acc);
                 const float4 c4 = reinterpret_cast<const float4*>(recs)[4];  // position 0: (t7, t8, dsc, opd)
                 __syncwarp();
