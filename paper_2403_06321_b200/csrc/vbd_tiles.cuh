@@ -722,7 +722,8 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
     __shared__ __align__(8) unsigned long long full[S], empty[S];
     const K1Args<R>& a = ta.a;
     static_assert(!XR || (sizeof(R) == 4 && UM && !KG), "K1T-X: fp32, one material per vertex");
-    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (KG || XR) ? -1 : ta.nkinds + ta.ncrec, ta.svpt, ta.xtg ? 1 : 3};
+    // CL (class tiles): x_t / y are not staged but read by the consumers (ta.xtg is then 1)
+    const TileSmem<R> L{ta.ent_cap, ta.nbr_cap, (KG || XR) ? -1 : ta.nkinds + ta.ncrec, ta.svpt, CL ? 1 : 3};
     typedef typename PlaneT<R>::T PL;
     PL* skind = reinterpret_cast<PL*>(smem);
     unsigned char* stages = smem + ((L.kinds_bytes() + 127) & ~(size_t)127);
@@ -811,7 +812,7 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                 bulk_g2s(st + L.off_hdr(), ta.desc + ta.tbeg + t, (unsigned)sizeof(TileDesc), bar);
                 if (eby) bulk_g2s(st + L.off_ent(), ta.tent + d.eb, eby, bar);
                 bulk_g2s(st + L.off_x(), a.pos + d.v0, vby, bar);
-                if (L.nxv == 3) {
+                if constexpr (!CL) {
                     bulk_g2s(st + L.off_xt(), a.xt + d.v0, vby, bar);
                     bulk_g2s(st + L.off_y(), a.y + d.v0, vby, bar);
                 } else {  // x_t / y (and the vertices' V mu |w|^2 sums) into L2 for the consumers
@@ -917,8 +918,8 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
         const bool act = lv < hnv;
         const int lvc = act ? lv : 0;
         const R4 xi4 = reinterpret_cast<const R4*>(st + L.off_x())[lvc];
-        const R4 xt4 = ta.xtg ? a.xt[hv0 + lvc] : reinterpret_cast<const R4*>(st + L.off_xt())[lvc];
-        const R4 y4 = ta.xtg ? a.y[hv0 + lvc] : reinterpret_cast<const R4*>(st + L.off_y())[lvc];
+        const R4 xt4 = CL ? a.xt[hv0 + lvc] : reinterpret_cast<const R4*>(st + L.off_xt())[lvc];
+        const R4 y4 = CL ? a.y[hv0 + lvc] : reinterpret_cast<const R4*>(st + L.off_y())[lvc];
         const R xi[3] = {xi4.x, xi4.y, xi4.z};
         const R dx[3] = {xi[0] - xt4.x, xi[1] - xt4.y, xi[2] - xt4.z};
         // NA = 4 / W accumulator sets: with W = 2, lane j sums entry positions j mod 4 (even
@@ -1178,7 +1179,7 @@ __global__ void __launch_bounds__(TV * W + 32, OCC) k1_tiles(const K1TArgs<R> ta
                 const R4 xi4 = reinterpret_cast<const R4*>(st + L.off_x())[lc];
                 R4 xt4, y4;
                 R svv = R(0);
-                if (ta.xtg) {  // issued before the sweep (used after it)
+                if constexpr (CL) {  // issued before the sweep (used after it)
                     ldg_nc(a.xt + hv0 + lc, xt4);
                     ldg_nc(a.y + hv0 + lc, y4);
                     svv = ldg_nc(a.vsv + hv0 + lc);
