@@ -1749,7 +1749,8 @@ void to_absolute(vbd_ctx* c)
 // groups (4 lanes per vertex, rounds = max ceil(d / 4), even) are cut into contiguous runs of
 // equal slot work, one run per CTA; each group's slots are [round][lane] int4 {n0, n1, n2,
 // kind}, padding = {n, n, n, nkinds} (zero position, zero record).
-// VBD_RESIDENT: unset = REPL when the replica fits one cluster, "0" off, "repl" / "glob" force.
+// VBD_RESIDENT: unset = REPL when the replica fits one cluster, else GLOB for fp32 scenes of at
+// most VBD_RES_GLOB_MAX (18000) vertices per colour; "0" off, "repl" / "glob" force.
 template <typename R> void ensure_resident(vbd_ctx* c)
 {
     if (c->res_mode >= 0) return;
@@ -1845,7 +1846,15 @@ template <typename R> void ensure_resident(vbd_ctx* c)
             break;
         }
     }
-    if (!mode && (want == "glob")) {
+    // GLOB by default for fp32 scenes whose colours are small enough for the per-colour graph to
+    // be launch-bound (C2, 12.7k vertices per colour: 2.13 -> 1.91 ms/step) but too large for
+    // one cluster's replica; C3 (24k per colour) is faster on the graph (2.61 vs 2.90)
+    long long cmax = 0;
+    for (int col = 0; col < c->ncolors; ++col) cmax = std::max(cmax, c->ccnt[col]);
+    const char* gme = getenv("VBD_RES_GLOB_MAX");
+    const long long glob_max = gme && *gme ? atoll(gme) : 18000;
+    const bool glob_auto = want.empty() && sizeof(R) == 4 && cmax <= glob_max;
+    if (!mode && (want == "glob" || glob_auto)) {
         ncta = sms;
         plan(ncta, cut, slot_cap, grp_cap);
         const size_t sm = smem_of(false, slot_cap, grp_cap);

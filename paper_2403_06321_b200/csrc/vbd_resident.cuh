@@ -90,18 +90,17 @@ __device__ __forceinline__ void stcg4(double4* p, double4 v)
 // generation (release); the others spin on it (acquire).  bar.sync orders the CTA around it.
 __device__ __forceinline__ void res_grid_barrier(unsigned* bar, unsigned ncta)
 {
+    // one monotonic 64-bit arrival counter (a multiple of ncta between barriers): each CTA adds
+    // 1 (release) and polls (acquire) until the count reaches the next multiple -- one atomic
+    // round trip per CTA, no generation word and no reset store
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned gen, arrived;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
-        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
-        if (arrived == ncta - 1) {
-            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
-        } else {
-            unsigned g = gen;
-            while (g == gen) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
-        }
+        unsigned long long* c = reinterpret_cast<unsigned long long*>(bar);
+        unsigned long long old;
+        asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(c) : "memory");
+        const unsigned long long target = (old / ncta + 1) * ncta;
+        unsigned long long cur = old + 1;
+        while (cur < target) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(c) : "memory");
     }
     __syncthreads();
 }

@@ -131,3 +131,22 @@ def test_device_generated_c1_bench_scene_resident(V, monkeypatch):
         ctx.close()
     assert xs[0][1] == 1 and xs[1][1] == 0
     assert np.array_equal(xs[0][0], xs[1][0])
+
+
+def test_device_generated_c2_bench_scene_grid_resident(V, monkeypatch):
+    """the bench's C2 workload (37^3, rho 0.95, extreme init) runs grid-resident by default
+    (too large for one cluster's replica, small enough to be launch-bound as a graph) and equals
+    the graph path bitwise"""
+    from paper_2403_06321_b200.scenes import build, config
+    cfg = config("c2")
+    xs = []
+    for mode in ("", "0"):
+        monkeypatch.setenv("VBD_RESIDENT", mode)
+        ctx, _ = build(cfg, precision="fp32")
+        monkeypatch.delenv("VBD_RESIDENT")
+        for _ in range(2):
+            ctx.step(cfg.step_params())
+        xs.append((ctx.get_state(x=True, v_t=True), ctx._info().resident))
+        ctx.close()
+    assert xs[0][1] == 2 and xs[1][1] == 0
+    assert np.array_equal(xs[0][0]["x"], xs[1][0]["x"]) and np.array_equal(xs[0][0]["v_t"], xs[1][0]["v_t"])
