@@ -408,3 +408,32 @@ def test_slab_p2p_irregular_mesh_k1t_x_bitwise(V, monkeypatch):
         lo = max(cuts[r] - 1, 0)
         own = slice((cuts[r] - lo) * plane, (cuts[r + 1] - lo) * plane)
         assert np.array_equal(xs[own], xf[cuts[r] * plane:cuts[r + 1] * plane]), r
+
+
+def test_slab_p2p_class_tiles_bitwise(V, monkeypatch):
+    """Grid-class tiles (one lane per interior vertex, neighbours in registers) inside three
+    slabs with the fused peer-memory halo: bitwise equal to one context (the slab boundary and
+    ghost planes are plain vertices; every slab's interior is class tiles)."""
+    for k, v in (("VBD_RESIDENT", "0"), ("VBD_TILE_V", "64"), ("VBD_ENTRY_ORDER", "code")):
+        monkeypatch.setenv(k, v)
+    beam = V.Beam(48, 14, 12, 0.02, 1e6, 1e7, 1e-6, fix_min_x=True)
+    full = V.DeviceContext.from_beams([beam], precision="fp32")
+    cuts = [0, 15, 31, beam.nx]
+    slabs = [V.DeviceContext.from_beams([beam], precision="fp32", slab=(cuts[r], cuts[r + 1]))
+             for r in range(3)]
+    for k in ("VBD_RESIDENT", "VBD_TILE_V", "VBD_ENTRY_ORDER"):
+        monkeypatch.delenv(k)
+    assert full._info().class_tiles > 0 and all(sc._info().class_tiles > 0 for sc in slabs)
+    from paper_2403_06321_b200.dist import SlabP2P
+    ex = SlabP2P.local(slabs)
+    p = full.step_params(1 / 120, 6, 0.9, 1e-10, "adaptive", G)
+    for _ in range(3):
+        full.step(p)
+        ex.step(p)
+    xf = full.get_state(x=True)["x"]
+    plane = beam.ny * beam.nz
+    for r, sctx in enumerate(slabs):
+        xs = sctx.get_state(x=True)["x"]
+        lo = max(cuts[r] - 1, 0)
+        own = slice((cuts[r] - lo) * plane, (cuts[r + 1] - lo) * plane)
+        assert np.array_equal(xs[own], xf[cuts[r] * plane:cuts[r + 1] * plane]), r
