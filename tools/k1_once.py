@@ -29,7 +29,7 @@ def main():
     i = ctx._info()
     print("tiles", i.tiles, "stages", i.tile_stages, "smem/CTA", i.tile_smem_bytes, "nbr_cap", i.tile_nbr_cap,
           "ent_cap", i.tile_ent_cap, "kinds", i.num_entry_kinds, "class_tiles", i.class_tiles,
-          "class_vertices", i.class_vertices, "of", i.num_solved)
+          "class_vertices", i.class_vertices, "of", i.num_solved, "class_records", i.class_records)
     print("k1 ms per colour:", ctx.profile_color_pass(cfg.h, reps=2))
     ctx.close()
 
