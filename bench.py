@@ -37,7 +37,9 @@ UNIT = "vertex-iterations/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 10; C1/C2/C3: enough for a >= 1 s timed region, "
+                         "so the clock sampler sees it -- 10000 / 600 / 500)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "c5j"])
     ap.add_argument("--scale", type=float, default=1.0, help="shrink c4/c5 (tests only)")
@@ -53,7 +55,11 @@ def parse():
                          "(rank order = vertex order) -- for the 1-rank vs N-rank bitwise test")
     ap.add_argument("--no-fp64-record", action="store_true",
                     help="skip the fp64 sub-record (the reference's precision) of the fp32 run")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.steps is None:
+        small = {"c1": 10000, "c2": 600, "c3": 500}
+        args.steps = small.get(args.config, 10) if args.impl == "ours" else 10
+    return args
 
 
 # ----------------------------------------------------------------------------------------
